@@ -1,0 +1,757 @@
+/*
+ * oracle/tbik_oracle.c -- CPU restatement of the TBIK hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline leg may load this library, and only as the checker.
+ * The product (paper_2511_17826_b200/, libtbik_b200.so) never links or calls it.
+ *
+ * Every function restates the reference algorithm it cites
+ * (/root/reference/proj/..., file:line) in plain C with strict IEEE binary32
+ * round-to-nearest arithmetic: built with -ffp-contract=off -fno-fast-math and
+ * explicit fmaf(), exactly like the reference build (CMakeLists.txt:20-21).
+ *
+ * Pinning: tests/test_oracle.py checks this restatement against
+ *   (1) the reference library itself, compiled unmodified from
+ *       /root/reference/proj/src into oracle/_ref/libtbik_ref.so (oracle/Makefile),
+ *   (2) the golden vectors committed under tests/golden/ (generated from (1) by
+ *       oracle/gen_golden.py), and the SPEC/SURVEY known-answer tests.
+ * The tree RMSNorm / tree log-softmax semantics (tbo_tree_rmsnorm,
+ * tbo_tree_logsoftmax) are NEW: the reference has only sequential rmsnorm
+ * (demo.cpp:11-34) and softmax_row (demo.cpp:84-97).  Those two are therefore
+ * "parity unpinned" against the reference and pinned only against this file
+ * (see DESIGN.md section 4).
+ *
+ * Status codes: 0 ok, 1 + tbik::ErrorCode (errors.hpp:8-20) on error.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#if defined(__FAST_MATH__)
+#error "the oracle requires strict IEEE semantics"
+#endif
+
+/* tbik::ErrorCode (errors.hpp:8-20), offset by one. */
+enum {
+  TBO_OK = 0,
+  TBO_BAD_DIMENSION = 1,
+  TBO_SHAPE_MISMATCH = 2,
+  TBO_BAD_MAGIC = 3,
+  TBO_TRUNCATED = 4,
+  TBO_UNKNOWN_DTYPE = 5,
+  TBO_PLAN_INFEASIBLE = 6,
+  TBO_SHARD_ERROR = 7,
+  TBO_BAD_WORLD_SIZE = 8,
+  TBO_COLLECTIVE_MISMATCH = 9,
+  TBO_BAD_ARGUMENT = 10,
+  TBO_IO = 11,
+};
+
+/* ---------------------------------------------------------------------------
+ * numerics.hpp:21-62 -- bit casts, bf16 storage rounding, canonical NaN.
+ * ------------------------------------------------------------------------- */
+static inline uint32_t f32_bits(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  return u;
+}
+static inline float f32_from_bits(uint32_t u) {
+  float x;
+  memcpy(&x, &u, 4);
+  return x;
+}
+
+/* numerics.hpp:49-56 */
+uint16_t tbo_bf16_round(float x) {
+  uint32_t u = f32_bits(x);
+  if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu) != 0) return 0x7FC0;
+  uint32_t bias = 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)((u + bias) >> 16);
+}
+
+/* numerics.hpp:44-46 */
+float tbo_bf16_to_f32(uint16_t b) { return f32_from_bits((uint32_t)b << 16); }
+
+static inline float load_elem(const void* p, int dtype, int64_t i) {
+  if (dtype == 0) return ((const float*)p)[i];
+  return tbo_bf16_to_f32(((const uint16_t*)p)[i]);
+}
+
+/* Matrix::widened (matrix.cpp:61-68): exact f32 copy of the payload. */
+static float* widen(const void* p, int dtype, int64_t n) {
+  float* w = (float*)malloc((size_t)n * sizeof(float));
+  if (!w) return NULL;
+  for (int64_t i = 0; i < n; ++i) w[i] = load_elem(p, dtype, i);
+  return w;
+}
+
+/* ---------------------------------------------------------------------------
+ * rng.hpp:15-60 -- counter-based SplitMix64 + Box-Muller (both outputs used).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  uint64_t seed, stream, counter;
+  double spare;
+  int has_spare;
+} tbo_rng;
+
+uint64_t tbo_mix64(uint64_t z) { /* rng.hpp:48-52 */
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static uint64_t rng_next_u64(tbo_rng* r) { /* rng.hpp:20-22 */
+  return tbo_mix64(r->counter++ ^
+                   tbo_mix64(r->stream ^ tbo_mix64(r->seed + 0x9E3779B97F4A7C15ull)));
+}
+
+static double rng_next_unit(tbo_rng* r) { /* rng.hpp:25-27 */
+  return (double)(rng_next_u64(r) >> 11) * 0x1.0p-53;
+}
+
+static double rng_next_normal(tbo_rng* r) { /* rng.hpp:31-43 */
+  if (r->has_spare) {
+    r->has_spare = 0;
+    return r->spare;
+  }
+  double u1 = 1.0 - rng_next_unit(r);
+  double u2 = rng_next_unit(r);
+  double rad = sqrt(-2.0 * log(u1));
+  double theta = 2.0 * 3.14159265358979323846 * u2;
+  r->spare = rad * sin(theta);
+  r->has_spare = 1;
+  return rad * cos(theta);
+}
+
+/* matrix_random_normal (matrix.cpp:163-181): row-major fill in index order;
+ * dtype 0 = f32, 1 = bf16 (bf16 entries pass through bf16_round). */
+int tbo_random_normal(uint64_t seed, uint64_t stream, int64_t rows, int64_t cols,
+                      int dtype, float mean, float stddev, void* out) {
+  if (rows < 1 || cols < 1) return TBO_BAD_DIMENSION;
+  if (stddev < 0.0f) return TBO_BAD_ARGUMENT;
+  tbo_rng r = {seed, stream, 0, 0.0, 0};
+  for (int64_t i = 0; i < rows * cols; ++i) {
+    double z = rng_next_normal(&r);
+    float v = (float)((double)mean + (double)stddev * z);
+    if (dtype == 0)
+      ((float*)out)[i] = v;
+    else
+      ((uint16_t*)out)[i] = tbo_bf16_round(v);
+  }
+  return TBO_OK;
+}
+
+uint64_t tbo_rng_u64(uint64_t seed, uint64_t stream, uint64_t counter) {
+  tbo_rng r = {seed, stream, counter, 0.0, 0};
+  return rng_next_u64(&r);
+}
+
+/* bit_fingerprint (matrix.cpp:143-161): FNV-1a over {rows,cols} u64 + payload. */
+uint64_t tbo_fingerprint(const void* p, int dtype, int64_t rows, int64_t cols) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  uint64_t dims[2] = {(uint64_t)rows, (uint64_t)cols};
+  const unsigned char* b = (const unsigned char*)dims;
+  for (size_t i = 0; i < sizeof(dims); ++i) {
+    h ^= b[i];
+    h *= 0x100000001B3ull;
+  }
+  size_t n = (size_t)(rows * cols) * (dtype == 0 ? 4 : 2);
+  b = (const unsigned char*)p;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= b[i];
+    h *= 0x100000001B3ull;
+  }
+  return h;
+}
+
+/* ---------------------------------------------------------------------------
+ * matmul.cpp:16-67 -- planner.
+ * ------------------------------------------------------------------------- */
+static int is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+static int64_t log2_exact(int64_t v) { /* matmul.cpp:18-22 */
+  int64_t l = 0;
+  while (((int64_t)1 << l) < v) ++l;
+  return l;
+}
+
+/* plan_blocks (matmul.cpp:24-67).  out = {tiles_total, k_first, leaves, depth} */
+int tbo_plan_blocks(int64_t K, int64_t block_k, int64_t k_first, int64_t c_max,
+                    int64_t out[4]) {
+  if (K < 1 || block_k < 1) return TBO_BAD_ARGUMENT;
+  if (!is_pow2(c_max)) return TBO_BAD_ARGUMENT;
+  int64_t tiles = (K + block_k - 1) / block_k;
+#define FEAS(kf) ((kf) >= 1 && tiles % (kf) == 0 && is_pow2(tiles / (kf)) && tiles / (kf) >= c_max)
+  int64_t kf = k_first;
+  if (kf == 0) {
+    for (int64_t c = 1; c <= tiles; ++c) {
+      if (FEAS(c)) {
+        kf = c;
+        break;
+      }
+    }
+    if (kf == 0) return TBO_PLAN_INFEASIBLE;
+  } else if (!FEAS(kf)) {
+    return TBO_PLAN_INFEASIBLE;
+  }
+#undef FEAS
+  out[0] = tiles;
+  out[1] = kf;
+  out[2] = tiles / kf;
+  out[3] = log2_exact(tiles / kf) + 1;
+  return TBO_OK;
+}
+
+/* make_row_shard_plan (layers.cpp:23-46).  bounds: 2*tp int64 [begin,end). */
+int tbo_make_row_shard_plan(int64_t K, int64_t block_k, int64_t k_first, int tp,
+                            int64_t c_max, int64_t* bounds) {
+  if (tp > c_max) return TBO_SHARD_ERROR;
+  int64_t plan[4];
+  int st = tbo_plan_blocks(K, block_k, k_first, c_max, plan);
+  if (st) return st;
+  if (plan[2] % tp != 0) return TBO_SHARD_ERROR;
+  int64_t group = plan[1] * block_k;
+  int64_t per = plan[2] / tp;
+  for (int r = 0; r < tp; ++r) {
+    int64_t b = r * per * group, e = (r + 1) * per * group;
+    if (e > K) e = K;
+    bounds[2 * r] = b;
+    bounds[2 * r + 1] = e;
+  }
+  return TBO_OK;
+}
+
+/* make_column_shard_plan (layers.cpp:9-21). */
+int tbo_make_column_shard_plan(int64_t N, int tp, int64_t* bounds) {
+  if (tp < 1 || N % tp != 0) return TBO_SHARD_ERROR;
+  int64_t w = N / tp;
+  for (int r = 0; r < tp; ++r) {
+    bounds[2 * r] = r * w;
+    bounds[2 * r + 1] = (r + 1) * w;
+  }
+  return TBO_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * The tree operator T(.) (oracle.cpp:11-20): T(lo half) + T(hi half).
+ * ------------------------------------------------------------------------- */
+static float tree_reduce_rec(const float* v, int64_t n) {
+  if (n == 1) return v[0];
+  int64_t h = n / 2;
+  float a = tree_reduce_rec(v, h);
+  float b = tree_reduce_rec(v + h, n - h);
+  return a + b;
+}
+
+int tbo_tree_reduce(const float* leaves, int64_t n, float* out) {
+  if (!is_pow2(n)) return TBO_BAD_ARGUMENT;
+  *out = tree_reduce_rec(leaves, n);
+  return TBO_OK;
+}
+
+/* leaf_dot (matmul.cpp:69-75): ascending-k fma chain from +0. */
+float tbo_leaf_dot(const float* a, const float* b, int64_t n) {
+  float p = 0.0f;
+  for (int64_t k = 0; k < n; ++k) p = fmaf(a[k], b[k], p);
+  return p;
+}
+
+/* ---------------------------------------------------------------------------
+ * tree_matmul (matmul.cpp:143-205) with the TileReducer binary counter
+ * (matmul.cpp:81-139), restated row by row (rows are independent; the tile
+ * grid over M/N does not affect bits, SPEC "Concurrency Model").
+ * block_m / block_n are accepted for API parity and ignored.
+ * ------------------------------------------------------------------------- */
+static void tile_reducer_push(float* acc, float* scratch, int64_t* count,
+                              int64_t depth, int64_t n, const float* partial,
+                              int64_t k_first) {
+  for (int64_t j = 0; j < n; ++j) acc[j] = acc[j] + partial[j];
+  int64_t l = 0;
+  while (l < depth) {
+    int64_t thr = l == 0 ? k_first : 2;
+    float* s = scratch + l * n;
+    if (count[l] + 1 == thr) {
+      for (int64_t j = 0; j < n; ++j) acc[j] = acc[j] + s[j];
+      memset(s, 0, (size_t)n * sizeof(float));
+      count[l] = 0;
+      ++l;
+    } else {
+      for (int64_t j = 0; j < n; ++j) s[j] = s[j] + acc[j];
+      count[l] += 1;
+      memset(acc, 0, (size_t)n * sizeof(float));
+      return;
+    }
+  }
+}
+
+int tbo_tree_matmul(const void* a, int adt, const void* b, int bdt, int64_t M,
+                    int64_t K, int64_t N, int64_t block_k, int64_t k_first,
+                    float* out) {
+  if (M < 1 || K < 1 || N < 1) return TBO_BAD_DIMENSION;
+  int64_t plan[4];
+  int st = tbo_plan_blocks(K, block_k, k_first, 1, plan);
+  if (st) return st;
+  const int64_t T = plan[0], kf = plan[1], depth = plan[3];
+  float* bw = widen(b, bdt, K * N);
+  if (!bw) return TBO_BAD_ARGUMENT;
+  int fail = 0;
+#pragma omp parallel
+  {
+    float* acc = (float*)calloc((size_t)N, sizeof(float));
+    float* scratch = (float*)calloc((size_t)(N * depth), sizeof(float));
+    float* partial = (float*)malloc((size_t)N * sizeof(float));
+    int64_t* count = (int64_t*)calloc((size_t)depth, sizeof(int64_t));
+    if (!acc || !scratch || !partial || !count) fail = 1;
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < M; ++i) {
+      if (fail) continue;
+      memset(acc, 0, (size_t)N * sizeof(float));
+      memset(scratch, 0, (size_t)(N * depth) * sizeof(float));
+      memset(count, 0, (size_t)depth * sizeof(int64_t));
+      for (int64_t t = 0; t < T; ++t) {
+        const int64_t k0 = t * block_k;
+        const int64_t kh = k0 + block_k <= K ? block_k : K - k0;
+        memset(partial, 0, (size_t)N * sizeof(float));
+        for (int64_t k = 0; k < kh; ++k) {
+          const float av = load_elem(a, adt, i * K + k0 + k);
+          const float* brow = bw + (k0 + k) * N;
+          for (int64_t j = 0; j < N; ++j) partial[j] = fmaf(av, brow[j], partial[j]);
+        }
+        tile_reducer_push(acc, scratch, count, depth, N, partial, kf);
+      }
+      memcpy(out + i * N, acc, (size_t)N * sizeof(float));
+    }
+    free(acc);
+    free(scratch);
+    free(partial);
+    free(count);
+  }
+  free(bw);
+  return fail ? TBO_BAD_ARGUMENT : TBO_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * global_tree_matmul (oracle.cpp:106-139): per element, leaf-group values by a
+ * sequential f32 fold of k_first tile dots, then the recursive tree T(.).
+ * The independent route the GPU kernels are compared against.
+ * ------------------------------------------------------------------------- */
+int tbo_global_tree_matmul(const void* a, int adt, const void* b, int bdt,
+                           int64_t M, int64_t K, int64_t N, int64_t block_k,
+                           int64_t k_first, int64_t c_max, float* out) {
+  if (M < 1 || K < 1 || N < 1) return TBO_BAD_DIMENSION;
+  int64_t plan[4];
+  int st = tbo_plan_blocks(K, block_k, k_first, c_max, plan);
+  if (st) return st;
+  const int64_t kf = plan[1], L = plan[2];
+  float* bw = widen(b, bdt, K * N);
+  if (!bw) return TBO_BAD_ARGUMENT;
+  int fail = 0;
+#pragma omp parallel
+  {
+    float* groups = (float*)malloc((size_t)(L * N) * sizeof(float));
+    float* p = (float*)malloc((size_t)N * sizeof(float));
+    float* leaves = (float*)malloc((size_t)L * sizeof(float));
+    if (!groups || !p || !leaves) fail = 1;
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < M; ++i) {
+      if (fail) continue;
+      for (int64_t leaf = 0; leaf < L; ++leaf) {
+        float* g = groups + leaf * N;
+        for (int64_t j = 0; j < N; ++j) g[j] = 0.0f;
+        for (int64_t t = leaf * kf; t < (leaf + 1) * kf; ++t) {
+          const int64_t k0 = t * block_k;
+          const int64_t kh = k0 + block_k <= K ? block_k : K - k0;
+          for (int64_t j = 0; j < N; ++j) p[j] = 0.0f;
+          for (int64_t k = 0; k < kh; ++k) {
+            const float av = load_elem(a, adt, i * K + k0 + k);
+            const float* brow = bw + (k0 + k) * N;
+            for (int64_t j = 0; j < N; ++j) p[j] = fmaf(av, brow[j], p[j]);
+          }
+          for (int64_t j = 0; j < N; ++j) g[j] = g[j] + p[j];
+        }
+      }
+      for (int64_t j = 0; j < N; ++j) {
+        for (int64_t leaf = 0; leaf < L; ++leaf) leaves[leaf] = groups[leaf * N + j];
+        out[i * N + j] = tree_reduce_rec(leaves, L);
+      }
+    }
+    free(groups);
+    free(p);
+    free(leaves);
+  }
+  free(bw);
+  return fail ? TBO_BAD_ARGUMENT : TBO_OK;
+}
+
+/* "Oracle tree over supplied leaf values": leaves[T][E] are per-tile partial
+ * products P_t (however computed -- e.g. dumped from the tcgen05 leaf); this
+ * applies exactly the reference's merge structure above the leaf
+ * (oracle.cpp:120-133 fold + oracle.cpp:11-20 tree).  T = leaves_total,
+ * k_first divides T and T / k_first is a power of two. */
+int tbo_tree_over_leaves(const float* leaves, int64_t T, int64_t E,
+                         int64_t k_first, float* out) {
+  if (T < 1 || E < 1 || k_first < 1 || T % k_first) return TBO_BAD_ARGUMENT;
+  const int64_t L = T / k_first;
+  if (!is_pow2(L)) return TBO_BAD_ARGUMENT;
+  float* g = (float*)malloc((size_t)L * sizeof(float));
+  if (!g) return TBO_BAD_ARGUMENT;
+  for (int64_t e = 0; e < E; ++e) {
+    for (int64_t l = 0; l < L; ++l) {
+      float acc = 0.0f;
+      for (int64_t t = l * k_first; t < (l + 1) * k_first; ++t)
+        acc = acc + leaves[t * E + e];
+      g[l] = acc;
+    }
+    out[e] = tree_reduce_rec(g, L);
+  }
+  free(g);
+  return TBO_OK;
+}
+
+/* sequential_matmul_f32 (oracle.cpp:68-85): one ascending fma chain over K. */
+int tbo_sequential_matmul(const void* a, int adt, const void* b, int bdt,
+                          int64_t M, int64_t K, int64_t N, float* out) {
+  float* bw = widen(b, bdt, K * N);
+  if (!bw) return TBO_BAD_ARGUMENT;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < M; ++i) {
+    float* o = out + i * N;
+    for (int64_t j = 0; j < N; ++j) o[j] = 0.0f;
+    for (int64_t k = 0; k < K; ++k) {
+      const float av = load_elem(a, adt, i * K + k);
+      const float* brow = bw + k * N;
+      for (int64_t j = 0; j < N; ++j) o[j] = fmaf(av, brow[j], o[j]);
+    }
+  }
+  free(bw);
+  return TBO_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * collective.cpp:52-106 -- tree all-reduce (Algorithm 2) and the ring stand-in.
+ * contributions: W consecutive blocks of `elems` f32, rank-indexed.
+ * ------------------------------------------------------------------------- */
+int tbo_tree_all_reduce(const float* contrib, int W, int64_t elems, float* out) {
+  if (!is_pow2(W)) return TBO_BAD_WORLD_SIZE; /* collective.cpp:11-16 */
+  float* local = (float*)malloc((size_t)(W * elems) * sizeof(float));
+  if (!local) return TBO_BAD_ARGUMENT;
+  memcpy(local, contrib, (size_t)(W * elems) * sizeof(float));
+  int rounds = 0;
+  while ((1 << (rounds + 1)) <= W) ++rounds; /* bit_width(W) - 1 */
+  for (int l = 1; l <= rounds; ++l) {       /* collective.cpp:67-74 */
+    int stride = 1 << l;
+    for (int left = 0; left < W; left += stride) {
+      int right = left + (1 << (l - 1));
+      float* d = local + (int64_t)left * elems;
+      const float* s = local + (int64_t)right * elems;
+      for (int64_t e = 0; e < elems; ++e) d[e] = d[e] + s[e];
+    }
+  }
+  memcpy(out, local, (size_t)elems * sizeof(float));
+  free(local);
+  return TBO_OK;
+}
+
+int tbo_ring_reduce(const float* contrib, int W, int64_t elems, float* out) {
+  if (!is_pow2(W)) return TBO_BAD_WORLD_SIZE;
+  memcpy(out, contrib, (size_t)elems * sizeof(float));
+  for (int r = 1; r < W; ++r)
+    for (int64_t e = 0; e < elems; ++e) out[e] = out[e] + contrib[(int64_t)r * elems + e];
+  return TBO_OK;
+}
+
+/* row_parallel_forward (layers.cpp:74-98): each rank runs tree_matmul on its
+ * contiguous leaf range with the GLOBAL k_first (layers.cpp:85-88), then the
+ * partials meet in the tree all-reduce. */
+int tbo_row_parallel_forward(const void* a, int adt, const void* b, int bdt,
+                             int64_t M, int64_t K, int64_t N, int64_t block_k,
+                             int64_t k_first, int tp, int64_t c_max, float* out) {
+  if (!is_pow2(tp)) return TBO_BAD_WORLD_SIZE;
+  int64_t bounds[2 * 64];
+  if (tp > 64) return TBO_BAD_ARGUMENT;
+  int st = tbo_make_row_shard_plan(K, block_k, k_first, tp, c_max, bounds);
+  if (st) return st;
+  int64_t gplan[4];
+  st = tbo_plan_blocks(K, block_k, k_first, c_max, gplan);
+  if (st) return st;
+  const size_t esz = adt == 0 ? 4 : 2, bsz = bdt == 0 ? 4 : 2;
+  float* parts = (float*)malloc((size_t)(tp * M * N) * sizeof(float));
+  if (!parts) return TBO_BAD_ARGUMENT;
+  for (int r = 0; r < tp && !st; ++r) {
+    const int64_t kb = bounds[2 * r], ke = bounds[2 * r + 1], kl = ke - kb;
+    unsigned char* as = (unsigned char*)malloc((size_t)(M * kl) * esz);
+    for (int64_t i = 0; i < M; ++i)
+      memcpy(as + (size_t)(i * kl) * esz, (const unsigned char*)a + (size_t)(i * K + kb) * esz,
+             (size_t)kl * esz);
+    const unsigned char* bs = (const unsigned char*)b + (size_t)(kb * N) * bsz;
+    st = tbo_tree_matmul(as, adt, bs, bdt, M, kl, N, block_k, gplan[1],
+                         parts + (int64_t)r * M * N);
+    free(as);
+  }
+  if (!st) st = tbo_tree_all_reduce(parts, tp, M * N, out);
+  free(parts);
+  return st;
+}
+
+/* ---------------------------------------------------------------------------
+ * rmsnorm (demo.cpp:11-34), the reference's SEQUENTIAL form: sum of squares
+ * by an ascending fma chain, ms = sum / cols, denom = sqrt(ms + eps),
+ * y = (x * gamma) / denom.
+ * ------------------------------------------------------------------------- */
+int tbo_rmsnorm_seq(const void* x, int dt, int64_t rows, int64_t cols,
+                    const float* gamma, float eps, float* out) {
+  for (int64_t i = 0; i < rows; ++i) {
+    float ss = 0.0f;
+    for (int64_t j = 0; j < cols; ++j) {
+      float v = load_elem(x, dt, i * cols + j);
+      ss = fmaf(v, v, ss);
+    }
+    float ms = ss / (float)cols;
+    float denom = sqrtf(ms + eps);
+    for (int64_t j = 0; j < cols; ++j)
+      out[i * cols + j] = (load_elem(x, dt, i * cols + j) * gamma[j]) / denom;
+  }
+  return TBO_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * NEW semantics (not in the reference): tree-ordered RMSNorm.
+ *
+ * Canonical order for the sum of squares of one row of n elements:
+ *   * the row is cut into chunks of TBO_CHUNK consecutive elements
+ *     (8 for bf16 = one 16-byte load, 4 for f32 = one 16-byte load);
+ *   * lane l in [0, 256) owns chunks c = l, l + 256, l + 512, ... and folds
+ *     their elements in ascending element order with an fma chain from +0;
+ *   * the 256 lane values are combined by the contiguous-halves tree T(.)
+ *     (oracle.cpp:11-20).
+ * Then ms = sum / n, denom = sqrt(ms + eps), y = (x * gamma) / denom exactly
+ * as demo.cpp:26-31.  Replicated across TP ranks, so TP-invariant trivially;
+ * row-independent, so batch-invariant.
+ * ------------------------------------------------------------------------- */
+#define TBO_LANES 256
+
+float tbo_tree_sumsq_row(const void* x, int dt, int64_t n) {
+  const int64_t chunk = dt == 0 ? 4 : 8;
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  float lanes[TBO_LANES];
+  for (int l = 0; l < TBO_LANES; ++l) {
+    float acc = 0.0f;
+    for (int64_t c = l; c < nchunks; c += TBO_LANES) {
+      for (int64_t e = c * chunk; e < c * chunk + chunk && e < n; ++e) {
+        float v = load_elem(x, dt, e);
+        acc = fmaf(v, v, acc);
+      }
+    }
+    lanes[l] = acc;
+  }
+  return tree_reduce_rec(lanes, TBO_LANES);
+}
+
+int tbo_tree_rmsnorm(const void* x, int dt, int64_t rows, int64_t cols,
+                     const float* gamma, float eps, float* out) {
+  if (rows < 1 || cols < 1) return TBO_BAD_DIMENSION;
+  const size_t esz = dt == 0 ? 4 : 2;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < rows; ++i) {
+    const void* row = (const unsigned char*)x + (size_t)(i * cols) * esz;
+    float ss = tbo_tree_sumsq_row(row, dt, cols);
+    float ms = ss / (float)cols;
+    float denom = sqrtf(ms + eps);
+    for (int64_t j = 0; j < cols; ++j)
+      out[i * cols + j] = (load_elem(row, dt, j) * gamma[j]) / denom;
+  }
+  return TBO_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * Shared, explicitly-rounded exp / log (NEW).  glibc expf/logf and CUDA's
+ * expf/logf are not bit-identical, so the GPU kernels and this oracle both
+ * use exactly this sequence of IEEE f32 operations (fmaf / * / + only, no
+ * contraction).  Accuracy: a few ulp (Cephes-style polynomials).
+ * ------------------------------------------------------------------------- */
+float tbo_exp(float x) {
+  if (x != x) return x;
+  if (x < -103.0f) return 0.0f;
+  if (x > 88.5f) return INFINITY;
+  const float magic = 12582912.0f; /* 1.5 * 2^23 */
+  float t = fmaf(x, 1.44269502162933349609f, magic);
+  float kf = t - magic;
+  float r = fmaf(kf, -0.693359375f, x);
+  r = fmaf(kf, 2.12194440e-4f, r);
+  float p = 1.9875691500e-4f;
+  p = fmaf(p, r, 1.3981999507e-3f);
+  p = fmaf(p, r, 8.3334519073e-3f);
+  p = fmaf(p, r, 4.1665795894e-2f);
+  p = fmaf(p, r, 1.6666665459e-1f);
+  p = fmaf(p, r, 5.0000001201e-1f);
+  float r2 = r * r;
+  float y = fmaf(p, r2, r);
+  y = y + 1.0f;
+  int k = (int)kf;
+  if (k < -125) { /* two-step scaling keeps 2^k representable */
+    y = y * f32_from_bits((uint32_t)(127 - 64) << 23);
+    k += 64;
+  }
+  return y * f32_from_bits((uint32_t)(k + 127) << 23);
+}
+
+float tbo_log(float x) { /* x > 0, finite */
+  if (!(x > 0.0f)) return x == 0.0f ? -INFINITY : NAN;
+  if (x == INFINITY) return x;
+  uint32_t u = f32_bits(x);
+  int e = 0;
+  if ((u & 0x7F800000u) == 0) { /* subnormal: scale by 2^32 */
+    x = x * 4294967296.0f;
+    u = f32_bits(x);
+    e = -32;
+  }
+  e += (int)((u >> 23) & 0xFF) - 127;
+  float m = f32_from_bits((u & 0x007FFFFFu) | 0x3F800000u); /* [1,2) */
+  if (m > 1.41421356237309504880f) {
+    m = m * 0.5f;
+    e += 1;
+  }
+  float xm = m - 1.0f;
+  float z = xm * xm;
+  float p = 7.0376836292e-2f;
+  p = fmaf(p, xm, -1.1514610310e-1f);
+  p = fmaf(p, xm, 1.1676998740e-1f);
+  p = fmaf(p, xm, -1.2420140846e-1f);
+  p = fmaf(p, xm, 1.4249322787e-1f);
+  p = fmaf(p, xm, -1.6668057665e-1f);
+  p = fmaf(p, xm, 2.0000714765e-1f);
+  p = fmaf(p, xm, -2.4999993993e-1f);
+  p = fmaf(p, xm, 3.3333331174e-1f);
+  float y = p * xm;
+  y = y * z;
+  float fe = (float)e;
+  y = fmaf(fe, -2.12194440e-4f, y);
+  y = fmaf(z, -0.5f, y);
+  float r = xm + y;
+  r = fmaf(fe, 0.693359375f, r);
+  return r;
+}
+
+/* ---------------------------------------------------------------------------
+ * NEW semantics: tree-ordered log-softmax / log-prob over a vocab row.
+ *
+ * State (m, s) = (running max, sum of exp(x - m)).  Empty = (-inf, 0).
+ *   fold(m,s; x):  x == -inf -> unchanged
+ *                  x <= m    -> s = s + exp(x - m)
+ *                  x >  m    -> s = s * exp(m - x); s = s + 1; m = x
+ *   merge((m1,s1) lo, (m2,s2) hi):  if m1 == -inf return hi; if m2 == -inf
+ *                  return lo; m = m1 >= m2 ? m1 : m2;
+ *                  s = s1 * exp(m1 - m) + s2 * exp(m2 - m)   (mul, mul, add)
+ * Canonical tree for a row of V logits cut into G contiguous equal vocab
+ * groups (G a power of two >= the largest TP size; V % G == 0):
+ *   * within a group of n = V / G logits: chunks of 4 consecutive logits,
+ *     lane l in [0,256) folds chunks l, l+256, ... in ascending element order;
+ *     the 256 lane states are merged by the contiguous-halves tree;
+ *   * the G group states are merged by the contiguous-halves tree.
+ * A TP rank owning G/TP consecutive groups computes exactly a subtree, so
+ * the cross-rank merge of (m, s) pairs (8 bytes per row per rank) continues
+ * the same tree (Theorem 1, applied to the (m,s) operator).
+ * lse = m + log(s);  logprob[j] = x[j] - lse.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  float m, s;
+} tbo_ms;
+
+static tbo_ms ms_fold(tbo_ms st, float x) {
+  if (x == -INFINITY) return st;
+  if (x <= st.m) {
+    st.s = st.s + tbo_exp(x - st.m);
+  } else {
+    st.s = st.s * tbo_exp(st.m - x);
+    st.s = st.s + 1.0f;
+    st.m = x;
+  }
+  return st;
+}
+
+static tbo_ms ms_merge(tbo_ms lo, tbo_ms hi) {
+  if (lo.m == -INFINITY) return hi;
+  if (hi.m == -INFINITY) return lo;
+  float m = lo.m >= hi.m ? lo.m : hi.m;
+  float a = lo.s * tbo_exp(lo.m - m);
+  float b = hi.s * tbo_exp(hi.m - m);
+  tbo_ms r = {m, a + b};
+  return r;
+}
+
+static tbo_ms ms_tree(const tbo_ms* v, int64_t n) {
+  if (n == 1) return v[0];
+  int64_t h = n / 2;
+  return ms_merge(ms_tree(v, h), ms_tree(v + h, n - h));
+}
+
+static tbo_ms ms_group(const float* x, int64_t n) {
+  const int64_t nchunks = (n + 3) / 4;
+  tbo_ms lanes[TBO_LANES];
+  for (int l = 0; l < TBO_LANES; ++l) {
+    tbo_ms st = {-INFINITY, 0.0f};
+    for (int64_t c = l; c < nchunks; c += TBO_LANES)
+      for (int64_t e = c * 4; e < c * 4 + 4 && e < n; ++e) st = ms_fold(st, x[e]);
+    lanes[l] = st;
+  }
+  return ms_tree(lanes, TBO_LANES);
+}
+
+/* Per-group (m, s) states: out_m/out_s are rows x G. */
+int tbo_logsoftmax_group_states(const float* logits, int64_t rows, int64_t V,
+                                int64_t G, float* out_m, float* out_s) {
+  if (!is_pow2(G) || V % G != 0) return TBO_SHARD_ERROR;
+  const int64_t n = V / G;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < rows; ++i)
+    for (int64_t g = 0; g < G; ++g) {
+      tbo_ms st = ms_group(logits + i * V + g * n, n);
+      out_m[i * G + g] = st.m;
+      out_s[i * G + g] = st.s;
+    }
+  return TBO_OK;
+}
+
+/* Full row: lse[rows]; logprobs (rows x V) optional (NULL to skip);
+ * target log-probs (rows) optional with targets[rows]. */
+int tbo_tree_logsoftmax(const float* logits, int64_t rows, int64_t V, int64_t G,
+                        float* lse, float* logprobs, const int64_t* targets,
+                        float* target_logprobs) {
+  if (rows < 1 || V < 1) return TBO_BAD_DIMENSION;
+  if (!is_pow2(G) || V % G != 0) return TBO_SHARD_ERROR;
+  const int64_t n = V / G;
+  int bad = 0;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < rows; ++i) {
+    tbo_ms* gs = (tbo_ms*)malloc((size_t)G * sizeof(tbo_ms));
+    if (!gs) {
+      bad = 1;
+      continue;
+    }
+    const float* x = logits + i * V;
+    for (int64_t g = 0; g < G; ++g) gs[g] = ms_group(x + g * n, n);
+    tbo_ms st = ms_tree(gs, G);
+    float l = st.m + tbo_log(st.s);
+    lse[i] = l;
+    if (logprobs)
+      for (int64_t j = 0; j < V; ++j) logprobs[i * V + j] = x[j] - l;
+    if (targets && target_logprobs) target_logprobs[i] = x[targets[i]] - l;
+    free(gs);
+  }
+  return bad ? TBO_BAD_ARGUMENT : TBO_OK;
+}
+
+/* softmax_row (demo.cpp:84-97), the reference's sequential form, with the
+ * libm exp the reference uses (not bit-comparable to any GPU kernel). */
+int tbo_softmax_row_seq(const float* logits, int64_t n, float* probs) {
+  float mx = logits[0];
+  for (int64_t j = 1; j < n; ++j)
+    if (logits[j] > mx) mx = logits[j];
+  float sum = 0.0f;
+  for (int64_t j = 0; j < n; ++j) {
+    probs[j] = expf(logits[j] - mx);
+    sum = sum + probs[j];
+  }
+  for (int64_t j = 0; j < n; ++j) probs[j] = probs[j] / sum;
+  return TBO_OK;
+}
