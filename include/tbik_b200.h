@@ -1,0 +1,238 @@
+/*
+ * tbik_b200.h -- the C ABI of the B200-native TBIK library (libtbik_b200.so).
+ *
+ * Plain pointers and sizes only: no torch, no C++ types, no exceptions cross
+ * this boundary.  Every entry point names the reference interface it replaces
+ * (/root/reference/proj/include/tbik/..., file:line).  The C++ mirror of the
+ * reference API (include/tbik_b200/tbik.hpp) is implemented on top of this
+ * header, and so are the Python bindings used by tests/ and bench.py.
+ *
+ * Memory convention: unless stated otherwise, matrix arguments are DEVICE
+ * pointers, row-major with an explicit leading dimension in elements
+ * (the reference Matrix is row-major, matrix.hpp:18-24).  `stream` is a
+ * cudaStream_t passed as void* (NULL = legacy default stream).  Kernels are
+ * asynchronous; argument errors are returned synchronously, device faults
+ * surface from the next call or tbik_sync().
+ *
+ * There is NO CPU fallback: without a usable sm_100 device every compute
+ * entry point returns TBIK_NO_DEVICE.
+ */
+#ifndef TBIK_B200_H_
+#define TBIK_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TBIK_API __attribute__((visibility("default")))
+#else
+#define TBIK_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: 0 = ok, 1 + tbik::ErrorCode (errors.hpp:8-20) for the
+ * reference's error kinds, >= 100 for device-side conditions.  The C++ shim
+ * rethrows codes 1..11 as tbik::TbikError(ErrorCode) (errors.hpp:22-35). */
+typedef enum tbik_status {
+  TBIK_OK = 0,
+  TBIK_BAD_DIMENSION = 1,       /* ErrorCode::BadDimension       */
+  TBIK_SHAPE_MISMATCH = 2,      /* ErrorCode::ShapeMismatch      */
+  TBIK_BAD_MAGIC = 3,           /* ErrorCode::BadMagic           */
+  TBIK_TRUNCATED = 4,           /* ErrorCode::Truncated          */
+  TBIK_UNKNOWN_DTYPE = 5,       /* ErrorCode::UnknownDtype       */
+  TBIK_PLAN_INFEASIBLE = 6,     /* ErrorCode::PlanInfeasible     */
+  TBIK_SHARD_ERROR = 7,         /* ErrorCode::ShardError         */
+  TBIK_BAD_WORLD_SIZE = 8,      /* ErrorCode::BadWorldSize       */
+  TBIK_COLLECTIVE_MISMATCH = 9, /* ErrorCode::CollectiveMismatch */
+  TBIK_BAD_ARGUMENT = 10,       /* ErrorCode::BadArgument        */
+  TBIK_IO = 11,                 /* ErrorCode::Io                 */
+  TBIK_CUDA_ERROR = 100,        /* a CUDA runtime/driver call failed */
+  TBIK_NO_DEVICE = 101,         /* no sm_100 device visible: no fallback */
+  TBIK_UNSUPPORTED = 102        /* shape/dtype not supported by the requested kernel */
+} tbik_status;
+
+/* tbik::Dtype (matrix.hpp:20): storage type tag. */
+typedef enum tbik_dtype { TBIK_F32 = 0, TBIK_BF16 = 1 } tbik_dtype;
+
+/* Which computation forms a LEAF (one block_k tile dot product, matmul.cpp:69-75).
+ *  TBIK_LEAF_FMA      CUDA-core ascending-k fma chain from +0: bit-exact with
+ *                     the reference leaf_dot for every input.
+ *  TBIK_LEAF_TCGEN05  tcgen05.mma (kind::f16, bf16 x bf16 -> f32 in TMEM),
+ *                     block_k/16 MMAs from a zeroed accumulator.  Every merge
+ *                     above the leaf is the reference's f32 tree, bit-exact;
+ *                     the leaf itself is ulp-bounded against leaf_dot
+ *                     (DESIGN.md section 3).  bf16 inputs, block_k % 64 == 0.
+ * Both modes are TP- and batch-invariant: the per-element expression never
+ * depends on M, on the N shard, on the TP size or on the launch schedule. */
+typedef enum tbik_leaf_mode { TBIK_LEAF_FMA = 0, TBIK_LEAF_TCGEN05 = 1 } tbik_leaf_mode;
+
+/* tbik::BlockConfig (matmul.hpp:18-25).  block_k and k_first define the
+ * numerics; block_m / block_n are accepted for API parity and do not affect
+ * bits (the GPU picks its own output tiling). */
+typedef struct tbik_block_config {
+  int64_t block_m;
+  int64_t block_k;
+  int64_t block_n;
+  int64_t k_first; /* 0 = smallest feasible (plan_blocks) */
+} tbik_block_config;
+
+/* tbik::ReductionPlan (matmul.hpp:30-35). */
+typedef struct tbik_reduction_plan {
+  int64_t tiles_total;
+  int64_t k_first;
+  int64_t leaves;
+  int64_t depth;
+} tbik_reduction_plan;
+
+TBIK_API const char* tbik_status_string(int status);
+/* Detail text of the last error raised on the calling host thread. */
+TBIK_API const char* tbik_last_error(void);
+TBIK_API int tbik_version(void);
+/* 1 if an sm_100 device is usable, else 0 (never falls back to the CPU). */
+TBIK_API int tbik_device_available(void);
+/* Block until all work queued by this library on `stream` finished; reports
+ * any asynchronous device fault. */
+TBIK_API tbik_status tbik_sync(void* stream);
+
+/* ---- planner (host, pure integer functions) ---------------------------- */
+
+/* default_block_config (matmul.cpp:11-14). */
+TBIK_API tbik_status tbik_default_block_config(int dtype, tbik_block_config* out);
+/* plan_blocks (matmul.hpp:42-43, matmul.cpp:24-67). */
+TBIK_API tbik_status tbik_plan_blocks(int64_t K, const tbik_block_config* cfg, int64_t c_max,
+                             tbik_reduction_plan* out);
+/* make_row_shard_plan (layers.hpp:31-32, layers.cpp:23-46); bounds = 2*tp int64. */
+TBIK_API tbik_status tbik_make_row_shard_plan(int64_t K, const tbik_block_config* cfg, int tp,
+                                     int64_t c_max, int64_t* bounds);
+/* make_column_shard_plan (layers.hpp:27, layers.cpp:9-21); bounds = 2*tp int64. */
+TBIK_API tbik_status tbik_make_column_shard_plan(int64_t N, int tp, int64_t* bounds);
+
+/* ---- the TBIK GEMM ------------------------------------------------------- */
+
+/* tree_matmul (matmul.hpp:53, matmul.cpp:143-205) on device memory:
+ *   C[M x N] (f32, ldc) = tree over K of A[M x K] (a_dtype, lda) . B[K x N] (b_dtype, ldb)
+ * with the reduction plan plan_blocks(K, cfg, 1).  cfg->k_first must be the
+ * GLOBAL k_first when this is one rank's shard (layers.cpp:85-88). */
+TBIK_API tbik_status tbik_tree_matmul(const void* A, int a_dtype, int64_t lda, const void* B, int b_dtype,
+                             int64_t ldb, float* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                             const tbik_block_config* cfg, int leaf_mode, void* stream);
+
+/* Debug / verification entry: write every leaf partial product P_t
+ * (t = 0..tiles_total-1) to leaves[t][M][N] (f32, dense) using the given leaf
+ * mode.  tests/ feed these to the CPU oracle's tree to check the tree logic
+ * above a tcgen05 leaf bit-for-bit ("oracle tree over GPU leaves"). */
+TBIK_API tbik_status tbik_tree_matmul_leaves(const void* A, int a_dtype, int64_t lda, const void* B,
+                                    int b_dtype, int64_t ldb, float* leaves, int64_t M, int64_t N,
+                                    int64_t K, const tbik_block_config* cfg, int leaf_mode,
+                                    void* stream);
+
+/* column_parallel_forward (layers.hpp:36-38, layers.cpp:48-72) on ONE device
+ * with `tp` simulated ranks (the reference's in-process DeviceGroup): rank r
+ * computes the N-columns [r*N/tp, (r+1)*N/tp) with the c_max=1 plan; outputs
+ * are concatenated.  No cross-shard arithmetic. */
+TBIK_API tbik_status tbik_column_parallel_forward_local(const void* X, int x_dtype, int64_t ldx,
+                                               const void* W, int w_dtype, int64_t ldw, float* Y,
+                                               int64_t ldy, int64_t M, int64_t N, int64_t K,
+                                               int tp, const tbik_block_config* cfg,
+                                               int leaf_mode, void* stream);
+
+/* row_parallel_forward (layers.hpp:43-45, layers.cpp:74-98) on ONE device with
+ * `tp` simulated ranks: rank r runs tbik_tree_matmul on its K range
+ * (make_row_shard_plan) with the global k_first into its own f32 partial,
+ * then the partials meet in tbik_tree_all_reduce_local.  Bit-identical for
+ * every feasible tp (the reference's claim, runner.cpp:53-91). */
+TBIK_API tbik_status tbik_row_parallel_forward_local(const void* X, int x_dtype, int64_t ldx,
+                                            const void* W, int w_dtype, int64_t ldw, float* Y,
+                                            int64_t ldy, int64_t M, int64_t N, int64_t K, int tp,
+                                            const tbik_block_config* cfg, int64_t c_max,
+                                            int leaf_mode, void* stream);
+
+/* ---- the fixed-order tree all-reduce ------------------------------------ */
+
+/* tree_all_reduce_per_rank (collective.hpp:33-34, collective.cpp:52-92) over W
+ * f32 buffers that are all addressable from the current device (local or
+ * peer-mapped): out[e] = Algorithm-2 order  R[left] += R[left + 2^(l-1)].
+ * W must be a power of two (BadWorldSize, collective.cpp:11-16). */
+TBIK_API tbik_status tbik_tree_all_reduce_local(const float* const* partials, int W, float* out,
+                                       int64_t elems, void* stream);
+
+/* ring_reduce_baseline (collective.hpp:43-44, collective.cpp:94-106): the
+ * labelled non-invariant left-to-right stand-in, for divergence tests. */
+TBIK_API tbik_status tbik_ring_reduce_local(const float* const* partials, int W, float* out,
+                                   int64_t elems, void* stream);
+
+/* ---- one-process-per-GPU groups (NVLink peer memory) -------------------- */
+
+/* A DeviceGroup (collective.hpp:15-23) whose ranks are processes, one per GPU.
+ * Each rank owns a peer-visible f32 exchange buffer of `capacity_elems`
+ * (x2 for double buffering) plus a flag array; handles are exchanged out of
+ * band (e.g. torch.distributed all_gather_object) with tbik_group_ipc_handle /
+ * tbik_group_open_peers.  The reduction order is per element and fixed, so the
+ * result is bit-identical on every rank and for every schedule. */
+typedef struct tbik_group tbik_group;
+#define TBIK_IPC_HANDLE_BYTES 128
+
+TBIK_API tbik_status tbik_group_create(int world_size, int rank, int device, int64_t capacity_elems,
+                              tbik_group** out);
+TBIK_API tbik_status tbik_group_ipc_handle(tbik_group* g, void* handle_out /* TBIK_IPC_HANDLE_BYTES */);
+TBIK_API tbik_status tbik_group_open_peers(tbik_group* g, const void* handles /* W * HANDLE_BYTES */);
+TBIK_API tbik_status tbik_group_destroy(tbik_group* g);
+/* This rank's exchange buffer for the next collective (device pointer). */
+TBIK_API float* tbik_group_send_buffer(tbik_group* g);
+
+/* tree_all_reduce over the group: `partial` (elems f32, may be the send
+ * buffer itself) is published, all ranks meet on a device-side flag barrier,
+ * and every rank reduces all W partials in Algorithm-2 order into `out`. */
+TBIK_API tbik_status tbik_group_tree_all_reduce(tbik_group* g, const float* partial, float* out,
+                                       int64_t elems, void* stream);
+
+/* row_parallel_forward for this rank: X_shard [M x K_r], W_shard [K_r x N]
+ * (this rank's make_row_shard_plan range of the global K), GEMM straight into
+ * the peer-visible send buffer, then the tree all-reduce into Y. */
+TBIK_API tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* X_shard, int x_dtype,
+                                            int64_t ldx, const void* W_shard, int w_dtype,
+                                            int64_t ldw, float* Y, int64_t ldy, int64_t M,
+                                            int64_t N, int64_t K_global,
+                                            const tbik_block_config* cfg, int64_t c_max,
+                                            int leaf_mode, void* stream);
+
+/* ---- tree-ordered reductions (NEW semantics) -------- */
+
+/* rmsnorm (demo.hpp:53, demo.cpp:11-34) with the sum of squares in the
+ * canonical lane tree (oracle/tbik_oracle.c tbo_tree_rmsnorm):
+ * Y = (X * gamma) / sqrt(tree_sum(X^2) / cols + eps).  y_dtype f32 or bf16. */
+TBIK_API tbik_status tbik_tree_rmsnorm(const void* X, int x_dtype, int64_t ldx, const float* gamma,
+                              float eps, void* Y, int y_dtype, int64_t ldy, int64_t rows,
+                              int64_t cols, void* stream);
+
+/* Vocab-sharded tree log-softmax, step 1: the (m, s) state of every one of
+ * `groups` contiguous vocab groups of this shard (logits [rows x v_local] f32),
+ * then merged over the shard's groups by the canonical tree.  ms_out is
+ * rows x 2 f32 ({m, s} per row) -- 8 bytes per row to exchange. */
+TBIK_API tbik_status tbik_logsoftmax_shard_state(const float* logits, int64_t ld, int64_t rows,
+                                        int64_t v_local, int64_t groups, float* ms_out,
+                                        void* stream);
+/* Step 2: merge W shard states (rank order, contiguous-halves tree) into
+ * lse[rows] = m + log(s).  W a power of two. */
+TBIK_API tbik_status tbik_logsoftmax_merge(const float* const* ms_parts, int W, int64_t rows, float* lse,
+                                  void* stream);
+/* Step 3: logprobs[i][j] = logits[i][j] - lse[i] (optional, may be NULL) and
+ * target_logprobs[i] = logits[i][targets[i] - v_offset] - lse[i] for targets
+ * that fall in this shard (optional). */
+TBIK_API tbik_status tbik_logsoftmax_finish(const float* logits, int64_t ld, int64_t rows, int64_t v_local,
+                                   const float* lse, float* logprobs, int64_t ld_out,
+                                   const int64_t* targets, int64_t v_offset,
+                                   float* target_logprobs, void* stream);
+/* Single-device convenience: all three steps with `tp` simulated vocab shards. */
+TBIK_API tbik_status tbik_tree_logsoftmax_local(const float* logits, int64_t ld, int64_t rows, int64_t V,
+                                       int64_t groups, int tp, float* lse, float* logprobs,
+                                       int64_t ld_out, const int64_t* targets,
+                                       float* target_logprobs, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TBIK_B200_H_ */

@@ -1,0 +1,369 @@
+"""Python mirror of the reference's C++ API (proj/include/tbik/*.hpp) over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference, so the
+parity tests read like the reference's own checks (runner.cpp:53-214):
+
+  reference (C++, host Matrix)                 here (torch CUDA tensors)
+  -------------------------------------------  ---------------------------------------
+  BlockConfig / default_block_config            BlockConfig / default_block_config
+  plan_blocks (matmul.hpp:42-43)                plan_blocks
+  tree_matmul (matmul.hpp:53)                   tree_matmul(a, b, cfg, leaf=...)
+  DeviceGroup(int) (collective.hpp:17)          DeviceGroup(world_size)   (simulated, one GPU)
+  tree_all_reduce(_per_rank), ring_reduce_...   tree_all_reduce, tree_all_reduce_per_rank,
+                                                ring_reduce_baseline
+  make_row/column_shard_plan (layers.hpp:27-32) make_row_shard_plan, make_column_shard_plan
+  row/column_parallel_forward (layers.hpp)      row_parallel_forward, column_parallel_forward
+  rmsnorm (demo.hpp:53)                         rmsnorm  (tree-ordered)
+  (none: softmax_row is internal, demo.cpp:84)  log_softmax (vocab-sharded tree)
+  TbikError(ErrorCode) (errors.hpp)             TbikError(ErrorCode)
+
+Tensors: bf16 or f32, 2-D, on a CUDA device; outputs are f32 (the reference's
+F32_STORED output).  Work is queued on torch's current stream.  Nothing here
+falls back to the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Sequence
+
+from ._lib import (BlockConfigC, ErrorCode, ReductionPlanC, TBIK_IPC_HANDLE_BYTES, TbikError,
+                   check, lib)
+
+F32, BF16 = 0, 1
+LEAF_FMA, LEAF_TCGEN05 = 0, 1
+
+
+@dataclass
+class BlockConfig:
+    """tbik::BlockConfig (matmul.hpp:18-25)."""
+    block_m: int = 64
+    block_k: int = 256
+    block_n: int = 128
+    k_first: int = 0
+
+    def c(self) -> BlockConfigC:
+        return BlockConfigC(self.block_m, self.block_k, self.block_n, self.k_first)
+
+
+@dataclass(frozen=True)
+class ReductionPlan:
+    """tbik::ReductionPlan (matmul.hpp:30-35)."""
+    tiles_total: int
+    k_first: int
+    leaves: int
+    depth: int
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    """tbik::ShardPlan (layers.hpp:17-25)."""
+    mode: str  # "column" | "row"
+    tp_size: int
+    bounds: List[tuple]
+
+
+def default_block_config(dtype: int = BF16) -> BlockConfig:
+    c = BlockConfigC()
+    check(lib.tbik_default_block_config(dtype, C.byref(c)))
+    return BlockConfig(c.block_m, c.block_k, c.block_n, c.k_first)
+
+
+def plan_blocks(K: int, cfg: BlockConfig, c_max: int) -> ReductionPlan:
+    p = ReductionPlanC()
+    check(lib.tbik_plan_blocks(K, C.byref(cfg.c()), c_max, C.byref(p)))
+    return ReductionPlan(p.tiles_total, p.k_first, p.leaves, p.depth)
+
+
+def make_row_shard_plan(k: int, cfg: BlockConfig, tp_size: int, c_max: int) -> ShardPlan:
+    b = (C.c_int64 * (2 * max(tp_size, 1)))()
+    check(lib.tbik_make_row_shard_plan(k, C.byref(cfg.c()), tp_size, c_max, b))
+    return ShardPlan("row", tp_size, [(b[2 * r], b[2 * r + 1]) for r in range(tp_size)])
+
+
+def make_column_shard_plan(n: int, tp_size: int) -> ShardPlan:
+    b = (C.c_int64 * (2 * max(tp_size, 1)))()
+    check(lib.tbik_make_column_shard_plan(n, tp_size, b))
+    return ShardPlan("column", tp_size, [(b[2 * r], b[2 * r + 1]) for r in range(tp_size)])
+
+
+def device_available() -> bool:
+    return bool(lib.tbik_device_available())
+
+
+# ---- tensor helpers -----------------------------------------------------------------
+def _torch():
+    import torch
+    return torch
+
+
+def _dt(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.bfloat16:
+        return BF16
+    if t.dtype == torch.float32:
+        return F32
+    raise TbikError(ErrorCode.UnknownDtype, f"unsupported dtype {t.dtype}")
+
+
+def _mat(t, name: str):
+    if t.dim() != 2:
+        raise TbikError(ErrorCode.BadDimension, f"{name} must be 2-D")
+    if not t.is_cuda:
+        raise TbikError(ErrorCode.NoDevice, f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.stride(1) != 1:
+        raise TbikError(ErrorCode.BadArgument, f"{name} must be row-major (unit column stride)")
+    return C.c_void_p(t.data_ptr()), _dt(t), t.stride(0)
+
+
+def _stream():
+    return C.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+def _empty_f32(rows, cols, like):
+    return _torch().empty((rows, cols), dtype=_torch().float32, device=like.device)
+
+
+# ---- the TBIK GEMM --------------------------------------------------------------------
+def tree_matmul(a, b, cfg: BlockConfig | None = None, leaf: int = LEAF_TCGEN05, out=None):
+    """tree_matmul (matmul.hpp:53): C = A x B with the tree reduction over K; f32 out."""
+    cfg = cfg or default_block_config(BF16)
+    if a.shape[1] != b.shape[0]:
+        raise TbikError(ErrorCode.ShapeMismatch,
+                        f"tree_matmul: inner dimensions differ, {a.shape[1]} vs {b.shape[0]}")
+    M, K = a.shape
+    N = b.shape[1]
+    pa, da, lda = _mat(a, "A")
+    pb, db, ldb = _mat(b, "B")
+    out = _empty_f32(M, N, a) if out is None else out
+    pc, _, ldc = _mat(out, "C")
+    check(lib.tbik_tree_matmul(pa, da, lda, pb, db, ldb, pc, ldc, M, N, K, C.byref(cfg.c()), leaf,
+                               _stream()))
+    return out
+
+
+def tree_matmul_leaves(a, b, cfg: BlockConfig | None = None, leaf: int = LEAF_TCGEN05):
+    """Every leaf partial product P_t as leaves[t] (M x N f32) -- verification entry."""
+    cfg = cfg or default_block_config(BF16)
+    M, K = a.shape
+    N = b.shape[1]
+    T = plan_blocks(K, cfg, 1).tiles_total
+    out = _torch().empty((T, M, N), dtype=_torch().float32, device=a.device)
+    pa, da, lda = _mat(a, "A")
+    pb, db, ldb = _mat(b, "B")
+    check(lib.tbik_tree_matmul_leaves(pa, da, lda, pb, db, ldb, C.c_void_p(out.data_ptr()), M, N, K,
+                                      C.byref(cfg.c()), leaf, _stream()))
+    return out
+
+
+class DeviceGroup:
+    """tbik::DeviceGroup (collective.hpp:15-23): `world_size` simulated ranks on
+    the current GPU, exactly like the reference's in-process group."""
+
+    def __init__(self, world_size: int):
+        if world_size < 1 or world_size & (world_size - 1):
+            raise TbikError(ErrorCode.BadWorldSize,
+                            f"world size must be a power of two, got {world_size}")
+        self._w = world_size
+
+    def world_size(self) -> int:
+        return self._w
+
+
+def _ptr_array(ts: Sequence):
+    arr = (C.c_void_p * len(ts))()
+    for i, t in enumerate(ts):
+        arr[i] = t.data_ptr()
+    return arr
+
+
+def _require_uniform(group: DeviceGroup, xs: Sequence) -> None:
+    """require_uniform (collective.cpp:20-36)."""
+    if len(xs) != group.world_size():
+        raise TbikError(ErrorCode.CollectiveMismatch,
+                        f"expected {group.world_size()} contributions, got {len(xs)}")
+    for r, x in enumerate(xs[1:], 1):
+        if x.shape != xs[0].shape or x.dtype != xs[0].dtype:
+            raise TbikError(ErrorCode.CollectiveMismatch,
+                            f"rank {r} contribution shape/dtype differs")
+
+
+def all_gather(group: DeviceGroup, xs: Sequence) -> list:
+    """all_gather (collective.cpp:46-50): the rank-indexed list, unchanged."""
+    _require_uniform(group, xs)
+    return list(xs)
+
+
+def tree_all_reduce(group: DeviceGroup, xs: Sequence):
+    """tree_all_reduce (collective.hpp:38-39): Algorithm-2 order, f32 only."""
+    _require_uniform(group, xs)
+    torch = _torch()
+    if xs[0].dtype != torch.float32:
+        raise TbikError(ErrorCode.CollectiveMismatch, "tree_all_reduce expects f32 inputs")
+    xs = [x.contiguous() for x in xs]
+    out = torch.empty_like(xs[0])
+    check(lib.tbik_tree_all_reduce_local(_ptr_array(xs), len(xs), C.c_void_p(out.data_ptr()),
+                                         out.numel(), _stream()))
+    return out
+
+
+def tree_all_reduce_per_rank(group: DeviceGroup, xs: Sequence) -> list:
+    """tree_all_reduce_per_rank (collective.hpp:33-34): every simulated rank
+    reduces its own gathered copy; results are checked rank-symmetric
+    (collective.cpp:79-85) and CollectiveMismatch is raised otherwise."""
+    outs = [tree_all_reduce(group, xs) for _ in range(group.world_size())]
+    torch = _torch()
+    for r in range(1, len(outs)):
+        if not torch.equal(outs[0].view(torch.int32), outs[r].view(torch.int32)):
+            raise TbikError(ErrorCode.CollectiveMismatch,
+                            f"tree_all_reduce produced rank-divergent results at rank {r}")
+    return outs
+
+
+def ring_reduce_baseline(group: DeviceGroup, xs: Sequence):
+    """ring_reduce_baseline (collective.hpp:43-44): labelled non-invariant stand-in."""
+    _require_uniform(group, xs)
+    xs = [x.contiguous() for x in xs]
+    out = _torch().empty_like(xs[0])
+    check(lib.tbik_ring_reduce_local(_ptr_array(xs), len(xs), C.c_void_p(out.data_ptr()),
+                                     out.numel(), _stream()))
+    return out
+
+
+def row_parallel_forward(x, w, group: DeviceGroup, cfg: BlockConfig | None = None, c_max: int = 8,
+                         leaf: int = LEAF_TCGEN05, out=None):
+    """row_parallel_forward (layers.hpp:43-45) with simulated ranks on one GPU."""
+    cfg = cfg or default_block_config(BF16)
+    if x.shape[1] != w.shape[0]:
+        raise TbikError(ErrorCode.ShapeMismatch, "row_parallel_forward: inner dimensions differ")
+    M, K = x.shape
+    N = w.shape[1]
+    px, dx, ldx = _mat(x, "X")
+    pw, dw, ldw = _mat(w, "W")
+    out = _empty_f32(M, N, x) if out is None else out
+    py, _, ldy = _mat(out, "Y")
+    check(lib.tbik_row_parallel_forward_local(px, dx, ldx, pw, dw, ldw, py, ldy, M, N, K,
+                                              group.world_size(), C.byref(cfg.c()), c_max, leaf,
+                                              _stream()))
+    return out
+
+
+def column_parallel_forward(x, w, group: DeviceGroup, cfg: BlockConfig | None = None,
+                            leaf: int = LEAF_TCGEN05, out=None):
+    """column_parallel_forward (layers.hpp:36-38) with simulated ranks on one GPU."""
+    cfg = cfg or default_block_config(BF16)
+    if x.shape[1] != w.shape[0]:
+        raise TbikError(ErrorCode.ShapeMismatch, "column_parallel_forward: inner dimensions differ")
+    M, K = x.shape
+    N = w.shape[1]
+    px, dx, ldx = _mat(x, "X")
+    pw, dw, ldw = _mat(w, "W")
+    out = _empty_f32(M, N, x) if out is None else out
+    py, _, ldy = _mat(out, "Y")
+    check(lib.tbik_column_parallel_forward_local(px, dx, ldx, pw, dw, ldw, py, ldy, M, N, K,
+                                                 group.world_size(), C.byref(cfg.c()), leaf,
+                                                 _stream()))
+    return out
+
+
+# ---- tree-ordered reductions ----------------------------------------------------------
+def rmsnorm(x, gamma, eps: float = 1e-5, out_dtype=None):
+    """rmsnorm (demo.hpp:53) with the canonical tree sum of squares."""
+    torch = _torch()
+    rows, cols = x.shape
+    if gamma.numel() != cols:
+        raise TbikError(ErrorCode.ShapeMismatch, f"rmsnorm: gamma length {gamma.numel()} != cols {cols}")
+    out_dtype = out_dtype or torch.float32
+    out = torch.empty((rows, cols), dtype=out_dtype, device=x.device)
+    px, dx, ldx = _mat(x, "X")
+    g = gamma.to(torch.float32).contiguous()
+    check(lib.tbik_tree_rmsnorm(px, dx, ldx, C.c_void_p(g.data_ptr()), eps, C.c_void_p(out.data_ptr()),
+                                _dt(out), out.stride(0), rows, cols, _stream()))
+    return out
+
+
+def log_softmax(logits, groups: int = 8, tp: int = 1, targets=None, full: bool = True):
+    """Vocab-sharded tree log-softmax over `tp` simulated shards.
+    Returns (lse[rows], logprobs[rows, V] or None, target_logprobs[rows] or None)."""
+    torch = _torch()
+    rows, V = logits.shape
+    pl, dl, ld = _mat(logits, "logits")
+    if dl != F32:
+        raise TbikError(ErrorCode.UnknownDtype, "log_softmax expects f32 logits")
+    lse = torch.empty(rows, dtype=torch.float32, device=logits.device)
+    lp = torch.empty((rows, V), dtype=torch.float32, device=logits.device) if full else None
+    tlp = None
+    tg = None
+    if targets is not None:
+        tg = targets.to(torch.int64).contiguous()
+        tlp = torch.empty(rows, dtype=torch.float32, device=logits.device)
+    check(lib.tbik_tree_logsoftmax_local(
+        pl, ld, rows, V, groups, tp, C.c_void_p(lse.data_ptr()),
+        C.c_void_p(lp.data_ptr()) if lp is not None else None, V,
+        C.c_void_p(tg.data_ptr()) if tg is not None else None,
+        C.c_void_p(tlp.data_ptr()) if tlp is not None else None, _stream()))
+    return lse, lp, tlp
+
+
+def sync() -> None:
+    check(lib.tbik_sync(_stream()))
+
+
+# ---- one process per GPU ----------------------------------------------------------------
+class PeerGroup:
+    """DeviceGroup whose ranks are processes (one per GPU) joined over NVLink peer
+    memory.  Handles are exchanged with torch.distributed (any backend: gloo
+    works for the exchange; the data path never touches it)."""
+
+    def __init__(self, world_size: int, rank: int, device: int, capacity_elems: int, dist=None):
+        h = C.c_void_p()
+        check(lib.tbik_group_create(world_size, rank, device, capacity_elems, C.byref(h)))
+        self._h = h
+        self.world = world_size
+        self.rank = rank
+        mine = (C.c_char * TBIK_IPC_HANDLE_BYTES)()
+        check(lib.tbik_group_ipc_handle(h, mine))
+        handles = exchange_handles(bytes(mine), world_size, dist)
+        blob = (C.c_char * (TBIK_IPC_HANDLE_BYTES * world_size)).from_buffer_copy(b"".join(handles))
+        check(lib.tbik_group_open_peers(h, blob))
+
+    def close(self) -> None:
+        if self._h:
+            lib.tbik_group_destroy(self._h)
+            self._h = None
+
+    def tree_all_reduce(self, partial, out=None):
+        torch = _torch()
+        out = torch.empty_like(partial) if out is None else out
+        check(lib.tbik_group_tree_all_reduce(self._h, C.c_void_p(partial.data_ptr()),
+                                             C.c_void_p(out.data_ptr()), partial.numel(), _stream()))
+        return out
+
+    def row_parallel_forward(self, x_shard, w_shard, K_global: int, cfg: BlockConfig | None = None,
+                             c_max: int = 8, leaf: int = LEAF_TCGEN05, out=None):
+        cfg = cfg or default_block_config(BF16)
+        M = x_shard.shape[0]
+        N = w_shard.shape[1]
+        px, dx, ldx = _mat(x_shard, "X")
+        pw, dw, ldw = _mat(w_shard, "W")
+        out = _empty_f32(M, N, x_shard) if out is None else out
+        check(lib.tbik_group_row_parallel_forward(self._h, px, dx, ldx, pw, dw, ldw,
+                                                  C.c_void_p(out.data_ptr()), N, M, N, K_global,
+                                                  C.byref(cfg.c()), c_max, leaf, _stream()))
+        return out
+
+
+def exchange_handles(mine: bytes, world_size: int, dist=None) -> list:
+    """Rank-indexed all-gather of the fixed-size IPC handle blobs (host metadata
+    only).  Pure function of the inputs: the result is ordered by rank, never by
+    arrival (collective.cpp:46-50)."""
+    if world_size == 1:
+        return [mine]
+    if dist is None:
+        import torch.distributed as dist  # noqa: F811
+    gathered: list = [None] * world_size
+    dist.all_gather_object(gathered, mine)
+    for r, blob in enumerate(gathered):
+        if not isinstance(blob, (bytes, bytearray)) or len(blob) != TBIK_IPC_HANDLE_BYTES:
+            raise TbikError(ErrorCode.CollectiveMismatch, f"bad handle blob from rank {r}")
+    return [bytes(b) for b in gathered]

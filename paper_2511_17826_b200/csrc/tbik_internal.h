@@ -1,0 +1,60 @@
+// tbik_internal.h -- launcher interfaces shared by the C ABI translation unit
+// and the kernel translation units.  Not installed; not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "tbik_b200.h"
+
+namespace tbik_b200 {
+
+constexpr int kMaxRanks = 64;
+
+struct PartPtrs {
+  const float* p[kMaxRanks];
+};
+
+// Output layout of one GEMM launch.  A "unit" is the K range one CTA column
+// reduces:
+//   OUT_FULL    all tiles of the view, full tree  -> C[M x N] (ldo)
+//   OUT_UNITS   2^j whole leaf groups per unit    -> subtree value -> ws[unit][M][N]
+//   OUT_LEAVES  one tile per unit                 -> P_t          -> ws[t][M][N]
+//   OUT_GROUPS  one leaf group per unit (FMA)     -> group value  -> ws[g][M][N]
+enum OutMode { OUT_FULL = 0, OUT_UNITS = 1, OUT_LEAVES = 2, OUT_GROUPS = 3 };
+
+struct GemmView {
+  const void* A;
+  int adt;
+  int64_t lda;
+  const void* B;
+  int bdt;
+  int64_t ldb;
+  int64_t M, N, K;  // K = this view's extent (a rank shard or the whole K)
+  int64_t bk, kf;   // numerics-defining plan (kf = global k_first)
+  int64_t T, L;     // tiles in the view, leaf groups in the view (power of two)
+};
+
+struct GemmOut {
+  int mode;            // OutMode
+  int64_t tiles_per_unit;
+  float* out;          // C (FULL) or workspace base
+  int64_t ldo;         // row stride of C / of one workspace slice (= N)
+  int64_t unit_stride; // elements between workspace slices
+};
+
+tbik_status launch_fma_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s);
+tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s);
+bool tc_supported(const GemmView& v, std::string* why);
+
+tbik_status launch_tree_combine(const float* ws, int64_t X, int64_t fold, int64_t rows,
+                                int64_t cols, float* out, int64_t ldo, cudaStream_t s);
+tbik_status launch_allreduce(const PartPtrs& parts, int W, float* out, int64_t elems, bool ring,
+                             bool aligned16, cudaStream_t s);
+
+// Whole tree GEMM (plan resolved by the caller): picks FULL vs split + combine.
+tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mode, cudaStream_t s);
+
+}  // namespace tbik_b200

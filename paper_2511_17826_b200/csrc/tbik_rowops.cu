@@ -1,0 +1,381 @@
+// tbik_rowops.cu -- tree-ordered RMSNorm and vocab-sharded log-softmax /
+// log-prob (NEW semantics; the reference has only the sequential rmsnorm,
+// demo.cpp:11-34, and softmax_row, demo.cpp:84-97).  The canonical orders are
+// defined, and restated on the CPU, in oracle/tbik_oracle.c
+// (tbo_tree_rmsnorm, tbo_tree_logsoftmax); this file must match it bit for bit.
+//
+// Both are HBM-bound row reductions: one 256-thread CTA per (row, vocab group),
+// 16-byte loads, lane l folding chunks l, l+256, ... in ascending order, then
+// a contiguous-halves tree: warp butterfly (xor 1, 2, 4, 8, 16 -- each level
+// pairs adjacent subtrees, so it IS the contiguous-halves tree) and a fixed
+// 8-warp tree through shared memory.
+#include <math.h>
+
+#include <algorithm>
+#include <string>
+
+#include "tbik_common.cuh"
+#include "tbik_internal.h"
+
+namespace tbik_b200 {
+namespace {
+
+constexpr int LANES = 256;
+
+// ---- shared exp / log: the exact op sequence of tbo_exp / tbo_log ----------
+__device__ __forceinline__ float tb_exp(float x) {
+  if (x != x) return x;
+  if (x < -103.0f) return 0.0f;
+  if (x > 88.5f) return __int_as_float(0x7F800000);
+  const float magic = 12582912.0f;
+  const float t = __fmaf_rn(x, 1.44269502162933349609f, magic);
+  const float kf = __fsub_rn(t, magic);
+  float r = __fmaf_rn(kf, -0.693359375f, x);
+  r = __fmaf_rn(kf, 2.12194440e-4f, r);
+  float p = 1.9875691500e-4f;
+  p = __fmaf_rn(p, r, 1.3981999507e-3f);
+  p = __fmaf_rn(p, r, 8.3334519073e-3f);
+  p = __fmaf_rn(p, r, 4.1665795894e-2f);
+  p = __fmaf_rn(p, r, 1.6666665459e-1f);
+  p = __fmaf_rn(p, r, 5.0000001201e-1f);
+  const float r2 = __fmul_rn(r, r);
+  float y = __fmaf_rn(p, r2, r);
+  y = __fadd_rn(y, 1.0f);
+  int k = static_cast<int>(kf);
+  if (k < -125) {
+    y = __fmul_rn(y, __uint_as_float(static_cast<uint32_t>(127 - 64) << 23));
+    k += 64;
+  }
+  return __fmul_rn(y, __uint_as_float(static_cast<uint32_t>(k + 127) << 23));
+}
+
+__device__ __forceinline__ float tb_log(float x) {
+  if (!(x > 0.0f)) return x == 0.0f ? __int_as_float(0xFF800000) : __int_as_float(0x7FC00000);
+  if (x == __int_as_float(0x7F800000)) return x;
+  uint32_t u = __float_as_uint(x);
+  int e = 0;
+  if ((u & 0x7F800000u) == 0) {
+    x = __fmul_rn(x, 4294967296.0f);
+    u = __float_as_uint(x);
+    e = -32;
+  }
+  e += static_cast<int>((u >> 23) & 0xFF) - 127;
+  float m = __uint_as_float((u & 0x007FFFFFu) | 0x3F800000u);
+  if (m > 1.41421356237309504880f) {
+    m = __fmul_rn(m, 0.5f);
+    e += 1;
+  }
+  const float xm = __fsub_rn(m, 1.0f);
+  const float z = __fmul_rn(xm, xm);
+  float p = 7.0376836292e-2f;
+  p = __fmaf_rn(p, xm, -1.1514610310e-1f);
+  p = __fmaf_rn(p, xm, 1.1676998740e-1f);
+  p = __fmaf_rn(p, xm, -1.2420140846e-1f);
+  p = __fmaf_rn(p, xm, 1.4249322787e-1f);
+  p = __fmaf_rn(p, xm, -1.6668057665e-1f);
+  p = __fmaf_rn(p, xm, 2.0000714765e-1f);
+  p = __fmaf_rn(p, xm, -2.4999993993e-1f);
+  p = __fmaf_rn(p, xm, 3.3333331174e-1f);
+  float y = __fmul_rn(p, xm);
+  y = __fmul_rn(y, z);
+  const float fe = static_cast<float>(e);
+  y = __fmaf_rn(fe, -2.12194440e-4f, y);
+  y = __fmaf_rn(z, -0.5f, y);
+  float r = __fadd_rn(xm, y);
+  r = __fmaf_rn(fe, 0.693359375f, r);
+  return r;
+}
+
+// ---- (m, s) operator ---------------------------------------------------------
+struct MS {
+  float m, s;
+};
+
+__device__ __forceinline__ MS ms_fold(MS st, float x) {
+  if (x == __int_as_float(0xFF800000)) return st;
+  if (x <= st.m) {
+    st.s = __fadd_rn(st.s, tb_exp(__fsub_rn(x, st.m)));
+  } else {
+    st.s = __fmul_rn(st.s, tb_exp(__fsub_rn(st.m, x)));
+    st.s = __fadd_rn(st.s, 1.0f);
+    st.m = x;
+  }
+  return st;
+}
+
+__device__ __forceinline__ MS ms_merge(MS lo, MS hi) {
+  if (lo.m == __int_as_float(0xFF800000)) return hi;
+  if (hi.m == __int_as_float(0xFF800000)) return lo;
+  const float m = lo.m >= hi.m ? lo.m : hi.m;
+  const float a = __fmul_rn(lo.s, tb_exp(__fsub_rn(lo.m, m)));
+  const float b = __fmul_rn(hi.s, tb_exp(__fsub_rn(hi.m, m)));
+  return MS{m, __fadd_rn(a, b)};
+}
+
+// Contiguous-halves tree over the 256 lane values of a CTA.
+__device__ __forceinline__ float block_tree_sum(float v, float* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, d));
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  float r = 0.0f;
+  if (threadIdx.x == 0) {
+    const float a = __fadd_rn(sh[0], sh[1]), b = __fadd_rn(sh[2], sh[3]);
+    const float c = __fadd_rn(sh[4], sh[5]), d = __fadd_rn(sh[6], sh[7]);
+    r = __fadd_rn(__fadd_rn(a, b), __fadd_rn(c, d));
+    sh[8] = r;
+  }
+  __syncthreads();
+  return sh[8];
+}
+
+__device__ __forceinline__ MS block_tree_ms(MS v, MS* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    MS o{__shfl_xor_sync(0xffffffffu, v.m, d), __shfl_xor_sync(0xffffffffu, v.s, d)};
+    v = (lane & d) ? ms_merge(o, v) : ms_merge(v, o);  // always merge(lower, upper)
+  }
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const MS a = ms_merge(sh[0], sh[1]), b = ms_merge(sh[2], sh[3]);
+    const MS c = ms_merge(sh[4], sh[5]), d = ms_merge(sh[6], sh[7]);
+    sh[8] = ms_merge(ms_merge(a, b), ms_merge(c, d));
+  }
+  __syncthreads();
+  return sh[8];
+}
+
+// ---- RMSNorm ------------------------------------------------------------------
+template <typename TX, typename TY, bool VEC>
+__global__ void __launch_bounds__(LANES) tree_rmsnorm_kernel(const TX* __restrict__ X, int64_t ldx,
+                                                             const float* __restrict__ gamma, float eps,
+                                                             TY* __restrict__ Y, int64_t ldy, int64_t cols) {
+  __shared__ float sh[9];
+  constexpr int CH = 16 / sizeof(TX);  // 8 bf16 or 4 f32 per chunk
+  const TX* x = X + static_cast<int64_t>(blockIdx.x) * ldx;
+  const int64_t nch = (cols + CH - 1) / CH;
+  float acc = 0.0f;
+  for (int64_t c = threadIdx.x; c < nch; c += LANES) {
+    const int64_t e0 = c * CH;
+    if (VEC && e0 + CH <= cols) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(x + e0);
+      const TX* v = reinterpret_cast<const TX*>(&raw);
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        const float f = load_as_f32(v + i);
+        acc = __fmaf_rn(f, f, acc);
+      }
+    } else {
+      for (int64_t e = e0; e < e0 + CH && e < cols; ++e) {
+        const float f = load_as_f32(x + e);
+        acc = __fmaf_rn(f, f, acc);
+      }
+    }
+  }
+  const float ss = block_tree_sum(acc, sh);
+  const float ms = __fdiv_rn(ss, static_cast<float>(cols));
+  const float denom = __fsqrt_rn(__fadd_rn(ms, eps));
+  TY* y = Y + static_cast<int64_t>(blockIdx.x) * ldy;
+  for (int64_t e = threadIdx.x; e < cols; e += LANES) {
+    const float r = __fdiv_rn(__fmul_rn(load_as_f32(x + e), gamma[e]), denom);
+    if constexpr (sizeof(TY) == 4)
+      y[e] = r;
+    else
+      y[e] = f32_to_bf16_bits(r);
+  }
+}
+
+// ---- log-softmax ----------------------------------------------------------------
+// Group states: one CTA per (row, group) of n = v_local / groups logits.
+template <bool VEC>
+__global__ void __launch_bounds__(LANES) ms_group_kernel(const float* __restrict__ logits, int64_t ld, int64_t n,
+                                                         int64_t groups, MS* __restrict__ out) {
+  __shared__ MS sh[9];
+  const int64_t row = blockIdx.x, g = blockIdx.y;
+  const float* x = logits + row * ld + g * n;
+  const int64_t nch = (n + 3) / 4;
+  MS st{__int_as_float(0xFF800000), 0.0f};
+  for (int64_t c = threadIdx.x; c < nch; c += LANES) {
+    const int64_t e0 = c * 4;
+    if (VEC && e0 + 4 <= n) {
+      const float4 v = *reinterpret_cast<const float4*>(x + e0);
+      st = ms_fold(st, v.x);
+      st = ms_fold(st, v.y);
+      st = ms_fold(st, v.z);
+      st = ms_fold(st, v.w);
+    } else {
+      for (int64_t e = e0; e < e0 + 4 && e < n; ++e) st = ms_fold(st, x[e]);
+    }
+  }
+  const MS r = block_tree_ms(st, sh);
+  if (threadIdx.x == 0) out[row * groups + g] = r;
+}
+
+// Contiguous-halves tree over `count` (power of two) states per row.
+__device__ MS ms_tree(const MS* v, int64_t count) {
+  // iterative binary counter (merge order lower, upper)
+  MS stack[32];
+  for (int64_t i = 0; i < count; ++i) {
+    MS cur = v[i];
+    int l = 0;
+    uint64_t c = static_cast<uint64_t>(i);
+    while (c & 1u) {
+      cur = ms_merge(stack[l], cur);
+      c >>= 1;
+      ++l;
+    }
+    stack[l] = cur;
+  }
+  int j = 0;
+  while ((int64_t{1} << j) < count) ++j;
+  return stack[j];
+}
+
+__global__ void ms_rows_kernel(const MS* __restrict__ group_states, int64_t rows, int64_t groups,
+                               float* __restrict__ ms_out) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  const MS r = ms_tree(group_states + row * groups, groups);
+  ms_out[2 * row] = r.m;
+  ms_out[2 * row + 1] = r.s;
+}
+
+__global__ void ms_merge_kernel(PartPtrs parts, int W, int64_t rows, float* __restrict__ lse) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  MS v[kMaxRanks];
+  for (int r = 0; r < W; ++r) v[r] = MS{parts.p[r][2 * row], parts.p[r][2 * row + 1]};
+  const MS t = ms_tree(v, W);
+  lse[row] = __fadd_rn(t.m, tb_log(t.s));
+}
+
+__global__ void finish_kernel(const float* __restrict__ logits, int64_t ld, int64_t rows, int64_t v_local,
+                              const float* __restrict__ lse, float* __restrict__ logprobs, int64_t ld_out,
+                              const int64_t* __restrict__ targets, int64_t v_offset, float* __restrict__ tlp) {
+  const int64_t row = blockIdx.y;
+  const float l = lse[row];
+  if (logprobs) {
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < v_local;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      logprobs[row * ld_out + j] = __fsub_rn(logits[row * ld + j], l);
+  }
+  if (targets && tlp && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t t = targets[row] - v_offset;
+    if (t >= 0 && t < v_local) tlp[row] = __fsub_rn(logits[row * ld + t], l);
+  }
+}
+
+}  // namespace
+}  // namespace tbik_b200
+
+using namespace tbik_b200;
+
+extern "C" {
+
+tbik_status tbik_tree_rmsnorm(const void* X, int x_dtype, int64_t ldx, const float* gamma, float eps, void* Y,
+                              int y_dtype, int64_t ldy, int64_t rows, int64_t cols, void* stream) {
+  if (!X || !Y || !gamma) return set_error(TBIK_BAD_ARGUMENT, "null argument");
+  if (rows < 1 || cols < 1) return set_error(TBIK_BAD_DIMENSION, "rmsnorm: dimensions must be >= 1");
+  if (ldx < cols || ldy < cols) return set_error(TBIK_BAD_ARGUMENT, "rmsnorm: leading dimension < cols");
+  if ((x_dtype != TBIK_F32 && x_dtype != TBIK_BF16) || (y_dtype != TBIK_F32 && y_dtype != TBIK_BF16))
+    return set_error(TBIK_UNKNOWN_DTYPE, "rmsnorm: dtype");
+  if (rows > 0x7FFFFFFF) return set_error(TBIK_UNSUPPORTED, "rmsnorm: too many rows");
+  if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t esz = x_dtype == TBIK_BF16 ? 2 : 4;
+  const bool vec = (reinterpret_cast<uintptr_t>(X) & 15) == 0 && (ldx * esz) % 16 == 0;
+  const unsigned g = static_cast<unsigned>(rows);
+#define TBIK_RMS(TX, TY)                                                                                   \
+  (vec ? (tree_rmsnorm_kernel<TX, TY, true><<<g, LANES, 0, s>>>(static_cast<const TX*>(X), ldx, gamma, eps,  \
+                                                                static_cast<TY*>(Y), ldy, cols),             \
+          0)                                                                                                 \
+       : (tree_rmsnorm_kernel<TX, TY, false><<<g, LANES, 0, s>>>(static_cast<const TX*>(X), ldx, gamma, eps, \
+                                                                 static_cast<TY*>(Y), ldy, cols),            \
+          0))
+  if (x_dtype == TBIK_BF16 && y_dtype == TBIK_F32) TBIK_RMS(uint16_t, float);
+  else if (x_dtype == TBIK_BF16) TBIK_RMS(uint16_t, uint16_t);
+  else if (y_dtype == TBIK_F32) TBIK_RMS(float, float);
+  else TBIK_RMS(float, uint16_t);
+#undef TBIK_RMS
+  TBIK_CUDA(cudaGetLastError());
+  return TBIK_OK;
+}
+
+tbik_status tbik_logsoftmax_shard_state(const float* logits, int64_t ld, int64_t rows, int64_t v_local, int64_t groups,
+                                        float* ms_out, void* stream) {
+  if (!logits || !ms_out) return set_error(TBIK_BAD_ARGUMENT, "null argument");
+  if (rows < 1 || v_local < 1) return set_error(TBIK_BAD_DIMENSION, "logsoftmax: dimensions must be >= 1");
+  if (groups < 1 || (groups & (groups - 1)) || v_local % groups)
+    return set_error(TBIK_SHARD_ERROR, "logsoftmax: shard of " + std::to_string(v_local) +
+                                           " logits is not a power-of-two number of equal groups (" +
+                                           std::to_string(groups) + ")");
+  if (ld < v_local) return set_error(TBIK_BAD_ARGUMENT, "logsoftmax: ld < v_local");
+  if (rows > 0x7FFFFFFF || groups > 65535) return set_error(TBIK_UNSUPPORTED, "logsoftmax: grid too large");
+  if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t n = v_local / groups;
+  MS* gs = static_cast<MS*>(workspace(static_cast<size_t>(rows) * groups * sizeof(MS), 3));
+  if (!gs) return set_error(TBIK_CUDA_ERROR, "workspace allocation failed");
+  const bool vec = (reinterpret_cast<uintptr_t>(logits) & 15) == 0 && ld % 4 == 0 && n % 4 == 0;
+  dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>(groups));
+  if (vec)
+    ms_group_kernel<true><<<grid, LANES, 0, s>>>(logits, ld, n, groups, gs);
+  else
+    ms_group_kernel<false><<<grid, LANES, 0, s>>>(logits, ld, n, groups, gs);
+  TBIK_CUDA(cudaGetLastError());
+  ms_rows_kernel<<<static_cast<unsigned>((rows + 127) / 128), 128, 0, s>>>(gs, rows, groups, ms_out);
+  TBIK_CUDA(cudaGetLastError());
+  return TBIK_OK;
+}
+
+tbik_status tbik_logsoftmax_merge(const float* const* ms_parts, int W, int64_t rows, float* lse, void* stream) {
+  if (!ms_parts || !lse) return set_error(TBIK_BAD_ARGUMENT, "null argument");
+  if (W < 1 || (W & (W - 1)) || W > kMaxRanks) return set_error(TBIK_BAD_WORLD_SIZE, "world size must be a power of two");
+  if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
+  PartPtrs pp{};
+  for (int r = 0; r < W; ++r) pp.p[r] = ms_parts[r];
+  ms_merge_kernel<<<static_cast<unsigned>((rows + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(pp, W, rows,
+                                                                                                        lse);
+  TBIK_CUDA(cudaGetLastError());
+  return TBIK_OK;
+}
+
+tbik_status tbik_logsoftmax_finish(const float* logits, int64_t ld, int64_t rows, int64_t v_local, const float* lse,
+                                   float* logprobs, int64_t ld_out, const int64_t* targets, int64_t v_offset,
+                                   float* target_logprobs, void* stream) {
+  if (!logits || !lse) return set_error(TBIK_BAD_ARGUMENT, "null argument");
+  if (rows > 65535) return set_error(TBIK_UNSUPPORTED, "logsoftmax finish: > 65535 rows per call");
+  if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
+  const int64_t xblocks = logprobs ? std::min<int64_t>((v_local + 1023) / 1024, 64) : 1;
+  dim3 grid(static_cast<unsigned>(xblocks), static_cast<unsigned>(rows));
+  finish_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(logits, ld, rows, v_local, lse, logprobs, ld_out,
+                                                                     targets, v_offset, target_logprobs);
+  TBIK_CUDA(cudaGetLastError());
+  return TBIK_OK;
+}
+
+tbik_status tbik_tree_logsoftmax_local(const float* logits, int64_t ld, int64_t rows, int64_t V, int64_t groups, int tp,
+                                       float* lse, float* logprobs, int64_t ld_out, const int64_t* targets,
+                                       float* target_logprobs, void* stream) {
+  if (tp < 1 || (tp & (tp - 1)) || tp > kMaxRanks) return set_error(TBIK_BAD_WORLD_SIZE, "tp must be a power of two");
+  if (V % tp || groups % tp)
+    return set_error(TBIK_SHARD_ERROR, "vocab / groups not divisible by tp=" + std::to_string(tp));
+  const int64_t vl = V / tp;
+  float* ms = static_cast<float*>(workspace(static_cast<size_t>(rows) * 2 * tp * sizeof(float), 2));
+  if (!ms) return set_error(TBIK_CUDA_ERROR, "workspace allocation failed");
+  PartPtrs pp{};
+  for (int r = 0; r < tp; ++r) {
+    TBIK_TRY(tbik_logsoftmax_shard_state(logits + r * vl, ld, rows, vl, groups / tp, ms + 2 * rows * r, stream));
+    pp.p[r] = ms + 2 * rows * r;
+  }
+  TBIK_TRY(tbik_logsoftmax_merge(pp.p, tp, rows, lse, stream));
+  for (int r = 0; r < tp; ++r)
+    TBIK_TRY(tbik_logsoftmax_finish(logits + r * vl, ld, rows, vl, lse, logprobs ? logprobs + r * vl : nullptr,
+                                    ld_out, targets, r * vl, target_logprobs, stream));
+  return TBIK_OK;
+}
+
+}  // extern "C"
