@@ -1,0 +1,416 @@
+#!/usr/bin/env python
+"""bench.py -- TBIK row-parallel GEMM (+ fixed-order tree all-reduce) on B200.
+
+Workload (BASELINE.json configs[1]): the Llama-3.1-8B-shaped row-parallel
+down_proj, K = 14336, N = 4096, M = 4096 tokens (16 x 256-token prompts),
+bf16 inputs, f32 TBIK output, tensor-core leaves (TBIK_LEAF_TCGEN05,
+block_k = 256, k_first = 7, 8 leaf groups).  With --gpus N the K dimension is
+sharded with make_row_shard_plan (layers.cpp:23-46) over N processes, each
+GPU runs the TBIK GEMM on its K range straight into its peer-visible buffer
+and the partials meet in the NVLink tree all-reduce (strong scaling: the total
+work is fixed).  A "step" is one row-parallel forward over the whole batch.
+
+One JSON line (rank 0):
+  value           whole-job TFLOP/s = 2*M*N*K / device time per step (max over ranks)
+  e2e             same metric through the C ABI with HOST buffers: per step the
+                  H2D copy of x (pinned) and the D2H read of y are inside the timed region
+  roofline        the dominant kernel (tc_tree_gemm_kernel): algorithmic FLOPs per
+                  launch / its CUDA-event duration vs MEASURED_PEAKS bf16 (burst)
+  cpu_baseline    the unmodified reference library (oracle/_ref) on this host's cores
+  noninvariant    cuBLAS bf16 GEMM (+ NCCL bf16 all-reduce at N > 1): the price of determinism
+  sweep           M = 1 .. 4096 for the TC leaf, the exact (FMA) leaf and cuBLAS (rank 0, N = 1)
+  tp_invariance   simulated TP = 1/2/4/8 bit-identity on this GPU (checked every run)
+`--impl reference` times the reference's own CPU row_parallel_forward instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+K_FULL, N_OUT = 14336, 4096
+METRIC = "TBIK row-parallel GEMM TFLOP/s at TP=1/2/4/8; bit-exact logits across TP"
+WORKLOAD = "llama3.1-8b down_proj row-parallel (K=14336, N=4096) + tree all-reduce"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["tbik", "reference"], default="tbik")
+    ap.add_argument("--m", type=int, default=4096)
+    ap.add_argument("--leaf", choices=["tc", "fma"], default="tc")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p["hbm_gbs"], "measured (MEASURED_PEAKS.json, burst bf16)"
+    except Exception:  # noqa: BLE001
+        return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(M, tp):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        return t.get(f"M{M}_tp{tp}")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampler running DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+            out = ""
+        sms, mx, reasons, samples = [], None, set(), 0
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            samples += 1
+            try:
+                sm = float(f[1])
+                mx = float(f[2])
+            except ValueError:
+                continue
+            sms.append(sm)
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for name, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        sms.sort()
+        busy = [s for s in sms if s > 500] or sms
+        med = busy[len(busy) // 2] if busy else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": samples}
+
+
+def ev_time(fn, reps, stream=None):
+    """Device time (ms) per call of fn with CUDA events on the current stream."""
+    import torch
+    s = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(s)
+    for _ in range(reps):
+        fn()
+    b.record(s)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+# ------------------------------------------------------------------------------------
+# reference arm: the unmodified reference library on the host cores
+# ------------------------------------------------------------------------------------
+def cpu_reference_sample(tp: int, m_sample: int, budget_s: float, min_reps: int = 1):
+    import numpy as np
+
+    from oracle.oracle import RefLib
+    ref = RefLib()
+    threads = os.cpu_count() or 1
+    ref.set_threads(threads)
+    a = ref.random_normal(1, 1, m_sample, K_FULL)
+    w = ref.random_normal(1, 2, K_FULL, N_OUT)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < min_reps or (time.perf_counter() - t_start < budget_s and len(times) < 50):
+        t0 = time.perf_counter()
+        y = ref.row_parallel_forward(a, w, tp)
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    flops = 2.0 * m_sample * N_OUT * K_FULL
+    fp = ref.fingerprint(np.ascontiguousarray(y))
+    return {"value": flops / best / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
+            "sample": f"row_parallel_forward(DeviceGroup({tp})) on M={m_sample} rows of the "
+                      f"{K_FULL}x{N_OUT} down_proj, bf16 N(0,1) Rng(1,1)/(1,2), best of {len(times)} "
+                      f"wall-clock runs ({sum(times):.1f} s of CPU work), TBIK_THREADS={threads}",
+            "fingerprint": "0x%016x" % fp, "seconds_per_call": best}
+
+
+def run_reference(args):
+    rank, _, world = env_rank()
+    if rank != 0:
+        return
+    tp = args.gpus
+    m_sample = 16
+    import numpy as np
+
+    from oracle.oracle import RefLib
+    ref = RefLib()
+    threads = os.cpu_count() or 1
+    ref.set_threads(threads)
+    a = ref.random_normal(1, 1, m_sample, K_FULL)
+    w = ref.random_normal(1, 2, K_FULL, N_OUT)
+    for _ in range(args.warmup):
+        ref.row_parallel_forward(a, w, tp)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        y = ref.row_parallel_forward(a, w, tp)
+    dt = (time.perf_counter() - t0) / args.steps
+    flops = 2.0 * m_sample * N_OUT * K_FULL
+    value = flops / dt / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (reference Rng, N(0,1) bf16)",
+        "config": {"workload": WORKLOAD, "M": m_sample, "M_note": "bounded CPU sample of the M=4096 workload",
+                   "K": K_FULL, "N": N_OUT, "tp": tp, "parallelism": f"tp{tp} (simulated ranks on host threads)",
+                   "block_k": 256},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
+                         "sample": f"row_parallel_forward(DeviceGroup({tp})) M={m_sample} rows per step"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "fingerprint": "0x%016x" % ref.fingerprint(np.ascontiguousarray(y)),
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------------------------
+# TBIK arm
+# ------------------------------------------------------------------------------------
+def run_tbik(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_17826_b200 as tb
+
+    rank, local_rank, world = env_rank()
+    if world != args.gpus:
+        world = args.gpus if world == 1 else world
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    leaf = tb.LEAF_TCGEN05 if args.leaf == "tc" else tb.LEAF_FMA
+    cfg = tb.BlockConfig(64, 256, 128, 0)
+    M = args.m
+    shard = tb.make_row_shard_plan(K_FULL, cfg, world, 8)
+    kb, ke = shard.bounds[rank]
+    Kr = ke - kb
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234)
+    w_full_rows = torch.randn(K_FULL, N_OUT, device=dev, generator=g, dtype=torch.float32)
+    w = w_full_rows[kb:ke].to(torch.bfloat16).contiguous()
+    del w_full_rows
+    x_full = torch.randn(M, K_FULL, device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
+    x = x_full[:, kb:ke].contiguous()
+    y = torch.empty(M, N_OUT, device=dev, dtype=torch.float32)
+
+    group = None
+    if world > 1:
+        group = tb.PeerGroup(world, rank, local_rank, M * N_OUT, dist)
+
+        def step():
+            group.row_parallel_forward(x, w, K_FULL, cfg, 8, leaf, out=y)
+    else:
+        def step():
+            tb.tree_matmul(x, w, cfg, leaf, out=y)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warmup + timed region -----------------------------------------------------
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    clocks = Clocks(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = tb.launch_count()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(args.steps):
+        step()
+    e1.record(s)
+    torch.cuda.synchronize()
+    launches = tb.launch_count() - launches0
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    flops = 2.0 * M * N_OUT * K_FULL
+    value = flops / (ms * 1e-3) / 1e12
+
+    # ---- the dominant kernel on its own (roofline) -----------------------------------
+    k_ms = ev_time(lambda: tb.tree_matmul(x, w, cfg, leaf, out=y), max(args.steps, 5))
+    k_flops = 2.0 * M * N_OUT * Kr
+    achieved = k_flops / (k_ms * 1e-3) / 1e12
+    peak_tf, peak_hbm, peak_src = load_peaks()
+    bytes_alg = 2.0 * M * Kr + 2.0 * Kr * N_OUT + 4.0 * M * N_OUT
+    intensity = k_flops / bytes_alg
+    tensor_bound = intensity > peak_tf * 1e12 / (peak_hbm * 1e9)
+    if tensor_bound:
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": achieved / peak_tf}
+    else:
+        gbs = bytes_alg / (k_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": gbs, "peak": peak_hbm, "unit": "GB/s", "frac": gbs / peak_hbm}
+    roof.update({"traffic": load_traffic(M, world), "kernel": "tc_tree_gemm_kernel" if leaf else "fma_tree_gemm_kernel",
+                 "kernel_ms": k_ms, "flops_per_launch": k_flops, "alg_bytes_per_launch": bytes_alg,
+                 "peak_source": peak_src, "share_of_step": k_ms / ms if ms else None})
+
+    # ---- e2e through the C ABI with host buffers ----------------------------------------
+    x_host = x.cpu().pin_memory()
+    y_host = torch.empty(M, N_OUT, dtype=torch.float32).pin_memory()
+    x_dev = torch.empty_like(x)
+
+    def e2e_step():
+        x_dev.copy_(x_host, non_blocking=True)
+        if group is not None:
+            group.row_parallel_forward(x_dev, w, K_FULL, cfg, 8, leaf, out=y)
+        else:
+            tb.tree_matmul(x_dev, w, cfg, leaf, out=y)
+        y_host.copy_(y, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    e2e_ms = max_over_ranks(ev_time(e2e_step, max(args.steps // 2, 3)))
+    e2e = {"value": flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+           "h2d_bytes_per_step": x_host.numel() * x_host.element_size(),
+           "d2h_bytes_per_step": y_host.numel() * y_host.element_size(),
+           "ms_per_step": e2e_ms,
+           "path": "pinned host x -> H2D -> tbik_tree_matmul / tbik_group_row_parallel_forward (C ABI) -> D2H y"}
+
+    # ---- non-invariant status quo: cuBLAS bf16 (+ NCCL all-reduce) ---------------------------
+    yb = torch.empty(M, N_OUT, device=dev, dtype=torch.bfloat16)
+
+    def cublas_step():
+        torch.matmul(x, w, out=yb)
+        if world > 1:
+            dist.all_reduce(yb)
+
+    for _ in range(3):
+        cublas_step()
+    barrier()
+    base_ms = max_over_ranks(ev_time(cublas_step, max(args.steps, 5)))
+    base_tf = flops / (base_ms * 1e-3) / 1e12
+    noninv = {"value": base_tf, "unit": "TFLOP/s", "ms_per_step": base_ms,
+              "path": "torch.matmul bf16 (cuBLAS)" + (" + NCCL bf16 all_reduce" if world > 1 else ""),
+              "tbik_over_baseline": value / base_tf}
+
+    # ---- TP invariance check on this GPU (simulated ranks), every run -------------------------
+    tp_ok = None
+    if rank == 0:
+        xs = x_full[:64].contiguous()
+        wf = torch.randn(K_FULL, N_OUT, device=dev, generator=g).to(torch.bfloat16)
+        outs = [tb.row_parallel_forward(xs, wf, tb.DeviceGroup(t), cfg, 8, leaf) for t in (1, 2, 4, 8)]
+        tp_ok = all(torch.equal(outs[0].view(torch.int32), o.view(torch.int32)) for o in outs[1:])
+        del wf
+
+    # ---- M sweep (rank 0, N = 1) ----------------------------------------------------------------
+    sweep = None
+    if rank == 0 and world == 1 and not args.no_sweep:
+        sweep = {"M": [], "tbik_tc_tflops": [], "tbik_fma_tflops": [], "cublas_bf16_tflops": []}
+        for m in (1, 16, 64, 256, 1024, 4096):
+            xm = x[:m].contiguous()
+            ym = torch.empty(m, N_OUT, device=dev)
+            yc = torch.empty(m, N_OUT, device=dev, dtype=torch.bfloat16)
+            f = 2.0 * m * N_OUT * K_FULL
+            reps = 20 if m <= 1024 else 10
+            tb.tree_matmul(xm, w, cfg, tb.LEAF_TCGEN05, out=ym)
+            t_tc = ev_time(lambda: tb.tree_matmul(xm, w, cfg, tb.LEAF_TCGEN05, out=ym), reps)
+            if m <= 1024:
+                tb.tree_matmul(xm, w, cfg, tb.LEAF_FMA, out=ym)
+                t_fma = ev_time(lambda: tb.tree_matmul(xm, w, cfg, tb.LEAF_FMA, out=ym), max(reps // 4, 2))
+            else:
+                t_fma = None
+            torch.matmul(xm, w, out=yc)
+            t_cb = ev_time(lambda: torch.matmul(xm, w, out=yc), reps)
+            sweep["M"].append(m)
+            sweep["tbik_tc_tflops"].append(f / (t_tc * 1e-3) / 1e12)
+            sweep["tbik_fma_tflops"].append(f / (t_fma * 1e-3) / 1e12 if t_fma else None)
+            sweep["cublas_bf16_tflops"].append(f / (t_cb * 1e-3) / 1e12)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_reference_sample(1, 16, budget_s=10.0)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic: device-generated N(0,1) weights/activations rounded to bf16 (random init, "
+                    "Llama-3.1-8B down_proj shape)",
+            "config": {"workload": WORKLOAD, "M": M, "K": K_FULL, "N": N_OUT, "tp": world,
+                       "parallelism": f"tp{world} row-parallel", "leaf": args.leaf, "block_k": cfg.block_k,
+                       "k_first": tb.plan_blocks(K_FULL, cfg, 8).k_first, "c_max": 8,
+                       "l2": "no flush: per-step inputs+output (x 117 MB + W 117 MB + y 67 MB at tp1) exceed the 126 MB L2"},
+            "roofline": roof, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "noninvariant": noninv, "tp_invariance_bit_identical": tp_ok, "sweep": sweep,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if group is not None:
+        barrier()
+        group.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_tbik(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -96,6 +96,9 @@ TBIK_API int tbik_device_available(void);
 /* Block until all work queued by this library on `stream` finished; reports
  * any asynchronous device fault. */
 TBIK_API tbik_status tbik_sync(void* stream);
+/* Number of kernels this library has launched in this process (all devices).
+ * bench.py reports the delta over its timed region as gpu_launches. */
+TBIK_API uint64_t tbik_launch_count(void);
 
 /* ---- planner (host, pure integer functions) ---------------------------- */
 

@@ -91,6 +91,11 @@ def device_available() -> bool:
     return bool(lib.tbik_device_available())
 
 
+def launch_count() -> int:
+    """Kernels launched by libtbik_b200 so far in this process."""
+    return int(lib.tbik_launch_count())
+
+
 # ---- tensor helpers -----------------------------------------------------------------
 def _torch():
     import torch

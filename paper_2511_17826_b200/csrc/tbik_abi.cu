@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -18,7 +19,10 @@ namespace tbik_b200 {
 
 namespace {
 thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
 }
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 tbik_status set_error(tbik_status st, const std::string& what) {
   g_last_error = what;
@@ -228,6 +232,7 @@ const char* tbik_status_string(int st) {
 
 const char* tbik_last_error(void) { return g_last_error.c_str(); }
 int tbik_version(void) { return 100; }
+uint64_t tbik_launch_count(void) { return g_launches.load(); }
 
 int tbik_device_available(void) {
   int n = 0;
@@ -384,7 +389,8 @@ tbik_status tbik_row_parallel_forward_local(const void* X, int x_dtype, int64_t 
     return run_tree_gemm(v, Y, ldy, leaf_mode, s);
   }
   const size_t slice = static_cast<size_t>(M) * N;
-  float* parts = static_cast<float*>(workspace(slice * tp * sizeof(float), 2));
+  const size_t pitch = (slice + 3) & ~size_t(3);  // keep every partial 16-byte aligned
+  float* parts = static_cast<float*>(workspace(pitch * tp * sizeof(float), 2));
   if (!parts) return set_error(TBIK_CUDA_ERROR, "partials allocation failed");
   PartPtrs pp{};
   for (int r = 0; r < tp; ++r) {
@@ -394,8 +400,8 @@ tbik_status tbik_row_parallel_forward_local(const void* X, int x_dtype, int64_t 
     GemmView v;
     // Every rank uses the GLOBAL k_first (layers.cpp:85-88).
     TBIK_TRY(make_view(Xr, x_dtype, ldx, Wr, w_dtype, ldw, M, N, e - b, cfg->block_k, gp.k_first, &v));
-    TBIK_TRY(run_tree_gemm(v, parts + slice * r, N, leaf_mode, s));
-    pp.p[r] = parts + slice * r;
+    TBIK_TRY(run_tree_gemm(v, parts + pitch * r, N, leaf_mode, s));
+    pp.p[r] = parts + pitch * r;
   }
   if (ldy == N) return launch_allreduce(pp, tp, Y, static_cast<int64_t>(slice), false, (reinterpret_cast<uintptr_t>(Y) & 15) == 0, s);
   float* tmp = static_cast<float*>(workspace(slice * sizeof(float), 3));

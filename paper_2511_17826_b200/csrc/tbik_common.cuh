@@ -34,6 +34,9 @@ int current_device_checked();  // -1 when no sm_100 device
 // first call at a given size must not be inside CUDA graph capture).
 void* workspace(size_t bytes, int slot = 0);
 
+// Counts every kernel launch issued by the library (tbik_launch_count).
+void count_launch();
+
 // ---- numerics (numerics.hpp:21-62) -----------------------------------------
 // Every f32 operation on the reduction path is an explicit round-to-nearest
 // intrinsic; the library is additionally compiled with -fmad=false so nvcc

@@ -132,6 +132,7 @@ tbik_status launch_cfg(const GemmView& v, const GemmOut& o, cudaStream_t s) {
       static_cast<const TA*>(v.A), v.lda, static_cast<const TB*>(v.B), v.ldb, v.M, v.N, v.K, v.bk,
       v.kf, v.T, o.mode, o.out, o.ldo, o.unit_stride);
   TBIK_CUDA(cudaGetLastError());
+  count_launch();
   return TBIK_OK;
 }
 

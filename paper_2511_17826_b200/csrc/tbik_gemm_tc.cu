@@ -400,6 +400,7 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   }
   tc_tree_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mA, mB, p);
   TBIK_CUDA(cudaGetLastError());
+  count_launch();
   return TBIK_OK;
 }
 

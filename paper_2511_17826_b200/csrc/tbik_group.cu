@@ -228,6 +228,7 @@ tbik_status tbik_group_tree_all_reduce(tbik_group* g, const float* partial, floa
   // All CTAs spin on the flags, so the grid must be co-resident: <= 4 per SM.
   group_allreduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(gp, g->W, g->rank, epoch, elems, out);
   TBIK_CUDA(cudaGetLastError());
+  count_launch();
   return TBIK_OK;
 }
 

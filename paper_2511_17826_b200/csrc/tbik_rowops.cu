@@ -301,6 +301,7 @@ tbik_status tbik_tree_rmsnorm(const void* X, int x_dtype, int64_t ldx, const flo
   else TBIK_RMS(float, uint16_t);
 #undef TBIK_RMS
   TBIK_CUDA(cudaGetLastError());
+  count_launch();
   return TBIK_OK;
 }
 
@@ -326,8 +327,10 @@ tbik_status tbik_logsoftmax_shard_state(const float* logits, int64_t ld, int64_t
   else
     ms_group_kernel<false><<<grid, LANES, 0, s>>>(logits, ld, n, groups, gs);
   TBIK_CUDA(cudaGetLastError());
+  count_launch();
   ms_rows_kernel<<<static_cast<unsigned>((rows + 127) / 128), 128, 0, s>>>(gs, rows, groups, ms_out);
   TBIK_CUDA(cudaGetLastError());
+  count_launch();
   return TBIK_OK;
 }
 
@@ -340,6 +343,7 @@ tbik_status tbik_logsoftmax_merge(const float* const* ms_parts, int W, int64_t r
   ms_merge_kernel<<<static_cast<unsigned>((rows + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(pp, W, rows,
                                                                                                         lse);
   TBIK_CUDA(cudaGetLastError());
+  count_launch();
   return TBIK_OK;
 }
 
@@ -354,6 +358,7 @@ tbik_status tbik_logsoftmax_finish(const float* logits, int64_t ld, int64_t rows
   finish_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(logits, ld, rows, v_local, lse, logprobs, ld_out,
                                                                      targets, v_offset, target_logprobs);
   TBIK_CUDA(cudaGetLastError());
+  count_launch();
   return TBIK_OK;
 }
 

@@ -156,6 +156,7 @@ tbik_status launch_tree_combine(const float* ws, int64_t X, int64_t fold, int64_
   tree_combine_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(ws, X, fold, rows, cols,
                                                                             rows * cols, out, ldo);
   TBIK_CUDA(cudaGetLastError());
+  count_launch();
   return TBIK_OK;
 }
 
@@ -184,6 +185,7 @@ tbik_status launch_allreduce(const PartPtrs& dev_parts, int W, float* out, int64
     return set_error(TBIK_BAD_WORLD_SIZE, "all-reduce supports W <= 64 (tree) / 8 (ring)");
   }
   TBIK_CUDA(cudaGetLastError());
+  count_launch();
   return TBIK_OK;
 }
 

@@ -102,8 +102,9 @@ def test_tc_tree_over_gpu_leaves(tb, cuda, orc, M, K, N):
 
 
 def test_tc_leaf_error_bound(tb, cuda, orc):
-    """The tcgen05 leaf vs the exact leaf_dot: |P_tc - P_exact| <= 2^-22 * sum|a_k b_k|
-    (measured bound)."""
+    """The tcgen05 leaf against exact (f64) arithmetic, next to the reference's own
+    fma-chain leaf: both are held to |P - exact| <= 2^-21 * sum_k |a_k b_k|
+    (the measured worst cases are printed and recorded in DESIGN.md section 3)."""
     M, K, N = 64, 4096, 512
     a, b = gen(orc, 5, M, K, N)
     cfg = tb.BlockConfig(64, 256, 128, 0)
@@ -111,12 +112,18 @@ def test_tc_leaf_error_bound(tb, cuda, orc):
     lf = tb.tree_matmul_leaves(to_dev(a), to_dev(b), cfg, tb.LEAF_FMA).cpu().numpy()
     af = (a.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
     bf = (b.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
-    worst = 0.0
+    w_tc = w_fma = w_diff = 0.0
     for t in range(lt.shape[0]):
-        absdot = np.abs(af[:, t * 256:(t + 1) * 256]) @ np.abs(bf[t * 256:(t + 1) * 256])
-        worst = max(worst, float(np.max(np.abs(lt[t].astype(np.float64) - lf[t]) / absdot)))
-    print(f"tc leaf worst |err| / sum|ab| = {worst:.3e} ({worst / 2.0 ** -24:.2f} * 2^-24)")
-    assert worst <= 2.0 ** -22
+        sl = slice(t * 256, (t + 1) * 256)
+        exact = af[:, sl] @ bf[sl]
+        absdot = np.abs(af[:, sl]) @ np.abs(bf[sl])
+        w_tc = max(w_tc, float(np.max(np.abs(lt[t] - exact) / absdot)))
+        w_fma = max(w_fma, float(np.max(np.abs(lf[t] - exact) / absdot)))
+        w_diff = max(w_diff, float(np.max(np.abs(lt[t].astype(np.float64) - lf[t]) / absdot)))
+    u = 2.0 ** -24
+    print(f"leaf error / sum|ab|: tcgen05 {w_tc / u:.2f}u, fma-chain {w_fma / u:.2f}u, "
+          f"|tc - fma| {w_diff / u:.2f}u  (u = 2^-24)")
+    assert w_tc <= 8 * u and w_fma <= 8 * u and w_diff <= 8 * u
 
 
 # ---------------------------------------------------------------------------------
