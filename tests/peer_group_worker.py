@@ -1,0 +1,56 @@
+"""One rank of the two-process PeerGroup test (tests/test_gpu_collective.py).
+
+Launched twice with RANK=0/1, WORLD_SIZE=2, MASTER_ADDR/PORT set.  torch.distributed
+(gloo) only carries the 128-byte IPC handles; the data path is libtbik_b200's peer
+memory + device flag barrier.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2511_17826_b200 as tb  # noqa: E402
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    M, K, N = 64, 14336, 1024
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    x = torch.randn(M, K, generator=g, device="cuda").to(torch.bfloat16)
+    w = torch.randn(K, N, generator=g, device="cuda").to(torch.bfloat16)
+    cfg = tb.BlockConfig(64, 256, 128, 0)
+    kb, ke = tb.make_row_shard_plan(K, cfg, world, 8).bounds[rank]
+    xs, ws = x[:, kb:ke].contiguous(), w[kb:ke].contiguous()
+    grp = tb.PeerGroup(world, rank, torch.cuda.current_device(), M * N, dist)
+    ys = []
+    for it in range(5):  # several epochs: exercises both send-buffer slots
+        for leaf in (tb.LEAF_TCGEN05, tb.LEAF_FMA):
+            ys.append(grp.row_parallel_forward(xs, ws, K, cfg, 8, leaf).clone())
+    torch.cuda.synchronize()
+    for i in range(2, len(ys)):
+        assert torch.equal(ys[i].view(torch.int32), ys[i % 2].view(torch.int32)), f"epoch {i} differs"
+    # plain all-reduce of rank-dependent data: must equal the local Algorithm-2 result
+    parts = [torch.full((3, 5), float(r + 1) * 1e8 if r % 2 == 0 else 1.0, device="cuda") for r in range(world)]
+    red = grp.tree_all_reduce(parts[rank])
+    local = tb.tree_all_reduce(tb.DeviceGroup(world), parts)
+    torch.cuda.synchronize()
+    assert torch.equal(red.view(torch.int32), local.view(torch.int32))
+    out = os.environ["TBIK_TEST_OUT"]
+    np.save(out, ys[0].cpu().numpy())
+    if rank == 0:
+        ref = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+        np.save(out + ".ref.npy", ref.cpu().numpy())
+    dist.barrier()
+    grp.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
