@@ -146,12 +146,12 @@ size_t dsize(int dt) { return dt == TBIK_BF16 ? 2 : 4; }
 tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mode, cudaStream_t s) {
   const size_t slice = static_cast<size_t>(v.M) * v.N;
   if (leaf_mode == TBIK_LEAF_TCGEN05) {
-    const int64_t tiles_mn = ((v.M + 127) / 128) * ((v.N + 127) / 128);
+    const int64_t tiles_mn = tc_pair_tiles(v.M, v.N);
     // Split the K range of each output tile into 2^j aligned subtrees only to
-    // fill the machine; the combine continues the same tree (Theorem 1), so
-    // the split never changes bits.
+    // fill the machine (74 CTA pairs); the combine continues the same tree
+    // (Theorem 1), so the split never changes bits.
     int64_t units = 1;
-    if (tiles_mn < 2 * 148) units = std::min<int64_t>(v.L, next_pow2((2 * 148 + tiles_mn - 1) / tiles_mn));
+    if (tiles_mn < 2 * 74) units = std::min<int64_t>(v.L, next_pow2((2 * 74 + tiles_mn - 1) / tiles_mn));
     if (units <= 1) {
       GemmOut o{OUT_FULL, v.T, C, ldc, 0};
       return launch_tc_gemm(v, o, s);

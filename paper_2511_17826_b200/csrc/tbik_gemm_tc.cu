@@ -1,34 +1,33 @@
-// tbik_gemm_tc.cu -- the TENSOR-CORE-LEAF TBIK GEMM for sm_100a.
+// tbik_gemm_tc.cu -- the TENSOR-CORE-LEAF TBIK GEMM for sm_100a (v2).
 //
-// One CTA owns a 128 x 128 output tile and a K range (a "unit") of whole leaf
-// tiles.  Warp roles (256 threads, one CTA per SM):
-//   warp 0      TMA producer: A tile [128 m x 64 k] (K-major) and B tile
-//               [64 k x 128 n] (the reference's row-major K x N weight, i.e.
-//               MN-major for the MMA -- no pre-transpose) into a 6-stage
-//               128B-swizzled shared-memory ring, completion on mbarriers.
-//   warp 1      MMA issuer: for every leaf tile t, block_k/16 tcgen05.mma
-//               (kind::f16, 128x128x16, bf16 -> f32) into a ZEROED TMEM
-//               accumulator (first MMA with accumulate = 0).  Two accumulator
-//               buffers (TMEM cols [0,128), [128,256)) so leaf t+1 is computed
-//               while leaf t is merged.
-//   warp 2      TMEM allocator (512 columns).
-//   warps 4-7   merge warps: thread (q, lane) owns output row 32q + lane and
-//               all 128 columns.  For every leaf they tcgen05.ld the leaf into
-//               registers and apply the reference's reduction verbatim with
-//               __fadd_rn:
-//                 level 0   g = ((0 + P_0) + P_1) + ... + P_{kf-1}
-//                           (TileReducer level 0, matmul.cpp:100-125)
-//                 levels>=1 binary counter over group values, new + old
-//                           (matmul.cpp:107-123; = T(.) of oracle.cpp:11-20)
-//               g lives in 128 registers; pending tree levels 1 and 2 live in
-//               TMEM (cols [256,384), [384,512)); deeper levels (touched once
-//               per 8+ groups) spill to an L2-resident global scratch.
+// Persistent, 2-CTA (cta_group::2) kernel.  A CTA pair (one cluster) owns a
+// 256 x 128 output tile: CTA rank r holds rows [m0 + 128 r, m0 + 128 r + 128)
+// of A in shared memory and columns [n0 + 64 r, n0 + 64 r + 64) of B; the
+// leader's single MMA thread issues tcgen05.mma.cta_group::2 (M=256, N=128,
+// K=16) that reads both CTAs' operands and writes each CTA's 128 x 128 f32
+// accumulator into that CTA's TMEM.  Per CTA and per K=16 step this moves
+// 6 KB through shared memory (A 4 KB + B 2 KB) instead of 8 KB for a 1-CTA
+// 128 x 128 tile.  Pairs loop over work items (output tile x K unit) with an
+// L2-grouped raster (8 M-blocks share one pass over W).
 //
-// Everything above the leaf is therefore bit-identical to the reference; the
-// leaf P_t itself is the tensor core's block_k-long accumulation (DESIGN.md
-// section 3 gives the measured ulp bound against leaf_dot).  Nothing in the
-// per-element arithmetic depends on M, on the N position, on the unit split or
-// on the TP shard, so the result is batch- and TP-invariant by construction.
+// Warp roles per CTA (256 threads, one CTA per SM):
+//   warp 0      TMA producer: 8-stage ring of {A 128x64, B 64x64} 128B-swizzled
+//               tiles (2SM TMA; completion counted on the leader's barrier)
+//   warp 1      (leader CTA) MMA issuer: for every leaf tile, block_k/16 MMAs into
+//               a ZEROED TMEM accumulator; two accumulators so leaf t+1 is computed
+//               while leaf t is merged
+//   warp 2      TMEM allocator (512 columns, cta_group::2)
+//   warps 4-7   merge warps: thread (q, lane) owns output row 32q + lane, 128
+//               columns.  For every leaf: tcgen05.ld + __fadd_rn, verbatim the
+//               reference's reduction:
+//                 level 0   g = ((0 + P_0) + P_1) + ... + P_{kf-1}   (matmul.cpp:100-125)
+//                 levels>=1 binary counter over group values (matmul.cpp:107-123)
+//               g in 128 registers; tree levels 1-2 in TMEM cols [256,512);
+//               deeper levels (touched once per 8+ groups) in L2-resident scratch.
+// The arithmetic above the leaf is bit-identical to the reference; the leaf is
+// the tensor core's block_k-long accumulation.  Nothing in
+// the per-element arithmetic depends on M, the tile position, the unit split, the
+// raster or the TP shard -> batch- and TP-invariant by construction.
 #include <mutex>
 #include <string>
 
@@ -39,32 +38,116 @@ namespace tbik_b200 {
 
 namespace {
 
-constexpr int BM = 128;
-constexpr int BN = 128;
-constexpr int KSTAGE = 64;  // K elements per pipeline stage (one 128 B swizzle row)
-constexpr int STAGES = 6;
-constexpr int A_STAGE_BYTES = BM * KSTAGE * 2;  // 16 KB
-constexpr int B_STAGE_BYTES = KSTAGE * BN * 2;  // 16 KB (two 64-column boxes)
-constexpr int B_BOX_BYTES = KSTAGE * 64 * 2;    // 8 KB
+constexpr int BM = 128;     // rows per CTA (the pair covers 256)
+constexpr int PAIR_M = 256;
+constexpr int BN = 128;     // columns per pair tile (MMA N); each CTA stages BN/2 of B
+constexpr int KSTAGE = 64;  // K per pipeline stage (one 128 B swizzle row of bf16)
+constexpr int STAGES = 8;
+constexpr int A_STAGE_BYTES = BM * KSTAGE * 2;        // 16 KB
+constexpr int B_STAGE_BYTES = KSTAGE * (BN / 2) * 2;  // 8 KB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int NUM_THREADS = 256;
 constexpr int TMEM_COLS = 512;
 constexpr int SLOT_LVL1 = 256;
 constexpr int SLOT_LVL2 = 384;
-constexpr uint32_t IDESC = umma_idesc_bf16(BM, BN, /*a_mn_major=*/0, /*b_mn_major=*/1);
-constexpr size_t SMEM_BYTES =
-    1024 /*align slack*/ + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 256 /*barriers*/;
+constexpr int GROUP_M = 8;  // raster: M-blocks that share one pass over W
+constexpr uint32_t IDESC = umma_idesc_bf16(PAIR_M, BN, /*a_mn_major=*/0, /*b_mn_major=*/1);
+constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
 
 struct TcParams {
   int M, N, K;
   int bk, kf, T;
   int tiles_per_unit;
+  int units;
   int mode;    // OUT_FULL / OUT_UNITS / OUT_LEAVES
   int levels;  // log2(groups per unit)
+  int mblocks, ntiles;
+  long long items;
   float* out;
   long long ldo;
   long long unit_stride;
-  float* scratch;  // [blocks][levels-2][BN][BM] when levels > 2
+  float* scratch;  // [gridDim.x][levels-2][BN][BM] when levels > 2
 };
+
+// ---- cluster / 2-CTA PTX -----------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Remote arrives use the default (.release, CTA-scope) semantics: the data they
+// guard is either async-proxy (TMA bytes are counted by complete_tx) or TMEM
+// (ordered by tcgen05.fence::before_thread_sync), so no cluster-scope fence is
+// needed -- a .release.cluster arrive costs a MEMBAR + ERRBAR per call.
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr), "r"(bytes)
+               : "memory");
+}
+// 2SM TMA: data lands in this CTA's smem, completion bytes go to the leader's barrier.
+__device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* map, uint32_t leader_bar,
+                                                int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_2cta(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// Arrive on the barrier at the same smem offset in every CTA of `mask`.
+__device__ __forceinline__ void umma_commit_2cta(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_2cta(uint32_t* smem_result, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_result)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc_2cta(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+
+struct Item {
+  int m0, n0, unit, t_begin, t_end;
+};
+
+__device__ __forceinline__ Item decode(const TcParams& p, long long item) {
+  Item it;
+  it.unit = static_cast<int>(item % p.units);
+  const long long rest = item / p.units;
+  const long long group = GROUP_M * static_cast<long long>(p.ntiles);
+  const int g = static_cast<int>(rest / group);
+  const int idx = static_cast<int>(rest % group);
+  const int gm = min(GROUP_M, p.mblocks - g * GROUP_M);
+  const int mb = g * GROUP_M + idx % gm;
+  const int nt = idx / gm;
+  it.m0 = mb * PAIR_M;
+  it.n0 = nt * BN;
+  it.t_begin = it.unit * p.tiles_per_unit;
+  it.t_end = min(p.T, it.t_begin + p.tiles_per_unit);
+  return it;
+}
 
 __device__ __forceinline__ int tile_chunks(const TcParams& p, int t) {
   const int kt0 = t * p.bk;
@@ -72,7 +155,7 @@ __device__ __forceinline__ int tile_chunks(const TcParams& p, int t) {
   return (kh + KSTAGE - 1) / KSTAGE;
 }
 
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     tc_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const TcParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -87,214 +170,230 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN;
-  const int m0 = blockIdx.y * BM;
-  const int unit = blockIdx.z;
-  const int t_begin = unit * p.tiles_per_unit;
-  const int t_end = min(p.T, t_begin + p.tiles_per_unit);
-  const int ntiles = t_end - t_begin;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const long long pair = blockIdx.x >> 1;
+  const long long npairs = gridDim.x >> 1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&full[s], 2);   // one arrive.expect_tx from each CTA of the pair (leader's copy used)
+      mbar_init(&empty[s], 1);  // one multicast commit from the leader's MMA thread
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tfull[b], 1);   // multicast commit
+      mbar_init(&tempty[b], 8);  // 4 merge warps x 2 CTAs (leader's copy used)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 2) tmem_alloc_2cta(tmem_slot, TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
+    // ---------------- TMA producer (both CTAs) ----------------
     if (elect_one()) {
+      const uint32_t full_leader0 = mapa(smem_u32(&full[0]), 0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = t_begin; t < t_end; ++t) {
-        const int nch = tile_chunks(p, t);
-        for (int c = 0; c < nch; ++c) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
-          const int k = t * p.bk + c * KSTAGE;
-          tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, &full[stage], k, m0);
-          tma_load_2d(sB + stage * B_STAGE_BYTES, &tmB, &full[stage], n0, k);
-          tma_load_2d(sB + stage * B_STAGE_BYTES + B_BOX_BYTES, &tmB, &full[stage], n0 + 64, k);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+      for (long long item = pair; item < p.items; item += npairs) {
+        const Item it = decode(p, item);
+        const int am = it.m0 + static_cast<int>(rank) * BM;
+        const int bn = it.n0 + static_cast<int>(rank) * (BN / 2);
+        for (int t = it.t_begin; t < it.t_end; ++t) {
+          const int nch = tile_chunks(p, t);
+          for (int c = 0; c < nch; ++c) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            const uint32_t fb = full_leader0 + stage * 8;
+            if (leader)
+              mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+            else
+              mbar_arrive_expect_tx_cluster(fb, STAGE_BYTES);
+            const int k = t * p.bk + c * KSTAGE;
+            tma_load_2d_2sm(sA + stage * A_STAGE_BYTES, &tmA, fb, k, am);
+            tma_load_2d_2sm(sB + stage * B_STAGE_BYTES, &tmB, fb, bn, k);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (elect_one()) {
+    // ---------------- MMA issuer (leader CTA only) ----------------
+    if (leader && elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int lt = 0; lt < ntiles; ++lt) {
-        const int buf = lt & 1;
-        const uint32_t use = static_cast<uint32_t>(lt >> 1);
-        mbar_wait(&tempty[buf], (use & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem_base + buf * BN;
-        const int nch = tile_chunks(p, t_begin + lt);
-        for (int c = 0; c < nch; ++c) {
-          mbar_wait(&full[stage], phase);
+      uint32_t acc_iter = 0;
+      for (long long item = pair; item < p.items; item += npairs) {
+        const Item it = decode(p, item);
+        for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
+          const int buf = acc_iter & 1;
+          const uint32_t use = acc_iter >> 1;
+          mbar_wait(&tempty[buf], (use & 1) ^ 1);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * A_STAGE_BYTES);
-          const uint32_t b_base = smem_u32(sB + stage * B_STAGE_BYTES);
+          const uint32_t d = tmem_base + buf * BN;
+          const int nch = tile_chunks(p, t);
+          for (int c = 0; c < nch; ++c) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a_base = smem_u32(sA + stage * A_STAGE_BYTES);
+            const uint32_t b_base = smem_u32(sB + stage * B_STAGE_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < KSTAGE / 16; ++kk) {
-            // A: K-major SW128, +32 B per 16-element K step inside the atom.
-            const uint64_t adesc = umma_desc_sw128(a_base + kk * 32, 16, 1024);
-            // B: MN-major SW128, 64-column atoms 8 KB apart (LBO), 8-row K
-            // groups 1 KB apart (SBO); +16 rows (2 KB) per K step.
-            const uint64_t bdesc = umma_desc_sw128(b_base + kk * 2048, B_BOX_BYTES, 1024);
-            umma_bf16(d, adesc, bdesc, IDESC, (c | kk) != 0 ? 1u : 0u);
+            for (int kk = 0; kk < KSTAGE / 16; ++kk) {
+              // A: K-major SW128, +32 B per 16-element K step inside the 128 B atom.
+              const uint64_t adesc = umma_desc_sw128(a_base + kk * 32, 16, 1024);
+              // B: MN-major SW128, one 64-column atom per CTA; 8-row K groups 1 KB
+              // apart (SBO); +16 K rows (2 KB) per step.
+              const uint64_t bdesc = umma_desc_sw128(b_base + kk * 2048, B_STAGE_BYTES, 1024);
+              umma_bf16_2cta(d, adesc, bdesc, IDESC, (c | kk) != 0 ? 1u : 0u);
+            }
+            umma_commit_2cta(&empty[stage], 0x3);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
-          umma_commit(&empty[stage]);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+          umma_commit_2cta(&tfull[buf], 0x3);
         }
-        umma_commit(&tfull[buf]);
       }
     }
     __syncwarp();
   } else if (warp >= 4) {
-    // ---------------- merge warps (the TBIK reduction) ----------------
+    // ---------------- merge warps (the TBIK reduction), both CTAs ----------------
     const int q = warp & 3;
     const int row_in_tile = q * 32 + lane;
-    const int grow = m0 + row_in_tile;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-    const bool row_ok = grow < p.M;
-    const int ncols = min(BN, p.N - n0);
-    float g[BN];
-#pragma unroll
-    for (int i = 0; i < BN; ++i) g[i] = 0.0f;
-    int t_in_group = 0;
-    uint32_t groups_done = 0;
+    const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
     float* scratch_base =
-        p.levels > 2 ? p.scratch + (static_cast<size_t>(blockIdx.z) * gridDim.y * gridDim.x +
-                                    static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) *
-                                       static_cast<size_t>(p.levels - 2) * (BM * BN)
+        p.levels > 2 ? p.scratch + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - 2) * (BM * BN)
                      : nullptr;
-
-    for (int lt = 0; lt < ntiles; ++lt) {
-      const int buf = lt & 1;
-      const uint32_t use = static_cast<uint32_t>(lt >> 1);
-      mbar_wait(&tfull[buf], use & 1);
-      tc_fence_after();
-      const uint32_t acc = lane_base + buf * BN;
-      if (p.mode == OUT_LEAVES) {
-        float* dst = p.out + static_cast<size_t>(t_begin + lt) * p.unit_stride +
-                     static_cast<size_t>(grow) * p.ldo + n0;
+    float g[BN];
+    uint32_t acc_iter = 0;
+    for (long long item = pair; item < p.items; item += npairs) {
+      const Item it = decode(p, item);
+      const int grow = it.m0 + static_cast<int>(rank) * BM + row_in_tile;
+      const bool row_ok = grow < p.M;
+      const int ncols = min(BN, p.N - it.n0);
+      int t_in_group = 0;
+      uint32_t groups_done = 0;
+      for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
+        const int buf = acc_iter & 1;
+        const uint32_t use = acc_iter >> 1;
+        mbar_wait(&tfull[buf], use & 1);
+        tc_fence_after();
+        const uint32_t acc = lane_base + buf * BN;
+        if (p.mode == OUT_LEAVES) {
+          float* dst = p.out + static_cast<size_t>(t) * p.unit_stride + static_cast<size_t>(grow) * p.ldo + it.n0;
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          float v[32];
-          tmem_ld32(acc + c * 32, v);
-          tmem_wait_ld();
-          if (row_ok) {
+          for (int c = 0; c < BN / 32; ++c) {
+            float v[32];
+            tmem_ld32(acc + c * 32, v);
+            tmem_wait_ld();
+            if (row_ok) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (c * 32 + i < ncols) dst[c * 32 + i] = v[i];
+              for (int i = 0; i < 32; ++i)
+                if (c * 32 + i < ncols) dst[c * 32 + i] = v[i];
+            }
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c) {
+            float v[32];
+            tmem_ld32(acc + c * 32, v);
+            tmem_wait_ld();
+            if (t_in_group == 0) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(0.0f, v[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], v[i]);
+            }
           }
         }
-      } else {
+        // Release the accumulator buffer to the leader's MMA thread.
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader)
+            mbar_arrive(&tempty[buf]);
+          else
+            mbar_arrive_cluster(tempty_leader0 + buf * 8);
+        }
+
+        if (p.mode == OUT_LEAVES) continue;
+        if (++t_in_group < p.kf) continue;
+        t_in_group = 0;
+
+        // Binary counter over completed groups (levels 1..p.levels).
+        int level = 1;
+        uint32_t c_bits = groups_done++;
+        while (c_bits & 1u) {
+          if (level <= 2) {
+            const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          float v[32];
-          tmem_ld32(acc + c * 32, v);
-          tmem_wait_ld();
-          if (t_in_group == 0) {
+            for (int c = 0; c < BN / 32; ++c) {
+              float v[32];
+              tmem_ld32(slot + c * 32, v);
+              tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(0.0f, v[i]);
+              for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], v[i]);
+            }
+          } else {
+            const float* s = scratch_base + static_cast<size_t>(level - 3) * (BM * BN) + row_in_tile;
+#pragma unroll
+            for (int i = 0; i < BN; ++i) g[i] = __fadd_rn(g[i], s[i * BM]);
+          }
+          c_bits >>= 1;
+          ++level;
+        }
+        if (level <= p.levels) {
+          if (level <= 2) {
+            const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) {
+              float v[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = g[c * 32 + i];
+              tmem_st32(slot + c * 32, v);
+            }
+            tmem_wait_st();
+          } else {
+            float* s = scratch_base + static_cast<size_t>(level - 3) * (BM * BN) + row_in_tile;
+#pragma unroll
+            for (int i = 0; i < BN; ++i) s[i * BM] = g[i];
+          }
+          continue;
+        }
+        // The carry left the top level: g is this unit's complete (sub)tree.
+        if (row_ok) {
+          float* dst = p.out + static_cast<size_t>(p.mode == OUT_UNITS ? it.unit : 0) * p.unit_stride +
+                       static_cast<size_t>(grow) * p.ldo + it.n0;
+          if (ncols == BN && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+            for (int i = 0; i < BN; i += 4)
+              *reinterpret_cast<float4*>(dst + i) = make_float4(g[i], g[i + 1], g[i + 2], g[i + 3]);
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], v[i]);
+            for (int i = 0; i < BN; ++i)
+              if (i < ncols) dst[i] = g[i];
           }
-        }
-      }
-      // Release the accumulator buffer to the MMA warp.
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
-
-      if (p.mode == OUT_LEAVES) continue;
-      if (++t_in_group < p.kf) continue;
-      t_in_group = 0;
-
-      // Binary counter over completed groups (levels 1..p.levels).
-      int level = 1;
-      uint32_t c_bits = groups_done++;
-      while (c_bits & 1u) {
-        if (level <= 2) {
-          const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
-#pragma unroll
-          for (int c = 0; c < BN / 32; ++c) {
-            float v[32];
-            tmem_ld32(slot + c * 32, v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], v[i]);
-          }
-        } else {
-          const float* s = scratch_base + static_cast<size_t>(level - 3) * (BM * BN) + row_in_tile;
-#pragma unroll
-          for (int i = 0; i < BN; ++i) g[i] = __fadd_rn(g[i], s[i * BM]);
-        }
-        c_bits >>= 1;
-        ++level;
-      }
-      if (level <= p.levels) {
-        if (level <= 2) {
-          const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
-#pragma unroll
-          for (int c = 0; c < BN / 32; ++c) {
-            float v[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = g[c * 32 + i];
-            tmem_st32(slot + c * 32, v);
-          }
-          tmem_wait_st();
-        } else {
-          float* s = scratch_base + static_cast<size_t>(level - 3) * (BM * BN) + row_in_tile;
-#pragma unroll
-          for (int i = 0; i < BN; ++i) s[i * BM] = g[i];
-        }
-        continue;
-      }
-      // The carry left the top level: g is this unit's complete (sub)tree.
-      if (row_ok) {
-        float* dst = p.out + static_cast<size_t>(p.mode == OUT_UNITS ? unit : 0) * p.unit_stride +
-                     static_cast<size_t>(grow) * p.ldo + n0;
-        if (ncols == BN && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-#pragma unroll
-          for (int i = 0; i < BN; i += 4)
-            *reinterpret_cast<float4*>(dst + i) = make_float4(g[i], g[i + 1], g[i + 2], g[i + 3]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < BN; ++i)
-            if (i < ncols) dst[i] = g[i];
         }
       }
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    tmem_dealloc_2cta(tmem_base, TMEM_COLS);
   }
 }
 
@@ -317,19 +416,28 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-tbik_status make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-                        uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+tbik_status make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
+                        uint32_t box_inner, uint32_t box_outer) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return set_error(TBIK_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {row_stride_bytes};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(TBIK_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
   return TBIK_OK;
+}
+
+int sm_count() {
+  static int n[16] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 16) return 148;
+  if (!n[dev]) cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+  return n[dev] ? n[dev] : 148;
 }
 
 }  // namespace
@@ -348,6 +456,8 @@ bool tc_supported(const GemmView& v, std::string* why) {
   return true;
 }
 
+int64_t tc_pair_tiles(int64_t M, int64_t N) { return ((M + PAIR_M - 1) / PAIR_M) * ((N + BN - 1) / BN); }
+
 tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) {
   std::string why;
   if (!tc_supported(v, &why)) return set_error(TBIK_UNSUPPORTED, why);
@@ -356,7 +466,7 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   TBIK_TRY(make_map_2d(&mA, v.A, static_cast<uint64_t>(v.K), static_cast<uint64_t>(v.M),
                        static_cast<uint64_t>(v.lda) * 2, KSTAGE, BM));
   TBIK_TRY(make_map_2d(&mB, v.B, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.K),
-                       static_cast<uint64_t>(v.ldb) * 2, 64, KSTAGE));
+                       static_cast<uint64_t>(v.ldb) * 2, BN / 2, KSTAGE));
   TcParams p{};
   p.M = static_cast<int>(v.M);
   p.N = static_cast<int>(v.N);
@@ -368,11 +478,10 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   p.out = o.out;
   p.ldo = o.ldo;
   p.unit_stride = o.unit_stride;
-  int64_t units;
   if (o.mode == OUT_LEAVES) {
     p.tiles_per_unit = 1;
     p.levels = 0;
-    units = v.T;
+    p.units = p.T;
   } else {
     p.tiles_per_unit = static_cast<int>(o.tiles_per_unit);
     if (p.tiles_per_unit % p.kf) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: unit not whole groups");
@@ -381,22 +490,27 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
     int lv = 0;
     while ((int64_t{1} << lv) < groups) ++lv;
     p.levels = lv;
-    units = (v.T + p.tiles_per_unit - 1) / p.tiles_per_unit;
-    if (o.mode == OUT_FULL && units != 1) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: FULL needs 1 unit");
+    p.units = static_cast<int>((v.T + p.tiles_per_unit - 1) / p.tiles_per_unit);
+    if (o.mode == OUT_FULL && p.units != 1) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: FULL needs 1 unit");
   }
-  dim3 grid(static_cast<unsigned>((v.N + BN - 1) / BN), static_cast<unsigned>((v.M + BM - 1) / BM),
-            static_cast<unsigned>(units));
-  if (grid.y > 65535 || grid.z > 65535) return set_error(TBIK_UNSUPPORTED, "tc gemm: grid too large");
+  p.mblocks = static_cast<int>((v.M + PAIR_M - 1) / PAIR_M);
+  p.ntiles = static_cast<int>((v.N + BN - 1) / BN);
+  p.items = static_cast<long long>(p.mblocks) * p.ntiles * p.units;
+  const long long max_pairs = sm_count() / 2;
+  const long long npairs = p.items < max_pairs ? p.items : max_pairs;
+  dim3 grid(static_cast<unsigned>(2 * npairs));
   if (p.levels > 2) {
-    const size_t n = static_cast<size_t>(grid.x) * grid.y * grid.z * (p.levels - 2) * BM * BN;
+    const size_t n = static_cast<size_t>(grid.x) * (p.levels - 2) * BM * BN;
     p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1));
     if (!p.scratch) return set_error(TBIK_CUDA_ERROR, "tc gemm: scratch allocation failed");
   }
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[16] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 16 && !attr_set[dev]) {
     TBIK_CUDA(cudaFuncSetAttribute(tc_tree_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(SMEM_BYTES)));
-    attr_set = true;
+    attr_set[dev] = true;
   }
   tc_tree_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mA, mB, p);
   TBIK_CUDA(cudaGetLastError());
