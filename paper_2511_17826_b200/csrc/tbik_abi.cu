@@ -146,7 +146,7 @@ size_t dsize(int dt) { return dt == TBIK_BF16 ? 2 : 4; }
 tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mode, cudaStream_t s) {
   const size_t slice = static_cast<size_t>(v.M) * v.N;
   if (leaf_mode == TBIK_LEAF_TCGEN05) {
-    const int64_t tiles_mn = tc_pair_tiles(v.M, v.N);
+    const int64_t tiles_mn = tc_pair_tiles(v);
     // Split the K range of each output tile into 2^j aligned subtrees only to
     // fill the machine (74 CTA pairs); the combine continues the same tree
     // (Theorem 1), so the split never changes bits.

@@ -267,3 +267,27 @@ def test_errors(tb, cuda):
     with pytest.raises(tb.TbikError) as e:
         tb.tree_matmul(x, w, tb.BlockConfig(64, 100, 128, 0), tb.LEAF_TCGEN05)
     assert e.value.code == tb.ErrorCode.Unsupported
+
+
+# ---------------------------------------------------------------------------------
+# the pair-tile width (BN = 128 / 256) and the raster are scheduling choices
+# ---------------------------------------------------------------------------------
+@pytest.mark.parametrize("M,K,N", [(300, 14336, 640), (64, 4096, 512), (513, 6144, 384)])
+def test_tc_tile_width_and_raster_invisible(tb, cuda, orc, M, K, N, monkeypatch):
+    torch.manual_seed(M)
+    x = torch.randn(M, K, device=cuda).to(torch.bfloat16)
+    w = torch.randn(K, N, device=cuda).to(torch.bfloat16)
+    cfg = tb.BlockConfig(64, 256, 128, 0)
+    outs, leaves = [], []
+    for bn, gm in (("128", "8"), ("256", "8"), ("256", "1"), ("128", "3")):
+        monkeypatch.setenv("TBIK_TC_BN", bn)
+        monkeypatch.setenv("TBIK_GROUP_M", gm)
+        outs.append(tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05))
+        leaves.append(tb.tree_matmul_leaves(x, w, cfg, tb.LEAF_TCGEN05))
+    for o in outs[1:]:
+        assert torch.equal(outs[0].view(torch.int32), o.view(torch.int32))
+    for lv in leaves[1:]:
+        assert torch.equal(leaves[0].view(torch.int32), lv.view(torch.int32))
+    plan = tb.plan_blocks(K, cfg, 1)
+    want = orc.tree_over_leaves(leaves[0].cpu().numpy(), plan.k_first)
+    assert np.array_equal(bits(outs[0].cpu().numpy()), bits(want))
