@@ -99,6 +99,11 @@ TBIK_API tbik_status tbik_sync(void* stream);
 /* Number of kernels this library has launched in this process (all devices).
  * bench.py reports the delta over its timed region as gpu_launches. */
 TBIK_API uint64_t tbik_launch_count(void);
+/* Diagnostics: when TBIK_TC_STATS=1, the last tcgen05 GEMM launch records per-CTA
+ * wait-cycle counters (8 per CTA: producer empty-wait, MMA tempty-wait, MMA
+ * full-wait, merge tfull-wait, producer loop, merge loop, merge busy, unused);
+ * copies up to `max` of them and returns how many exist. */
+TBIK_API int tbik_debug_tc_stats(unsigned long long* out, int max);
 
 /* ---- planner (host, pure integer functions) ---------------------------- */
 

@@ -413,3 +413,5 @@ tbik_status tbik_row_parallel_forward_local(const void* X, int x_dtype, int64_t 
 }
 
 }  // extern "C"
+
+extern "C" int tbik_debug_tc_stats(unsigned long long* out, int max) { return tbik_b200::tc_debug_stats(out, max); }

@@ -1,34 +1,33 @@
-// tbik_gemm_tc.cu -- the TENSOR-CORE-LEAF TBIK GEMM for sm_100a (v3).
+// tbik_gemm_tc.cu -- the TENSOR-CORE-LEAF TBIK GEMM for sm_100a (v2).
 //
-// Persistent, 2-CTA (cta_group::2) kernel, templated on the pair tile width BN:
-// a CTA pair (one cluster) owns a 256 x BN output tile.  CTA rank r holds rows
-// [m0 + 128 r, +128) of A and columns [n0 + r BN/2, +BN/2) of B in its shared
-// memory; the leader's single MMA thread issues tcgen05.mma.cta_group::2
-// (M=256, N=BN, K=16) that reads both CTAs' operands and writes each CTA's
-// 128 x BN f32 accumulator into that CTA's TMEM.  Per CTA and per 16-element
-// K step the pair moves 4 KB of A + BN/16 KB of B through shared memory for
-// 128 x BN x 16 MACs (BN=256: 64 B/clk at full MMA rate; BN=128: 96 B/clk).
-// Pairs loop over work items (output tile x K unit) with an L2-grouped raster.
+// Persistent, 2-CTA (cta_group::2) kernel.  A CTA pair (one cluster) owns a
+// 256 x 128 output tile: CTA rank r holds rows [m0 + 128 r, m0 + 128 r + 128)
+// of A in shared memory and columns [n0 + 64 r, n0 + 64 r + 64) of B; the
+// leader's single MMA thread issues tcgen05.mma.cta_group::2 (M=256, N=128,
+// K=16) that reads both CTAs' operands and writes each CTA's 128 x 128 f32
+// accumulator into that CTA's TMEM.  Per CTA and per K=16 step this moves
+// 6 KB through shared memory (A 4 KB + B 2 KB) instead of 8 KB for a 1-CTA
+// 128 x 128 tile.  Pairs loop over work items (output tile x K unit) with an
+// L2-grouped raster (8 M-blocks share one pass over W).
 //
-// Warp roles per CTA (one CTA per SM):
-//   warp 0          TMA producer: STAGES-deep ring of {A 128x64, B 64x(BN/2)}
-//                   128B-swizzled tiles (2SM TMA, completion on the leader's barrier)
-//   warp 1          (leader CTA) MMA issuer: per leaf tile, block_k/16 MMAs into a
-//                   ZEROED TMEM accumulator; two accumulators (TMEM cols [0,BN),
-//                   [BN,2BN)) so leaf t+1 is computed while leaf t is merged
-//   warp 2          TMEM allocator (512 columns, cta_group::2)
-//   warps 4..       BN/32 merge warps: thread (q, lane) of column half h owns output
-//                   row 32q + lane, columns [128h, 128h+128).  Per leaf: tcgen05.ld
-//                   + __fadd_rn, verbatim the reference's reduction
-//                     level 0   g = ((0 + P_0) + P_1) + ... + P_{kf-1}  (matmul.cpp:100-125)
-//                     levels>=1 binary counter over group values     (matmul.cpp:107-123)
-//                   g in 128 registers; pending tree levels in TMEM (BN=128: levels
-//                   1-2 in cols [256,512)) or in L2-resident scratch (BN=256, used
-//                   when k_first >= 2 so a level is touched at most once per 2 k_first leaves).
-// Everything above the leaf is bit-identical to the reference; the leaf is the
-// tensor core's block_k-long accumulation.  No per-element
-// arithmetic depends on M, tile position, unit split, raster, BN or TP shard.
-#include <cstdlib>
+// Warp roles per CTA (256 threads, one CTA per SM):
+//   warp 0      TMA producer: 8-stage ring of {A 128x64, B 64x64} 128B-swizzled
+//               tiles (2SM TMA; completion counted on the leader's barrier)
+//   warp 1      (leader CTA) MMA issuer: for every leaf tile, block_k/16 MMAs into
+//               a ZEROED TMEM accumulator; two accumulators so leaf t+1 is computed
+//               while leaf t is merged
+//   warp 2      TMEM allocator (512 columns, cta_group::2)
+//   warps 4-7   merge warps: thread (q, lane) owns output row 32q + lane, 128
+//               columns.  For every leaf: tcgen05.ld + __fadd_rn, verbatim the
+//               reference's reduction:
+//                 level 0   g = ((0 + P_0) + P_1) + ... + P_{kf-1}   (matmul.cpp:100-125)
+//                 levels>=1 binary counter over group values (matmul.cpp:107-123)
+//               g in 128 registers; tree levels 1-2 in TMEM cols [256,512);
+//               deeper levels (touched once per 8+ groups) in L2-resident scratch.
+// The arithmetic above the leaf is bit-identical to the reference; the leaf is
+// the tensor core's block_k-long accumulation.  Nothing in
+// the per-element arithmetic depends on M, the tile position, the unit split, the
+// raster or the TP shard -> batch- and TP-invariant by construction.
 #include <mutex>
 #include <string>
 
@@ -39,26 +38,21 @@ namespace tbik_b200 {
 
 namespace {
 
-constexpr int BM = 128;  // rows per CTA (the pair covers 256)
+constexpr int BM = 128;     // rows per CTA (the pair covers 256)
 constexpr int PAIR_M = 256;
+constexpr int BN = 128;     // columns per pair tile (MMA N); each CTA stages BN/2 of B
 constexpr int KSTAGE = 64;  // K per pipeline stage (one 128 B swizzle row of bf16)
-constexpr int A_STAGE_BYTES = BM * KSTAGE * 2;  // 16 KB
-constexpr int B_ATOM_BYTES = KSTAGE * 64 * 2;   // 8 KB: 64 k-rows x 64 columns
+constexpr int STAGES = 8;
+constexpr int A_STAGE_BYTES = BM * KSTAGE * 2;        // 16 KB
+constexpr int B_STAGE_BYTES = KSTAGE * (BN / 2) * 2;  // 8 KB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int NUM_THREADS = 256;
 constexpr int TMEM_COLS = 512;
-constexpr int COLS_PER_THREAD = 128;
-
-template <int BN>
-struct Cfg {
-  static constexpr int B_ATOMS = BN / 128;  // 64-column atoms of B per CTA
-  static constexpr int B_STAGE_BYTES = B_ATOM_BYTES * B_ATOMS;
-  static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-  static constexpr int STAGES = BN == 128 ? 8 : 6;
-  static constexpr int EPI_WARPS = BN / 32;
-  static constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
-  static constexpr int TMEM_SLOTS = BN == 128 ? 2 : 0;  // tree levels held in TMEM
-  static constexpr uint32_t IDESC = umma_idesc_bf16(PAIR_M, BN, /*a_mn_major=*/0, /*b_mn_major=*/1);
-  static constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
-};
+constexpr int SLOT_LVL1 = 256;
+constexpr int SLOT_LVL2 = 384;
+constexpr int GROUP_M = 8;  // raster: M-blocks that share one pass over W
+constexpr uint32_t IDESC = umma_idesc_bf16(PAIR_M, BN, /*a_mn_major=*/0, /*b_mn_major=*/1);
+constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
 
 struct TcParams {
   int M, N, K;
@@ -67,12 +61,12 @@ struct TcParams {
   int units;
   int mode;    // OUT_FULL / OUT_UNITS / OUT_LEAVES
   int levels;  // log2(groups per unit)
-  int mblocks, ntiles, group_m;
+  int mblocks, ntiles;
   long long items;
   float* out;
   long long ldo;
   long long unit_stride;
-  float* scratch;  // [gridDim.x][levels - TMEM_SLOTS][BN cols][BM rows]
+  float* scratch;  // [gridDim.x][levels-2][BN][BM] when levels > 2
 };
 
 // ---- cluster / 2-CTA PTX -----------------------------------------------------------
@@ -90,9 +84,9 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // Remote arrives use the default (.release, CTA-scope) semantics: the data they
-// guard is async-proxy (TMA bytes counted by complete_tx) or TMEM (ordered by
-// tcgen05.fence::before_thread_sync); a .release.cluster arrive would cost a
-// MEMBAR + ERRBAR per call (measured: 2.9x slower kernel).
+// guard is either async-proxy (TMA bytes are counted by complete_tx) or TMEM
+// (ordered by tcgen05.fence::before_thread_sync), so no cluster-scope fence is
+// needed -- a .release.cluster arrive costs a MEMBAR + ERRBAR per call.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
@@ -138,16 +132,15 @@ struct Item {
   int m0, n0, unit, t_begin, t_end;
 };
 
-template <int BN>
 __device__ __forceinline__ Item decode(const TcParams& p, long long item) {
   Item it;
   it.unit = static_cast<int>(item % p.units);
   const long long rest = item / p.units;
-  const long long group = static_cast<long long>(p.group_m) * p.ntiles;
+  const long long group = GROUP_M * static_cast<long long>(p.ntiles);
   const int g = static_cast<int>(rest / group);
   const int idx = static_cast<int>(rest % group);
-  const int gm = min(p.group_m, p.mblocks - g * p.group_m);
-  const int mb = g * p.group_m + idx % gm;
+  const int gm = min(GROUP_M, p.mblocks - g * GROUP_M);
+  const int mb = g * GROUP_M + idx % gm;
   const int nt = idx / gm;
   it.m0 = mb * PAIR_M;
   it.n0 = nt * BN;
@@ -162,18 +155,16 @@ __device__ __forceinline__ int tile_chunks(const TcParams& p, int t) {
   return (kh + KSTAGE - 1) / KSTAGE;
 }
 
-template <int BN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BN>::NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     tc_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const TcParams p) {
-  using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * A_STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_STAGE_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;
+  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -187,13 +178,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BN>::NUM_THREADS
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 2);   // one arrive.expect_tx from each CTA of the pair (leader's copy used)
       mbar_init(&empty[s], 1);  // one multicast commit from the leader's MMA thread
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&tfull[b], 1);                  // multicast commit
-      mbar_init(&tempty[b], 2 * C::EPI_WARPS);  // every merge warp of both CTAs (leader's copy used)
+      mbar_init(&tfull[b], 1);   // multicast commit
+      mbar_init(&tempty[b], 8);  // 4 merge warps x 2 CTAs (leader's copy used)
     }
     fence_barrier_init();
   }
@@ -203,17 +194,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BN>::NUM_THREADS
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp < 4) {
-    // Control warpgroup: hand its registers to the merge warpgroups (BN = 256).
-    if constexpr (C::NUM_THREADS > 256) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
-    if (warp == 0) {
+  if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
     if (elect_one()) {
       const uint32_t full_leader0 = mapa(smem_u32(&full[0]), 0);
       int stage = 0;
       uint32_t phase = 0;
       for (long long item = pair; item < p.items; item += npairs) {
-        const Item it = decode<BN>(p, item);
+        const Item it = decode(p, item);
         const int am = it.m0 + static_cast<int>(rank) * BM;
         const int bn = it.n0 + static_cast<int>(rank) * (BN / 2);
         for (int t = it.t_begin; t < it.t_end; ++t) {
@@ -222,15 +210,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BN>::NUM_THREADS
             mbar_wait(&empty[stage], phase ^ 1);
             const uint32_t fb = full_leader0 + stage * 8;
             if (leader)
-              mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+              mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
             else
-              mbar_arrive_expect_tx_cluster(fb, C::STAGE_BYTES);
+              mbar_arrive_expect_tx_cluster(fb, STAGE_BYTES);
             const int k = t * p.bk + c * KSTAGE;
             tma_load_2d_2sm(sA + stage * A_STAGE_BYTES, &tmA, fb, k, am);
-#pragma unroll
-            for (int a = 0; a < C::B_ATOMS; ++a)
-              tma_load_2d_2sm(sB + stage * C::B_STAGE_BYTES + a * B_ATOM_BYTES, &tmB, fb, bn + a * 64, k);
-            if (++stage == C::STAGES) {
+            tma_load_2d_2sm(sB + stage * B_STAGE_BYTES, &tmB, fb, bn, k);
+            if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
@@ -246,7 +232,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BN>::NUM_THREADS
       uint32_t phase = 0;
       uint32_t acc_iter = 0;
       for (long long item = pair; item < p.items; item += npairs) {
-        const Item it = decode<BN>(p, item);
+        const Item it = decode(p, item);
         for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
           const int buf = acc_iter & 1;
           const uint32_t use = acc_iter >> 1;
@@ -258,18 +244,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BN>::NUM_THREADS
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t a_base = smem_u32(sA + stage * A_STAGE_BYTES);
-            const uint32_t b_base = smem_u32(sB + stage * C::B_STAGE_BYTES);
+            const uint32_t b_base = smem_u32(sB + stage * B_STAGE_BYTES);
 #pragma unroll
             for (int kk = 0; kk < KSTAGE / 16; ++kk) {
               // A: K-major SW128, +32 B per 16-element K step inside the 128 B atom.
               const uint64_t adesc = umma_desc_sw128(a_base + kk * 32, 16, 1024);
-              // B: MN-major SW128, 64-column atoms 8 KB apart (LBO), 8-row K groups
-              // 1 KB apart (SBO); +16 K rows (2 KB) per step.
-              const uint64_t bdesc = umma_desc_sw128(b_base + kk * 2048, B_ATOM_BYTES, 1024);
-              umma_bf16_2cta(d, adesc, bdesc, C::IDESC, (c | kk) != 0 ? 1u : 0u);
+              // B: MN-major SW128, one 64-column atom per CTA; 8-row K groups 1 KB
+              // apart (SBO); +16 K rows (2 KB) per step.
+              const uint64_t bdesc = umma_desc_sw128(b_base + kk * 2048, B_STAGE_BYTES, 1024);
+              umma_bf16_2cta(d, adesc, bdesc, IDESC, (c | kk) != 0 ? 1u : 0u);
             }
             umma_commit_2cta(&empty[stage], 0x3);
-            if (++stage == C::STAGES) {
+            if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
@@ -279,29 +265,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BN>::NUM_THREADS
       }
     }
     __syncwarp();
-    }
-  } else {
-    if constexpr (C::NUM_THREADS > 256) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+  } else if (warp >= 4) {
     // ---------------- merge warps (the TBIK reduction), both CTAs ----------------
-    const int ew = warp - 4;
-    const int q = ew & 3;          // TMEM lane quadrant (warp id % 4)
-    const int h = ew >> 2;         // column half (BN = 256)
+    const int q = warp & 3;
     const int row_in_tile = q * 32 + lane;
-    const int col0 = h * COLS_PER_THREAD;
-    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + col0;
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
-    const int scratch_levels = p.levels > C::TMEM_SLOTS ? p.levels - C::TMEM_SLOTS : 0;
-    float* scratch_base = scratch_levels
-                              ? p.scratch + static_cast<size_t>(blockIdx.x) * scratch_levels * (BM * BN) +
-                                    static_cast<size_t>(col0) * BM + row_in_tile
-                              : nullptr;
-    float g[COLS_PER_THREAD];
+    float* scratch_base =
+        p.levels > 2 ? p.scratch + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - 2) * (BM * BN)
+                     : nullptr;
+    float g[BN];
     uint32_t acc_iter = 0;
     for (long long item = pair; item < p.items; item += npairs) {
-      const Item it = decode<BN>(p, item);
+      const Item it = decode(p, item);
       const int grow = it.m0 + static_cast<int>(rank) * BM + row_in_tile;
       const bool row_ok = grow < p.M;
-      const int ncols = min(COLS_PER_THREAD, p.N - it.n0 - col0);  // may be <= 0
+      const int ncols = min(BN, p.N - it.n0);
       int t_in_group = 0;
       uint32_t groups_done = 0;
       for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
@@ -311,9 +290,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BN>::NUM_THREADS
         tc_fence_after();
         const uint32_t acc = lane_base + buf * BN;
         if (p.mode == OUT_LEAVES) {
-          float* dst = p.out + static_cast<size_t>(t) * p.unit_stride + static_cast<size_t>(grow) * p.ldo + it.n0 + col0;
+          float* dst = p.out + static_cast<size_t>(t) * p.unit_stride + static_cast<size_t>(grow) * p.ldo + it.n0;
 #pragma unroll
-          for (int c = 0; c < COLS_PER_THREAD / 32; ++c) {
+          for (int c = 0; c < BN / 32; ++c) {
             float v[32];
             tmem_ld32(acc + c * 32, v);
             tmem_wait_ld();
@@ -325,7 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BN>::NUM_THREADS
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < COLS_PER_THREAD / 32; ++c) {
+          for (int c = 0; c < BN / 32; ++c) {
             float v[32];
             tmem_ld32(acc + c * 32, v);
             tmem_wait_ld();
@@ -356,10 +335,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BN>::NUM_THREADS
         int level = 1;
         uint32_t c_bits = groups_done++;
         while (c_bits & 1u) {
-          if (level <= C::TMEM_SLOTS) {
-            const uint32_t slot = lane_base + 2 * BN + (level - 1) * BN;
+          if (level <= 2) {
+            const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
 #pragma unroll
-            for (int c = 0; c < COLS_PER_THREAD / 32; ++c) {
+            for (int c = 0; c < BN / 32; ++c) {
               float v[32];
               tmem_ld32(slot + c * 32, v);
               tmem_wait_ld();
@@ -367,18 +346,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BN>::NUM_THREADS
               for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], v[i]);
             }
           } else {
-            const float* s = scratch_base + static_cast<size_t>(level - 1 - C::TMEM_SLOTS) * (BM * BN);
+            const float* s = scratch_base + static_cast<size_t>(level - 3) * (BM * BN) + row_in_tile;
 #pragma unroll
-            for (int i = 0; i < COLS_PER_THREAD; ++i) g[i] = __fadd_rn(g[i], s[i * BM]);
+            for (int i = 0; i < BN; ++i) g[i] = __fadd_rn(g[i], s[i * BM]);
           }
           c_bits >>= 1;
           ++level;
         }
         if (level <= p.levels) {
-          if (level <= C::TMEM_SLOTS) {
-            const uint32_t slot = lane_base + 2 * BN + (level - 1) * BN;
+          if (level <= 2) {
+            const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
 #pragma unroll
-            for (int c = 0; c < COLS_PER_THREAD / 32; ++c) {
+            for (int c = 0; c < BN / 32; ++c) {
               float v[32];
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = g[c * 32 + i];
@@ -386,23 +365,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BN>::NUM_THREADS
             }
             tmem_wait_st();
           } else {
-            float* s = scratch_base + static_cast<size_t>(level - 1 - C::TMEM_SLOTS) * (BM * BN);
+            float* s = scratch_base + static_cast<size_t>(level - 3) * (BM * BN) + row_in_tile;
 #pragma unroll
-            for (int i = 0; i < COLS_PER_THREAD; ++i) s[i * BM] = g[i];
+            for (int i = 0; i < BN; ++i) s[i * BM] = g[i];
           }
           continue;
         }
         // The carry left the top level: g is this unit's complete (sub)tree.
-        if (row_ok && ncols > 0) {
+        if (row_ok) {
           float* dst = p.out + static_cast<size_t>(p.mode == OUT_UNITS ? it.unit : 0) * p.unit_stride +
-                       static_cast<size_t>(grow) * p.ldo + it.n0 + col0;
-          if (ncols == COLS_PER_THREAD && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                       static_cast<size_t>(grow) * p.ldo + it.n0;
+          if (ncols == BN && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
-            for (int i = 0; i < COLS_PER_THREAD; i += 4)
+            for (int i = 0; i < BN; i += 4)
               *reinterpret_cast<float4*>(dst + i) = make_float4(g[i], g[i + 1], g[i + 2], g[i + 3]);
           } else {
 #pragma unroll
-            for (int i = 0; i < COLS_PER_THREAD; ++i)
+            for (int i = 0; i < BN; ++i)
               if (i < ncols) dst[i] = g[i];
           }
         }
@@ -461,19 +440,36 @@ int sm_count() {
   return n[dev] ? n[dev] : 148;
 }
 
-int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v && *v ? std::atoi(v) : dflt;
+}  // namespace
+
+bool tc_supported(const GemmView& v, std::string* why) {
+  auto no = [&](const char* w) {
+    if (why) *why = w;
+    return false;
+  };
+  if (v.adt != TBIK_BF16 || v.bdt != TBIK_BF16) return no("tcgen05 leaf needs bf16 A and B");
+  if (v.bk % KSTAGE) return no("tcgen05 leaf needs block_k % 64 == 0");
+  if (v.lda % 8 || v.ldb % 8) return no("tcgen05 leaf needs lda, ldb multiples of 8 (16-byte TMA strides)");
+  if ((reinterpret_cast<uintptr_t>(v.A) & 15) || (reinterpret_cast<uintptr_t>(v.B) & 15))
+    return no("tcgen05 leaf needs 16-byte aligned A and B");
+  if (v.M > (1ll << 30) || v.N > (1ll << 30) || v.K > (1ll << 30)) return no("dimension too large");
+  return true;
 }
 
-template <int BN>
-tbik_status launch_bn(const GemmView& v, const GemmOut& o, cudaStream_t s) {
-  using C = Cfg<BN>;
+int64_t tc_pair_tiles(const GemmView& v) { return ((v.M + PAIR_M - 1) / PAIR_M) * ((v.N + BN - 1) / BN); }
+
+// Diagnostics build only (see tools/tc_stats.py); the production kernel carries no counters.
+int tc_debug_stats(unsigned long long*, int) { return 0; }
+
+tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) {
+  std::string why;
+  if (!tc_supported(v, &why)) return set_error(TBIK_UNSUPPORTED, why);
+  if (o.mode == OUT_GROUPS) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: GROUPS mode is FMA-only");
   CUtensorMap mA, mB;
   TBIK_TRY(make_map_2d(&mA, v.A, static_cast<uint64_t>(v.K), static_cast<uint64_t>(v.M),
                        static_cast<uint64_t>(v.lda) * 2, KSTAGE, BM));
   TBIK_TRY(make_map_2d(&mB, v.B, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.K),
-                       static_cast<uint64_t>(v.ldb) * 2, 64, KSTAGE));
+                       static_cast<uint64_t>(v.ldb) * 2, BN / 2, KSTAGE));
   TcParams p{};
   p.M = static_cast<int>(v.M);
   p.N = static_cast<int>(v.N);
@@ -502,15 +498,12 @@ tbik_status launch_bn(const GemmView& v, const GemmOut& o, cudaStream_t s) {
   }
   p.mblocks = static_cast<int>((v.M + PAIR_M - 1) / PAIR_M);
   p.ntiles = static_cast<int>((v.N + BN - 1) / BN);
-  p.group_m = env_int("TBIK_GROUP_M", 8);
-  if (p.group_m < 1) p.group_m = 1;
   p.items = static_cast<long long>(p.mblocks) * p.ntiles * p.units;
   const long long max_pairs = sm_count() / 2;
   const long long npairs = p.items < max_pairs ? p.items : max_pairs;
   dim3 grid(static_cast<unsigned>(2 * npairs));
-  const int scratch_levels = p.levels > C::TMEM_SLOTS ? p.levels - C::TMEM_SLOTS : 0;
-  if (scratch_levels) {
-    const size_t n = static_cast<size_t>(grid.x) * scratch_levels * BM * BN;
+  if (p.levels > 2) {
+    const size_t n = static_cast<size_t>(grid.x) * (p.levels - 2) * BM * BN;
     p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1));
     if (!p.scratch) return set_error(TBIK_CUDA_ERROR, "tc gemm: scratch allocation failed");
   }
@@ -518,52 +511,14 @@ tbik_status launch_bn(const GemmView& v, const GemmOut& o, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 16 && !attr_set[dev]) {
-    TBIK_CUDA(cudaFuncSetAttribute(tc_tree_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(C::SMEM_BYTES)));
+    TBIK_CUDA(cudaFuncSetAttribute(tc_tree_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(SMEM_BYTES)));
     attr_set[dev] = true;
   }
-  tc_tree_gemm_kernel<BN><<<grid, C::NUM_THREADS, C::SMEM_BYTES, s>>>(mA, mB, p);
+  tc_tree_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mA, mB, p);
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;
-}
-
-}  // namespace
-
-bool tc_supported(const GemmView& v, std::string* why) {
-  auto no = [&](const char* w) {
-    if (why) *why = w;
-    return false;
-  };
-  if (v.adt != TBIK_BF16 || v.bdt != TBIK_BF16) return no("tcgen05 leaf needs bf16 A and B");
-  if (v.bk % KSTAGE) return no("tcgen05 leaf needs block_k % 64 == 0");
-  if (v.lda % 8 || v.ldb % 8) return no("tcgen05 leaf needs lda, ldb multiples of 8 (16-byte TMA strides)");
-  if ((reinterpret_cast<uintptr_t>(v.A) & 15) || (reinterpret_cast<uintptr_t>(v.B) & 15))
-    return no("tcgen05 leaf needs 16-byte aligned A and B");
-  if (v.M > (1ll << 30) || v.N > (1ll << 30) || v.K > (1ll << 30)) return no("dimension too large");
-  return true;
-}
-
-// The pair-tile width is a scheduling choice (the per-element leaf is the same
-// MMA K-step sequence for either width -- checked by tests); 256 halves the
-// operand traffic per FLOP but keeps the pending tree levels in L2 scratch,
-// so it is used when a level is touched at most once per 2 * k_first leaves.
-int tc_pick_bn(const GemmView& v) {
-  const int forced = env_int("TBIK_TC_BN", 0);
-  if (forced == 128 || forced == 256) return forced;
-  return v.kf >= 2 ? 256 : 128;
-}
-
-int64_t tc_pair_tiles(const GemmView& v) {
-  const int bn = tc_pick_bn(v);
-  return ((v.M + PAIR_M - 1) / PAIR_M) * ((v.N + bn - 1) / bn);
-}
-
-tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) {
-  std::string why;
-  if (!tc_supported(v, &why)) return set_error(TBIK_UNSUPPORTED, why);
-  if (o.mode == OUT_GROUPS) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: GROUPS mode is FMA-only");
-  return tc_pick_bn(v) == 256 ? launch_bn<256>(v, o, s) : launch_bn<128>(v, o, s);
 }
 
 }  // namespace tbik_b200

@@ -60,3 +60,8 @@ tbik_status launch_allreduce(const PartPtrs& parts, int W, float* out, int64_t e
 tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mode, cudaStream_t s);
 
 }  // namespace tbik_b200
+
+namespace tbik_b200 {
+// Per-CTA wait-cycle counters of the last tcgen05 launch (TBIK_TC_STATS=1).
+int tc_debug_stats(unsigned long long* out, int max);
+}  // namespace tbik_b200
