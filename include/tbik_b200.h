@@ -240,6 +240,37 @@ TBIK_API tbik_status tbik_tree_logsoftmax_local(const float* logits, int64_t ld,
                                        int64_t ld_out, const int64_t* targets,
                                        float* target_logprobs, void* stream);
 
+/* ---- per-token kernels of a TBIK decoder forward ----------
+ * The reference's toy model (demo.cpp:164-241) has no attention / RoPE; these
+ * complete a Llama / Qwen-shaped forward whose every element is a fixed,
+ * shard-independent sequence of RN f32 ops (restated in oracle/tbik_oracle.c). */
+
+/* out[i] = table[ids[i]] (bf16 rows of width H); BadArgument on an id >= V. */
+TBIK_API tbik_status tbik_embedding(const void* table, int64_t V, int64_t H, const int64_t* ids, int64_t rows,
+                                    void* out, void* stream);
+/* Rotate-half RoPE on f32 columns [col0, col0 + heads*head_dim) of x, bf16 out;
+ * cos/sin tables are f32 [max_pos][head_dim/2], positions int32 [rows]. */
+TBIK_API tbik_status tbik_rope(const float* x, int64_t ldx, int64_t col0, int heads, int head_dim,
+                               const int* positions, const float* cos_table, const float* sin_table,
+                               void* out, int64_t ldo, int64_t rows, void* stream);
+/* storage_cast (demo.cpp:50-52): bf16_round of an f32 block. */
+TBIK_API tbik_status tbik_cast_bf16(const float* x, int64_t ldx, int64_t rows, int64_t cols, void* out,
+                                    int64_t ldo, void* stream);
+/* Causal GQA prefill attention over `batch` sequences of seq_len tokens (rows are
+ * sequence-major), head_dim 128, bf16 in / bf16 out, fixed key order + online
+ * softmax with the shared exp. */
+TBIK_API tbik_status tbik_attention_prefill(const void* q, int64_t ldq, const void* k, int64_t ldk,
+                                            const void* v, int64_t ldv, int64_t batch, int seq_len,
+                                            int n_q_heads, int n_kv_heads, int head_dim, float scale,
+                                            void* out, int64_t ldo, void* stream);
+/* act = bf16(silu(gate) * up), gate = columns [0, inter), up = [inter, 2 inter)
+ * of gate_up (f32) -- silu (demo.cpp:36-45) with the shared exp. */
+TBIK_API tbik_status tbik_silu_mul(const float* gate_up, int64_t ld, int64_t rows, int64_t inter, void* out,
+                                   int64_t ldo, void* stream);
+/* h = bf16(h + f) in place (demo.cpp:216). */
+TBIK_API tbik_status tbik_residual_add(void* h, int64_t ldh, const float* f, int64_t ldf, int64_t rows,
+                                       int64_t cols, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

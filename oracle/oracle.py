@@ -105,6 +105,44 @@ class Oracle(_Lib):
         L.tbo_log.argtypes = [f32]
         L.tbo_tree_logsoftmax.argtypes = [PF, i64, i64, i64, PF, PF, PI64, PF]
         L.tbo_logsoftmax_group_states.argtypes = [PF, i64, i64, i64, PF, PF]
+        L.tbo_silu_mul.argtypes = [PF, i64, i64, i64, vp, i64]
+        L.tbo_residual_add.argtypes = [vp, i64, PF, i64, i64, i64]
+        L.tbo_rope.argtypes = [PF, i64, i64, C.c_int, C.c_int, vp, PF, PF, vp, i64, i64]
+        L.tbo_attention_prefill.argtypes = [vp, i64, vp, i64, vp, i64, i64, C.c_int, C.c_int, C.c_int,
+                                            C.c_float, vp, i64]
+
+    # -- decoder per-token kernels (numpy in/out; bf16 as uint16 bits) ---------
+    def silu_mul(self, gu: np.ndarray, inter: int):
+        gu = np.ascontiguousarray(gu, np.float32)
+        out = np.empty((gu.shape[0], inter), np.uint16)
+        _check(self.lib.tbo_silu_mul(gu.ctypes.data_as(PF), gu.shape[1], gu.shape[0], inter, _p(out), inter),
+               "silu_mul")
+        return out
+
+    def residual_add(self, h: np.ndarray, f: np.ndarray):
+        h = np.ascontiguousarray(h, np.uint16).copy()
+        f = np.ascontiguousarray(f, np.float32)
+        _check(self.lib.tbo_residual_add(_p(h), h.shape[1], f.ctypes.data_as(PF), f.shape[1], h.shape[0],
+                                         h.shape[1]), "residual_add")
+        return h
+
+    def rope(self, x, col0, heads, head_dim, positions, cos_t, sin_t):
+        x = np.ascontiguousarray(x, np.float32)
+        pos = np.ascontiguousarray(positions, np.int32)
+        c = np.ascontiguousarray(cos_t, np.float32)
+        s = np.ascontiguousarray(sin_t, np.float32)
+        out = np.empty((x.shape[0], heads * head_dim), np.uint16)
+        _check(self.lib.tbo_rope(x.ctypes.data_as(PF), x.shape[1], col0, heads, head_dim, _p(pos),
+                                 c.ctypes.data_as(PF), s.ctypes.data_as(PF), _p(out), heads * head_dim,
+                                 x.shape[0]), "rope")
+        return out
+
+    def attention_prefill(self, q, k, v, batch, seq_len, nq, nkv, scale):
+        q, k, v = (np.ascontiguousarray(t, np.uint16) for t in (q, k, v))
+        out = np.empty((batch * seq_len, nq * 128), np.uint16)
+        _check(self.lib.tbo_attention_prefill(_p(q), q.shape[1], _p(k), k.shape[1], _p(v), v.shape[1], batch,
+                                              seq_len, nq, nkv, scale, _p(out), nq * 128), "attention")
+        return out
 
     # -- inputs -------------------------------------------------------------
     def random_normal(self, seed, stream, rows, cols, dtype="bf16", mean=0.0, std=1.0):

@@ -755,3 +755,92 @@ int tbo_softmax_row_seq(const float* logits, int64_t n, float* probs) {
   for (int64_t j = 0; j < n; ++j) probs[j] = probs[j] / sum;
   return TBO_OK;
 }
+
+/* ---------------------------------------------------------------------------
+ * Per-token kernels of the decoder forward (NEW; the reference demo has no
+ * attention or RoPE).  Same op sequences as csrc/tbik_model.cu.
+ * ------------------------------------------------------------------------- */
+
+/* act = bf16(silu(gate) * up) with silu(z) = z / (1 + exp(-z))  (demo.cpp:36-45) */
+int tbo_silu_mul(const float* gu, int64_t ld, int64_t rows, int64_t inter, uint16_t* out, int64_t ldo) {
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t j = 0; j < inter; ++j) {
+      float z = gu[r * ld + j];
+      float s = z / (1.0f + tbo_exp(-z));
+      out[r * ldo + j] = tbo_bf16_round(s * gu[r * ld + inter + j]);
+    }
+  return TBO_OK;
+}
+
+/* h = bf16(h + f)  (demo.cpp:216) */
+int tbo_residual_add(uint16_t* h, int64_t ldh, const float* f, int64_t ldf, int64_t rows, int64_t cols) {
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t j = 0; j < cols; ++j)
+      h[r * ldh + j] = tbo_bf16_round(tbo_bf16_to_f32(h[r * ldh + j]) + f[r * ldf + j]);
+  return TBO_OK;
+}
+
+/* rotate-half RoPE, bf16 out */
+int tbo_rope(const float* x, int64_t ldx, int64_t col0, int heads, int D, const int* pos, const float* cos_t,
+             const float* sin_t, uint16_t* out, int64_t ldo, int64_t rows) {
+  const int half = D / 2;
+  for (int64_t r = 0; r < rows; ++r) {
+    const float* xr = x + r * ldx + col0;
+    const int p = pos[r];
+    for (int e = 0; e < heads * D; ++e) {
+      const int h = e / D, d = e % D;
+      const float* xh = xr + h * D;
+      float v;
+      if (d < half)
+        v = xh[d] * cos_t[p * half + d] - xh[d + half] * sin_t[p * half + d];
+      else
+        v = xh[d] * cos_t[p * half + d - half] + xh[d - half] * sin_t[p * half + d - half];
+      out[r * ldo + e] = tbo_bf16_round(v);
+    }
+  }
+  return TBO_OK;
+}
+
+/* Causal GQA prefill attention, head_dim 128: per (row, head) the score of key
+ * j is the contiguous-halves tree over 32 lane partials (lane l: fma chain over
+ * dims 4l..4l+3), times scale; online softmax over j = 0..i ascending. */
+int tbo_attention_prefill(const uint16_t* q, int64_t ldq, const uint16_t* k, int64_t ldk, const uint16_t* v,
+                          int64_t ldv, int64_t batch, int S, int nq, int nkv, float scale, uint16_t* out,
+                          int64_t ldo) {
+  if (nkv < 1 || nq % nkv) return TBO_BAD_DIMENSION;
+  for (int64_t row = 0; row < batch * S; ++row) {
+    const int64_t seq0 = (row / S) * S;
+    const int i = (int)(row - seq0);
+    for (int h = 0; h < nq; ++h) {
+      const int kh = h / (nq / nkv);
+      float m = -INFINITY, l = 0.0f, o[128];
+      for (int d = 0; d < 128; ++d) o[d] = 0.0f;
+      for (int j = 0; j <= i; ++j) {
+        const int64_t kr = seq0 + j;
+        float part[32];
+        for (int ln = 0; ln < 32; ++ln) {
+          float a = 0.0f;
+          for (int t = 0; t < 4; ++t)
+            a = fmaf(tbo_bf16_to_f32(q[row * ldq + h * 128 + ln * 4 + t]),
+                     tbo_bf16_to_f32(k[kr * ldk + kh * 128 + ln * 4 + t]), a);
+          part[ln] = a;
+        }
+        /* xor butterfly 1,2,4,8,16 == contiguous-halves tree over the 32 lanes */
+        const float s = tree_reduce_rec(part, 32) * scale;
+        const uint16_t* vr = v + kr * ldv + kh * 128;
+        if (s > m) {
+          const float a = tbo_exp(m - s);
+          l = l * a + 1.0f;
+          for (int d = 0; d < 128; ++d) o[d] = o[d] * a + tbo_bf16_to_f32(vr[d]);
+          m = s;
+        } else {
+          const float pj = tbo_exp(s - m);
+          l = l + pj;
+          for (int d = 0; d < 128; ++d) o[d] = fmaf(pj, tbo_bf16_to_f32(vr[d]), o[d]);
+        }
+      }
+      for (int d = 0; d < 128; ++d) out[row * ldo + h * 128 + d] = tbo_bf16_round(o[d] / l);
+    }
+  }
+  return TBO_OK;
+}

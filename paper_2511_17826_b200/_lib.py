@@ -105,6 +105,13 @@ _SIGS = {
     "tbik_logsoftmax_merge": (ci, [C.POINTER(vp), ci, i64, PF, vp]),
     "tbik_logsoftmax_finish": (ci, [PF, i64, i64, i64, PF, PF, i64, vp, i64, PF, vp]),
     "tbik_tree_logsoftmax_local": (ci, [PF, i64, i64, i64, i64, ci, PF, PF, i64, vp, PF, vp]),
+    "tbik_embedding": (ci, [vp, i64, i64, vp, i64, vp, vp]),
+    "tbik_rope": (ci, [PF, i64, i64, ci, ci, vp, PF, PF, vp, i64, i64, vp]),
+    "tbik_cast_bf16": (ci, [PF, i64, i64, i64, vp, i64, vp]),
+    "tbik_attention_prefill": (ci, [vp, i64, vp, i64, vp, i64, i64, ci, ci, ci, ci, C.c_float, vp, i64, vp]),
+    "tbik_silu_mul": (ci, [PF, i64, i64, i64, vp, i64, vp]),
+    "tbik_residual_add": (ci, [vp, i64, PF, i64, i64, i64, vp]),
+    "tbik_debug_tc_stats": (ci, [C.POINTER(C.c_ulonglong), ci]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -1,0 +1,75 @@
+// tbik_mathfn.cuh -- the shared, explicitly-rounded exp / log used by every
+// kernel that needs a transcendental (log-softmax, SiLU, attention).  The exact
+// same operation sequence is restated on the CPU in oracle/tbik_oracle.c
+// (tbo_exp / tbo_log), so GPU and oracle agree bit for bit; glibc and CUDA expf /
+// logf do not.
+#pragma once
+
+#include "tbik_common.cuh"
+
+namespace tbik_b200 {
+
+__device__ __forceinline__ float tb_exp(float x) {
+  if (x != x) return x;
+  if (x < -103.0f) return 0.0f;
+  if (x > 88.5f) return __int_as_float(0x7F800000);
+  const float magic = 12582912.0f;
+  const float t = __fmaf_rn(x, 1.44269502162933349609f, magic);
+  const float kf = __fsub_rn(t, magic);
+  float r = __fmaf_rn(kf, -0.693359375f, x);
+  r = __fmaf_rn(kf, 2.12194440e-4f, r);
+  float p = 1.9875691500e-4f;
+  p = __fmaf_rn(p, r, 1.3981999507e-3f);
+  p = __fmaf_rn(p, r, 8.3334519073e-3f);
+  p = __fmaf_rn(p, r, 4.1665795894e-2f);
+  p = __fmaf_rn(p, r, 1.6666665459e-1f);
+  p = __fmaf_rn(p, r, 5.0000001201e-1f);
+  const float r2 = __fmul_rn(r, r);
+  float y = __fmaf_rn(p, r2, r);
+  y = __fadd_rn(y, 1.0f);
+  int k = static_cast<int>(kf);
+  if (k < -125) {
+    y = __fmul_rn(y, __uint_as_float(static_cast<uint32_t>(127 - 64) << 23));
+    k += 64;
+  }
+  return __fmul_rn(y, __uint_as_float(static_cast<uint32_t>(k + 127) << 23));
+}
+
+__device__ __forceinline__ float tb_log(float x) {
+  if (!(x > 0.0f)) return x == 0.0f ? __int_as_float(0xFF800000) : __int_as_float(0x7FC00000);
+  if (x == __int_as_float(0x7F800000)) return x;
+  uint32_t u = __float_as_uint(x);
+  int e = 0;
+  if ((u & 0x7F800000u) == 0) {
+    x = __fmul_rn(x, 4294967296.0f);
+    u = __float_as_uint(x);
+    e = -32;
+  }
+  e += static_cast<int>((u >> 23) & 0xFF) - 127;
+  float m = __uint_as_float((u & 0x007FFFFFu) | 0x3F800000u);
+  if (m > 1.41421356237309504880f) {
+    m = __fmul_rn(m, 0.5f);
+    e += 1;
+  }
+  const float xm = __fsub_rn(m, 1.0f);
+  const float z = __fmul_rn(xm, xm);
+  float p = 7.0376836292e-2f;
+  p = __fmaf_rn(p, xm, -1.1514610310e-1f);
+  p = __fmaf_rn(p, xm, 1.1676998740e-1f);
+  p = __fmaf_rn(p, xm, -1.2420140846e-1f);
+  p = __fmaf_rn(p, xm, 1.4249322787e-1f);
+  p = __fmaf_rn(p, xm, -1.6668057665e-1f);
+  p = __fmaf_rn(p, xm, 2.0000714765e-1f);
+  p = __fmaf_rn(p, xm, -2.4999993993e-1f);
+  p = __fmaf_rn(p, xm, 3.3333331174e-1f);
+  float y = __fmul_rn(p, xm);
+  y = __fmul_rn(y, z);
+  const float fe = static_cast<float>(e);
+  y = __fmaf_rn(fe, -2.12194440e-4f, y);
+  y = __fmaf_rn(z, -0.5f, y);
+  float r = __fadd_rn(xm, y);
+  r = __fmaf_rn(fe, 0.693359375f, r);
+  return r;
+}
+
+}  // namespace tbik_b200

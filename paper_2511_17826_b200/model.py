@@ -1,0 +1,239 @@
+"""TBIK decoder forward: Llama-3.1-8B / Qwen3-32B-shaped prefill (SURVEY §8 F3,
+BASELINE configs[2] and configs[3]).
+
+The reference's toy model (demo.cpp:164-241: rmsnorm -> column-parallel gate/up
+-> silu * up -> row-parallel down -> residual rounded through bf16 -> column-
+parallel lm head -> softmax) is the structural template; this adds what a real
+decoder needs -- GQA attention with RoPE (and Qwen3's per-head q/k RMSNorm) --
+with every reduction in a fixed, shard-independent order:
+
+  rmsnorm            tbik_tree_rmsnorm            replicated, per token
+  qkv / gate_up / lm column_parallel_forward      per column: identical at any TP
+  RoPE, attention    tbik_rope, tbik_attention_prefill   per token / (seq, head)
+  o_proj, down_proj  row_parallel_forward         TBIK tree GEMM + tree all-reduce
+  residual           tbik_residual_add            h = bf16(h + f)  (demo.cpp:216)
+  log-probs          tbik_tree_logsoftmax_local   vocab-sharded (m, s) tree
+
+so logits and log-probs are bit-identical for TP = 1/2/4/8 and for any batch
+composition.  TP ranks are simulated on one GPU (the reference's in-process
+DeviceGroup); one process per GPU uses the same kernels through PeerGroup.
+Weights are random-init (there is no checkpoint access); the shapes are the
+public HF configs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import api
+from ._lib import check, lib
+
+
+@dataclass
+class DecoderConfig:
+    name: str
+    hidden: int
+    intermediate: int
+    n_heads: int
+    n_kv_heads: int
+    vocab: int
+    n_layers: int
+    head_dim: int = 128
+    rms_eps: float = 1e-5
+    rope_theta: float = 500000.0
+    rope_llama3: Optional[dict] = None
+    qk_norm: bool = False
+    block_k: int = 256        # numerics-defining leaf width for every GEMM
+    block_k_down: int = 256   # down_proj (Qwen3-32B needs 128: K=25600)
+    c_max: int = 8
+    vocab_groups: int = 8
+    max_pos: int = 4096
+    weight_std: float = 0.02
+
+
+def llama31_8b(n_layers: int = 32) -> DecoderConfig:
+    return DecoderConfig("llama3.1-8b", 4096, 14336, 32, 8, 128256, n_layers, rope_theta=500000.0,
+                         rope_llama3=dict(factor=8.0, low_freq_factor=1.0, high_freq_factor=4.0,
+                                          original_max_position_embeddings=8192))
+
+
+def qwen3_32b(n_layers: int = 64) -> DecoderConfig:
+    return DecoderConfig("qwen3-32b", 5120, 25600, 64, 8, 151936, n_layers, rms_eps=1e-6, rope_theta=1000000.0,
+                         qk_norm=True, block_k_down=128)
+
+
+def rope_tables(cfg: DecoderConfig):
+    """cos/sin [max_pos, head_dim/2] f32, computed in float64 on the host (HF
+    rotary embedding, with Llama-3 frequency scaling when configured)."""
+    d = cfg.head_dim
+    inv = 1.0 / (cfg.rope_theta ** (np.arange(0, d, 2, dtype=np.float64) / d))
+    if cfg.rope_llama3:
+        s = cfg.rope_llama3
+        factor, lo, hi = s["factor"], s["low_freq_factor"], s["high_freq_factor"]
+        orig = s["original_max_position_embeddings"]
+        lo_wl, hi_wl = orig / lo, orig / hi
+        wl = 2 * math.pi / inv
+        scaled = np.where(wl > lo_wl, inv / factor, inv)
+        smooth = (orig / wl - lo) / (hi - lo)
+        smoothed = (1 - smooth) * scaled / factor + smooth * scaled
+        medium = ~(wl < hi_wl) & ~(wl > lo_wl)
+        inv = np.where(medium, smoothed, scaled)
+    ang = np.arange(cfg.max_pos, dtype=np.float64)[:, None] * inv[None, :]
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+
+
+@dataclass
+class LayerWeights:
+    ln1: object
+    wqkv: object
+    wo: object
+    ln2: object
+    wgu: object
+    wd: object
+    q_norm: object = None
+    k_norm: object = None
+
+
+@dataclass
+class DecoderWeights:
+    embed: object
+    layers: List[LayerWeights] = field(default_factory=list)
+    ln_f: object = None
+    lm_head: object = None
+
+
+def random_weights(cfg: DecoderConfig, seed: int = 0, device="cuda") -> DecoderWeights:
+    """Random-init weights of the named architecture, generated on the device
+    from fixed per-tensor seeds (independent of TP and batch, like
+    make_demo_weights, demo.cpp:123-162)."""
+    import torch
+    g = torch.Generator(device=device)
+    counter = [seed * 1000003]
+
+    def normal(shape, std, mean=0.0, dtype=torch.bfloat16):
+        counter[0] += 1
+        g.manual_seed(counter[0])
+        t = torch.empty(shape, device=device, dtype=torch.float32)
+        t.normal_(mean, std, generator=g)
+        return t.to(dtype)
+
+    H, I, D = cfg.hidden, cfg.intermediate, cfg.head_dim
+    nq, nkv = cfg.n_heads, cfg.n_kv_heads
+    w = DecoderWeights(embed=normal((cfg.vocab, H), 1.0))
+    for _ in range(cfg.n_layers):
+        lw = LayerWeights(
+            ln1=normal((H,), 0.02, 1.0, torch.float32),
+            wqkv=normal((H, (nq + 2 * nkv) * D), cfg.weight_std),
+            wo=normal((nq * D, H), cfg.weight_std),
+            ln2=normal((H,), 0.02, 1.0, torch.float32),
+            wgu=normal((H, 2 * I), cfg.weight_std),
+            wd=normal((I, H), cfg.weight_std))
+        if cfg.qk_norm:
+            lw.q_norm = normal((D,), 0.02, 1.0, torch.float32)
+            lw.k_norm = normal((D,), 0.02, 1.0, torch.float32)
+        w.layers.append(lw)
+    w.ln_f = normal((H,), 0.02, 1.0, torch.float32)
+    w.lm_head = normal((H, cfg.vocab), cfg.weight_std)
+    return w
+
+
+def _vp(t):
+    return C.c_void_p(t.data_ptr())
+
+
+class TbikDecoder:
+    """Prefill forward of a TBIK decoder with `tp` simulated ranks."""
+
+    def __init__(self, cfg: DecoderConfig, weights: DecoderWeights, leaf: int = api.LEAF_TCGEN05):
+        import torch
+        self.cfg, self.w, self.leaf = cfg, weights, leaf
+        cos, sin = rope_tables(cfg)
+        dev = weights.embed.device
+        self.cos = torch.from_numpy(cos).to(dev)
+        self.sin = torch.from_numpy(sin).to(dev)
+        self.bcfg = api.BlockConfig(64, cfg.block_k, 128, 0)
+        self.bcfg_down = api.BlockConfig(64, cfg.block_k_down, 128, 0)
+
+    # -- building blocks ------------------------------------------------------------
+    def _col(self, x, w, tp):
+        return api.column_parallel_forward(x, w, api.DeviceGroup(tp), self.bcfg, self.leaf)
+
+    def _row(self, x, w, tp, cfg):
+        return api.row_parallel_forward(x, w, api.DeviceGroup(tp), cfg, self.cfg.c_max, self.leaf)
+
+    def _norm(self, x, gamma):
+        import torch
+        return api.rmsnorm(x, gamma, self.cfg.rms_eps, out_dtype=torch.bfloat16)
+
+    def _stream(self):
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def _rope(self, src, ld, col0, heads, pos, rows):
+        import torch
+        D = self.cfg.head_dim
+        out = torch.empty(rows, heads * D, device=src.device, dtype=torch.bfloat16)
+        check(lib.tbik_rope(_vp(src), ld, col0, heads, D, _vp(pos), _vp(self.cos), _vp(self.sin), _vp(out),
+                            heads * D, rows, self._stream()))
+        return out
+
+    def _qk_normed(self, qkv, col0, heads, gamma, rows):
+        """Qwen3 q/k norm: per-head tree RMSNorm over head_dim (f32 out)."""
+        D = self.cfg.head_dim
+        blk = qkv[:, col0:col0 + heads * D].contiguous().view(rows * heads, D)
+        return api.rmsnorm(blk, gamma, self.cfg.rms_eps).view(rows, heads * D)
+
+    # -- forward ------------------------------------------------------------------------
+    def forward(self, tokens, tp: int = 1):
+        """tokens: int64 [B, S] on the device.  Returns f32 logits [B*S, vocab]."""
+        import torch
+        cfg, w = self.cfg, self.w
+        B, S = tokens.shape
+        M = B * S
+        dev = tokens.device
+        H, D, nq, nkv, I = cfg.hidden, cfg.head_dim, cfg.n_heads, cfg.n_kv_heads, cfg.intermediate
+        if S > cfg.max_pos:
+            raise api.TbikError(api.ErrorCode.BadDimension, "sequence longer than the RoPE table")
+        ids = tokens.reshape(M).contiguous()
+        pos = torch.arange(S, device=dev, dtype=torch.int32).repeat(B).contiguous()
+        h = torch.empty(M, H, device=dev, dtype=torch.bfloat16)
+        check(lib.tbik_embedding(_vp(w.embed), cfg.vocab, H, _vp(ids), M, _vp(h), self._stream()))
+        qcols = nq * D
+        kcols = nkv * D
+        scale = 1.0 / math.sqrt(D)
+        for lw in w.layers:
+            a = self._norm(h, lw.ln1)
+            qkv = self._col(a, lw.wqkv, tp)                      # f32 [M, (nq + 2 nkv) D]
+            ld = qkv.stride(0)
+            if cfg.qk_norm:
+                qn = self._qk_normed(qkv, 0, nq, lw.q_norm, M)
+                kn = self._qk_normed(qkv, qcols, nkv, lw.k_norm, M)
+                q = self._rope(qn, qcols, 0, nq, pos, M)
+                k = self._rope(kn, kcols, 0, nkv, pos, M)
+            else:
+                q = self._rope(qkv, ld, 0, nq, pos, M)
+                k = self._rope(qkv, ld, qcols, nkv, pos, M)
+            v = torch.empty(M, kcols, device=dev, dtype=torch.bfloat16)
+            check(lib.tbik_cast_bf16(C.c_void_p(qkv.data_ptr() + 4 * (qcols + kcols)), ld, M, kcols, _vp(v),
+                                     kcols, self._stream()))
+            attn = torch.empty(M, qcols, device=dev, dtype=torch.bfloat16)
+            check(lib.tbik_attention_prefill(_vp(q), qcols, _vp(k), kcols, _vp(v), kcols, B, S, nq, nkv, D,
+                                             scale, _vp(attn), qcols, self._stream()))
+            o = self._row(attn, lw.wo, tp, self.bcfg)            # f32 [M, H], tree all-reduce over tp
+            check(lib.tbik_residual_add(_vp(h), H, _vp(o), H, M, H, self._stream()))
+            a = self._norm(h, lw.ln2)
+            gu = self._col(a, lw.wgu, tp)                        # f32 [M, 2I]
+            act = torch.empty(M, I, device=dev, dtype=torch.bfloat16)
+            check(lib.tbik_silu_mul(_vp(gu), 2 * I, M, I, _vp(act), I, self._stream()))
+            d = self._row(act, lw.wd, tp, self.bcfg_down)        # f32 [M, H]
+            check(lib.tbik_residual_add(_vp(h), H, _vp(d), H, M, H, self._stream()))
+        a = self._norm(h, w.ln_f)
+        return self._col(a, w.lm_head, tp)                      # f32 logits [M, vocab]
+
+    def log_probs(self, logits, tp: int = 1, targets=None, full: bool = True):
+        """Vocab-sharded tree log-softmax over `tp` simulated vocab shards."""
+        return api.log_softmax(logits, self.cfg.vocab_groups, tp, targets, full)

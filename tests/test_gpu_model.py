@@ -1,0 +1,141 @@
+"""GPU tests of the TBIK decoder forward (BASELINE configs[2]/[3]).
+
+* each per-token kernel (SiLU*up, residual, RoPE, causal GQA attention) equals
+  its oracle restatement bit for bit;
+* the Llama-3.1-8B-shaped forward gives bit-identical logits AND log-probs at
+  TP = 1/2/4/8 (the north-star claim), for both leaf kinds of the TBIK GEMM;
+* batch invariance: a sequence's logits do not depend on what else is batched;
+* the Qwen3-32B-shaped stack (q/k norm, block_k=128 down_proj) at TP=8 is
+  batch- and TP-invariant together.
+Layer counts are reduced for test time; every layer is identical in kind.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import bits
+
+pytestmark = pytest.mark.gpu
+
+
+def u16(t):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def test_silu_mul_and_residual_vs_oracle(tb, cuda, orc):
+    import ctypes as C
+    rng = np.random.default_rng(0)
+    gu = (rng.standard_normal((37, 2 * 300)) * 4).astype(np.float32)
+    dgu = torch.from_numpy(gu).to(cuda)
+    out = torch.empty(37, 300, device=cuda, dtype=torch.bfloat16)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    tb.api.check(tb.lib.tbik_silu_mul(C.c_void_p(dgu.data_ptr()), 600, 37, 300, C.c_void_p(out.data_ptr()), 300, s))
+    assert np.array_equal(u16(out), orc.silu_mul(gu, 300))
+    h = torch.randn(37, 300, device=cuda).to(torch.bfloat16)
+    f = torch.randn(37, 300, device=cuda)
+    want = orc.residual_add(u16(h), f.cpu().numpy())
+    tb.api.check(tb.lib.tbik_residual_add(C.c_void_p(h.data_ptr()), 300, C.c_void_p(f.data_ptr()), 300, 37, 300, s))
+    assert np.array_equal(u16(h), want)
+
+
+def test_rope_and_attention_vs_oracle(tb, cuda, orc):
+    import ctypes as C
+
+    from paper_2511_17826_b200 import model as mdl
+    cfg = mdl.llama31_8b(1)
+    cos, sin = mdl.rope_tables(cfg)
+    B, S, nq, nkv, D = 2, 48, 4, 2, 128
+    rng = np.random.default_rng(1)
+    qkv = rng.standard_normal((B * S, (nq + 2 * nkv) * D)).astype(np.float32)
+    pos = np.tile(np.arange(S, dtype=np.int32), B)
+    dq = torch.from_numpy(qkv).to(cuda)
+    dpos = torch.from_numpy(pos).to(cuda)
+    dcos, dsin = torch.from_numpy(cos).to(cuda), torch.from_numpy(sin).to(cuda)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    q = torch.empty(B * S, nq * D, device=cuda, dtype=torch.bfloat16)
+    k = torch.empty(B * S, nkv * D, device=cuda, dtype=torch.bfloat16)
+    ld = qkv.shape[1]
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    tb.api.check(tb.lib.tbik_rope(vp(dq), ld, 0, nq, D, vp(dpos), vp(dcos), vp(dsin), vp(q), nq * D, B * S, s))
+    tb.api.check(tb.lib.tbik_rope(vp(dq), ld, nq * D, nkv, D, vp(dpos), vp(dcos), vp(dsin), vp(k), nkv * D, B * S, s))
+    assert np.array_equal(u16(q), orc.rope(qkv, 0, nq, D, pos, cos, sin))
+    assert np.array_equal(u16(k), orc.rope(qkv, nq * D, nkv, D, pos, cos, sin))
+    v = torch.from_numpy(qkv[:, (nq + nkv) * D:].copy()).to(cuda).to(torch.bfloat16)
+    out = torch.empty(B * S, nq * D, device=cuda, dtype=torch.bfloat16)
+    scale = 1.0 / np.sqrt(D)
+    tb.api.check(tb.lib.tbik_attention_prefill(vp(q), nq * D, vp(k), nkv * D, vp(v), nkv * D, B, S, nq, nkv, D,
+                                               scale, vp(out), nq * D, s))
+    want = orc.attention_prefill(u16(q), u16(k), u16(v), B, S, nq, nkv, scale)
+    assert np.array_equal(u16(out), want)
+    # close to a float64 causal softmax attention on the same bf16 inputs
+    qf = u16(q).astype(np.uint32) << 16
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        q.float().view(B, S, nq, D).transpose(1, 2), k.float().view(B, S, nkv, D).transpose(1, 2)
+        .repeat_interleave(nq // nkv, 1), v.float().view(B, S, nkv, D).transpose(1, 2).repeat_interleave(nq // nkv, 1),
+        is_causal=True).transpose(1, 2).reshape(B * S, nq * D)
+    assert (out.float() - ref).abs().max().item() < 2e-2
+    del qf
+
+
+@pytest.fixture(scope="module")
+def llama2(cuda):
+    from paper_2511_17826_b200 import model as mdl
+    cfg = mdl.llama31_8b(n_layers=2)
+    w = mdl.random_weights(cfg, seed=1)
+    return cfg, w
+
+
+@pytest.mark.parametrize("leaf", ["tc", "fma"])
+def test_llama_forward_bit_identical_across_tp(tb, cuda, llama2, leaf):
+    from paper_2511_17826_b200 import model as mdl
+    cfg, w = llama2
+    dec = mdl.TbikDecoder(cfg, w, tb.LEAF_TCGEN05 if leaf == "tc" else tb.LEAF_FMA)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(5)
+    B, S = (2, 128) if leaf == "tc" else (1, 16)
+    tokens = torch.randint(0, cfg.vocab, (B, S), device=cuda, generator=g)
+    targets = torch.randint(0, cfg.vocab, (B * S,), device=cuda, generator=g)
+    ref_logits = ref_lp = None
+    for tp in (1, 2, 4, 8):
+        logits = dec.forward(tokens, tp)
+        lse, lp, tlp = dec.log_probs(logits, tp, targets)
+        assert torch.isfinite(logits).all()
+        if ref_logits is None:
+            ref_logits, ref_lp, ref_tlp = logits, lp, tlp
+            continue
+        assert torch.equal(logits.view(torch.int32), ref_logits.view(torch.int32)), f"logits differ at tp={tp}"
+        assert torch.equal(lp.view(torch.int32), ref_lp.view(torch.int32)), f"log-probs differ at tp={tp}"
+        assert torch.equal(tlp.view(torch.int32), ref_tlp.view(torch.int32))
+
+
+def test_llama_forward_batch_invariance(tb, cuda, llama2):
+    from paper_2511_17826_b200 import model as mdl
+    cfg, w = llama2
+    dec = mdl.TbikDecoder(cfg, w)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(6)
+    tokens = torch.randint(0, cfg.vocab, (3, 64), device=cuda, generator=g)
+    full = dec.forward(tokens, 2)
+    for b in range(3):
+        one = dec.forward(tokens[b:b + 1].contiguous(), 4)
+        assert torch.equal(one.view(torch.int32), full[b * 64:(b + 1) * 64].view(torch.int32)), b
+
+
+def test_qwen3_stack_tp8_batch_sweep(tb, cuda):
+    from paper_2511_17826_b200 import model as mdl
+    cfg = mdl.qwen3_32b(n_layers=2)
+    w = mdl.random_weights(cfg, seed=2)
+    dec = mdl.TbikDecoder(cfg, w)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(7)
+    S = 32
+    tokens = torch.randint(0, cfg.vocab, (8, S), device=cuda, generator=g)
+    ref = dec.forward(tokens[:1].contiguous(), 1)          # batch 1, TP 1
+    _, ref_lp, _ = dec.log_probs(ref, 1)
+    for batch in (2, 8):
+        out = dec.forward(tokens[:batch].contiguous(), 8)  # batch > 1, TP 8
+        assert torch.equal(out[:S].view(torch.int32), ref.view(torch.int32)), f"batch {batch}"
+        _, lp, _ = dec.log_probs(out, 8)
+        assert torch.equal(lp[:S].view(torch.int32), ref_lp.view(torch.int32))
+    del w
+    torch.cuda.empty_cache()
