@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--leaf", choices=["tc", "fma"], default="tc")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-forward", action="store_true",
+                    help="skip the full Llama-3.1-8B forward (logits bit-identity across TP)")
     return ap.parse_args()
 
 
@@ -373,6 +375,14 @@ def run_tbik(args):
             sweep["tbik_fma_tflops"].append(f / (t_fma * 1e-3) / 1e12 if t_fma else None)
             sweep["cublas_bf16_tflops"].append(f / (t_cb * 1e-3) / 1e12)
 
+    # ---- the metric's second half: bit-exact logits across TP on the Llama forward ----
+    forward = None
+    if rank == 0 and world == 1 and not args.no_forward:
+        del w, x, x_full, y, yb, x_host, y_host, x_dev
+        torch.cuda.empty_cache()
+        from tools.forward_bench import run as forward_run
+        forward = forward_run("llama3.1-8b", 32, 4, 256, reps=3, tps=(1, 2, 4, 8))
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -395,6 +405,7 @@ def run_tbik(args):
             "roofline": roof, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "noninvariant": noninv, "tp_invariance_bit_identical": tp_ok, "sweep": sweep,
             "cpu_baseline": cpu,
+            "forward": forward,
         }
         print(json.dumps(line))
     if group is not None:
