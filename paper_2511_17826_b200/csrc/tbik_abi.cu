@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -147,11 +148,18 @@ tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mod
   const size_t slice = static_cast<size_t>(v.M) * v.N;
   if (leaf_mode == TBIK_LEAF_TCGEN05) {
     const int64_t tiles_mn = tc_pair_tiles(v);
-    // Split the K range of each output tile into 2^j aligned subtrees only to
-    // fill the machine (74 CTA pairs); the combine continues the same tree
-    // (Theorem 1), so the split never changes bits.
-    int64_t units = 1;
-    if (tiles_mn < 2 * 74) units = std::min<int64_t>(v.L, next_pow2((2 * 74 + tiles_mn - 1) / tiles_mn));
+    // Split the K range of each output tile into 2^j aligned subtrees only when
+    // the machine would otherwise idle; the combine continues the same tree
+    // (Theorem 1), so the split never changes bits.  Measured on B200
+    // (tools/tune_units.py, K=14336 N=4096): a split only pays below 64 pair
+    // tiles, and then only by 2 (deeper splits lose to the extra subtree
+    // traffic and the per-item pipeline refill).
+    int64_t units = tiles_mn >= 64 ? 1 : std::min<int64_t>(v.L, 2);
+    (void)next_pow2;
+    if (const char* e = std::getenv("TBIK_TC_UNITS")) {  // tuning override (power of two <= leaves)
+      const int64_t u = std::atoll(e);
+      if (u >= 1 && u <= v.L && (u & (u - 1)) == 0) units = u;
+    }
     if (units <= 1) {
       GemmOut o{OUT_FULL, v.T, C, ldc, 0};
       return launch_tc_gemm(v, o, s);
