@@ -801,46 +801,43 @@ int tbo_rope(const float* x, int64_t ldx, int64_t col0, int heads, int D, const 
   return TBO_OK;
 }
 
-/* Causal GQA prefill attention, head_dim 128: per (row, head) the score of key
- * j is the contiguous-halves tree over 32 lane partials (lane l: fma chain over
- * dims 4l..4l+3), times scale; online softmax over j = 0..i ascending. */
+/* Causal GQA prefill attention, head_dim 128 (csrc/tbik_model.cu attn2_kernel):
+ * per (sequence, q head, query i), keys j = 0..i:
+ *   s_j = (ascending-d fma chain q[d] k_j[d] from +0) * scale
+ *   m   = max_j s_j  (exact);  p_j = exp(s_j - m);  l = ascending sum of p_j
+ *   o[d]= ascending-j fma chain of p_j v_j[d] from +0;  out = bf16(o[d] / l) */
 int tbo_attention_prefill(const uint16_t* q, int64_t ldq, const uint16_t* k, int64_t ldk, const uint16_t* v,
                           int64_t ldv, int64_t batch, int S, int nq, int nkv, float scale, uint16_t* out,
                           int64_t ldo) {
   if (nkv < 1 || nq % nkv) return TBO_BAD_DIMENSION;
+  float* p = (float*)malloc((size_t)S * sizeof(float));
+  if (!p) return TBO_BAD_ARGUMENT;
   for (int64_t row = 0; row < batch * S; ++row) {
     const int64_t seq0 = (row / S) * S;
     const int i = (int)(row - seq0);
     for (int h = 0; h < nq; ++h) {
       const int kh = h / (nq / nkv);
-      float m = -INFINITY, l = 0.0f, o[128];
-      for (int d = 0; d < 128; ++d) o[d] = 0.0f;
+      float m = -INFINITY;
       for (int j = 0; j <= i; ++j) {
         const int64_t kr = seq0 + j;
-        float part[32];
-        for (int ln = 0; ln < 32; ++ln) {
-          float a = 0.0f;
-          for (int t = 0; t < 4; ++t)
-            a = fmaf(tbo_bf16_to_f32(q[row * ldq + h * 128 + ln * 4 + t]),
-                     tbo_bf16_to_f32(k[kr * ldk + kh * 128 + ln * 4 + t]), a);
-          part[ln] = a;
-        }
-        /* xor butterfly 1,2,4,8,16 == contiguous-halves tree over the 32 lanes */
-        const float s = tree_reduce_rec(part, 32) * scale;
-        const uint16_t* vr = v + kr * ldv + kh * 128;
-        if (s > m) {
-          const float a = tbo_exp(m - s);
-          l = l * a + 1.0f;
-          for (int d = 0; d < 128; ++d) o[d] = o[d] * a + tbo_bf16_to_f32(vr[d]);
-          m = s;
-        } else {
-          const float pj = tbo_exp(s - m);
-          l = l + pj;
-          for (int d = 0; d < 128; ++d) o[d] = fmaf(pj, tbo_bf16_to_f32(vr[d]), o[d]);
-        }
+        float a = 0.0f;
+        for (int d = 0; d < 128; ++d)
+          a = fmaf(tbo_bf16_to_f32(q[row * ldq + h * 128 + d]), tbo_bf16_to_f32(k[kr * ldk + kh * 128 + d]), a);
+        p[j] = a * scale;
+        m = fmaxf(m, p[j]);
       }
-      for (int d = 0; d < 128; ++d) out[row * ldo + h * 128 + d] = tbo_bf16_round(o[d] / l);
+      float l = 0.0f;
+      for (int j = 0; j <= i; ++j) {
+        p[j] = tbo_exp(p[j] - m);
+        l = l + p[j];
+      }
+      for (int d = 0; d < 128; ++d) {
+        float o = 0.0f;
+        for (int j = 0; j <= i; ++j) o = fmaf(p[j], tbo_bf16_to_f32(v[(seq0 + j) * ldv + kh * 128 + d]), o);
+        out[row * ldo + h * 128 + d] = tbo_bf16_round(o / l);
+      }
     }
   }
+  free(p);
   return TBO_OK;
 }

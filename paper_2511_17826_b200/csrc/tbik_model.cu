@@ -71,69 +71,172 @@ __global__ void cast_kernel(const float* __restrict__ x, int64_t ldx, int64_t co
     out[row * ldo + j] = f32_to_bf16_bits(x[row * ldx + j]);
 }
 
-// ---- causal GQA prefill attention ---------------------------------------------------------
-// One warp per (sequence, q head, query).  Lane l owns head dims [4l, 4l+4) (D = 128).
-// score_j = T(lane partial fma chains) * scale   (T = contiguous-halves butterfly)
-// online softmax over keys j = 0..i ascending with the shared exp:
-//   s > m: a = exp(m - s); l = l*a + 1; o = o*a + v_j; m = s
-//   else : p = exp(s - m); l = l + p;   o = fma(p, v_j, o)
-// out = o / l, rounded to bf16.  Fixed order per (seq, head, query): batch- and
-// TP-(head-sharding-)invariant.
-__global__ void __launch_bounds__(256) attn_kernel(const uint16_t* __restrict__ q, int64_t ldq,
-                                                   const uint16_t* __restrict__ k, int64_t ldk,
-                                                   const uint16_t* __restrict__ v, int64_t ldv, int S, int nq,
-                                                   int nkv, float scale, uint16_t* __restrict__ out, int64_t ldo,
-                                                   int64_t total_rows) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  // gw enumerates (row = token, head)
-  const int64_t row = gw / nq;
-  const int h = static_cast<int>(gw - row * nq);
-  if (row >= total_rows) return;
-  const int64_t seq0 = (row / S) * S;  // first token of this sequence
-  const int i = static_cast<int>(row - seq0);
+// ---- causal GQA prefill attention, tiled two-pass form -------------------------------------
+// Canonical order (restated in oracle tbo_attention_prefill), per (sequence, q head,
+// query i), keys j = 0..i:
+//   s_j = (ascending-d fma chain of q[d] k_j[d] from +0) * scale
+//   m   = max_j s_j                                  (exact, order-free)
+//   p_j = exp(s_j - m)                               (shared exp)
+//   l   = ((p_0 + p_1) + p_2) + ...                  (ascending j)
+//   o[d]= fma chain over ascending j of p_j v_j[d]   (from +0)
+//   out = bf16(o[d] / l)
+// One CTA = (64-query block, q head, sequence), 256 threads; K / V key blocks of
+// 64 staged through shared memory as f32; scores for the whole causal prefix kept
+// in shared memory (S <= 512).  Thread (i = t % 64, part = t / 64): 4 key phases in
+// the score pass, 4 x 32-dim slices in the P.V pass; 4 independent fma chains each
+// for ILP.  Per-query arithmetic never depends on the batch or the head sharding.
+constexpr int AQ = 64;       // queries per CTA
+constexpr int AK = 64;       // keys per staged block
+constexpr int AD = 128;      // head dim
+constexpr int AKP = AD + 4;  // padded f32 row of a staged K/V block
+
+__global__ void __launch_bounds__(256) attn2_kernel(const uint16_t* __restrict__ q, int64_t ldq,
+                                                    const uint16_t* __restrict__ k, int64_t ldk,
+                                                    const uint16_t* __restrict__ v, int64_t ldv, int S, int nq,
+                                                    int nkv, float scale, uint16_t* __restrict__ out, int64_t ldo) {
+  extern __shared__ float sm[];
+  float* kv = sm;                // [AK][AKP]
+  float* P = sm + AK * AKP;      // [AQ][S + 1]
+  float* red = P + AQ * (S + 1);  // [4][AQ] partial maxima, then l
+  const int pst = S + 1;
+  const int tid = threadIdx.x;
+  const int qi = tid & (AQ - 1);
+  const int part = tid >> 6;  // 0..3
+  const int qb = blockIdx.x, h = blockIdx.y;
+  const int64_t seq0 = static_cast<int64_t>(blockIdx.z) * S;
   const int kh = h / (nq / nkv);
-  const uint16_t* qp = q + row * ldq + h * 128 + lane * 4;
-  const uint2 qraw = *reinterpret_cast<const uint2*>(qp);
-  const float q0 = bf(qraw.x & 0xFFFF), q1 = bf(qraw.x >> 16), q2 = bf(qraw.y & 0xFFFF), q3 = bf(qraw.y >> 16);
-  float m = __int_as_float(0xFF800000), l = 0.0f;
-  float o0 = 0.0f, o1 = 0.0f, o2 = 0.0f, o3 = 0.0f;
-  for (int j = 0; j <= i; ++j) {
-    const int64_t kr = seq0 + j;
-    const uint2 kraw = *reinterpret_cast<const uint2*>(k + kr * ldk + kh * 128 + lane * 4);
-    float part = 0.0f;
-    part = __fmaf_rn(q0, bf(kraw.x & 0xFFFF), part);
-    part = __fmaf_rn(q1, bf(kraw.x >> 16), part);
-    part = __fmaf_rn(q2, bf(kraw.y & 0xFFFF), part);
-    part = __fmaf_rn(q3, bf(kraw.y >> 16), part);
+  const int i = qb * AQ + qi;  // query position in the sequence
+  const bool valid = i < S;
+  const int last_key = min(S, (qb + 1) * AQ) - 1;  // keys needed by this block
+
+  // q row in registers (f32).
+  float qr[AD];
+  {
+    const uint16_t* qp = q + (seq0 + (valid ? i : 0)) * ldq + h * AD;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) part = __fadd_rn(part, __shfl_xor_sync(0xffffffffu, part, d));
-    const float s = __fmul_rn(part, scale);
-    const uint2 vraw = *reinterpret_cast<const uint2*>(v + kr * ldv + kh * 128 + lane * 4);
-    const float v0 = bf(vraw.x & 0xFFFF), v1 = bf(vraw.x >> 16), v2 = bf(vraw.y & 0xFFFF), v3 = bf(vraw.y >> 16);
-    if (s > m) {
-      const float a = tb_exp(__fsub_rn(m, s));
-      l = __fadd_rn(__fmul_rn(l, a), 1.0f);
-      o0 = __fadd_rn(__fmul_rn(o0, a), v0);
-      o1 = __fadd_rn(__fmul_rn(o1, a), v1);
-      o2 = __fadd_rn(__fmul_rn(o2, a), v2);
-      o3 = __fadd_rn(__fmul_rn(o3, a), v3);
-      m = s;
-    } else {
-      const float pj = tb_exp(__fsub_rn(s, m));
-      l = __fadd_rn(l, pj);
-      o0 = __fmaf_rn(pj, v0, o0);
-      o1 = __fmaf_rn(pj, v1, o1);
-      o2 = __fmaf_rn(pj, v2, o2);
-      o3 = __fmaf_rn(pj, v3, o3);
+    for (int d = 0; d < AD; d += 8) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(qp + d);
+      const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        qr[d + 2 * e] = __uint_as_float(w[e] << 16);
+        qr[d + 2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+      }
     }
   }
-  uint16_t* op = out + row * ldo + h * 128 + lane * 4;
-  const uint32_t lo = static_cast<uint32_t>(f32_to_bf16_bits(__fdiv_rn(o0, l))) |
-                      (static_cast<uint32_t>(f32_to_bf16_bits(__fdiv_rn(o1, l))) << 16);
-  const uint32_t hi = static_cast<uint32_t>(f32_to_bf16_bits(__fdiv_rn(o2, l))) |
-                      (static_cast<uint32_t>(f32_to_bf16_bits(__fdiv_rn(o3, l))) << 16);
-  *reinterpret_cast<uint2*>(op) = make_uint2(lo, hi);
+
+  // ---- pass 1: scores ----
+  for (int kb = 0; kb * AK <= last_key; ++kb) {
+    __syncthreads();
+    for (int e = tid; e < AK * AD / 8; e += blockDim.x) {  // stage K block as f32
+      const int r = e / (AD / 8), c = (e % (AD / 8)) * 8;
+      const int key = kb * AK + r;
+      float* dst = kv + r * AKP + c;
+      if (key <= last_key) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(k + (seq0 + key) * ldk + kh * AD + c);
+        const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          dst[2 * x] = __uint_as_float(w[x] << 16);
+          dst[2 * x + 1] = __uint_as_float(w[x] & 0xFFFF0000u);
+        }
+      }
+    }
+    __syncthreads();
+    // keys jj = part + 4 * (4 r + u), u = 0..3 in flight together
+#pragma unroll 1
+    for (int r = 0; r < AK / 16; ++r) {
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      const float* kr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) kr[u] = kv + (part + 4 * (4 * r + u)) * AKP;
+#pragma unroll
+      for (int d = 0; d < AD; d += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 kk = *reinterpret_cast<const float4*>(kr[u] + d);
+          acc[u] = __fmaf_rn(qr[d], kk.x, acc[u]);
+          acc[u] = __fmaf_rn(qr[d + 1], kk.y, acc[u]);
+          acc[u] = __fmaf_rn(qr[d + 2], kk.z, acc[u]);
+          acc[u] = __fmaf_rn(qr[d + 3], kk.w, acc[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int key = kb * AK + part + 4 * (4 * r + u);
+        if (key <= i && valid) P[qi * pst + key] = __fmul_rn(acc[u], scale);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- softmax: exact max, shared exp, ascending sum ----
+  float mx = __int_as_float(0xFF800000);
+  if (valid)
+    for (int j = part; j <= i; j += 4) mx = fmaxf(mx, P[qi * pst + j]);
+  red[part * AQ + qi] = mx;
+  __syncthreads();
+  mx = fmaxf(fmaxf(red[qi], red[AQ + qi]), fmaxf(red[2 * AQ + qi], red[3 * AQ + qi]));
+  if (valid)
+    for (int j = part; j <= i; j += 4) P[qi * pst + j] = tb_exp(__fsub_rn(P[qi * pst + j], mx));
+  __syncthreads();
+  if (part == 0) {
+    float l = 0.0f;
+    if (valid)
+      for (int j = 0; j <= i; ++j) l = __fadd_rn(l, P[qi * pst + j]);
+    red[qi] = l;
+  }
+
+  // ---- pass 2: o[d] = sum_j p_j v_j[d], dims [32 part, 32 part + 32) ----
+  float o[32];
+#pragma unroll
+  for (int d = 0; d < 32; ++d) o[d] = 0.0f;
+  const int d0 = part * 32;
+  for (int kb = 0; kb * AK <= last_key; ++kb) {
+    __syncthreads();
+    for (int e = tid; e < AK * AD / 8; e += blockDim.x) {  // stage V block as f32
+      const int r = e / (AD / 8), c = (e % (AD / 8)) * 8;
+      const int key = kb * AK + r;
+      float* dst = kv + r * AKP + c;
+      if (key <= last_key) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(v + (seq0 + key) * ldv + kh * AD + c);
+        const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          dst[2 * x] = __uint_as_float(w[x] << 16);
+          dst[2 * x + 1] = __uint_as_float(w[x] & 0xFFFF0000u);
+        }
+      }
+    }
+    __syncthreads();
+    const int jend = valid ? min(i, kb * AK + AK - 1) : -1;
+    for (int j = kb * AK; j <= jend; ++j) {
+      const float pj = P[qi * pst + j];
+      const float* vr = kv + (j - kb * AK) * AKP + d0;
+#pragma unroll
+      for (int d = 0; d < 32; d += 4) {
+        const float4 vv = *reinterpret_cast<const float4*>(vr + d);
+        o[d] = __fmaf_rn(pj, vv.x, o[d]);
+        o[d + 1] = __fmaf_rn(pj, vv.y, o[d + 1]);
+        o[d + 2] = __fmaf_rn(pj, vv.z, o[d + 2]);
+        o[d + 3] = __fmaf_rn(pj, vv.w, o[d + 3]);
+      }
+    }
+  }
+  __syncthreads();
+  if (valid) {
+    const float l = red[qi];
+    uint16_t* op = out + (seq0 + i) * ldo + h * AD + d0;
+#pragma unroll
+    for (int d = 0; d < 32; d += 8) {
+      uint32_t w[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+        w[x] = static_cast<uint32_t>(f32_to_bf16_bits(__fdiv_rn(o[d + 2 * x], l))) |
+               (static_cast<uint32_t>(f32_to_bf16_bits(__fdiv_rn(o[d + 2 * x + 1], l))) << 16);
+      *reinterpret_cast<uint4*>(op + d) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
 }
 
 // ---- SiLU(gate) * up  (demo.cpp:36-45, :171-174) ---------------------------------------
@@ -228,13 +331,23 @@ tbik_status tbik_attention_prefill(const void* q, int64_t ldq, const void* k, in
   if (head_dim != 128) return set_error(TBIK_UNSUPPORTED, "attention: head_dim must be 128");
   if (n_kv_heads < 1 || n_q_heads % n_kv_heads) return set_error(TBIK_BAD_DIMENSION, "attention: bad GQA heads");
   if (ldq % 4 || ldk % 4 || ldv % 4 || ldo % 4) return set_error(TBIK_BAD_ARGUMENT, "attention: strides % 4");
+  if (seq_len < 1 || seq_len > 512) return set_error(TBIK_UNSUPPORTED, "attention: seq_len must be in [1, 512]");
+  if (batch < 1 || batch > 65535 || n_q_heads > 65535) return set_error(TBIK_BAD_DIMENSION, "attention: grid");
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
+       reinterpret_cast<uintptr_t>(out)) & 15 || ldq % 8 || ldk % 8 || ldv % 8 || ldo % 8)
+    return set_error(TBIK_BAD_ARGUMENT, "attention: 16-byte aligned rows required");
   TBIK_TRY(need_device());
-  const int64_t rows = batch * seq_len;
-  const int64_t warps = rows * n_q_heads;
-  const int64_t blocks = (warps * 32 + 255) / 256;
-  attn_kernel<<<static_cast<unsigned>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  const size_t smem = (static_cast<size_t>(AK) * AKP + static_cast<size_t>(AQ) * (seq_len + 1) + 4 * AQ) * 4;
+  static size_t attr = 0;
+  if (attr < smem) {
+    TBIK_CUDA(cudaFuncSetAttribute(attn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr = smem;
+  }
+  dim3 grid(static_cast<unsigned>((seq_len + AQ - 1) / AQ), static_cast<unsigned>(n_q_heads),
+            static_cast<unsigned>(batch));
+  attn2_kernel<<<grid, 256, smem, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(q), ldq, static_cast<const uint16_t*>(k), ldk, static_cast<const uint16_t*>(v), ldv,
-      seq_len, n_q_heads, n_kv_heads, scale, static_cast<uint16_t*>(out), ldo, rows);
+      seq_len, n_q_heads, n_kv_heads, scale, static_cast<uint16_t*>(out), ldo);
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;
