@@ -241,25 +241,58 @@ __global__ void __launch_bounds__(256) attn2_kernel(const uint16_t* __restrict__
 
 // ---- SiLU(gate) * up  (demo.cpp:36-45, :171-174) ---------------------------------------
 // gu: f32 [M, ld] with gate in columns [0, I) and up in [I, 2I).  silu(z) = z / (1 + exp(-z)).
+__device__ __forceinline__ uint16_t silu_mul1(float z, float up) {
+  const float s = __fdiv_rn(z, __fadd_rn(1.0f, tb_exp(-z)));
+  return f32_to_bf16_bits(__fmul_rn(s, up));
+}
+
+// VEC: 4 consecutive columns per thread (16-byte loads, 8-byte stores).
+template <bool VEC>
 __global__ void silu_mul_kernel(const float* __restrict__ gu, int64_t ld, int64_t I, uint16_t* __restrict__ out,
                                 int64_t ldo) {
   const int64_t row = blockIdx.y;
-  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < I;
-       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float z = gu[row * ld + j];
-    const float s = __fdiv_rn(z, __fadd_rn(1.0f, tb_exp(-z)));
-    out[row * ldo + j] = f32_to_bf16_bits(__fmul_rn(s, gu[row * ld + I + j]));
+  const float* g = gu + row * ld;
+  uint16_t* o = out + row * ldo;
+  const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (VEC) {
+    for (int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; j < I; j += step * 4) {
+      const float4 z = *reinterpret_cast<const float4*>(g + j);
+      const float4 u = *reinterpret_cast<const float4*>(g + I + j);
+      const uint32_t lo = silu_mul1(z.x, u.x) | (static_cast<uint32_t>(silu_mul1(z.y, u.y)) << 16);
+      const uint32_t hi = silu_mul1(z.z, u.z) | (static_cast<uint32_t>(silu_mul1(z.w, u.w)) << 16);
+      *reinterpret_cast<uint2*>(o + j) = make_uint2(lo, hi);
+    }
+  } else {
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < I; j += step)
+      o[j] = silu_mul1(g[j], g[I + j]);
   }
 }
 
 // ---- residual: h = bf16(h + f)  (demo.cpp:216) -------------------------------------------------
+template <bool VEC>
 __global__ void residual_kernel(uint16_t* __restrict__ h, int64_t ldh, const float* __restrict__ f, int64_t ldf,
                                 int64_t cols) {
   const int64_t row = blockIdx.y;
-  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < cols;
-       j += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    h[row * ldh + j] = f32_to_bf16_bits(__fadd_rn(bf(h[row * ldh + j]), f[row * ldf + j]));
+  uint16_t* hr = h + row * ldh;
+  const float* fr = f + row * ldf;
+  const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (VEC) {
+    for (int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; j < cols; j += step * 4) {
+      const uint2 hv = *reinterpret_cast<const uint2*>(hr + j);
+      const float4 fv = *reinterpret_cast<const float4*>(fr + j);
+      const uint32_t lo = f32_to_bf16_bits(__fadd_rn(bf(hv.x & 0xFFFF), fv.x)) |
+                          (static_cast<uint32_t>(f32_to_bf16_bits(__fadd_rn(bf(hv.x >> 16), fv.y))) << 16);
+      const uint32_t hi = f32_to_bf16_bits(__fadd_rn(bf(hv.y & 0xFFFF), fv.z)) |
+                          (static_cast<uint32_t>(f32_to_bf16_bits(__fadd_rn(bf(hv.y >> 16), fv.w))) << 16);
+      *reinterpret_cast<uint2*>(hr + j) = make_uint2(lo, hi);
+    }
+  } else {
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < cols; j += step)
+      hr[j] = f32_to_bf16_bits(__fadd_rn(bf(hr[j]), fr[j]));
+  }
 }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 tbik_status need_device() {
   if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
@@ -358,8 +391,13 @@ tbik_status tbik_silu_mul(const float* gate_up, int64_t ld, int64_t rows, int64_
   if (!gate_up || !out) return set_error(TBIK_BAD_ARGUMENT, "null argument");
   if (rows < 1 || inter < 1 || rows > 65535) return set_error(TBIK_BAD_DIMENSION, "silu_mul: bad dimensions");
   TBIK_TRY(need_device());
-  silu_mul_kernel<<<row_grid(rows, inter, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      gate_up, ld, inter, static_cast<uint16_t*>(out), ldo);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (inter % 4 == 0 && ld % 4 == 0 && ldo % 4 == 0 && aligned16(gate_up) && aligned16(out))
+    silu_mul_kernel<true><<<row_grid(rows, inter / 4, 256), 256, 0, s>>>(gate_up, ld, inter,
+                                                                        static_cast<uint16_t*>(out), ldo);
+  else
+    silu_mul_kernel<false><<<row_grid(rows, inter, 256), 256, 0, s>>>(gate_up, ld, inter,
+                                                                     static_cast<uint16_t*>(out), ldo);
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;
@@ -370,8 +408,11 @@ tbik_status tbik_residual_add(void* h, int64_t ldh, const float* f, int64_t ldf,
   if (!h || !f) return set_error(TBIK_BAD_ARGUMENT, "null argument");
   if (rows < 1 || cols < 1 || rows > 65535) return set_error(TBIK_BAD_DIMENSION, "residual: bad dimensions");
   TBIK_TRY(need_device());
-  residual_kernel<<<row_grid(rows, cols, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<uint16_t*>(h), ldh, f, ldf, cols);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cols % 4 == 0 && ldh % 4 == 0 && ldf % 4 == 0 && aligned16(h) && aligned16(f))
+    residual_kernel<true><<<row_grid(rows, cols / 4, 256), 256, 0, s>>>(static_cast<uint16_t*>(h), ldh, f, ldf, cols);
+  else
+    residual_kernel<false><<<row_grid(rows, cols, 256), 256, 0, s>>>(static_cast<uint16_t*>(h), ldh, f, ldf, cols);
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;
