@@ -28,6 +28,7 @@
 // the tensor core's block_k-long accumulation.  Nothing in
 // the per-element arithmetic depends on M, the tile position, the unit split, the
 // raster or the TP shard -> batch- and TP-invariant by construction.
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -456,15 +457,28 @@ bool tc_supported(const GemmView& v, std::string* why) {
   return true;
 }
 
-int64_t tc_pair_tiles(const GemmView& v) { return ((v.M + PAIR_M - 1) / PAIR_M) * ((v.N + BN - 1) / BN); }
+bool tc_use_wide(const GemmView& v);
+int64_t tc_pair_tiles(const GemmView& v) {
+  if (tc_use_wide(v)) return tc_wide_pair_tiles(v);
+  return ((v.M + PAIR_M - 1) / PAIR_M) * ((v.N + BN - 1) / BN);
+}
 
 // Diagnostics build only (see tools/tc_stats.py); the production kernel carries no counters.
 int tc_debug_stats(unsigned long long*, int) { return 0; }
+
+// 256 x 256 pair tiles (tbik_gemm_tc_wide.cu) when the level-1 traffic allows it;
+// TBIK_TC_WIDE=0/1 forces the choice (a pure scheduling knob: same bits).
+bool tc_use_wide(const GemmView& v) {
+  const char* e = std::getenv("TBIK_TC_WIDE");
+  if (e && *e) return std::atoi(e) != 0;
+  return false;
+}
 
 tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) {
   std::string why;
   if (!tc_supported(v, &why)) return set_error(TBIK_UNSUPPORTED, why);
   if (o.mode == OUT_GROUPS) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: GROUPS mode is FMA-only");
+  if (tc_use_wide(v)) return launch_tc_gemm_wide(v, o, s);
   CUtensorMap mA, mB;
   TBIK_TRY(make_map_2d(&mA, v.A, static_cast<uint64_t>(v.K), static_cast<uint64_t>(v.M),
                        static_cast<uint64_t>(v.lda) * 2, KSTAGE, BM));

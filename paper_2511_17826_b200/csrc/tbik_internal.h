@@ -50,6 +50,9 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s);
 bool tc_supported(const GemmView& v, std::string* why);
 // Output tiles of the tcgen05 kernel (one per CTA pair): 256 rows x 128 columns.
 int64_t tc_pair_tiles(const GemmView& v);
+// The 256 x 256 pair-tile variant (tbik_gemm_tc_wide.cu).
+tbik_status launch_tc_gemm_wide(const GemmView& v, const GemmOut& o, cudaStream_t s);
+int64_t tc_wide_pair_tiles(const GemmView& v);
 
 tbik_status launch_tree_combine(const float* ws, int64_t X, int64_t fold, int64_t rows,
                                 int64_t cols, float* out, int64_t ldo, cudaStream_t s);
