@@ -10,25 +10,34 @@
 // 128 x 128 tile.  Pairs loop over work items (output tile x K unit) with an
 // L2-grouped raster (8 M-blocks share one pass over W).
 //
-// Warp roles per CTA (256 threads, one CTA per SM):
+// Warp roles per CTA (384 threads, one CTA per SM):
 //   warp 0      TMA producer: 8-stage ring of {A 128x64, B 64x64} 128B-swizzled
 //               tiles (2SM TMA; completion counted on the leader's barrier)
 //   warp 1      (leader CTA) MMA issuer: for every leaf tile, block_k/16 MMAs into
 //               a ZEROED TMEM accumulator; two accumulators so leaf t+1 is computed
 //               while leaf t is merged
 //   warp 2      TMEM allocator (512 columns, cta_group::2)
-//   warps 4-7   merge warps: thread (q, lane) owns output row 32q + lane, 128
-//               columns.  For every leaf: tcgen05.ld + __fadd_rn, verbatim the
-//               reference's reduction:
+//   warps 4-11  merge warps: warp w may read TMEM lanes 32(w%4)..; thread (w, lane)
+//               owns output row 32(w%4) + lane, columns 64((w-4)/4) + [0, 64).
+//               For every leaf: tcgen05.ld + __fadd_rn, verbatim the reference's
+//               reduction:
 //                 level 0   g = ((0 + P_0) + P_1) + ... + P_{kf-1}   (matmul.cpp:100-125)
 //                 levels>=1 binary counter over group values (matmul.cpp:107-123)
-//               g in 128 registers; tree levels 1-2 in TMEM cols [256,512);
-//               deeper levels (touched once per 8+ groups) in L2-resident scratch.
+//               g in 64 registers; tree levels 1-2 in TMEM cols [256,512);
+//               deeper levels (touched once per 8+ groups) in L2-resident scratch
+//               ([col/4][row][4] slabs, 512 B per warp access).  Results leave
+//               through a 128B-swizzled 32 x 32 smem box and a TMA store.
+//   Why this shape (measured, tools/ab_epi.py): the MMA operand reads and TMA
+//   writes keep the SM's shared-memory/L1 data port ~90% busy, so every byte the
+//   merge moves through L1 costs tensor throughput.  Row-per-thread STG.128
+//   costs 32 wavefronts per 512 B; the TMA store path ~4x fewer (+5% at
+//   k_first = 1), and 8 merge warps another +6%.
 // The arithmetic above the leaf is bit-identical to the reference; the leaf is
 // the tensor core's block_k-long accumulation.  Nothing in
 // the per-element arithmetic depends on M, the tile position, the unit split, the
 // raster or the TP shard -> batch- and TP-invariant by construction.
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 
@@ -47,13 +56,19 @@ constexpr int STAGES = 8;
 constexpr int A_STAGE_BYTES = BM * KSTAGE * 2;        // 16 KB
 constexpr int B_STAGE_BYTES = KSTAGE * (BN / 2) * 2;  // 8 KB
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-constexpr int NUM_THREADS = 256;
 constexpr int TMEM_COLS = 512;
 constexpr int SLOT_LVL1 = 256;
 constexpr int SLOT_LVL2 = 384;
 constexpr int GROUP_M = 8;  // raster: M-blocks that share one pass over W
 constexpr uint32_t IDESC = umma_idesc_bf16(PAIR_M, BN, /*a_mn_major=*/0, /*b_mn_major=*/1);
-constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+// Output staging for the TMA store: per merge warp, XB buffers of 32 rows x
+// 32 f32 (4 KB, 128B-swizzled).
+constexpr int OUT_BUF_BYTES = 32 * 32 * 4;
+constexpr int out_bufs(int epi) { return epi == 4 ? 2 : 1; }
+constexpr size_t smem_bytes(int epi, int nst) {
+  return 1024 + static_cast<size_t>(nst) * STAGE_BYTES + 1024 +
+         static_cast<size_t>(epi) * out_bufs(epi) * OUT_BUF_BYTES;
+}
 
 struct TcParams {
   int M, N, K;
@@ -68,6 +83,10 @@ struct TcParams {
   long long ldo;
   long long unit_stride;
   float* scratch;  // [gridDim.x][levels-2][BN][BM] when levels > 2
+  int tma_store;   // 1: results leave through tmC (TMA), 0: direct row stores
+  int debug;       // TBIK_TC_DEBUG (perf experiments only; wrong results): 1 = skip the merge,
+                   // 2 = skip the output store, 4 = skip the tree above level 0,
+                   // 8 = skip the scratch levels, 16 = direct (non-TMA) output stores
 };
 
 // ---- cluster / 2-CTA PTX -----------------------------------------------------------
@@ -156,18 +175,39 @@ __device__ __forceinline__ int tile_chunks(const TcParams& p, int t) {
   return (kh + KSTAGE - 1) / KSTAGE;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+               "r"(src), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// EPI merge warps (4 or 8; with 8, two warps share each TMEM lane quarter and
+// split the 128 columns), LB = 32-column TMEM loads in flight per wait, NST
+// pipeline stages.
+template <int EPI, int LB, int NST>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
     tc_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        const TcParams p) {
+                        const __grid_constant__ CUtensorMap tmC, const TcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* sB = smem + NST * A_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + NST * B_STAGE_BYTES);
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* sC = smem + NST * STAGE_BYTES + 1024;  // 1024-aligned output staging
+  constexpr int XB = out_bufs(EPI);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -179,13 +219,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 2);   // one arrive.expect_tx from each CTA of the pair (leader's copy used)
       mbar_init(&empty[s], 1);  // one multicast commit from the leader's MMA thread
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);   // multicast commit
-      mbar_init(&tempty[b], 8);  // 4 merge warps x 2 CTAs (leader's copy used)
+      mbar_init(&tempty[b], 2 * EPI);  // EPI merge warps x 2 CTAs (leader's copy used)
     }
     fence_barrier_init();
   }
@@ -195,6 +235,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  if (warp < 4) {
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
     if (elect_one()) {
@@ -217,7 +258,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             const int k = t * p.bk + c * KSTAGE;
             tma_load_2d_2sm(sA + stage * A_STAGE_BYTES, &tmA, fb, k, am);
             tma_load_2d_2sm(sB + stage * B_STAGE_BYTES, &tmB, fb, bn, k);
-            if (++stage == STAGES) {
+            if (++stage == NST) {
               stage = 0;
               phase ^= 1;
             }
@@ -256,7 +297,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               umma_bf16_2cta(d, adesc, bdesc, IDESC, (c | kk) != 0 ? 1u : 0u);
             }
             umma_commit_2cta(&empty[stage], 0x3);
-            if (++stage == STAGES) {
+            if (++stage == NST) {
               stage = 0;
               phase ^= 1;
             }
@@ -266,22 +307,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
+  }
+  } else {
     // ---------------- merge warps (the TBIK reduction), both CTAs ----------------
-    const int q = warp & 3;
+    constexpr int COLS = BN * 4 / EPI;  // columns owned by this warp
+    constexpr int NCH = COLS / 32;
+    static_assert(NCH % LB == 0, "LB must divide the chunk count");
+    const int q = warp & 3;  // a warp may only touch TMEM lanes 32*(warp%4)..
+    const int col0 = ((warp - 4) >> 2) * COLS;
     const int row_in_tile = q * 32 + lane;
-    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + col0;
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
+    // Scratch levels (>= 3) are [col/4][row][4] slabs: a warp's float4 access is
+    // 512 contiguous bytes.
     float* scratch_base =
-        p.levels > 2 ? p.scratch + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - 2) * (BM * BN)
+        p.levels > 2
+            ? p.scratch + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - 2) * (BM * BN) +
+                           static_cast<size_t>(col0) * BM + static_cast<size_t>(row_in_tile) * 4
                      : nullptr;
-    float g[BN];
+
+    float g[COLS];
+    int xb = 0;  // output staging buffer toggle
     uint32_t acc_iter = 0;
     for (long long item = pair; item < p.items; item += npairs) {
       const Item it = decode(p, item);
       const int grow = it.m0 + static_cast<int>(rank) * BM + row_in_tile;
       const bool row_ok = grow < p.M;
-      const int ncols = min(BN, p.N - it.n0);
+      const int ncols = min(COLS, p.N - it.n0 - col0);
       int t_in_group = 0;
       uint32_t groups_done = 0;
       for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
@@ -290,10 +342,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&tfull[buf], use & 1);
         tc_fence_after();
         const uint32_t acc = lane_base + buf * BN;
+        if (p.debug & 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (leader)
+              mbar_arrive(&tempty[buf]);
+            else
+              mbar_arrive_cluster(tempty_leader0 + buf * 8);
+          }
+          continue;
+        }
         if (p.mode == OUT_LEAVES) {
-          float* dst = p.out + static_cast<size_t>(t) * p.unit_stride + static_cast<size_t>(grow) * p.ldo + it.n0;
+          float* dst =
+              p.out + static_cast<size_t>(t) * p.unit_stride + static_cast<size_t>(grow) * p.ldo + it.n0 + col0;
 #pragma unroll
-          for (int c = 0; c < BN / 32; ++c) {
+          for (int c = 0; c < NCH; ++c) {
             float v[32];
             tmem_ld32(acc + c * 32, v);
             tmem_wait_ld();
@@ -305,16 +369,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < BN / 32; ++c) {
-            float v[32];
-            tmem_ld32(acc + c * 32, v);
-            tmem_wait_ld();
-            if (t_in_group == 0) {
+          for (int c0 = 0; c0 < NCH; c0 += LB) {
+            uint32_t r[LB][32];
 #pragma unroll
-              for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(0.0f, v[i]);
-            } else {
+            for (int j = 0; j < LB; ++j) tmem_ld32r(acc + (c0 + j) * 32, r[j]);
+            #pragma unroll
+            for (int j = 0; j < LB; ++j) tmem_wait_ld_dep(r[j]);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], v[i]);
+            for (int j = 0; j < LB; ++j) {
+              if (t_in_group == 0) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) g[(c0 + j) * 32 + i] = __fadd_rn(0.0f, __uint_as_float(r[j][i]));
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  g[(c0 + j) * 32 + i] = __fadd_rn(g[(c0 + j) * 32 + i], __uint_as_float(r[j][i]));
+              }
             }
           }
         }
@@ -331,6 +401,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (p.mode == OUT_LEAVES) continue;
         if (++t_in_group < p.kf) continue;
         t_in_group = 0;
+        if (p.debug & 4) continue;
 
         // Binary counter over completed groups (levels 1..p.levels).
         int level = 1;
@@ -339,17 +410,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (level <= 2) {
             const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
 #pragma unroll
-            for (int c = 0; c < BN / 32; ++c) {
-              float v[32];
-              tmem_ld32(slot + c * 32, v);
-              tmem_wait_ld();
+            for (int c0 = 0; c0 < NCH; c0 += LB) {
+              uint32_t r[LB][32];
 #pragma unroll
-              for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], v[i]);
+              for (int j = 0; j < LB; ++j) tmem_ld32r(slot + (c0 + j) * 32, r[j]);
+              #pragma unroll
+            for (int j = 0; j < LB; ++j) tmem_wait_ld_dep(r[j]);
+#pragma unroll
+              for (int j = 0; j < LB; ++j)
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  g[(c0 + j) * 32 + i] = __fadd_rn(g[(c0 + j) * 32 + i], __uint_as_float(r[j][i]));
             }
           } else {
-            const float* s = scratch_base + static_cast<size_t>(level - 3) * (BM * BN) + row_in_tile;
+            const float* s = scratch_base + static_cast<size_t>(level - 3) * (BM * BN);
+            if (!(p.debug & 8))
 #pragma unroll
-            for (int i = 0; i < BN; ++i) g[i] = __fadd_rn(g[i], s[i * BM]);
+            for (int i = 0; i < COLS; i += 4) {
+              const float4 x = *reinterpret_cast<const float4*>(s + i * BM);
+              g[i] = __fadd_rn(g[i], x.x);
+              g[i + 1] = __fadd_rn(g[i + 1], x.y);
+              g[i + 2] = __fadd_rn(g[i + 2], x.z);
+              g[i + 3] = __fadd_rn(g[i + 3], x.w);
+            }
           }
           c_bits >>= 1;
           ++level;
@@ -358,7 +441,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (level <= 2) {
             const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
 #pragma unroll
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = 0; c < NCH; ++c) {
               float v[32];
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = g[c * 32 + i];
@@ -366,28 +449,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             }
             tmem_wait_st();
           } else {
-            float* s = scratch_base + static_cast<size_t>(level - 3) * (BM * BN) + row_in_tile;
+            float* s = scratch_base + static_cast<size_t>(level - 3) * (BM * BN);
+            if (!(p.debug & 8))
 #pragma unroll
-            for (int i = 0; i < BN; ++i) s[i * BM] = g[i];
+            for (int i = 0; i < COLS; i += 4)
+              *reinterpret_cast<float4*>(s + i * BM) = make_float4(g[i], g[i + 1], g[i + 2], g[i + 3]);
           }
           continue;
         }
         // The carry left the top level: g is this unit's complete (sub)tree.
-        if (row_ok) {
-          float* dst = p.out + static_cast<size_t>(p.mode == OUT_UNITS ? it.unit : 0) * p.unit_stride +
-                       static_cast<size_t>(grow) * p.ldo + it.n0;
-          if (ncols == BN && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        if (p.debug & 2) continue;
+        if (p.tma_store) {
+          // Row-per-lane registers -> 128B-swizzled 32 x 32 smem box (conflict-free
+          // 16 B stores) -> one TMA store per box; the tensor map clips ragged edges.
 #pragma unroll
-            for (int i = 0; i < BN; i += 4)
+          for (int c = 0; c < NCH; ++c) {
+            if (lane == 0) bulk_wait_read<XB - 1>();
+            __syncwarp();
+            uint8_t* buf = sC + ((warp - 4) * XB + xb) * OUT_BUF_BYTES;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                  make_float4(g[c * 32 + 4 * j], g[c * 32 + 4 * j + 1], g[c * 32 + 4 * j + 2], g[c * 32 + 4 * j + 3]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&tmC, smem_u32(buf), it.n0 + col0 + c * 32, grow - lane,
+                           p.mode == OUT_UNITS ? it.unit : 0);
+              bulk_commit();
+            }
+            if constexpr (XB == 2) xb ^= 1;
+          }
+        } else if (row_ok) {
+          float* dst = p.out + static_cast<size_t>(p.mode == OUT_UNITS ? it.unit : 0) * p.unit_stride +
+                       static_cast<size_t>(grow) * p.ldo + it.n0 + col0;
+          if (ncols == COLS && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+            for (int i = 0; i < COLS; i += 4)
               *reinterpret_cast<float4*>(dst + i) = make_float4(g[i], g[i + 1], g[i + 2], g[i + 3]);
           } else {
 #pragma unroll
-            for (int i = 0; i < BN; ++i)
+            for (int i = 0; i < COLS; ++i)
               if (i < ncols) dst[i] = g[i];
           }
         }
       }
     }
+    if (p.tma_store && lane == 0) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -429,6 +537,23 @@ tbik_status make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(TBIK_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return TBIK_OK;
+}
+
+// f32 output [units][M][N] (row stride, unit stride in bytes), 32 x 32 boxes,
+// 128B swizzle (matches the merge warps' staging layout).
+tbik_status make_map_out(CUtensorMap* map, float* base, uint64_t n, uint64_t m, uint64_t units,
+                         uint64_t row_stride_bytes, uint64_t unit_stride_bytes) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return set_error(TBIK_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {n, m, units};
+  cuuint64_t strides[2] = {row_stride_bytes, unit_stride_bytes};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(TBIK_CUDA_ERROR, "cuTensorMapEncodeTiled(out) failed: " + std::to_string(r));
   return TBIK_OK;
 }
 
@@ -510,6 +635,11 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
     p.units = static_cast<int>((v.T + p.tiles_per_unit - 1) / p.tiles_per_unit);
     if (o.mode == OUT_FULL && p.units != 1) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: FULL needs 1 unit");
   }
+  static const int dbg = [] {
+    const char* e = std::getenv("TBIK_TC_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.debug = dbg;
   p.mblocks = static_cast<int>((v.M + PAIR_M - 1) / PAIR_M);
   p.ntiles = static_cast<int>((v.N + BN - 1) / BN);
   p.items = static_cast<long long>(p.mblocks) * p.ntiles * p.units;
@@ -521,15 +651,34 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
     p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1));
     if (!p.scratch) return set_error(TBIK_CUDA_ERROR, "tc gemm: scratch allocation failed");
   }
-  static bool attr_set[16] = {false};
+  static const int variant = [] {
+    // 8 merge warps (two per TMEM lane quarter, 64 columns each) is the default;
+    // TBIK_TC_EPI=4 selects the 4-warp variant (same bits).
+    const char* e = std::getenv("TBIK_TC_EPI");
+    return e && std::atoi(e) == 4 ? 0 : 1;
+  }();
+  // Results leave through a TMA store when the output is 16-byte addressable.
+  CUtensorMap mC;
+  std::memset(&mC, 0, sizeof(mC));
+  const uint64_t ustride = o.mode == OUT_UNITS ? static_cast<uint64_t>(o.unit_stride)
+                                               : static_cast<uint64_t>(o.ldo) * static_cast<uint64_t>(v.M);
+  p.tma_store = o.mode != OUT_LEAVES && !(dbg & 16) && (reinterpret_cast<uintptr_t>(o.out) & 15) == 0 &&
+                o.ldo % 4 == 0 && ustride % 4 == 0;
+  if (p.tma_store)
+    TBIK_TRY(make_map_out(&mC, o.out, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.M),
+                          static_cast<uint64_t>(p.units), static_cast<uint64_t>(o.ldo) * 4, ustride * 4));
+  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams) =
+      variant == 0 ? tc_tree_gemm_kernel<4, 1, STAGES> : tc_tree_gemm_kernel<8, 1, STAGES>;
+  const int nthreads = variant ? 128 + 32 * 8 : 128 + 32 * 4;
+  const size_t smem = variant ? smem_bytes(8, STAGES) : smem_bytes(4, STAGES);
+  static bool attr_set[16][2] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 16 && !attr_set[dev]) {
-    TBIK_CUDA(cudaFuncSetAttribute(tc_tree_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(SMEM_BYTES)));
-    attr_set[dev] = true;
+  if (dev >= 0 && dev < 16 && !attr_set[dev][variant]) {
+    TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr_set[dev][variant] = true;
   }
-  tc_tree_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mA, mB, p);
+  kern<<<grid, nthreads, smem, s>>>(mA, mB, mC, p);
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;
