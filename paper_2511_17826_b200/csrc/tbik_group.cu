@@ -1,24 +1,36 @@
 // tbik_group.cu -- DeviceGroup (collective.hpp:15-23) with one process per
 // GPU: the fixed-order tree all-reduce over NVLink peer memory.
 //
-// Each rank allocates one device region { send buffers [2][capacity] f32,
-// flags [W] u32 } and exports it with CUDA IPC; every rank maps every peer's
-// region.  A collective with epoch e (host counter, starts at 1):
-//   1. the rank's partial is in its send buffer slot (e & 1) (the row-parallel
-//      GEMM writes it there directly; otherwise one D2D copy);
-//   2. the kernel's first CTA publishes "epoch e ready" into flags[rank] of
-//      EVERY peer (st.release.sys after __threadfence_system), then every CTA
-//      waits until its own flags[0..W) all reach e (ld.acquire.sys);
-//   3. every rank reduces all W slots (e & 1) in Algorithm-2 order
-//      (collective.cpp:67-74) straight from peer memory into its output.
-// Double buffering + the per-collective barrier make slot reuse safe: a peer
-// that publishes epoch e+1 has finished reading epoch e's slot.
-// The sum order is per element and fixed, so all ranks produce identical
-// bits -- the rank-symmetry the reference asserts (collective.cpp:79-85).
+// Each rank allocates one device region
+//   { send [2][capacity] f32, result [2][capacity] f32, control block }
+// and exports it with CUDA IPC; every rank maps every peer's region.  A
+// collective with epoch e (host counter, starts at 1):
+//   1. the rank's partial is in its send slot (e & 1) (the row-parallel GEMM
+//      writes it there directly; otherwise one D2D copy);
+//   2. barrier A: the kernel publishes "epoch e ready" into ready[rank] of EVERY
+//      peer (st.release.sys after __threadfence_system), then waits until its
+//      own ready[0..W) all reach e (ld.acquire.sys);
+//   3a. small payloads (one-shot): every rank reduces all W slots in
+//      Algorithm-2 order (collective.cpp:67-74) straight from peer memory into
+//      its output -- one kernel, one barrier, W-1 remote reads per element;
+//   3b. large payloads (reduce-scatter + push all-gather): rank r reduces only
+//      element slice r (W-1 remote reads per element of the slice) and STORES
+//      the reduced slice into the result slot (e & 1) of every rank over
+//      NVLink; the last CTA to finish publishes done[rank] = e to every peer
+//      (barrier B), and a second kernel waits for all W done flags and copies
+//      the local result slot into the caller's output.  Per rank this moves
+//      (W-1)/W of the payload in each NVLink direction instead of (W-1)x in.
+// The per-element order is the same in 3a and 3b (Algorithm 2 over ranks
+// 0..W-1), so every rank, every path and every schedule give identical bits:
+// the rank symmetry the reference asserts (collective.cpp:79-85).
+// Slot reuse is safe: a peer reaches epoch e+2 (same parity) only after
+// barrier A of e+1, which every rank enters only after finishing epoch e.
 // NCCL / NVLS in-switch reduction are never used for the sum (order not
 // controllable); NCCL appears only in bench.py's labelled baseline.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -51,15 +63,29 @@ struct HandleBlob {
 };
 static_assert(sizeof(HandleBlob) == TBIK_IPC_HANDLE_BYTES, "handle blob size");
 
-size_t flags_offset(int64_t capacity) { return static_cast<size_t>(2 * capacity) * sizeof(float); }
+// Control block after the four slots: ready[64] u32, done[64] u32, counter u32.
+constexpr size_t kCtlBytes = 1024;
+size_t flags_offset(int64_t capacity) { return static_cast<size_t>(4 * capacity) * sizeof(float); }
+uint32_t* ready_flags(char* region, int64_t capacity) {
+  return reinterpret_cast<uint32_t*>(region + flags_offset(capacity));
+}
+uint32_t* done_flags(char* region, int64_t capacity) { return ready_flags(region, capacity) + 64; }
+uint32_t* cta_counter(char* region, int64_t capacity) { return ready_flags(region, capacity) + 128; }
+float* result_ptr(char* region, int64_t capacity, uint32_t epoch) {
+  return reinterpret_cast<float*>(region) + static_cast<size_t>(2 + (epoch & 1u)) * capacity;
+}
+// Payloads at or above this many bytes take the reduce-scatter + push path.
+constexpr int64_t kTwoPhaseBytes = int64_t(1) << 20;
 
 float* slot_ptr(char* region, int64_t capacity, uint32_t epoch) {
   return reinterpret_cast<float*>(region) + static_cast<size_t>(epoch & 1u) * capacity;
 }
 
 struct GroupPtrs {
-  const float* src[kMaxRanks];
-  uint32_t* flags[kMaxRanks];  // flags array of every rank (peer-mapped)
+  const float* src[8];   // send slot (e & 1) of every rank (peer-mapped)
+  float* dst[8];         // result slot (e & 1) of every rank (peer-mapped)
+  uint32_t* flags[8];    // ready[] array of every rank (peer-mapped)
+  uint32_t* done[8];     // done[] array of every rank (peer-mapped)
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -71,8 +97,8 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
-__global__ void group_allreduce_kernel(GroupPtrs g, int W, int rank, uint32_t epoch, int64_t elems,
-                                       float* __restrict__ out) {
+// Barrier A: publish "epoch ready" to every peer (block 0), wait for all W.
+__device__ __forceinline__ void barrier_ready(const GroupPtrs& g, int W, int rank, uint32_t epoch) {
   if (blockIdx.x == 0 && threadIdx.x < W) {
     __threadfence_system();
     st_release_sys(g.flags[threadIdx.x] + rank, epoch);
@@ -84,40 +110,99 @@ __global__ void group_allreduce_kernel(GroupPtrs g, int W, int rank, uint32_t ep
       }
   }
   __syncthreads();
+}
+
+// Algorithm 2 (collective.cpp:67-74) over the W rank values of one float4:
+// for l = 1..log2 W, R[left] += R[left + 2^(l-1)] at every left step 2^l.
+__device__ __forceinline__ float4 tree4(const GroupPtrs& g, int W, int64_t i) {
+  float4 r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (k < W) r[k] = reinterpret_cast<const float4*>(g.src[k])[i];
+#pragma unroll
+  for (int l = 1; l <= 3; ++l) {
+    const int st = 1 << l, h = 1 << (l - 1);
+#pragma unroll
+    for (int left = 0; left < 8; left += st)
+      if (left + h < W) {
+        r[left].x = __fadd_rn(r[left].x, r[left + h].x);
+        r[left].y = __fadd_rn(r[left].y, r[left + h].y);
+        r[left].z = __fadd_rn(r[left].z, r[left + h].z);
+        r[left].w = __fadd_rn(r[left].w, r[left + h].w);
+      }
+  }
+  return r[0];
+}
+
+__device__ __forceinline__ float tree1(const GroupPtrs& g, int W, int64_t e) {
+  float r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (k < W) r[k] = g.src[k][e];
+#pragma unroll
+  for (int l = 1; l <= 3; ++l) {
+    const int st = 1 << l, h = 1 << (l - 1);
+#pragma unroll
+    for (int left = 0; left < 8; left += st)
+      if (left + h < W) r[left] = __fadd_rn(r[left], r[left + h]);
+  }
+  return r[0];
+}
+
+// 3a: one-shot -- every rank reduces every element.
+__global__ void group_allreduce_kernel(GroupPtrs g, int W, int rank, uint32_t epoch, int64_t elems,
+                                       float* __restrict__ out) {
+  barrier_ready(g, W, rank, epoch);
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t n4 = elems / 4;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
-    float4 r[kMaxRanks <= 8 ? 8 : 8];
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride)
+    reinterpret_cast<float4*>(out)[i] = tree4(g, W, i);
+  for (int64_t e = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < elems; e += stride)
+    out[e] = tree1(g, W, e);
+}
+
+// 3b, phase 1: reduce slice `rank` (float4 units [lo, hi)) and push it into
+// every rank's result slot; the last CTA publishes done[rank] = epoch to all.
+__global__ void group_reduce_scatter_push_kernel(GroupPtrs g, int W, int rank, uint32_t epoch, int64_t lo,
+                                                 int64_t hi, uint32_t* __restrict__ counter) {
+  barrier_ready(g, W, rank, epoch);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = lo + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < hi; i += stride) {
+    const float4 v = tree4(g, W, i);
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      if (k < W) r[k] = reinterpret_cast<const float4*>(g.src[k])[i];
-#pragma unroll
-    for (int l = 1; l <= 3; ++l) {
-      const int st = 1 << l, h = 1 << (l - 1);
-#pragma unroll
-      for (int left = 0; left < 8; left += st)
-        if (left + h < W) {
-          r[left].x = __fadd_rn(r[left].x, r[left + h].x);
-          r[left].y = __fadd_rn(r[left].y, r[left + h].y);
-          r[left].z = __fadd_rn(r[left].z, r[left + h].z);
-          r[left].w = __fadd_rn(r[left].w, r[left + h].w);
-        }
-    }
-    reinterpret_cast<float4*>(out)[i] = r[0];
+      if (k < W) reinterpret_cast<float4*>(g.dst[(rank + k) & (W - 1)])[i] = v;  // stagger the peers
   }
-  for (int64_t e = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < elems; e += stride) {
-    float r[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (k < W) r[k] = g.src[k][e];
-#pragma unroll
-    for (int l = 1; l <= 3; ++l) {
-      const int st = 1 << l, h = 1 << (l - 1);
-#pragma unroll
-      for (int left = 0; left < 8; left += st)
-        if (left + h < W) r[left] = __fadd_rn(r[left], r[left + h]);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(counter, 1u);
+    if (prev == gridDim.x - 1) {
+      *counter = 0;  // the next epoch's kernel starts after this one (stream order)
+      __threadfence_system();
+      for (int r = 0; r < W; ++r) st_release_sys(g.done[r] + rank, epoch);
     }
-    out[e] = r[0];
+  }
+}
+
+// 3b, phase 2: wait until every rank has pushed its slice, then copy the local
+// result slot into the caller's output.
+__global__ void group_gather_wait_copy_kernel(const uint32_t* done, int W, uint32_t epoch,
+                                              const float* __restrict__ result, float* __restrict__ out,
+                                              int64_t elems) {
+  if (threadIdx.x == 0)
+    for (int r = 0; r < W; ++r)
+      while (static_cast<int32_t>(ld_acquire_sys(done + r) - epoch) < 0) {
+      }
+  __syncthreads();
+  if (result == out) return;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if ((reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    for (int64_t i = t0; i < elems / 4; i += stride)
+      reinterpret_cast<float4*>(out)[i] = reinterpret_cast<const float4*>(result)[i];
+  } else {
+    for (int64_t i = t0; i < elems; i += stride) out[i] = result[i];
   }
 }
 
@@ -142,13 +227,13 @@ tbik_status tbik_group_create(int world_size, int rank, int device, int64_t capa
   g->rank = rank;
   g->device = device;
   g->capacity = capacity_elems;
-  g->region_bytes = flags_offset(capacity_elems) + 256;
+  g->region_bytes = flags_offset(capacity_elems) + kCtlBytes;
   cudaError_t e = cudaMalloc(&g->region, g->region_bytes);
   if (e != cudaSuccess) {
     delete g;
     return cuda_status(e, "cudaMalloc(group region)");
   }
-  e = cudaMemset(g->region + flags_offset(capacity_elems), 0, 256);
+  e = cudaMemset(g->region + flags_offset(capacity_elems), 0, kCtlBytes);
   if (e != cudaSuccess) {
     cudaFree(g->region);
     delete g;
@@ -220,7 +305,30 @@ tbik_status tbik_group_tree_all_reduce(tbik_group* g, const float* partial, floa
   GroupPtrs gp{};
   for (int r = 0; r < g->W; ++r) {
     gp.src[r] = slot_ptr(g->peer_region[r], g->capacity, epoch);
-    gp.flags[r] = reinterpret_cast<uint32_t*>(g->peer_region[r] + flags_offset(g->capacity));
+    gp.dst[r] = result_ptr(g->peer_region[r], g->capacity, epoch);
+    gp.flags[r] = ready_flags(g->peer_region[r], g->capacity);
+    gp.done[r] = done_flags(g->peer_region[r], g->capacity);
+  }
+  static const int64_t two_phase_bytes = [] {
+    const char* e = std::getenv("TBIK_AR_TWO_PHASE_BYTES");  // schedule knob only: same bits either way
+    return e && *e ? std::atoll(e) : kTwoPhaseBytes;
+  }();
+  // The path must be the same on every rank: it depends only on (W, elems).
+  if (g->W > 1 && elems % 4 == 0 && elems * 4 >= two_phase_bytes) {
+    const int64_t n4 = elems / 4;
+    const int64_t lo = n4 * g->rank / g->W, hi = n4 * (g->rank + 1) / g->W;
+    int64_t blocks = (hi - lo + 255) / 256;
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 2));
+    group_reduce_scatter_push_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+        gp, g->W, g->rank, epoch, lo, hi, cta_counter(g->region, g->capacity));
+    TBIK_CUDA(cudaGetLastError());
+    count_launch();
+    int64_t cblocks = std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 4));
+    group_gather_wait_copy_kernel<<<static_cast<unsigned>(cblocks), 256, 0, s>>>(
+        done_flags(g->region, g->capacity), g->W, epoch, result_ptr(g->region, g->capacity, epoch), out, elems);
+    TBIK_CUDA(cudaGetLastError());
+    count_launch();
+    return TBIK_OK;
   }
   int64_t blocks = (elems / 4 + 255) / 256;
   if (blocks > 148 * 4) blocks = 148 * 4;

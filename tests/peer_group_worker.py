@@ -28,7 +28,8 @@ def main():
     cfg = tb.BlockConfig(64, 256, 128, 0)
     kb, ke = tb.make_row_shard_plan(K, cfg, world, 8).bounds[rank]
     xs, ws = x[:, kb:ke].contiguous(), w[kb:ke].contiguous()
-    grp = tb.PeerGroup(world, rank, torch.cuda.current_device(), M * N, dist)
+    E_big = (1 << 20) + 4  # > 1 MiB of f32: the reduce-scatter + push path
+    grp = tb.PeerGroup(world, rank, torch.cuda.current_device(), max(M * N, E_big), dist)
     ys = []
     for it in range(5):  # several epochs: exercises both send-buffer slots
         for leaf in (tb.LEAF_TCGEN05, tb.LEAF_FMA):
@@ -42,6 +43,21 @@ def main():
     local = tb.tree_all_reduce(tb.DeviceGroup(world), parts)
     torch.cuda.synchronize()
     assert torch.equal(red.view(torch.int32), local.view(torch.int32))
+    # large payloads take the two-phase path; interleave with one-shot epochs and an
+    # unaligned output view -- every result must equal the local Algorithm-2 result
+    gb = torch.Generator(device="cuda")
+    gb.manual_seed(99)
+    big = [torch.randn(E_big, device="cuda", generator=gb) * (1e6 if r % 2 else 1.0) for r in range(world)]
+    local_big = tb.tree_all_reduce(tb.DeviceGroup(world), big)
+    for it in range(4):
+        red_big = grp.tree_all_reduce(big[rank])
+        small = grp.tree_all_reduce(parts[rank])
+        buf = torch.empty(E_big + 1, device="cuda")
+        odd = grp.tree_all_reduce(big[rank], out=buf[1:])
+        torch.cuda.synchronize()
+        assert torch.equal(red_big.view(torch.int32), local_big.view(torch.int32)), f"two-phase differs ({it})"
+        assert torch.equal(odd.view(torch.int32), local_big.view(torch.int32)), f"unaligned out differs ({it})"
+        assert torch.equal(small.view(torch.int32), local.view(torch.int32)), f"one-shot differs ({it})"
     out = os.environ["TBIK_TEST_OUT"]
     np.save(out, ys[0].cpu().numpy())
     if rank == 0:
