@@ -303,27 +303,30 @@ def run_tbik(args):
                  "peak_source": peak_src, "share_of_step": k_ms / ms if ms else None})
 
     # ---- e2e through the C ABI with host buffers ----------------------------------------
+    # tbik_tree_matmul_hostio / tbik_group_row_parallel_forward_hostio: pinned host x in,
+    # pinned host y out; the H2D of row chunk i+1, the GEMM (+ tree all-reduce) of chunk i
+    # and the D2H of chunk i-1 overlap (bit-identical to the device call: batch invariance).
     x_host = x.cpu().pin_memory()
     y_host = torch.empty(M, N_OUT, dtype=torch.float32).pin_memory()
-    x_dev = torch.empty_like(x)
 
     def e2e_step():
-        x_dev.copy_(x_host, non_blocking=True)
         if group is not None:
-            group.row_parallel_forward(x_dev, w, K_FULL, cfg, 8, leaf, out=y)
+            group.row_parallel_forward_hostio(x_host, w, K_FULL, cfg, 8, leaf, out=y_host)
         else:
-            tb.tree_matmul(x_dev, w, cfg, leaf, out=y)
-        y_host.copy_(y, non_blocking=True)
+            tb.tree_matmul_hostio(x_host, w, cfg, leaf, out=y_host)
 
     for _ in range(2):
         e2e_step()
+    torch.cuda.synchronize()
+    e2e_same = bool(torch.equal(y_host.view(torch.int32), y.cpu().view(torch.int32)))
     barrier()
     e2e_ms = max_over_ranks(ev_time(e2e_step, max(args.steps // 2, 3)))
     e2e = {"value": flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
            "h2d_bytes_per_step": x_host.numel() * x_host.element_size(),
            "d2h_bytes_per_step": y_host.numel() * y_host.element_size(),
-           "ms_per_step": e2e_ms,
-           "path": "pinned host x -> H2D -> tbik_tree_matmul / tbik_group_row_parallel_forward (C ABI) -> D2H y"}
+           "ms_per_step": e2e_ms, "bit_identical_to_device_call": e2e_same,
+           "path": "pinned host x -> tbik_tree_matmul_hostio / tbik_group_row_parallel_forward_hostio (C ABI: "
+                   "row-chunked H2D | GEMM + tree all-reduce | D2H on three streams) -> pinned host y"}
 
     # ---- non-invariant status quo: cuBLAS bf16 (+ NCCL all-reduce) ---------------------------
     yb = torch.empty(M, N_OUT, device=dev, dtype=torch.bfloat16)
@@ -378,10 +381,16 @@ def run_tbik(args):
     # ---- the metric's second half: bit-exact logits across TP on the Llama forward ----
     forward = None
     if rank == 0 and world == 1 and not args.no_forward:
-        del w, x, x_full, y, yb, x_host, y_host, x_dev
+        del w, x, x_full, y, yb, x_host, y_host
         torch.cuda.empty_cache()
         from tools.forward_bench import run as forward_run
         forward = forward_run("llama3.1-8b", 32, 4, 256, reps=3, tps=(1, 2, 4, 8))
+
+    rowops = None
+    if rank == 0 and world == 1 and not args.no_forward:
+        torch.cuda.empty_cache()
+        from tools.rowops_bench import run as rowops_run
+        rowops = rowops_run(reps=10, tps=(1, 8))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -406,6 +415,7 @@ def run_tbik(args):
             "noninvariant": noninv, "tp_invariance_bit_identical": tp_ok, "sweep": sweep,
             "cpu_baseline": cpu,
             "forward": forward,
+            "rowops_c5": rowops,
         }
         print(json.dumps(line))
     if group is not None:

@@ -188,6 +188,9 @@ TBIK_API tbik_status tbik_group_create(int world_size, int rank, int device, int
 TBIK_API tbik_status tbik_group_ipc_handle(tbik_group* g, void* handle_out /* TBIK_IPC_HANDLE_BYTES */);
 TBIK_API tbik_status tbik_group_open_peers(tbik_group* g, const void* handles /* W * HANDLE_BYTES */);
 TBIK_API tbik_status tbik_group_destroy(tbik_group* g);
+/* World size / rank of the group (0 / -1 for a null handle). */
+TBIK_API int tbik_group_world_size(const tbik_group* g);
+TBIK_API int tbik_group_rank(const tbik_group* g);
 /* This rank's exchange buffer for the next collective (device pointer). */
 TBIK_API float* tbik_group_send_buffer(tbik_group* g);
 
@@ -206,6 +209,32 @@ TBIK_API tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* 
                                             int64_t N, int64_t K_global,
                                             const tbik_block_config* cfg, int64_t c_max,
                                             int leaf_mode, void* stream);
+
+/* ---- host-buffer entry points (the reference's Matrix in / Matrix out) ---- */
+
+/* tree_matmul (matmul.hpp:53) with HOST activations A_host [M x K] and a HOST
+ * f32 result C_host [M x N]; the weights B stay in device memory.  Rows are
+ * streamed in chunks of `chunk_rows` (0 = default): the H2D copy of chunk i+1,
+ * the GEMM of chunk i and the D2H copy of chunk i-1 overlap on three streams.
+ * Bit-identical to tbik_tree_matmul on device buffers (batch invariance).
+ * Returns once enqueued; `stream` is ordered after the last D2H copy
+ * (tbik_sync(stream) waits).  Page-locked host buffers give full overlap. */
+TBIK_API tbik_status tbik_tree_matmul_hostio(const void* A_host, int a_dtype, int64_t lda, const void* B,
+                                    int b_dtype, int64_t ldb, float* C_host, int64_t ldc, int64_t M,
+                                    int64_t N, int64_t K, const tbik_block_config* cfg, int leaf_mode,
+                                    int64_t chunk_rows, void* stream);
+
+/* tbik_group_row_parallel_forward with this rank's HOST X shard [M x K_shard]
+ * (K_shard = its make_row_shard_plan range) and a HOST Y [M x N], same
+ * pipeline; one collective epoch per row chunk (every rank must pass the same
+ * M and chunk_rows). */
+TBIK_API tbik_status tbik_group_row_parallel_forward_hostio(tbik_group* g, const void* X_host_shard,
+                                                   int x_dtype, int64_t ldx, const void* W_shard,
+                                                   int w_dtype, int64_t ldw, float* Y_host,
+                                                   int64_t ldy, int64_t M, int64_t N, int64_t K_shard,
+                                                   int64_t K_global, const tbik_block_config* cfg,
+                                                   int64_t c_max, int leaf_mode, int64_t chunk_rows,
+                                                   void* stream);
 
 /* ---- tree-ordered reductions (NEW semantics) -------- */
 

@@ -147,6 +147,28 @@ def tree_matmul(a, b, cfg: BlockConfig | None = None, leaf: int = LEAF_TCGEN05, 
     return out
 
 
+def tree_matmul_hostio(a_host, b, cfg: BlockConfig | None = None, leaf: int = LEAF_TCGEN05, out=None,
+                       chunk_rows: int = 0):
+    """tree_matmul with HOST activations and a HOST f32 result (weights `b` on the
+    device): H2D, GEMM and D2H overlap over row chunks (tbik_tree_matmul_hostio).
+    Asynchronous on the current stream like every other entry point."""
+    torch = _torch()
+    cfg = cfg or default_block_config(_dt(a_host))
+    M, K = a_host.shape
+    N = b.shape[1]
+    if a_host.is_cuda or not b.is_cuda:
+        raise TbikError(ErrorCode.BadArgument, "tree_matmul_hostio: A must be a host tensor, B a device tensor")
+    if a_host.stride(1) != 1 or b.stride(1) != 1:
+        raise TbikError(ErrorCode.BadArgument, "tree_matmul_hostio: row-major operands required")
+    out = torch.empty((M, N), dtype=torch.float32, pin_memory=True) if out is None else out
+    if out.is_cuda or out.dtype != torch.float32 or out.stride(1) != 1:
+        raise TbikError(ErrorCode.BadArgument, "tree_matmul_hostio: out must be a host f32 row-major tensor")
+    check(lib.tbik_tree_matmul_hostio(C.c_void_p(a_host.data_ptr()), _dt(a_host), a_host.stride(0),
+                                      C.c_void_p(b.data_ptr()), _dt(b), b.stride(0), C.c_void_p(out.data_ptr()),
+                                      out.stride(0), M, N, K, C.byref(cfg.c()), leaf, chunk_rows, _stream()))
+    return out
+
+
 def tree_matmul_leaves(a, b, cfg: BlockConfig | None = None, leaf: int = LEAF_TCGEN05):
     """Every leaf partial product P_t as leaves[t] (M x N f32) -- verification entry."""
     cfg = cfg or default_block_config(BF16)
@@ -356,6 +378,25 @@ class PeerGroup:
                                                   C.c_void_p(out.data_ptr()), N, M, N, K_global,
                                                   C.byref(cfg.c()), c_max, leaf, _stream()))
         return out
+
+
+def _group_row_parallel_hostio(self, x_host_shard, w_shard, K_global: int, cfg: BlockConfig | None = None,
+                               c_max: int = 8, leaf: int = LEAF_TCGEN05, out=None, chunk_rows: int = 0):
+    """PeerGroup.row_parallel_forward with this rank's HOST X shard and a HOST f32
+    result (tbik_group_row_parallel_forward_hostio)."""
+    torch = _torch()
+    cfg = cfg or default_block_config(BF16)
+    M, Kr = x_host_shard.shape
+    N = w_shard.shape[1]
+    out = torch.empty((M, N), dtype=torch.float32, pin_memory=True) if out is None else out
+    check(lib.tbik_group_row_parallel_forward_hostio(
+        self._h, C.c_void_p(x_host_shard.data_ptr()), _dt(x_host_shard), x_host_shard.stride(0),
+        C.c_void_p(w_shard.data_ptr()), _dt(w_shard), w_shard.stride(0), C.c_void_p(out.data_ptr()), out.stride(0),
+        M, N, Kr, K_global, C.byref(cfg.c()), c_max, leaf, chunk_rows, _stream()))
+    return out
+
+
+PeerGroup.row_parallel_forward_hostio = _group_row_parallel_hostio
 
 
 def exchange_handles(mine: bytes, world_size: int, dist=None) -> list:

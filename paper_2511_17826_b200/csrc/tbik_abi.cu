@@ -49,12 +49,12 @@ struct Arena {
   size_t bytes = 0;
 };
 std::mutex g_ws_mu;
-Arena g_ws[16][4];
+Arena g_ws[16][8];
 }  // namespace
 
 void* workspace(size_t bytes, int slot) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16 || slot < 0 || slot >= 4) return nullptr;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16 || slot < 0 || slot >= 8) return nullptr;
   std::lock_guard<std::mutex> lk(g_ws_mu);
   Arena& a = g_ws[dev][slot];
   if (a.bytes >= bytes && a.ptr) return a.ptr;

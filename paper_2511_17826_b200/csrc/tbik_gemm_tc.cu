@@ -19,8 +19,9 @@
 //   warp 2      TMEM allocator (512 columns, cta_group::2)
 //   warps 4-11  merge warps: warp w may read TMEM lanes 32(w%4)..; thread (w, lane)
 //               owns output row 32(w%4) + lane, columns 64((w-4)/4) + [0, 64).
-//               For every leaf: tcgen05.ld + __fadd_rn, verbatim the reference's
-//               reduction:
+//               For every leaf: both tcgen05.ld chunks in flight (with the
+//               level-1 slot when k_first == 1), one wait, the accumulator is
+//               released, then __fadd_rn verbatim the reference's reduction:
 //                 level 0   g = ((0 + P_0) + P_1) + ... + P_{kf-1}   (matmul.cpp:100-125)
 //                 levels>=1 binary counter over group values (matmul.cpp:107-123)
 //               g in 64 registers; tree levels 1-2 in TMEM cols [256,512);
@@ -190,10 +191,11 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// EPI merge warps (4 or 8; with 8, two warps share each TMEM lane quarter and
-// split the 128 columns), LB = 32-column TMEM loads in flight per wait, NST
-// pipeline stages.
-template <int EPI, int LB, int NST>
+// EPI merge warps (two per TMEM lane quarter, splitting the 128 columns), NST
+// pipeline stages.  KF1 (used when k_first == 1, where every leaf completes a
+// group and g need not persist across leaves): the level-1 slot is loaded in the
+// same batch as the leaf, so an odd leaf costs one TMEM round trip, not two.
+template <int EPI, bool KF1, int NST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
     tc_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const TcParams p) {
@@ -310,24 +312,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
   }
   } else {
     // ---------------- merge warps (the TBIK reduction), both CTAs ----------------
-    constexpr int COLS = BN * 4 / EPI;  // columns owned by this warp
+    constexpr int COLS = BN * 4 / EPI;  // columns owned by this thread (64)
     constexpr int NCH = COLS / 32;
-    static_assert(NCH % LB == 0, "LB must divide the chunk count");
     const int q = warp & 3;  // a warp may only touch TMEM lanes 32*(warp%4)..
     const int col0 = ((warp - 4) >> 2) * COLS;
     const int row_in_tile = q * 32 + lane;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + col0;
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
-    // Scratch levels (>= 3) are [col/4][row][4] slabs: a warp's float4 access is
-    // 512 contiguous bytes.
+    // TMEM holds tree levels 1-2; levels >= 3 live in scratch as [col/4][row][4]
+    // slabs (a warp's float4 access is 512 contiguous bytes).
     float* scratch_base =
         p.levels > 2
             ? p.scratch + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - 2) * (BM * BN) +
                            static_cast<size_t>(col0) * BM + static_cast<size_t>(row_in_tile) * 4
-                     : nullptr;
+            : nullptr;
 
-    float g[COLS];
-    int xb = 0;  // output staging buffer toggle
+    float g[COLS];  // level 0: the running leaf-group value
+    int xb = 0;      // output staging buffer toggle
     uint32_t acc_iter = 0;
     for (long long item = pair; item < p.items; item += npairs) {
       const Item it = decode(p, item);
@@ -342,53 +343,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
         mbar_wait(&tfull[buf], use & 1);
         tc_fence_after();
         const uint32_t acc = lane_base + buf * BN;
-        if (p.debug & 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if (leader)
-              mbar_arrive(&tempty[buf]);
-            else
-              mbar_arrive_cluster(tempty_leader0 + buf * 8);
-          }
-          continue;
-        }
-        if (p.mode == OUT_LEAVES) {
-          float* dst =
-              p.out + static_cast<size_t>(t) * p.unit_stride + static_cast<size_t>(grow) * p.ldo + it.n0 + col0;
+        // Both 32-column chunks in flight at once, one wait (for k_first == 1 on an
+        // odd group: each leaf chunk together with the level-1 slot chunk it merges
+        // with); the accumulator goes back to the MMA issuer as soon as the values
+        // are in registers.
+        uint32_t r[NCH][32];
+        const bool odd = KF1 && p.levels >= 1 && (groups_done & 1u);
+        if (!(p.debug & 1)) {
+          if (odd) {
+            // leaf chunk + level-1 slot chunk per round trip: g = (0 + P) + S1
 #pragma unroll
-          for (int c = 0; c < NCH; ++c) {
-            float v[32];
-            tmem_ld32(acc + c * 32, v);
-            tmem_wait_ld();
-            if (row_ok) {
+            for (int c = 0; c < NCH; ++c) {
+              tmem_ld32r(acc + c * 32, r[0]);
+              tmem_ld32r(lane_base + SLOT_LVL1 + c * 32, r[1]);
+              tmem_wait_ld_dep(r[0]);
+              tmem_wait_ld_dep(r[1]);
 #pragma unroll
               for (int i = 0; i < 32; ++i)
-                if (c * 32 + i < ncols) dst[c * 32 + i] = v[i];
+                g[c * 32 + i] = __fadd_rn(__fadd_rn(0.0f, __uint_as_float(r[0][i])), __uint_as_float(r[1][i]));
             }
-          }
-        } else {
+          } else {
 #pragma unroll
-          for (int c0 = 0; c0 < NCH; c0 += LB) {
-            uint32_t r[LB][32];
+            for (int c = 0; c < NCH; ++c) tmem_ld32r(acc + c * 32, r[c]);
 #pragma unroll
-            for (int j = 0; j < LB; ++j) tmem_ld32r(acc + (c0 + j) * 32, r[j]);
-            #pragma unroll
-            for (int j = 0; j < LB; ++j) tmem_wait_ld_dep(r[j]);
-#pragma unroll
-            for (int j = 0; j < LB; ++j) {
-              if (t_in_group == 0) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) g[(c0 + j) * 32 + i] = __fadd_rn(0.0f, __uint_as_float(r[j][i]));
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                  g[(c0 + j) * 32 + i] = __fadd_rn(g[(c0 + j) * 32 + i], __uint_as_float(r[j][i]));
-              }
-            }
+            for (int c = 0; c < NCH; ++c) tmem_wait_ld_dep(r[c]);
           }
         }
-        // Release the accumulator buffer to the leader's MMA thread.
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -397,67 +377,91 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
           else
             mbar_arrive_cluster(tempty_leader0 + buf * 8);
         }
-
-        if (p.mode == OUT_LEAVES) continue;
-        if (++t_in_group < p.kf) continue;
+        if (p.debug & 1) continue;
+        int unit_out = p.mode == OUT_UNITS ? it.unit : 0;
+        if (p.mode == OUT_LEAVES) {
+          // verification dump: the raw leaf P_t goes to slice t
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) g[c * 32 + i] = __uint_as_float(r[c][i]);
+          unit_out = t;
+        } else {
+        // level 0: g = ((0 + P_0) + P_1) + ... + P_{kf-1}   (matmul.cpp:100-125; 0 + P
+        // canonicalises a -0 leaf like matmul.cpp:101-103)
+        if (odd) {
+          // g already holds (0 + P) + S1
+        } else if (KF1 || t_in_group == 0) {  // KF1 <=> k_first == 1: every leaf starts a group
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(0.0f, __uint_as_float(r[c][i]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], __uint_as_float(r[c][i]));
+        }
+        if (!KF1 && ++t_in_group < p.kf) continue;
         t_in_group = 0;
         if (p.debug & 4) continue;
 
-        // Binary counter over completed groups (levels 1..p.levels).
-        int level = 1;
-        uint32_t c_bits = groups_done++;
-        while (c_bits & 1u) {
-          if (level <= 2) {
-            const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
-#pragma unroll
-            for (int c0 = 0; c0 < NCH; c0 += LB) {
-              uint32_t r[LB][32];
-#pragma unroll
-              for (int j = 0; j < LB; ++j) tmem_ld32r(slot + (c0 + j) * 32, r[j]);
-              #pragma unroll
-            for (int j = 0; j < LB; ++j) tmem_wait_ld_dep(r[j]);
-#pragma unroll
-              for (int j = 0; j < LB; ++j)
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                  g[(c0 + j) * 32 + i] = __fadd_rn(g[(c0 + j) * 32 + i], __uint_as_float(r[j][i]));
-            }
-          } else {
-            const float* s = scratch_base + static_cast<size_t>(level - 3) * (BM * BN);
-            if (!(p.debug & 8))
-#pragma unroll
-            for (int i = 0; i < COLS; i += 4) {
-              const float4 x = *reinterpret_cast<const float4*>(s + i * BM);
-              g[i] = __fadd_rn(g[i], x.x);
-              g[i + 1] = __fadd_rn(g[i + 1], x.y);
-              g[i + 2] = __fadd_rn(g[i + 2], x.z);
-              g[i + 3] = __fadd_rn(g[i + 3], x.w);
-            }
+        // Binary counter over completed groups (levels 1..p.levels, matmul.cpp:107-123):
+        // levels 1-2 in TMEM columns [256, 512), deeper levels (touched once per 8+
+        // groups) in L2-resident scratch.
+        if (p.levels >= 1) {
+          int level = 1;
+          uint32_t c_bits = groups_done++;
+          if (odd) {  // the level-1 merge happened with the leaf load
+            c_bits >>= 1;
+            level = 2;
           }
-          c_bits >>= 1;
-          ++level;
-        }
-        if (level <= p.levels) {
-          if (level <= 2) {
-            const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
+          while (c_bits & 1u) {
+            if (level <= 2) {
+              const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
 #pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-              float v[32];
+              for (int c = 0; c < NCH; ++c) tmem_ld32r(slot + c * 32, r[c]);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = g[c * 32 + i];
-              tmem_st32(slot + c * 32, v);
+              for (int c = 0; c < NCH; ++c) tmem_wait_ld_dep(r[c]);
+#pragma unroll
+              for (int c = 0; c < NCH; ++c)
+#pragma unroll
+                for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], __uint_as_float(r[c][i]));
+            } else if (!(p.debug & 8)) {
+              const float* sp = scratch_base + static_cast<size_t>(level - 3) * (BM * BN);
+#pragma unroll
+              for (int i = 0; i < COLS; i += 4) {
+                const float4 x = *reinterpret_cast<const float4*>(sp + i * BM);
+                g[i] = __fadd_rn(g[i], x.x);
+                g[i + 1] = __fadd_rn(g[i + 1], x.y);
+                g[i + 2] = __fadd_rn(g[i + 2], x.z);
+                g[i + 3] = __fadd_rn(g[i + 3], x.w);
+              }
             }
-            tmem_wait_st();
-          } else {
-            float* s = scratch_base + static_cast<size_t>(level - 3) * (BM * BN);
-            if (!(p.debug & 8))
-#pragma unroll
-            for (int i = 0; i < COLS; i += 4)
-              *reinterpret_cast<float4*>(s + i * BM) = make_float4(g[i], g[i + 1], g[i + 2], g[i + 3]);
+            c_bits >>= 1;
+            ++level;
           }
-          continue;
+          if (level <= p.levels) {
+            if (level <= 2) {
+              const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
+#pragma unroll
+              for (int c = 0; c < NCH; ++c) {
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = g[c * 32 + i];
+                tmem_st32(slot + c * 32, v);
+              }
+              tmem_wait_st();
+            } else if (!(p.debug & 8)) {
+              float* sp = scratch_base + static_cast<size_t>(level - 3) * (BM * BN);
+#pragma unroll
+              for (int i = 0; i < COLS; i += 4)
+                *reinterpret_cast<float4*>(sp + i * BM) = make_float4(g[i], g[i + 1], g[i + 2], g[i + 3]);
+            }
+            continue;
+          }
         }
-        // The carry left the top level: g is this unit's complete (sub)tree.
+        }  // the carry left the top level: g is this unit's complete (sub)tree
         if (p.debug & 2) continue;
         if (p.tma_store) {
           // Row-per-lane registers -> 128B-swizzled 32 x 32 smem box (conflict-free
@@ -466,23 +470,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
           for (int c = 0; c < NCH; ++c) {
             if (lane == 0) bulk_wait_read<XB - 1>();
             __syncwarp();
-            uint8_t* buf = sC + ((warp - 4) * XB + xb) * OUT_BUF_BYTES;
+            uint8_t* sbuf = sC + ((warp - 4) * XB + xb) * OUT_BUF_BYTES;
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-              *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+              *reinterpret_cast<float4*>(sbuf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
                   make_float4(g[c * 32 + 4 * j], g[c * 32 + 4 * j + 1], g[c * 32 + 4 * j + 2], g[c * 32 + 4 * j + 3]);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_3d(&tmC, smem_u32(buf), it.n0 + col0 + c * 32, grow - lane,
-                           p.mode == OUT_UNITS ? it.unit : 0);
+              tma_store_3d(&tmC, smem_u32(sbuf), it.n0 + col0 + c * 32, grow - lane, unit_out);
               bulk_commit();
             }
             if constexpr (XB == 2) xb ^= 1;
           }
         } else if (row_ok) {
-          float* dst = p.out + static_cast<size_t>(p.mode == OUT_UNITS ? it.unit : 0) * p.unit_stride +
-                       static_cast<size_t>(grow) * p.ldo + it.n0 + col0;
+          float* dst = p.out + static_cast<size_t>(unit_out) * p.unit_stride + static_cast<size_t>(grow) * p.ldo +
+                       it.n0 + col0;
           if (ncols == COLS && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
             for (int i = 0; i < COLS; i += 4)
@@ -646,37 +649,31 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   const long long max_pairs = sm_count() / 2;
   const long long npairs = p.items < max_pairs ? p.items : max_pairs;
   dim3 grid(static_cast<unsigned>(2 * npairs));
+  const bool kf1 = p.kf == 1;
   if (p.levels > 2) {
     const size_t n = static_cast<size_t>(grid.x) * (p.levels - 2) * BM * BN;
     p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1));
     if (!p.scratch) return set_error(TBIK_CUDA_ERROR, "tc gemm: scratch allocation failed");
   }
-  static const int variant = [] {
-    // 8 merge warps (two per TMEM lane quarter, 64 columns each) is the default;
-    // TBIK_TC_EPI=4 selects the 4-warp variant (same bits).
-    const char* e = std::getenv("TBIK_TC_EPI");
-    return e && std::atoi(e) == 4 ? 0 : 1;
-  }();
   // Results leave through a TMA store when the output is 16-byte addressable.
   CUtensorMap mC;
   std::memset(&mC, 0, sizeof(mC));
-  const uint64_t ustride = o.mode == OUT_UNITS ? static_cast<uint64_t>(o.unit_stride)
-                                               : static_cast<uint64_t>(o.ldo) * static_cast<uint64_t>(v.M);
-  p.tma_store = o.mode != OUT_LEAVES && !(dbg & 16) && (reinterpret_cast<uintptr_t>(o.out) & 15) == 0 &&
-                o.ldo % 4 == 0 && ustride % 4 == 0;
+  const uint64_t ustride = o.mode != OUT_FULL ? static_cast<uint64_t>(o.unit_stride)
+                                              : static_cast<uint64_t>(o.ldo) * static_cast<uint64_t>(v.M);
+  p.tma_store = !(dbg & 16) && (reinterpret_cast<uintptr_t>(o.out) & 15) == 0 && o.ldo % 4 == 0 && ustride % 4 == 0;
   if (p.tma_store)
     TBIK_TRY(make_map_out(&mC, o.out, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.M),
                           static_cast<uint64_t>(p.units), static_cast<uint64_t>(o.ldo) * 4, ustride * 4));
   void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams) =
-      variant == 0 ? tc_tree_gemm_kernel<4, 1, STAGES> : tc_tree_gemm_kernel<8, 1, STAGES>;
-  const int nthreads = variant ? 128 + 32 * 8 : 128 + 32 * 4;
-  const size_t smem = variant ? smem_bytes(8, STAGES) : smem_bytes(4, STAGES);
+      kf1 ? tc_tree_gemm_kernel<8, true, STAGES> : tc_tree_gemm_kernel<8, false, STAGES>;
+  const int nthreads = 128 + 32 * 8;
+  const size_t smem = smem_bytes(8, STAGES);
   static bool attr_set[16][2] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 16 && !attr_set[dev][variant]) {
+  if (dev >= 0 && dev < 16 && !attr_set[dev][kf1]) {
     TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr_set[dev][variant] = true;
+    attr_set[dev][kf1] = true;
   }
   kern<<<grid, nthreads, smem, s>>>(mA, mB, mC, p);
   TBIK_CUDA(cudaGetLastError());

@@ -287,6 +287,9 @@ tbik_status tbik_group_destroy(tbik_group* g) {
   return TBIK_OK;
 }
 
+int tbik_group_world_size(const tbik_group* g) { return g ? g->W : 0; }
+int tbik_group_rank(const tbik_group* g) { return g ? g->rank : -1; }
+
 float* tbik_group_send_buffer(tbik_group* g) {
   if (!g) return nullptr;
   return slot_ptr(g->region, g->capacity, g->epoch + 1);

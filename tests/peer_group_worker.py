@@ -58,6 +58,11 @@ def main():
         assert torch.equal(red_big.view(torch.int32), local_big.view(torch.int32)), f"two-phase differs ({it})"
         assert torch.equal(odd.view(torch.int32), local_big.view(torch.int32)), f"unaligned out differs ({it})"
         assert torch.equal(small.view(torch.int32), local.view(torch.int32)), f"one-shot differs ({it})"
+    # host-buffer pipeline through the group: chunked epochs, same bits as the device call
+    xh = x[:, kb:ke].contiguous().cpu().pin_memory()
+    yh = grp.row_parallel_forward_hostio(xh, ws, K, cfg, 8, tb.LEAF_TCGEN05, chunk_rows=24)
+    torch.cuda.synchronize()
+    assert torch.equal(yh.view(torch.int32), ys[0].cpu().view(torch.int32)), "host-io group result differs"
     out = os.environ["TBIK_TEST_OUT"]
     np.save(out, ys[0].cpu().numpy())
     if rank == 0:

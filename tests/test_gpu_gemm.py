@@ -291,3 +291,33 @@ def test_tc_tile_width_and_raster_invisible(tb, cuda, orc, M, K, N, monkeypatch)
     plan = tb.plan_blocks(K, cfg, 1)
     want = orc.tree_over_leaves(leaves[0].cpu().numpy(), plan.k_first)
     assert np.array_equal(bits(outs[0].cpu().numpy()), bits(want))
+
+
+# ---------------------------------------------------------------------------------
+# host-buffer entry point: chunked H2D / GEMM / D2H pipeline == device call, bit for bit
+# ---------------------------------------------------------------------------------
+@pytest.mark.parametrize("leaf", LEAVES)
+@pytest.mark.parametrize("M,chunk", [(1, 0), (300, 0), (700, 256), (1000, 97), (2048, 0)])
+def test_hostio_equals_device(tb, cuda, leaf, M, chunk):
+    K, N = 14336, 512
+    g = torch.Generator().manual_seed(M)
+    x = torch.randn(M, K, generator=g).to(torch.bfloat16)
+    w = torch.randn(K, N, generator=g).to(torch.bfloat16).cuda()
+    cfg = tb.BlockConfig(64, 256, 128, 0)
+    ref = tb.tree_matmul(x.cuda(), w, cfg, leaf_id(tb, leaf))
+    xp = x.pin_memory()
+    y = tb.tree_matmul_hostio(xp, w, cfg, leaf_id(tb, leaf), chunk_rows=chunk)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int32), ref.cpu().view(torch.int32))
+    # pageable host buffers and a strided host output view take the same path
+    big = torch.zeros(M, N + 3)
+    y2 = tb.tree_matmul_hostio(x, w, cfg, leaf_id(tb, leaf), out=big[:, 1:N + 1], chunk_rows=chunk)
+    torch.cuda.synchronize()
+    assert torch.equal(y2.view(torch.int32), ref.cpu().view(torch.int32))
+    assert float(big[:, 0].abs().sum()) == 0.0 and float(big[:, N + 1:].abs().sum()) == 0.0
+
+
+def test_hostio_rejects_device_activations(tb, cuda):
+    w = torch.zeros(256, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(tb.TbikError):
+        tb.tree_matmul_hostio(torch.zeros(4, 256, dtype=torch.bfloat16, device="cuda"), w)
