@@ -635,18 +635,22 @@ float tbo_log(float x) { /* x > 0, finite */
 /* ---------------------------------------------------------------------------
  * NEW semantics: tree-ordered log-softmax / log-prob over a vocab row.
  *
- * State (m, s) = (running max, sum of exp(x - m)).  Empty = (-inf, 0).
- *   fold(m,s; x):  x == -inf -> unchanged
- *                  x <= m    -> s = s + exp(x - m)
- *                  x >  m    -> s = s * exp(m - x); s = s + 1; m = x
+ * State (m, s) = (max, sum of exp(x - m)).  Empty = (-inf, 0).
  *   merge((m1,s1) lo, (m2,s2) hi):  if m1 == -inf return hi; if m2 == -inf
  *                  return lo; m = m1 >= m2 ? m1 : m2;
  *                  s = s1 * exp(m1 - m) + s2 * exp(m2 - m)   (mul, mul, add)
  * Canonical tree for a row of V logits cut into G contiguous equal vocab
  * groups (G a power of two >= the largest TP size; V % G == 0):
  *   * within a group of n = V / G logits: chunks of 4 consecutive logits,
- *     lane l in [0,256) folds chunks l, l+256, ... in ascending element order;
- *     the 256 lane states are merged by the contiguous-halves tree;
+ *     lane l in [0,256) owns chunks l, l+256, ... (ascending); it consumes them
+ *     in BLOCKS of 8 of its chunks (<= 32 logits, ascending element order):
+ *       block state: m_b = sequential max (x > m ? x : m) over the block from
+ *       its first element; s_b = ((0 + e_0) + e_1) + ... with e_i =
+ *       exp(x_i - m_b) in ascending element order; m_b == -inf -> empty;
+ *     the lane state is the left fold merge(merge(B_0, B_1), B_2) ... of its
+ *     block states (two-pass inside a register-sized block: no serial
+ *     max-rescale chain per element);
+ *   * the 256 lane states are merged by the contiguous-halves tree;
  *   * the G group states are merged by the contiguous-halves tree.
  * A TP rank owning G/TP consecutive groups computes exactly a subtree, so
  * the cross-rank merge of (m, s) pairs (8 bytes per row per rank) continues
@@ -656,18 +660,6 @@ float tbo_log(float x) { /* x > 0, finite */
 typedef struct {
   float m, s;
 } tbo_ms;
-
-static tbo_ms ms_fold(tbo_ms st, float x) {
-  if (x == -INFINITY) return st;
-  if (x <= st.m) {
-    st.s = st.s + tbo_exp(x - st.m);
-  } else {
-    st.s = st.s * tbo_exp(st.m - x);
-    st.s = st.s + 1.0f;
-    st.m = x;
-  }
-  return st;
-}
 
 static tbo_ms ms_merge(tbo_ms lo, tbo_ms hi) {
   if (lo.m == -INFINITY) return hi;
@@ -685,13 +677,42 @@ static tbo_ms ms_tree(const tbo_ms* v, int64_t n) {
   return ms_merge(ms_tree(v, h), ms_tree(v + h, n - h));
 }
 
+#define TBO_MS_BLOCK 8 /* chunks of 4 logits per lane block */
+
 static tbo_ms ms_group(const float* x, int64_t n) {
   const int64_t nchunks = (n + 3) / 4;
   tbo_ms lanes[TBO_LANES];
   for (int l = 0; l < TBO_LANES; ++l) {
     tbo_ms st = {-INFINITY, 0.0f};
-    for (int64_t c = l; c < nchunks; c += TBO_LANES)
-      for (int64_t e = c * 4; e < c * 4 + 4 && e < n; ++e) st = ms_fold(st, x[e]);
+    for (int64_t c0 = l; c0 < nchunks; c0 += (int64_t)TBO_LANES * TBO_MS_BLOCK) {
+      /* one block: chunks c0, c0+256, ... (at most TBO_MS_BLOCK of them) */
+      float m = -INFINITY;
+      int first = 1;
+      for (int j = 0; j < TBO_MS_BLOCK; ++j) {
+        const int64_t c = c0 + (int64_t)j * TBO_LANES;
+        if (c >= nchunks) break;
+        for (int64_t e = c * 4; e < c * 4 + 4 && e < n; ++e) {
+          if (first) {
+            m = x[e];
+            first = 0;
+          } else {
+            m = x[e] > m ? x[e] : m;
+          }
+        }
+      }
+      tbo_ms b = {-INFINITY, 0.0f};
+      if (m != -INFINITY) {
+        float sum = 0.0f;
+        for (int j = 0; j < TBO_MS_BLOCK; ++j) {
+          const int64_t c = c0 + (int64_t)j * TBO_LANES;
+          if (c >= nchunks) break;
+          for (int64_t e = c * 4; e < c * 4 + 4 && e < n; ++e) sum = sum + tbo_exp(x[e] - m);
+        }
+        b.m = m;
+        b.s = sum;
+      }
+      st = ms_merge(st, b);
+    }
     lanes[l] = st;
   }
   return ms_tree(lanes, TBO_LANES);

@@ -11,7 +11,7 @@
 // L2-grouped raster (8 M-blocks share one pass over W).
 //
 // Warp roles per CTA (384 threads, one CTA per SM):
-//   warp 0      TMA producer: 8-stage ring of {A 128x64, B 64x64} 128B-swizzled
+//   warp 0      TMA producer: 6-stage ring of {A 128x64, B 64x64} 128B-swizzled
 //               tiles (2SM TMA; completion counted on the leader's barrier)
 //   warp 1      (leader CTA) MMA issuer: for every leaf tile, block_k/16 MMAs into
 //               a ZEROED TMEM accumulator; two accumulators so leaf t+1 is computed
@@ -24,10 +24,16 @@
 //               released, then __fadd_rn verbatim the reference's reduction:
 //                 level 0   g = ((0 + P_0) + P_1) + ... + P_{kf-1}   (matmul.cpp:100-125)
 //                 levels>=1 binary counter over group values (matmul.cpp:107-123)
-//               g in 64 registers; tree levels 1-2 in TMEM cols [256,512);
-//               deeper levels (touched once per 8+ groups) in L2-resident scratch
-//               ([col/4][row][4] slabs, 512 B per warp access).  Results leave
-//               through a 128B-swizzled 32 x 32 smem box and a TMA store.
+//               g in 64 registers; tree levels 1-2 in TMEM cols [256,512),
+//               level 3 in an 8 KB shared-memory region per warp (also the
+//               output staging), deeper levels (touched once per 16+ groups) in
+//               L2-resident scratch ([col/4][row][4] slabs, 512 B per warp
+//               access).  Results leave through 128B-swizzled 32 x 32 smem boxes
+//               and TMA stores.
+//   Measured (profiles/r01_tc_merge_ablation*.txt): an L2 round trip for a
+//   scratch level stalls the merge for longer than the accumulator double
+//   buffer can absorb (-20 % at k_first = 1), hence level 3 on chip at the
+//   price of 2 pipeline stages (-1..3 % with the merge disabled).
 //   Why this shape (measured, tools/ab_epi.py): the MMA operand reads and TMA
 //   writes keep the SM's shared-memory/L1 data port ~90% busy, so every byte the
 //   merge moves through L1 costs tensor throughput.  Row-per-thread STG.128
@@ -53,7 +59,7 @@ constexpr int BM = 128;     // rows per CTA (the pair covers 256)
 constexpr int PAIR_M = 256;
 constexpr int BN = 128;     // columns per pair tile (MMA N); each CTA stages BN/2 of B
 constexpr int KSTAGE = 64;  // K per pipeline stage (one 128 B swizzle row of bf16)
-constexpr int STAGES = 8;
+constexpr int STAGES = 6;
 constexpr int A_STAGE_BYTES = BM * KSTAGE * 2;        // 16 KB
 constexpr int B_STAGE_BYTES = KSTAGE * (BN / 2) * 2;  // 8 KB
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
@@ -62,13 +68,15 @@ constexpr int SLOT_LVL1 = 256;
 constexpr int SLOT_LVL2 = 384;
 constexpr int GROUP_M = 8;  // raster: M-blocks that share one pass over W
 constexpr uint32_t IDESC = umma_idesc_bf16(PAIR_M, BN, /*a_mn_major=*/0, /*b_mn_major=*/1);
-// Output staging for the TMA store: per merge warp, XB buffers of 32 rows x
-// 32 f32 (4 KB, 128B-swizzled).
+// Tree level 3 lives in shared memory: per merge warp an 8 KB region holding its
+// 32 rows x 64 columns as [16 float4 columns][32 lanes][float4] (conflict-free
+// 16-byte accesses).  The same region doubles as the warp's output staging for
+// the TMA store (two 32 x 32 f32 boxes, 128B-swizzled): level 3 is consumed by
+// the carry that produces the output, and rewritten only 4+ groups later.
 constexpr int OUT_BUF_BYTES = 32 * 32 * 4;
-constexpr int out_bufs(int epi) { return epi == 4 ? 2 : 1; }
+constexpr int L3_WARP_BYTES = 32 * 64 * 4;
 constexpr size_t smem_bytes(int epi, int nst) {
-  return 1024 + static_cast<size_t>(nst) * STAGE_BYTES + 1024 +
-         static_cast<size_t>(epi) * out_bufs(epi) * OUT_BUF_BYTES;
+  return 1024 + static_cast<size_t>(nst) * STAGE_BYTES + 1024 + static_cast<size_t>(epi) * L3_WARP_BYTES;
 }
 
 struct TcParams {
@@ -83,7 +91,7 @@ struct TcParams {
   float* out;
   long long ldo;
   long long unit_stride;
-  float* scratch;  // [gridDim.x][levels-2][BN][BM] when levels > 2
+  float* scratch;  // [gridDim.x][levels-3][BN][BM] when levels > 3
   int tma_store;   // 1: results leave through tmC (TMA), 0: direct row stores
   int debug;       // TBIK_TC_DEBUG (perf experiments only; wrong results): 1 = skip the merge,
                    // 2 = skip the output store, 4 = skip the tree above level 0,
@@ -208,8 +216,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* sC = smem + NST * STAGE_BYTES + 1024;  // 1024-aligned output staging
-  constexpr int XB = out_bufs(EPI);
+  uint8_t* sL3 = smem + NST * STAGE_BYTES + 1024;  // 1024-aligned level-3 / output staging
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -319,13 +326,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
     const int row_in_tile = q * 32 + lane;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + col0;
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
-    // TMEM holds tree levels 1-2; levels >= 3 live in scratch as [col/4][row][4]
-    // slabs (a warp's float4 access is 512 contiguous bytes).
+    // TMEM holds tree levels 1-2, shared memory level 3 (this warp's sL3 region);
+    // levels >= 4 live in scratch as [col/4][row][4] slabs (a warp's float4
+    // access is 512 contiguous bytes).
     float* scratch_base =
-        p.levels > 2
-            ? p.scratch + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - 2) * (BM * BN) +
+        p.levels > 3
+            ? p.scratch + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - 3) * (BM * BN) +
                            static_cast<size_t>(col0) * BM + static_cast<size_t>(row_in_tile) * 4
             : nullptr;
+    uint8_t* l3 = sL3 + (warp - 4) * L3_WARP_BYTES;  // [16][32 lanes][float4]
 
     float g[COLS];  // level 0: the running leaf-group value
     int xb = 0;      // output staging buffer toggle
@@ -427,8 +436,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
               for (int c = 0; c < NCH; ++c)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], __uint_as_float(r[c][i]));
+            } else if (level == 3) {
+#pragma unroll
+              for (int i = 0; i < COLS; i += 4) {
+                const float4 x = *reinterpret_cast<const float4*>(l3 + ((i / 4) * 32 + lane) * 16);
+                g[i] = __fadd_rn(g[i], x.x);
+                g[i + 1] = __fadd_rn(g[i + 1], x.y);
+                g[i + 2] = __fadd_rn(g[i + 2], x.z);
+                g[i + 3] = __fadd_rn(g[i + 3], x.w);
+              }
+              __syncwarp();  // the region may become output staging right after
             } else if (!(p.debug & 8)) {
-              const float* sp = scratch_base + static_cast<size_t>(level - 3) * (BM * BN);
+              const float* sp = scratch_base + static_cast<size_t>(level - 4) * (BM * BN);
 #pragma unroll
               for (int i = 0; i < COLS; i += 4) {
                 const float4 x = *reinterpret_cast<const float4*>(sp + i * BM);
@@ -452,8 +471,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
                 tmem_st32(slot + c * 32, v);
               }
               tmem_wait_st();
+            } else if (level == 3) {
+              if (lane == 0) bulk_wait_read<0>();  // earlier output boxes staged here
+              __syncwarp();
+#pragma unroll
+              for (int i = 0; i < COLS; i += 4)
+                *reinterpret_cast<float4*>(l3 + ((i / 4) * 32 + lane) * 16) =
+                    make_float4(g[i], g[i + 1], g[i + 2], g[i + 3]);
             } else if (!(p.debug & 8)) {
-              float* sp = scratch_base + static_cast<size_t>(level - 3) * (BM * BN);
+              float* sp = scratch_base + static_cast<size_t>(level - 4) * (BM * BN);
 #pragma unroll
               for (int i = 0; i < COLS; i += 4)
                 *reinterpret_cast<float4*>(sp + i * BM) = make_float4(g[i], g[i + 1], g[i + 2], g[i + 3]);
@@ -468,9 +494,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
           // 16 B stores) -> one TMA store per box; the tensor map clips ragged edges.
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
-            if (lane == 0) bulk_wait_read<XB - 1>();
+            if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
-            uint8_t* sbuf = sC + ((warp - 4) * XB + xb) * OUT_BUF_BYTES;
+            uint8_t* sbuf = l3 + xb * OUT_BUF_BYTES;
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               *reinterpret_cast<float4*>(sbuf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
@@ -481,7 +507,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
               tma_store_3d(&tmC, smem_u32(sbuf), it.n0 + col0 + c * 32, grow - lane, unit_out);
               bulk_commit();
             }
-            if constexpr (XB == 2) xb ^= 1;
+            xb ^= 1;
           }
         } else if (row_ok) {
           float* dst = p.out + static_cast<size_t>(unit_out) * p.unit_stride + static_cast<size_t>(grow) * p.ldo +
@@ -650,8 +676,8 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   const long long npairs = p.items < max_pairs ? p.items : max_pairs;
   dim3 grid(static_cast<unsigned>(2 * npairs));
   const bool kf1 = p.kf == 1;
-  if (p.levels > 2) {
-    const size_t n = static_cast<size_t>(grid.x) * (p.levels - 2) * BM * BN;
+  if (p.levels > 3) {
+    const size_t n = static_cast<size_t>(grid.x) * (p.levels - 3) * BM * BN;
     p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1));
     if (!p.scratch) return set_error(TBIK_CUDA_ERROR, "tc gemm: scratch allocation failed");
   }

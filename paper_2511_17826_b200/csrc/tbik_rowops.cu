@@ -28,18 +28,6 @@ struct MS {
   float m, s;
 };
 
-__device__ __forceinline__ MS ms_fold(MS st, float x) {
-  if (x == __int_as_float(0xFF800000)) return st;
-  if (x <= st.m) {
-    st.s = __fadd_rn(st.s, tb_exp(__fsub_rn(x, st.m)));
-  } else {
-    st.s = __fmul_rn(st.s, tb_exp(__fsub_rn(st.m, x)));
-    st.s = __fadd_rn(st.s, 1.0f);
-    st.m = x;
-  }
-  return st;
-}
-
 __device__ __forceinline__ MS ms_merge(MS lo, MS hi) {
   if (lo.m == __int_as_float(0xFF800000)) return hi;
   if (hi.m == __int_as_float(0xFF800000)) return lo;
@@ -86,47 +74,139 @@ __device__ __forceinline__ MS block_tree_ms(MS v, MS* sh) {
 }
 
 // ---- RMSNorm ------------------------------------------------------------------
+// Pass 1 folds lane l's 16-byte chunks (l, l+256, ...) with an fma chain and
+// keeps the first CACHE of them in registers; pass 2 revisits the same chunks
+// with 16-byte loads of gamma and 16-byte stores (no second trip to memory for
+// rows up to CACHE*256 chunks: 8192 bf16 / 4096 f32 columns).
+template <typename TY>
+__device__ __forceinline__ void store_chunk(TY* y, const float* r, int n);
+template <>
+__device__ __forceinline__ void store_chunk<float>(float* y, const float* r, int n) {
+  if (n == 4) {
+    *reinterpret_cast<float4*>(y) = make_float4(r[0], r[1], r[2], r[3]);
+  } else if (n == 8) {
+    *reinterpret_cast<float4*>(y) = make_float4(r[0], r[1], r[2], r[3]);
+    *reinterpret_cast<float4*>(y + 4) = make_float4(r[4], r[5], r[6], r[7]);
+  }
+}
+template <>
+__device__ __forceinline__ void store_chunk<uint16_t>(uint16_t* y, const float* r, int n) {
+  if (n == 8) {
+    uint4 o;
+    o.x = f32_to_bf16_bits(r[0]) | (static_cast<uint32_t>(f32_to_bf16_bits(r[1])) << 16);
+    o.y = f32_to_bf16_bits(r[2]) | (static_cast<uint32_t>(f32_to_bf16_bits(r[3])) << 16);
+    o.z = f32_to_bf16_bits(r[4]) | (static_cast<uint32_t>(f32_to_bf16_bits(r[5])) << 16);
+    o.w = f32_to_bf16_bits(r[6]) | (static_cast<uint32_t>(f32_to_bf16_bits(r[7])) << 16);
+    *reinterpret_cast<uint4*>(y) = o;
+  } else if (n == 4) {
+    uint2 o;
+    o.x = f32_to_bf16_bits(r[0]) | (static_cast<uint32_t>(f32_to_bf16_bits(r[1])) << 16);
+    o.y = f32_to_bf16_bits(r[2]) | (static_cast<uint32_t>(f32_to_bf16_bits(r[3])) << 16);
+    *reinterpret_cast<uint2*>(y) = o;
+  }
+}
+
 template <typename TX, typename TY, bool VEC>
 __global__ void __launch_bounds__(LANES) tree_rmsnorm_kernel(const TX* __restrict__ X, int64_t ldx,
                                                              const float* __restrict__ gamma, float eps,
                                                              TY* __restrict__ Y, int64_t ldy, int64_t cols) {
   __shared__ float sh[9];
   constexpr int CH = 16 / sizeof(TX);  // 8 bf16 or 4 f32 per chunk
+  constexpr int CACHE = 4;
   const TX* x = X + static_cast<int64_t>(blockIdx.x) * ldx;
+  TY* y = Y + static_cast<int64_t>(blockIdx.x) * ldy;
   const int64_t nch = (cols + CH - 1) / CH;
   float acc = 0.0f;
-  for (int64_t c = threadIdx.x; c < nch; c += LANES) {
-    const int64_t e0 = c * CH;
-    if (VEC && e0 + CH <= cols) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(x + e0);
-      const TX* v = reinterpret_cast<const TX*>(&raw);
+  if constexpr (VEC) {
+    uint4 cache[CACHE];
 #pragma unroll
-      for (int i = 0; i < CH; ++i) {
-        const float f = load_as_f32(v + i);
-        acc = __fmaf_rn(f, f, acc);
+    for (int k = 0; k < CACHE; ++k) {
+      const int64_t c = threadIdx.x + static_cast<int64_t>(k) * LANES;
+      if (c < nch && c * CH + CH <= cols) cache[k] = *reinterpret_cast<const uint4*>(x + c * CH);
+    }
+    for (int64_t c = threadIdx.x, k = 0; c < nch; c += LANES, ++k) {
+      const int64_t e0 = c * CH;
+      if (e0 + CH <= cols) {
+        uint4 raw;
+        if (k < CACHE) {
+#pragma unroll
+          for (int j = 0; j < CACHE; ++j)
+            if (j == k) raw = cache[j];
+        } else {
+          raw = *reinterpret_cast<const uint4*>(x + e0);
+        }
+        const TX* v = reinterpret_cast<const TX*>(&raw);
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          const float f = load_as_f32(v + i);
+          acc = __fmaf_rn(f, f, acc);
+        }
+      } else {
+        for (int64_t e = e0; e < cols; ++e) {
+          const float f = load_as_f32(x + e);
+          acc = __fmaf_rn(f, f, acc);
+        }
       }
-    } else {
-      for (int64_t e = e0; e < e0 + CH && e < cols; ++e) {
+    }
+    const float ss = block_tree_sum(acc, sh);
+    const float ms = __fdiv_rn(ss, static_cast<float>(cols));
+    const float denom = __fsqrt_rn(__fadd_rn(ms, eps));
+    const bool yvec = (reinterpret_cast<uintptr_t>(y) & 15) == 0 && (reinterpret_cast<uintptr_t>(gamma) & 15) == 0;
+    for (int64_t c = threadIdx.x, k = 0; c < nch; c += LANES, ++k) {
+      const int64_t e0 = c * CH;
+      if (yvec && e0 + CH <= cols) {
+        uint4 raw;
+        if (k < CACHE) {
+#pragma unroll
+          for (int j = 0; j < CACHE; ++j)
+            if (j == k) raw = cache[j];
+        } else {
+          raw = *reinterpret_cast<const uint4*>(x + e0);
+        }
+        const TX* v = reinterpret_cast<const TX*>(&raw);
+        float gm[CH], r[CH];
+#pragma unroll
+        for (int i = 0; i < CH; i += 4) *reinterpret_cast<float4*>(gm + i) = *reinterpret_cast<const float4*>(gamma + e0 + i);
+#pragma unroll
+        for (int i = 0; i < CH; ++i) r[i] = __fdiv_rn(__fmul_rn(load_as_f32(v + i), gm[i]), denom);
+        store_chunk<TY>(y + e0, r, CH);
+      } else {
+        for (int64_t e = e0; e < e0 + CH && e < cols; ++e) {
+          const float r = __fdiv_rn(__fmul_rn(load_as_f32(x + e), gamma[e]), denom);
+          if constexpr (sizeof(TY) == 4)
+            y[e] = r;
+          else
+            y[e] = f32_to_bf16_bits(r);
+        }
+      }
+    }
+  } else {
+    for (int64_t c = threadIdx.x; c < nch; c += LANES)
+      for (int64_t e = c * CH; e < c * CH + CH && e < cols; ++e) {
         const float f = load_as_f32(x + e);
         acc = __fmaf_rn(f, f, acc);
       }
+    const float ss = block_tree_sum(acc, sh);
+    const float ms = __fdiv_rn(ss, static_cast<float>(cols));
+    const float denom = __fsqrt_rn(__fadd_rn(ms, eps));
+    for (int64_t e = threadIdx.x; e < cols; e += LANES) {
+      const float r = __fdiv_rn(__fmul_rn(load_as_f32(x + e), gamma[e]), denom);
+      if constexpr (sizeof(TY) == 4)
+        y[e] = r;
+      else
+        y[e] = f32_to_bf16_bits(r);
     }
-  }
-  const float ss = block_tree_sum(acc, sh);
-  const float ms = __fdiv_rn(ss, static_cast<float>(cols));
-  const float denom = __fsqrt_rn(__fadd_rn(ms, eps));
-  TY* y = Y + static_cast<int64_t>(blockIdx.x) * ldy;
-  for (int64_t e = threadIdx.x; e < cols; e += LANES) {
-    const float r = __fdiv_rn(__fmul_rn(load_as_f32(x + e), gamma[e]), denom);
-    if constexpr (sizeof(TY) == 4)
-      y[e] = r;
-    else
-      y[e] = f32_to_bf16_bits(r);
   }
 }
 
 // ---- log-softmax ----------------------------------------------------------------
-// Group states: one CTA per (row, group) of n = v_local / groups logits.
+// Group states: one CTA per (row, group) of n = v_local / groups logits.  Lane l
+// owns chunks l, l+256, ... of 4 logits and consumes them in blocks of MSB of its
+// chunks (tbo_tree_logsoftmax): block max (sequential, ascending), then
+// s = ((0 + exp(x_0 - m)) + exp(x_1 - m)) + ...; blocks fold left with ms_merge.
+// The block's 32 logits stay in registers between the two passes.
+constexpr int MSB = 8;
+
 template <bool VEC>
 __global__ void __launch_bounds__(LANES) ms_group_kernel(const float* __restrict__ logits, int64_t ld, int64_t n,
                                                          int64_t groups, MS* __restrict__ out) {
@@ -134,18 +214,40 @@ __global__ void __launch_bounds__(LANES) ms_group_kernel(const float* __restrict
   const int64_t row = blockIdx.x, g = blockIdx.y;
   const float* x = logits + row * ld + g * n;
   const int64_t nch = (n + 3) / 4;
-  MS st{__int_as_float(0xFF800000), 0.0f};
-  for (int64_t c = threadIdx.x; c < nch; c += LANES) {
-    const int64_t e0 = c * 4;
-    if (VEC && e0 + 4 <= n) {
-      const float4 v = *reinterpret_cast<const float4*>(x + e0);
-      st = ms_fold(st, v.x);
-      st = ms_fold(st, v.y);
-      st = ms_fold(st, v.z);
-      st = ms_fold(st, v.w);
-    } else {
-      for (int64_t e = e0; e < e0 + 4 && e < n; ++e) st = ms_fold(st, x[e]);
+  const float NEG_INF = __int_as_float(0xFF800000);
+  MS st{NEG_INF, 0.0f};
+  for (int64_t c0 = threadIdx.x; c0 < nch; c0 += static_cast<int64_t>(LANES) * MSB) {
+    float v[MSB * 4];
+    int cnt[MSB];  // valid logits in each chunk (4, or fewer in the group's last chunk)
+#pragma unroll
+    for (int j = 0; j < MSB; ++j) {
+      const int64_t c = c0 + static_cast<int64_t>(j) * LANES;
+      const int64_t e0 = c * 4;
+      cnt[j] = c < nch ? (n - e0 < 4 ? static_cast<int>(n - e0) : 4) : 0;
+      if (VEC && cnt[j] == 4) {
+        const float4 q = *reinterpret_cast<const float4*>(x + e0);
+        v[4 * j] = q.x;
+        v[4 * j + 1] = q.y;
+        v[4 * j + 2] = q.z;
+        v[4 * j + 3] = q.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[4 * j + i] = i < cnt[j] ? x[e0 + i] : NEG_INF;
+      }
     }
+    float m = v[0];  // chunk c0 < nch always holds >= 1 logit
+#pragma unroll
+    for (int k = 1; k < MSB * 4; ++k)
+      if (k % 4 < cnt[k / 4]) m = v[k] > m ? v[k] : m;
+    MS b{NEG_INF, 0.0f};
+    if (m != NEG_INF) {
+      float sum = 0.0f;
+#pragma unroll
+      for (int k = 0; k < MSB * 4; ++k)
+        if (k % 4 < cnt[k / 4]) sum = __fadd_rn(sum, tb_exp(__fsub_rn(v[k], m)));
+      b = MS{m, sum};
+    }
+    st = ms_merge(st, b);
   }
   const MS r = block_tree_ms(st, sh);
   if (threadIdx.x == 0) out[row * groups + g] = r;
@@ -191,13 +293,23 @@ __global__ void ms_merge_kernel(PartPtrs parts, int W, int64_t rows, float* __re
 
 __global__ void finish_kernel(const float* __restrict__ logits, int64_t ld, int64_t rows, int64_t v_local,
                               const float* __restrict__ lse, float* __restrict__ logprobs, int64_t ld_out,
-                              const int64_t* __restrict__ targets, int64_t v_offset, float* __restrict__ tlp) {
+                              const int64_t* __restrict__ targets, int64_t v_offset, float* __restrict__ tlp,
+                              bool vec) {
   const int64_t row = blockIdx.y;
   const float l = lse[row];
   if (logprobs) {
-    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < v_local;
-         j += static_cast<int64_t>(gridDim.x) * blockDim.x)
-      logprobs[row * ld_out + j] = __fsub_rn(logits[row * ld + j], l);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (vec) {
+      const float4* src = reinterpret_cast<const float4*>(logits + row * ld);
+      float4* dst = reinterpret_cast<float4*>(logprobs + row * ld_out);
+      for (int64_t j = t0; j < v_local / 4; j += stride) {
+        const float4 q = src[j];
+        dst[j] = make_float4(__fsub_rn(q.x, l), __fsub_rn(q.y, l), __fsub_rn(q.z, l), __fsub_rn(q.w, l));
+      }
+    } else {
+      for (int64_t j = t0; j < v_local; j += stride) logprobs[row * ld_out + j] = __fsub_rn(logits[row * ld + j], l);
+    }
   }
   if (targets && tlp && blockIdx.x == 0 && threadIdx.x == 0) {
     const int64_t t = targets[row] - v_offset;
@@ -290,10 +402,13 @@ tbik_status tbik_logsoftmax_finish(const float* logits, int64_t ld, int64_t rows
   if (!logits || !lse) return set_error(TBIK_BAD_ARGUMENT, "null argument");
   if (rows > 65535) return set_error(TBIK_UNSUPPORTED, "logsoftmax finish: > 65535 rows per call");
   if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
-  const int64_t xblocks = logprobs ? std::min<int64_t>((v_local + 1023) / 1024, 64) : 1;
+  const bool vec = logprobs && (reinterpret_cast<uintptr_t>(logits) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(logprobs) & 15) == 0 && ld % 4 == 0 && ld_out % 4 == 0 &&
+                   v_local % 4 == 0;
+  const int64_t xblocks = logprobs ? std::min<int64_t>((v_local + 4095) / 4096, 16) : 1;
   dim3 grid(static_cast<unsigned>(xblocks), static_cast<unsigned>(rows));
   finish_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(logits, ld, rows, v_local, lse, logprobs, ld_out,
-                                                                     targets, v_offset, target_logprobs);
+                                                                     targets, v_offset, target_logprobs, vec);
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;
