@@ -106,6 +106,42 @@ __device__ __forceinline__ void store_chunk<uint16_t>(uint16_t* y, const float* 
   }
 }
 
+// (x * gamma) / denom, correctly rounded, with one reciprocal per row: q0 =
+// RN(n * RN(1/d)), e = n - q0 * d (exact by fma), q = RN(q0 + e * RN(1/d)) is
+// RN(n / d) (Markstein's theorem; no under/overflow in range, guarded).
+__device__ __forceinline__ float div_rn_rcp(float n, float d, float rcp) {
+  const float q0 = __fmul_rn(n, rcp);
+  const float e = __fmaf_rn(-q0, d, n);
+  const float q = __fmaf_rn(e, rcp, q0);
+  const float aq = fabsf(q0);
+  return (aq < 0x1p-100f || aq > 0x1p100f) ? __fdiv_rn(n, d) : q;
+}
+
+template <typename TX>
+__device__ __forceinline__ float sumsq_chunk(const uint4& raw, float acc) {
+  constexpr int CH = 16 / sizeof(TX);
+  const TX* v = reinterpret_cast<const TX*>(&raw);
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    const float f = load_as_f32(v + i);
+    acc = __fmaf_rn(f, f, acc);
+  }
+  return acc;
+}
+
+template <typename TX, typename TY>
+__device__ __forceinline__ void norm_chunk(const uint4& raw, const float* __restrict__ gamma, int64_t e0, float denom,
+                                           float rcp, TY* y) {
+  constexpr int CH = 16 / sizeof(TX);
+  const TX* v = reinterpret_cast<const TX*>(&raw);
+  float gm[CH], r[CH];
+#pragma unroll
+  for (int i = 0; i < CH; i += 4) *reinterpret_cast<float4*>(gm + i) = *reinterpret_cast<const float4*>(gamma + e0 + i);
+#pragma unroll
+  for (int i = 0; i < CH; ++i) r[i] = div_rn_rcp(__fmul_rn(load_as_f32(v + i), gm[i]), denom, rcp);
+  store_chunk<TY>(y + e0, r, CH);
+}
+
 template <typename TX, typename TY, bool VEC>
 __global__ void __launch_bounds__(LANES) tree_rmsnorm_kernel(const TX* __restrict__ X, int64_t ldx,
                                                              const float* __restrict__ gamma, float eps,
@@ -116,69 +152,56 @@ __global__ void __launch_bounds__(LANES) tree_rmsnorm_kernel(const TX* __restric
   const TX* x = X + static_cast<int64_t>(blockIdx.x) * ldx;
   TY* y = Y + static_cast<int64_t>(blockIdx.x) * ldy;
   const int64_t nch = (cols + CH - 1) / CH;
+  const int64_t nfull = cols / CH;  // chunks with CH valid elements
   float acc = 0.0f;
   if constexpr (VEC) {
     uint4 cache[CACHE];
 #pragma unroll
     for (int k = 0; k < CACHE; ++k) {
       const int64_t c = threadIdx.x + static_cast<int64_t>(k) * LANES;
-      if (c < nch && c * CH + CH <= cols) cache[k] = *reinterpret_cast<const uint4*>(x + c * CH);
+      if (c < nfull) cache[k] = *reinterpret_cast<const uint4*>(x + c * CH);
     }
-    for (int64_t c = threadIdx.x, k = 0; c < nch; c += LANES, ++k) {
-      const int64_t e0 = c * CH;
-      if (e0 + CH <= cols) {
-        uint4 raw;
-        if (k < CACHE) {
+    // pass 1: lane fold over chunks l, l+256, ... (cached ones first, same order)
 #pragma unroll
-          for (int j = 0; j < CACHE; ++j)
-            if (j == k) raw = cache[j];
-        } else {
-          raw = *reinterpret_cast<const uint4*>(x + e0);
-        }
-        const TX* v = reinterpret_cast<const TX*>(&raw);
-#pragma unroll
-        for (int i = 0; i < CH; ++i) {
-          const float f = load_as_f32(v + i);
-          acc = __fmaf_rn(f, f, acc);
-        }
-      } else {
-        for (int64_t e = e0; e < cols; ++e) {
-          const float f = load_as_f32(x + e);
-          acc = __fmaf_rn(f, f, acc);
-        }
+    for (int k = 0; k < CACHE; ++k) {
+      const int64_t c = threadIdx.x + static_cast<int64_t>(k) * LANES;
+      if (c < nfull) acc = sumsq_chunk<TX>(cache[k], acc);
+    }
+    for (int64_t c = threadIdx.x + static_cast<int64_t>(CACHE) * LANES; c < nfull; c += LANES)
+      acc = sumsq_chunk<TX>(*reinterpret_cast<const uint4*>(x + c * CH), acc);
+    if (nfull < nch && threadIdx.x == nfull % LANES)  // ragged last chunk, in its lane's order
+      for (int64_t e = nfull * CH; e < cols; ++e) {
+        const float f = load_as_f32(x + e);
+        acc = __fmaf_rn(f, f, acc);
       }
-    }
     const float ss = block_tree_sum(acc, sh);
     const float ms = __fdiv_rn(ss, static_cast<float>(cols));
     const float denom = __fsqrt_rn(__fadd_rn(ms, eps));
+    const float rcp = __frcp_rn(denom);
     const bool yvec = (reinterpret_cast<uintptr_t>(y) & 15) == 0 && (reinterpret_cast<uintptr_t>(gamma) & 15) == 0;
-    for (int64_t c = threadIdx.x, k = 0; c < nch; c += LANES, ++k) {
-      const int64_t e0 = c * CH;
-      if (yvec && e0 + CH <= cols) {
-        uint4 raw;
-        if (k < CACHE) {
+    if (yvec) {
 #pragma unroll
-          for (int j = 0; j < CACHE; ++j)
-            if (j == k) raw = cache[j];
-        } else {
-          raw = *reinterpret_cast<const uint4*>(x + e0);
-        }
-        const TX* v = reinterpret_cast<const TX*>(&raw);
-        float gm[CH], r[CH];
-#pragma unroll
-        for (int i = 0; i < CH; i += 4) *reinterpret_cast<float4*>(gm + i) = *reinterpret_cast<const float4*>(gamma + e0 + i);
-#pragma unroll
-        for (int i = 0; i < CH; ++i) r[i] = __fdiv_rn(__fmul_rn(load_as_f32(v + i), gm[i]), denom);
-        store_chunk<TY>(y + e0, r, CH);
-      } else {
-        for (int64_t e = e0; e < e0 + CH && e < cols; ++e) {
-          const float r = __fdiv_rn(__fmul_rn(load_as_f32(x + e), gamma[e]), denom);
-          if constexpr (sizeof(TY) == 4)
-            y[e] = r;
-          else
-            y[e] = f32_to_bf16_bits(r);
-        }
+      for (int k = 0; k < CACHE; ++k) {
+        const int64_t c = threadIdx.x + static_cast<int64_t>(k) * LANES;
+        if (c < nfull) norm_chunk<TX, TY>(cache[k], gamma, c * CH, denom, rcp, y);
       }
+      for (int64_t c = threadIdx.x + static_cast<int64_t>(CACHE) * LANES; c < nfull; c += LANES)
+        norm_chunk<TX, TY>(*reinterpret_cast<const uint4*>(x + c * CH), gamma, c * CH, denom, rcp, y);
+    } else {
+      for (int64_t e = threadIdx.x; e < nfull * CH; e += LANES) {
+        const float r = div_rn_rcp(__fmul_rn(load_as_f32(x + e), gamma[e]), denom, rcp);
+        if constexpr (sizeof(TY) == 4)
+          y[e] = r;
+        else
+          y[e] = f32_to_bf16_bits(r);
+      }
+    }
+    for (int64_t e = nfull * CH + threadIdx.x; e < cols; e += LANES) {
+      const float r = div_rn_rcp(__fmul_rn(load_as_f32(x + e), gamma[e]), denom, rcp);
+      if constexpr (sizeof(TY) == 4)
+        y[e] = r;
+      else
+        y[e] = f32_to_bf16_bits(r);
     }
   } else {
     for (int64_t c = threadIdx.x; c < nch; c += LANES)
@@ -189,8 +212,9 @@ __global__ void __launch_bounds__(LANES) tree_rmsnorm_kernel(const TX* __restric
     const float ss = block_tree_sum(acc, sh);
     const float ms = __fdiv_rn(ss, static_cast<float>(cols));
     const float denom = __fsqrt_rn(__fadd_rn(ms, eps));
+    const float rcp = __frcp_rn(denom);
     for (int64_t e = threadIdx.x; e < cols; e += LANES) {
-      const float r = __fdiv_rn(__fmul_rn(load_as_f32(x + e), gamma[e]), denom);
+      const float r = div_rn_rcp(__fmul_rn(load_as_f32(x + e), gamma[e]), denom, rcp);
       if constexpr (sizeof(TY) == 4)
         y[e] = r;
       else
