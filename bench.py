@@ -129,6 +129,27 @@ class Clocks:
         return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": samples}
 
 
+def ev_time_flushed(fn, reps):
+    """Device time (ms) per call of fn, each call preceded by an L2 eviction that
+    READS 256 MB (no dirty lines left to write back inside the timed call)."""
+    import torch
+    flush = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+    sink = torch.empty((), device="cuda")
+    fn()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(reps):
+        torch.sum(flush, dim=0, out=sink)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        tot += a.elapsed_time(b)
+    del flush
+    return tot / reps
+
+
 def ev_time(fn, reps, stream=None):
     """Device time (ms) per call of fn with CUDA events on the current stream."""
     import torch
@@ -357,22 +378,20 @@ def run_tbik(args):
     # ---- M sweep (rank 0, N = 1) ----------------------------------------------------------------
     sweep = None
     if rank == 0 and world == 1 and not args.no_sweep:
-        sweep = {"M": [], "tbik_tc_tflops": [], "tbik_fma_tflops": [], "cublas_bf16_tflops": []}
+        sweep = {"M": [], "tbik_tc_tflops": [], "tbik_fma_tflops": [], "cublas_bf16_tflops": [],
+                 "timing": "per call, after a 256 MB read that evicts W (117 MB) from L2"}
         for m in (1, 16, 64, 256, 1024, 4096):
             xm = x[:m].contiguous()
             ym = torch.empty(m, N_OUT, device=dev)
             yc = torch.empty(m, N_OUT, device=dev, dtype=torch.bfloat16)
             f = 2.0 * m * N_OUT * K_FULL
             reps = 20 if m <= 1024 else 10
-            tb.tree_matmul(xm, w, cfg, tb.LEAF_TCGEN05, out=ym)
-            t_tc = ev_time(lambda: tb.tree_matmul(xm, w, cfg, tb.LEAF_TCGEN05, out=ym), reps)
+            t_tc = ev_time_flushed(lambda: tb.tree_matmul(xm, w, cfg, tb.LEAF_TCGEN05, out=ym), reps)
             if m <= 1024:
-                tb.tree_matmul(xm, w, cfg, tb.LEAF_FMA, out=ym)
-                t_fma = ev_time(lambda: tb.tree_matmul(xm, w, cfg, tb.LEAF_FMA, out=ym), max(reps // 4, 2))
+                t_fma = ev_time_flushed(lambda: tb.tree_matmul(xm, w, cfg, tb.LEAF_FMA, out=ym), max(reps // 4, 2))
             else:
                 t_fma = None
-            torch.matmul(xm, w, out=yc)
-            t_cb = ev_time(lambda: torch.matmul(xm, w, out=yc), reps)
+            t_cb = ev_time_flushed(lambda: torch.matmul(xm, w, out=yc), reps)
             sweep["M"].append(m)
             sweep["tbik_tc_tflops"].append(f / (t_tc * 1e-3) / 1e12)
             sweep["tbik_fma_tflops"].append(f / (t_fma * 1e-3) / 1e12 if t_fma else None)

@@ -236,6 +236,20 @@ TBIK_API tbik_status tbik_group_row_parallel_forward_hostio(tbik_group* g, const
                                                    int64_t c_max, int leaf_mode, int64_t chunk_rows,
                                                    void* stream);
 
+/* ---- the reference's TBIK matrix file (host only) ------------------------ */
+
+/* matrix_write (matrix.hpp:86, matrix.cpp:211-233): "TBIK", u16 version 1,
+ * u16 dtype (0 f32 / 1 bf16), u64 rows, u64 cols, little-endian row-major
+ * payload from the host buffer `data`.  TBIK_IO on open/short-write failure. */
+TBIK_API tbik_status tbik_matrix_write(const char* path, const void* data, int dtype, int64_t rows,
+                              int64_t cols);
+/* matrix_read (matrix.hpp:87, matrix.cpp:235-284) in two calls: the header,
+ * then the payload into a host buffer of capacity_bytes.  Errors as the
+ * reference: TBIK_IO, TBIK_TRUNCATED, TBIK_BAD_MAGIC, TBIK_UNKNOWN_DTYPE
+ * (unknown version or dtype code). */
+TBIK_API tbik_status tbik_matrix_read_header(const char* path, int* dtype, int64_t* rows, int64_t* cols);
+TBIK_API tbik_status tbik_matrix_read(const char* path, void* out, int64_t capacity_bytes);
+
 /* ---- tree-ordered reductions (NEW semantics) -------- */
 
 /* rmsnorm (demo.hpp:53, demo.cpp:11-34) with the sum of squares in the

@@ -165,6 +165,9 @@ TBIK_CPP_API std::uint64_t bit_diff_count(const Matrix& a, const Matrix& b);
 TBIK_CPP_API std::uint64_t bit_fingerprint(const Matrix& m);
 TBIK_CPP_API Matrix matrix_random_normal(Rng& rng, std::int64_t rows, std::int64_t cols, Dtype dtype,
                                          float mean, float stddev);
+// matrix.hpp:86-87: the TBIK file format (tbik_matrix_write / tbik_matrix_read).
+TBIK_CPP_API void matrix_write(const std::string& path, const Matrix& m);
+TBIK_CPP_API Matrix matrix_read(const std::string& path);
 
 // ---- matmul.hpp:18-53 ----------------------------------------------------------
 struct BlockConfig {

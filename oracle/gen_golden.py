@@ -29,6 +29,22 @@ def hexf(x) -> str:
     return "0x%08x" % int(np.float32(x).view(np.uint32))
 
 
+def write_tbik_io_case(r: RefLib) -> None:
+    """Golden I/O in the reference's own TBIK file format (matrix.cpp:211-233),
+    written by the reference's matrix_write: a ragged-K tree_matmul case
+    (K = 1000 -> 4 tiles of block_k 256, the last 232 wide) with its inputs and
+    the reference output; diffable byte for byte against a GPU run."""
+    d = os.path.join(os.path.dirname(OUT), "tbik_io")
+    os.makedirs(d, exist_ok=True)
+    a = r.random_normal(11, 1, 8, 1000, "bf16")
+    b = r.random_normal(11, 2, 1000, 64, "bf16")
+    c = r.tree_matmul(a, b, 256)
+    for name, m in (("a", a), ("b", b), ("c_tree", c)):
+        st = r.matrix_write(os.path.join(d, f"{name}.tbik"), m)
+        if st:
+            raise OracleError(f"ref_matrix_write failed: {st}")
+
+
 def main() -> None:
     r = RefLib()
     g: dict = {"generator": "oracle/gen_golden.py over oracle/_ref/libtbik_ref.so "
@@ -148,6 +164,8 @@ def main() -> None:
     g["theorem1_exhaustive"] = {"pass": ok, "failures": fails}
     ok, diffs = r.check_collective_symmetry(8, 8)
     g["collective_symmetry"] = {"pass": ok, "diffs": diffs}
+
+    write_tbik_io_case(r)
 
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     with open(OUT, "w") as f:

@@ -329,6 +329,8 @@ class RefLib(_Lib):
         L.ref_fma_witness.argtypes = [PF]
         L.ref_leaf_order_witness.restype = u64
         L.ref_leaf_order_witness.argtypes = [PF, PF, PF]
+        L.ref_matrix_write.argtypes = [C.c_char_p, vp, C.c_int, i64, i64]
+        L.ref_matrix_read.argtypes = [C.c_char_p, C.POINTER(C.c_int), PI64, PI64, vp, i64]
 
     @staticmethod
     def _cfg(block_m, block_k, block_n, k_first):
@@ -336,6 +338,23 @@ class RefLib(_Lib):
 
     def set_threads(self, n: int) -> None:
         self.lib.ref_set_threads(n)
+
+    def matrix_write(self, path, m) -> int:
+        """The reference's matrix_write (matrix.cpp:211-233); returns its status (0 ok,
+        1 + ErrorCode on TbikError)."""
+        r, c = m.shape
+        return int(self.lib.ref_matrix_write(os.fsencode(path), _p(m), _dt(m), r, c))
+
+    def matrix_read(self, path):
+        """The reference's matrix_read (matrix.cpp:235-284) -> (status, array or None)."""
+        dt, r, c = C.c_int(), C.c_int64(), C.c_int64()
+        st = int(self.lib.ref_matrix_read(os.fsencode(path), C.byref(dt), C.byref(r), C.byref(c), None, 0))
+        if st:
+            return st, None
+        out = np.empty((r.value, c.value), np.float32 if dt.value == 0 else np.uint16)
+        st = int(self.lib.ref_matrix_read(os.fsencode(path), C.byref(dt), C.byref(r), C.byref(c), _p(out),
+                                          out.nbytes))
+        return st, out
 
     def worker_count(self) -> int:
         return int(self.lib.ref_worker_count())

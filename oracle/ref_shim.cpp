@@ -308,4 +308,29 @@ std::uint64_t ref_leaf_order_witness(float a[8], float b[8], float out[2]) {
   return w.seed;
 }
 
+// matrix_write / matrix_read (matrix.hpp:86-87), unmodified reference code.
+int ref_matrix_write(const char* path, const void* data, int dtype, std::int64_t rows, std::int64_t cols) {
+  return guarded([&] { matrix_write(path, make_matrix(data, dtype, rows, cols)); });
+}
+
+// Reads a TBIK file with the reference; fills dims/dtype and copies the
+// payload when `out` is non-null (capacity in bytes).
+int ref_matrix_read(const char* path, int* dtype, std::int64_t* rows, std::int64_t* cols, void* out,
+                    std::int64_t capacity) {
+  return guarded([&] {
+    Matrix m = matrix_read(path);
+    *dtype = static_cast<int>(m.dtype());
+    *rows = m.rows();
+    *cols = m.cols();
+    if (!out) return;
+    if (m.dtype() == Dtype::F32) {
+      const auto& d = m.f32_data();
+      if (static_cast<std::int64_t>(d.size() * 4) <= capacity) std::memcpy(out, d.data(), d.size() * 4);
+    } else {
+      const auto& d = m.bf16_data();
+      if (static_cast<std::int64_t>(d.size() * 2) <= capacity) std::memcpy(out, d.data(), d.size() * 2);
+    }
+  });
+}
+
 }  // extern "C"

@@ -8,6 +8,7 @@ from ._lib import ErrorCode, TbikError, header_functions, lib  # noqa: F401
 from .api import (BF16, F32, LEAF_FMA, LEAF_TCGEN05, BlockConfig, DeviceGroup,  # noqa: F401
                   PeerGroup, ReductionPlan, ShardPlan, all_gather, column_parallel_forward,
                   default_block_config, device_available, launch_count, exchange_handles, log_softmax,
+                  matrix_read, matrix_write,
                   make_column_shard_plan, make_row_shard_plan, plan_blocks, ring_reduce_baseline,
                   rmsnorm, row_parallel_forward, sync, tree_all_reduce, tree_all_reduce_per_rank,
                   tree_matmul, tree_matmul_hostio, tree_matmul_leaves)

@@ -24,6 +24,7 @@ falls back to the CPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import List, Sequence
 
@@ -330,6 +331,30 @@ def log_softmax(logits, groups: int = 8, tp: int = 1, targets=None, full: bool =
         C.c_void_p(tg.data_ptr()) if tg is not None else None,
         C.c_void_p(tlp.data_ptr()) if tlp is not None else None, _stream()))
     return lse, lp, tlp
+
+
+# ---- the reference's TBIK matrix file -------------------------------------------------
+def matrix_write(path: str, m) -> None:
+    """matrix_write (matrix.hpp:86): m is a host (CPU) f32 or bf16 2-D tensor."""
+    torch = _torch()
+    if m.is_cuda:
+        raise TbikError(ErrorCode.BadArgument, "matrix_write: host tensor expected")
+    if m.dim() != 2 or m.dtype not in (torch.float32, torch.bfloat16):
+        raise TbikError(ErrorCode.UnknownDtype, "matrix_write: 2-D f32 or bf16 tensor expected")
+    c = m.contiguous()
+    check(lib.tbik_matrix_write(os.fsencode(path), C.c_void_p(c.data_ptr()), _dt(c), c.shape[0], c.shape[1]))
+
+
+def matrix_read(path: str):
+    """matrix_read (matrix.hpp:87): returns a host f32 or bf16 tensor."""
+    torch = _torch()
+    dt, rows, cols = C.c_int(), C.c_int64(), C.c_int64()
+    check(lib.tbik_matrix_read_header(os.fsencode(path), C.byref(dt), C.byref(rows), C.byref(cols)))
+    out = torch.empty((rows.value, cols.value), dtype=torch.float32 if dt.value == F32 else torch.bfloat16)
+    nbytes = out.numel() * out.element_size()
+    buf = out if nbytes else torch.empty(1, dtype=torch.uint8)
+    check(lib.tbik_matrix_read(os.fsencode(path), C.c_void_p(buf.data_ptr()), max(nbytes, 1)))
+    return out
 
 
 def sync() -> None:

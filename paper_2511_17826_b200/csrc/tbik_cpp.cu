@@ -321,4 +321,25 @@ Matrix rmsnorm(const Matrix& x, const std::vector<float>& gamma, float eps) {
   return download_f32(dy, x.rows(), x.cols());
 }
 
+void matrix_write(const std::string& path, const Matrix& m) {
+  check_status(tbik_matrix_write(path.c_str(), m.raw(), static_cast<int>(m.dtype()), m.rows(), m.cols()));
+}
+
+Matrix matrix_read(const std::string& path) {
+  int dt = 0;
+  std::int64_t rows = 0, cols = 0;
+  check_status(tbik_matrix_read_header(path.c_str(), &dt, &rows, &cols));
+  const std::size_t n = static_cast<std::size_t>(rows) * static_cast<std::size_t>(cols);
+  if (dt == TBIK_F32) {
+    std::vector<float> v(n ? n : 1);
+    check_status(tbik_matrix_read(path.c_str(), v.data(), static_cast<std::int64_t>(v.size() * 4)));
+    v.resize(n);
+    return Matrix::from_f32(rows, cols, std::move(v));
+  }
+  std::vector<std::uint16_t> v(n ? n : 1);
+  check_status(tbik_matrix_read(path.c_str(), v.data(), static_cast<std::int64_t>(v.size() * 2)));
+  v.resize(n);
+  return Matrix::from_bf16(rows, cols, std::move(v));
+}
+
 }  // namespace tbik

@@ -75,9 +75,19 @@ constexpr uint32_t IDESC = umma_idesc_bf16(PAIR_M, BN, /*a_mn_major=*/0, /*b_mn_
 // the carry that produces the output, and rewritten only 4+ groups later.
 constexpr int OUT_BUF_BYTES = 32 * 32 * 4;
 constexpr int L3_WARP_BYTES = 32 * 64 * 4;
-constexpr size_t smem_bytes(int epi, int nst) {
-  return 1024 + static_cast<size_t>(nst) * STAGE_BYTES + 1024 + static_cast<size_t>(epi) * L3_WARP_BYTES;
+// Small-M variants stage only ABOX (< 128) rows of A per stage: the MMA still reads
+// a 128-row A window, so consecutive stages' A windows overlap (stride ABOX x 128 B)
+// and rows >= ABOX of a window are another stage's bytes -- they only feed output
+// rows >= M, which are never stored.  The freed shared memory buys pipeline depth
+// for weight streaming (12 stages at ABOX = 32, 9 at 64, 6 at 128).
+constexpr int a_region_bytes(int abox, int nst) { return (nst - 1) * abox * 128 + A_STAGE_BYTES; }
+constexpr int stages_for(int abox) { return abox == 32 ? 12 : abox == 64 ? 9 : STAGES; }
+constexpr size_t smem_bytes(int epi, int abox) {
+  return 1024 + static_cast<size_t>(a_region_bytes(abox, stages_for(abox))) +
+         static_cast<size_t>(stages_for(abox)) * B_STAGE_BYTES + 1024 + static_cast<size_t>(epi) * L3_WARP_BYTES;
 }
+static_assert(smem_bytes(8, 32) <= 232448 && smem_bytes(8, 64) <= 232448 && smem_bytes(8, 128) <= 232448,
+              "shared memory budget");
 
 struct TcParams {
   int M, N, K;
@@ -199,24 +209,27 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// EPI merge warps (two per TMEM lane quarter, splitting the 128 columns), NST
-// pipeline stages.  KF1 (used when k_first == 1, where every leaf completes a
+// EPI merge warps (two per TMEM lane quarter, splitting the 128 columns), ABOX
+// A rows staged per stage (128, or 64 / 32 for small M; stage count follows).  KF1 (used when k_first == 1, where every leaf completes a
 // group and g need not persist across leaves): the level-1 slot is loaded in the
 // same batch as the leaf, so an odd leaf costs one TMEM round trip, not two.
-template <int EPI, bool KF1, int NST>
+template <int EPI, bool KF1, int ABOX>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
     tc_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const TcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + NST * A_STAGE_BYTES;
+  constexpr int NST = stages_for(ABOX);
+  constexpr int A_STRIDE = ABOX * 128;  // bytes between consecutive stages' A windows
+  constexpr uint32_t TX_BYTES = A_STRIDE + B_STAGE_BYTES;
+  uint8_t* sB = smem + a_region_bytes(ABOX, NST);
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + NST * B_STAGE_BYTES);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* sL3 = smem + NST * STAGE_BYTES + 1024;  // 1024-aligned level-3 / output staging
+  uint8_t* sL3 = sB + NST * B_STAGE_BYTES + 1024;  // 1024-aligned level-3 / output staging
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -261,11 +274,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             const uint32_t fb = full_leader0 + stage * 8;
             if (leader)
-              mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+              mbar_arrive_expect_tx(&full[stage], TX_BYTES);
             else
-              mbar_arrive_expect_tx_cluster(fb, STAGE_BYTES);
+              mbar_arrive_expect_tx_cluster(fb, TX_BYTES);
             const int k = t * p.bk + c * KSTAGE;
-            tma_load_2d_2sm(sA + stage * A_STAGE_BYTES, &tmA, fb, k, am);
+            tma_load_2d_2sm(sA + stage * A_STRIDE, &tmA, fb, k, am);
             tma_load_2d_2sm(sB + stage * B_STAGE_BYTES, &tmB, fb, bn, k);
             if (++stage == NST) {
               stage = 0;
@@ -294,7 +307,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
           for (int c = 0; c < nch; ++c) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            const uint32_t a_base = smem_u32(sA + stage * A_STAGE_BYTES);
+            const uint32_t a_base = smem_u32(sA + stage * A_STRIDE);
             const uint32_t b_base = smem_u32(sB + stage * B_STAGE_BYTES);
 #pragma unroll
             for (int kk = 0; kk < KSTAGE / 16; ++kk) {
@@ -633,9 +646,16 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   if (!tc_supported(v, &why)) return set_error(TBIK_UNSUPPORTED, why);
   if (o.mode == OUT_GROUPS) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: GROUPS mode is FMA-only");
   if (tc_use_wide(v)) return launch_tc_gemm_wide(v, o, s);
+  // A rows staged per stage: the fewest that still cover every row of the pair
+  // tile's leader CTA (TBIK_TC_ABOX overrides, a pure scheduling knob).
+  int abox = v.M <= 32 ? 32 : v.M <= 64 ? 64 : 128;
+  if (const char* e = std::getenv("TBIK_TC_ABOX")) {
+    const int a = std::atoi(e);
+    if ((a == 32 && v.M <= 32) || (a == 64 && v.M <= 64) || a == 128) abox = a;
+  }
   CUtensorMap mA, mB;
   TBIK_TRY(make_map_2d(&mA, v.A, static_cast<uint64_t>(v.K), static_cast<uint64_t>(v.M),
-                       static_cast<uint64_t>(v.lda) * 2, KSTAGE, BM));
+                       static_cast<uint64_t>(v.lda) * 2, KSTAGE, static_cast<uint32_t>(abox)));
   TBIK_TRY(make_map_2d(&mB, v.B, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.K),
                        static_cast<uint64_t>(v.ldb) * 2, BN / 2, KSTAGE));
   TcParams p{};
@@ -691,15 +711,18 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
     TBIK_TRY(make_map_out(&mC, o.out, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.M),
                           static_cast<uint64_t>(p.units), static_cast<uint64_t>(o.ldo) * 4, ustride * 4));
   void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams) =
-      kf1 ? tc_tree_gemm_kernel<8, true, STAGES> : tc_tree_gemm_kernel<8, false, STAGES>;
+      abox == 32 ? (kf1 ? tc_tree_gemm_kernel<8, true, 32> : tc_tree_gemm_kernel<8, false, 32>)
+      : abox == 64 ? (kf1 ? tc_tree_gemm_kernel<8, true, 64> : tc_tree_gemm_kernel<8, false, 64>)
+                   : (kf1 ? tc_tree_gemm_kernel<8, true, 128> : tc_tree_gemm_kernel<8, false, 128>);
   const int nthreads = 128 + 32 * 8;
-  const size_t smem = smem_bytes(8, STAGES);
-  static bool attr_set[16][2] = {};
+  const size_t smem = smem_bytes(8, abox);
+  const int vi = (abox == 32 ? 0 : abox == 64 ? 1 : 2) * 2 + (kf1 ? 1 : 0);
+  static bool attr_set[16][6] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 16 && !attr_set[dev][kf1]) {
+  if (dev >= 0 && dev < 16 && !attr_set[dev][vi]) {
     TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr_set[dev][kf1] = true;
+    attr_set[dev][vi] = true;
   }
   kern<<<grid, nthreads, smem, s>>>(mA, mB, mC, p);
   TBIK_CUDA(cudaGetLastError());

@@ -35,6 +35,34 @@ __device__ __forceinline__ float tb_exp(float x) {
   return __fmul_rn(y, __uint_as_float(static_cast<uint32_t>(k + 127) << 23));
 }
 
+// tb_exp for x in [-inf, 0] (no NaN): the same operation sequence as tb_exp, so
+// the same bits, with the branches turned into selects and the exponent taken
+// from the magic-number sum (t = magic + kf exactly, |kf| < 2^22) instead of a
+// float->int conversion.  Used on the log-softmax hot loop (x - max <= 0).
+__device__ __forceinline__ float tb_exp_nonpos(float x) {
+  const float magic = 12582912.0f;  // 0x4B400000
+  const float t = __fmaf_rn(x, 1.44269502162933349609f, magic);
+  const float kf = __fsub_rn(t, magic);
+  float r = __fmaf_rn(kf, -0.693359375f, x);
+  r = __fmaf_rn(kf, 2.12194440e-4f, r);
+  float p = 1.9875691500e-4f;
+  p = __fmaf_rn(p, r, 1.3981999507e-3f);
+  p = __fmaf_rn(p, r, 8.3334519073e-3f);
+  p = __fmaf_rn(p, r, 4.1665795894e-2f);
+  p = __fmaf_rn(p, r, 1.6666665459e-1f);
+  p = __fmaf_rn(p, r, 5.0000001201e-1f);
+  const float r2 = __fmul_rn(r, r);
+  float y = __fmaf_rn(p, r2, r);
+  y = __fadd_rn(y, 1.0f);
+  // k = t_bits - magic_bits; 2^k has bits (k + 127) << 23 = (t_bits << 23) + C (mod 2^32)
+  const uint32_t tb = __float_as_uint(t);
+  const bool tiny = kf < -125.0f;
+  y = __fmul_rn(y, tiny ? __uint_as_float(static_cast<uint32_t>(127 - 64) << 23) : 1.0f);  // *1 is exact
+  const uint32_t sc = (tb << 23) + ((127u - 0x4B400000u) << 23) + (tiny ? (64u << 23) : 0u);
+  const float res = __fmul_rn(y, __uint_as_float(sc));
+  return x < -103.0f ? 0.0f : res;
+}
+
 __device__ __forceinline__ float tb_log(float x) {
   if (!(x > 0.0f)) return x == 0.0f ? __int_as_float(0xFF800000) : __int_as_float(0x7FC00000);
   if (x == __int_as_float(0x7F800000)) return x;

@@ -32,8 +32,8 @@ __device__ __forceinline__ MS ms_merge(MS lo, MS hi) {
   if (lo.m == __int_as_float(0xFF800000)) return hi;
   if (hi.m == __int_as_float(0xFF800000)) return lo;
   const float m = lo.m >= hi.m ? lo.m : hi.m;
-  const float a = __fmul_rn(lo.s, tb_exp(__fsub_rn(lo.m, m)));
-  const float b = __fmul_rn(hi.s, tb_exp(__fsub_rn(hi.m, m)));
+  const float a = __fmul_rn(lo.s, tb_exp_nonpos(__fsub_rn(lo.m, m)));  // arguments <= 0
+  const float b = __fmul_rn(hi.s, tb_exp_nonpos(__fsub_rn(hi.m, m)));
   return MS{m, __fadd_rn(a, b)};
 }
 
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(LANES) tree_rmsnorm_kernel(const TX* __restric
 constexpr int MSB = 8;
 
 template <bool VEC>
-__global__ void __launch_bounds__(LANES) ms_group_kernel(const float* __restrict__ logits, int64_t ld, int64_t n,
+__global__ void __launch_bounds__(LANES, 4) ms_group_kernel(const float* __restrict__ logits, int64_t ld, int64_t n,
                                                          int64_t groups, MS* __restrict__ out) {
   __shared__ MS sh[9];
   const int64_t row = blockIdx.x, g = blockIdx.y;
@@ -240,36 +240,65 @@ __global__ void __launch_bounds__(LANES) ms_group_kernel(const float* __restrict
   const int64_t nch = (n + 3) / 4;
   const float NEG_INF = __int_as_float(0xFF800000);
   MS st{NEG_INF, 0.0f};
+  const int64_t nfull = n / 4;  // chunks holding 4 logits
   for (int64_t c0 = threadIdx.x; c0 < nch; c0 += static_cast<int64_t>(LANES) * MSB) {
     float v[MSB * 4];
-    int cnt[MSB];  // valid logits in each chunk (4, or fewer in the group's last chunk)
+    MS b{NEG_INF, 0.0f};
+    if (VEC && c0 + static_cast<int64_t>(MSB - 1) * LANES < nfull) {
+      // full block: MSB float4 loads, no guards
 #pragma unroll
-    for (int j = 0; j < MSB; ++j) {
-      const int64_t c = c0 + static_cast<int64_t>(j) * LANES;
-      const int64_t e0 = c * 4;
-      cnt[j] = c < nch ? (n - e0 < 4 ? static_cast<int>(n - e0) : 4) : 0;
-      if (VEC && cnt[j] == 4) {
-        const float4 q = *reinterpret_cast<const float4*>(x + e0);
+      for (int j = 0; j < MSB; ++j) {
+        const float4 q = *reinterpret_cast<const float4*>(x + (c0 + static_cast<int64_t>(j) * LANES) * 4);
         v[4 * j] = q.x;
         v[4 * j + 1] = q.y;
         v[4 * j + 2] = q.z;
         v[4 * j + 3] = q.w;
-      } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) v[4 * j + i] = i < cnt[j] ? x[e0 + i] : NEG_INF;
       }
-    }
-    float m = v[0];  // chunk c0 < nch always holds >= 1 logit
+      // canonical max: sequential m = x > m ? x : m.  fmaxf gives the same bits
+      // unless the maximum is a zero (only its sign is ambiguous): redo those.
+      float m = v[0];
 #pragma unroll
-    for (int k = 1; k < MSB * 4; ++k)
-      if (k % 4 < cnt[k / 4]) m = v[k] > m ? v[k] : m;
-    MS b{NEG_INF, 0.0f};
-    if (m != NEG_INF) {
-      float sum = 0.0f;
+      for (int k = 1; k < MSB * 4; ++k) m = fmaxf(m, v[k]);
+      if (m == 0.0f) {
+        m = v[0];
 #pragma unroll
-      for (int k = 0; k < MSB * 4; ++k)
-        if (k % 4 < cnt[k / 4]) sum = __fadd_rn(sum, tb_exp(__fsub_rn(v[k], m)));
-      b = MS{m, sum};
+        for (int k = 1; k < MSB * 4; ++k) m = v[k] > m ? v[k] : m;
+      }
+      if (m != NEG_INF) {
+        float sum = 0.0f;
+#pragma unroll
+        for (int k = 0; k < MSB * 4; ++k) sum = __fadd_rn(sum, tb_exp_nonpos(__fsub_rn(v[k], m)));
+        b = MS{m, sum};
+      }
+    } else {
+      int cnt[MSB];  // valid logits in each chunk (4, or fewer in the group's last chunk)
+#pragma unroll
+      for (int j = 0; j < MSB; ++j) {
+        const int64_t c = c0 + static_cast<int64_t>(j) * LANES;
+        const int64_t e0 = c * 4;
+        cnt[j] = c < nch ? (n - e0 < 4 ? static_cast<int>(n - e0) : 4) : 0;
+        if (VEC && cnt[j] == 4) {
+          const float4 q = *reinterpret_cast<const float4*>(x + e0);
+          v[4 * j] = q.x;
+          v[4 * j + 1] = q.y;
+          v[4 * j + 2] = q.z;
+          v[4 * j + 3] = q.w;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[4 * j + i] = i < cnt[j] ? x[e0 + i] : NEG_INF;
+        }
+      }
+      float m = v[0];  // chunk c0 < nch always holds >= 1 logit
+#pragma unroll
+      for (int k = 1; k < MSB * 4; ++k)
+        if (k % 4 < cnt[k / 4]) m = v[k] > m ? v[k] : m;
+      if (m != NEG_INF) {
+        float sum = 0.0f;
+#pragma unroll
+        for (int k = 0; k < MSB * 4; ++k)
+          if (k % 4 < cnt[k / 4]) sum = __fadd_rn(sum, tb_exp_nonpos(__fsub_rn(v[k], m)));
+        b = MS{m, sum};
+      }
     }
     st = ms_merge(st, b);
   }

@@ -321,3 +321,23 @@ def test_hostio_rejects_device_activations(tb, cuda):
     w = torch.zeros(256, 64, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(tb.TbikError):
         tb.tree_matmul_hostio(torch.zeros(4, 256, dtype=torch.bfloat16, device="cuda"), w)
+
+
+def test_tbik_file_golden_case(tb, cuda):
+    """Golden I/O in the reference's TBIK file format (tests/golden/tbik_io, written
+    by the reference's matrix_write): the exact-leaf GPU GEMM reproduces the stored
+    reference output bit for bit, and the GPU result written back with
+    tbik_matrix_write is byte-identical to the reference's file."""
+    import os
+    d = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "tbik_io")
+    a = tb.matrix_read(os.path.join(d, "a.tbik"))
+    b = tb.matrix_read(os.path.join(d, "b.tbik"))
+    c = tb.matrix_read(os.path.join(d, "c_tree.tbik"))
+    y = tb.tree_matmul(a.cuda(), b.cuda(), tb.BlockConfig(64, 256, 128, 0), tb.LEAF_FMA).cpu()
+    assert torch.equal(y.view(torch.int32), c.view(torch.int32))
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        p = os.path.join(td, "y.tbik")
+        tb.matrix_write(p, y)
+        with open(p, "rb") as f1, open(os.path.join(d, "c_tree.tbik"), "rb") as f2:
+            assert f1.read() == f2.read()
