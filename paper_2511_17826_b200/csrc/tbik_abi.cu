@@ -147,14 +147,17 @@ size_t dsize(int dt) { return dt == TBIK_BF16 ? 2 : 4; }
 tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mode, cudaStream_t s) {
   const size_t slice = static_cast<size_t>(v.M) * v.N;
   if (leaf_mode == TBIK_LEAF_TCGEN05) {
-    const int64_t tiles_mn = tc_pair_tiles(v);
+    const int64_t tiles_mn = tc_tiles(v);
     // Split the K range of each output tile into 2^j aligned subtrees only when
     // the machine would otherwise idle; the combine continues the same tree
     // (Theorem 1), so the split never changes bits.  Measured on B200
-    // (tools/tune_units.py, K=14336 N=4096): a split only pays below 64 pair
-    // tiles, and then only by 2 (deeper splits lose to the extra subtree
-    // traffic and the per-item pipeline refill).
-    int64_t units = tiles_mn >= 64 ? 1 : std::min<int64_t>(v.L, 2);
+    // (tools/tune_units.py, tools/tune_small.py, K=14336 N=4096): split until the
+    // work items fill ~7/8 of the concurrent slots (74 CTA pairs / 148 CTAs) and
+    // no further (2 for 32 pair tiles, 4 for 32 single-CTA tiles); deeper splits
+    // lose to the extra subtree traffic and the per-item pipeline refill.
+    const int64_t enough = tc_parallel_slots(v) * 7 / 8;
+    int64_t units = 1;
+    while (units * 2 <= v.L && tiles_mn * units * 2 <= enough) units *= 2;
     (void)next_pow2;
     if (const char* e = std::getenv("TBIK_TC_UNITS")) {  // tuning override (power of two <= leaves)
       const int64_t u = std::atoll(e);

@@ -68,6 +68,7 @@ constexpr int SLOT_LVL1 = 256;
 constexpr int SLOT_LVL2 = 384;
 constexpr int GROUP_M = 8;  // raster: M-blocks that share one pass over W
 constexpr uint32_t IDESC = umma_idesc_bf16(PAIR_M, BN, /*a_mn_major=*/0, /*b_mn_major=*/1);
+constexpr uint32_t IDESC_1CTA = umma_idesc_bf16(BM, BN, /*a_mn_major=*/0, /*b_mn_major=*/1);
 // Tree level 3 lives in shared memory: per merge warp an 8 KB region holding its
 // 32 rows x 64 columns as [16 float4 columns][32 lanes][float4] (conflict-free
 // 16-byte accesses).  The same region doubles as the warp's output staging for
@@ -80,13 +81,23 @@ constexpr int L3_WARP_BYTES = 32 * 64 * 4;
 // and rows >= ABOX of a window are another stage's bytes -- they only feed output
 // rows >= M, which are never stored.  The freed shared memory buys pipeline depth
 // for weight streaming (12 stages at ABOX = 32, 9 at 64, 6 at 128).
+// Single-CTA variants (PAIR = false, for M <= 128): a CTA owns a 128 x 128 tile
+// alone (tcgen05.mma.cta_group::1, M = 128) and stages all 128 columns of B (two
+// 64-column atoms) -- half the MMA work per weight column of the pair tile, whose
+// second 128 rows would be padding at small M.
+constexpr int b_stage_bytes(bool pair) { return pair ? B_STAGE_BYTES : 2 * B_STAGE_BYTES; }
 constexpr int a_region_bytes(int abox, int nst) { return (nst - 1) * abox * 128 + A_STAGE_BYTES; }
-constexpr int stages_for(int abox) { return abox == 32 ? 12 : abox == 64 ? 9 : STAGES; }
-constexpr size_t smem_bytes(int epi, int abox) {
-  return 1024 + static_cast<size_t>(a_region_bytes(abox, stages_for(abox))) +
-         static_cast<size_t>(stages_for(abox)) * B_STAGE_BYTES + 1024 + static_cast<size_t>(epi) * L3_WARP_BYTES;
+constexpr int stages_for(int abox, bool pair) {
+  return pair ? (abox == 32 ? 12 : abox == 64 ? 9 : STAGES) : (abox == 32 ? 7 : abox == 64 ? 6 : 4);
 }
-static_assert(smem_bytes(8, 32) <= 232448 && smem_bytes(8, 64) <= 232448 && smem_bytes(8, 128) <= 232448,
+constexpr size_t smem_bytes(int epi, int abox, bool pair) {
+  return 1024 + static_cast<size_t>(a_region_bytes(abox, stages_for(abox, pair))) +
+         static_cast<size_t>(stages_for(abox, pair)) * b_stage_bytes(pair) + 1024 +
+         static_cast<size_t>(epi) * L3_WARP_BYTES;
+}
+static_assert(smem_bytes(8, 32, true) <= 232448 && smem_bytes(8, 64, true) <= 232448 &&
+                  smem_bytes(8, 128, true) <= 232448 && smem_bytes(8, 32, false) <= 232448 &&
+                  smem_bytes(8, 64, false) <= 232448 && smem_bytes(8, 128, false) <= 232448,
               "shared memory budget");
 
 struct TcParams {
@@ -97,6 +108,7 @@ struct TcParams {
   int mode;    // OUT_FULL / OUT_UNITS / OUT_LEAVES
   int levels;  // log2(groups per unit)
   int mblocks, ntiles;
+  int tile_m;  // rows per work item: 256 (CTA pair) or 128 (single CTA)
   long long items;
   float* out;
   long long ldo;
@@ -181,7 +193,7 @@ __device__ __forceinline__ Item decode(const TcParams& p, long long item) {
   const int gm = min(GROUP_M, p.mblocks - g * GROUP_M);
   const int mb = g * GROUP_M + idx % gm;
   const int nt = idx / gm;
-  it.m0 = mb * PAIR_M;
+  it.m0 = mb * p.tile_m;
   it.n0 = nt * BN;
   it.t_begin = it.unit * p.tiles_per_unit;
   it.t_end = min(p.T, it.t_begin + p.tiles_per_unit);
@@ -213,45 +225,51 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // A rows staged per stage (128, or 64 / 32 for small M; stage count follows).  KF1 (used when k_first == 1, where every leaf completes a
 // group and g need not persist across leaves): the level-1 slot is loaded in the
 // same batch as the leaf, so an odd leaf costs one TMEM round trip, not two.
-template <int EPI, bool KF1, int ABOX>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
+template <int EPI, bool KF1, int ABOX, bool PAIR>
+__global__ void __launch_bounds__(128 + 32 * EPI, 1)
     tc_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const TcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  constexpr int NST = stages_for(ABOX);
+  constexpr int NST = stages_for(ABOX, PAIR);
   constexpr int A_STRIDE = ABOX * 128;  // bytes between consecutive stages' A windows
-  constexpr uint32_t TX_BYTES = A_STRIDE + B_STAGE_BYTES;
+  constexpr int B_STAGE = b_stage_bytes(PAIR);
+  constexpr uint32_t TX_BYTES = A_STRIDE + B_STAGE;
   uint8_t* sB = smem + a_region_bytes(ABOX, NST);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + NST * B_STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + NST * B_STAGE);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* sL3 = sB + NST * B_STAGE_BYTES + 1024;  // 1024-aligned level-3 / output staging
+  uint8_t* sL3 = sB + NST * B_STAGE + 1024;  // 1024-aligned level-3 / output staging
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
+  const uint32_t rank = PAIR ? cluster_rank() : 0;
   const bool leader = rank == 0;
-  const long long pair = blockIdx.x >> 1;
-  const long long npairs = gridDim.x >> 1;
+  const long long pair = PAIR ? blockIdx.x >> 1 : blockIdx.x;  // work-item stream of this pair / CTA
+  const long long npairs = PAIR ? gridDim.x >> 1 : gridDim.x;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < NST; ++s) {
-      mbar_init(&full[s], 2);   // one arrive.expect_tx from each CTA of the pair (leader's copy used)
+      mbar_init(&full[s], PAIR ? 2 : 1);  // one arrive.expect_tx per CTA (leader's copy used)
       mbar_init(&empty[s], 1);  // one multicast commit from the leader's MMA thread
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);   // multicast commit
-      mbar_init(&tempty[b], 2 * EPI);  // EPI merge warps x 2 CTAs (leader's copy used)
+      mbar_init(&tempty[b], PAIR ? 2 * EPI : EPI);  // EPI merge warps per CTA (leader's copy used)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc_2cta(tmem_slot, TMEM_COLS);
+  if (warp == 2) {
+    if constexpr (PAIR)
+      tmem_alloc_2cta(tmem_slot, TMEM_COLS);
+    else
+      tmem_alloc(tmem_slot, TMEM_COLS);
+  }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -278,8 +296,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
             else
               mbar_arrive_expect_tx_cluster(fb, TX_BYTES);
             const int k = t * p.bk + c * KSTAGE;
-            tma_load_2d_2sm(sA + stage * A_STRIDE, &tmA, fb, k, am);
-            tma_load_2d_2sm(sB + stage * B_STAGE_BYTES, &tmB, fb, bn, k);
+            if constexpr (PAIR) {
+              tma_load_2d_2sm(sA + stage * A_STRIDE, &tmA, fb, k, am);
+              tma_load_2d_2sm(sB + stage * B_STAGE, &tmB, fb, bn, k);
+            } else {  // all 128 columns: two 64-column atoms
+              tma_load_2d(sA + stage * A_STRIDE, &tmA, &full[stage], k, am);
+              tma_load_2d(sB + stage * B_STAGE, &tmB, &full[stage], bn, k);
+              tma_load_2d(sB + stage * B_STAGE + B_STAGE_BYTES, &tmB, &full[stage], bn + BN / 2, k);
+            }
             if (++stage == NST) {
               stage = 0;
               phase ^= 1;
@@ -308,23 +332,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t a_base = smem_u32(sA + stage * A_STRIDE);
-            const uint32_t b_base = smem_u32(sB + stage * B_STAGE_BYTES);
+            const uint32_t b_base = smem_u32(sB + stage * B_STAGE);
 #pragma unroll
             for (int kk = 0; kk < KSTAGE / 16; ++kk) {
               // A: K-major SW128, +32 B per 16-element K step inside the 128 B atom.
               const uint64_t adesc = umma_desc_sw128(a_base + kk * 32, 16, 1024);
-              // B: MN-major SW128, one 64-column atom per CTA; 8-row K groups 1 KB
-              // apart (SBO); +16 K rows (2 KB) per step.
+              // B: MN-major SW128, 64-column atoms 8 KB apart (LBO; one atom per CTA
+              // in a pair, two in a single CTA); 8-row K groups 1 KB apart (SBO);
+              // +16 K rows (2 KB) per step.
               const uint64_t bdesc = umma_desc_sw128(b_base + kk * 2048, B_STAGE_BYTES, 1024);
-              umma_bf16_2cta(d, adesc, bdesc, IDESC, (c | kk) != 0 ? 1u : 0u);
+              if constexpr (PAIR)
+                umma_bf16_2cta(d, adesc, bdesc, IDESC, (c | kk) != 0 ? 1u : 0u);
+              else
+                umma_bf16(d, adesc, bdesc, IDESC_1CTA, (c | kk) != 0 ? 1u : 0u);
             }
-            umma_commit_2cta(&empty[stage], 0x3);
+            if constexpr (PAIR)
+              umma_commit_2cta(&empty[stage], 0x3);
+            else
+              umma_commit(&empty[stage]);
             if (++stage == NST) {
               stage = 0;
               phase ^= 1;
             }
           }
-          umma_commit_2cta(&tfull[buf], 0x3);
+          if constexpr (PAIR)
+            umma_commit_2cta(&tfull[buf], 0x3);
+          else
+            umma_commit(&tfull[buf]);
         }
       }
     }
@@ -544,7 +578,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * EPI, 1)
   cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc_2cta(tmem_base, TMEM_COLS);
+    if constexpr (PAIR)
+      tmem_dealloc_2cta(tmem_base, TMEM_COLS);
+    else
+      tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
@@ -625,9 +662,25 @@ bool tc_supported(const GemmView& v, std::string* why) {
 }
 
 bool tc_use_wide(const GemmView& v);
+// Single-CTA 128 x 128 tiles when every row fits one CTA (M <= 128): the pair
+// tile's second 128 rows would be MMA work on padding.  TBIK_TC_PAIR=0/1 forces
+// the choice (a pure scheduling knob: same bits).
+bool tc_use_pair(const GemmView& v) {
+  if (const char* e = std::getenv("TBIK_TC_PAIR"))
+    if (*e) return std::atoi(e) != 0;
+  return v.M > BM;
+}
+
 int64_t tc_pair_tiles(const GemmView& v) {
   if (tc_use_wide(v)) return tc_wide_pair_tiles(v);
   return ((v.M + PAIR_M - 1) / PAIR_M) * ((v.N + BN - 1) / BN);
+}
+
+int64_t tc_parallel_slots(const GemmView& v) { return tc_use_pair(v) && !tc_use_wide(v) ? sm_count() / 2 : sm_count(); }
+
+int64_t tc_tiles(const GemmView& v) {
+  if (tc_use_wide(v) || tc_use_pair(v)) return tc_pair_tiles(v);
+  return ((v.M + BM - 1) / BM) * ((v.N + BN - 1) / BN);
 }
 
 // Diagnostics build only (see tools/tc_stats.py); the production kernel carries no counters.
@@ -689,12 +742,14 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
     return e ? std::atoi(e) : 0;
   }();
   p.debug = dbg;
-  p.mblocks = static_cast<int>((v.M + PAIR_M - 1) / PAIR_M);
+  const bool pair = tc_use_pair(v);
+  p.tile_m = pair ? PAIR_M : BM;
+  p.mblocks = static_cast<int>((v.M + p.tile_m - 1) / p.tile_m);
   p.ntiles = static_cast<int>((v.N + BN - 1) / BN);
   p.items = static_cast<long long>(p.mblocks) * p.ntiles * p.units;
-  const long long max_pairs = sm_count() / 2;
-  const long long npairs = p.items < max_pairs ? p.items : max_pairs;
-  dim3 grid(static_cast<unsigned>(2 * npairs));
+  const long long slots = pair ? sm_count() / 2 : sm_count();
+  const long long nstreams = p.items < slots ? p.items : slots;
+  dim3 grid(static_cast<unsigned>(pair ? 2 * nstreams : nstreams));
   const bool kf1 = p.kf == 1;
   if (p.levels > 3) {
     const size_t n = static_cast<size_t>(grid.x) * (p.levels - 3) * BM * BN;
@@ -710,22 +765,39 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   if (p.tma_store)
     TBIK_TRY(make_map_out(&mC, o.out, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.M),
                           static_cast<uint64_t>(p.units), static_cast<uint64_t>(o.ldo) * 4, ustride * 4));
-  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams) =
-      abox == 32 ? (kf1 ? tc_tree_gemm_kernel<8, true, 32> : tc_tree_gemm_kernel<8, false, 32>)
-      : abox == 64 ? (kf1 ? tc_tree_gemm_kernel<8, true, 64> : tc_tree_gemm_kernel<8, false, 64>)
-                   : (kf1 ? tc_tree_gemm_kernel<8, true, 128> : tc_tree_gemm_kernel<8, false, 128>);
+  using Kern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
+  static const Kern table[2][3][2] = {
+      {{tc_tree_gemm_kernel<8, false, 32, false>, tc_tree_gemm_kernel<8, true, 32, false>},
+       {tc_tree_gemm_kernel<8, false, 64, false>, tc_tree_gemm_kernel<8, true, 64, false>},
+       {tc_tree_gemm_kernel<8, false, 128, false>, tc_tree_gemm_kernel<8, true, 128, false>}},
+      {{tc_tree_gemm_kernel<8, false, 32, true>, tc_tree_gemm_kernel<8, true, 32, true>},
+       {tc_tree_gemm_kernel<8, false, 64, true>, tc_tree_gemm_kernel<8, true, 64, true>},
+       {tc_tree_gemm_kernel<8, false, 128, true>, tc_tree_gemm_kernel<8, true, 128, true>}}};
+  const int ai = abox == 32 ? 0 : abox == 64 ? 1 : 2;
+  const Kern kern = table[pair][ai][kf1];
   const int nthreads = 128 + 32 * 8;
-  const size_t smem = smem_bytes(8, abox);
-  const int vi = (abox == 32 ? 0 : abox == 64 ? 1 : 2) * 2 + (kf1 ? 1 : 0);
-  static bool attr_set[16][6] = {};
+  const size_t smem = smem_bytes(8, abox, pair);
+  static bool attr_set[16][2][3][2] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 16 && !attr_set[dev][vi]) {
+  if (dev >= 0 && dev < 16 && !attr_set[dev][pair][ai][kf1]) {
     TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr_set[dev][vi] = true;
+    if (pair) TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+    attr_set[dev][pair][ai][kf1] = true;
   }
-  kern<<<grid, nthreads, smem, s>>>(mA, mB, mC, p);
-  TBIK_CUDA(cudaGetLastError());
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = dim3(nthreads);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = pair ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  TBIK_CUDA(cudaLaunchKernelEx(&lc, kern, mA, mB, mC, p));
   count_launch();
   return TBIK_OK;
 }

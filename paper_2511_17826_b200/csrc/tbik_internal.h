@@ -50,6 +50,10 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s);
 bool tc_supported(const GemmView& v, std::string* why);
 // Output tiles of the tcgen05 kernel (one per CTA pair): 256 rows x 128 columns.
 int64_t tc_pair_tiles(const GemmView& v);
+// Work tiles of the variant launch_tc_gemm picks for v (pair 256 x 128 or single
+// CTA 128 x 128) and how many run concurrently (CTA pairs or CTAs).
+int64_t tc_tiles(const GemmView& v);
+int64_t tc_parallel_slots(const GemmView& v);
 // The 256 x 256 pair-tile variant (tbik_gemm_tc_wide.cu).
 tbik_status launch_tc_gemm_wide(const GemmView& v, const GemmOut& o, cudaStream_t s);
 int64_t tc_wide_pair_tiles(const GemmView& v);

@@ -237,3 +237,26 @@ class TbikDecoder:
     def log_probs(self, logits, tp: int = 1, targets=None, full: bool = True):
         """Vocab-sharded tree log-softmax over `tp` simulated vocab shards."""
         return api.log_softmax(logits, self.cfg.vocab_groups, tp, targets, full)
+
+    # -- CUDA graphs -------------------------------------------------------------------
+    def capture(self, tokens, tp: int = 1, full_logprobs: bool = True):
+        """Capture one forward + log-softmax over the static token tensor `tokens`
+        into a CUDA graph (no per-launch host cost on replay; bits unchanged).
+        Returns (graph, (logits, lse, logprobs)); refill `tokens` in place and call
+        graph.replay().  Two eager warm-up passes size the library's workspaces
+        first, so nothing is allocated inside the capture; a later call that grows
+        a workspace (a larger shape) invalidates the graph."""
+        import torch
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                logits = self.forward(tokens, tp)
+                self.log_probs(logits, tp, full=full_logprobs)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            logits = self.forward(tokens, tp)
+            lse, lp, _ = self.log_probs(logits, tp, full=full_logprobs)
+        return graph, (logits, lse, lp)

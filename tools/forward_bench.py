@@ -95,6 +95,13 @@ def run(model="llama3.1-8b", layers=0, batch=4, seq=256, reps=3, tps=(1, 2, 4, 8
         return dec.log_probs(logits, 1, full=True)
 
     ms = timeit(tbik_step, reps)
+    graph, (g_logits, _, _) = dec.capture(tokens, 1, True)
+    ms_graph = timeit(graph.replay, reps)
+    eager_logits = dec.forward(tokens, 1)
+    graph.replay()
+    torch.cuda.synchronize()
+    graph_same = bool(torch.equal(eager_logits.view(torch.int32), g_logits.view(torch.int32)))
+    del graph, g_logits, eager_logits
     l0 = tb.launch_count()
     tbik_step()
     torch.cuda.synchronize()
@@ -117,6 +124,8 @@ def run(model="llama3.1-8b", layers=0, batch=4, seq=256, reps=3, tps=(1, 2, 4, 8
         "model": cfg.name, "layers": cfg.n_layers, "batch": batch, "seq": seq, "tokens": M,
         "data": "synthetic: random-init N(0, 0.02) bf16 weights, uniform random token ids",
         "tbik_ms": ms, "tbik_tokens_per_s": M / (ms * 1e-3),
+        "tbik_graph_ms": ms_graph, "tbik_graph_tokens_per_s": M / (ms_graph * 1e-3),
+        "graph_bit_identical_to_eager": graph_same,
         "noninvariant_ms": base_ms, "noninvariant_tokens_per_s": M / (base_ms * 1e-3),
         "noninvariant_path": "cuBLAS bf16 GEMMs + PyTorch SDPA + torch norms/softmax, same weights",
         "tbik_over_noninvariant": base_ms / ms,

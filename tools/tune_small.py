@@ -38,17 +38,22 @@ for M in (int(a) for a in (sys.argv[1:] or ["1", "16", "32", "64", "128", "256"]
     x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     y = torch.empty(M, N, device="cuda")
     ref = None
-    for abox in ("32", "64", "128"):
-        if int(abox) < M and abox != "128":
+    for pair in ("0", "1"):
+        if pair == "0" and M > 128:
             continue
-        for u in ("1", "2", "4", "8"):
-            os.environ["TBIK_TC_ABOX"] = abox
-            os.environ["TBIK_TC_UNITS"] = u
-            ms = timed(lambda: tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05, out=y))
-            ref = y.clone() if ref is None else ref
-            same = torch.equal(ref.view(torch.int32), y.view(torch.int32))
-            print(f"M={M} abox={abox} units={u}: {ms*1e3:8.1f} us {2*M*N*K/ms/1e9:7.1f} TFLOP/s "
-                  f"W-stream {2*K*N/ms/1e6:6.0f} GB/s bits_equal={same}", flush=True)
+        for abox in ("32", "64", "128"):
+            if int(abox) < M and abox != "128":
+                continue
+            for u in ("1", "2", "4"):
+                os.environ["TBIK_TC_PAIR"] = pair
+                os.environ["TBIK_TC_ABOX"] = abox
+                os.environ["TBIK_TC_UNITS"] = u
+                ms = timed(lambda: tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05, out=y))
+                ref = y.clone() if ref is None else ref
+                same = torch.equal(ref.view(torch.int32), y.view(torch.int32))
+                print(f"M={M} pair={pair} abox={abox} units={u}: {ms*1e3:8.1f} us {2*M*N*K/ms/1e9:7.1f} TFLOP/s "
+                      f"W-stream {2*K*N/ms/1e6:6.0f} GB/s bits_equal={same}", flush=True)
+    os.environ.pop("TBIK_TC_PAIR")
     os.environ.pop("TBIK_TC_UNITS")
     os.environ.pop("TBIK_TC_ABOX")
     yb = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
