@@ -403,13 +403,20 @@ def run_tbik(args):
         del w, x, x_full, y, yb, x_host, y_host
         torch.cuda.empty_cache()
         from tools.forward_bench import run as forward_run
-        forward = forward_run("llama3.1-8b", 32, 4, 256, reps=3, tps=(1, 2, 4, 8))
+        try:
+            forward = forward_run("llama3.1-8b", 32, 4, 256, reps=3, tps=(1, 2, 4, 8))
+        except Exception as e:  # noqa: BLE001 -- the headline line must still print
+            forward = {"error": f"{type(e).__name__}: {e}"[:300]}
+            torch.cuda.synchronize()
 
     rowops = None
     if rank == 0 and world == 1 and not args.no_forward:
         torch.cuda.empty_cache()
         from tools.rowops_bench import run as rowops_run
-        rowops = rowops_run(reps=10, tps=(1, 8))
+        try:
+            rowops = rowops_run(reps=10, tps=(1, 8))
+        except Exception as e:  # noqa: BLE001
+            rowops = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -26,8 +26,9 @@ __global__ void embed_kernel(const uint16_t* __restrict__ table, int64_t H, cons
                              int64_t V, uint16_t* __restrict__ out, int* __restrict__ bad) {
   const int64_t row = blockIdx.x;
   const int64_t id = ids[row];
-  if (id < 0 || id >= V) {
+  if (id < 0 || id >= V) {  // flagged; the row is zeroed so the output stays defined
     if (threadIdx.x == 0) *bad = 1;
+    for (int64_t j = threadIdx.x; j < H; j += blockDim.x) out[row * H + j] = 0;
     return;
   }
   const uint16_t* src = table + id * H;
@@ -325,6 +326,13 @@ tbik_status tbik_embedding(const void* table, int64_t V, int64_t H, const int64_
                                                            static_cast<uint16_t*>(out), bad);
   TBIK_CUDA(cudaGetLastError());
   count_launch();
+  // Out-of-range ids are reported synchronously (BadArgument) on an eager stream;
+  // inside CUDA-graph capture no host sync is possible, so the check is skipped
+  // (the kernel zeroes the row of such an id) -- callers validate ids before
+  // capturing.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  TBIK_CUDA(cudaStreamIsCapturing(s, &cap));
+  if (cap != cudaStreamCaptureStatusNone) return TBIK_OK;
   int hbad = 0;
   TBIK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   TBIK_CUDA(cudaStreamSynchronize(s));
