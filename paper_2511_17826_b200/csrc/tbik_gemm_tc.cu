@@ -636,16 +636,27 @@ tbik_status make_map_out(CUtensorMap* map, float* base, uint64_t n, uint64_t m, 
   return TBIK_OK;
 }
 
+thread_local int g_sm_cap = 0;  // set_tc_sm_cap: leave SMs free for a concurrent kernel
+
 int sm_count() {
   static int n[16] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 16) return 148;
-  if (!n[dev]) cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
-  return n[dev] ? n[dev] : 148;
+  int sms = 148;
+  if (dev >= 0 && dev < 16) {
+    if (!n[dev]) cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (n[dev]) sms = n[dev];
+  }
+  return g_sm_cap > 0 && g_sm_cap < sms ? (g_sm_cap & ~1) : sms;
 }
 
 }  // namespace
+
+int set_tc_sm_cap(int cap) {
+  const int old = g_sm_cap;
+  g_sm_cap = cap;
+  return old;
+}
 
 bool tc_supported(const GemmView& v, std::string* why) {
   auto no = [&](const char* w) {

@@ -45,6 +45,10 @@ struct tbik_group {
   char* peer_region[tbik_b200::kMaxRanks] = {};
   bool opened[tbik_b200::kMaxRanks] = {};
   uint32_t epoch = 0;
+  // GEMM / all-reduce overlap (tbik_group_row_parallel_forward): a side stream for
+  // the collectives and its events, created on first use.
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_gemm = nullptr, ev_ar[2] = {nullptr, nullptr};
 };
 
 namespace tbik_b200 {
@@ -280,6 +284,13 @@ tbik_status tbik_group_destroy(tbik_group* g) {
   if (!g) return TBIK_OK;
   cudaSetDevice(g->device);
   cudaDeviceSynchronize();
+  if (g->side) {
+    cudaStreamDestroy(g->side);
+    cudaEventDestroy(g->ev_start);
+    cudaEventDestroy(g->ev_gemm);
+    cudaEventDestroy(g->ev_ar[0]);
+    cudaEventDestroy(g->ev_ar[1]);
+  }
   for (int r = 0; r < g->W; ++r)
     if (g->opened[r]) cudaIpcCloseMemHandle(g->peer_region[r]);
   cudaFree(g->region);
@@ -295,12 +306,15 @@ float* tbik_group_send_buffer(tbik_group* g) {
   return slot_ptr(g->region, g->capacity, g->epoch + 1);
 }
 
-tbik_status tbik_group_tree_all_reduce(tbik_group* g, const float* partial, float* out, int64_t elems, void* stream) {
+namespace {
+// max_blocks > 0 bounds every collective kernel's grid (the CTAs that can run
+// beside a GEMM occupying the other SMs).
+tbik_status group_all_reduce(tbik_group* g, const float* partial, float* out, int64_t elems, cudaStream_t s,
+                             int64_t max_blocks) {
   if (!g || !out) return set_error(TBIK_BAD_ARGUMENT, "null argument");
   if (elems < 0 || elems > g->capacity) return set_error(TBIK_COLLECTIVE_MISMATCH, "elems exceed group capacity");
   for (int r = 0; r < g->W; ++r)
     if (!g->peer_region[r]) return set_error(TBIK_COLLECTIVE_MISMATCH, "peers not opened");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint32_t epoch = ++g->epoch;
   float* mine = slot_ptr(g->region, g->capacity, epoch);
   if (partial && partial != mine)
@@ -321,12 +335,12 @@ tbik_status tbik_group_tree_all_reduce(tbik_group* g, const float* partial, floa
     const int64_t n4 = elems / 4;
     const int64_t lo = n4 * g->rank / g->W, hi = n4 * (g->rank + 1) / g->W;
     int64_t blocks = (hi - lo + 255) / 256;
-    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 2));
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, max_blocks > 0 ? max_blocks : 148 * 2));
     group_reduce_scatter_push_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
         gp, g->W, g->rank, epoch, lo, hi, cta_counter(g->region, g->capacity));
     TBIK_CUDA(cudaGetLastError());
     count_launch();
-    int64_t cblocks = std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 4));
+    int64_t cblocks = std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, max_blocks > 0 ? max_blocks : 148 * 4));
     group_gather_wait_copy_kernel<<<static_cast<unsigned>(cblocks), 256, 0, s>>>(
         done_flags(g->region, g->capacity), g->W, epoch, result_ptr(g->region, g->capacity, epoch), out, elems);
     TBIK_CUDA(cudaGetLastError());
@@ -335,12 +349,18 @@ tbik_status tbik_group_tree_all_reduce(tbik_group* g, const float* partial, floa
   }
   int64_t blocks = (elems / 4 + 255) / 256;
   if (blocks > 148 * 4) blocks = 148 * 4;
+  if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
   // All CTAs spin on the flags, so the grid must be co-resident: <= 4 per SM.
   group_allreduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(gp, g->W, g->rank, epoch, elems, out);
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;
+}
+}  // namespace
+
+tbik_status tbik_group_tree_all_reduce(tbik_group* g, const float* partial, float* out, int64_t elems, void* stream) {
+  return group_all_reduce(g, partial, out, elems, static_cast<cudaStream_t>(stream), 0);
 }
 
 tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* X_shard, int x_dtype, int64_t ldx,
@@ -357,11 +377,67 @@ tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* X_shard, 
   const int64_t Kr = bounds[2 * g->rank + 1] - bounds[2 * g->rank];
   tbik_block_config local = *cfg;
   local.k_first = gp.k_first;  // layers.cpp:85-88
-  // GEMM straight into the peer-visible slot of the coming epoch.
-  float* send = tbik_group_send_buffer(g);
-  TBIK_TRY(tbik_tree_matmul(X_shard, x_dtype, ldx, W_shard, w_dtype, ldw, send, N, M, N, Kr, &local, leaf_mode,
-                            stream));
-  return tbik_group_tree_all_reduce(g, send, Y, M * N, stream);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t xsz = x_dtype == TBIK_BF16 ? 2 : 4;
+
+  // Overlap (GEMM -> all-reduce): rows in chunks; the GEMM of
+  // chunk c+1 runs on all but kReserve SMs while the tree all-reduce of chunk c
+  // runs beside it on a side stream.  Each chunk is one collective epoch whose
+  // partial the GEMM writes straight into that epoch's peer-visible send slot;
+  // the GEMM of chunk c+2 (same slot parity) waits for chunk c's all-reduce to
+  // finish, i.e. for every peer to have read the slot.  Chunking rows never
+  // changes bits (batch invariance), and every rank cuts the same chunks (they
+  // depend only on M).  TBIK_GROUP_OVERLAP=0 disables it.
+  static const bool overlap_on = [] {
+    const char* e = std::getenv("TBIK_GROUP_OVERLAP");
+    return !(e && *e && std::atoi(e) == 0);
+  }();
+  constexpr int kChunks = 4, kReserve = 16;
+  const bool overlap = overlap_on && g->W > 1 && M >= 2 * 256 && M * N * 4 >= (int64_t(8) << 20);
+  if (!overlap) {
+    // GEMM straight into the peer-visible slot of the coming epoch.
+    float* send = tbik_group_send_buffer(g);
+    TBIK_TRY(tbik_tree_matmul(X_shard, x_dtype, ldx, W_shard, w_dtype, ldw, send, N, M, N, Kr, &local, leaf_mode,
+                              stream));
+    return tbik_group_tree_all_reduce(g, send, Y, M * N, stream);
+  }
+  if (!g->side) {
+    TBIK_CUDA(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+    TBIK_CUDA(cudaEventCreateWithFlags(&g->ev_start, cudaEventDisableTiming));
+    TBIK_CUDA(cudaEventCreateWithFlags(&g->ev_gemm, cudaEventDisableTiming));
+    TBIK_CUDA(cudaEventCreateWithFlags(&g->ev_ar[0], cudaEventDisableTiming));
+    TBIK_CUDA(cudaEventCreateWithFlags(&g->ev_ar[1], cudaEventDisableTiming));
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+  const int64_t chunk = ((M + kChunks - 1) / kChunks + 255) / 256 * 256;
+  TBIK_CUDA(cudaEventRecord(g->ev_start, s));
+  TBIK_CUDA(cudaStreamWaitEvent(g->side, g->ev_start, 0));
+  const uint32_t base = g->epoch;
+  const int prev_cap = set_tc_sm_cap(sms - kReserve);
+  tbik_status st = TBIK_OK;
+  int64_t c = 0;
+  for (int64_t r0 = 0; r0 < M && st == TBIK_OK; r0 += chunk, ++c) {
+    const int64_t rows = std::min(chunk, M - r0);
+    if (c >= 2 && (st = cudaStreamWaitEvent(s, g->ev_ar[c & 1], 0) == cudaSuccess ? TBIK_OK
+                                                                                : set_error(TBIK_CUDA_ERROR, "wait")))
+      break;
+    float* send = slot_ptr(g->region, g->capacity, base + static_cast<uint32_t>(c) + 1);
+    st = tbik_tree_matmul(static_cast<const char*>(X_shard) + r0 * ldx * xsz, x_dtype, ldx, W_shard, w_dtype, ldw,
+                          send, N, rows, N, Kr, &local, leaf_mode, s);
+    if (st != TBIK_OK) break;
+    if (cudaEventRecord(g->ev_gemm, s) != cudaSuccess || cudaStreamWaitEvent(g->side, g->ev_gemm, 0) != cudaSuccess) {
+      st = set_error(TBIK_CUDA_ERROR, "overlap event");
+      break;
+    }
+    st = group_all_reduce(g, send, Y + r0 * N, rows * N, g->side, 4 * kReserve);
+    if (st == TBIK_OK && cudaEventRecord(g->ev_ar[c & 1], g->side) != cudaSuccess)
+      st = set_error(TBIK_CUDA_ERROR, "overlap event");
+  }
+  set_tc_sm_cap(prev_cap);
+  TBIK_TRY(st);
+  TBIK_CUDA(cudaStreamWaitEvent(s, g->ev_ar[(c - 1) & 1], 0));
+  return TBIK_OK;
 }
 
 }  // extern "C"

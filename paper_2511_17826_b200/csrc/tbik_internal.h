@@ -53,6 +53,10 @@ int64_t tc_pair_tiles(const GemmView& v);
 // Work tiles of the variant launch_tc_gemm picks for v (pair 256 x 128 or single
 // CTA 128 x 128) and how many run concurrently (CTA pairs or CTAs).
 int64_t tc_tiles(const GemmView& v);
+// Caps the SMs the tcgen05 GEMM's persistent grid may occupy on this host thread
+// (0 = all); returns the previous cap.  Used to leave SMs for a concurrent
+// all-reduce kernel (tbik_group.cu).
+int set_tc_sm_cap(int cap);
 int64_t tc_parallel_slots(const GemmView& v);
 // The 256 x 256 pair-tile variant (tbik_gemm_tc_wide.cu).
 tbik_status launch_tc_gemm_wide(const GemmView& v, const GemmOut& o, cudaStream_t s);

@@ -29,7 +29,8 @@ def main():
     kb, ke = tb.make_row_shard_plan(K, cfg, world, 8).bounds[rank]
     xs, ws = x[:, kb:ke].contiguous(), w[kb:ke].contiguous()
     E_big = (1 << 20) + 4  # > 1 MiB of f32: the reduce-scatter + push path
-    grp = tb.PeerGroup(world, rank, torch.cuda.current_device(), max(M * N, E_big), dist)
+    Mo, No = 1024, 2048  # >= 8 MiB of f32 output: the overlapped GEMM / all-reduce chunk pipeline
+    grp = tb.PeerGroup(world, rank, torch.cuda.current_device(), max(M * N, E_big, Mo * No), dist)
     ys = []
     for it in range(5):  # several epochs: exercises both send-buffer slots
         for leaf in (tb.LEAF_TCGEN05, tb.LEAF_FMA):
@@ -58,6 +59,14 @@ def main():
         assert torch.equal(red_big.view(torch.int32), local_big.view(torch.int32)), f"two-phase differs ({it})"
         assert torch.equal(odd.view(torch.int32), local_big.view(torch.int32)), f"unaligned out differs ({it})"
         assert torch.equal(small.view(torch.int32), local.view(torch.int32)), f"one-shot differs ({it})"
+    # overlapped chunk pipeline (GEMM of chunk c+1 beside the all-reduce of chunk c)
+    xo = torch.randn(Mo, K, generator=g, device="cuda").to(torch.bfloat16)
+    wo = torch.randn(K, No, generator=g, device="cuda").to(torch.bfloat16)
+    yo_ref = tb.tree_matmul(xo, wo, cfg, tb.LEAF_TCGEN05)
+    for it in range(3):
+        yo = grp.row_parallel_forward(xo[:, kb:ke].contiguous(), wo[kb:ke].contiguous(), K, cfg, 8, tb.LEAF_TCGEN05)
+        torch.cuda.synchronize()
+        assert torch.equal(yo.view(torch.int32), yo_ref.view(torch.int32)), f"overlapped forward differs ({it})"
     # host-buffer pipeline through the group: chunked epochs, same bits as the device call
     xh = x[:, kb:ke].contiguous().cpu().pin_memory()
     yh = grp.row_parallel_forward_hostio(xh, ws, K, cfg, 8, tb.LEAF_TCGEN05, chunk_rows=24)
