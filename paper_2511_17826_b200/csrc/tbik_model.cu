@@ -81,17 +81,17 @@ __global__ void cast_kernel(const float* __restrict__ x, int64_t ldx, int64_t co
 //   l   = ((p_0 + p_1) + p_2) + ...                  (ascending j)
 //   o[d]= fma chain over ascending j of p_j v_j[d]   (from +0)
 //   out = bf16(o[d] / l)
-// One CTA = (64-query block, q head, sequence), 256 threads; K / V key blocks of
+// One CTA = (32-query block, q head, sequence), 128 threads; K / V key blocks of
 // 64 staged through shared memory as f32; scores for the whole causal prefix kept
 // in shared memory (S <= 512).  Thread (i = t % 64, part = t / 64): 4 key phases in
 // the score pass, 4 x 32-dim slices in the P.V pass; 4 independent fma chains each
 // for ILP.  Per-query arithmetic never depends on the batch or the head sharding.
-constexpr int AQ = 64;       // queries per CTA
+constexpr int AQ = 32;       // queries per CTA
 constexpr int AK = 64;       // keys per staged block
 constexpr int AD = 128;      // head dim
 constexpr int AKP = AD + 4;  // padded f32 row of a staged K/V block
 
-__global__ void __launch_bounds__(256) attn2_kernel(const uint16_t* __restrict__ q, int64_t ldq,
+__global__ void __launch_bounds__(4 * AQ, 3) attn2_kernel(const uint16_t* __restrict__ q, int64_t ldq,
                                                     const uint16_t* __restrict__ k, int64_t ldk,
                                                     const uint16_t* __restrict__ v, int64_t ldv, int S, int nq,
                                                     int nkv, float scale, uint16_t* __restrict__ out, int64_t ldo) {
@@ -102,9 +102,12 @@ __global__ void __launch_bounds__(256) attn2_kernel(const uint16_t* __restrict__
   const int pst = S + 1;
   const int tid = threadIdx.x;
   const int qi = tid & (AQ - 1);
-  const int part = tid >> 6;  // 0..3
-  const int qb = blockIdx.x, h = blockIdx.y;
-  const int64_t seq0 = static_cast<int64_t>(blockIdx.z) * S;
+  const int part = tid / AQ;  // 0..3
+  // grid (head, sequence, query block) with the query block slowest and reversed:
+  // the heaviest (longest causal prefix) blocks are scheduled first and the light
+  // ones fill the tail of the last wave.
+  const int qb = static_cast<int>(gridDim.z) - 1 - static_cast<int>(blockIdx.z), h = blockIdx.x;
+  const int64_t seq0 = static_cast<int64_t>(blockIdx.y) * S;
   const int kh = h / (nq / nkv);
   const int i = qb * AQ + qi;  // query position in the sequence
   const bool valid = i < S;
@@ -384,9 +387,9 @@ tbik_status tbik_attention_prefill(const void* q, int64_t ldq, const void* k, in
     TBIK_CUDA(cudaFuncSetAttribute(attn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     attr = smem;
   }
-  dim3 grid(static_cast<unsigned>((seq_len + AQ - 1) / AQ), static_cast<unsigned>(n_q_heads),
-            static_cast<unsigned>(batch));
-  attn2_kernel<<<grid, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+  dim3 grid(static_cast<unsigned>(n_q_heads), static_cast<unsigned>(batch),
+            static_cast<unsigned>((seq_len + AQ - 1) / AQ));
+  attn2_kernel<<<grid, 4 * AQ, smem, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(q), ldq, static_cast<const uint16_t*>(k), ldk, static_cast<const uint16_t*>(v), ldv,
       seq_len, n_q_heads, n_kv_heads, scale, static_cast<uint16_t*>(out), ldo);
   TBIK_CUDA(cudaGetLastError());
