@@ -115,6 +115,8 @@ struct TcParams {
   long long unit_stride;
   float* scratch;  // [gridDim.x][levels-3][BN][BM] when levels > 3
   int tma_store;   // 1: results leave through tmC (TMA), 0: direct row stores
+  int pf;          // L2 prefetch distance in K chunks (0: off; measured slower, kept as a knob)
+  int group_m;     // raster: M-blocks that share one pass over W
   int debug;       // TBIK_TC_DEBUG (perf experiments only; wrong results): 1 = skip the merge,
                    // 2 = skip the output store, 4 = skip the tree above level 0,
                    // 8 = skip the scratch levels, 16 = direct (non-TMA) output stores
@@ -154,6 +156,13 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMa
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
       : "memory");
 }
+// L2 prefetch of a future TMA tile (no shared memory, no barrier).
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void umma_bf16_2cta(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                                uint32_t accumulate) {
   asm volatile(
@@ -187,11 +196,12 @@ __device__ __forceinline__ Item decode(const TcParams& p, long long item) {
   Item it;
   it.unit = static_cast<int>(item % p.units);
   const long long rest = item / p.units;
-  const long long group = GROUP_M * static_cast<long long>(p.ntiles);
+  const int group_m = p.group_m;
+  const long long group = group_m * static_cast<long long>(p.ntiles);
   const int g = static_cast<int>(rest / group);
   const int idx = static_cast<int>(rest % group);
-  const int gm = min(GROUP_M, p.mblocks - g * GROUP_M);
-  const int mb = g * GROUP_M + idx % gm;
+  const int gm = min(group_m, p.mblocks - g * group_m);
+  const int mb = g * group_m + idx % gm;
   const int nt = idx / gm;
   it.m0 = mb * p.tile_m;
   it.n0 = nt * BN;
@@ -286,9 +296,18 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         const Item it = decode(p, item);
         const int am = it.m0 + static_cast<int>(rank) * BM;
         const int bn = it.n0 + static_cast<int>(rank) * (BN / 2);
+        const int k_end = min(it.t_end * p.bk, p.K);
         for (int t = it.t_begin; t < it.t_end; ++t) {
           const int nch = tile_chunks(p, t);
           for (int c = 0; c < nch; ++c) {
+            if (p.pf) {  // warm L2 for the chunk pf stages ahead (its DRAM latency overlaps)
+              const int kp = t * p.bk + (c + p.pf) * KSTAGE;
+              if (kp < k_end) {
+                tma_prefetch_l2(&tmA, kp, am);
+                tma_prefetch_l2(&tmB, bn, kp);
+                if constexpr (!PAIR) tma_prefetch_l2(&tmB, bn + BN / 2, kp);
+              }
+            }
             mbar_wait(&empty[stage], phase ^ 1);
             const uint32_t fb = full_leader0 + stage * 8;
             if (leader)
@@ -687,7 +706,7 @@ int64_t tc_pair_tiles(const GemmView& v) {
   return ((v.M + PAIR_M - 1) / PAIR_M) * ((v.N + BN - 1) / BN);
 }
 
-int64_t tc_parallel_slots(const GemmView& v) { return tc_use_pair(v) && !tc_use_wide(v) ? sm_count() / 2 : sm_count(); }
+int64_t tc_parallel_slots(const GemmView& v) { return tc_use_wide(v) || tc_use_pair(v) ? sm_count() / 2 : sm_count(); }
 
 int64_t tc_tiles(const GemmView& v) {
   if (tc_use_wide(v) || tc_use_pair(v)) return tc_pair_tiles(v);
@@ -753,6 +772,16 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
     return e ? std::atoi(e) : 0;
   }();
   p.debug = dbg;
+  static const int pf = [] {
+    const char* e = std::getenv("TBIK_TC_PF");
+    return e && *e ? std::atoi(e) : 0;
+  }();
+  p.pf = pf;
+  {  // raster knob (pure scheduling, same bits), read per launch
+    const char* e = std::getenv("TBIK_TC_GROUP_M");
+    const int gm = e && *e ? std::atoi(e) : GROUP_M;
+    p.group_m = gm >= 1 ? gm : GROUP_M;
+  }
   const bool pair = tc_use_pair(v);
   p.tile_m = pair ? PAIR_M : BM;
   p.mblocks = static_cast<int>((v.M + p.tile_m - 1) / p.tile_m);

@@ -270,24 +270,33 @@ def test_errors(tb, cuda):
 
 
 # ---------------------------------------------------------------------------------
-# the pair-tile width (BN = 128 / 256) and the raster are scheduling choices
+# every launch-shape knob is a scheduling choice: pair / single-CTA tiles, 256-wide
+# pair tiles, A rows staged per stage, raster grouping, K split -- same bits
 # ---------------------------------------------------------------------------------
-@pytest.mark.parametrize("M,K,N", [(300, 14336, 640), (64, 4096, 512), (513, 6144, 384)])
-def test_tc_tile_width_and_raster_invisible(tb, cuda, orc, M, K, N, monkeypatch):
+SCHEDULES = [{}, {"TBIK_TC_WIDE": "1"}, {"TBIK_TC_GROUP_M": "1"}, {"TBIK_TC_GROUP_M": "3", "TBIK_TC_UNITS": "2"},
+             {"TBIK_TC_PAIR": "0"}, {"TBIK_TC_PAIR": "0", "TBIK_TC_UNITS": "4"}, {"TBIK_TC_PAIR": "1"},
+             {"TBIK_TC_ABOX": "32"}, {"TBIK_TC_ABOX": "64", "TBIK_TC_PAIR": "1"}]
+
+
+@pytest.mark.parametrize("M,K,N", [(300, 14336, 640), (64, 4096, 512), (513, 6144, 384), (20, 4096, 200),
+                                   (128, 2048, 136)])
+def test_tc_schedules_invisible(tb, cuda, orc, M, K, N, monkeypatch):
     torch.manual_seed(M)
     x = torch.randn(M, K, device=cuda).to(torch.bfloat16)
     w = torch.randn(K, N, device=cuda).to(torch.bfloat16)
     cfg = tb.BlockConfig(64, 256, 128, 0)
     outs, leaves = [], []
-    for bn, gm in (("128", "8"), ("256", "8"), ("256", "1"), ("128", "3")):
-        monkeypatch.setenv("TBIK_TC_BN", bn)
-        monkeypatch.setenv("TBIK_GROUP_M", gm)
+    for env in SCHEDULES:
+        for k in ("TBIK_TC_WIDE", "TBIK_TC_GROUP_M", "TBIK_TC_UNITS", "TBIK_TC_PAIR", "TBIK_TC_ABOX"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         outs.append(tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05))
         leaves.append(tb.tree_matmul_leaves(x, w, cfg, tb.LEAF_TCGEN05))
-    for o in outs[1:]:
-        assert torch.equal(outs[0].view(torch.int32), o.view(torch.int32))
-    for lv in leaves[1:]:
-        assert torch.equal(leaves[0].view(torch.int32), lv.view(torch.int32))
+    for env, o in zip(SCHEDULES[1:], outs[1:]):
+        assert torch.equal(outs[0].view(torch.int32), o.view(torch.int32)), f"schedule {env} changed the bits"
+    for env, lv in zip(SCHEDULES[1:], leaves[1:]):
+        assert torch.equal(leaves[0].view(torch.int32), lv.view(torch.int32)), f"schedule {env} changed a leaf"
     plan = tb.plan_blocks(K, cfg, 1)
     want = orc.tree_over_leaves(leaves[0].cpu().numpy(), plan.k_first)
     assert np.array_equal(bits(outs[0].cpu().numpy()), bits(want))
