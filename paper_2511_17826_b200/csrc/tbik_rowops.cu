@@ -271,32 +271,44 @@ __global__ void __launch_bounds__(LANES, 4) ms_group_kernel(const float* __restr
         b = MS{m, sum};
       }
     } else {
-      int cnt[MSB];  // valid logits in each chunk (4, or fewer in the group's last chunk)
+      // the lane's last (partial) block: nv < MSB chunks, the last possibly ragged;
+      // loops stop at nv so the absent chunks cost nothing
+      int nv = 0;
+#pragma unroll
+      for (int j = 0; j < MSB; ++j)
+        if (c0 + static_cast<int64_t>(j) * LANES < nch) nv = j + 1;
+      const int64_t clast = c0 + static_cast<int64_t>(nv - 1) * LANES;
+      const int last_cnt = n - clast * 4 < 4 ? static_cast<int>(n - clast * 4) : 4;
 #pragma unroll
       for (int j = 0; j < MSB; ++j) {
-        const int64_t c = c0 + static_cast<int64_t>(j) * LANES;
-        const int64_t e0 = c * 4;
-        cnt[j] = c < nch ? (n - e0 < 4 ? static_cast<int>(n - e0) : 4) : 0;
-        if (VEC && cnt[j] == 4) {
+        if (j >= nv) break;
+        const int64_t e0 = (c0 + static_cast<int64_t>(j) * LANES) * 4;
+        if (VEC && (j < nv - 1 || last_cnt == 4)) {
           const float4 q = *reinterpret_cast<const float4*>(x + e0);
           v[4 * j] = q.x;
           v[4 * j + 1] = q.y;
           v[4 * j + 2] = q.z;
           v[4 * j + 3] = q.w;
         } else {
+          const int cj = j < nv - 1 ? 4 : last_cnt;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) v[4 * j + i] = i < cnt[j] ? x[e0 + i] : NEG_INF;
+          for (int i = 0; i < 4; ++i) v[4 * j + i] = i < cj ? x[e0 + i] : NEG_INF;
         }
       }
-      float m = v[0];  // chunk c0 < nch always holds >= 1 logit
+      const int nel = (nv - 1) * 4 + last_cnt;  // valid logits, in ascending order
+      float m = v[0];
 #pragma unroll
-      for (int k = 1; k < MSB * 4; ++k)
-        if (k % 4 < cnt[k / 4]) m = v[k] > m ? v[k] : m;
+      for (int k = 1; k < MSB * 4; ++k) {
+        if (k >= nel) break;
+        m = v[k] > m ? v[k] : m;
+      }
       if (m != NEG_INF) {
         float sum = 0.0f;
 #pragma unroll
-        for (int k = 0; k < MSB * 4; ++k)
-          if (k % 4 < cnt[k / 4]) sum = __fadd_rn(sum, tb_exp_nonpos(__fsub_rn(v[k], m)));
+        for (int k = 0; k < MSB * 4; ++k) {
+          if (k >= nel) break;
+          sum = __fadd_rn(sum, tb_exp_nonpos(__fsub_rn(v[k], m)));
+        }
         b = MS{m, sum};
       }
     }
