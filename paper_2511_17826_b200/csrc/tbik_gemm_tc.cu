@@ -87,17 +87,22 @@ constexpr int L3_WARP_BYTES = 32 * 64 * 4;
 // second 128 rows would be padding at small M.
 constexpr int b_stage_bytes(bool pair) { return pair ? B_STAGE_BYTES : 2 * B_STAGE_BYTES; }
 constexpr int a_region_bytes(int abox, int nst) { return (nst - 1) * abox * 128 + A_STAGE_BYTES; }
-constexpr int stages_for(int abox, bool pair) {
-  return pair ? (abox == 32 ? 12 : abox == 64 ? 9 : STAGES) : (abox == 32 ? 7 : abox == 64 ? 6 : 4);
+// DEEP (pair tiles, 128-row A staging, k_first > 1): 8 stages instead of 6; tree
+// level 3 moves to scratch (touched once per 4 groups) and each merge warp keeps
+// a single 4 KB output staging box.
+constexpr int stages_for(int abox, bool pair, bool deep = false) {
+  return deep ? 8 : pair ? (abox == 32 ? 12 : abox == 64 ? 9 : STAGES) : (abox == 32 ? 7 : abox == 64 ? 6 : 4);
 }
-constexpr size_t smem_bytes(int epi, int abox, bool pair) {
-  return 1024 + static_cast<size_t>(a_region_bytes(abox, stages_for(abox, pair))) +
-         static_cast<size_t>(stages_for(abox, pair)) * b_stage_bytes(pair) + 1024 +
-         static_cast<size_t>(epi) * L3_WARP_BYTES;
+constexpr int warp_region_bytes(bool deep) { return deep ? OUT_BUF_BYTES : L3_WARP_BYTES; }
+constexpr size_t smem_bytes(int epi, int abox, bool pair, bool deep = false) {
+  return 1024 + static_cast<size_t>(a_region_bytes(abox, stages_for(abox, pair, deep))) +
+         static_cast<size_t>(stages_for(abox, pair, deep)) * b_stage_bytes(pair) + 1024 +
+         static_cast<size_t>(epi) * warp_region_bytes(deep);
 }
 static_assert(smem_bytes(8, 32, true) <= 232448 && smem_bytes(8, 64, true) <= 232448 &&
                   smem_bytes(8, 128, true) <= 232448 && smem_bytes(8, 32, false) <= 232448 &&
-                  smem_bytes(8, 64, false) <= 232448 && smem_bytes(8, 128, false) <= 232448,
+                  smem_bytes(8, 64, false) <= 232448 && smem_bytes(8, 128, false) <= 232448 &&
+                  smem_bytes(8, 128, true, true) <= 232448,
               "shared memory budget");
 
 struct TcParams {
@@ -235,14 +240,14 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // A rows staged per stage (128, or 64 / 32 for small M; stage count follows).  KF1 (used when k_first == 1, where every leaf completes a
 // group and g need not persist across leaves): the level-1 slot is loaded in the
 // same batch as the leaf, so an odd leaf costs one TMEM round trip, not two.
-template <int EPI, bool KF1, int ABOX, bool PAIR>
+template <int EPI, bool KF1, int ABOX, bool PAIR, bool DEEP>
 __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     tc_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const TcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  constexpr int NST = stages_for(ABOX, PAIR);
+  constexpr int NST = stages_for(ABOX, PAIR, DEEP);
   constexpr int A_STRIDE = ABOX * 128;  // bytes between consecutive stages' A windows
   constexpr int B_STAGE = b_stage_bytes(PAIR);
   constexpr uint32_t TX_BYTES = A_STRIDE + B_STAGE;
@@ -395,12 +400,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     // TMEM holds tree levels 1-2, shared memory level 3 (this warp's sL3 region);
     // levels >= 4 live in scratch as [col/4][row][4] slabs (a warp's float4
     // access is 512 contiguous bytes).
+    constexpr int FS = DEEP ? 3 : 4;  // first scratch level
     float* scratch_base =
-        p.levels > 3
-            ? p.scratch + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - 3) * (BM * BN) +
+        p.levels >= FS
+            ? p.scratch + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - FS + 1) * (BM * BN) +
                            static_cast<size_t>(col0) * BM + static_cast<size_t>(row_in_tile) * 4
             : nullptr;
-    uint8_t* l3 = sL3 + (warp - 4) * L3_WARP_BYTES;  // [16][32 lanes][float4]
+    uint8_t* l3 = sL3 + (warp - 4) * warp_region_bytes(DEEP);  // [16][32 lanes][float4] (+ staging)
 
     float g[COLS];  // level 0: the running leaf-group value
     int xb = 0;      // output staging buffer toggle
@@ -502,7 +508,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               for (int c = 0; c < NCH; ++c)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], __uint_as_float(r[c][i]));
-            } else if (level == 3) {
+            } else if (!DEEP && level == 3) {
 #pragma unroll
               for (int i = 0; i < COLS; i += 4) {
                 const float4 x = *reinterpret_cast<const float4*>(l3 + ((i / 4) * 32 + lane) * 16);
@@ -513,7 +519,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               }
               __syncwarp();  // the region may become output staging right after
             } else if (!(p.debug & 8)) {
-              const float* sp = scratch_base + static_cast<size_t>(level - 4) * (BM * BN);
+              const float* sp = scratch_base + static_cast<size_t>(level - FS) * (BM * BN);
 #pragma unroll
               for (int i = 0; i < COLS; i += 4) {
                 const float4 x = *reinterpret_cast<const float4*>(sp + i * BM);
@@ -537,7 +543,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                 tmem_st32(slot + c * 32, v);
               }
               tmem_wait_st();
-            } else if (level == 3) {
+            } else if (!DEEP && level == 3) {
               if (lane == 0) bulk_wait_read<0>();  // earlier output boxes staged here
               __syncwarp();
 #pragma unroll
@@ -545,7 +551,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                 *reinterpret_cast<float4*>(l3 + ((i / 4) * 32 + lane) * 16) =
                     make_float4(g[i], g[i + 1], g[i + 2], g[i + 3]);
             } else if (!(p.debug & 8)) {
-              float* sp = scratch_base + static_cast<size_t>(level - 4) * (BM * BN);
+              float* sp = scratch_base + static_cast<size_t>(level - FS) * (BM * BN);
 #pragma unroll
               for (int i = 0; i < COLS; i += 4)
                 *reinterpret_cast<float4*>(sp + i * BM) = make_float4(g[i], g[i + 1], g[i + 2], g[i + 3]);
@@ -560,9 +566,14 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           // 16 B stores) -> one TMA store per box; the tensor map clips ragged edges.
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
-            if (lane == 0) bulk_wait_read<1>();
+            if (lane == 0) {
+              if constexpr (DEEP)
+                bulk_wait_read<0>();  // one staging box per warp
+              else
+                bulk_wait_read<1>();
+            }
             __syncwarp();
-            uint8_t* sbuf = l3 + xb * OUT_BUF_BYTES;
+            uint8_t* sbuf = l3 + (DEEP ? 0 : xb * OUT_BUF_BYTES);
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               *reinterpret_cast<float4*>(sbuf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
@@ -791,8 +802,16 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   const long long nstreams = p.items < slots ? p.items : slots;
   dim3 grid(static_cast<unsigned>(pair ? 2 * nstreams : nstreams));
   const bool kf1 = p.kf == 1;
-  if (p.levels > 3) {
-    const size_t n = static_cast<size_t>(grid.x) * (p.levels - 3) * BM * BN;
+  // DEEP: 8 stages with tree level 3 in scratch, for pair tiles at k_first > 1.
+  // Measured slower than 6 stages + level 3 on chip (1108 vs 1146 TFLOP/s at the
+  // bench shape, profiles/r01_tc_deep_vs_l3smem.txt): off unless TBIK_TC_DEEP=1
+  // (a pure scheduling knob -- same bits).
+  bool deep = false;
+  if (const char* e = std::getenv("TBIK_TC_DEEP"))
+    if (*e) deep = pair && abox == 128 && !kf1 && std::atoi(e) != 0;
+  const int first_scratch = deep ? 3 : 4;
+  if (p.levels >= first_scratch) {
+    const size_t n = static_cast<size_t>(grid.x) * (p.levels - first_scratch + 1) * BM * BN;
     p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1));
     if (!p.scratch) return set_error(TBIK_CUDA_ERROR, "tc gemm: scratch allocation failed");
   }
@@ -807,23 +826,23 @@ tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) 
                           static_cast<uint64_t>(p.units), static_cast<uint64_t>(o.ldo) * 4, ustride * 4));
   using Kern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
   static const Kern table[2][3][2] = {
-      {{tc_tree_gemm_kernel<8, false, 32, false>, tc_tree_gemm_kernel<8, true, 32, false>},
-       {tc_tree_gemm_kernel<8, false, 64, false>, tc_tree_gemm_kernel<8, true, 64, false>},
-       {tc_tree_gemm_kernel<8, false, 128, false>, tc_tree_gemm_kernel<8, true, 128, false>}},
-      {{tc_tree_gemm_kernel<8, false, 32, true>, tc_tree_gemm_kernel<8, true, 32, true>},
-       {tc_tree_gemm_kernel<8, false, 64, true>, tc_tree_gemm_kernel<8, true, 64, true>},
-       {tc_tree_gemm_kernel<8, false, 128, true>, tc_tree_gemm_kernel<8, true, 128, true>}}};
+      {{tc_tree_gemm_kernel<8, false, 32, false, false>, tc_tree_gemm_kernel<8, true, 32, false, false>},
+       {tc_tree_gemm_kernel<8, false, 64, false, false>, tc_tree_gemm_kernel<8, true, 64, false, false>},
+       {tc_tree_gemm_kernel<8, false, 128, false, false>, tc_tree_gemm_kernel<8, true, 128, false, false>}},
+      {{tc_tree_gemm_kernel<8, false, 32, true, false>, tc_tree_gemm_kernel<8, true, 32, true, false>},
+       {tc_tree_gemm_kernel<8, false, 64, true, false>, tc_tree_gemm_kernel<8, true, 64, true, false>},
+       {tc_tree_gemm_kernel<8, false, 128, true, false>, tc_tree_gemm_kernel<8, true, 128, true, false>}}};
   const int ai = abox == 32 ? 0 : abox == 64 ? 1 : 2;
-  const Kern kern = table[pair][ai][kf1];
+  const Kern kern = deep ? tc_tree_gemm_kernel<8, false, 128, true, true> : table[pair][ai][kf1];
   const int nthreads = 128 + 32 * 8;
-  const size_t smem = smem_bytes(8, abox, pair);
-  static bool attr_set[16][2][3][2] = {};
+  const size_t smem = smem_bytes(8, abox, pair, deep);
+  static bool attr_set[16][2][3][2][2] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 16 && !attr_set[dev][pair][ai][kf1]) {
+  if (dev >= 0 && dev < 16 && !attr_set[dev][pair][ai][kf1][deep]) {
     TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     if (pair) TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-    attr_set[dev][pair][ai][kf1] = true;
+    attr_set[dev][pair][ai][kf1][deep] = true;
   }
   cudaLaunchConfig_t lc{};
   lc.gridDim = grid;

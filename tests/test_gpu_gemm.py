@@ -275,7 +275,7 @@ def test_errors(tb, cuda):
 # ---------------------------------------------------------------------------------
 SCHEDULES = [{}, {"TBIK_TC_WIDE": "1"}, {"TBIK_TC_GROUP_M": "1"}, {"TBIK_TC_GROUP_M": "3", "TBIK_TC_UNITS": "2"},
              {"TBIK_TC_PAIR": "0"}, {"TBIK_TC_PAIR": "0", "TBIK_TC_UNITS": "4"}, {"TBIK_TC_PAIR": "1"},
-             {"TBIK_TC_ABOX": "32"}, {"TBIK_TC_ABOX": "64", "TBIK_TC_PAIR": "1"}]
+             {"TBIK_TC_ABOX": "32"}, {"TBIK_TC_ABOX": "64", "TBIK_TC_PAIR": "1"}, {"TBIK_TC_DEEP": "1"}]
 
 
 @pytest.mark.parametrize("M,K,N", [(300, 14336, 640), (64, 4096, 512), (513, 6144, 384), (20, 4096, 200),
@@ -287,7 +287,7 @@ def test_tc_schedules_invisible(tb, cuda, orc, M, K, N, monkeypatch):
     cfg = tb.BlockConfig(64, 256, 128, 0)
     outs, leaves = [], []
     for env in SCHEDULES:
-        for k in ("TBIK_TC_WIDE", "TBIK_TC_GROUP_M", "TBIK_TC_UNITS", "TBIK_TC_PAIR", "TBIK_TC_ABOX"):
+        for k in ("TBIK_TC_WIDE", "TBIK_TC_GROUP_M", "TBIK_TC_UNITS", "TBIK_TC_PAIR", "TBIK_TC_ABOX", "TBIK_TC_DEEP"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
