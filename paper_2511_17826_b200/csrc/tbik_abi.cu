@@ -49,12 +49,12 @@ struct Arena {
   size_t bytes = 0;
 };
 std::mutex g_ws_mu;
-Arena g_ws[16][8];
+Arena g_ws[16][12];
 }  // namespace
 
 void* workspace(size_t bytes, int slot) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16 || slot < 0 || slot >= 8) return nullptr;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16 || slot < 0 || slot >= 12) return nullptr;
   std::lock_guard<std::mutex> lk(g_ws_mu);
   Arena& a = g_ws[dev][slot];
   if (a.bytes >= bytes && a.ptr) return a.ptr;
@@ -143,6 +143,23 @@ int64_t next_pow2(int64_t v) {
 }
 size_t dsize(int dt) { return dt == TBIK_BF16 ? 2 : 4; }
 }  // namespace
+
+// TMA needs 16-byte row strides and base addresses.  A bf16 operand that has
+// neither (any K or N not a multiple of 8) is copied once into a padded buffer
+// (workspace slot `slot`, row stride rounded up to 8 elements); the padding is
+// never read (the tensor map's extent is the true width), so the bits are those
+// of the unpadded call.
+tbik_status pad_operand(const void** p, int64_t* ld, int64_t rows, int64_t cols, int slot, cudaStream_t s) {
+  const bool ok = (*ld % 8 == 0) && (reinterpret_cast<uintptr_t>(*p) & 15) == 0;
+  if (ok) return TBIK_OK;
+  const int64_t ldp = (cols + 7) / 8 * 8;
+  void* buf = workspace(static_cast<size_t>(rows) * ldp * 2, slot);
+  if (!buf) return set_error(TBIK_CUDA_ERROR, "tc gemm: padding buffer allocation failed");
+  TBIK_CUDA(cudaMemcpy2DAsync(buf, ldp * 2, *p, *ld * 2, cols * 2, rows, cudaMemcpyDeviceToDevice, s));
+  *p = buf;
+  *ld = ldp;
+  return TBIK_OK;
+}
 
 tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mode, cudaStream_t s) {
   const size_t slice = static_cast<size_t>(v.M) * v.N;

@@ -232,13 +232,17 @@ Matrix tree_matmul(const Matrix& a, const Matrix& b, const BlockConfig& cfg, Lea
   if (a.cols() != b.rows())
     fail(ErrorCode::ShapeMismatch,
          "tree_matmul: inner dimensions differ, " + std::to_string(a.cols()) + " vs " + std::to_string(b.rows()));
-  DevBuf da = upload(a), db = upload(b), dc(static_cast<std::size_t>(a.rows() * b.cols()) * 4);
+  // The weights go to the device once; the activations stream host -> device and
+  // the f32 result device -> host in row chunks overlapped with the GEMM
+  // (tbik_tree_matmul_hostio) -- the reference's Matrix-in / Matrix-out call.
+  DevBuf db = upload(b);
+  std::vector<float> out(static_cast<std::size_t>(a.rows() * b.cols()));
   tbik_block_config c = c_cfg(cfg);
-  check_status(tbik_tree_matmul(da.p, static_cast<int>(a.dtype()), a.cols(), db.p, static_cast<int>(b.dtype()),
-                                b.cols(), static_cast<float*>(dc.p), b.cols(), a.rows(), b.cols(), a.cols(), &c,
-                                static_cast<int>(leaf), nullptr));
+  check_status(tbik_tree_matmul_hostio(a.raw(), static_cast<int>(a.dtype()), a.cols(), db.p,
+                                       static_cast<int>(b.dtype()), b.cols(), out.data(), b.cols(), a.rows(),
+                                       b.cols(), a.cols(), &c, static_cast<int>(leaf), 0, nullptr));
   check_status(tbik_sync(nullptr));
-  return download_f32(dc, a.rows(), b.cols());
+  return Matrix::from_f32(a.rows(), b.cols(), std::move(out));
 }
 
 // ---- collective.hpp --------------------------------------------------------------------

@@ -735,7 +735,12 @@ bool tc_use_wide(const GemmView& v) {
   return false;
 }
 
-tbik_status launch_tc_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s) {
+tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t s) {
+  GemmView v = v_in;
+  if (v.adt == TBIK_BF16 && v.bdt == TBIK_BF16) {  // any K / N: pad strides for TMA
+    TBIK_TRY(pad_operand(&v.A, &v.lda, v.M, v.K, 8, s));
+    TBIK_TRY(pad_operand(&v.B, &v.ldb, v.K, v.N, 9, s));
+  }
   std::string why;
   if (!tc_supported(v, &why)) return set_error(TBIK_UNSUPPORTED, why);
   if (o.mode == OUT_GROUPS) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: GROUPS mode is FMA-only");

@@ -67,6 +67,10 @@ tbik_status launch_tree_combine(const float* ws, int64_t X, int64_t fold, int64_
 tbik_status launch_allreduce(const PartPtrs& parts, int W, float* out, int64_t elems, bool ring,
                              bool aligned16, cudaStream_t s);
 
+// Copies a bf16 operand whose row stride or base is not 16-byte aligned into a
+// padded buffer (workspace slot `slot`); no-op otherwise.
+tbik_status pad_operand(const void** p, int64_t* ld, int64_t rows, int64_t cols, int slot, cudaStream_t s);
+
 // Whole tree GEMM (plan resolved by the caller): picks FULL vs split + combine.
 tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mode, cudaStream_t s);
 

@@ -350,3 +350,37 @@ def test_tbik_file_golden_case(tb, cuda):
         tb.matrix_write(p, y)
         with open(p, "rb") as f1, open(os.path.join(d, "c_tree.tbik"), "rb") as f2:
             assert f1.read() == f2.read()
+
+
+# ---------------------------------------------------------------------------------
+# seeded random shapes (ragged M / N / K, every block_k the TC leaf supports)
+# ---------------------------------------------------------------------------------
+def _random_shapes(n, seed=20261017):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        bk = int(rng.choice([64, 128, 256]))
+        M = int(rng.integers(1, 300))
+        N = int(rng.integers(1, 300))
+        K = int(rng.integers(1, 24)) * 8 * int(rng.choice([1, 3, 11]))  # lda % 8 == 0 for TMA
+        out.append((M, K, N, bk))
+    return out
+
+
+@pytest.mark.parametrize("M,K,N,bk", _random_shapes(10))
+def test_random_shapes_both_leaves(tb, cuda, orc, M, K, N, bk):
+    a, b = gen(orc, 7 * M + N, M, K, N)
+    cfg = tb.BlockConfig(64, bk, 128, 0)
+    da, db = to_dev(a), to_dev(b)
+    # exact leaf: the reference algorithm bit for bit
+    want = orc.global_tree_matmul(a, b, bk, 0, 1)
+    y = tb.tree_matmul(da, db, cfg, tb.LEAF_FMA).cpu().numpy()
+    assert np.array_equal(bits(y), bits(want))
+    # tensor-core leaf: the oracle tree over the GPU's own leaves, bit for bit
+    y = tb.tree_matmul(da, db, cfg, tb.LEAF_TCGEN05)
+    leaves = tb.tree_matmul_leaves(da, db, cfg, tb.LEAF_TCGEN05)
+    plan = tb.plan_blocks(K, cfg, 1)
+    want_tc = orc.tree_over_leaves(leaves.cpu().numpy(), plan.k_first)
+    assert np.array_equal(bits(y.cpu().numpy()), bits(want_tc))
+    rel = np.abs(y.cpu().numpy() - want).max() / max(np.abs(want).max(), 1e-30)
+    assert rel < 1e-5
