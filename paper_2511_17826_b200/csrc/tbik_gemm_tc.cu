@@ -87,11 +87,14 @@ constexpr int L3_WARP_BYTES = 32 * 64 * 4;
 // second 128 rows would be padding at small M.
 constexpr int b_stage_bytes(bool pair) { return pair ? B_STAGE_BYTES : 2 * B_STAGE_BYTES; }
 constexpr int a_region_bytes(int abox, int nst) { return (nst - 1) * abox * 128 + A_STAGE_BYTES; }
-// DEEP (pair tiles, 128-row A staging, k_first > 1): 8 stages instead of 6; tree
-// level 3 moves to scratch (touched once per 4 groups) and each merge warp keeps
-// a single 4 KB output staging box.
+// DEEP: no shared-memory tree level 3 (it moves to scratch) and a single 4 KB
+// output staging box per merge warp; the 32 KB freed per warp pair buys pipeline
+// stages.  Free when a work item has <= 2 tree levels (K split into units, TP
+// shards, short K) -- the default then; with 3+ levels the on-chip level 3 wins
+// (measured, profiles/r01_tc_deep_vs_l3smem.txt).
 constexpr int stages_for(int abox, bool pair, bool deep = false) {
-  return deep ? 8 : pair ? (abox == 32 ? 12 : abox == 64 ? 9 : STAGES) : (abox == 32 ? 7 : abox == 64 ? 6 : 4);
+  return deep ? (pair ? (abox == 32 ? 15 : abox == 64 ? 11 : 8) : (abox == 32 ? 9 : abox == 64 ? 7 : 6))
+              : (pair ? (abox == 32 ? 12 : abox == 64 ? 9 : STAGES) : (abox == 32 ? 7 : abox == 64 ? 6 : 4));
 }
 constexpr int warp_region_bytes(bool deep) { return deep ? OUT_BUF_BYTES : L3_WARP_BYTES; }
 constexpr size_t smem_bytes(int epi, int abox, bool pair, bool deep = false) {
@@ -102,7 +105,9 @@ constexpr size_t smem_bytes(int epi, int abox, bool pair, bool deep = false) {
 static_assert(smem_bytes(8, 32, true) <= 232448 && smem_bytes(8, 64, true) <= 232448 &&
                   smem_bytes(8, 128, true) <= 232448 && smem_bytes(8, 32, false) <= 232448 &&
                   smem_bytes(8, 64, false) <= 232448 && smem_bytes(8, 128, false) <= 232448 &&
-                  smem_bytes(8, 128, true, true) <= 232448,
+                  smem_bytes(8, 32, true, true) <= 232448 && smem_bytes(8, 64, true, true) <= 232448 &&
+                  smem_bytes(8, 128, true, true) <= 232448 && smem_bytes(8, 32, false, true) <= 232448 &&
+                  smem_bytes(8, 64, false, true) <= 232448 && smem_bytes(8, 128, false, true) <= 232448,
               "shared memory budget");
 
 struct TcParams {
@@ -807,13 +812,12 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   const long long nstreams = p.items < slots ? p.items : slots;
   dim3 grid(static_cast<unsigned>(pair ? 2 * nstreams : nstreams));
   const bool kf1 = p.kf == 1;
-  // DEEP: 8 stages with tree level 3 in scratch, for pair tiles at k_first > 1.
-  // Measured slower than 6 stages + level 3 on chip (1108 vs 1146 TFLOP/s at the
-  // bench shape, profiles/r01_tc_deep_vs_l3smem.txt): off unless TBIK_TC_DEEP=1
-  // (a pure scheduling knob -- same bits).
-  bool deep = false;
+  // DEEP (see stages_for) when the items have at most 2 tree levels; with 3+ the
+  // on-chip level 3 measured faster (1146 vs 1108 TFLOP/s at the bench shape).
+  // TBIK_TC_DEEP=0/1 forces it (a pure scheduling knob -- same bits).
+  bool deep = p.levels <= 2;
   if (const char* e = std::getenv("TBIK_TC_DEEP"))
-    if (*e) deep = pair && abox == 128 && !kf1 && std::atoi(e) != 0;
+    if (*e) deep = std::atoi(e) != 0;
   const int first_scratch = deep ? 3 : 4;
   if (p.levels >= first_scratch) {
     const size_t n = static_cast<size_t>(grid.x) * (p.levels - first_scratch + 1) * BM * BN;
@@ -830,15 +834,15 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
     TBIK_TRY(make_map_out(&mC, o.out, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.M),
                           static_cast<uint64_t>(p.units), static_cast<uint64_t>(o.ldo) * 4, ustride * 4));
   using Kern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
-  static const Kern table[2][3][2] = {
-      {{tc_tree_gemm_kernel<8, false, 32, false, false>, tc_tree_gemm_kernel<8, true, 32, false, false>},
-       {tc_tree_gemm_kernel<8, false, 64, false, false>, tc_tree_gemm_kernel<8, true, 64, false, false>},
-       {tc_tree_gemm_kernel<8, false, 128, false, false>, tc_tree_gemm_kernel<8, true, 128, false, false>}},
-      {{tc_tree_gemm_kernel<8, false, 32, true, false>, tc_tree_gemm_kernel<8, true, 32, true, false>},
-       {tc_tree_gemm_kernel<8, false, 64, true, false>, tc_tree_gemm_kernel<8, true, 64, true, false>},
-       {tc_tree_gemm_kernel<8, false, 128, true, false>, tc_tree_gemm_kernel<8, true, 128, true, false>}}};
+#define TBIK_TC_K(D, P)                                                                                  \
+  {{tc_tree_gemm_kernel<8, false, 32, P, D>, tc_tree_gemm_kernel<8, true, 32, P, D>},                   \
+   {tc_tree_gemm_kernel<8, false, 64, P, D>, tc_tree_gemm_kernel<8, true, 64, P, D>},                   \
+   {tc_tree_gemm_kernel<8, false, 128, P, D>, tc_tree_gemm_kernel<8, true, 128, P, D>}}
+  static const Kern table[2][2][3][2] = {{TBIK_TC_K(false, false), TBIK_TC_K(false, true)},
+                                         {TBIK_TC_K(true, false), TBIK_TC_K(true, true)}};
+#undef TBIK_TC_K
   const int ai = abox == 32 ? 0 : abox == 64 ? 1 : 2;
-  const Kern kern = deep ? tc_tree_gemm_kernel<8, false, 128, true, true> : table[pair][ai][kf1];
+  const Kern kern = table[deep][pair][ai][kf1];
   const int nthreads = 128 + 32 * 8;
   const size_t smem = smem_bytes(8, abox, pair, deep);
   static bool attr_set[16][2][3][2][2] = {};
