@@ -241,10 +241,17 @@ def run_tbik(args):
     rank, local_rank, world = env_rank()
     if world != args.gpus:
         world = args.gpus if world == 1 else world
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # TBIK_BENCH_SHARE_GPU=1: every rank on device 0 with a gloo control plane -- a
+    # functional check of the N > 1 path on a one-GPU box (timings meaningless).
+    share = os.environ.get("TBIK_BENCH_SHARE_GPU") == "1"
+    dev_index = 0 if share else local_rank
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     leaf = tb.LEAF_TCGEN05 if args.leaf == "tc" else tb.LEAF_FMA
     cfg = tb.BlockConfig(64, 256, 128, 0)
     M = args.m
@@ -262,7 +269,7 @@ def run_tbik(args):
 
     group = None
     if world > 1:
-        group = tb.PeerGroup(world, rank, local_rank, M * N_OUT, dist)
+        group = tb.PeerGroup(world, rank, dev_index, M * N_OUT, dist)
 
         def step():
             group.row_parallel_forward(x, w, K_FULL, cfg, 8, leaf, out=y)
@@ -277,7 +284,7 @@ def run_tbik(args):
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], device=dev)
+        t = torch.tensor([v], device="cpu" if share else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -285,7 +292,7 @@ def run_tbik(args):
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
-    clocks = Clocks(local_rank)
+    clocks = Clocks(dev_index)
     clocks.start()
     time.sleep(0.3)
     barrier()
@@ -299,6 +306,7 @@ def run_tbik(args):
     e1.record(s)
     torch.cuda.synchronize()
     launches = tb.launch_count() - launches0
+    y_step = y.clone()  # the step's result (y is reused below by the single-GPU roofline timing)
     barrier()
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
@@ -339,7 +347,7 @@ def run_tbik(args):
     for _ in range(2):
         e2e_step()
     torch.cuda.synchronize()
-    e2e_same = bool(torch.equal(y_host.view(torch.int32), y.cpu().view(torch.int32)))
+    e2e_same = bool(torch.equal(y_host.view(torch.int32), y_step.cpu().view(torch.int32)))
     barrier()
     e2e_ms = max_over_ranks(ev_time(e2e_step, max(args.steps // 2, 3)))
     e2e = {"value": flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
@@ -354,7 +362,7 @@ def run_tbik(args):
 
     def cublas_step():
         torch.matmul(x, w, out=yb)
-        if world > 1:
+        if world > 1 and not share:
             dist.all_reduce(yb)
 
     for _ in range(3):
@@ -400,7 +408,7 @@ def run_tbik(args):
     # ---- the metric's second half: bit-exact logits across TP on the Llama forward ----
     forward = None
     if rank == 0 and world == 1 and not args.no_forward:
-        del w, x, x_full, y, yb, x_host, y_host
+        del w, x, x_full, y, yb, x_host, y_host, y_step
         torch.cuda.empty_cache()
         from tools.forward_bench import run as forward_run
         try:
