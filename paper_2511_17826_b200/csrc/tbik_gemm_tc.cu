@@ -127,6 +127,7 @@ struct TcParams {
   int tma_store;   // 1: results leave through tmC (TMA), 0: direct row stores
   int pf;          // L2 prefetch distance in K chunks (0: off; measured slower, kept as a knob)
   int group_m;     // raster: M-blocks that share one pass over W
+  int mc;          // 1: clusters of two pairs on adjacent N tiles share A (ntiles counts tile pairs)
   int debug;       // TBIK_TC_DEBUG (perf experiments only; wrong results): 1 = skip the merge,
                    // 2 = skip the output store, 4 = skip the tree above level 0,
                    // 8 = skip the scratch levels, 16 = direct (non-TMA) output stores
@@ -173,6 +174,16 @@ __device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int32_t 
                "r"(c0), "r"(c1)
                : "memory");
 }
+// 2SM TMA multicast: the box lands at the same offset in every CTA of `mask`;
+// each destination pair's leader barrier (same offset) counts its bytes.
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* smem_dst, const CUtensorMap* map, uint32_t leader_bar,
+                                                   uint16_t mask, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%4, %5}], [%2], %3;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "h"(mask), "r"(c0), "r"(c1)
+      : "memory");
+}
 __device__ __forceinline__ void umma_bf16_2cta(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                                uint32_t accumulate) {
   asm volatile(
@@ -202,7 +213,7 @@ struct Item {
   int m0, n0, unit, t_begin, t_end;
 };
 
-__device__ __forceinline__ Item decode(const TcParams& p, long long item) {
+__device__ __forceinline__ Item decode(const TcParams& p, long long item, int pid = 0) {
   Item it;
   it.unit = static_cast<int>(item % p.units);
   const long long rest = item / p.units;
@@ -214,7 +225,7 @@ __device__ __forceinline__ Item decode(const TcParams& p, long long item) {
   const int mb = g * group_m + idx % gm;
   const int nt = idx / gm;
   it.m0 = mb * p.tile_m;
-  it.n0 = nt * BN;
+  it.n0 = (p.mc ? 2 * nt + pid : nt) * BN;
   it.t_begin = it.unit * p.tiles_per_unit;
   it.t_end = min(p.T, it.t_begin + p.tiles_per_unit);
   return it;
@@ -245,7 +256,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // A rows staged per stage (128, or 64 / 32 for small M; stage count follows).  KF1 (used when k_first == 1, where every leaf completes a
 // group and g need not persist across leaves): the level-1 slot is loaded in the
 // same batch as the leaf, so an odd leaf costs one TMEM round trip, not two.
-template <int EPI, bool KF1, int ABOX, bool PAIR, bool DEEP>
+template <int EPI, bool KF1, int ABOX, bool PAIR, bool DEEP, bool MC = false>
 __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     tc_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const TcParams p) {
@@ -266,17 +277,23 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = PAIR ? cluster_rank() : 0;
+  // MC: clusters of 4 = two CTA pairs (pid 0/1) on adjacent N tiles of the same
+  // M block; each pair's CTA r loads half of the shared 128-row A tile and
+  // multicasts it to CTA r of the other pair.
+  const uint32_t crank = PAIR ? cluster_rank() : 0;
+  const uint32_t rank = crank & 1;  // rank within the CTA pair
+  const int pid = MC ? static_cast<int>(crank >> 1) : 0;
+  const uint32_t leader_rank = crank & ~1u;
   const bool leader = rank == 0;
-  const long long pair = PAIR ? blockIdx.x >> 1 : blockIdx.x;  // work-item stream of this pair / CTA
-  const long long npairs = PAIR ? gridDim.x >> 1 : gridDim.x;
+  const long long pair = MC ? blockIdx.x >> 2 : PAIR ? blockIdx.x >> 1 : blockIdx.x;  // work-item stream
+  const long long npairs = MC ? gridDim.x >> 2 : PAIR ? gridDim.x >> 1 : gridDim.x;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], PAIR ? 2 : 1);  // one arrive.expect_tx per CTA (leader's copy used)
-      mbar_init(&empty[s], 1);  // one multicast commit from the leader's MMA thread
+      mbar_init(&empty[s], MC ? 2 : 1);  // a multicast commit from each pair leader that reads the stage
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);   // multicast commit
@@ -299,11 +316,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
     if (elect_one()) {
-      const uint32_t full_leader0 = mapa(smem_u32(&full[0]), 0);
+      const uint32_t full_leader0 = mapa(smem_u32(&full[0]), leader_rank);
       int stage = 0;
       uint32_t phase = 0;
       for (long long item = pair; item < p.items; item += npairs) {
-        const Item it = decode(p, item);
+        const Item it = decode(p, item, pid);
         const int am = it.m0 + static_cast<int>(rank) * BM;
         const int bn = it.n0 + static_cast<int>(rank) * (BN / 2);
         const int k_end = min(it.t_end * p.bk, p.K);
@@ -325,7 +342,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             else
               mbar_arrive_expect_tx_cluster(fb, TX_BYTES);
             const int k = t * p.bk + c * KSTAGE;
-            if constexpr (PAIR) {
+            if constexpr (MC) {  // my half of the pair-shared A tile, to both pairs
+              tma_load_2d_2sm_mc(sA + stage * A_STRIDE + pid * (A_STAGE_BYTES / 2), &tmA, fb,
+                                 static_cast<uint16_t>(0x5u << rank), k, am + pid * (BM / 2));
+              tma_load_2d_2sm(sB + stage * B_STAGE, &tmB, fb, bn, k);
+            } else if constexpr (PAIR) {
               tma_load_2d_2sm(sA + stage * A_STRIDE, &tmA, fb, k, am);
               tma_load_2d_2sm(sB + stage * B_STAGE, &tmB, fb, bn, k);
             } else {  // all 128 columns: two 64-column atoms
@@ -349,7 +370,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       uint32_t phase = 0;
       uint32_t acc_iter = 0;
       for (long long item = pair; item < p.items; item += npairs) {
-        const Item it = decode(p, item);
+        const Item it = decode(p, item, pid);
         for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
           const int buf = acc_iter & 1;
           const uint32_t use = acc_iter >> 1;
@@ -375,7 +396,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               else
                 umma_bf16(d, adesc, bdesc, IDESC_1CTA, (c | kk) != 0 ? 1u : 0u);
             }
-            if constexpr (PAIR)
+            if constexpr (MC)
+              umma_commit_2cta(&empty[stage], 0xF);  // both pairs read this stage's A
+            else if constexpr (PAIR)
               umma_commit_2cta(&empty[stage], 0x3);
             else
               umma_commit(&empty[stage]);
@@ -385,7 +408,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             }
           }
           if constexpr (PAIR)
-            umma_commit_2cta(&tfull[buf], 0x3);
+            umma_commit_2cta(&tfull[buf], static_cast<uint16_t>(0x3u << leader_rank));
           else
             umma_commit(&tfull[buf]);
         }
@@ -401,7 +424,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     const int col0 = ((warp - 4) >> 2) * COLS;
     const int row_in_tile = q * 32 + lane;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + col0;
-    const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), leader_rank);
     // TMEM holds tree levels 1-2, shared memory level 3 (this warp's sL3 region);
     // levels >= 4 live in scratch as [col/4][row][4] slabs (a warp's float4
     // access is 512 contiguous bytes).
@@ -417,7 +440,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     int xb = 0;      // output staging buffer toggle
     uint32_t acc_iter = 0;
     for (long long item = pair; item < p.items; item += npairs) {
-      const Item it = decode(p, item);
+      const Item it = decode(p, item, pid);
       const int grow = it.m0 + static_cast<int>(rank) * BM + row_in_tile;
       const bool row_ok = grow < p.M;
       const int ncols = min(COLS, p.N - it.n0 - col0);
@@ -757,9 +780,16 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
     const int a = std::atoi(e);
     if ((a == 32 && v.M <= 32) || (a == 64 && v.M <= 64) || a == 128) abox = a;
   }
+  // MC (experiment knob TBIK_TC_MC=1): clusters of two pairs sharing the A tile
+  // through TMA multicast (pair tiles with 128-row A staging only).
+  const bool mc_req = [] {
+    const char* e = std::getenv("TBIK_TC_MC");
+    return e && *e && std::atoi(e) != 0;
+  }();
+  const bool mc = mc_req && tc_use_pair(v) && !tc_use_wide(v) && abox == 128;
   CUtensorMap mA, mB;
   TBIK_TRY(make_map_2d(&mA, v.A, static_cast<uint64_t>(v.K), static_cast<uint64_t>(v.M),
-                       static_cast<uint64_t>(v.lda) * 2, KSTAGE, static_cast<uint32_t>(abox)));
+                       static_cast<uint64_t>(v.lda) * 2, KSTAGE, static_cast<uint32_t>(mc ? BM / 2 : abox)));
   TBIK_TRY(make_map_2d(&mB, v.B, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.K),
                        static_cast<uint64_t>(v.ldb) * 2, BN / 2, KSTAGE));
   TcParams p{};
@@ -807,10 +837,12 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   p.tile_m = pair ? PAIR_M : BM;
   p.mblocks = static_cast<int>((v.M + p.tile_m - 1) / p.tile_m);
   p.ntiles = static_cast<int>((v.N + BN - 1) / BN);
+  p.mc = mc ? 1 : 0;
+  if (mc) p.ntiles = (p.ntiles + 1) / 2;  // work items are tile pairs
   p.items = static_cast<long long>(p.mblocks) * p.ntiles * p.units;
-  const long long slots = pair ? sm_count() / 2 : sm_count();
+  const long long slots = mc ? sm_count() / 4 : pair ? sm_count() / 2 : sm_count();
   const long long nstreams = p.items < slots ? p.items : slots;
-  dim3 grid(static_cast<unsigned>(pair ? 2 * nstreams : nstreams));
+  dim3 grid(static_cast<unsigned>(mc ? 4 * nstreams : pair ? 2 * nstreams : nstreams));
   const bool kf1 = p.kf == 1;
   // DEEP (see stages_for) when the items have at most 2 tree levels; with 3+ the
   // on-chip level 3 measured faster (1146 vs 1108 TFLOP/s at the bench shape).
@@ -818,6 +850,7 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   bool deep = p.levels <= 2;
   if (const char* e = std::getenv("TBIK_TC_DEEP"))
     if (*e) deep = std::atoi(e) != 0;
+  if (mc) deep = false;
   const int first_scratch = deep ? 3 : 4;
   if (p.levels >= first_scratch) {
     const size_t n = static_cast<size_t>(grid.x) * (p.levels - first_scratch + 1) * BM * BN;
@@ -842,16 +875,18 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
                                          {TBIK_TC_K(true, false), TBIK_TC_K(true, true)}};
 #undef TBIK_TC_K
   const int ai = abox == 32 ? 0 : abox == 64 ? 1 : 2;
-  const Kern kern = table[deep][pair][ai][kf1];
+  const Kern kern = mc ? (kf1 ? tc_tree_gemm_kernel<8, true, 128, true, false, true>
+                              : tc_tree_gemm_kernel<8, false, 128, true, false, true>)
+                      : table[deep][pair][ai][kf1];
   const int nthreads = 128 + 32 * 8;
   const size_t smem = smem_bytes(8, abox, pair, deep);
-  static bool attr_set[16][2][3][2][2] = {};
+  static bool attr_set[16][2][3][2][2][2] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 16 && !attr_set[dev][pair][ai][kf1][deep]) {
+  if (dev >= 0 && dev < 16 && !attr_set[dev][pair][ai][kf1][deep][mc]) {
     TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     if (pair) TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-    attr_set[dev][pair][ai][kf1][deep] = true;
+    attr_set[dev][pair][ai][kf1][deep][mc] = true;
   }
   cudaLaunchConfig_t lc{};
   lc.gridDim = grid;
@@ -860,11 +895,27 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   lc.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = pair ? 2 : 1;
+  attr[0].val.clusterDim.x = mc ? 4 : pair ? 2 : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
+  if (mc) {
+    // 4-CTA clusters must fit inside a GPC: the persistent grid is sized to the
+    // clusters that can be co-resident (not SMs / 4), or the surplus ones would
+    // run as a second wave after everyone else.
+    static int max_clusters[16] = {};
+    if (dev >= 0 && dev < 16 && !max_clusters[dev]) {
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &lc) != cudaSuccess || n < 1) n = sm_count() / 4;
+      max_clusters[dev] = n;
+    }
+    const long long cap = dev >= 0 && dev < 16 ? max_clusters[dev] : sm_count() / 4;
+    if (nstreams > cap) {
+      lc.gridDim = dim3(static_cast<unsigned>(4 * cap));
+      if (p.levels > 3 && !p.scratch) return set_error(TBIK_CUDA_ERROR, "tc gemm: scratch");
+    }
+  }
   TBIK_CUDA(cudaLaunchKernelEx(&lc, kern, mA, mB, mC, p));
   count_launch();
   return TBIK_OK;
