@@ -167,6 +167,17 @@ def ev_time(fn, reps, stream=None):
 # ------------------------------------------------------------------------------------
 # reference arm: the unmodified reference library on the host cores
 # ------------------------------------------------------------------------------------
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_sample(tp: int, m_sample: int, budget_s: float, min_reps: int = 1):
     import numpy as np
 
@@ -185,7 +196,15 @@ def cpu_reference_sample(tp: int, m_sample: int, budget_s: float, min_reps: int 
     best = min(times)
     flops = 2.0 * m_sample * N_OUT * K_FULL
     fp = ref.fingerprint(np.ascontiguousarray(y))
+    # one-thread point: a single call on M=1 row
+    ref.set_threads(1)
+    a1 = a[:1].copy()
+    t0 = time.perf_counter()
+    ref.row_parallel_forward(a1, w, tp)
+    t1 = time.perf_counter() - t0
+    ref.set_threads(threads)
     return {"value": flops / best / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
+            "cpu_model": cpu_model(), "one_thread_m1_tflops": 2.0 * N_OUT * K_FULL / t1 / 1e12,
             "sample": f"row_parallel_forward(DeviceGroup({tp})) on M={m_sample} rows of the "
                       f"{K_FULL}x{N_OUT} down_proj, bf16 N(0,1) Rng(1,1)/(1,2), best of {len(times)} "
                       f"wall-clock runs ({sum(times):.1f} s of CPU work), TBIK_THREADS={threads}",
@@ -222,6 +241,7 @@ def run_reference(args):
                    "K": K_FULL, "N": N_OUT, "tp": tp, "parallelism": f"tp{tp} (simulated ranks on host threads)",
                    "block_k": 256},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
                          "sample": f"row_parallel_forward(DeviceGroup({tp})) M={m_sample} rows per step"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "fingerprint": "0x%016x" % ref.fingerprint(np.ascontiguousarray(y)),
