@@ -425,6 +425,25 @@ def run_tbik(args):
             sweep["tbik_fma_tflops"].append(f / (t_fma * 1e-3) / 1e12 if t_fma else None)
             sweep["cublas_bf16_tflops"].append(f / (t_cb * 1e-3) / 1e12)
 
+    # ---- per-rank GEMM of each TP shard (rank 0, N = 1): the compute side of TP = 2/4/8 ----
+    tp_shards = None
+    if rank == 0 and world == 1 and not args.no_sweep:
+        tp_shards = {"note": "rank 0's row-parallel shard GEMM (K/tp, global k_first) on this GPU; the NVLink "
+                             "all-reduce is not in these numbers (one GPU)", "tp": [], "per_rank_tflops": [],
+                     "per_rank_ms": []}
+        for t in (1, 2, 4, 8):
+            sp = tb.make_row_shard_plan(K_FULL, cfg, t, 8)
+            kb0, ke0 = sp.bounds[0]
+            xs_t = x_full[:, kb0:ke0].contiguous()
+            ws_t = w[kb0:ke0].contiguous() if world == 1 else None
+            cfg_t = tb.BlockConfig(64, 256, 128, tb.plan_blocks(K_FULL, cfg, 8).k_first)
+            yt = torch.empty(M, N_OUT, device=dev)
+            ms_t = ev_time(lambda: tb.tree_matmul(xs_t, ws_t, cfg_t, leaf, out=yt), max(args.steps, 5))
+            tp_shards["tp"].append(t)
+            tp_shards["per_rank_ms"].append(ms_t)
+            tp_shards["per_rank_tflops"].append(2.0 * M * N_OUT * (ke0 - kb0) / (ms_t * 1e-3) / 1e12)
+            del xs_t, ws_t, yt
+
     # ---- the metric's second half: bit-exact logits across TP on the Llama forward ----
     forward = None
     if rank == 0 and world == 1 and not args.no_forward:
@@ -467,6 +486,7 @@ def run_tbik(args):
                        "l2": "no flush: per-step inputs+output (x 117 MB + W 117 MB + y 67 MB at tp1) exceed the 126 MB L2"},
             "roofline": roof, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "noninvariant": noninv, "tp_invariance_bit_identical": tp_ok, "sweep": sweep,
+            "tp_shard_gemm": tp_shards,
             "cpu_baseline": cpu,
             "forward": forward,
             "rowops_c5": rowops,

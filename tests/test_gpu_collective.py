@@ -79,23 +79,27 @@ def _free_port() -> int:
     return p
 
 
-def test_peer_group_two_processes(tb, cuda, tmp_path):
-    """Two ranks (processes) run the IPC group end to end: row-parallel down_proj
-    shards -> peer-visible buffers -> flag barrier -> tree all-reduce.  Both ranks
-    must produce bit-identical outputs equal to the single-process TP=1 result."""
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_group_processes(tb, cuda, tmp_path, world):
+    """`world` ranks (processes sharing this GPU) run the IPC group end to end:
+    row-parallel down_proj shards -> peer-visible buffers -> flag barriers -> tree
+    all-reduce (one-shot and two-phase), the overlapped chunk pipeline and the
+    host-buffer path.  Every rank must produce bit-identical outputs equal to the
+    single-process TP=1 result."""
     worker = os.path.join(ROOT, "tests", "peer_group_worker.py")
     port = _free_port()
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE="2")
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world))
     procs = []
-    for r in range(2):
+    for r in range(world):
         e = dict(env, RANK=str(r), LOCAL_RANK="0", TBIK_TEST_OUT=str(tmp_path / f"rank{r}.npy"))
         procs.append(subprocess.Popen([sys.executable, worker], env=e, stdout=subprocess.PIPE,
                                       stderr=subprocess.STDOUT, text=True))
-    outs = [p.communicate(timeout=240)[0] for p in procs]
+    outs = [p.communicate(timeout=420)[0] for p in procs]
     for p, o in zip(procs, outs):
         assert p.returncode == 0, o
-    y0 = np.load(tmp_path / "rank0.npy")
-    y1 = np.load(tmp_path / "rank1.npy")
-    assert np.array_equal(bits(y0), bits(y1)), "ranks diverged"
+    ys = [np.load(tmp_path / f"rank{r}.npy") for r in range(world)]
+    for r in range(1, world):
+        assert np.array_equal(bits(ys[0]), bits(ys[r])), f"rank {r} diverged"
+    y0 = ys[0]
     ref = np.load(tmp_path / "rank0.npy.ref.npy")
     assert np.array_equal(bits(y0), bits(ref)), "group result != TP=1 result"
