@@ -96,11 +96,15 @@ constexpr int stages_for(int abox, bool pair, bool deep = false) {
   return deep ? (pair ? (abox == 32 ? 15 : abox == 64 ? 11 : 8) : (abox == 32 ? 9 : abox == 64 ? 7 : 6))
               : (pair ? (abox == 32 ? 12 : abox == 64 ? 9 : STAGES) : (abox == 32 ? 7 : abox == 64 ? 6 : 4));
 }
-constexpr int warp_region_bytes(bool deep) { return deep ? OUT_BUF_BYTES : L3_WARP_BYTES; }
+// Per merge warp: level-3 slab (32 rows x its columns) that doubles as output
+// staging; 16 merge warps own 32 columns each (4 KB, one staging box).
+constexpr int warp_region_bytes(bool deep, int epi = 8) {
+  return deep || epi == 16 ? OUT_BUF_BYTES : L3_WARP_BYTES;
+}
 constexpr size_t smem_bytes(int epi, int abox, bool pair, bool deep = false) {
   return 1024 + static_cast<size_t>(a_region_bytes(abox, stages_for(abox, pair, deep))) +
          static_cast<size_t>(stages_for(abox, pair, deep)) * b_stage_bytes(pair) + 1024 +
-         static_cast<size_t>(epi) * warp_region_bytes(deep);
+         static_cast<size_t>(epi) * warp_region_bytes(deep, epi);
 }
 static_assert(smem_bytes(8, 32, true) <= 232448 && smem_bytes(8, 64, true) <= 232448 &&
                   smem_bytes(8, 128, true) <= 232448 && smem_bytes(8, 32, false) <= 232448 &&
@@ -434,7 +438,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             ? p.scratch + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - FS + 1) * (BM * BN) +
                            static_cast<size_t>(col0) * BM + static_cast<size_t>(row_in_tile) * 4
             : nullptr;
-    uint8_t* l3 = sL3 + (warp - 4) * warp_region_bytes(DEEP);  // [16][32 lanes][float4] (+ staging)
+    uint8_t* l3 = sL3 + (warp - 4) * warp_region_bytes(DEEP, EPI);  // [COLS/4][32 lanes][float4] (+ staging)
+    constexpr bool ONE_BOX = DEEP || EPI == 16;  // a single staging box per warp
 
     float g[COLS];  // level 0: the running leaf-group value
     int xb = 0;      // output staging buffer toggle
@@ -456,7 +461,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         // odd group: each leaf chunk together with the level-1 slot chunk it merges
         // with); the accumulator goes back to the MMA issuer as soon as the values
         // are in registers.
-        uint32_t r[NCH][32];
+        uint32_t r[NCH < 2 ? 2 : NCH][32];
         const bool odd = KF1 && p.levels >= 1 && (groups_done & 1u);
         if (!(p.debug & 1)) {
           if (odd) {
@@ -595,13 +600,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
             if (lane == 0) {
-              if constexpr (DEEP)
+              if constexpr (ONE_BOX)
                 bulk_wait_read<0>();  // one staging box per warp
               else
                 bulk_wait_read<1>();
             }
             __syncwarp();
-            uint8_t* sbuf = l3 + (DEEP ? 0 : xb * OUT_BUF_BYTES);
+            uint8_t* sbuf = l3 + (ONE_BOX ? 0 : xb * OUT_BUF_BYTES);
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               *reinterpret_cast<float4*>(sbuf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
@@ -875,18 +880,27 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
                                          {TBIK_TC_K(true, false), TBIK_TC_K(true, true)}};
 #undef TBIK_TC_K
   const int ai = abox == 32 ? 0 : abox == 64 ? 1 : 2;
+  // EPI16 (experiment knob TBIK_TC_EPI=16): 16 merge warps of 32 columns, pair
+  // tiles with 128-row staging, not DEEP / MC.
+  const bool epi16 = [] {
+    const char* e = std::getenv("TBIK_TC_EPI");
+    return e && std::atoi(e) == 16;
+  }() && pair && abox == 128 && !deep && !mc;
   const Kern kern = mc ? (kf1 ? tc_tree_gemm_kernel<8, true, 128, true, false, true>
                               : tc_tree_gemm_kernel<8, false, 128, true, false, true>)
-                      : table[deep][pair][ai][kf1];
-  const int nthreads = 128 + 32 * 8;
-  const size_t smem = smem_bytes(8, abox, pair, deep);
-  static bool attr_set[16][2][3][2][2][2] = {};
+                   : epi16 ? (kf1 ? tc_tree_gemm_kernel<16, true, 128, true, false, false>
+                                  : tc_tree_gemm_kernel<16, false, 128, true, false, false>)
+                           : table[deep][pair][ai][kf1];
+  const int epi = epi16 ? 16 : 8;
+  const int nthreads = 128 + 32 * epi;
+  const size_t smem = smem_bytes(epi, abox, pair, deep);
+  static bool attr_set[16][2][3][2][2][2][2] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 16 && !attr_set[dev][pair][ai][kf1][deep][mc]) {
+  if (dev >= 0 && dev < 16 && !attr_set[dev][pair][ai][kf1][deep][mc][epi16]) {
     TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     if (pair) TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-    attr_set[dev][pair][ai][kf1][deep][mc] = true;
+    attr_set[dev][pair][ai][kf1][deep][mc][epi16] = true;
   }
   cudaLaunchConfig_t lc{};
   lc.gridDim = grid;
