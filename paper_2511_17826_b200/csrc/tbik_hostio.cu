@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "tbik_common.cuh"
 #include "tbik_internal.h"
@@ -72,8 +73,24 @@ tbik_status pipeline(const void* A_host, int adt, int64_t lda, int64_t K, float*
                      int64_t N, int64_t chunk, cudaStream_t s, F compute) {
   HostIoCtx* cx = nullptr;
   TBIK_TRY(ctx_for_device(&cx));
-  if (chunk <= 0) chunk = default_chunk(M);
-  chunk = std::min(chunk, M);
+  // Row chunks: a fixed size when the caller asks for one; by default ramped
+  // (128, 256, then up to 512, then 256, 128) so the pipeline fills and drains on
+  // small copies while the bulk moves in large ones.
+  std::vector<int64_t> sizes;
+  if (chunk > 0) {
+    chunk = std::min(chunk, M);
+    for (int64_t r = 0; r < M; r += chunk) sizes.push_back(std::min(chunk, M - r));
+  } else if (M >= 1024) {
+    chunk = default_chunk(M);
+    const int64_t mid = M - 768;
+    sizes = {128, 256};
+    for (int64_t r = 0; r < mid; r += chunk) sizes.push_back(std::min(chunk, mid - r));
+    sizes.push_back(256);
+    sizes.push_back(128);
+  } else {
+    chunk = std::min(default_chunk(M), M);
+    for (int64_t r = 0; r < M; r += chunk) sizes.push_back(std::min(chunk, M - r));
+  }
   const size_t es = esize(adt);
   const size_t a_bytes = static_cast<size_t>(chunk) * K * es, c_bytes = static_cast<size_t>(chunk) * N * 4;
   char* dA[2];
@@ -85,10 +102,11 @@ tbik_status pipeline(const void* A_host, int adt, int64_t lda, int64_t K, float*
   }
   TBIK_CUDA(cudaEventRecord(cx->start, s));
   TBIK_CUDA(cudaStreamWaitEvent(cx->h2d, cx->start, 0));
-  const int64_t nchunks = (M + chunk - 1) / chunk;
-  for (int64_t i = 0; i < nchunks; ++i) {
+  const int64_t nchunks = static_cast<int64_t>(sizes.size());
+  int64_t r0 = 0;
+  for (int64_t i = 0; i < nchunks; r0 += sizes[i], ++i) {
     const int b = static_cast<int>(i & 1);
-    const int64_t r0 = i * chunk, rows = std::min(chunk, M - r0);
+    const int64_t rows = sizes[i];
     if (i >= 2) TBIK_CUDA(cudaStreamWaitEvent(cx->h2d, cx->comp_done[b], 0));  // dA[b] consumed
     if (lda == K)  // contiguous rows: one linear copy (the 2D path is slower on the copy engines)
       TBIK_CUDA(cudaMemcpyAsync(dA[b], static_cast<const char*>(A_host) + r0 * lda * es, rows * K * es,
