@@ -128,6 +128,16 @@ TBIK_API tbik_status tbik_tree_matmul(const void* A, int a_dtype, int64_t lda, c
                              int64_t ldb, float* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
                              const tbik_block_config* cfg, int leaf_mode, void* stream);
 
+/* The gate_up projection with SiLU(gate) * up fused (demo.cpp:171-174): B's 2*I
+ * columns interleave gate_j (column 2j) and up_j (column 2j+1); the tree GEMM's
+ * f32 values g feed act[M x I] (bf16, ld_act) = bf16(silu(g[2j]) * g[2j+1]) --
+ * bit-identical to tbik_tree_matmul followed by the same SiLU*up (the epilogue
+ * runs in the tcgen05 kernel when it can, otherwise through a workspace). */
+TBIK_API tbik_status tbik_tree_matmul_silu_mul(const void* A, int a_dtype, int64_t lda, const void* B,
+                                      int b_dtype, int64_t ldb, void* act, int64_t ld_act, int64_t M,
+                                      int64_t I, int64_t K, const tbik_block_config* cfg, int leaf_mode,
+                                      void* stream);
+
 /* Debug / verification entry: write every leaf partial product P_t
  * (t = 0..tiles_total-1) to leaves[t][M][N] (f32, dense) using the given leaf
  * mode.  tests/ feed these to the CPU oracle's tree to check the tree logic

@@ -86,6 +86,7 @@ _SIGS = {
     "tbik_make_column_shard_plan": (ci, [i64, ci, PI64]),
     "tbik_tree_matmul": (ci, [vp, ci, i64, vp, ci, i64, PF, i64, i64, i64, i64, PCFG, ci, vp]),
     "tbik_tree_matmul_leaves": (ci, [vp, ci, i64, vp, ci, i64, PF, i64, i64, i64, PCFG, ci, vp]),
+    "tbik_tree_matmul_silu_mul": (ci, [vp, ci, i64, vp, ci, i64, vp, i64, i64, i64, i64, PCFG, ci, vp]),
     "tbik_column_parallel_forward_local": (ci, [vp, ci, i64, vp, ci, i64, PF, i64, i64, i64, i64, ci,
                                                 PCFG, ci, vp]),
     "tbik_row_parallel_forward_local": (ci, [vp, ci, i64, vp, ci, i64, PF, i64, i64, i64, i64, ci,

@@ -294,6 +294,40 @@ def column_parallel_forward(x, w, group: DeviceGroup, cfg: BlockConfig | None = 
     return out
 
 
+def interleave_gate_up(w):
+    """[gate | up] (K x 2I) -> columns interleaved gate_0, up_0, gate_1, up_1, ... --
+    the B layout of tree_matmul_silu_mul (a pure column permutation: each column's
+    tree GEMM is unchanged)."""
+    K, N2 = w.shape
+    inter = N2 // 2
+    return w.view(K, 2, inter).transpose(1, 2).reshape(K, N2).contiguous()
+
+
+def tree_matmul_silu_mul(x, w_il, group: DeviceGroup | None = None, cfg: BlockConfig | None = None,
+                         leaf: int = LEAF_TCGEN05, out=None):
+    """bf16(silu(x @ W_gate) * (x @ W_up)) with W's columns interleaved (interleave_gate_up),
+    column-parallel over `group`'s simulated ranks: rank r owns gate/up pairs
+    [r I/tp, (r+1) I/tp) (layers.cpp:48-72).  SiLU*up runs in the GEMM epilogue."""
+    torch = _torch()
+    cfg = cfg or default_block_config(BF16)
+    tp = group.world_size() if group is not None else 1
+    M, K = x.shape
+    N2 = w_il.shape[1]
+    inter = N2 // 2
+    if w_il.shape[0] != K or N2 % 2 or inter % tp:
+        raise TbikError(ErrorCode.ShapeMismatch, "tree_matmul_silu_mul: bad shapes")
+    out = torch.empty((M, inter), dtype=torch.bfloat16, device=x.device) if out is None else out
+    px, dx, ldx = _mat(x, "X")
+    _, dw, ldw = _mat(w_il, "W")
+    ir = inter // tp
+    for r in range(tp):
+        pw = C.c_void_p(w_il.data_ptr() + 2 * ir * r * w_il.element_size())
+        po = C.c_void_p(out.data_ptr() + ir * r * out.element_size())
+        check(lib.tbik_tree_matmul_silu_mul(px, dx, ldx, pw, dw, ldw, po, out.stride(0), M, ir, K,
+                                            C.byref(cfg.c()), leaf, _stream()))
+    return out
+
+
 # ---- tree-ordered reductions ----------------------------------------------------------
 def rmsnorm(x, gamma, eps: float = 1e-5, out_dtype=None):
     """rmsnorm (demo.hpp:53) with the canonical tree sum of squares."""

@@ -161,25 +161,30 @@ tbik_status pad_operand(const void** p, int64_t* ld, int64_t rows, int64_t cols,
   return TBIK_OK;
 }
 
+int64_t tc_split_units(const GemmView& v) {
+  const int64_t tiles_mn = tc_tiles(v);
+  // Split the K range of each output tile into 2^j aligned subtrees only when
+  // the machine would otherwise idle; the combine continues the same tree
+  // (Theorem 1), so the split never changes bits.  Measured on B200
+  // (tools/tune_units.py, tools/tune_small.py, K=14336 N=4096): split until the
+  // work items fill ~7/8 of the concurrent slots (74 CTA pairs / 148 CTAs) and
+  // no further (2 for 32 pair tiles, 4 for 32 single-CTA tiles); deeper splits
+  // lose to the extra subtree traffic and the per-item pipeline refill.
+  const int64_t enough = tc_parallel_slots(v) * 7 / 8;
+  int64_t units = 1;
+  while (units * 2 <= v.L && tiles_mn * units * 2 <= enough) units *= 2;
+  (void)next_pow2;
+  if (const char* e = std::getenv("TBIK_TC_UNITS")) {  // tuning override (power of two <= leaves)
+    const int64_t u = std::atoll(e);
+    if (u >= 1 && u <= v.L && (u & (u - 1)) == 0) units = u;
+  }
+  return units;
+}
+
 tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mode, cudaStream_t s) {
   const size_t slice = static_cast<size_t>(v.M) * v.N;
   if (leaf_mode == TBIK_LEAF_TCGEN05) {
-    const int64_t tiles_mn = tc_tiles(v);
-    // Split the K range of each output tile into 2^j aligned subtrees only when
-    // the machine would otherwise idle; the combine continues the same tree
-    // (Theorem 1), so the split never changes bits.  Measured on B200
-    // (tools/tune_units.py, tools/tune_small.py, K=14336 N=4096): split until the
-    // work items fill ~7/8 of the concurrent slots (74 CTA pairs / 148 CTAs) and
-    // no further (2 for 32 pair tiles, 4 for 32 single-CTA tiles); deeper splits
-    // lose to the extra subtree traffic and the per-item pipeline refill.
-    const int64_t enough = tc_parallel_slots(v) * 7 / 8;
-    int64_t units = 1;
-    while (units * 2 <= v.L && tiles_mn * units * 2 <= enough) units *= 2;
-    (void)next_pow2;
-    if (const char* e = std::getenv("TBIK_TC_UNITS")) {  // tuning override (power of two <= leaves)
-      const int64_t u = std::atoll(e);
-      if (u >= 1 && u <= v.L && (u & (u - 1)) == 0) units = u;
-    }
+    const int64_t units = tc_split_units(v);
     if (units <= 1) {
       GemmOut o{OUT_FULL, v.T, C, ldc, 0};
       return launch_tc_gemm(v, o, s);
@@ -322,6 +327,30 @@ tbik_status tbik_tree_matmul(const void* A, int a_dtype, int64_t lda, const void
   GemmView v;
   TBIK_TRY(make_view(A, a_dtype, lda, B, b_dtype, ldb, M, N, K, cfg->block_k, cfg->k_first, &v));
   return run_tree_gemm(v, C, ldc, leaf_mode, static_cast<cudaStream_t>(stream));
+}
+
+tbik_status tbik_tree_matmul_silu_mul(const void* A, int a_dtype, int64_t lda, const void* B, int b_dtype,
+                                      int64_t ldb, void* act, int64_t ld_act, int64_t M, int64_t I, int64_t K,
+                                      const tbik_block_config* cfg, int leaf_mode, void* stream) {
+  if (!cfg || !act) return set_error(TBIK_BAD_ARGUMENT, "null argument");
+  if (I < 1) return set_error(TBIK_BAD_DIMENSION, "silu_mul: inter must be >= 1");
+  const int64_t N = 2 * I;
+  TBIK_TRY(check_mat(A, a_dtype, M, K, lda, "A"));
+  TBIK_TRY(check_mat(B, b_dtype, K, N, ldb, "B"));
+  if (ld_act < I) return set_error(TBIK_BAD_ARGUMENT, "act: leading dimension < inter");
+  TBIK_TRY(require_device());
+  GemmView v;
+  TBIK_TRY(make_view(A, a_dtype, lda, B, b_dtype, ldb, M, N, K, cfg->block_k, cfg->k_first, &v));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (leaf_mode == TBIK_LEAF_TCGEN05 && tc_split_units(v) <= 1) {
+    GemmOut o{OUT_FULL, v.T, nullptr, N, 0, static_cast<uint16_t*>(act), ld_act};
+    return launch_tc_gemm(v, o, s);  // SiLU*up in the GEMM epilogue
+  }
+  // split launches / exact leaf: f32 tree GEMM, then the same SiLU*up as a kernel
+  float* tmp = static_cast<float*>(workspace(static_cast<size_t>(M) * N * sizeof(float), 10));
+  if (!tmp) return set_error(TBIK_CUDA_ERROR, "workspace allocation failed");
+  TBIK_TRY(run_tree_gemm(v, tmp, N, leaf_mode, s));
+  return launch_silu_mul_il(tmp, N, M, I, static_cast<uint16_t*>(act), ld_act, s);
 }
 
 tbik_status tbik_tree_matmul_leaves(const void* A, int a_dtype, int64_t lda, const void* B, int b_dtype,

@@ -50,6 +50,7 @@
 
 #include "tbik_common.cuh"
 #include "tbik_internal.h"
+#include "tbik_mathfn.cuh"
 
 namespace tbik_b200 {
 
@@ -132,6 +133,8 @@ struct TcParams {
   int pf;          // L2 prefetch distance in K chunks (0: off; measured slower, kept as a knob)
   int group_m;     // raster: M-blocks that share one pass over W
   int mc;          // 1: clusters of two pairs on adjacent N tiles share A (ntiles counts tile pairs)
+  uint16_t* act;   // non-null: SiLU*up epilogue -- columns interleave gate (even) / up (odd);
+  long long ld_act;  //   act[row][j] = bf16(silu(g[2j]) * g[2j+1]) replaces the f32 store
   int debug;       // TBIK_TC_DEBUG (perf experiments only; wrong results): 1 = skip the merge,
                    // 2 = skip the output store, 4 = skip the tree above level 0,
                    // 8 = skip the scratch levels, 16 = direct (non-TMA) output stores
@@ -594,7 +597,31 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         }
         }  // the carry left the top level: g is this unit's complete (sub)tree
         if (p.debug & 2) continue;
-        if (p.tma_store) {
+        if (p.act) {
+          // fused SiLU(gate) * up (tb_silu_mul_bf16, the same ops as tbik_silu_mul):
+          // this thread's 64 columns are 32 (gate, up) pairs -> 32 bf16 outputs
+          if (row_ok) {
+            uint16_t* dst = p.act + static_cast<size_t>(grow) * p.ld_act + (it.n0 + col0) / 2;
+            const int npair = ncols / 2;
+            if (npair == COLS / 2 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+              for (int q8 = 0; q8 < COLS / 16; ++q8) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int c = q8 * 16 + 4 * e;
+                  w[e] = static_cast<uint32_t>(tb_silu_mul_bf16(g[c], g[c + 1])) |
+                         (static_cast<uint32_t>(tb_silu_mul_bf16(g[c + 2], g[c + 3])) << 16);
+                }
+                *reinterpret_cast<uint4*>(dst + q8 * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+              }
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < COLS / 2; ++jj)
+                if (jj < npair) dst[jj] = tb_silu_mul_bf16(g[2 * jj], g[2 * jj + 1]);
+            }
+          }
+        } else if (p.tma_store) {
           // Row-per-lane registers -> 128B-swizzled 32 x 32 smem box (conflict-free
           // 16 B stores) -> one TMA store per box; the tensor map clips ragged edges.
 #pragma unroll
@@ -777,7 +804,7 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   std::string why;
   if (!tc_supported(v, &why)) return set_error(TBIK_UNSUPPORTED, why);
   if (o.mode == OUT_GROUPS) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: GROUPS mode is FMA-only");
-  if (tc_use_wide(v)) return launch_tc_gemm_wide(v, o, s);
+  if (tc_use_wide(v) && !o.act) return launch_tc_gemm_wide(v, o, s);
   // A rows staged per stage: the fewest that still cover every row of the pair
   // tile's leader CTA (TBIK_TC_ABOX overrides, a pure scheduling knob).
   int abox = v.M <= 32 ? 32 : v.M <= 64 ? 64 : 128;
@@ -808,6 +835,9 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   p.out = o.out;
   p.ldo = o.ldo;
   p.unit_stride = o.unit_stride;
+  p.act = o.act;
+  p.ld_act = o.ld_act;
+  if (o.act && (o.mode != OUT_FULL || v.N % 2)) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: SiLU epilogue needs FULL mode and even N");
   if (o.mode == OUT_LEAVES) {
     p.tiles_per_unit = 1;
     p.levels = 0;
@@ -867,7 +897,8 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   std::memset(&mC, 0, sizeof(mC));
   const uint64_t ustride = o.mode != OUT_FULL ? static_cast<uint64_t>(o.unit_stride)
                                               : static_cast<uint64_t>(o.ldo) * static_cast<uint64_t>(v.M);
-  p.tma_store = !(dbg & 16) && (reinterpret_cast<uintptr_t>(o.out) & 15) == 0 && o.ldo % 4 == 0 && ustride % 4 == 0;
+  p.tma_store = !o.act && !(dbg & 16) && (reinterpret_cast<uintptr_t>(o.out) & 15) == 0 && o.ldo % 4 == 0 &&
+                ustride % 4 == 0;
   if (p.tma_store)
     TBIK_TRY(make_map_out(&mC, o.out, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.M),
                           static_cast<uint64_t>(p.units), static_cast<uint64_t>(o.ldo) * 4, ustride * 4));

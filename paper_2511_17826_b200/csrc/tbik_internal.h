@@ -43,6 +43,8 @@ struct GemmOut {
   float* out;          // C (FULL) or workspace base
   int64_t ldo;         // row stride of C / of one workspace slice (= N)
   int64_t unit_stride; // elements between workspace slices
+  uint16_t* act = nullptr;  // FULL only: write bf16(silu(gate) * up) of interleaved column pairs here
+  int64_t ld_act = 0;       //   (row stride in elements; `out` is unused then)
 };
 
 tbik_status launch_fma_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s);
@@ -70,6 +72,14 @@ tbik_status launch_allreduce(const PartPtrs& parts, int W, float* out, int64_t e
 // Copies a bf16 operand whose row stride or base is not 16-byte aligned into a
 // padded buffer (workspace slot `slot`); no-op otherwise.
 tbik_status pad_operand(const void** p, int64_t* ld, int64_t rows, int64_t cols, int slot, cudaStream_t s);
+
+// bf16(silu(gate) * up) over an f32 [rows x 2*inter] matrix whose columns
+// interleave gate_j (2j) and up_j (2j+1) (tbik_model.cu).
+tbik_status launch_silu_mul_il(const float* gu, int64_t ld, int64_t rows, int64_t inter, uint16_t* out, int64_t ldo,
+                               cudaStream_t s);
+
+// K-split factor run_tree_gemm uses for the tcgen05 leaf (1 = one FULL launch).
+int64_t tc_split_units(const GemmView& v);
 
 // Whole tree GEMM (plan resolved by the caller): picks FULL vs split + combine.
 tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mode, cudaStream_t s);

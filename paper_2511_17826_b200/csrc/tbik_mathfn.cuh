@@ -63,6 +63,16 @@ __device__ __forceinline__ float tb_exp_nonpos(float x) {
   return x < -103.0f ? 0.0f : res;
 }
 
+// bf16(silu(z) * up), silu(z) = z / (1 + exp(-z))  (demo.cpp:36-45, :171-174) -- the
+// one definition used by the SiLU*up kernel and the gate_up GEMM epilogue.
+__device__ __forceinline__ uint16_t tb_silu_mul_bf16(float z, float up) {
+  const float sl = __fdiv_rn(z, __fadd_rn(1.0f, tb_exp(-z)));
+  const float r = __fmul_rn(sl, up);
+  const uint32_t u = __float_as_uint(r);
+  if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu) != 0) return 0x7FC0;
+  return static_cast<uint16_t>((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+}
+
 __device__ __forceinline__ float tb_log(float x) {
   if (!(x > 0.0f)) return x == 0.0f ? __int_as_float(0xFF800000) : __int_as_float(0x7FC00000);
   if (x == __int_as_float(0x7F800000)) return x;

@@ -245,9 +245,18 @@ __global__ void __launch_bounds__(4 * AQ, 3) attn2_kernel(const uint16_t* __rest
 
 // ---- SiLU(gate) * up  (demo.cpp:36-45, :171-174) ---------------------------------------
 // gu: f32 [M, ld] with gate in columns [0, I) and up in [I, 2I).  silu(z) = z / (1 + exp(-z)).
-__device__ __forceinline__ uint16_t silu_mul1(float z, float up) {
-  const float s = __fdiv_rn(z, __fadd_rn(1.0f, tb_exp(-z)));
-  return f32_to_bf16_bits(__fmul_rn(s, up));
+__device__ __forceinline__ uint16_t silu_mul1(float z, float up) { return tb_silu_mul_bf16(z, up); }
+
+// Interleaved layout (gate_j at column 2j, up_j at 2j+1), the fallback of the
+// fused gate_up GEMM (tbik_tree_matmul_silu_mul) when its epilogue cannot run.
+__global__ void silu_mul_il_kernel(const float* __restrict__ gu, int64_t ld, int64_t I, uint16_t* __restrict__ out,
+                                   int64_t ldo) {
+  const int64_t row = blockIdx.y;
+  const float* g = gu + row * ld;
+  uint16_t* o = out + row * ldo;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < I;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    o[j] = silu_mul1(g[2 * j], g[2 * j + 1]);
 }
 
 // VEC: 4 consecutive columns per thread (16-byte loads, 8-byte stores).
@@ -310,6 +319,16 @@ dim3 row_grid(int64_t rows, int64_t cols, int threads) {
 }
 
 }  // namespace
+
+tbik_status launch_silu_mul_il(const float* gu, int64_t ld, int64_t rows, int64_t inter, uint16_t* out, int64_t ldo,
+                               cudaStream_t s) {
+  if (rows > 65535) return set_error(TBIK_BAD_DIMENSION, "silu_mul: bad dimensions");
+  silu_mul_il_kernel<<<row_grid(rows, inter, 256), 256, 0, s>>>(gu, ld, inter, out, ldo);
+  TBIK_CUDA(cudaGetLastError());
+  count_launch();
+  return TBIK_OK;
+}
+
 }  // namespace tbik_b200
 
 using namespace tbik_b200;

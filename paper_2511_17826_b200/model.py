@@ -104,6 +104,7 @@ class DecoderWeights:
     layers: List[LayerWeights] = field(default_factory=list)
     ln_f: object = None
     lm_head: object = None
+    gate_up_interleaved: bool = False  # set by TbikDecoder (gate/up columns interleaved in place)
 
 
 def random_weights(cfg: DecoderConfig, seed: int = 0, device="cuda") -> DecoderWeights:
@@ -156,6 +157,12 @@ class TbikDecoder:
         self.cos = torch.from_numpy(cos).to(dev)
         self.sin = torch.from_numpy(sin).to(dev)
         self.bcfg = api.BlockConfig(64, cfg.block_k, 128, 0)
+        # gate_up weights are kept with gate/up columns interleaved so SiLU*up runs
+        # in the GEMM epilogue (a column permutation: the per-column tree is unchanged)
+        if not getattr(weights, "gate_up_interleaved", False):
+            for lw in weights.layers:
+                lw.wgu = api.interleave_gate_up(lw.wgu)
+            weights.gate_up_interleaved = True
         self.bcfg_down = api.BlockConfig(64, cfg.block_k_down, 128, 0)
 
     # -- building blocks ------------------------------------------------------------
@@ -226,9 +233,7 @@ class TbikDecoder:
             o = self._row(attn, lw.wo, tp, self.bcfg)            # f32 [M, H], tree all-reduce over tp
             check(lib.tbik_residual_add(_vp(h), H, _vp(o), H, M, H, self._stream()))
             a = self._norm(h, lw.ln2)
-            gu = self._col(a, lw.wgu, tp)                        # f32 [M, 2I]
-            act = torch.empty(M, I, device=dev, dtype=torch.bfloat16)
-            check(lib.tbik_silu_mul(_vp(gu), 2 * I, M, I, _vp(act), I, self._stream()))
+            act = api.tree_matmul_silu_mul(a, lw.wgu, api.DeviceGroup(tp), self.bcfg, self.leaf)  # bf16 [M, I]
             d = self._row(act, lw.wd, tp, self.bcfg_down)        # f32 [M, H]
             check(lib.tbik_residual_add(_vp(h), H, _vp(d), H, M, H, self._stream()))
         a = self._norm(h, w.ln_f)

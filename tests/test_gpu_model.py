@@ -139,3 +139,26 @@ def test_qwen3_stack_tp8_batch_sweep(tb, cuda):
         assert torch.equal(lp[:S].view(torch.int32), ref_lp.view(torch.int32))
     del w
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("leaf", ["tc", "fma"])
+@pytest.mark.parametrize("M", [64, 300, 2048])
+def test_fused_silu_gate_up_equals_unfused(tb, cuda, leaf, M):
+    """SiLU*up in the gate_up GEMM epilogue == column-parallel tree GEMM followed by
+    tbik_silu_mul, bit for bit, for every simulated TP size (epilogue and fallback)."""
+    import ctypes as C
+    lf = tb.LEAF_TCGEN05 if leaf == "tc" else tb.LEAF_FMA
+    K, inter = 4096, 1024
+    g = torch.Generator(device=cuda).manual_seed(M)
+    x = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(K, 2 * inter, device=cuda, generator=g) * 0.02).to(torch.bfloat16)
+    cfg = tb.BlockConfig(64, 256, 128, 0)
+    gu = tb.column_parallel_forward(x, w, tb.DeviceGroup(1), cfg, lf)
+    ref = torch.empty(M, inter, device=cuda, dtype=torch.bfloat16)
+    tb.api.check(tb.lib.tbik_silu_mul(C.c_void_p(gu.data_ptr()), 2 * inter, M, inter, C.c_void_p(ref.data_ptr()),
+                                      inter, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    w_il = tb.interleave_gate_up(w)
+    for tp in (1, 2, 4, 8):
+        act = tb.tree_matmul_silu_mul(x, w_il, tb.DeviceGroup(tp), cfg, lf)
+        torch.cuda.synchronize()
+        assert torch.equal(act.view(torch.int16), ref.view(torch.int16)), f"tp={tp}"

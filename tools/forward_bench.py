@@ -58,7 +58,10 @@ def torch_forward(cfg, w, tokens):
         h = h + o @ lw.wo
         a = rms(h, lw.ln2)
         gu = a @ lw.wgu
-        h = h + (torch.nn.functional.silu(gu[:, :I]) * gu[:, I:]) @ lw.wd
+        if getattr(w, "gate_up_interleaved", False):  # TbikDecoder keeps gate/up interleaved
+            h = h + (torch.nn.functional.silu(gu[:, 0::2]) * gu[:, 1::2]) @ lw.wd
+        else:
+            h = h + (torch.nn.functional.silu(gu[:, :I]) * gu[:, I:]) @ lw.wd
     a = rms(h, w.ln_f)
     logits = (a @ w.lm_head).float()
     return torch.log_softmax(logits, -1)
