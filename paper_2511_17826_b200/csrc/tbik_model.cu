@@ -138,12 +138,13 @@ __global__ void __launch_bounds__(4 * AQ, 3) attn2_kernel(const uint16_t* __rest
       float* dst = kv + r * AKP + c;
       if (key <= last_key) {
         const uint4 raw = *reinterpret_cast<const uint4*>(k + (seq0 + key) * ldk + kh * AD + c);
-        const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          dst[2 * x] = __uint_as_float(w[x] << 16);
-          dst[2 * x + 1] = __uint_as_float(w[x] & 0xFFFF0000u);
-        }
+        // two 16-byte stores (scalar stores at a 32-byte lane stride were 8-way bank conflicts)
+        reinterpret_cast<float4*>(dst)[0] =
+            make_float4(__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xFFFF0000u),
+                        __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xFFFF0000u));
+        reinterpret_cast<float4*>(dst)[1] =
+            make_float4(__uint_as_float(raw.z << 16), __uint_as_float(raw.z & 0xFFFF0000u),
+                        __uint_as_float(raw.w << 16), __uint_as_float(raw.w & 0xFFFF0000u));
       }
     }
     __syncthreads();
@@ -204,12 +205,13 @@ __global__ void __launch_bounds__(4 * AQ, 3) attn2_kernel(const uint16_t* __rest
       float* dst = kv + r * AKP + c;
       if (key <= last_key) {
         const uint4 raw = *reinterpret_cast<const uint4*>(v + (seq0 + key) * ldv + kh * AD + c);
-        const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          dst[2 * x] = __uint_as_float(w[x] << 16);
-          dst[2 * x + 1] = __uint_as_float(w[x] & 0xFFFF0000u);
-        }
+        // two 16-byte stores (scalar stores at a 32-byte lane stride were 8-way bank conflicts)
+        reinterpret_cast<float4*>(dst)[0] =
+            make_float4(__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xFFFF0000u),
+                        __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xFFFF0000u));
+        reinterpret_cast<float4*>(dst)[1] =
+            make_float4(__uint_as_float(raw.z << 16), __uint_as_float(raw.z & 0xFFFF0000u),
+                        __uint_as_float(raw.w << 16), __uint_as_float(raw.w & 0xFFFF0000u));
       }
     }
     __syncthreads();
