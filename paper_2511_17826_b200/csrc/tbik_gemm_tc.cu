@@ -879,10 +879,13 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   const long long nstreams = p.items < slots ? p.items : slots;
   dim3 grid(static_cast<unsigned>(mc ? 4 * nstreams : pair ? 2 * nstreams : nstreams));
   const bool kf1 = p.kf == 1;
-  // DEEP (see stages_for) when the items have at most 2 tree levels; with 3+ the
-  // on-chip level 3 measured faster (1146 vs 1108 TFLOP/s at the bench shape).
+  // DEEP (see stages_for) when the items have at most 2 tree levels, or when there
+  // are at most 2 waves of them: short launches are bound by load latency and the
+  // extra stages pay for level 3 in scratch (K=14336, N=4096: M=256..1024 +5..9%,
+  // M=2048 even; profiles/r01_tc_deep_midm.txt).  With 3+ levels and many waves
+  // the on-chip level 3 measured faster (1146 vs 1108 TFLOP/s at the bench shape).
   // TBIK_TC_DEEP=0/1 forces it (a pure scheduling knob -- same bits).
-  bool deep = p.levels <= 2;
+  bool deep = p.levels <= 2 || p.items <= 2 * slots;
   if (const char* e = std::getenv("TBIK_TC_DEEP"))
     if (*e) deep = std::atoi(e) != 0;
   if (mc) deep = false;

@@ -63,6 +63,28 @@ __device__ __forceinline__ float tb_exp_nonpos(float x) {
   return x < -103.0f ? 0.0f : res;
 }
 
+// tb_exp_nonpos for x >= -86 (then k >= -124: no gradual-underflow scaling and
+// no flush to zero apply), bit-identical to it on that range and for NaN.  The
+// caller proves the range for a whole block of arguments first.
+__device__ __forceinline__ float tb_exp_nonpos_normal(float x) {
+  const float magic = 12582912.0f;
+  const float t = __fmaf_rn(x, 1.44269502162933349609f, magic);
+  const float kf = __fsub_rn(t, magic);
+  float r = __fmaf_rn(kf, -0.693359375f, x);
+  r = __fmaf_rn(kf, 2.12194440e-4f, r);
+  float p = 1.9875691500e-4f;
+  p = __fmaf_rn(p, r, 1.3981999507e-3f);
+  p = __fmaf_rn(p, r, 8.3334519073e-3f);
+  p = __fmaf_rn(p, r, 4.1665795894e-2f);
+  p = __fmaf_rn(p, r, 1.6666665459e-1f);
+  p = __fmaf_rn(p, r, 5.0000001201e-1f);
+  const float r2 = __fmul_rn(r, r);
+  float y = __fmaf_rn(p, r2, r);
+  y = __fadd_rn(y, 1.0f);
+  const uint32_t sc = (__float_as_uint(t) << 23) + ((127u - 0x4B400000u) << 23);
+  return __fmul_rn(y, __uint_as_float(sc));
+}
+
 // bf16(silu(z) * up), silu(z) = z / (1 + exp(-z))  (demo.cpp:36-45, :171-174) -- the
 // one definition used by the SiLU*up kernel and the gate_up GEMM epilogue.
 __device__ __forceinline__ uint16_t tb_silu_mul_bf16(float z, float up) {

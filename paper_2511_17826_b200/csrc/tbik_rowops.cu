@@ -256,9 +256,12 @@ __global__ void __launch_bounds__(LANES, 4) ms_group_kernel(const float* __restr
       }
       // canonical max: sequential m = x > m ? x : m.  fmaxf gives the same bits
       // unless the maximum is a zero (only its sign is ambiguous): redo those.
-      float m = v[0];
+      float m = v[0], lo = v[0];
 #pragma unroll
-      for (int k = 1; k < MSB * 4; ++k) m = fmaxf(m, v[k]);
+      for (int k = 1; k < MSB * 4; ++k) {
+        m = fmaxf(m, v[k]);
+        lo = fminf(lo, v[k]);
+      }
       if (m == 0.0f) {
         m = v[0];
 #pragma unroll
@@ -266,8 +269,15 @@ __global__ void __launch_bounds__(LANES, 4) ms_group_kernel(const float* __restr
       }
       if (m != NEG_INF) {
         float sum = 0.0f;
+        // every x - m >= lo - m (rounding is monotone): when that is >= -86 no
+        // element needs tb_exp_nonpos's underflow handling (NaNs agree either way)
+        if (__fsub_rn(lo, m) >= -86.0f) {
 #pragma unroll
-        for (int k = 0; k < MSB * 4; ++k) sum = __fadd_rn(sum, tb_exp_nonpos(__fsub_rn(v[k], m)));
+          for (int k = 0; k < MSB * 4; ++k) sum = __fadd_rn(sum, tb_exp_nonpos_normal(__fsub_rn(v[k], m)));
+        } else {
+#pragma unroll
+          for (int k = 0; k < MSB * 4; ++k) sum = __fadd_rn(sum, tb_exp_nonpos(__fsub_rn(v[k], m)));
+        }
         b = MS{m, sum};
       }
     } else {

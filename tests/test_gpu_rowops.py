@@ -75,3 +75,41 @@ def test_logsoftmax_bad_groups(tb, cuda):
     with pytest.raises(tb.TbikError) as e:
         tb.log_softmax(x, 8, 3)
     assert e.value.code == tb.ErrorCode.BadWorldSize
+
+
+@pytest.mark.parametrize("cols,dt,out", [(5120, "bf16", "bf16"), (4096, "bf16", "f32"), (9000, "bf16", "bf16"),
+                                         (100, "f32", "f32"), (1000, "f32", "bf16")])
+def test_tree_rmsnorm_many_rows(tb, cuda, orc, cols, dt, out):
+    """2049 rows (several waves of CTAs, odd count), rows beyond the register
+    cache (9000 columns) and ragged rows: oracle bits, and the same bits for a
+    slice of the batch (batch invariance)."""
+    rows = 2049
+    x = orc.random_normal(cols, 3, rows, cols, dt)
+    gamma = orc.random_normal(cols, 4, 1, cols, "f32", 1.0, 0.02)[0]
+    od = torch.bfloat16 if out == "bf16" else torch.float32
+    dx = to_dev(x)
+    got = tb.rmsnorm(dx, to_dev(gamma), 1e-5, out_dtype=od)
+    want = orc.tree_rmsnorm(x, gamma, 1e-5)
+    got_f = got.float().cpu().numpy()
+    want_t = torch.from_numpy(want)
+    want_f = (want_t.to(torch.bfloat16).float() if out == "bf16" else want_t).numpy()
+    assert np.array_equal(bits(got_f), bits(want_f))
+    few = tb.rmsnorm(dx[2040:].contiguous(), to_dev(gamma), 1e-5, out_dtype=od)
+    assert torch.equal(got[2040:].view(torch.int16 if out == "bf16" else torch.int32),
+                       few.view(torch.int16 if out == "bf16" else torch.int32))
+
+
+def test_logsoftmax_wide_range_blocks(tb, cuda, orc):
+    """Logit blocks whose spread exceeds the exp fast path's range (x - max < -86)
+    mixed with narrow ones: both exp paths must give the oracle's bits."""
+    rng = np.random.default_rng(5)
+    V = 32768
+    x = (rng.standard_normal((3, V)) * 2).astype(np.float32)
+    x[0, ::97] -= 120.0
+    x[1, ::1000] += 95.0
+    x[2, 5::333] = -np.inf
+    lse_w, lp_w, _ = orc.tree_logsoftmax(x, 8, full=True)
+    for tp in (1, 8):
+        lse, lp, _ = tb.log_softmax(to_dev(x), 8, tp, full=True)
+        assert np.array_equal(bits(lse.cpu().numpy()), bits(lse_w)), f"lse tp={tp}"
+        assert np.array_equal(bits(lp.cpu().numpy()), bits(lp_w)), f"logprobs tp={tp}"

@@ -39,7 +39,7 @@ for M in (int(a) for a in (sys.argv[1:] or ["1", "16", "32", "64", "128", "256"]
     y = torch.empty(M, N, device="cuda")
     ref = None
     for pair in ("0", "1"):
-        if pair == "0" and M > 128:
+        if pair == "0" and M > int(os.environ.get("TUNE_SINGLE_MAX_M", "128")):
             continue
         for abox in ("32", "64", "128"):
             if int(abox) < M and abox != "128":
