@@ -1,17 +1,23 @@
 // tbik_gemm_tc_wide.cu -- the 256 x 256 pair-tile variant of the tcgen05 TBIK GEMM.
 //
-// Why a second kernel: at a 256 x 128 pair tile every K=16 MMA step moves
-// 6 KB of operands per SM out of shared memory plus 6 KB of TMA writes into it,
-// 96 + 96 B/clk at full MMA rate against ~128 B/clk of shared-memory bandwidth,
-// which caps the tensor pipe near 2/3 (measured 64.6 %).  A 256 x 256 pair tile
-// halves the ratio (64 + 64 B/clk).  Its two 128 x 256 f32 TMEM accumulators fill
-// all 512 TMEM columns, so tree level 1 (touched once per leaf group) lives in a
-// 128 KB shared-memory slot, leaving 3 operand stages; deeper levels (touched at
-// most once per 2 groups) go to L2-resident scratch.  Used when k_first >= 2.
+// Why a second kernel: the 256 x 128 kernel sits at ~14-15 TB/s of L2 -> SM
+// crossbar traffic whether or not it merges (profiles/r01_tc_pipeline_ceiling.txt:
+// 1221-1279 TFLOP/s with the merge switched off); a 256 x 256 pair tile pulls a
+// third fewer bytes per flop (32 KB per 64-deep K step per SM for 2x the MMA work).
+//
+// TMEM (512 columns) holds ONE 128 x 256 f32 accumulator, split into two
+// 128-column halves that the MMA issuer fills in turn (per K step: half 0's four
+// N=128 MMAs, then half 1's), so half 0 of a leaf is drained by its four merge
+// warps while half 1's last MMAs run, and half 1 while the next leaf's first
+// half-0 MMAs run -- a single accumulator that never stalls the tensor pipe,
+// leaving columns 256-511 for tree level 1.  Level 0 (the running leaf-group
+// value) lives in the merge warps' registers, levels >= 2 (touched at most once
+// per 2 groups) in L2-resident scratch; all of shared memory goes to operand
+// stages.  When the last round of tiles would leave pairs idle, its tiles are
+// split into 256 x 128 half items (one half of the accumulator / merge warps).
 //
 // Arithmetic is identical to the 256 x 128 kernel (tbik_gemm_tc.cu) -- the same
-// tcgen05 K-step sequence per leaf (the leaf value does not depend on the MMA N
-// shape, checked by tests/test_gpu_gemm.py) and the same __fadd_rn tree.
+// tcgen05 N=128 K-step sequence per leaf half and the same __fadd_rn tree.
 #include <mutex>
 #include <string>
 
@@ -26,19 +32,19 @@ constexpr int BM = 128;
 constexpr int PAIR_M = 256;
 constexpr int BN = 256;
 constexpr int KSTAGE = 64;
-constexpr int STAGES = 3;
+constexpr int KB_MAX = 4;  // K steps per accumulator-half block in the MMA issue order (p.kb <= 4)
 constexpr int A_STAGE_BYTES = BM * KSTAGE * 2;  // 16 KB
 constexpr int B_ATOM_BYTES = KSTAGE * 64 * 2;   // 8 KB
 constexpr int B_STAGE_BYTES = 2 * B_ATOM_BYTES;  // 128 columns of B per CTA
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-constexpr int SLOT1_BYTES = BM * BN * 4;  // tree level 1 in shared memory
 constexpr int EPI = 8;
 constexpr int NUM_THREADS = 128 + 32 * EPI;
 constexpr int COLS = 128;  // per merge thread
 constexpr int TMEM_COLS = 512;
 constexpr int GROUP_M = 8;
 constexpr uint32_t IDESC = umma_idesc_bf16(PAIR_M, BN, /*a_mn_major=*/0, /*b_mn_major=*/1);
-constexpr size_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + SLOT1_BYTES + 256;
+constexpr uint32_t IDESC_HALF = umma_idesc_bf16(PAIR_M, BN / 2, 0, 1);
+constexpr size_t smem_bytes(int st) { return 1024 + static_cast<size_t>(st) * STAGE_BYTES + 256; }
 
 struct WParams {
   int M, N, K;
@@ -49,10 +55,14 @@ struct WParams {
   int levels;
   int mblocks, ntiles;
   long long items;
+  long long full_items;  // items [0, full_items) are whole tiles, the rest halves
+  long long split_base;  // whole-tile index of the first split tile
   float* out;
   long long ldo;
   long long unit_stride;
-  float* scratch;  // [gridDim.x][levels - 1][BN cols][BM rows]
+  float* scratch;  // [gridDim.x][levels - 1][BN/4][BM rows][4] (levels >= 2)
+  int kb;          // K steps per half block (1, 2 or 4)
+  int debug;       // TBIK_TC_DEBUG ablations: bit 0 skips the merge, bit 2 the tree above level 0
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -109,10 +119,17 @@ __device__ __forceinline__ void tmem_dealloc_2cta(uint32_t taddr, uint32_t ncols
 
 struct Item {
   int m0, n0, unit, t_begin, t_end;
+  int mask;  // active accumulator halves (bit h: columns n0 + 128h .. +128)
 };
 
 __device__ __forceinline__ Item decode(const WParams& p, long long item) {
   Item it;
+  it.mask = 3;
+  if (item >= p.full_items) {
+    const long long j = item - p.full_items;
+    it.mask = 1 << static_cast<int>(j & 1);
+    item = p.split_base + (j >> 1);
+  }
   it.unit = static_cast<int>(item % p.units);
   const long long rest = item / p.units;
   const long long group = GROUP_M * static_cast<long long>(p.ntiles);
@@ -134,6 +151,7 @@ __device__ __forceinline__ int tile_chunks(const WParams& p, int t) {
   return (kh + KSTAGE - 1) / KSTAGE;
 }
 
+template <int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     tc_tree_gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const WParams p) {
@@ -141,10 +159,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-  float* slot1 = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + SLOT1_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* tfull = empty + STAGES;  // per accumulator half
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -162,9 +179,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&full[s], 2);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 2 * EPI);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&tfull[h], 1);
+      mbar_init(&tempty[h], 2 * (EPI / 2));  // the half's merge warps in both CTAs
     }
     fence_barrier_init();
   }
@@ -178,6 +195,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
     if (warp == 0) {
       // ---------------- TMA producer (both CTAs) ----------------
+      // per stage: A rows [am, am+128) x 64 K, and for each active half h the
+      // 64 columns n0 + 128h + 64*rank (the pair's N=128 MMA B operand is split
+      // across the two CTAs' shared memories)
       if (elect_one()) {
         const uint32_t full_leader0 = mapa(smem_u32(&full[0]), 0);
         int stage = 0;
@@ -185,20 +205,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         for (long long item = pair; item < p.items; item += npairs) {
           const Item it = decode(p, item);
           const int am = it.m0 + static_cast<int>(rank) * BM;
-          const int bn = it.n0 + static_cast<int>(rank) * (BN / 2);
+          const uint32_t tx = A_STAGE_BYTES + (it.mask == 3 ? 2 : 1) * B_ATOM_BYTES;
           for (int t = it.t_begin; t < it.t_end; ++t) {
             const int nch = tile_chunks(p, t);
             for (int c = 0; c < nch; ++c) {
               mbar_wait(&empty[stage], phase ^ 1);
               const uint32_t fb = full_leader0 + stage * 8;
               if (leader)
-                mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+                mbar_arrive_expect_tx(&full[stage], tx);
               else
-                mbar_arrive_expect_tx_cluster(fb, STAGE_BYTES);
+                mbar_arrive_expect_tx_cluster(fb, tx);
               const int k = t * p.bk + c * KSTAGE;
               tma_load_2d_2sm(sA + stage * A_STAGE_BYTES, &tmA, fb, k, am);
-              tma_load_2d_2sm(sB + stage * B_STAGE_BYTES, &tmB, fb, bn, k);
-              tma_load_2d_2sm(sB + stage * B_STAGE_BYTES + B_ATOM_BYTES, &tmB, fb, bn + 64, k);
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                if (it.mask >> h & 1)
+                  tma_load_2d_2sm(sB + stage * B_STAGE_BYTES + h * B_ATOM_BYTES, &tmB, fb,
+                                  it.n0 + h * 128 + static_cast<int>(rank) * 64, k);
               if (++stage == STAGES) {
                 stage = 0;
                 phase ^= 1;
@@ -213,34 +236,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if (leader && elect_one()) {
         int stage = 0;
         uint32_t phase = 0;
-        uint32_t acc_iter = 0;
+        uint32_t hiter[2] = {0, 0};  // leaves accumulated so far per half
         for (long long item = pair; item < p.items; item += npairs) {
           const Item it = decode(p, item);
-          for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
-            const int buf = acc_iter & 1;
-            const uint32_t use = acc_iter >> 1;
-            mbar_wait(&tempty[buf], (use & 1) ^ 1);
-            tc_fence_after();
-            const uint32_t d = tmem_base + buf * BN;
+          for (int t = it.t_begin; t < it.t_end; ++t) {
             const int nch = tile_chunks(p, t);
-            for (int c = 0; c < nch; ++c) {
-              mbar_wait(&full[stage], phase);
-              tc_fence_after();
-              const uint32_t a_base = smem_u32(sA + stage * A_STAGE_BYTES);
-              const uint32_t b_base = smem_u32(sB + stage * B_STAGE_BYTES);
+            // K steps in blocks of KB: half 0's MMAs for the block, then half 1's.  A
+            // half's last block ends 2*KB half-steps before the other half needs
+            // the tensor pipe again, so each half is drained while the other half
+            // computes (KB = 1 would leave the merge warps one N=128 K step).
+            for (int c0 = 0; c0 < nch; c0 += p.kb) {
+              const int nb = min(p.kb, nch - c0);
+              int st[KB_MAX];
+              uint32_t ph[KB_MAX];
 #pragma unroll
-              for (int kk = 0; kk < KSTAGE / 16; ++kk) {
-                const uint64_t adesc = umma_desc_sw128(a_base + kk * 32, 16, 1024);
-                const uint64_t bdesc = umma_desc_sw128(b_base + kk * 2048, B_ATOM_BYTES, 1024);
-                umma_bf16_2cta(d, adesc, bdesc, IDESC, (c | kk) != 0 ? 1u : 0u);
+              for (int j = 0; j < KB_MAX; ++j) {
+                if (j >= nb) break;
+                st[j] = stage;
+                ph[j] = phase;
+                if (++stage == STAGES) {
+                  stage = 0;
+                  phase ^= 1;
+                }
               }
-              umma_commit_2cta(&empty[stage], 0x3);
-              if (++stage == STAGES) {
-                stage = 0;
-                phase ^= 1;
+              int hdone = 0;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                if (!(it.mask >> h & 1)) continue;
+                if (c0 == 0) {  // the half's previous leaf has been drained
+                  mbar_wait(&tempty[h], (hiter[h] & 1) ^ 1);
+                  tc_fence_after();
+                }
+#pragma unroll
+                for (int j = 0; j < KB_MAX; ++j) {
+                  if (j >= nb) break;
+                  const int c = c0 + j;
+                  if (hdone == 0) {  // first use of this stage
+                    mbar_wait(&full[st[j]], ph[j]);
+                    tc_fence_after();
+                  }
+                  const uint32_t a_base = smem_u32(sA + st[j] * A_STAGE_BYTES);
+                  const uint32_t b_base = smem_u32(sB + st[j] * B_STAGE_BYTES) + h * B_ATOM_BYTES;
+#pragma unroll
+                  for (int kk = 0; kk < KSTAGE / 16; ++kk) {
+                    const uint64_t adesc = umma_desc_sw128(a_base + kk * 32, 16, 1024);
+                    const uint64_t bdesc = umma_desc_sw128(b_base + kk * 2048, B_ATOM_BYTES, 1024);
+                    umma_bf16_2cta(tmem_base + h * 128, adesc, bdesc, IDESC_HALF, (c | kk) != 0 ? 1u : 0u);
+                  }
+                }
+                if (c0 + nb == nch) {
+                  umma_commit_2cta(&tfull[h], 0x3);
+                  ++hiter[h];
+                }
+                ++hdone;
               }
+#pragma unroll
+              for (int j = 0; j < KB_MAX; ++j)
+                if (j < nb) umma_commit_2cta(&empty[st[j]], 0x3);
             }
-            umma_commit_2cta(&tfull[buf], 0x3);
           }
         }
       }
@@ -248,33 +301,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
-    // ---------------- merge warps: 2 per TMEM lane quadrant, 128 columns each ----------------
+    // ---------------- merge warps: 4 per accumulator half, one per TMEM lane quadrant ----------------
     const int ew = warp - 4;
-    const int q = ew & 3;
-    const int h = ew >> 2;
+    const int q = ew & 3;   // TMEM lanes 32q.. (a warp may only touch lanes 32*(warp%4)..)
+    const int h = ew >> 2;  // accumulator half: columns 128h .. 128h + 127
     const int row_in_tile = q * 32 + lane;
     const int col0 = h * COLS;
-    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + col0;
-    const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
-    float* l1 = slot1 + static_cast<size_t>(col0) * BM + row_in_tile;  // [col][row]
-    float* scratch_base = p.levels > 1 ? p.scratch + static_cast<size_t>(blockIdx.x) * (p.levels - 1) * (BM * BN) +
-                                             static_cast<size_t>(col0) * BM + row_in_tile
-                                       : nullptr;
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t acc = lane_base + h * 128;
+    const uint32_t slot1 = lane_base + 256 + h * 128;  // tree level 1
+    const uint32_t tempty_leader = mapa(smem_u32(&tempty[h]), 0);
+    // scratch slab per level >= 2: [col/4][row][4] -- a warp's float4 access is 512
+    // contiguous bytes
+    float* scratch_base = p.levels >= 2 ? p.scratch + static_cast<size_t>(blockIdx.x) * (p.levels - 1) * (BM * BN) +
+                                              static_cast<size_t>(col0) * BM + static_cast<size_t>(row_in_tile) * 4
+                                        : nullptr;
     float g[COLS];
-    uint32_t acc_iter = 0;
+    uint32_t hiter = 0;
     for (long long item = pair; item < p.items; item += npairs) {
       const Item it = decode(p, item);
+      if (!(it.mask >> h & 1)) continue;
       const int grow = it.m0 + static_cast<int>(rank) * BM + row_in_tile;
       const bool row_ok = grow < p.M;
       const int ncols = min(COLS, p.N - it.n0 - col0);  // may be <= 0
       int t_in_group = 0;
       uint32_t groups_done = 0;
-      for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
-        const int buf = acc_iter & 1;
-        const uint32_t use = acc_iter >> 1;
-        mbar_wait(&tfull[buf], use & 1);
+      for (int t = it.t_begin; t < it.t_end; ++t, ++hiter) {
+        mbar_wait(&tfull[h], hiter & 1);
         tc_fence_after();
-        const uint32_t acc = lane_base + buf * BN;
         if (p.mode == OUT_LEAVES) {
           float* dst = p.out + static_cast<size_t>(t) * p.unit_stride + static_cast<size_t>(grow) * p.ldo + it.n0 + col0;
 #pragma unroll
@@ -287,47 +341,74 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 if (c * 32 + i < ncols) dst[c * 32 + i] = v[i];
             }
           }
-        } else if (t_in_group == 0) {
+        } else if (!(p.debug & 1)) {
+          // level 0: g = ((0 + P_0) + P_1) + ... (matmul.cpp:100-125), two 32-column
+          // chunks in flight per wait
 #pragma unroll
-          for (int c = 0; c < COLS / 32; ++c) {
-            float v[32];
-            tmem_ld32(acc + c * 32, v);
+          for (int c = 0; c < COLS / 32; c += 2) {
+            uint32_t r0[32], r1[32];
+            tmem_ld32r(acc + c * 32, r0);
+            tmem_ld32r(acc + c * 32 + 32, r1);
+            tmem_wait_ld_dep(r0);
+            tmem_wait_ld_dep(r1);
+            if (t_in_group == 0) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(0.0f, v[i]);
-          }
-        } else {
+              for (int i = 0; i < 32; ++i) {
+                g[c * 32 + i] = __fadd_rn(0.0f, __uint_as_float(r0[i]));
+                g[c * 32 + 32 + i] = __fadd_rn(0.0f, __uint_as_float(r1[i]));
+              }
+            } else {
 #pragma unroll
-          for (int c = 0; c < COLS / 32; ++c) {
-            float v[32];
-            tmem_ld32(acc + c * 32, v);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], v[i]);
+              for (int i = 0; i < 32; ++i) {
+                g[c * 32 + i] = __fadd_rn(g[c * 32 + i], __uint_as_float(r0[i]));
+                g[c * 32 + 32 + i] = __fadd_rn(g[c * 32 + 32 + i], __uint_as_float(r1[i]));
+              }
+            }
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
           if (leader)
-            mbar_arrive(&tempty[buf]);
+            mbar_arrive(&tempty[h]);
           else
-            mbar_arrive_cluster(tempty_leader0 + buf * 8);
+            mbar_arrive_cluster(tempty_leader);
         }
 
-        if (p.mode == OUT_LEAVES) continue;
+        if (p.mode == OUT_LEAVES || (p.debug & 1)) continue;
         if (++t_in_group < p.kf) continue;
         t_in_group = 0;
+        if (p.debug & 4) continue;  // ablation: level 0 only
 
-        // Binary counter over completed groups: level 1 in shared memory, deeper in scratch.
+        // Binary counter over completed groups (matmul.cpp:107-123): level 1 in
+        // TMEM columns 256-511, deeper levels in scratch.
         int level = 1;
         uint32_t c_bits = groups_done++;
         while (c_bits & 1u) {
           if (level == 1) {
 #pragma unroll
-            for (int i = 0; i < COLS; ++i) g[i] = __fadd_rn(g[i], l1[i * BM]);
-          } else {
-            const float* s = scratch_base + static_cast<size_t>(level - 2) * (BM * BN);
+            for (int c = 0; c < COLS / 32; c += 2) {
+              uint32_t r0[32], r1[32];
+              tmem_ld32r(slot1 + c * 32, r0);
+              tmem_ld32r(slot1 + c * 32 + 32, r1);
+              tmem_wait_ld_dep(r0);
+              tmem_wait_ld_dep(r1);
 #pragma unroll
-            for (int i = 0; i < COLS; ++i) g[i] = __fadd_rn(g[i], s[i * BM]);
+              for (int i = 0; i < 32; ++i) {
+                g[c * 32 + i] = __fadd_rn(g[c * 32 + i], __uint_as_float(r0[i]));
+                g[c * 32 + 32 + i] = __fadd_rn(g[c * 32 + 32 + i], __uint_as_float(r1[i]));
+              }
+            }
+          } else if (!(p.debug & 8)) {
+            const float* sp = scratch_base + static_cast<size_t>(level - 2) * (BM * BN);
+#pragma unroll
+            for (int i = 0; i < COLS; i += 4) {
+              const float4 x = *reinterpret_cast<const float4*>(sp + i * BM);
+              g[i] = __fadd_rn(g[i], x.x);
+              g[i + 1] = __fadd_rn(g[i + 1], x.y);
+              g[i + 2] = __fadd_rn(g[i + 2], x.z);
+              g[i + 3] = __fadd_rn(g[i + 3], x.w);
+            }
           }
           c_bits >>= 1;
           ++level;
@@ -335,15 +416,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (level <= p.levels) {
           if (level == 1) {
 #pragma unroll
-            for (int i = 0; i < COLS; ++i) l1[i * BM] = g[i];
-          } else {
-            float* s = scratch_base + static_cast<size_t>(level - 2) * (BM * BN);
+            for (int c = 0; c < COLS / 32; ++c) {
+              float v[32];
 #pragma unroll
-            for (int i = 0; i < COLS; ++i) s[i * BM] = g[i];
+              for (int i = 0; i < 32; ++i) v[i] = g[c * 32 + i];
+              tmem_st32(slot1 + c * 32, v);
+            }
+            tmem_wait_st();
+          } else if (!(p.debug & 16)) {
+            float* sp = scratch_base + static_cast<size_t>(level - 2) * (BM * BN);
+#pragma unroll
+            for (int i = 0; i < COLS; i += 4)
+              *reinterpret_cast<float4*>(sp + i * BM) = make_float4(g[i], g[i + 1], g[i + 2], g[i + 3]);
           }
           continue;
         }
-        if (row_ok && ncols > 0) {
+        if (row_ok && ncols > 0 && !(p.debug & 32)) {
           float* dst = p.out + static_cast<size_t>(p.mode == OUT_UNITS ? it.unit : 0) * p.unit_stride +
                        static_cast<size_t>(grow) * p.ldo + it.n0 + col0;
           if (ncols == COLS && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
@@ -433,25 +521,66 @@ tbik_status launch_tc_gemm_wide(const GemmView& v, const GemmOut& o, cudaStream_
   }
   p.mblocks = static_cast<int>((v.M + PAIR_M - 1) / PAIR_M);
   p.ntiles = static_cast<int>((v.N + BN - 1) / BN);
-  p.items = static_cast<long long>(p.mblocks) * p.ntiles * p.units;
+  const long long tiles = static_cast<long long>(p.mblocks) * p.ntiles * p.units;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long max_pairs = sms / 2;
-  const long long npairs = p.items < max_pairs ? p.items : max_pairs;
+  const long long npairs = tiles < max_pairs ? tiles : max_pairs;
+  // Items go to pairs round-robin.  When the last round would leave at least half
+  // of the pairs idle, its tiles become two half items each (TBIK_TC_WIDE_SPLIT=0
+  // turns this off -- a pure scheduling knob).
+  static const bool split_ok = [] {
+    const char* e = std::getenv("TBIK_TC_WIDE_SPLIT");
+    return !(e && *e == '0');
+  }();
+  const long long tail = tiles % npairs;
+  if (split_ok && tiles > npairs && tail > 0 && 2 * tail <= npairs) {
+    p.full_items = tiles - tail;
+    p.split_base = tiles - tail;
+    p.items = p.full_items + 2 * tail;
+  } else {
+    p.full_items = tiles;
+    p.split_base = tiles;
+    p.items = tiles;
+  }
   dim3 grid(static_cast<unsigned>(2 * npairs));
-  if (p.levels > 1) {
+  if (p.levels >= 2) {
     const size_t n = static_cast<size_t>(grid.x) * (p.levels - 1) * BM * BN;
     p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1));
     if (!p.scratch) return set_error(TBIK_CUDA_ERROR, "tc gemm: scratch allocation failed");
   }
-  static bool attr_set[16] = {false};
-  if (dev >= 0 && dev < 16 && !attr_set[dev]) {
-    TBIK_CUDA(cudaFuncSetAttribute(tc_tree_gemm_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(SMEM_BYTES)));
-    attr_set[dev] = true;
+  static const int dbg = [] {
+    const char* e = std::getenv("TBIK_TC_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.debug = dbg;
+  static const int kb = [] {
+    const char* e = std::getenv("TBIK_TC_WIDE_KB");
+    const int v = e ? std::atoi(e) : 2;
+    return v == 1 || v == 4 ? v : 2;
+  }();
+  p.kb = kb;
+  // operand stages (TBIK_TC_WIDE_STAGES=4/5/6, a pure scheduling knob)
+  static const int st = [] {
+    const char* e = std::getenv("TBIK_TC_WIDE_STAGES");
+    const int v = e ? std::atoi(e) : 6;
+    return v == 4 || v == 5 ? v : 6;
+  }();
+  static bool attr_set[16][3] = {};
+  if (dev >= 0 && dev < 16 && !attr_set[dev][st - 4]) {
+    const void* fn = st == 4 ? reinterpret_cast<const void*>(tc_tree_gemm_wide_kernel<4>)
+                   : st == 5 ? reinterpret_cast<const void*>(tc_tree_gemm_wide_kernel<5>)
+                             : reinterpret_cast<const void*>(tc_tree_gemm_wide_kernel<6>);
+    TBIK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_bytes(st))));
+    attr_set[dev][st - 4] = true;
   }
-  tc_tree_gemm_wide_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mA, mB, p);
+  if (st == 4)
+    tc_tree_gemm_wide_kernel<4><<<grid, NUM_THREADS, smem_bytes(4), s>>>(mA, mB, p);
+  else if (st == 5)
+    tc_tree_gemm_wide_kernel<5><<<grid, NUM_THREADS, smem_bytes(5), s>>>(mA, mB, p);
+  else
+    tc_tree_gemm_wide_kernel<6><<<grid, NUM_THREADS, smem_bytes(6), s>>>(mA, mB, p);
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;

@@ -384,3 +384,19 @@ def test_random_shapes_both_leaves(tb, cuda, orc, M, K, N, bk):
     assert np.array_equal(bits(y.cpu().numpy()), bits(want_tc))
     rel = np.abs(y.cpu().numpy() - want).max() / max(np.abs(want).max(), 1e-30)
     assert rel < 1e-5
+
+
+@pytest.mark.parametrize("M,K,N", [(2560, 3072, 2048), (4096, 14336, 4096), (700, 25600, 5120)])
+def test_tc_wide_tiles_and_split_tail(tb, cuda, M, K, N, monkeypatch):
+    """256 x 256 pair tiles (split accumulator halves, level 1 in TMEM, deeper levels
+    in scratch) and the 256 x 128 half items of a short last round give the bits
+    of the 256 x 128 kernel (80 / 256 tiles on 74 pairs: split tail; 3 x 20: none)."""
+    g = torch.Generator(device=cuda).manual_seed(K + N)
+    x = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = torch.randn(K, N, device=cuda, generator=g).to(torch.bfloat16)
+    cfg = tb.BlockConfig(64, 256 if K % 256 == 0 and K != 25600 else 128, 128, 0)
+    monkeypatch.setenv("TBIK_TC_WIDE", "0")
+    want = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+    monkeypatch.setenv("TBIK_TC_WIDE", "1")
+    got = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+    assert torch.equal(want.view(torch.int32), got.view(torch.int32))
