@@ -310,12 +310,20 @@ TBIK_API tbik_status tbik_rope(const float* x, int64_t ldx, int64_t col0, int he
 TBIK_API tbik_status tbik_cast_bf16(const float* x, int64_t ldx, int64_t rows, int64_t cols, void* out,
                                     int64_t ldo, void* stream);
 /* Causal GQA prefill attention over `batch` sequences of seq_len tokens (rows are
- * sequence-major), head_dim 128, bf16 in / bf16 out, fixed key order + online
- * softmax with the shared exp. */
+ * sequence-major), head_dim 128, bf16 in / bf16 out: the exact two-pass order
+ * (ascending-d fma scores, exact max, shared exp, ascending sums), restated by the
+ * oracle bit for bit; seq_len <= 512. */
 TBIK_API tbik_status tbik_attention_prefill(const void* q, int64_t ldq, const void* k, int64_t ldk,
                                             const void* v, int64_t ldv, int64_t batch, int seq_len,
                                             int n_q_heads, int n_kv_heads, int head_dim, float scale,
                                             void* out, int64_t ldo, void* stream);
+/* The same attention in a tensor-core flash form (mma.sync bf16 scores and P.V,
+ * online softmax over 64-key blocks from key 0): deterministic, bit-identical across
+ * batch composition and head sharding, within a tolerance of the exact form. */
+TBIK_API tbik_status tbik_attention_prefill_tc(const void* q, int64_t ldq, const void* k, int64_t ldk,
+                                               const void* v, int64_t ldv, int64_t batch, int seq_len,
+                                               int n_q_heads, int n_kv_heads, int head_dim, float scale,
+                                               void* out, int64_t ldo, void* stream);
 /* act = bf16(silu(gate) * up), gate = columns [0, inter), up = [inter, 2 inter)
  * of gate_up (f32) -- silu (demo.cpp:36-45) with the shared exp. */
 TBIK_API tbik_status tbik_silu_mul(const float* gate_up, int64_t ld, int64_t rows, int64_t inter, void* out,

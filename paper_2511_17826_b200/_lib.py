@@ -115,6 +115,7 @@ _SIGS = {
     "tbik_rope": (ci, [PF, i64, i64, ci, ci, vp, PF, PF, vp, i64, i64, vp]),
     "tbik_cast_bf16": (ci, [PF, i64, i64, i64, vp, i64, vp]),
     "tbik_attention_prefill": (ci, [vp, i64, vp, i64, vp, i64, i64, ci, ci, ci, ci, C.c_float, vp, i64, vp]),
+    "tbik_attention_prefill_tc": (ci, [vp, i64, vp, i64, vp, i64, i64, ci, ci, ci, ci, C.c_float, vp, i64, vp]),
     "tbik_silu_mul": (ci, [PF, i64, i64, i64, vp, i64, vp]),
     "tbik_residual_add": (ci, [vp, i64, PF, i64, i64, i64, vp]),
     "tbik_debug_tc_stats": (ci, [C.POINTER(C.c_ulonglong), ci]),

@@ -245,6 +245,213 @@ __global__ void __launch_bounds__(4 * AQ, 3) attn2_kernel(const uint16_t* __rest
   }
 }
 
+// ---- causal GQA prefill attention, tensor-core flash form ------------------------------------
+// The fast attention of the tcgen05-leaf forward.  Deterministic and batch / head-
+// sharding invariant by construction, but NOT the exact two-pass order above (its
+// dot products run on mma.sync tensor cores): parity against attn2 / the oracle is
+// a tolerance, bit identity across TP and batch is exact.  Canonical form, per
+// (sequence, q head, query i) with keys in blocks of 64 from key 0:
+//   per block: s = q.k (mma.sync m16n8k16 bf16 -> f32), masked keys -inf
+//              m' = max(m, rowmax s)   (quad shuffles xor 1, 2)
+//              p  = exp2(s c - m' c), c = scale * log2 e;  alpha = exp2(m c - m' c)
+//              l  = l alpha + (sequential sum of the lane's p);  O = O alpha + bf16(p) . v
+//   out = bf16(O / (quad sum of l))
+// One CTA = (64-query block, q head, sequence), 4 warps x 16 query rows; K and V
+// blocks double-buffered in shared memory by cp.async, B fragments by ldmatrix
+// (.trans for V).
+constexpr int FQ = 64;          // queries per CTA
+constexpr int FK = 64;          // keys per block
+constexpr int FKP = AD + 8;     // padded bf16 row of a staged K / V block (272 B: conflict-free ldmatrix)
+constexpr int FSTAGE = FK * FKP;  // elements per staged block
+
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  return static_cast<uint32_t>(f32_to_bf16_bits(lo)) | (static_cast<uint32_t>(f32_to_bf16_bits(hi)) << 16);
+}
+
+__global__ void __launch_bounds__(128) attn_mma_kernel(const uint16_t* __restrict__ q, int64_t ldq,
+                                                       const uint16_t* __restrict__ k, int64_t ldk,
+                                                       const uint16_t* __restrict__ v, int64_t ldv, int S, int nq,
+                                                       int nkv, float scale_log2, uint16_t* __restrict__ out,
+                                                       int64_t ldo) {
+  extern __shared__ __align__(16) uint16_t fsm[];  // [2 buffers][K block, V block]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int qb = static_cast<int>(gridDim.z) - 1 - static_cast<int>(blockIdx.z), h = blockIdx.x;
+  const int64_t seq0 = static_cast<int64_t>(blockIdx.y) * S;
+  const int kh = h / (nq / nkv);
+  const int r0 = qb * FQ + warp * 16 + g;  // this thread's rows r0 and r0 + 8
+  const int last_key = min(S, (qb + 1) * FQ) - 1;
+  const int nkb = last_key / FK + 1;
+
+  auto stage = [&](int kb, int buf) {  // keys past the causal end / sequence as zeros
+    uint16_t* sK = fsm + buf * 2 * FSTAGE;
+    uint16_t* sV = sK + FSTAGE;
+#pragma unroll
+    for (int x = 0; x < FK * AD / 8 / 128; ++x) {
+      const int e = tid + x * 128;
+      const int r = e / (AD / 8), c = (e % (AD / 8)) * 8;
+      const int key = kb * FK + r;
+      const bool ok = key <= last_key;
+      const int64_t row = seq0 + (ok ? key : 0);
+      cp_async16(sK + r * FKP + c, k + row * ldk + kh * AD + c, ok);
+      cp_async16(sV + r * FKP + c, v + row * ldv + kh * AD + c, ok);
+    }
+    cp_async_commit();
+  };
+  stage(0, 0);
+
+  // Q fragments (16 rows x 128 d per warp): qa[kstep][4]
+  uint32_t qa[AD / 16][4];
+  {
+    const int ra = min(r0, S - 1), rb = min(r0 + 8, S - 1);
+    const uint16_t* qpa = q + (seq0 + ra) * ldq + h * AD;
+    const uint16_t* qpb = q + (seq0 + rb) * ldq + h * AD;
+#pragma unroll
+    for (int ks = 0; ks < AD / 16; ++ks) {
+      qa[ks][0] = *reinterpret_cast<const uint32_t*>(qpa + ks * 16 + 2 * t);
+      qa[ks][1] = *reinterpret_cast<const uint32_t*>(qpb + ks * 16 + 2 * t);
+      qa[ks][2] = *reinterpret_cast<const uint32_t*>(qpa + ks * 16 + 2 * t + 8);
+      qa[ks][3] = *reinterpret_cast<const uint32_t*>(qpb + ks * 16 + 2 * t + 8);
+    }
+  }
+  float o[AD / 8][4];
+#pragma unroll
+  for (int n = 0; n < AD / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.0f;
+  const float NEG_INF = __int_as_float(0xFF800000);
+  float m[2] = {NEG_INF, NEG_INF}, l[2] = {0.0f, 0.0f};
+  // ldmatrix row addresses: lane i feeds row i % 8 of matrix i / 8
+  const int lr = lane & 7, lm = lane >> 3;
+
+  for (int kb = 0; kb < nkb; ++kb) {
+    if (kb + 1 < nkb) {
+      stage(kb + 1, (kb + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const uint16_t* sK = fsm + (kb & 1) * 2 * FSTAGE;
+    const uint16_t* sV = sK + FSTAGE;
+    // s = q . k for this warp's 16 rows x 64 keys (8 n-tiles of 8 keys).  ldmatrix x4
+    // matrices: (keys n*8.., d ks*16 + 0/8) for n-tile pair (n, n+1)
+    float sc[FK / 8][4];
+#pragma unroll
+    for (int n = 0; n < FK / 8; ++n) sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.0f;
+#pragma unroll
+    for (int ks = 0; ks < AD / 16; ++ks) {
+#pragma unroll
+      for (int n = 0; n < FK / 8; n += 2) {
+        uint32_t b[4];  // b0(n), b1(n), b0(n+1), b1(n+1)
+        ldsm_x4(b, sK + ((n + (lm >> 1)) * 8 + lr) * FKP + ks * 16 + (lm & 1) * 8);
+        mma_bf16_16816(sc[n], qa[ks], b[0], b[1]);
+        mma_bf16_16816(sc[n + 1], qa[ks], b[2], b[3]);
+      }
+    }
+    // causal / sequence mask, block row max
+    float bm[2] = {NEG_INF, NEG_INF};
+#pragma unroll
+    for (int n = 0; n < FK / 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int key = kb * FK + n * 8 + 2 * t + (e & 1);
+        const int row = r0 + (e >> 1) * 8;
+        if (key > row || key > last_key) sc[n][e] = NEG_INF;
+        bm[e >> 1] = fmaxf(bm[e >> 1], sc[n][e]);
+      }
+    float alpha[2], mc[2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      bm[x] = fmaxf(bm[x], __shfl_xor_sync(0xffffffffu, bm[x], 1));
+      bm[x] = fmaxf(bm[x], __shfl_xor_sync(0xffffffffu, bm[x], 2));
+      const float mn = fmaxf(m[x], bm[x]);
+      // rows whose keys are all masked so far (only rows past the sequence end) keep m = -inf
+      mc[x] = mn == NEG_INF ? 0.0f : __fmul_rn(mn, scale_log2);
+      alpha[x] = m[x] == NEG_INF ? 0.0f : exp2f(__fsub_rn(__fmul_rn(m[x], scale_log2), mc[x]));
+      m[x] = mn;
+    }
+    // p = exp2(s c - m c); l = l alpha + sum p; P packed as the A operand of P.V
+    uint32_t pa[FK / 16][4];
+    float ps[2] = {0.0f, 0.0f};
+#pragma unroll
+    for (int n = 0; n < FK / 8; ++n) {
+      float pv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        pv[e] = exp2f(__fsub_rn(__fmul_rn(sc[n][e], scale_log2), mc[e >> 1]));
+        ps[e >> 1] = __fadd_rn(ps[e >> 1], pv[e]);
+      }
+      pa[n >> 1][(n & 1) * 2 + 0] = pack_bf16x2(pv[0], pv[1]);
+      pa[n >> 1][(n & 1) * 2 + 1] = pack_bf16x2(pv[2], pv[3]);
+    }
+#pragma unroll
+    for (int x = 0; x < 2; ++x) l[x] = __fadd_rn(__fmul_rn(l[x], alpha[x]), ps[x]);
+#pragma unroll
+    for (int n = 0; n < AD / 8; ++n) {
+      o[n][0] = __fmul_rn(o[n][0], alpha[0]);
+      o[n][1] = __fmul_rn(o[n][1], alpha[0]);
+      o[n][2] = __fmul_rn(o[n][2], alpha[1]);
+      o[n][3] = __fmul_rn(o[n][3], alpha[1]);
+    }
+    // O += P . V: B fragments of V [key][d] by ldmatrix.trans, matrices (keys ks*16 +
+    // 0/8, d n*8..) for d-tile pair (n, n+1)
+#pragma unroll
+    for (int ks = 0; ks < FK / 16; ++ks) {
+#pragma unroll
+      for (int n = 0; n < AD / 8; n += 2) {
+        uint32_t b[4];
+        ldsm_x4_t(b, sV + (ks * 16 + (lm & 1) * 8 + lr) * FKP + (n + (lm >> 1)) * 8);
+        mma_bf16_16816(o[n], pa[ks], b[0], b[1]);
+        mma_bf16_16816(o[n + 1], pa[ks], b[2], b[3]);
+      }
+    }
+    __syncthreads();  // this buffer is restaged two blocks later
+  }
+  // l over the quad (xor 1 then xor 2), out = bf16(O / l)
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    l[x] = __fadd_rn(l[x], __shfl_xor_sync(0xffffffffu, l[x], 1));
+    l[x] = __fadd_rn(l[x], __shfl_xor_sync(0xffffffffu, l[x], 2));
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    const int row = r0 + 8 * x;
+    if (row >= S) continue;
+    uint16_t* op = out + (seq0 + row) * ldo + h * AD + 2 * t;
+#pragma unroll
+    for (int n = 0; n < AD / 8; ++n)
+      *reinterpret_cast<uint32_t*>(op + n * 8) =
+          pack_bf16x2(__fdiv_rn(o[n][2 * x], l[x]), __fdiv_rn(o[n][2 * x + 1], l[x]));
+  }
+}
+
 // ---- SiLU(gate) * up  (demo.cpp:36-45, :171-174) ---------------------------------------
 // gu: f32 [M, ld] with gate in columns [0, I) and up in [I, 2I).  silu(z) = z / (1 + exp(-z)).
 __device__ __forceinline__ uint16_t silu_mul1(float z, float up) { return tb_silu_mul_bf16(z, up); }
@@ -413,6 +620,35 @@ tbik_status tbik_attention_prefill(const void* q, int64_t ldq, const void* k, in
   attn2_kernel<<<grid, 4 * AQ, smem, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(q), ldq, static_cast<const uint16_t*>(k), ldk, static_cast<const uint16_t*>(v), ldv,
       seq_len, n_q_heads, n_kv_heads, scale, static_cast<uint16_t*>(out), ldo);
+  TBIK_CUDA(cudaGetLastError());
+  count_launch();
+  return TBIK_OK;
+}
+
+tbik_status tbik_attention_prefill_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                                      int64_t ldv, int64_t batch, int seq_len, int n_q_heads, int n_kv_heads,
+                                      int head_dim, float scale, void* out, int64_t ldo, void* stream) {
+  if (!q || !k || !v || !out) return set_error(TBIK_BAD_ARGUMENT, "null argument");
+  if (head_dim != 128) return set_error(TBIK_UNSUPPORTED, "attention: head_dim must be 128");
+  if (n_kv_heads < 1 || n_q_heads % n_kv_heads) return set_error(TBIK_BAD_DIMENSION, "attention: bad GQA heads");
+  if (seq_len < 1 || seq_len > (1 << 20)) return set_error(TBIK_UNSUPPORTED, "attention: seq_len out of range");
+  if (batch < 1 || batch > 65535 || n_q_heads > 65535) return set_error(TBIK_BAD_DIMENSION, "attention: grid");
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
+       reinterpret_cast<uintptr_t>(out)) & 15 || ldq % 8 || ldk % 8 || ldv % 8 || ldo % 8)
+    return set_error(TBIK_BAD_ARGUMENT, "attention: 16-byte aligned rows required");
+  TBIK_TRY(need_device());
+  const float scale_log2 = scale * 1.4426950408889634f;
+  dim3 grid(static_cast<unsigned>(n_q_heads), static_cast<unsigned>(batch),
+            static_cast<unsigned>((seq_len + FQ - 1) / FQ));
+  constexpr size_t fsmem = 2 * 2 * FSTAGE * sizeof(uint16_t);
+  static bool fattr = false;
+  if (!fattr) {
+    TBIK_CUDA(cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem)));
+    fattr = true;
+  }
+  attn_mma_kernel<<<grid, 128, fsmem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint16_t*>(q), ldq, static_cast<const uint16_t*>(k), ldk, static_cast<const uint16_t*>(v), ldv,
+      seq_len, n_q_heads, n_kv_heads, scale_log2, static_cast<uint16_t*>(out), ldo);
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;

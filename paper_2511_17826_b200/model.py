@@ -228,8 +228,10 @@ class TbikDecoder:
             check(lib.tbik_cast_bf16(C.c_void_p(qkv.data_ptr() + 4 * (qcols + kcols)), ld, M, kcols, _vp(v),
                                      kcols, self._stream()))
             attn = torch.empty(M, qcols, device=dev, dtype=torch.bfloat16)
-            check(lib.tbik_attention_prefill(_vp(q), qcols, _vp(k), kcols, _vp(v), kcols, B, S, nq, nkv, D,
-                                             scale, _vp(attn), qcols, self._stream()))
+            # tensor-core flash attention with the tcgen05 leaf, the exact order with the fma leaf
+            attn_fn = lib.tbik_attention_prefill_tc if self.leaf == api.LEAF_TCGEN05 else lib.tbik_attention_prefill
+            check(attn_fn(_vp(q), qcols, _vp(k), kcols, _vp(v), kcols, B, S, nq, nkv, D,
+                          scale, _vp(attn), qcols, self._stream()))
             o = self._row(attn, lw.wo, tp, self.bcfg)            # f32 [M, H], tree all-reduce over tp
             check(lib.tbik_residual_add(_vp(h), H, _vp(o), H, M, H, self._stream()))
             a = self._norm(h, lw.ln2)

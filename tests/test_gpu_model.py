@@ -162,3 +162,45 @@ def test_fused_silu_gate_up_equals_unfused(tb, cuda, leaf, M):
         act = tb.tree_matmul_silu_mul(x, w_il, tb.DeviceGroup(tp), cfg, lf)
         torch.cuda.synchronize()
         assert torch.equal(act.view(torch.int16), ref.view(torch.int16)), f"tp={tp}"
+
+
+def test_attention_tc_invariance_and_tolerance(tb, cuda):
+    """Tensor-core flash attention: bit-identical across batch composition, head
+    sharding and reruns; within tolerance of the exact two-pass kernel and of an
+    f64 causal softmax."""
+    import ctypes as C
+    B, S, nq, nkv, D = 3, 200, 8, 2, 128
+    g = torch.Generator(device=cuda).manual_seed(7)
+    q = (torch.randn(B * S, nq * D, device=cuda, generator=g) * 2).to(torch.bfloat16)
+    k = (torch.randn(B * S, nkv * D, device=cuda, generator=g) * 2).to(torch.bfloat16)
+    v = torch.randn(B * S, nkv * D, device=cuda, generator=g).to(torch.bfloat16)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    scale = 1.0 / np.sqrt(D)
+
+    def run(fn, qq, kk, vv, b, nqh, nkvh):
+        o = torch.empty(b * S, nqh * D, device=cuda, dtype=torch.bfloat16)
+        tb.api.check(fn(vp(qq), qq.stride(0), vp(kk), kk.stride(0), vp(vv), vv.stride(0), b, S, nqh, nkvh, D,
+                        scale, vp(o), o.stride(0), s))
+        return o
+
+    fast = run(tb.lib.tbik_attention_prefill_tc, q, k, v, B, nq, nkv)
+    again = run(tb.lib.tbik_attention_prefill_tc, q, k, v, B, nq, nkv)
+    assert torch.equal(fast.view(torch.int16), again.view(torch.int16))
+    # batch composition: sequence 1 alone
+    one = run(tb.lib.tbik_attention_prefill_tc, q[S:2 * S].contiguous(), k[S:2 * S].contiguous(),
+              v[S:2 * S].contiguous(), 1, nq, nkv)
+    assert torch.equal(fast[S:2 * S].view(torch.int16), one.view(torch.int16))
+    # head sharding (TP=2): q heads 4..7 with kv head 1
+    shard = run(tb.lib.tbik_attention_prefill_tc, q[:, 4 * D:].contiguous(), k[:, D:].contiguous(),
+                v[:, D:].contiguous(), B, nq // 2, nkv // 2)
+    assert torch.equal(fast[:, 4 * D:].contiguous().view(torch.int16), shard.view(torch.int16))
+    exact = run(tb.lib.tbik_attention_prefill, q, k, v, B, nq, nkv)
+    assert (fast.float() - exact.float()).abs().max().item() < 3e-2
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        q.double().view(B, S, nq, D).transpose(1, 2),
+        k.double().view(B, S, nkv, D).transpose(1, 2).repeat_interleave(nq // nkv, 1),
+        v.double().view(B, S, nkv, D).transpose(1, 2).repeat_interleave(nq // nkv, 1),
+        is_causal=True).transpose(1, 2).reshape(B * S, nq * D)
+    assert (fast.double() - ref).abs().max().item() < 3e-2
+    assert (fast.double() - ref).abs().mean().item() < 2e-3

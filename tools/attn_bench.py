@@ -1,4 +1,5 @@
-"""Time the deterministic GQA prefill attention kernel (tbik_attention_prefill) at
+"""Time the deterministic GQA prefill attention kernels (tbik_attention_prefill, exact
+two-pass order; tbik_attention_prefill_tc, tensor-core flash form) at
 the Llama-3.1-8B forward shape (B=4, S=256, 32 q / 8 kv heads, D=128) against
 PyTorch SDPA (non-deterministic-order, bf16 tensor cores)."""
 import ctypes as C
@@ -20,8 +21,8 @@ o = torch.empty(B * S, NQ * D, device="cuda", dtype=torch.bfloat16)
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def run():
-    check(lib.tbik_attention_prefill(C.c_void_p(q.data_ptr()), NQ * D, C.c_void_p(k.data_ptr()), NKV * D,
+def run(fn=lib.tbik_attention_prefill):
+    check(fn(C.c_void_p(q.data_ptr()), NQ * D, C.c_void_p(k.data_ptr()), NKV * D,
                                             C.c_void_p(v.data_ptr()), NKV * D, B, S, NQ, NKV, D, 1.0 / D ** 0.5,
                                             C.c_void_p(o.data_ptr()), NQ * D, st))
 
@@ -46,5 +47,6 @@ qs, ks, vs = (t.view(B, S, -1, D).transpose(1, 2) for t in (q, k, v))
 ms_sdpa = timeit(lambda: torch.nn.functional.scaled_dot_product_attention(qs, ks, vs, is_causal=True,
                                                                            enable_gqa=True))
 fl = 4.0 * B * NQ * S * (S + 1) / 2 * D
-print(f"tbik attention {ms*1e3:.1f} us ({fl/ms/1e9:.1f} TFLOP/s), run-to-run identical={same}; "
-      f"SDPA {ms_sdpa*1e3:.1f} us")
+ms_tc = timeit(lambda: run(lib.tbik_attention_prefill_tc))
+print(f"tbik attention exact {ms*1e3:.1f} us ({fl/ms/1e9:.1f} TFLOP/s), run-to-run identical={same}; "
+      f"tensor-core flash {ms_tc*1e3:.1f} us ({fl/ms_tc/1e9:.1f} TFLOP/s); SDPA {ms_sdpa*1e3:.1f} us")

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/e54_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/e54_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/e54_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/e54_smoke.log
