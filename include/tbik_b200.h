@@ -331,6 +331,12 @@ TBIK_API tbik_status tbik_silu_mul(const float* gate_up, int64_t ld, int64_t row
 /* h = bf16(h + f) in place (demo.cpp:216). */
 TBIK_API tbik_status tbik_residual_add(void* h, int64_t ldh, const float* f, int64_t ldf, int64_t rows,
                                        int64_t cols, void* stream);
+/* h = bf16(h + f) in place, then y = tree RMSNorm of the new h (bf16 -> bf16):
+ * exactly tbik_residual_add followed by tbik_tree_rmsnorm, in one pass when the
+ * rows are 16-byte aligned with cols % 8 == 0 and cols <= 8192. */
+TBIK_API tbik_status tbik_residual_rmsnorm(void* h, int64_t ldh, const float* f, int64_t ldf, const float* gamma,
+                                           float eps, void* y, int64_t ldy, int64_t rows, int64_t cols,
+                                           void* stream);
 
 #ifdef __cplusplus
 }

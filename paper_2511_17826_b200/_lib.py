@@ -118,6 +118,7 @@ _SIGS = {
     "tbik_attention_prefill_tc": (ci, [vp, i64, vp, i64, vp, i64, i64, ci, ci, ci, ci, C.c_float, vp, i64, vp]),
     "tbik_silu_mul": (ci, [PF, i64, i64, i64, vp, i64, vp]),
     "tbik_residual_add": (ci, [vp, i64, PF, i64, i64, i64, vp]),
+    "tbik_residual_rmsnorm": (ci, [vp, i64, PF, i64, PF, C.c_float, vp, i64, i64, i64, vp]),
     "tbik_debug_tc_stats": (ci, [C.POINTER(C.c_ulonglong), ci]),
     "tbik_matrix_write": (ci, [C.c_char_p, vp, ci, i64, i64]),
     "tbik_matrix_read_header": (ci, [C.c_char_p, C.POINTER(ci), PI64, PI64]),

@@ -63,6 +63,42 @@ __global__ void rope_kernel(const float* __restrict__ x, int64_t ldx, int64_t co
   }
 }
 
+// Vectorised form (D % 8 == 0, 16-byte aligned rows): thread = (head, 4 dims d..d+3
+// of the first half); it produces out[d..d+3] and out[d+D/2..+3] with the same
+// operations as rope_kernel.  Several rows per CTA (blockDim.y).
+__global__ void rope_vec_kernel(const float* __restrict__ x, int64_t ldx, int64_t col0, int heads, int D,
+                                const int* __restrict__ pos, const float* __restrict__ cos_t,
+                                const float* __restrict__ sin_t, uint16_t* __restrict__ out, int64_t ldo,
+                                int64_t rows) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
+  if (row >= rows) return;
+  const int half = D / 2, qpr = half / 4;  // float4 quads per half head
+  const int p = pos[row];
+  for (int e = threadIdx.x; e < heads * qpr; e += blockDim.x) {
+    const int h = e / qpr, d = (e - h * qpr) * 4;
+    const float* xh = x + row * ldx + col0 + h * D;
+    const float4 a = *reinterpret_cast<const float4*>(xh + d);
+    const float4 b = *reinterpret_cast<const float4*>(xh + d + half);
+    const float4 c = *reinterpret_cast<const float4*>(cos_t + static_cast<int64_t>(p) * half + d);
+    const float4 sn = *reinterpret_cast<const float4*>(sin_t + static_cast<int64_t>(p) * half + d);
+    const float lo0 = __fsub_rn(__fmul_rn(a.x, c.x), __fmul_rn(b.x, sn.x));
+    const float lo1 = __fsub_rn(__fmul_rn(a.y, c.y), __fmul_rn(b.y, sn.y));
+    const float lo2 = __fsub_rn(__fmul_rn(a.z, c.z), __fmul_rn(b.z, sn.z));
+    const float lo3 = __fsub_rn(__fmul_rn(a.w, c.w), __fmul_rn(b.w, sn.w));
+    const float hi0 = __fadd_rn(__fmul_rn(b.x, c.x), __fmul_rn(a.x, sn.x));
+    const float hi1 = __fadd_rn(__fmul_rn(b.y, c.y), __fmul_rn(a.y, sn.y));
+    const float hi2 = __fadd_rn(__fmul_rn(b.z, c.z), __fmul_rn(a.z, sn.z));
+    const float hi3 = __fadd_rn(__fmul_rn(b.w, c.w), __fmul_rn(a.w, sn.w));
+    uint16_t* o = out + row * ldo + h * D;
+    *reinterpret_cast<uint2*>(o + d) =
+        make_uint2(f32_to_bf16_bits(lo0) | (static_cast<uint32_t>(f32_to_bf16_bits(lo1)) << 16),
+                   f32_to_bf16_bits(lo2) | (static_cast<uint32_t>(f32_to_bf16_bits(lo3)) << 16));
+    *reinterpret_cast<uint2*>(o + d + half) =
+        make_uint2(f32_to_bf16_bits(hi0) | (static_cast<uint32_t>(f32_to_bf16_bits(hi1)) << 16),
+                   f32_to_bf16_bits(hi2) | (static_cast<uint32_t>(f32_to_bf16_bits(hi3)) << 16));
+  }
+}
+
 // f32 -> bf16 copy of a column block (V of qkv, storage casts).
 __global__ void cast_kernel(const float* __restrict__ x, int64_t ldx, int64_t cols, uint16_t* __restrict__ out,
                             int64_t ldo) {
@@ -577,8 +613,19 @@ tbik_status tbik_rope(const float* x, int64_t ldx, int64_t col0, int heads, int 
   if (!x || !positions || !cos_table || !sin_table || !out) return set_error(TBIK_BAD_ARGUMENT, "null argument");
   if (head_dim % 2 || heads < 1 || rows < 1) return set_error(TBIK_BAD_DIMENSION, "rope: bad dimensions");
   TBIK_TRY(need_device());
-  rope_kernel<<<static_cast<unsigned>(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      x, ldx, col0, heads, head_dim, positions, cos_table, sin_table, static_cast<uint16_t*>(out), ldo);
+  const bool vec = head_dim % 8 == 0 && ldx % 4 == 0 && col0 % 4 == 0 && ldo % 4 == 0 &&
+                   (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 7) == 0 &&
+                   (reinterpret_cast<uintptr_t>(cos_table) & 15) == 0 && (reinterpret_cast<uintptr_t>(sin_table) & 15) == 0;
+  if (vec) {
+    const int threads = heads * head_dim / 8;
+    const int tx = threads < 256 ? ((threads + 31) / 32) * 32 : 256;
+    const int ty = 256 / tx;
+    rope_vec_kernel<<<static_cast<unsigned>((rows + ty - 1) / ty), dim3(tx, ty), 0, static_cast<cudaStream_t>(stream)>>>(
+        x, ldx, col0, heads, head_dim, positions, cos_table, sin_table, static_cast<uint16_t*>(out), ldo, rows);
+  } else {
+    rope_kernel<<<static_cast<unsigned>(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        x, ldx, col0, heads, head_dim, positions, cos_table, sin_table, static_cast<uint16_t*>(out), ldo);
+  }
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;

@@ -223,6 +223,60 @@ __global__ void __launch_bounds__(LANES) tree_rmsnorm_kernel(const TX* __restric
   }
 }
 
+// h = bf16(h + f) (tbik_residual_add, demo.cpp:216) fused with the tree RMSNorm of
+// the new h (bf16 -> bf16): the new row chunks are written back and kept in
+// registers as the norm's cache, so the norm sees exactly the bits
+// tree_rmsnorm_kernel would read.  cols % 8 == 0, cols <= CACHE * 256 * 8, 16-byte
+// aligned rows (the launcher checks; otherwise it runs the two kernels).
+__global__ void __launch_bounds__(LANES) residual_rmsnorm_kernel(uint16_t* __restrict__ Hm, int64_t ldh,
+                                                                 const float* __restrict__ F, int64_t ldf,
+                                                                 const float* __restrict__ gamma, float eps,
+                                                                 uint16_t* __restrict__ Y, int64_t ldy, int64_t cols) {
+  __shared__ float sh[9];
+  constexpr int CH = 8;
+  constexpr int CACHE = 4;
+  uint16_t* h = Hm + static_cast<int64_t>(blockIdx.x) * ldh;
+  const float* f = F + static_cast<int64_t>(blockIdx.x) * ldf;
+  uint16_t* y = Y + static_cast<int64_t>(blockIdx.x) * ldy;
+  const int64_t nfull = cols / CH;
+  uint4 cache[CACHE];
+#pragma unroll
+  for (int k = 0; k < CACHE; ++k) {
+    const int64_t c = threadIdx.x + static_cast<int64_t>(k) * LANES;
+    if (c < nfull) {
+      const uint4 hv = *reinterpret_cast<const uint4*>(h + c * CH);
+      const float4 f0 = *reinterpret_cast<const float4*>(f + c * CH);
+      const float4 f1 = *reinterpret_cast<const float4*>(f + c * CH + 4);
+      uint4 nv;
+      nv.x = f32_to_bf16_bits(__fadd_rn(bf16_bits_to_f32(hv.x & 0xFFFF), f0.x)) |
+             (static_cast<uint32_t>(f32_to_bf16_bits(__fadd_rn(bf16_bits_to_f32(hv.x >> 16), f0.y))) << 16);
+      nv.y = f32_to_bf16_bits(__fadd_rn(bf16_bits_to_f32(hv.y & 0xFFFF), f0.z)) |
+             (static_cast<uint32_t>(f32_to_bf16_bits(__fadd_rn(bf16_bits_to_f32(hv.y >> 16), f0.w))) << 16);
+      nv.z = f32_to_bf16_bits(__fadd_rn(bf16_bits_to_f32(hv.z & 0xFFFF), f1.x)) |
+             (static_cast<uint32_t>(f32_to_bf16_bits(__fadd_rn(bf16_bits_to_f32(hv.z >> 16), f1.y))) << 16);
+      nv.w = f32_to_bf16_bits(__fadd_rn(bf16_bits_to_f32(hv.w & 0xFFFF), f1.z)) |
+             (static_cast<uint32_t>(f32_to_bf16_bits(__fadd_rn(bf16_bits_to_f32(hv.w >> 16), f1.w))) << 16);
+      *reinterpret_cast<uint4*>(h + c * CH) = nv;
+      cache[k] = nv;
+    }
+  }
+  float acc = 0.0f;
+#pragma unroll
+  for (int k = 0; k < CACHE; ++k) {
+    const int64_t c = threadIdx.x + static_cast<int64_t>(k) * LANES;
+    if (c < nfull) acc = sumsq_chunk<uint16_t>(cache[k], acc);
+  }
+  const float ss = block_tree_sum(acc, sh);
+  const float ms = __fdiv_rn(ss, static_cast<float>(cols));
+  const float denom = __fsqrt_rn(__fadd_rn(ms, eps));
+  const float rcp = __frcp_rn(denom);
+#pragma unroll
+  for (int k = 0; k < CACHE; ++k) {
+    const int64_t c = threadIdx.x + static_cast<int64_t>(k) * LANES;
+    if (c < nfull) norm_chunk<uint16_t, uint16_t>(cache[k], gamma, c * CH, denom, rcp, y);
+  }
+}
+
 // ---- log-softmax ----------------------------------------------------------------
 // Group states: one CTA per (row, group) of n = v_local / groups logits.  Lane l
 // owns chunks l, l+256, ... of 4 logits and consumes them in blocks of MSB of its
@@ -427,6 +481,28 @@ tbik_status tbik_tree_rmsnorm(const void* X, int x_dtype, int64_t ldx, const flo
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;
+}
+
+tbik_status tbik_residual_rmsnorm(void* h, int64_t ldh, const float* f, int64_t ldf, const float* gamma, float eps,
+                                  void* y, int64_t ldy, int64_t rows, int64_t cols, void* stream) {
+  if (!h || !f || !gamma || !y) return set_error(TBIK_BAD_ARGUMENT, "null argument");
+  if (rows < 1 || cols < 1) return set_error(TBIK_BAD_DIMENSION, "residual_rmsnorm: dimensions must be >= 1");
+  if (ldh < cols || ldf < cols || ldy < cols) return set_error(TBIK_BAD_ARGUMENT, "residual_rmsnorm: leading dimension < cols");
+  if (rows > 0x7FFFFFFF) return set_error(TBIK_UNSUPPORTED, "residual_rmsnorm: too many rows");
+  const auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (cols % 8 == 0 && cols <= 4 * LANES * 8 && ldh % 8 == 0 && ldf % 4 == 0 && ldy % 8 == 0 && a16(h) && a16(f) &&
+      a16(y) && a16(gamma)) {
+    if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
+    residual_rmsnorm_kernel<<<static_cast<unsigned>(rows), LANES, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<uint16_t*>(h), ldh, f, ldf, gamma, eps, static_cast<uint16_t*>(y), ldy, cols);
+    TBIK_CUDA(cudaGetLastError());
+    count_launch();
+    return TBIK_OK;
+  }
+  // unfused: the same two kernels back to back (same bits)
+  const tbik_status st = tbik_residual_add(h, ldh, f, ldf, rows, cols, stream);
+  if (st != TBIK_OK) return st;
+  return tbik_tree_rmsnorm(h, TBIK_BF16, ldh, gamma, eps, y, TBIK_BF16, ldy, rows, cols, stream);
 }
 
 tbik_status tbik_logsoftmax_shard_state(const float* logits, int64_t ld, int64_t rows, int64_t v_local, int64_t groups,

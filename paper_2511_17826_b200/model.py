@@ -11,7 +11,7 @@ with every reduction in a fixed, shard-independent order:
   qkv / gate_up / lm column_parallel_forward      per column: identical at any TP
   RoPE, attention    tbik_rope, tbik_attention_prefill   per token / (seq, head)
   o_proj, down_proj  row_parallel_forward         TBIK tree GEMM + tree all-reduce
-  residual           tbik_residual_add            h = bf16(h + f)  (demo.cpp:216)
+  residual + norm    tbik_residual_rmsnorm        h = bf16(h + f)  (demo.cpp:216), then tree RMSNorm
   log-probs          tbik_tree_logsoftmax_local   vocab-sharded (m, s) tree
 
 so logits and log-probs are bit-identical for TP = 1/2/4/8 and for any batch
@@ -176,6 +176,15 @@ class TbikDecoder:
         import torch
         return api.rmsnorm(x, gamma, self.cfg.rms_eps, out_dtype=torch.bfloat16)
 
+    def _residual_norm(self, h, f, gamma):
+        """h = bf16(h + f) in place, returns tree_rmsnorm(h) (bf16) -- one fused pass."""
+        import torch
+        M, H = h.shape
+        y = torch.empty(M, H, device=h.device, dtype=torch.bfloat16)
+        check(lib.tbik_residual_rmsnorm(_vp(h), h.stride(0), _vp(f), f.stride(0), _vp(gamma), self.cfg.rms_eps,
+                                        _vp(y), H, M, H, self._stream()))
+        return y
+
     def _stream(self):
         import torch
         return C.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -212,8 +221,8 @@ class TbikDecoder:
         qcols = nq * D
         kcols = nkv * D
         scale = 1.0 / math.sqrt(D)
-        for lw in w.layers:
-            a = self._norm(h, lw.ln1)
+        a = self._norm(h, w.layers[0].ln1) if w.layers else None
+        for li, lw in enumerate(w.layers):
             qkv = self._col(a, lw.wqkv, tp)                      # f32 [M, (nq + 2 nkv) D]
             ld = qkv.stride(0)
             if cfg.qk_norm:
@@ -233,12 +242,13 @@ class TbikDecoder:
             check(attn_fn(_vp(q), qcols, _vp(k), kcols, _vp(v), kcols, B, S, nq, nkv, D,
                           scale, _vp(attn), qcols, self._stream()))
             o = self._row(attn, lw.wo, tp, self.bcfg)            # f32 [M, H], tree all-reduce over tp
-            check(lib.tbik_residual_add(_vp(h), H, _vp(o), H, M, H, self._stream()))
-            a = self._norm(h, lw.ln2)
+            a = self._residual_norm(h, o, lw.ln2)               # h = bf16(h + o); a = norm(h)
             act = api.tree_matmul_silu_mul(a, lw.wgu, api.DeviceGroup(tp), self.bcfg, self.leaf)  # bf16 [M, I]
             d = self._row(act, lw.wd, tp, self.bcfg_down)        # f32 [M, H]
-            check(lib.tbik_residual_add(_vp(h), H, _vp(d), H, M, H, self._stream()))
-        a = self._norm(h, w.ln_f)
+            nxt = w.layers[li + 1].ln1 if li + 1 < len(w.layers) else w.ln_f
+            a = self._residual_norm(h, d, nxt)                  # next layer's ln1 (or ln_f)
+        if not w.layers:
+            a = self._norm(h, w.ln_f)
         return self._col(a, w.lm_head, tp)                      # f32 logits [M, vocab]
 
     def log_probs(self, logits, tp: int = 1, targets=None, full: bool = True):

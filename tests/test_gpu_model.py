@@ -204,3 +204,25 @@ def test_attention_tc_invariance_and_tolerance(tb, cuda):
         is_causal=True).transpose(1, 2).reshape(B * S, nq * D)
     assert (fast.double() - ref).abs().max().item() < 3e-2
     assert (fast.double() - ref).abs().mean().item() < 2e-3
+
+
+@pytest.mark.parametrize("rows,cols", [(37, 4096), (5, 5120), (3, 8192), (4, 9000), (2, 100)])
+def test_residual_rmsnorm_fused_equals_two_kernels(tb, cuda, rows, cols):
+    """tbik_residual_rmsnorm == tbik_residual_add then tbik_tree_rmsnorm, bit for bit
+    (fused pass for 16-byte rows with cols % 8 == 0 and cols <= 8192, else the two
+    kernels)."""
+    import ctypes as C
+    g = torch.Generator(device=cuda).manual_seed(cols)
+    h0 = torch.randn(rows, cols, device=cuda, generator=g).to(torch.bfloat16)
+    f = torch.randn(rows, cols, device=cuda, generator=g)
+    gamma = torch.randn(cols, device=cuda, generator=g) * 0.1 + 1
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    h1 = h0.clone()
+    y1 = torch.empty(rows, cols, device=cuda, dtype=torch.bfloat16)
+    tb.api.check(tb.lib.tbik_residual_rmsnorm(vp(h1), cols, vp(f), cols, vp(gamma), 1e-5, vp(y1), cols, rows, cols, s))
+    h2 = h0.clone()
+    tb.api.check(tb.lib.tbik_residual_add(vp(h2), cols, vp(f), cols, rows, cols, s))
+    y2 = tb.rmsnorm(h2, gamma, 1e-5, out_dtype=torch.bfloat16)
+    assert torch.equal(h1.view(torch.int16), h2.view(torch.int16))
+    assert torch.equal(y1.view(torch.int16), y2.view(torch.int16))
