@@ -85,6 +85,63 @@ __device__ __forceinline__ float tb_exp_nonpos_normal(float x) {
   return __fmul_rn(y, __uint_as_float(sc));
 }
 
+// Packed two-lane f32 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2): each lane is
+// the IEEE RN operation of the scalar form, so results are bit-identical and the
+// instruction count of a polynomial halves.
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b,
+                                                     unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2_add(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// tb_exp_nonpos_normal of two arguments at once (x in [-86, 0] or NaN), same bits.
+__device__ __forceinline__ void tb_exp_nonpos_normal2(float a, float b, float& ea, float& eb) {
+  const unsigned long long magic = f2_pack(12582912.0f, 12582912.0f);
+  const unsigned long long x = f2_pack(a, b);
+  const unsigned long long t = f2_fma(x, f2_pack(1.44269502162933349609f, 1.44269502162933349609f), magic);
+  const unsigned long long kf = f2_sub(t, magic);
+  unsigned long long r = f2_fma(kf, f2_pack(-0.693359375f, -0.693359375f), x);
+  r = f2_fma(kf, f2_pack(2.12194440e-4f, 2.12194440e-4f), r);
+  unsigned long long p = f2_fma(f2_pack(1.9875691500e-4f, 1.9875691500e-4f), r,
+                                f2_pack(1.3981999507e-3f, 1.3981999507e-3f));
+  p = f2_fma(p, r, f2_pack(8.3334519073e-3f, 8.3334519073e-3f));
+  p = f2_fma(p, r, f2_pack(4.1665795894e-2f, 4.1665795894e-2f));
+  p = f2_fma(p, r, f2_pack(1.6666665459e-1f, 1.6666665459e-1f));
+  p = f2_fma(p, r, f2_pack(5.0000001201e-1f, 5.0000001201e-1f));
+  const unsigned long long r2 = f2_mul(r, r);
+  unsigned long long y = f2_fma(p, r2, r);
+  y = f2_add(y, f2_pack(1.0f, 1.0f));
+  float tl, th;
+  f2_unpack(t, tl, th);
+  const uint32_t sl = (__float_as_uint(tl) << 23) + ((127u - 0x4B400000u) << 23);
+  const uint32_t sh = (__float_as_uint(th) << 23) + ((127u - 0x4B400000u) << 23);
+  f2_unpack(f2_mul(y, f2_pack(__uint_as_float(sl), __uint_as_float(sh))), ea, eb);
+}
+
 // bf16(silu(z) * up), silu(z) = z / (1 + exp(-z))  (demo.cpp:36-45, :171-174) -- the
 // one definition used by the SiLU*up kernel and the gate_up GEMM epilogue.
 __device__ __forceinline__ uint16_t tb_silu_mul_bf16(float z, float up) {

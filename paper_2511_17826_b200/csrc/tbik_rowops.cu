@@ -326,8 +326,14 @@ __global__ void __launch_bounds__(LANES, 4) ms_group_kernel(const float* __restr
         // every x - m >= lo - m (rounding is monotone): when that is >= -86 no
         // element needs tb_exp_nonpos's underflow handling (NaNs agree either way)
         if (__fsub_rn(lo, m) >= -86.0f) {
+          const unsigned long long m2 = f2_pack(m, m);
 #pragma unroll
-          for (int k = 0; k < MSB * 4; ++k) sum = __fadd_rn(sum, tb_exp_nonpos_normal(__fsub_rn(v[k], m)));
+          for (int k = 0; k < MSB * 4; k += 2) {
+            float d0, d1, e0, e1;
+            f2_unpack(f2_sub(f2_pack(v[k], v[k + 1]), m2), d0, d1);
+            tb_exp_nonpos_normal2(d0, d1, e0, e1);
+            sum = __fadd_rn(__fadd_rn(sum, e0), e1);
+          }
         } else {
 #pragma unroll
           for (int k = 0; k < MSB * 4; ++k) sum = __fadd_rn(sum, tb_exp_nonpos(__fsub_rn(v[k], m)));
