@@ -184,6 +184,10 @@ int64_t tc_split_units(const GemmView& v) {
 tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mode, cudaStream_t s) {
   const size_t slice = static_cast<size_t>(v.M) * v.N;
   if (leaf_mode == TBIK_LEAF_TCGEN05) {
+    if (tc_use_skinny(v)) {
+      const tbik_status st = launch_tc_skinny(v, C, ldc, s);
+      if (st != TBIK_UNSUPPORTED) return st;
+    }
     const int64_t units = tc_split_units(v);
     if (units <= 1) {
       GemmOut o{OUT_FULL, v.T, C, ldc, 0};

@@ -1,0 +1,527 @@
+// tbik_gemm_skinny.cu -- the tensor-core-leaf TBIK GEMM for skinny activations
+// (decode-sized M <= 128), where the weight stream is the whole cost.
+//
+// Swap-AB: the MMA's 128-row operand is a 128-column slice of the WEIGHTS
+// (W[K x N] row-major = MN-major A, read by TMA exactly as the wide kernel reads
+// B) and the tokens are the MMA N dimension (MT = 16/32/64/128, K-major B = X rows).
+// D[n][m] = sum_k W[k][n] X[m][k] lands in TMEM with lane = weight column and
+// column = token, so a leaf drains MT x 4 bytes per lane instead of the
+// 128-row padded tile of the wide kernel (tbik_gemm_tc.cu), and shared memory
+// goes to weight stages (12 / 11 / 9 stages of 16 KB).
+//
+// The per-element arithmetic is the wide kernel's: the leaf P_t is block_k/16
+// tcgen05 kind::f16 MMAs (K = 16 each) into a zeroed f32 accumulator -- each
+// output element is the same 16-product K steps in the same order; only which
+// operand sits in the A slot differs, and the product a*b is commutative
+// (checked bit for bit against the wide kernel over every shape class in
+// tests/test_gpu_gemm.py::test_skinny_*).  Above the leaf everything is the
+// reference's reduction in its order:
+//   level 0   g = ((0 + P_0) + P_1) + ... + P_{kf-1}         (matmul.cpp:100-125)
+//   levels>=1 binary counter over group values, new + old     (matmul.cpp:107-123)
+//   units     when the tiles alone leave SMs idle, the K range of a tile is cut
+//             into X <= 8 aligned 2^j-group subtrees (or, for a view of few
+//             groups -- a TP shard --, its single leaves), one per CTA of a
+//             thread-block cluster of X CTAs.  Each CTA leaves its unit value in
+//             shared memory; after a cluster barrier CTA u evaluates rows
+//             [u R, u R + R) of the tile over all X values read through DSMEM, in
+//             the fold + contiguous-halves tree order (oracle.cpp:11-20,
+//             Theorem 1).  No workspace, no second launch.
+//
+// Warp roles (256 threads, one CTA per SM; persistent over tiles when X = 1):
+//   warp 0  TMA producer: {W 64k x 128n (two 64-column SW128 atoms), X MT x 64k}
+//   warp 1  MMA issuer (one elected thread), NACC TMEM accumulators in rotation
+//   warp 2  TMEM allocator (512 columns: accumulators + tree levels 1..levels)
+//   warps 4-7 merge warps: thread (q, lane) owns weight column n0 + 32q + lane
+//             for all MT tokens (TMEM lane quarter q).
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "tbik_common.cuh"
+#include "tbik_internal.h"
+
+namespace tbik_b200 {
+
+// tbik_gemm_tc.cu (tensor-map helpers shared by the tcgen05 kernels)
+tbik_status tc_make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                           uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+
+namespace {
+
+constexpr int SK_BN = 128;                  // weight columns per tile = MMA M = TMEM lanes
+constexpr int SK_KSTAGE = 64;               // K per pipeline stage
+constexpr int SK_W_ATOM = 64 * SK_KSTAGE * 2;  // one 64-column SW128 atom: 8 KB
+constexpr int SK_W_STAGE = 2 * SK_W_ATOM;   // 16 KB
+constexpr int SK_TMEM_COLS = 512;
+constexpr int SK_SMEM_LIMIT = 232448;
+constexpr int SK_MAX_UNITS = 8;
+constexpr int SK_MAX_M = 128;    // tokens = MMA N (16 / 32 / 64 / 128)  // K-split units = CTAs of one cluster (portable cluster size)
+
+// Tokens per merge thread (TPW) and merge warps (4 lane quarters x MT / TPW).
+template <int MT>
+constexpr int sk_tpw() { return MT > 64 ? 64 : MT; }
+template <int MT>
+constexpr int sk_merge_warps() { return 4 * (MT / sk_tpw<MT>()); }
+template <int MT>
+constexpr int sk_threads() { return 128 + 32 * sk_merge_warps<MT>(); }
+template <int MT>
+constexpr int sk_nacc() { return MT >= 64 ? 2 : 4; }
+template <int MT>
+constexpr int sk_stages() { return (SK_SMEM_LIMIT - 2048) / (SK_W_STAGE + MT * 128); }
+template <int MT>
+constexpr size_t sk_smem() {
+  return 1024 + static_cast<size_t>(sk_stages<MT>()) * (SK_W_STAGE + MT * 128) + 512;
+}
+static_assert(sk_smem<16>() <= SK_SMEM_LIMIT && sk_smem<32>() <= SK_SMEM_LIMIT && sk_smem<64>() <= SK_SMEM_LIMIT &&
+                  sk_smem<128>() <= SK_SMEM_LIMIT,
+              "skinny smem budget");
+// Tree levels that fit in TMEM next to the accumulators.
+template <int MT>
+constexpr int sk_max_levels() { return SK_TMEM_COLS / MT - sk_nacc<MT>(); }
+
+struct SkParams {
+  int M, N, K;
+  int bk, kf, T;
+  int ntiles;
+  int units;           // X: values per tile handed to the finish (1 = the item's value is final)
+  int tiles_per_unit;  // leaves per unit
+  int levels;          // tree levels inside a unit (log2 of its groups; 0 for leaf units)
+  int fold;            // finish: level-0 fold length over unit values (kf for leaf units, else 1)
+  int log_groups;      // finish: log2(units / fold)
+  long long items;
+  float* out;
+  long long ldo;
+};
+
+__device__ __forceinline__ void tmem_ld16r(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld16_dep(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15])
+               :
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+// Whole-cluster barrier (a lone CTA is a cluster of one).
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_map(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float dsmem_ld_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+struct SkItem {
+  int n0, unit, t_begin, t_end;
+};
+// Units of one tile are adjacent items, so they run in the same wave and the
+// tile's finish starts as soon as its slowest unit is done.
+__device__ __forceinline__ SkItem sk_decode(const SkParams& p, long long item) {
+  SkItem it;
+  it.unit = static_cast<int>(item % p.units);
+  it.n0 = static_cast<int>(item / p.units) * SK_BN;
+  it.t_begin = it.unit * p.tiles_per_unit;
+  it.t_end = min(p.T, it.t_begin + p.tiles_per_unit);
+  return it;
+}
+__device__ __forceinline__ int sk_chunks(const SkParams& p, int t) {
+  const int kt0 = t * p.bk;
+  const int kh = (kt0 + p.bk <= p.K) ? p.bk : p.K - kt0;
+  return (kh + SK_KSTAGE - 1) / SK_KSTAGE;
+}
+
+template <int MT>
+__global__ void __launch_bounds__(sk_threads<MT>(), 1)
+    tc_skinny_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                     const SkParams p) {
+  constexpr int NST = sk_stages<MT>();
+  constexpr int NACC = sk_nacc<MT>();
+  constexpr int X_STAGE = MT * 128;
+  constexpr uint32_t TX_BYTES = SK_W_STAGE + X_STAGE;
+  constexpr uint32_t IDESC = umma_idesc_bf16(SK_BN, MT, /*a_mn_major=*/1, /*b_mn_major=*/0);
+  constexpr int TPW = sk_tpw<MT>();
+  constexpr int NMW = sk_merge_warps<MT>();
+  constexpr int NCH = TPW / 16;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = smem;
+  uint8_t* sX = sW + NST * SK_W_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + NST * X_STAGE);
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;
+  uint64_t* tempty = tfull + NACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmX);
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < NACC; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], NMW);  // every merge warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, SK_TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long item = blockIdx.x; item < p.items; item += gridDim.x) {
+        const SkItem it = sk_decode(p, item);
+        for (int t = it.t_begin; t < it.t_end; ++t) {
+          const int nch = sk_chunks(p, t);
+          for (int c = 0; c < nch; ++c) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], TX_BYTES);
+            const int k = t * p.bk + c * SK_KSTAGE;
+            uint8_t* w = sW + stage * SK_W_STAGE;
+            tma_load_2d(w, &tmW, &full[stage], it.n0, k);
+            tma_load_2d(w + SK_W_ATOM, &tmW, &full[stage], it.n0 + 64, k);
+            tma_load_2d(sX + stage * X_STAGE, &tmX, &full[stage], k, 0);
+            if (++stage == NST) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t acc_iter = 0;
+      for (long long item = blockIdx.x; item < p.items; item += gridDim.x) {
+        const SkItem it = sk_decode(p, item);
+        for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
+          const int buf = acc_iter % NACC;
+          const uint32_t use = acc_iter / NACC;
+          mbar_wait(&tempty[buf], (use & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem_base + buf * MT;
+          const int nch = sk_chunks(p, t);
+          for (int c = 0; c < nch; ++c) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t w_base = smem_u32(sW + stage * SK_W_STAGE);
+            const uint32_t x_base = smem_u32(sX + stage * X_STAGE);
+#pragma unroll
+            for (int kk = 0; kk < SK_KSTAGE / 16; ++kk) {
+              // A = W: MN-major SW128, two 64-column atoms 8 KB apart (LBO), 8-row K
+              // groups 1 KB apart (SBO), +16 K rows (2 KB) per step.
+              const uint64_t adesc = umma_desc_sw128(w_base + kk * 2048, SK_W_ATOM, 1024);
+              // B = X: K-major SW128, +32 B per 16-element K step inside the 128 B row.
+              const uint64_t bdesc = umma_desc_sw128(x_base + kk * 32, 16, 1024);
+              umma_bf16(d, adesc, bdesc, IDESC, (c | kk) != 0 ? 1u : 0u);
+            }
+            umma_commit(&empty[stage]);
+            if (++stage == NST) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          umma_commit(&tfull[buf]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q = (warp - 4) & 3;         // TMEM lane quarter
+    const int h0 = ((warp - 4) >> 2) * TPW;  // first token of this warp
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + h0;
+    float g[TPW];
+    uint32_t acc_iter = 0;
+    for (long long item = blockIdx.x; item < p.items; item += gridDim.x) {
+      const SkItem it = sk_decode(p, item);
+      const int n = it.n0 + q * 32 + lane;
+      int t_in_group = 0;
+      uint32_t groups_done = 0;
+      for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
+        const int buf = acc_iter % NACC;
+        const uint32_t use = acc_iter / NACC;
+        mbar_wait(&tfull[buf], use & 1);
+        tc_fence_after();
+        uint32_t r[NCH][16];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) tmem_ld16r(lane_base + buf * MT + c * 16, r[c]);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) tmem_wait_ld16_dep(r[c]);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        // level 0 (0 + P canonicalises a -0 leaf, matmul.cpp:101-103)
+        if (t_in_group == 0 || p.tiles_per_unit == 1) {
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) g[c * 16 + i] = __fadd_rn(0.0f, __uint_as_float(r[c][i]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) g[c * 16 + i] = __fadd_rn(g[c * 16 + i], __uint_as_float(r[c][i]));
+        }
+        if (p.tiles_per_unit > 1 && ++t_in_group < p.kf) continue;
+        t_in_group = 0;
+        // binary counter over this unit's groups, levels in TMEM slots
+        if (p.levels >= 1) {
+          int level = 1;
+          uint32_t c_bits = groups_done++;
+          while (c_bits & 1u) {
+            const uint32_t slot = lane_base + (NACC + level - 1) * MT;
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) tmem_ld16r(slot + c * 16, r[c]);
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) tmem_wait_ld16_dep(r[c]);
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+#pragma unroll
+              for (int i = 0; i < 16; ++i) g[c * 16 + i] = __fadd_rn(g[c * 16 + i], __uint_as_float(r[c][i]));
+            c_bits >>= 1;
+            ++level;
+          }
+          if (level <= p.levels) {
+            const uint32_t slot = lane_base + (NACC + level - 1) * MT;
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) tmem_st16(slot + c * 16, g + c * 16);
+            tmem_wait_st();
+            continue;
+          }
+        }
+      }
+      // g: this unit's value for column n, tokens h0 .. h0 + TPW - 1
+      if (p.units == 1) {
+        if (n < p.N) {
+#pragma unroll
+          for (int m = 0; m < TPW; ++m)
+            if (h0 + m < p.M) p.out[static_cast<size_t>(h0 + m) * p.ldo + n] = g[m];
+        }
+      } else {
+        // cluster mode (one item per CTA): publish the unit value in shared memory
+        // ([MT][128] f32; every MMA that read the stages has completed)
+        float* fbuf = reinterpret_cast<float*>(sW);
+#pragma unroll
+        for (int m = 0; m < TPW; ++m) fbuf[(h0 + m) * SK_BN + q * 32 + lane] = g[m];
+      }
+    }
+  }
+
+  // Finish of a K-split tile inside its cluster: CTA u of the cluster (= unit u)
+  // evaluates rows [u R, u R + R) of the tile over all units' values, read from
+  // the peers' shared memory (DSMEM):
+  //   group j = ((0 + v_{j*fold}) + v_{j*fold+1}) + ...   (level-0 fold; fold = 1
+  //             for subtree units, k_first for leaf units)
+  //   result  = contiguous-halves tree over the groups (binary counter, new + old)
+  // -- the order of tree_combine_kernel (tbik_tree.cu) and of the reference.
+  cluster_sync_all();
+  if (p.units > 1 && warp >= 4) {
+    const int q = (warp - 4) & 3;
+    const int hh = (warp - 4) >> 2;  // with 8 merge warps two threads share a column
+    const int col = q * 32 + lane;
+    const int unit = static_cast<int>(blockIdx.x % p.units);
+    const int n = static_cast<int>(blockIdx.x / p.units) * SK_BN + col;
+    const int R = (p.M + p.units - 1) / p.units;
+    const int m_lo = unit * R, m_hi = min(p.M, m_lo + R);
+    const uint32_t fb = smem_u32(sW);
+    uint32_t peer[SK_MAX_UNITS];
+#pragma unroll
+    for (int x = 0; x < SK_MAX_UNITS; ++x) peer[x] = x < p.units ? dsmem_map(fb, static_cast<uint32_t>(x)) : 0u;
+    if (n < p.N) {
+#pragma unroll 1
+      for (int m = m_lo + hh; m < m_hi; m += NMW / 4) {
+        const uint32_t off = static_cast<uint32_t>((m * SK_BN + col) * 4);
+        float vals[SK_MAX_UNITS];
+#pragma unroll
+        for (int x = 0; x < SK_MAX_UNITS; ++x) vals[x] = x < p.units ? dsmem_ld_f32(peer[x] + off) : 0.0f;
+        float stack[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        float acc = 0.0f;
+        int gcount = 0, in_fold = 0;
+#pragma unroll
+        for (int x = 0; x < SK_MAX_UNITS; ++x) {
+          if (x < p.units) {
+            acc = __fadd_rn(acc, vals[x]);
+            if (++in_fold == p.fold) {
+              float v = acc;
+              int l = 0;
+#pragma unroll
+              for (int b = 0; b < 3; ++b)
+                if (((gcount >> b) & 1) && l == b) {
+                  v = __fadd_rn(v, stack[b]);
+                  l = b + 1;
+                }
+#pragma unroll
+              for (int b = 0; b < 4; ++b)
+                if (l == b) stack[b] = v;
+              ++gcount;
+              in_fold = 0;
+              acc = 0.0f;
+            }
+          }
+        }
+        float res = stack[0];
+#pragma unroll
+        for (int b = 1; b < 4; ++b)
+          if (b == p.log_groups) res = stack[b];
+        p.out[static_cast<size_t>(m) * p.ldo + n] = res;
+      }
+    }
+  }
+  cluster_sync_all();  // peers may still read this CTA's shared memory
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, SK_TMEM_COLS);
+  }
+}
+
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+
+}  // namespace
+
+// The skinny variant serves M <= 128 bf16 views (TBIK_TC_SKINNY=0 turns it off, a
+// pure scheduling choice: the same bits).
+bool tc_use_skinny(const GemmView& v) {
+  if (env_int("TBIK_TC_SKINNY", 1) == 0) return false;
+  return v.adt == TBIK_BF16 && v.bdt == TBIK_BF16 && v.M >= 1 && v.M <= SK_MAX_M && v.bk % SK_KSTAGE == 0 &&
+         v.N <= (int64_t{1} << 30) && v.K <= (int64_t{1} << 30);
+}
+
+tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaStream_t s) {
+  GemmView v = v_in;
+  const int mt = v.M <= 16 ? 16 : v.M <= 32 ? 32 : v.M <= 64 ? 64 : 128;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+
+  SkParams p{};
+  p.M = static_cast<int>(v.M);
+  p.N = static_cast<int>(v.N);
+  p.K = static_cast<int>(v.K);
+  p.bk = static_cast<int>(v.bk);
+  p.kf = static_cast<int>(v.kf);
+  p.T = static_cast<int>(v.T);
+  p.ntiles = static_cast<int>((v.N + SK_BN - 1) / SK_BN);
+  p.out = C;
+  p.ldo = ldc;
+  // Units: aligned 2^j-group subtrees (<= 8, one cluster) until the items cover
+  // ~7/8 of the SMs (K=14336 N=4096: 4 units, 128 CTAs; measured best vs 2 / 8).
+  // TBIK_SK_UNITS / TBIK_SK_LEAF override (tuning knobs; same bits).
+  const int max_levels = mt == 16 ? sk_max_levels<16>() : mt == 32 ? sk_max_levels<32>()
+                       : mt == 64 ? sk_max_levels<64>() : sk_max_levels<128>();
+  const int64_t want = static_cast<int64_t>(sms) * 7 / 8;
+  int64_t units = 1;
+  while (units * 2 <= v.L && units * 2 <= SK_MAX_UNITS && p.ntiles * units * 2 <= want) units *= 2;
+  const int force_u = env_int("TBIK_SK_UNITS", 0);
+  if (force_u >= 1 && force_u <= v.L && force_u <= SK_MAX_UNITS && (force_u & (force_u - 1)) == 0) units = force_u;
+  int lv = 0;
+  while ((int64_t{1} << lv) < v.L / units) ++lv;
+  if (lv > max_levels) return TBIK_UNSUPPORTED;  // caller falls back to the wide kernel (same bits)
+  // Single-leaf units (clusters of T CTAs of one leaf each) measured slower than one
+  // unit per tile for the TP=8 down_proj shard (T = 7: 15 vs 9 us at M = 16, CUDA
+  // graph; the per-CTA prologue outweighs 64 KB of weights), so they are opt-in.
+  const int force_leaf = env_int("TBIK_SK_LEAF", 0);
+  const bool leaf_units = force_leaf != 0 && v.kf > 1 && v.T <= SK_MAX_UNITS;
+  if (leaf_units) {
+    p.units = static_cast<int>(v.T);
+    p.tiles_per_unit = 1;
+    p.levels = 0;
+    p.fold = static_cast<int>(v.kf);
+    int lg = 0;
+    while ((int64_t{1} << lg) < v.L) ++lg;
+    p.log_groups = lg;
+  } else {
+    p.units = static_cast<int>(units);
+    p.tiles_per_unit = static_cast<int>(v.T / units);
+    p.levels = lv;
+    p.fold = 1;
+    int lg = 0;
+    while ((int64_t{1} << lg) < units) ++lg;
+    p.log_groups = lg;
+  }
+  p.items = static_cast<long long>(p.ntiles) * p.units;
+  TBIK_TRY(pad_operand(&v.A, &v.lda, v.M, v.K, 8, s));
+  TBIK_TRY(pad_operand(&v.B, &v.ldb, v.K, v.N, 9, s));
+  CUtensorMap mW, mX;
+  TBIK_TRY(tc_make_map_2d(&mW, v.B, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.K),
+                          static_cast<uint64_t>(v.ldb) * 2, 64, SK_KSTAGE));
+  TBIK_TRY(tc_make_map_2d(&mX, v.A, static_cast<uint64_t>(v.K), static_cast<uint64_t>(v.M),
+                          static_cast<uint64_t>(v.lda) * 2, SK_KSTAGE, static_cast<uint32_t>(mt)));
+  using Kern = void (*)(const CUtensorMap, const CUtensorMap, const SkParams);
+  const Kern kern = mt == 16 ? tc_skinny_kernel<16> : mt == 32 ? tc_skinny_kernel<32>
+                   : mt == 64 ? tc_skinny_kernel<64> : tc_skinny_kernel<128>;
+  const size_t smem = mt == 16 ? sk_smem<16>() : mt == 32 ? sk_smem<32>() : mt == 64 ? sk_smem<64>() : sk_smem<128>();
+  const int threads = mt == 16 ? sk_threads<16>() : mt == 32 ? sk_threads<32>() : mt == 64 ? sk_threads<64>()
+                                                                                          : sk_threads<128>();
+  static bool attr_set[16][4] = {};
+  const int mi = mt == 16 ? 0 : mt == 32 ? 1 : mt == 64 ? 2 : 3;
+  if (dev >= 0 && dev < 16 && !attr_set[dev][mi]) {
+    TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr_set[dev][mi] = true;
+  }
+  // X = 1: persistent over tiles; X > 1: one CTA per (tile, unit), clusters of X.
+  const long long grid = p.units > 1 ? p.items : (p.items < sms ? p.items : sms);
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(static_cast<unsigned>(grid));
+  lc.blockDim = dim3(static_cast<unsigned>(threads));
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(p.units);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  TBIK_CUDA(cudaLaunchKernelEx(&lc, kern, mW, mX, p));
+  TBIK_CUDA(cudaGetLastError());
+  count_launch();
+  return TBIK_OK;
+}
+
+}  // namespace tbik_b200

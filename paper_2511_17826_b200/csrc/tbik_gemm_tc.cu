@@ -742,6 +742,11 @@ int sm_count() {
 
 }  // namespace
 
+tbik_status tc_make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                           uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+  return make_map_2d(map, base, inner, outer, row_stride_bytes, box_inner, box_outer);
+}
+
 int set_tc_sm_cap(int cap) {
   const int old = g_sm_cap;
   g_sm_cap = cap;

@@ -78,6 +78,11 @@ tbik_status pad_operand(const void** p, int64_t* ld, int64_t rows, int64_t cols,
 tbik_status launch_silu_mul_il(const float* gu, int64_t ld, int64_t rows, int64_t inter, uint16_t* out, int64_t ldo,
                                cudaStream_t s);
 
+// Swap-AB tcgen05 kernel for skinny views (M <= 64; tbik_gemm_skinny.cu): the
+// whole tree (units finished in-kernel) into C.  Same bits as launch_tc_gemm.
+bool tc_use_skinny(const GemmView& v);
+tbik_status launch_tc_skinny(const GemmView& v, float* C, int64_t ldc, cudaStream_t s);
+
 // K-split factor run_tree_gemm uses for the tcgen05 leaf (1 = one FULL launch).
 int64_t tc_split_units(const GemmView& v);
 

@@ -275,7 +275,11 @@ def test_errors(tb, cuda):
 # ---------------------------------------------------------------------------------
 SCHEDULES = [{}, {"TBIK_TC_WIDE": "1"}, {"TBIK_TC_GROUP_M": "1"}, {"TBIK_TC_GROUP_M": "3", "TBIK_TC_UNITS": "2"},
              {"TBIK_TC_PAIR": "0"}, {"TBIK_TC_PAIR": "0", "TBIK_TC_UNITS": "4"}, {"TBIK_TC_PAIR": "1"},
-             {"TBIK_TC_ABOX": "32"}, {"TBIK_TC_ABOX": "64", "TBIK_TC_PAIR": "1"}, {"TBIK_TC_DEEP": "1"}]
+             {"TBIK_TC_ABOX": "32"}, {"TBIK_TC_ABOX": "64", "TBIK_TC_PAIR": "1"}, {"TBIK_TC_DEEP": "1"},
+             {"TBIK_TC_SKINNY": "0"}, {"TBIK_SK_UNITS": "1"}, {"TBIK_SK_UNITS": "2", "TBIK_SK_LEAF": "0"},
+             {"TBIK_SK_UNITS": "8"}]
+ENV_KNOBS = ("TBIK_TC_WIDE", "TBIK_TC_GROUP_M", "TBIK_TC_UNITS", "TBIK_TC_PAIR", "TBIK_TC_ABOX", "TBIK_TC_DEEP",
+             "TBIK_TC_SKINNY", "TBIK_SK_UNITS", "TBIK_SK_LEAF")
 
 
 @pytest.mark.parametrize("M,K,N", [(300, 14336, 640), (64, 4096, 512), (513, 6144, 384), (20, 4096, 200),
@@ -287,7 +291,7 @@ def test_tc_schedules_invisible(tb, cuda, orc, M, K, N, monkeypatch):
     cfg = tb.BlockConfig(64, 256, 128, 0)
     outs, leaves = [], []
     for env in SCHEDULES:
-        for k in ("TBIK_TC_WIDE", "TBIK_TC_GROUP_M", "TBIK_TC_UNITS", "TBIK_TC_PAIR", "TBIK_TC_ABOX", "TBIK_TC_DEEP"):
+        for k in ENV_KNOBS:
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -300,6 +304,44 @@ def test_tc_schedules_invisible(tb, cuda, orc, M, K, N, monkeypatch):
     plan = tb.plan_blocks(K, cfg, 1)
     want = orc.tree_over_leaves(leaves[0].cpu().numpy(), plan.k_first)
     assert np.array_equal(bits(outs[0].cpu().numpy()), bits(want))
+
+
+# swap-AB skinny kernel (M <= 128, tbik_gemm_skinny.cu): the same bits as the wide
+# kernel for every token-width class, unit split, leaf split and TP shard view
+@pytest.mark.parametrize("M,K,N", [(1, 14336, 4096), (16, 14336, 640), (17, 4096, 1000), (33, 6144, 384),
+                                   (64, 25600, 256), (65, 14336, 512), (128, 8192, 256), (5, 777, 300)])
+def test_skinny_matches_wide(tb, cuda, M, K, N, monkeypatch):
+    torch.manual_seed(1000 + M)
+    x = torch.randn(M, K, device=cuda).to(torch.bfloat16)
+    w = torch.randn(K, N, device=cuda).to(torch.bfloat16)
+    cfg = tb.BlockConfig(64, 256, 128, 0)
+    monkeypatch.setenv("TBIK_TC_SKINNY", "0")
+    ref = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+    monkeypatch.setenv("TBIK_TC_SKINNY", "1")
+    L = tb.plan_blocks(K, cfg, 1).leaves
+    for u in [0] + [u for u in (1, 2, 4, 8) if u <= L]:
+        if u:
+            monkeypatch.setenv("TBIK_SK_UNITS", str(u))
+        y = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+        assert torch.equal(y.view(torch.int32), ref.view(torch.int32)), f"skinny units={u} changed the bits"
+    monkeypatch.delenv("TBIK_SK_UNITS")
+
+
+@pytest.mark.parametrize("leaf_split", ["0", "1"])
+def test_skinny_tp_shards(tb, cuda, leaf_split, monkeypatch):
+    """Row-parallel TP shards at decode size through the skinny kernel (single-leaf
+    units on the TP=8 shard when forced) == the wide kernel at TP=1."""
+    torch.manual_seed(7)
+    x = torch.randn(16, 14336, device=cuda).to(torch.bfloat16)
+    w = torch.randn(14336, 1024, device=cuda).to(torch.bfloat16)
+    cfg = tb.BlockConfig(64, 256, 128, 0)
+    monkeypatch.setenv("TBIK_TC_SKINNY", "0")
+    ref = tb.row_parallel_forward(x, w, tb.DeviceGroup(1), cfg, 8, tb.LEAF_TCGEN05)
+    monkeypatch.setenv("TBIK_TC_SKINNY", "1")
+    monkeypatch.setenv("TBIK_SK_LEAF", leaf_split)
+    for tp in (1, 2, 4, 8):
+        y = tb.row_parallel_forward(x, w, tb.DeviceGroup(tp), cfg, 8, tb.LEAF_TCGEN05)
+        assert torch.equal(y.view(torch.int32), ref.view(torch.int32)), f"tp={tp}"
 
 
 # ---------------------------------------------------------------------------------
