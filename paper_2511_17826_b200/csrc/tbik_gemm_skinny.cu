@@ -131,9 +131,12 @@ __device__ __forceinline__ uint32_t dsmem_map(uint32_t smem_addr, uint32_t rank)
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
   return r;
 }
-__device__ __forceinline__ float dsmem_ld_f32(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+__device__ __forceinline__ float4 dsmem_ld_f32x4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
   return v;
 }
 
@@ -355,31 +358,38 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
   // -- the order of tree_combine_kernel (tbik_tree.cu) and of the reference.
   cluster_sync_all();
   if (p.units > 1 && warp >= 4) {
-    const int q = (warp - 4) & 3;
-    const int hh = (warp - 4) >> 2;  // with 8 merge warps two threads share a column
-    const int col = q * 32 + lane;
+    // work items: (row, 4-column quad) of this CTA's row slice, 16-byte DSMEM loads
+    // from every unit, two items in flight per thread
+    const int tid = threadIdx.x - 128;
     const int unit = static_cast<int>(blockIdx.x % p.units);
-    const int n = static_cast<int>(blockIdx.x / p.units) * SK_BN + col;
+    const int n0 = static_cast<int>(blockIdx.x / p.units) * SK_BN;
     const int R = (p.M + p.units - 1) / p.units;
     const int m_lo = unit * R, m_hi = min(p.M, m_lo + R);
+    const int nitems = (m_hi > m_lo ? m_hi - m_lo : 0) * (SK_BN / 4);
     const uint32_t fb = smem_u32(sW);
     uint32_t peer[SK_MAX_UNITS];
 #pragma unroll
     for (int x = 0; x < SK_MAX_UNITS; ++x) peer[x] = x < p.units ? dsmem_map(fb, static_cast<uint32_t>(x)) : 0u;
-    if (n < p.N) {
-#pragma unroll 1
-      for (int m = m_lo + hh; m < m_hi; m += NMW / 4) {
-        const uint32_t off = static_cast<uint32_t>((m * SK_BN + col) * 4);
-        float vals[SK_MAX_UNITS];
+#pragma unroll 2
+    for (int idx = tid; idx < nitems; idx += 32 * NMW) {
+      const int m = m_lo + idx / (SK_BN / 4);
+      const int c4 = (idx % (SK_BN / 4)) * 4;
+      const uint32_t off = static_cast<uint32_t>((m * SK_BN + c4) * 4);
+      float4 vals[SK_MAX_UNITS];
 #pragma unroll
-        for (int x = 0; x < SK_MAX_UNITS; ++x) vals[x] = x < p.units ? dsmem_ld_f32(peer[x] + off) : 0.0f;
+      for (int x = 0; x < SK_MAX_UNITS; ++x)
+        vals[x] = x < p.units ? dsmem_ld_f32x4(peer[x] + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float res[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
         float stack[4] = {0.0f, 0.0f, 0.0f, 0.0f};
         float acc = 0.0f;
         int gcount = 0, in_fold = 0;
 #pragma unroll
         for (int x = 0; x < SK_MAX_UNITS; ++x) {
           if (x < p.units) {
-            acc = __fadd_rn(acc, vals[x]);
+            const float vx = j == 0 ? vals[x].x : j == 1 ? vals[x].y : j == 2 ? vals[x].z : vals[x].w;
+            acc = __fadd_rn(acc, vx);
             if (++in_fold == p.fold) {
               float v = acc;
               int l = 0;
@@ -398,11 +408,19 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
             }
           }
         }
-        float res = stack[0];
+        res[j] = stack[0];
 #pragma unroll
         for (int b = 1; b < 4; ++b)
-          if (b == p.log_groups) res = stack[b];
-        p.out[static_cast<size_t>(m) * p.ldo + n] = res;
+          if (b == p.log_groups) res[j] = stack[b];
+      }
+      const int n = n0 + c4;
+      float* dst = p.out + static_cast<size_t>(m) * p.ldo + n;
+      if (n + 3 < p.N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        *reinterpret_cast<float4*>(dst) = make_float4(res[0], res[1], res[2], res[3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (n + j < p.N) dst[j] = res[j];
       }
     }
   }
