@@ -203,6 +203,9 @@ TBIK_API int tbik_group_world_size(const tbik_group* g);
 TBIK_API int tbik_group_rank(const tbik_group* g);
 /* This rank's exchange buffer for the next collective (device pointer). */
 TBIK_API float* tbik_group_send_buffer(tbik_group* g);
+/* Diagnostics: how many row-parallel forwards of this group ran as ONE fused
+ * kernel (tcgen05 GEMM + tile-flag tree all-reduce over peer memory). */
+TBIK_API int64_t tbik_group_fused_count(const tbik_group* g);
 
 /* tree_all_reduce over the group: `partial` (elems f32, may be the send
  * buffer itself) is published, all ranks meet on a device-side flag barrier,

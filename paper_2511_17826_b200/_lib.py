@@ -100,6 +100,7 @@ _SIGS = {
     "tbik_group_send_buffer": (vp, [vp]),
     "tbik_group_world_size": (ci, [vp]),
     "tbik_group_rank": (ci, [vp]),
+    "tbik_group_fused_count": (i64, [vp]),
     "tbik_tree_matmul_hostio": (ci, [vp, ci, i64, vp, ci, i64, PF, i64, i64, i64, i64, PCFG, ci, i64, vp]),
     "tbik_group_row_parallel_forward_hostio": (ci, [vp, vp, ci, i64, vp, ci, i64, PF, i64, i64, i64, i64, i64,
                                                     PCFG, i64, ci, i64, vp]),

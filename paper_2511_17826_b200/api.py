@@ -418,6 +418,10 @@ class PeerGroup:
             lib.tbik_group_destroy(self._h)
             self._h = None
 
+    def fused_count(self) -> int:
+        """Row-parallel forwards that ran as one fused GEMM + tree all-reduce kernel."""
+        return int(lib.tbik_group_fused_count(self._h))
+
     def tree_all_reduce(self, partial, out=None):
         torch = _torch()
         out = torch.empty_like(partial) if out is None else out

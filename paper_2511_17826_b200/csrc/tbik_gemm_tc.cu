@@ -135,6 +135,14 @@ struct TcParams {
   int mc;          // 1: clusters of two pairs on adjacent N tiles share A (ntiles counts tile pairs)
   uint16_t* act;   // non-null: SiLU*up epilogue -- columns interleave gate (even) / up (odd);
   long long ld_act;  //   act[row][j] = bf16(silu(g[2j]) * g[2j+1]) replaces the f32 store
+  // Fused tree all-reduce (ar_W > 1; FULL mode, pair tiles): owner(item) = item % ar_W.
+  int ar_W, ar_rank;
+  uint32_t ar_epoch;
+  const float* ar_src[8];
+  float* ar_dst[8];
+  uint32_t* ar_flags[8];
+  uint32_t* ar_done[8];
+  uint32_t* ar_counter;
   int debug;       // TBIK_TC_DEBUG (perf experiments only; wrong results): 1 = skip the merge,
                    // 2 = skip the output store, 4 = skip the tree above level 0,
                    // 8 = skip the scratch levels, 16 = direct (non-TMA) output stores
@@ -255,15 +263,120 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_complete() {  // all but the N most recent groups WRITTEN
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Bounded spin: a peer that never arrives traps (a CUDA error) instead of hanging.
+__device__ __forceinline__ void spin_until_epoch(const uint32_t* f, uint32_t epoch) {
+  long long n = 0;
+  while (static_cast<int32_t>(ld_acquire_sys(f) - epoch) < 0) {
+    __nanosleep(128);
+    if (++n > (1ll << 27)) __trap();
+  }
+}
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+// Publish "my half of item `item` is in my send slot" to the item's owner rank:
+// flags[owner][(item * 2 + cta) * W + my_rank] = epoch.
+__device__ __forceinline__ void ar_publish(const TcParams& p, long long item, uint32_t cta) {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __threadfence_system();
+  const int owner = static_cast<int>(item % p.ar_W);
+  st_release_sys(p.ar_flags[owner] + ((item * 2 + cta) * p.ar_W + p.ar_rank), p.ar_epoch);
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Fused all-reduce, warps 2-3 (see the kernel): reduce this rank's items of this
+// pair from the peers' send slots, push to every rank's result slot, publish done.
+__device__ __forceinline__ void ar_reduce_owned(const TcParams& p, long long pair, long long npairs, int pid,
+                                             uint32_t rank) {
+    const int rt = threadIdx.x - 64;  // 0..63
+  const int W = p.ar_W;
+  for (long long item = pair; item < p.items; item += npairs) {
+    if (static_cast<int>(item % W) != p.ar_rank) continue;
+    const Item it = decode(p, item, pid);
+    if (rt < W) spin_until_epoch(p.ar_flags[p.ar_rank] + ((item * 2 + rank) * W + rt), p.ar_epoch);
+    named_bar(2, 64);
+    const int r0 = it.m0 + static_cast<int>(rank) * BM;
+    const int rows = min(BM, p.M - r0);
+    const int cols = min(BN, p.N - it.n0);
+    if (rows <= 0) continue;
+    if (cols == BN && (p.ldo & 3) == 0) {
+      const int nq = rows * (BN / 4);
+      for (int idx = rt; idx < nq; idx += 64) {
+        const size_t e4 = (static_cast<size_t>(r0 + idx / (BN / 4)) * p.ldo + it.n0) / 4 + idx % (BN / 4);
+        float4 r[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < W) r[k] = __ldcv(reinterpret_cast<const float4*>(p.ar_src[k]) + e4);
+#pragma unroll
+        for (int l = 1; l <= 3; ++l) {
+          const int st = 1 << l, h = 1 << (l - 1);
+#pragma unroll
+          for (int left = 0; left < 8; left += st)
+            if (left + h < W) {
+              r[left].x = __fadd_rn(r[left].x, r[left + h].x);
+              r[left].y = __fadd_rn(r[left].y, r[left + h].y);
+              r[left].z = __fadd_rn(r[left].z, r[left + h].z);
+              r[left].w = __fadd_rn(r[left].w, r[left + h].w);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < W) reinterpret_cast<float4*>(p.ar_dst[(p.ar_rank + k) & (W - 1)])[e4] = r[0];
+      }
+    } else {
+      const int ne = rows * cols;
+      for (int idx = rt; idx < ne; idx += 64) {
+        const size_t e = static_cast<size_t>(r0 + idx / cols) * p.ldo + it.n0 + idx % cols;
+        float r[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < W) r[k] = __ldcv(p.ar_src[k] + e);
+#pragma unroll
+        for (int l = 1; l <= 3; ++l) {
+          const int st = 1 << l, h = 1 << (l - 1);
+#pragma unroll
+          for (int left = 0; left < 8; left += st)
+            if (left + h < W) r[left] = __fadd_rn(r[left], r[left + h]);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < W) p.ar_dst[(p.ar_rank + k) & (W - 1)][e] = r[0];
+      }
+    }
+  }
+  // every CTA of this rank is done with its owned items: the last one tells all peers
+  __threadfence_system();
+  named_bar(2, 64);
+  if (rt == 0) {
+    const uint32_t prev = atomicAdd(p.ar_counter, 1u);
+    if (prev == gridDim.x - 1) {
+      *p.ar_counter = 0;
+      __threadfence_system();
+      for (int r = 0; r < W; ++r) st_release_sys(p.ar_done[r] + p.ar_rank, p.ar_epoch);
+    }
+  }
 }
 
 // EPI merge warps (two per TMEM lane quarter, splitting the 128 columns), ABOX
 // A rows staged per stage (128, or 64 / 32 for small M; stage count follows).  KF1 (used when k_first == 1, where every leaf completes a
 // group and g need not persist across leaves): the level-1 slot is loaded in the
 // same batch as the leaf, so an odd leaf costs one TMEM round trip, not two.
-template <int EPI, bool KF1, int ABOX, bool PAIR, bool DEEP, bool MC = false>
+// AR: the fused tree all-reduce variant (pair tiles, FULL mode; tbik_group.cu).
+template <int EPI, bool KF1, int ABOX, bool PAIR, bool DEEP, bool MC = false, bool AR = false>
 __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     tc_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const TcParams p) {
@@ -422,6 +535,14 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       }
     }
     __syncwarp();
+  } else if (AR) {
+    // ---------------- fused tree all-reduce (warps 2-3, both CTAs) ----------------
+    // For every item this pair computes and this rank owns (item % W == rank): wait
+    // until all W ranks published this CTA's 128-row half of it, reduce it in
+    // Algorithm-2 order (collective.cpp:67-74) straight from the peers' send slots
+    // and push the result into every rank's result slot over NVLink -- while the
+    // tensor cores of the same SM already work on the next items.
+    ar_reduce_owned(p, pair, npairs, pid, rank);
   }
   } else {
     // ---------------- merge warps (the TBIK reduction), both CTAs ----------------
@@ -660,8 +781,20 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           }
         }
       }
+      if constexpr (AR) {
+        // fused all-reduce: the previous item's stores have completed once only this
+        // item's NCH store groups may still be pending; publish it to its owner
+        if (lane == 0) bulk_wait_complete<NCH>();
+        named_bar(1, 32 * EPI);
+        if (warp == 4 && lane == 0 && item >= pair + npairs) ar_publish(p, item - npairs, rank);
+      }
     }
     if (p.tma_store && lane == 0) bulk_wait_all();
+    if constexpr (AR) {
+      named_bar(1, 32 * EPI);
+      if (warp == 4 && lane == 0 && pair < p.items)  // this pair's last item
+        ar_publish(p, pair + (p.items - 1 - pair) / npairs * npairs, rank);
+    }
   }
 
   tc_fence_before();
@@ -727,6 +860,7 @@ tbik_status make_map_out(CUtensorMap* map, float* base, uint64_t n, uint64_t m, 
 }
 
 thread_local int g_sm_cap = 0;  // set_tc_sm_cap: leave SMs free for a concurrent kernel
+thread_local FusedAr* g_fused_ar = nullptr;  // set_tc_fused_ar
 
 int sm_count() {
   static int n[16] = {0};
@@ -745,6 +879,12 @@ int sm_count() {
 tbik_status tc_make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                            uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
   return make_map_2d(map, base, inner, outer, row_stride_bytes, box_inner, box_outer);
+}
+
+FusedAr* set_tc_fused_ar(FusedAr* ctx) {
+  FusedAr* old = g_fused_ar;
+  g_fused_ar = ctx;
+  return old;
 }
 
 int set_tc_sm_cap(int cap) {
@@ -910,6 +1050,25 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   if (p.tma_store)
     TBIK_TRY(make_map_out(&mC, o.out, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.M),
                           static_cast<uint64_t>(p.units), static_cast<uint64_t>(o.ldo) * 4, ustride * 4));
+  // Fused GEMM -> tree all-reduce (tbik_group.cu) for FULL pair-tile launches whose
+  // output is the group's send slot.
+  if (FusedAr* ar = g_fused_ar) {
+    const bool ok = pair && !mc && abox == 128 && o.mode == OUT_FULL && !o.act && p.tma_store && o.ldo == v.N && ar->W > 1 &&
+                    ar->W <= 8 && p.items * 2 * ar->W <= ar->flag_capacity && o.out == ar->src[ar->rank];
+    if (ok) {
+      p.ar_W = ar->W;
+      p.ar_rank = ar->rank;
+      p.ar_epoch = ar->epoch;
+      for (int r = 0; r < 8; ++r) {
+        p.ar_src[r] = ar->src[r];
+        p.ar_dst[r] = ar->dst[r];
+        p.ar_flags[r] = ar->flags[r];
+        p.ar_done[r] = ar->done[r];
+      }
+      p.ar_counter = ar->counter;
+      ar->used = true;
+    }
+  }
   using Kern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
 #define TBIK_TC_K(D, P)                                                                                  \
   {{tc_tree_gemm_kernel<8, false, 32, P, D>, tc_tree_gemm_kernel<8, true, 32, P, D>},                   \
@@ -924,8 +1083,13 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   const bool epi16 = [] {
     const char* e = std::getenv("TBIK_TC_EPI");
     return e && std::atoi(e) == 16;
-  }() && pair && abox == 128 && !deep && !mc;
-  const Kern kern = mc ? (kf1 ? tc_tree_gemm_kernel<8, true, 128, true, false, true>
+  }() && pair && abox == 128 && !deep && !mc && p.ar_W <= 1;
+  const bool ar_on = p.ar_W > 1;
+  const Kern kern = ar_on ? (deep ? (kf1 ? tc_tree_gemm_kernel<8, true, 128, true, true, false, true>
+                                         : tc_tree_gemm_kernel<8, false, 128, true, true, false, true>)
+                                  : (kf1 ? tc_tree_gemm_kernel<8, true, 128, true, false, false, true>
+                                         : tc_tree_gemm_kernel<8, false, 128, true, false, false, true>))
+                   : mc ? (kf1 ? tc_tree_gemm_kernel<8, true, 128, true, false, true>
                               : tc_tree_gemm_kernel<8, false, 128, true, false, true>)
                    : epi16 ? (kf1 ? tc_tree_gemm_kernel<16, true, 128, true, false, false>
                                   : tc_tree_gemm_kernel<16, false, 128, true, false, false>)
@@ -933,13 +1097,13 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   const int epi = epi16 ? 16 : 8;
   const int nthreads = 128 + 32 * epi;
   const size_t smem = smem_bytes(epi, abox, pair, deep);
-  static bool attr_set[16][2][3][2][2][2][2] = {};
+  static bool attr_set[16][2][3][2][2][2][2][2] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 16 && !attr_set[dev][pair][ai][kf1][deep][mc][epi16]) {
+  if (dev >= 0 && dev < 16 && !attr_set[dev][pair][ai][kf1][deep][mc][epi16][ar_on]) {
     TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     if (pair) TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-    attr_set[dev][pair][ai][kf1][deep][mc][epi16] = true;
+    attr_set[dev][pair][ai][kf1][deep][mc][epi16][ar_on] = true;
   }
   cudaLaunchConfig_t lc{};
   lc.gridDim = grid;

@@ -45,6 +45,7 @@ struct tbik_group {
   char* peer_region[tbik_b200::kMaxRanks] = {};
   bool opened[tbik_b200::kMaxRanks] = {};
   uint32_t epoch = 0;
+  int64_t fused = 0;  // row-parallel forwards that took the fused GEMM + all-reduce kernel
   // GEMM / all-reduce overlap (tbik_group_row_parallel_forward): a side stream for
   // the collectives and its events, created on first use.
   cudaStream_t side = nullptr;
@@ -75,6 +76,13 @@ uint32_t* ready_flags(char* region, int64_t capacity) {
 }
 uint32_t* done_flags(char* region, int64_t capacity) { return ready_flags(region, capacity) + 64; }
 uint32_t* cta_counter(char* region, int64_t capacity) { return ready_flags(region, capacity) + 128; }
+uint32_t* fused_counter(char* region, int64_t capacity) { return ready_flags(region, capacity) + 129; }
+// Tile flags of the fused GEMM -> all-reduce, after the control block:
+// [item][cta of the pair][source rank] u32 (an item is a 256 x 128 output tile).
+int64_t tile_flag_words(int64_t capacity, int W) { return 2 * int64_t(W) * (capacity / (256 * 128) + 1024); }
+uint32_t* tile_flags(char* region, int64_t capacity) {
+  return reinterpret_cast<uint32_t*>(region + flags_offset(capacity) + 1024);
+}
 float* result_ptr(char* region, int64_t capacity, uint32_t epoch) {
   return reinterpret_cast<float*>(region) + static_cast<size_t>(2 + (epoch & 1u)) * capacity;
 }
@@ -231,13 +239,13 @@ tbik_status tbik_group_create(int world_size, int rank, int device, int64_t capa
   g->rank = rank;
   g->device = device;
   g->capacity = capacity_elems;
-  g->region_bytes = flags_offset(capacity_elems) + kCtlBytes;
+  g->region_bytes = flags_offset(capacity_elems) + kCtlBytes + tile_flag_words(capacity_elems, world_size) * 4;
   cudaError_t e = cudaMalloc(&g->region, g->region_bytes);
   if (e != cudaSuccess) {
     delete g;
     return cuda_status(e, "cudaMalloc(group region)");
   }
-  e = cudaMemset(g->region + flags_offset(capacity_elems), 0, kCtlBytes);
+  e = cudaMemset(g->region + flags_offset(capacity_elems), 0, g->region_bytes - flags_offset(capacity_elems));
   if (e != cudaSuccess) {
     cudaFree(g->region);
     delete g;
@@ -300,6 +308,7 @@ tbik_status tbik_group_destroy(tbik_group* g) {
 
 int tbik_group_world_size(const tbik_group* g) { return g ? g->W : 0; }
 int tbik_group_rank(const tbik_group* g) { return g ? g->rank : -1; }
+int64_t tbik_group_fused_count(const tbik_group* g) { return g ? g->fused : 0; }
 
 float* tbik_group_send_buffer(tbik_group* g) {
   if (!g) return nullptr;
@@ -379,6 +388,54 @@ tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* X_shard, 
   local.k_first = gp.k_first;  // layers.cpp:85-88
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t xsz = x_dtype == TBIK_BF16 ? 2 : 4;
+
+  // Fused GEMM -> all-reduce (one kernel, tile by tile; TBIK_GROUP_FUSED=0 disables):
+  // the tcgen05 GEMM writes its partial into this epoch's peer-visible send slot,
+  // publishes every finished 256 x 128 tile to the tile's owner rank (item % W), and
+  // warps 2-3 of every CTA reduce the tiles this rank owns in Algorithm-2 order
+  // straight from the peers' slots and push the result into every rank's result
+  // slot -- the NVLink traffic overlaps the tensor-core work of the same kernel.  A
+  // short wait kernel then copies the result slot to Y once all W ranks are done.
+  // Taken when the GEMM is one FULL pair-tile launch (M > 128, >= 7/8 of the CTA
+  // pairs busy); otherwise the partial already sits in the send slot and the
+  // regular tree all-reduce runs.  The choice depends only on (M, N, K / W), i.e.
+  // it is the same on every rank.
+  static const bool fused_on = [] {
+    const char* e = std::getenv("TBIK_GROUP_FUSED");
+    return !(e && *e && std::atoi(e) == 0);
+  }();
+  if (fused_on && g->W > 1 && leaf_mode == TBIK_LEAF_TCGEN05) {
+    for (int r = 0; r < g->W; ++r)
+      if (!g->peer_region[r]) return set_error(TBIK_COLLECTIVE_MISMATCH, "peers not opened");
+    const uint32_t epoch = g->epoch + 1;
+    FusedAr ar;
+    ar.W = g->W;
+    ar.rank = g->rank;
+    ar.epoch = epoch;
+    for (int r = 0; r < g->W; ++r) {
+      ar.src[r] = slot_ptr(g->peer_region[r], g->capacity, epoch);
+      ar.dst[r] = result_ptr(g->peer_region[r], g->capacity, epoch);
+      ar.flags[r] = tile_flags(g->peer_region[r], g->capacity);
+      ar.done[r] = done_flags(g->peer_region[r], g->capacity);
+    }
+    ar.counter = fused_counter(g->region, g->capacity);
+    ar.flag_capacity = tile_flag_words(g->capacity, g->W);
+    float* send = slot_ptr(g->region, g->capacity, epoch);
+    FusedAr* prev = set_tc_fused_ar(&ar);
+    const tbik_status st =
+        tbik_tree_matmul(X_shard, x_dtype, ldx, W_shard, w_dtype, ldw, send, N, M, N, Kr, &local, leaf_mode, stream);
+    set_tc_fused_ar(prev);
+    TBIK_TRY(st);
+    if (!ar.used) return group_all_reduce(g, send, Y, M * N, s, 0);
+    g->epoch = epoch;
+    ++g->fused;
+    int64_t cblocks = std::max<int64_t>(1, std::min<int64_t>((M * N / 4 + 255) / 256, 148 * 4));
+    group_gather_wait_copy_kernel<<<static_cast<unsigned>(cblocks), 256, 0, s>>>(
+        done_flags(g->region, g->capacity), g->W, epoch, result_ptr(g->region, g->capacity, epoch), Y, M * N);
+    TBIK_CUDA(cudaGetLastError());
+    count_launch();
+    return TBIK_OK;
+  }
 
   // Overlap (GEMM -> all-reduce): rows in chunks; the GEMM of
   // chunk c+1 runs on all but kReserve SMs while the tree all-reduce of chunk c

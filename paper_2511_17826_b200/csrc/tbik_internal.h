@@ -60,6 +60,23 @@ int64_t tc_tiles(const GemmView& v);
 // all-reduce kernel (tbik_group.cu).
 int set_tc_sm_cap(int cap);
 int64_t tc_parallel_slots(const GemmView& v);
+
+// Fused GEMM -> tree all-reduce (tbik_group.cu): while set on this host thread, a
+// FULL-mode pair-tile launch_tc_gemm writes its partial into the group's send slot
+// AND reduces the tiles this rank owns inside the same kernel (see
+// tbik_gemm_tc.cu); `used` reports whether the launch took the fused path.
+struct FusedAr {
+  int W = 0, rank = 0;
+  uint32_t epoch = 0;
+  const float* src[8] = {};  // send slot of every rank (peer-mapped)
+  float* dst[8] = {};        // result slot of every rank (peer-mapped)
+  uint32_t* flags[8] = {};   // tile-flag array of every rank: [item][cta][W] u32
+  uint32_t* done[8] = {};    // done[] of every rank
+  uint32_t* counter = nullptr;
+  int64_t flag_capacity = 0; // u32 words per tile-flag array
+  bool used = false;
+};
+FusedAr* set_tc_fused_ar(FusedAr* ctx);
 // The 256 x 256 pair-tile variant (tbik_gemm_tc_wide.cu).
 tbik_status launch_tc_gemm_wide(const GemmView& v, const GemmOut& o, cudaStream_t s);
 int64_t tc_wide_pair_tiles(const GemmView& v);

@@ -67,6 +67,18 @@ def main():
         yo = grp.row_parallel_forward(xo[:, kb:ke].contiguous(), wo[kb:ke].contiguous(), K, cfg, 8, tb.LEAF_TCGEN05)
         torch.cuda.synchronize()
         assert torch.equal(yo.view(torch.int32), yo_ref.view(torch.int32)), f"overlapped forward differs ({it})"
+    # ragged rows (M % 256 != 0): the fused GEMM -> all-reduce tile flags / halves
+    xr = xo[:1000].contiguous()
+    yr_ref = tb.tree_matmul(xr, wo, cfg, tb.LEAF_TCGEN05)
+    for it in range(2):
+        yr = grp.row_parallel_forward(xr[:, kb:ke].contiguous(), wo[kb:ke].contiguous(), K, cfg, 8, tb.LEAF_TCGEN05)
+        torch.cuda.synchronize()
+        assert torch.equal(yr.view(torch.int32), yr_ref.view(torch.int32)), f"ragged forward differs ({it})"
+    fused = grp.fused_count()
+    if os.environ.get("TBIK_GROUP_FUSED", "1") != "0":
+        assert fused == 5, f"fused GEMM + all-reduce kernel ran {fused} times, expected 5"
+    else:
+        assert fused == 0
     # host-buffer pipeline through the group: chunked epochs, same bits as the device call
     xh = x[:, kb:ke].contiguous().cpu().pin_memory()
     yh = grp.row_parallel_forward_hostio(xh, ws, K, cfg, 8, tb.LEAF_TCGEN05, chunk_rows=24)

@@ -79,16 +79,21 @@ def _free_port() -> int:
     return p
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_peer_group_processes(tb, cuda, tmp_path, world):
+def test_peer_group_processes(tb, cuda, tmp_path, world, fused):
     """`world` ranks (processes sharing this GPU) run the IPC group end to end:
     row-parallel down_proj shards -> peer-visible buffers -> flag barriers -> tree
-    all-reduce (one-shot and two-phase), the overlapped chunk pipeline and the
+    all-reduce (one-shot and two-phase), the fused one-kernel GEMM + all-reduce or
+    the overlapped chunk pipeline, and the
     host-buffer path.  Every rank must produce bit-identical outputs equal to the
     single-process TP=1 result."""
     worker = os.path.join(ROOT, "tests", "peer_group_worker.py")
     port = _free_port()
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world))
+    # fused=1: large row-parallel outputs take the one-kernel GEMM + tile-flag tree
+    # all-reduce (tbik_gemm_tc.cu AR variant); fused=0: the chunked two-stream overlap
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world),
+               TBIK_GROUP_FUSED=fused)
     procs = []
     for r in range(world):
         e = dict(env, RANK=str(r), LOCAL_RANK="0", TBIK_TEST_OUT=str(tmp_path / f"rank{r}.npy"))

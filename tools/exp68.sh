@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_collective.py -q -x -k peer_group_processes > gpurun_out/e68_pytest.txt 2>&1; echo "rc=$?" >> gpurun_out/e68_pytest.txt
+timeout 300 python bench.py --steps 10 --warmup 3 > gpurun_out/e68_bench.txt 2>&1; echo "rc=$?" >> gpurun_out/e68_bench.txt
