@@ -19,9 +19,10 @@
 //   warp 2      TMEM allocator (512 columns, cta_group::2)
 //   warps 4-11  merge warps: warp w may read TMEM lanes 32(w%4)..; thread (w, lane)
 //               owns output row 32(w%4) + lane, columns 64((w-4)/4) + [0, 64).
-//               For every leaf: both tcgen05.ld chunks in flight (with the
-//               level-1 slot when k_first == 1), one wait, the accumulator is
-//               released, then __fadd_rn verbatim the reference's reduction:
+//               For every leaf: both tcgen05.ld chunks in flight, one wait, the
+//               accumulator is released, then __fadd_rn verbatim the reference's
+//               reduction (k_first == 1: tree level 1 is formed in registers --
+//               an even group waits there for its odd sibling):
 //                 level 0   g = ((0 + P_0) + P_1) + ... + P_{kf-1}   (matmul.cpp:100-125)
 //                 levels>=1 binary counter over group values (matmul.cpp:107-123)
 //               g in 64 registers; tree levels 1-2 in TMEM cols [256,512),
@@ -373,8 +374,9 @@ __device__ __forceinline__ void ar_reduce_owned(const TcParams& p, long long pai
 
 // EPI merge warps (two per TMEM lane quarter, splitting the 128 columns), ABOX
 // A rows staged per stage (128, or 64 / 32 for small M; stage count follows).  KF1 (used when k_first == 1, where every leaf completes a
-// group and g need not persist across leaves): the level-1 slot is loaded in the
-// same batch as the leaf, so an odd leaf costs one TMEM round trip, not two.
+// group): tree level 1 never touches TMEM -- an even group stays in registers
+// and the odd sibling merges into it, so a pair of leaves costs two accumulator
+// drains instead of two drains + a level-1 store + load.
 // AR: the fused tree all-reduce variant (pair tiles, FULL mode; tbik_group.cu).
 template <int EPI, bool KF1, int ABOX, bool PAIR, bool DEEP, bool MC = false, bool AR = false>
 __global__ void __launch_bounds__(128 + 32 * EPI, 1)
@@ -588,24 +590,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         uint32_t r[NCH < 2 ? 2 : NCH][32];
         const bool odd = KF1 && p.levels >= 1 && (groups_done & 1u);
         if (!(p.debug & 1)) {
-          if (odd) {
-            // leaf chunk + level-1 slot chunk per round trip: g = (0 + P) + S1
 #pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-              tmem_ld32r(acc + c * 32, r[0]);
-              tmem_ld32r(lane_base + SLOT_LVL1 + c * 32, r[1]);
-              tmem_wait_ld_dep(r[0]);
-              tmem_wait_ld_dep(r[1]);
+          for (int c = 0; c < NCH; ++c) tmem_ld32r(acc + c * 32, r[c]);
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                g[c * 32 + i] = __fadd_rn(__fadd_rn(0.0f, __uint_as_float(r[0][i])), __uint_as_float(r[1][i]));
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) tmem_ld32r(acc + c * 32, r[c]);
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) tmem_wait_ld_dep(r[c]);
-          }
+          for (int c = 0; c < NCH; ++c) tmem_wait_ld_dep(r[c]);
         }
         tc_fence_before();
         __syncwarp();
@@ -628,7 +616,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         // level 0: g = ((0 + P_0) + P_1) + ... + P_{kf-1}   (matmul.cpp:100-125; 0 + P
         // canonicalises a -0 leaf like matmul.cpp:101-103)
         if (odd) {
-          // g already holds (0 + P) + S1
+          // level 1 in registers: g holds the previous group S1 (kept since the even
+          // leaf); the new group (0 + P) merges with it, new + old (matmul.cpp:107-123)
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              g[c * 32 + i] = __fadd_rn(__fadd_rn(0.0f, __uint_as_float(r[c][i])), g[c * 32 + i]);
         } else if (KF1 || t_in_group == 0) {  // KF1 <=> k_first == 1: every leaf starts a group
 #pragma unroll
           for (int c = 0; c < NCH; ++c)
@@ -647,6 +641,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         // Binary counter over completed groups (levels 1..p.levels, matmul.cpp:107-123):
         // levels 1-2 in TMEM columns [256, 512), deeper levels (touched once per 8+
         // groups) in L2-resident scratch.
+        if (KF1 && p.levels >= 1 && !odd) {  // even group: stays in registers as level 1
+          ++groups_done;
+          continue;
+        }
         if (p.levels >= 1) {
           int level = 1;
           uint32_t c_bits = groups_done++;
@@ -1030,7 +1028,10 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   // M=2048 even; profiles/r01_tc_deep_midm.txt).  With 3+ levels and many waves
   // the on-chip level 3 measured faster (1146 vs 1108 TFLOP/s at the bench shape).
   // TBIK_TC_DEEP=0/1 forces it (a pure scheduling knob -- same bits).
-  bool deep = p.levels <= 2 || p.items <= 2 * slots;
+  // ... but not with 4+ levels (k_first = 1, K = 4096: 16 groups per item), where two
+  // scratch levels cost more than the extra stages buy (tools/midm_sweep.py: o_proj
+  // K=4096 N=4096 M=512..1024 +8-11 % without DEEP, down_proj K=14336 unchanged).
+  bool deep = p.levels <= 2 || (p.items <= 2 * slots && p.levels <= 3);
   if (const char* e = std::getenv("TBIK_TC_DEEP"))
     if (*e) deep = std::atoi(e) != 0;
   if (mc) deep = false;
