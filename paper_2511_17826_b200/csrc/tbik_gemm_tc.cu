@@ -558,7 +558,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     // TMEM holds tree levels 1-2, shared memory level 3 (this warp's sL3 region);
     // levels >= 4 live in scratch as [col/4][row][4] slabs (a warp's float4
     // access is 512 contiguous bytes).
-    constexpr int FS = DEEP ? 3 : 4;  // first scratch level
+    // k_first == 1 keeps level 1 in registers, so its TMEM columns hold level 3
+    // (off the shared-memory port the MMA operand reads saturate); scratch from 4.
+    constexpr int FS = KF1 ? 4 : DEEP ? 3 : 4;  // first scratch level
     float* scratch_base =
         p.levels >= FS
             ? p.scratch + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - FS + 1) * (BM * BN) +
@@ -653,8 +655,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             level = 2;
           }
           while (c_bits & 1u) {
-            if (level <= 2) {
-              const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
+            if (KF1 ? (level == 2 || level == 3) : level <= 2) {
+              const uint32_t slot = lane_base + (level == 2 ? SLOT_LVL2 : SLOT_LVL1);
 #pragma unroll
               for (int c = 0; c < NCH; ++c) tmem_ld32r(slot + c * 32, r[c]);
 #pragma unroll
@@ -663,7 +665,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               for (int c = 0; c < NCH; ++c)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], __uint_as_float(r[c][i]));
-            } else if (!DEEP && level == 3) {
+            } else if (!KF1 && !DEEP && level == 3) {
 #pragma unroll
               for (int i = 0; i < COLS; i += 4) {
                 const float4 x = *reinterpret_cast<const float4*>(l3 + ((i / 4) * 32 + lane) * 16);
@@ -688,8 +690,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             ++level;
           }
           if (level <= p.levels) {
-            if (level <= 2) {
-              const uint32_t slot = lane_base + (level == 1 ? SLOT_LVL1 : SLOT_LVL2);
+            if (KF1 ? (level == 2 || level == 3) : level <= 2) {
+              const uint32_t slot = lane_base + (level == 2 ? SLOT_LVL2 : SLOT_LVL1);
 #pragma unroll
               for (int c = 0; c < NCH; ++c) {
                 float v[32];
@@ -698,7 +700,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                 tmem_st32(slot + c * 32, v);
               }
               tmem_wait_st();
-            } else if (!DEEP && level == 3) {
+            } else if (!KF1 && !DEEP && level == 3) {
               if (lane == 0) bulk_wait_read<0>();  // earlier output boxes staged here
               __syncwarp();
 #pragma unroll
@@ -1031,11 +1033,11 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   // ... but not with 4+ levels (k_first = 1, K = 4096: 16 groups per item), where two
   // scratch levels cost more than the extra stages buy (tools/midm_sweep.py: o_proj
   // K=4096 N=4096 M=512..1024 +8-11 % without DEEP, down_proj K=14336 unchanged).
-  bool deep = p.levels <= 2 || (p.items <= 2 * slots && p.levels <= 3);
+  bool deep = p.levels <= 2 || (p.items <= 2 * slots && p.levels <= 3) || (kf1 && p.levels <= 4);
   if (const char* e = std::getenv("TBIK_TC_DEEP"))
     if (*e) deep = std::atoi(e) != 0;
   if (mc) deep = false;
-  const int first_scratch = deep ? 3 : 4;
+  const int first_scratch = kf1 ? 4 : deep ? 3 : 4;
   if (p.levels >= first_scratch) {
     const size_t n = static_cast<size_t>(grid.x) * (p.levels - first_scratch + 1) * BM * BN;
     p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1));
