@@ -29,8 +29,10 @@
 //               level 3 in an 8 KB shared-memory region per warp (also the
 //               output staging), deeper levels (touched once per 16+ groups) in
 //               L2-resident scratch ([col/4][row][4] slabs, 512 B per warp
-//               access).  Results leave through 128B-swizzled 32 x 32 smem boxes
-//               and TMA stores.
+//               access).  k_first == 1 shifts this up by one: level 1 in
+//               registers, 2-3 in TMEM, 4 in shared memory, 5+ in scratch.
+//               Results leave through 128B-swizzled 32 x 32 smem boxes and TMA
+//               stores.
 //   Measured (profiles/r01_tc_merge_ablation*.txt): an L2 round trip for a
 //   scratch level stalls the merge for longer than the accumulator double
 //   buffer can absorb (-20 % at k_first = 1), hence level 3 on chip at the
@@ -560,7 +562,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     // access is 512 contiguous bytes).
     // k_first == 1 keeps level 1 in registers, so its TMEM columns hold level 3
     // (off the shared-memory port the MMA operand reads saturate); scratch from 4.
-    constexpr int FS = KF1 ? 4 : DEEP ? 3 : 4;  // first scratch level
+    // ... and shared memory (when not DEEP) holds level 4.
+    constexpr int SL = KF1 ? 4 : 3;                        // the shared-memory level
+    constexpr int FS = DEEP ? SL : SL + 1;                 // first scratch level
     float* scratch_base =
         p.levels >= FS
             ? p.scratch + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - FS + 1) * (BM * BN) +
@@ -665,7 +669,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               for (int c = 0; c < NCH; ++c)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], __uint_as_float(r[c][i]));
-            } else if (!KF1 && !DEEP && level == 3) {
+            } else if (!DEEP && level == SL) {
 #pragma unroll
               for (int i = 0; i < COLS; i += 4) {
                 const float4 x = *reinterpret_cast<const float4*>(l3 + ((i / 4) * 32 + lane) * 16);
@@ -700,7 +704,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                 tmem_st32(slot + c * 32, v);
               }
               tmem_wait_st();
-            } else if (!KF1 && !DEEP && level == 3) {
+            } else if (!DEEP && level == SL) {
               if (lane == 0) bulk_wait_read<0>();  // earlier output boxes staged here
               __syncwarp();
 #pragma unroll
@@ -1033,11 +1037,13 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   // ... but not with 4+ levels (k_first = 1, K = 4096: 16 groups per item), where two
   // scratch levels cost more than the extra stages buy (tools/midm_sweep.py: o_proj
   // K=4096 N=4096 M=512..1024 +8-11 % without DEEP, down_proj K=14336 unchanged).
-  bool deep = p.levels <= 2 || (p.items <= 2 * slots && p.levels <= 3) || (kf1 && p.levels <= 4);
+  // k_first == 1 keeps levels 1-3 off shared memory, so DEEP is free up to 3 levels
+  // there and the shared-memory level 4 beats scratch above.
+  bool deep = kf1 ? p.levels <= 3 : p.levels <= 2 || (p.items <= 2 * slots && p.levels <= 3);
   if (const char* e = std::getenv("TBIK_TC_DEEP"))
     if (*e) deep = std::atoi(e) != 0;
   if (mc) deep = false;
-  const int first_scratch = kf1 ? 4 : deep ? 3 : 4;
+  const int first_scratch = (kf1 ? 4 : 3) + (deep ? 0 : 1);
   if (p.levels >= first_scratch) {
     const size_t n = static_cast<size_t>(grid.x) * (p.levels - first_scratch + 1) * BM * BN;
     p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1));
