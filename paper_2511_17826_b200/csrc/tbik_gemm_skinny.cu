@@ -66,7 +66,7 @@ constexpr int sk_merge_warps() { return 4 * (MT / sk_tpw<MT>()); }
 template <int MT>
 constexpr int sk_threads() { return 128 + 32 * sk_merge_warps<MT>(); }
 template <int MT>
-constexpr int sk_nacc() { return MT >= 64 ? 2 : 4; }
+constexpr int sk_nacc() { return MT >= 128 ? 2 : 4; }
 template <int MT>
 constexpr int sk_stages() { return (SK_SMEM_LIMIT - 2048) / (SK_W_STAGE + MT * 128); }
 template <int MT>
@@ -133,10 +133,11 @@ __device__ __forceinline__ uint32_t dsmem_map(uint32_t smem_addr, uint32_t rank)
 }
 __device__ __forceinline__ float4 dsmem_ld_f32x4(uint32_t addr) {
   float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(addr)
-               : "memory");
+  // not volatile: the data is published by the cluster barrier (which carries the
+  // memory clobber), so the loads of several items may be scheduled together
+  asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "r"(addr));
   return v;
 }
 
@@ -357,10 +358,11 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
   //   result  = contiguous-halves tree over the groups (binary counter, new + old)
   // -- the order of tree_combine_kernel (tbik_tree.cu) and of the reference.
   cluster_sync_all();
-  if (p.units > 1 && warp >= 4) {
+  if (p.units > 1) {
     // work items: (row, 4-column quad) of this CTA's row slice, 16-byte DSMEM loads
-    // from every unit, two items in flight per thread
-    const int tid = threadIdx.x - 128;
+    // from every unit, spread over all warps (their roles are done), two items in
+    // flight per thread
+    const int tid = threadIdx.x;
     const int unit = static_cast<int>(blockIdx.x % p.units);
     const int n0 = static_cast<int>(blockIdx.x / p.units) * SK_BN;
     const int R = (p.M + p.units - 1) / p.units;
@@ -371,7 +373,7 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
 #pragma unroll
     for (int x = 0; x < SK_MAX_UNITS; ++x) peer[x] = x < p.units ? dsmem_map(fb, static_cast<uint32_t>(x)) : 0u;
 #pragma unroll 2
-    for (int idx = tid; idx < nitems; idx += 32 * NMW) {
+    for (int idx = tid; idx < nitems; idx += static_cast<int>(blockDim.x)) {
       const int m = m_lo + idx / (SK_BN / 4);
       const int c4 = (idx % (SK_BN / 4)) * 4;
       const uint32_t off = static_cast<uint32_t>((m * SK_BN + c4) * 4);
@@ -451,7 +453,9 @@ bool tc_use_skinny(const GemmView& v) {
 
 tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaStream_t s) {
   GemmView v = v_in;
-  const int mt = v.M <= 16 ? 16 : v.M <= 32 ? 32 : v.M <= 64 ? 64 : 128;
+  int mt = v.M <= 16 ? 16 : v.M <= 32 ? 32 : v.M <= 64 ? 64 : 128;
+  const int force_mt = env_int("TBIK_SK_MT", 0);  // tuning knob: a wider token tile (same bits)
+  if ((force_mt == 32 || force_mt == 64 || force_mt == 128) && force_mt >= mt) mt = force_mt;
   int dev = 0;
   cudaGetDevice(&dev);
   int sms = 148;
