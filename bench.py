@@ -487,6 +487,10 @@ def run_tbik(args):
             "roofline": roof, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "noninvariant": noninv, "tp_invariance_bit_identical": tp_ok, "sweep": sweep,
             "tp_shard_gemm": tp_shards,
+            "collective": None if group is None else {
+                "path": "fused: one tcgen05 kernel = GEMM + tile-flag tree all-reduce over peer memory"
+                        if group.fused_count() > 0 else "GEMM, then tree all-reduce kernels",
+                "fused_calls": group.fused_count()},
             "cpu_baseline": cpu,
             "forward": forward,
             "rowops_c5": rowops,
