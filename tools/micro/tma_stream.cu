@@ -30,12 +30,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
                ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(pol) : "memory");
 }
 
-struct P { int K, N, strip_boxes, units, box_rows, stages, hint; };
+struct P { int K, N, strip_boxes, units, box_rows, stages, hint, xrows; };
 
-__global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ CUtensorMap tm, const P p) {
+__global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tx, const P p) {
   extern __shared__ uint8_t raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-  const int stage_bytes = p.strip_boxes * p.box_rows * 128;
+  const int stage_bytes = p.strip_boxes * p.box_rows * 128 + p.xrows * 128;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + p.stages * stage_bytes);
   uint64_t* empty = full + p.stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
       mbar_arrive_expect_tx(&full[st], stage_bytes);
       for (int b = 0; b < p.strip_boxes; ++b)
         tma_load_2d(sm + st * stage_bytes + b * p.box_rows * 128, &tm, &full[st], (strip * p.strip_boxes + b) * 64, k0 + i * p.box_rows, pol);
+      if (p.xrows) tma_load_2d(sm + st * stage_bytes + p.strip_boxes * p.box_rows * 128, &tx, &full[st], k0 + i * p.box_rows, 0, pol);
       if (++st == p.stages) { st = 0; ph ^= 1; }
     }
   } else if (warp == 1 && lane == 0) {
@@ -85,17 +86,22 @@ int main() {
   CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
   EncFn enc = reinterpret_cast<EncFn>(fn);
   CK(cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 230000));
-  struct V { int strip_boxes, units, box_rows, stages, hint, promo; };
+  struct V { int strip_boxes, units, box_rows, stages, hint, promo, xrows; };
   std::vector<V> vs = {
-      {2, 4, 64, 11, 0, 2}, {2, 4, 64, 11, 1, 2}, {2, 4, 64, 11, 0, 0}, {2, 4, 64, 11, 0, 1},
-      {2, 4, 64, 6, 0, 2}, {2, 4, 128, 6, 0, 2}, {2, 4, 32, 22, 0, 2}, {2, 4, 32, 12, 0, 2},
-      {2, 2, 64, 11, 0, 2}, {2, 8, 64, 11, 0, 2}, {1, 2, 64, 24, 0, 2}, {1, 4, 64, 24, 0, 2},
-      {4, 2, 64, 6, 0, 2}, {4, 4, 64, 6, 0, 2}, {4, 4, 32, 12, 0, 2}, {8, 4, 32, 6, 0, 2},
-      {8, 8, 32, 6, 0, 2}, {64, 128, 8, 3, 0, 2}, {64, 128, 4, 6, 0, 2}, {16, 32, 16, 6, 0, 2},
+      {2, 4, 64, 11, 0, 2, 0}, {2, 4, 64, 11, 0, 2, 16}, {2, 4, 64, 9, 0, 2, 64}, {2, 4, 64, 7, 0, 2, 128},
+      {2, 4, 64, 7, 0, 2, 0}, {2, 4, 64, 4, 0, 2, 0}, {2, 4, 64, 7, 1, 2, 128},
   };
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  void* xbuf; CK(cudaMalloc(&xbuf, size_t(128) * K * 2)); CK(cudaMemset(xbuf, 0, size_t(128) * K * 2));
   for (const V& v : vs) {
     std::vector<CUtensorMap> maps(4);
+    CUtensorMap xm;
+    if (v.xrows) {
+      cuuint64_t dims[2] = {cuuint64_t(K), 128}; cuuint64_t str[1] = {cuuint64_t(K) * 2};
+      cuuint32_t box[2] = {64, cuuint32_t(v.xrows)}; cuuint32_t es[2] = {1, 1};
+      if (enc(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xbuf, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) return 1;
+    } else xm = maps[0];
     for (int i = 0; i < 4; ++i) {
       cuuint64_t dims[2] = {cuuint64_t(N), cuuint64_t(K)}; cuuint64_t str[1] = {cuuint64_t(N) * 2};
       cuuint32_t box[2] = {64, cuuint32_t(v.box_rows)}; cuuint32_t es[2] = {1, 1};
@@ -104,22 +110,23 @@ int main() {
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) { printf("encode failed %d\n", r); return 1; }
     }
-    P p{K, N, v.strip_boxes, v.units, v.box_rows, v.stages, v.hint};
+    P p{K, N, v.strip_boxes, v.units, v.box_rows, v.stages, v.hint, v.xrows};
+    if (!v.xrows) xm = maps[0];
     const int strips = N / (64 * v.strip_boxes);
     const int grid = strips * v.units;
-    const size_t smem = 1024 + size_t(v.stages) * v.strip_boxes * v.box_rows * 128 + 1024;
+    const size_t smem = 1024 + size_t(v.stages) * (v.strip_boxes * v.box_rows * 128 + v.xrows * 128) + 1024;
     if (smem > 230000) { printf("skip smem\n"); continue; }
-    for (int i = 0; i < 4; ++i) stream_kernel<<<grid, 64, smem>>>(maps[i], p);
+    for (int i = 0; i < 4; ++i) stream_kernel<<<grid, 64, smem>>>(maps[i], xm, p);
     CK(cudaDeviceSynchronize());
     const int reps = 40;
     cudaEventRecord(e0);
-    for (int i = 0; i < reps; ++i) stream_kernel<<<grid, 64, smem>>>(maps[i % 4], p);
+    for (int i = 0; i < reps; ++i) stream_kernel<<<grid, 64, smem>>>(maps[i % 4], xm, p);
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     const double us = ms * 1e3 / reps;
-    printf("strip %4d cols  units %3d  grid %4d  box_rows %3d  stages %2d  stage %6d B  hint %d promo %d : %6.1f us  %6.0f GB/s\n",
-           v.strip_boxes * 64, v.units, grid, v.box_rows, v.stages, v.strip_boxes * v.box_rows * 128, v.hint, v.promo, us, bytes / us / 1e3);
+    printf("strip %4d cols  units %3d  grid %4d  box_rows %3d  stages %2d  stage %6d B  hint %d promo %d xrows %3d : %6.1f us  %6.0f GB/s\n",
+           v.strip_boxes * 64, v.units, grid, v.box_rows, v.stages, v.strip_boxes * v.box_rows * 128, v.hint, v.promo, v.xrows, us, bytes / us / 1e3);
   }
   return 0;
 }
