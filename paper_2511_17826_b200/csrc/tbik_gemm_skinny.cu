@@ -33,6 +33,7 @@
 //   warp 2  TMEM allocator (512 columns: accumulators + tree levels 1..levels)
 //   warps 4-7 merge warps: thread (q, lane) owns weight column n0 + 32q + lane
 //             for all MT tokens (TMEM lane quarter q).
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -49,7 +50,7 @@ tbik_status tc_make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, u
 
 namespace {
 
-constexpr int SK_BN = 128;                  // weight columns per tile = MMA M = TMEM lanes
+constexpr int SK_BN = 128;                  // weight columns per tile (BNW = 128: MMA M = 128)
 constexpr int SK_KSTAGE = 64;               // K per pipeline stage
 constexpr int SK_W_ATOM = 64 * SK_KSTAGE * 2;  // one 64-column SW128 atom: 8 KB
 constexpr int SK_W_STAGE = 2 * SK_W_ATOM;   // 16 KB
@@ -67,14 +68,20 @@ template <int MT>
 constexpr int sk_threads() { return 128 + 32 * sk_merge_warps<MT>(); }
 template <int MT>
 constexpr int sk_nacc() { return MT >= 128 ? 2 : 4; }
-template <int MT>
-constexpr int sk_stages() { return (SK_SMEM_LIMIT - 2048) / (SK_W_STAGE + MT * 128); }
-template <int MT>
+// BNW = weight columns per tile: 128 (MMA M = 128, all TMEM lanes) or 64 (MMA
+// M = 64: rows land in TMEM lanes 0-15 of each 32-lane quarter, CUTLASS
+// mma_traits_sm100.hpp "half subpartitions" atom) -- twice the tiles for short K.
+template <int BNW>
+constexpr int sk_w_stage() { return BNW / 64 * SK_W_ATOM; }
+template <int MT, int BNW = 128>
+constexpr int sk_stages() { return (SK_SMEM_LIMIT - 2048) / (sk_w_stage<BNW>() + MT * 128); }
+template <int MT, int BNW = 128>
 constexpr size_t sk_smem() {
-  return 1024 + static_cast<size_t>(sk_stages<MT>()) * (SK_W_STAGE + MT * 128) + 512;
+  return 1024 + static_cast<size_t>(sk_stages<MT, BNW>()) * (sk_w_stage<BNW>() + MT * 128) + 512;
 }
 static_assert(sk_smem<16>() <= SK_SMEM_LIMIT && sk_smem<32>() <= SK_SMEM_LIMIT && sk_smem<64>() <= SK_SMEM_LIMIT &&
-                  sk_smem<128>() <= SK_SMEM_LIMIT,
+                  sk_smem<128>() <= SK_SMEM_LIMIT && sk_smem<16, 64>() <= SK_SMEM_LIMIT &&
+                  sk_smem<128, 64>() <= SK_SMEM_LIMIT,
               "skinny smem budget");
 // Tree levels that fit in TMEM next to the accumulators.
 template <int MT>
@@ -90,6 +97,7 @@ struct SkParams {
   int fold;            // finish: level-0 fold length over unit values (kf for leaf units, else 1)
   int log_groups;      // finish: log2(units / fold)
   long long items;
+  int bn;              // weight columns per tile (the kernel's BNW)
   float* out;
   long long ldo;
 };
@@ -149,7 +157,7 @@ struct SkItem {
 __device__ __forceinline__ SkItem sk_decode(const SkParams& p, long long item) {
   SkItem it;
   it.unit = static_cast<int>(item % p.units);
-  it.n0 = static_cast<int>(item / p.units) * SK_BN;
+  it.n0 = static_cast<int>(item / p.units) * p.bn;
   it.t_begin = it.unit * p.tiles_per_unit;
   it.t_end = min(p.T, it.t_begin + p.tiles_per_unit);
   return it;
@@ -160,15 +168,17 @@ __device__ __forceinline__ int sk_chunks(const SkParams& p, int t) {
   return (kh + SK_KSTAGE - 1) / SK_KSTAGE;
 }
 
-template <int MT>
+template <int MT, int BNW>
 __global__ void __launch_bounds__(sk_threads<MT>(), 1)
     tc_skinny_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                      const SkParams p) {
-  constexpr int NST = sk_stages<MT>();
+  constexpr int NST = sk_stages<MT, BNW>();
+  constexpr int W_STAGE = sk_w_stage<BNW>();
+  constexpr int LPQ = BNW / 4;  // valid TMEM lanes (tile columns) per 32-lane quarter
   constexpr int NACC = sk_nacc<MT>();
   constexpr int X_STAGE = MT * 128;
-  constexpr uint32_t TX_BYTES = SK_W_STAGE + X_STAGE;
-  constexpr uint32_t IDESC = umma_idesc_bf16(SK_BN, MT, /*a_mn_major=*/1, /*b_mn_major=*/0);
+  constexpr uint32_t TX_BYTES = W_STAGE + X_STAGE;
+  constexpr uint32_t IDESC = umma_idesc_bf16(BNW, MT, /*a_mn_major=*/1, /*b_mn_major=*/0);
   constexpr int TPW = sk_tpw<MT>();
   constexpr int NMW = sk_merge_warps<MT>();
   constexpr int NCH = TPW / 16;
@@ -176,7 +186,7 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
-  uint8_t* sX = sW + NST * SK_W_STAGE;
+  uint8_t* sX = sW + NST * W_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(sX + NST * X_STAGE);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
@@ -217,9 +227,9 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], TX_BYTES);
             const int k = t * p.bk + c * SK_KSTAGE;
-            uint8_t* w = sW + stage * SK_W_STAGE;
+            uint8_t* w = sW + stage * W_STAGE;
             tma_load_2d(w, &tmW, &full[stage], it.n0, k);
-            tma_load_2d(w + SK_W_ATOM, &tmW, &full[stage], it.n0 + 64, k);
+            if constexpr (BNW == 128) tma_load_2d(w + SK_W_ATOM, &tmW, &full[stage], it.n0 + 64, k);
             tma_load_2d(sX + stage * X_STAGE, &tmX, &full[stage], k, 0);
             if (++stage == NST) {
               stage = 0;
@@ -247,7 +257,7 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
           for (int c = 0; c < nch; ++c) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            const uint32_t w_base = smem_u32(sW + stage * SK_W_STAGE);
+            const uint32_t w_base = smem_u32(sW + stage * W_STAGE);
             const uint32_t x_base = smem_u32(sX + stage * X_STAGE);
 #pragma unroll
             for (int kk = 0; kk < SK_KSTAGE / 16; ++kk) {
@@ -277,7 +287,8 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
     uint32_t acc_iter = 0;
     for (long long item = blockIdx.x; item < p.items; item += gridDim.x) {
       const SkItem it = sk_decode(p, item);
-      const int n = it.n0 + q * 32 + lane;
+      const int n = it.n0 + q * LPQ + lane;
+      const bool lane_ok = lane < LPQ;  // BNW = 64: lanes 16-31 of a quarter hold no row
       int t_in_group = 0;
       uint32_t groups_done = 0;
       for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
@@ -335,7 +346,7 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
       }
       // g: this unit's value for column n, tokens h0 .. h0 + TPW - 1
       if (p.units == 1) {
-        if (n < p.N) {
+        if (lane_ok && n < p.N) {
 #pragma unroll
           for (int m = 0; m < TPW; ++m)
             if (h0 + m < p.M) p.out[static_cast<size_t>(h0 + m) * p.ldo + n] = g[m];
@@ -345,7 +356,9 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
         // ([MT][128] f32; every MMA that read the stages has completed)
         float* fbuf = reinterpret_cast<float*>(sW);
 #pragma unroll
-        for (int m = 0; m < TPW; ++m) fbuf[(h0 + m) * SK_BN + q * 32 + lane] = g[m];
+        if (lane_ok)
+#pragma unroll
+          for (int m = 0; m < TPW; ++m) fbuf[(h0 + m) * BNW + q * LPQ + lane] = g[m];
       }
     }
   }
@@ -364,19 +377,19 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
     // flight per thread
     const int tid = threadIdx.x;
     const int unit = static_cast<int>(blockIdx.x % p.units);
-    const int n0 = static_cast<int>(blockIdx.x / p.units) * SK_BN;
+    const int n0 = static_cast<int>(blockIdx.x / p.units) * BNW;
     const int R = (p.M + p.units - 1) / p.units;
     const int m_lo = unit * R, m_hi = min(p.M, m_lo + R);
-    const int nitems = (m_hi > m_lo ? m_hi - m_lo : 0) * (SK_BN / 4);
+    const int nitems = (m_hi > m_lo ? m_hi - m_lo : 0) * (BNW / 4);
     const uint32_t fb = smem_u32(sW);
     uint32_t peer[SK_MAX_UNITS];
 #pragma unroll
     for (int x = 0; x < SK_MAX_UNITS; ++x) peer[x] = x < p.units ? dsmem_map(fb, static_cast<uint32_t>(x)) : 0u;
 #pragma unroll 2
     for (int idx = tid; idx < nitems; idx += static_cast<int>(blockDim.x)) {
-      const int m = m_lo + idx / (SK_BN / 4);
-      const int c4 = (idx % (SK_BN / 4)) * 4;
-      const uint32_t off = static_cast<uint32_t>((m * SK_BN + c4) * 4);
+      const int m = m_lo + idx / (BNW / 4);
+      const int c4 = (idx % (BNW / 4)) * 4;
+      const uint32_t off = static_cast<uint32_t>((m * BNW + c4) * 4);
       float4 vals[SK_MAX_UNITS];
 #pragma unroll
       for (int x = 0; x < SK_MAX_UNITS; ++x)
@@ -468,15 +481,23 @@ tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaSt
   p.bk = static_cast<int>(v.bk);
   p.kf = static_cast<int>(v.kf);
   p.T = static_cast<int>(v.T);
-  p.ntiles = static_cast<int>((v.N + SK_BN - 1) / SK_BN);
   p.out = C;
   p.ldo = ldc;
+  const int64_t want = static_cast<int64_t>(sms) * 7 / 8;
+  // Tile width: 64-column tiles (MMA M = 64) when 128-column tiles cover at most
+  // half the SMs even with the deepest K split -- short K (TP shards) at decode
+  // sizes (measured, tools/decode_bench.py: TP=4 shard M >= 64 -11..16 %, TP=8
+  // -2..5 %; TP=1/2 stay faster with 128 columns and K units).
+  int bn = (v.N + SK_BN - 1) / SK_BN * std::min<int64_t>(v.L, SK_MAX_UNITS) <= want / 2 ? 64 : SK_BN;
+  const int force_bn = env_int("TBIK_SK_BN", 0);  // tuning knob (same bits)
+  if (force_bn == 64 || force_bn == 128) bn = force_bn;
+  p.bn = bn;
+  p.ntiles = static_cast<int>((v.N + bn - 1) / bn);
   // Units: aligned 2^j-group subtrees (<= 8, one cluster) until the items cover
   // ~7/8 of the SMs (K=14336 N=4096: 4 units, 128 CTAs; measured best vs 2 / 8).
   // TBIK_SK_UNITS / TBIK_SK_LEAF override (tuning knobs; same bits).
   const int max_levels = mt == 16 ? sk_max_levels<16>() : mt == 32 ? sk_max_levels<32>()
                        : mt == 64 ? sk_max_levels<64>() : sk_max_levels<128>();
-  const int64_t want = static_cast<int64_t>(sms) * 7 / 8;
   int64_t units = 1;
   while (units * 2 <= v.L && units * 2 <= SK_MAX_UNITS && p.ntiles * units * 2 <= want) units *= 2;
   const int force_u = env_int("TBIK_SK_UNITS", 0);
@@ -515,16 +536,21 @@ tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaSt
   TBIK_TRY(tc_make_map_2d(&mX, v.A, static_cast<uint64_t>(v.K), static_cast<uint64_t>(v.M),
                           static_cast<uint64_t>(v.lda) * 2, SK_KSTAGE, static_cast<uint32_t>(mt)));
   using Kern = void (*)(const CUtensorMap, const CUtensorMap, const SkParams);
-  const Kern kern = mt == 16 ? tc_skinny_kernel<16> : mt == 32 ? tc_skinny_kernel<32>
-                   : mt == 64 ? tc_skinny_kernel<64> : tc_skinny_kernel<128>;
-  const size_t smem = mt == 16 ? sk_smem<16>() : mt == 32 ? sk_smem<32>() : mt == 64 ? sk_smem<64>() : sk_smem<128>();
+  const Kern kern = bn == 128 ? (mt == 16 ? tc_skinny_kernel<16, 128> : mt == 32 ? tc_skinny_kernel<32, 128>
+                                 : mt == 64 ? tc_skinny_kernel<64, 128> : tc_skinny_kernel<128, 128>)
+                              : (mt == 16 ? tc_skinny_kernel<16, 64> : mt == 32 ? tc_skinny_kernel<32, 64>
+                                 : mt == 64 ? tc_skinny_kernel<64, 64> : tc_skinny_kernel<128, 64>);
+  const size_t smem = bn == 128 ? (mt == 16 ? sk_smem<16, 128>() : mt == 32 ? sk_smem<32, 128>()
+                                   : mt == 64 ? sk_smem<64, 128>() : sk_smem<128, 128>())
+                                : (mt == 16 ? sk_smem<16, 64>() : mt == 32 ? sk_smem<32, 64>()
+                                   : mt == 64 ? sk_smem<64, 64>() : sk_smem<128, 64>());
   const int threads = mt == 16 ? sk_threads<16>() : mt == 32 ? sk_threads<32>() : mt == 64 ? sk_threads<64>()
                                                                                           : sk_threads<128>();
-  static bool attr_set[16][4] = {};
-  const int mi = mt == 16 ? 0 : mt == 32 ? 1 : mt == 64 ? 2 : 3;
-  if (dev >= 0 && dev < 16 && !attr_set[dev][mi]) {
+  static bool attr_set[16][4][2] = {};
+  const int mi = mt == 16 ? 0 : mt == 32 ? 1 : mt == 64 ? 2 : 3, bi = bn == 128 ? 1 : 0;
+  if (dev >= 0 && dev < 16 && !attr_set[dev][mi][bi]) {
     TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr_set[dev][mi] = true;
+    attr_set[dev][mi][bi] = true;
   }
   // X = 1: persistent over tiles; X > 1: one CTA per (tile, unit), clusters of X.
   const long long grid = p.units > 1 ? p.items : (p.items < sms ? p.items : sms);

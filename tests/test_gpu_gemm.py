@@ -277,9 +277,9 @@ SCHEDULES = [{}, {"TBIK_TC_WIDE": "1"}, {"TBIK_TC_GROUP_M": "1"}, {"TBIK_TC_GROU
              {"TBIK_TC_PAIR": "0"}, {"TBIK_TC_PAIR": "0", "TBIK_TC_UNITS": "4"}, {"TBIK_TC_PAIR": "1"},
              {"TBIK_TC_ABOX": "32"}, {"TBIK_TC_ABOX": "64", "TBIK_TC_PAIR": "1"}, {"TBIK_TC_DEEP": "1"},
              {"TBIK_TC_SKINNY": "0"}, {"TBIK_SK_UNITS": "1"}, {"TBIK_SK_UNITS": "2", "TBIK_SK_LEAF": "0"},
-             {"TBIK_SK_UNITS": "8"}]
+             {"TBIK_SK_UNITS": "8"}, {"TBIK_SK_BN": "64"}]
 ENV_KNOBS = ("TBIK_TC_WIDE", "TBIK_TC_GROUP_M", "TBIK_TC_UNITS", "TBIK_TC_PAIR", "TBIK_TC_ABOX", "TBIK_TC_DEEP",
-             "TBIK_TC_SKINNY", "TBIK_SK_UNITS", "TBIK_SK_LEAF")
+             "TBIK_TC_SKINNY", "TBIK_SK_UNITS", "TBIK_SK_LEAF", "TBIK_SK_BN")
 
 
 @pytest.mark.parametrize("M,K,N", [(300, 14336, 640), (64, 4096, 512), (513, 6144, 384), (20, 4096, 200),
@@ -319,12 +319,15 @@ def test_skinny_matches_wide(tb, cuda, M, K, N, monkeypatch):
     ref = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
     monkeypatch.setenv("TBIK_TC_SKINNY", "1")
     L = tb.plan_blocks(K, cfg, 1).leaves
-    for u in [0] + [u for u in (1, 2, 4, 8) if u <= L]:
-        if u:
-            monkeypatch.setenv("TBIK_SK_UNITS", str(u))
-        y = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
-        assert torch.equal(y.view(torch.int32), ref.view(torch.int32)), f"skinny units={u} changed the bits"
-    monkeypatch.delenv("TBIK_SK_UNITS")
+    for bn in ("128", "64"):  # 128-column tiles (MMA M = 128) / 64-column tiles (M = 64)
+        monkeypatch.setenv("TBIK_SK_BN", bn)
+        for u in [0] + [u for u in (1, 2, 4, 8) if u <= L]:
+            if u:
+                monkeypatch.setenv("TBIK_SK_UNITS", str(u))
+            y = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+            assert torch.equal(y.view(torch.int32), ref.view(torch.int32)), f"skinny bn={bn} units={u} changed the bits"
+        monkeypatch.delenv("TBIK_SK_UNITS", raising=False)
+    monkeypatch.delenv("TBIK_SK_BN")
 
 
 @pytest.mark.parametrize("leaf_split", ["0", "1"])

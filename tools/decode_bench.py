@@ -106,8 +106,8 @@ for tp in (1, 2, 4, 8):
                           ("sk_noleaf", {"TBIK_TC_SKINNY": "1", "TBIK_SK_LEAF": "0"}),
                           ("sk_u2", {"TBIK_TC_SKINNY": "1", "TBIK_SK_UNITS": "2", "TBIK_SK_LEAF": "0"}),
                           ("sk_u4", {"TBIK_TC_SKINNY": "1", "TBIK_SK_UNITS": "4", "TBIK_SK_LEAF": "0"}),
-                          ("sk_mt64", {"TBIK_TC_SKINNY": "1", "TBIK_SK_MT": "64"}),
-                          ("sk_mt128", {"TBIK_TC_SKINNY": "1", "TBIK_SK_MT": "128"})):
+                          ("sk_bn64", {"TBIK_TC_SKINNY": "1", "TBIK_SK_BN": "64"}),
+                          ("sk_bn128", {"TBIK_TC_SKINNY": "1", "TBIK_SK_BN": "128"})):
             set_env(env)
             f = lambda i: tb.tree_matmul(x, wsh[i], cfg_s, tb.LEAF_TCGEN05, out=y)  # noqa: E731
             st = graph_time(f)
