@@ -170,9 +170,12 @@ int64_t tc_split_units(const GemmView& v) {
   // work items fill ~7/8 of the concurrent slots (74 CTA pairs / 148 CTAs) and
   // no further (2 for 32 pair tiles, 4 for 32 single-CTA tiles); deeper splits
   // lose to the extra subtree traffic and the per-item pipeline refill.
+  // ... and only while every unit keeps >= 16 leaves: with fewer, the per-item
+  // pipeline fill, final carry and the extra combine pass cost more than the idle
+  // SMs (tools/midm_sweep.py: K=4096 N=4096 M=256 330 -> 387 TFLOP/s unsplit).
   const int64_t enough = tc_parallel_slots(v) * 7 / 8;
   int64_t units = 1;
-  while (units * 2 <= v.L && tiles_mn * units * 2 <= enough) units *= 2;
+  while (units * 2 <= v.L && tiles_mn * units * 2 <= enough && v.T / (units * 2) >= 16) units *= 2;
   (void)next_pow2;
   if (const char* e = std::getenv("TBIK_TC_UNITS")) {  // tuning override (power of two <= leaves)
     const int64_t u = std::atoll(e);

@@ -1139,7 +1139,7 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
     const long long cap = dev >= 0 && dev < 16 ? max_clusters[dev] : sm_count() / 4;
     if (nstreams > cap) {
       lc.gridDim = dim3(static_cast<unsigned>(4 * cap));
-      if (p.levels > 3 && !p.scratch) return set_error(TBIK_CUDA_ERROR, "tc gemm: scratch");
+      if (p.levels >= first_scratch && !p.scratch) return set_error(TBIK_CUDA_ERROR, "tc gemm: scratch");
     }
   }
   TBIK_CUDA(cudaLaunchKernelEx(&lc, kern, mA, mB, mC, p));

@@ -11,12 +11,16 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2511_17826_b200 as tb  # noqa: E402
 
 cfg = tb.BlockConfig(64, 256, 128, 0)
-KNOBS = ("TBIK_TC_WIDE", "TBIK_TC_UNITS", "TBIK_TC_DEEP", "TBIK_TC_GROUP_M", "TBIK_TC_SKINNY", "TBIK_TC_EPI")
+KNOBS = ("TBIK_TC_WIDE", "TBIK_TC_UNITS", "TBIK_TC_DEEP", "TBIK_TC_GROUP_M", "TBIK_TC_SKINNY", "TBIK_TC_EPI",
+         "TBIK_TC_MC")
 VARIANTS = [("default", {}), ("wide", {"TBIK_TC_WIDE": "1"}), ("units2", {"TBIK_TC_UNITS": "2"}),
             ("units4", {"TBIK_TC_UNITS": "4"}), ("deep0", {"TBIK_TC_DEEP": "0"}), ("deep1", {"TBIK_TC_DEEP": "1"}),
             ("gm4", {"TBIK_TC_GROUP_M": "4"}), ("epi16", {"TBIK_TC_EPI": "16"})]
 if "--epi" in sys.argv:
     VARIANTS = [("default", {}), ("epi16", {"TBIK_TC_EPI": "16"})]
+if "--mc" in sys.argv:
+    VARIANTS = [("default", {}), ("mc", {"TBIK_TC_MC": "1"}), ("mc_u1", {"TBIK_TC_MC": "1", "TBIK_TC_UNITS": "1"}),
+                ("mc_u2", {"TBIK_TC_MC": "1", "TBIK_TC_UNITS": "2"}), ("units1", {"TBIK_TC_UNITS": "1"})]
 
 
 def graph_time(fn, reps=10):
@@ -41,6 +45,8 @@ def graph_time(fn, reps=10):
 for K, N in ((14336, 4096), (4096, 4096), (4096, 28672)):
     ws = [torch.randn(K, N, device="cuda").to(torch.bfloat16) for _ in range(3)]
     for M in ((1024, 2048, 4096) if "--epi" in sys.argv else (256, 512, 768, 1024, 1536, 2048)):
+        if "--mc" in sys.argv and M > 1024:
+            continue
         x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         y = torch.empty(M, N, device="cuda")
         ref = None
