@@ -136,6 +136,7 @@ struct TcParams {
   int pf;          // L2 prefetch distance in K chunks (0: off; measured slower, kept as a knob)
   int group_m;     // raster: M-blocks that share one pass over W
   int mc;          // 1: clusters of two pairs on adjacent N tiles share A (ntiles counts tile pairs)
+  int acc4;        // 1: four TMEM accumulators (items without tree levels leave cols 256-511 free)
   uint16_t* act;   // non-null: SiLU*up epilogue -- columns interleave gate (even) / up (odd);
   long long ld_act;  //   act[row][j] = bf16(silu(g[2j]) * g[2j+1]) replaces the f32 store
   // Fused tree all-reduce (ar_W > 1; FULL mode, pair tiles): owner(item) = item % ar_W.
@@ -395,8 +396,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + NST * B_STAGE);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // Two TMEM accumulators, or four when the items carry no tree level (one leaf
+  // group per item: TP shards) -- the level slots' columns [256, 512) are free
+  // then, and the MMA may run up to three leaves ahead of the output epilogue.
+  uint64_t* tempty = tfull + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
   uint8_t* sL3 = sB + NST * B_STAGE + 1024;  // 1024-aligned level-3 / output staging
 
   const int warp = threadIdx.x >> 5;
@@ -419,7 +423,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       mbar_init(&full[s], PAIR ? 2 : 1);  // one arrive.expect_tx per CTA (leader's copy used)
       mbar_init(&empty[s], MC ? 2 : 1);  // a multicast commit from each pair leader that reads the stage
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 4; ++b) {
       mbar_init(&tfull[b], 1);   // multicast commit
       mbar_init(&tempty[b], PAIR ? 2 * EPI : EPI);  // EPI merge warps per CTA (leader's copy used)
     }
@@ -496,8 +500,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       for (long long item = pair; item < p.items; item += npairs) {
         const Item it = decode(p, item, pid);
         for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
-          const int buf = acc_iter & 1;
-          const uint32_t use = acc_iter >> 1;
+          const int buf = p.acc4 ? acc_iter & 3 : acc_iter & 1;
+          const uint32_t use = p.acc4 ? acc_iter >> 2 : acc_iter >> 1;
           mbar_wait(&tempty[buf], (use & 1) ^ 1);
           tc_fence_after();
           const uint32_t d = tmem_base + buf * BN;
@@ -584,8 +588,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       int t_in_group = 0;
       uint32_t groups_done = 0;
       for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
-        const int buf = acc_iter & 1;
-        const uint32_t use = acc_iter >> 1;
+        const int buf = p.acc4 ? acc_iter & 3 : acc_iter & 1;
+        const uint32_t use = p.acc4 ? acc_iter >> 2 : acc_iter >> 1;
         mbar_wait(&tfull[buf], use & 1);
         tc_fence_after();
         const uint32_t acc = lane_base + buf * BN;
@@ -1022,6 +1026,9 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   p.mblocks = static_cast<int>((v.M + p.tile_m - 1) / p.tile_m);
   p.ntiles = static_cast<int>((v.N + BN - 1) / BN);
   p.mc = mc ? 1 : 0;
+  p.acc4 = p.levels == 0 ? 1 : 0;  // no level slot in TMEM (TBIK_TC_ACC4=0 turns it off)
+  if (const char* e = std::getenv("TBIK_TC_ACC4"))
+    if (*e && std::atoi(e) == 0) p.acc4 = 0;
   if (mc) p.ntiles = (p.ntiles + 1) / 2;  // work items are tile pairs
   p.items = static_cast<long long>(p.mblocks) * p.ntiles * p.units;
   const long long slots = mc ? sm_count() / 4 : pair ? sm_count() / 2 : sm_count();

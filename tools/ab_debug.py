@@ -34,9 +34,14 @@ if len(sys.argv) > 1 and sys.argv[1] == "run":
     print(f"{2 * M * K * N / t / 1e6:.0f}")
     sys.exit(0)
 
-for K, N, M in ((4096, 4096, 2048), (4096, 4096, 4096), (14336, 4096, 4096), (4096, 28672, 1024)):
+SHAPES = ((4096, 4096, 2048), (4096, 4096, 4096), (14336, 4096, 4096), (4096, 28672, 1024))
+DBG = ("0", "1", "2", "4", "6")
+if "--store" in sys.argv:  # TMA-store output staging vs direct row stores (debug 16)
+    SHAPES = ((4096, 4096, 4096), (1792, 4096, 4096), (14336, 4096, 4096), (4096, 28672, 1024))
+    DBG = ("0", "16", "2")
+for K, N, M in SHAPES:
     line = [f"K={K} N={N} M={M}"]
-    for dbg in ("0", "1", "2", "4", "6"):
+    for dbg in DBG:
         env = dict(os.environ, TBIK_TC_DEBUG=dbg)
         out = subprocess.run([sys.executable, __file__, "run", str(K), str(N), str(M)], env=env,
                              capture_output=True, text=True).stdout.strip()
