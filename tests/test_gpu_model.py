@@ -121,6 +121,24 @@ def test_llama_forward_batch_invariance(tb, cuda, llama2):
         assert torch.equal(one.view(torch.int32), full[b * 64:(b + 1) * 64].view(torch.int32)), b
 
 
+def test_llama_forward_graph_decode_size(tb, cuda, llama2):
+    """A CUDA-graph capture of a decode-sized forward (2 x 16 tokens: every GEMM on
+    the swap-AB skinny kernel, its K split in thread-block clusters) replays to
+    the eager bits, at TP = 1 and 8."""
+    from paper_2511_17826_b200 import model as mdl
+    cfg, w = llama2
+    dec = mdl.TbikDecoder(cfg, w)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(8)
+    tokens = torch.randint(0, cfg.vocab, (2, 16), device=cuda, generator=g)
+    for tp in (1, 8):
+        eager = dec.forward(tokens, tp).clone()
+        graph, (logits, _lse, _lp) = dec.capture(tokens, tp)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(logits.view(torch.int32), eager.view(torch.int32)), f"graph replay differs at tp={tp}"
+
+
 def test_qwen3_stack_tp8_batch_sweep(tb, cuda):
     from paper_2511_17826_b200 import model as mdl
     cfg = mdl.qwen3_32b(n_layers=2)
