@@ -309,7 +309,8 @@ def test_tc_schedules_invisible(tb, cuda, orc, M, K, N, monkeypatch):
 # swap-AB skinny kernel (M <= 128, tbik_gemm_skinny.cu): the same bits as the wide
 # kernel for every token-width class, unit split, leaf split and TP shard view
 @pytest.mark.parametrize("M,K,N", [(1, 14336, 4096), (16, 14336, 640), (17, 4096, 1000), (33, 6144, 384),
-                                   (64, 25600, 256), (65, 14336, 512), (128, 8192, 256), (5, 777, 300)])
+                                   (64, 25600, 256), (65, 14336, 512), (128, 8192, 256), (5, 777, 300),
+                                   (16, 4096, 40000)])  # > 148 tiles: persistent CTAs over several tiles
 def test_skinny_matches_wide(tb, cuda, M, K, N, monkeypatch):
     torch.manual_seed(1000 + M)
     x = torch.randn(M, K, device=cuda).to(torch.bfloat16)
