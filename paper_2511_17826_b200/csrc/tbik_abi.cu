@@ -349,9 +349,12 @@ tbik_status tbik_tree_matmul_silu_mul(const void* A, int a_dtype, int64_t lda, c
   GemmView v;
   TBIK_TRY(make_view(A, a_dtype, lda, B, b_dtype, ldb, M, N, K, cfg->block_k, cfg->k_first, &v));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (leaf_mode == TBIK_LEAF_TCGEN05 && tc_split_units(v) <= 1) {
+  // SiLU*up in the wide GEMM's epilogue; decode sizes (M <= 128) go through the
+  // skinny weight-streaming kernel instead (the separate SiLU*up pass over M x N
+  // f32 is small there), same bits either way.
+  if (leaf_mode == TBIK_LEAF_TCGEN05 && !tc_use_skinny(v) && tc_split_units(v) <= 1) {
     GemmOut o{OUT_FULL, v.T, nullptr, N, 0, static_cast<uint16_t*>(act), ld_act};
-    return launch_tc_gemm(v, o, s);  // SiLU*up in the GEMM epilogue
+    return launch_tc_gemm(v, o, s);
   }
   // split launches / exact leaf: f32 tree GEMM, then the same SiLU*up as a kernel
   float* tmp = static_cast<float*>(workspace(static_cast<size_t>(M) * N * sizeof(float), 10));
