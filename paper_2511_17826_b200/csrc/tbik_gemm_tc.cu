@@ -46,7 +46,6 @@
 // the tensor core's block_k-long accumulation.  Nothing in
 // the per-element arithmetic depends on M, the tile position, the unit split, the
 // raster or the TP shard -> batch- and TP-invariant by construction.
-#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -137,8 +136,7 @@ struct TcParams {
   int pf;          // L2 prefetch distance in K chunks (0: off; measured slower, kept as a knob)
   int group_m;     // raster: M-blocks that share one pass over W
   int mc;          // 1: clusters of two pairs on adjacent N tiles share A (ntiles counts tile pairs)
-  int nacc;        // TMEM accumulators: 2, 3 or 4 (the level slots the items leave free)
-  int acc2_col;    // TMEM column of accumulator 2 (256 or 384); accumulator 3 at 384
+  int acc4;        // 1: four TMEM accumulators (items without tree levels leave cols 256-511 free)
   uint16_t* act;   // non-null: SiLU*up epilogue -- columns interleave gate (even) / up (odd);
   long long ld_act;  //   act[row][j] = bf16(silu(g[2j]) * g[2j+1]) replaces the f32 store
   // Fused tree all-reduce (ar_W > 1; FULL mode, pair tiles): owner(item) = item % ar_W.
@@ -502,11 +500,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       for (long long item = pair; item < p.items; item += npairs) {
         const Item it = decode(p, item, pid);
         for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
-          const int buf = static_cast<int>(acc_iter % static_cast<uint32_t>(p.nacc));
-          const uint32_t use = acc_iter / static_cast<uint32_t>(p.nacc);
+          const int buf = p.acc4 ? acc_iter & 3 : acc_iter & 1;
+          const uint32_t use = p.acc4 ? acc_iter >> 2 : acc_iter >> 1;
           mbar_wait(&tempty[buf], (use & 1) ^ 1);
           tc_fence_after();
-          const uint32_t d = tmem_base + (buf < 2 ? buf * BN : buf == 2 ? p.acc2_col : 384);
+          const uint32_t d = tmem_base + buf * BN;
           const int nch = tile_chunks(p, t);
           for (int c = 0; c < nch; ++c) {
             mbar_wait(&full[stage], phase);
@@ -590,11 +588,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       int t_in_group = 0;
       uint32_t groups_done = 0;
       for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
-        const int buf = static_cast<int>(acc_iter % static_cast<uint32_t>(p.nacc));
-        const uint32_t use = acc_iter / static_cast<uint32_t>(p.nacc);
+        const int buf = p.acc4 ? acc_iter & 3 : acc_iter & 1;
+        const uint32_t use = p.acc4 ? acc_iter >> 2 : acc_iter >> 1;
         mbar_wait(&tfull[buf], use & 1);
         tc_fence_after();
-        const uint32_t acc = lane_base + (buf < 2 ? buf * BN : buf == 2 ? p.acc2_col : 384);
+        const uint32_t acc = lane_base + buf * BN;
         // Both 32-column chunks in flight at once, one wait (for k_first == 1 on an
         // odd group: each leaf chunk together with the level-1 slot chunk it merges
         // with); the accumulator goes back to the MMA issuer as soon as the values
@@ -1028,18 +1026,9 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   p.mblocks = static_cast<int>((v.M + p.tile_m - 1) / p.tile_m);
   p.ntiles = static_cast<int>((v.N + BN - 1) / BN);
   p.mc = mc ? 1 : 0;
-  // TMEM level slots in use: k_first > 1 -> levels 1, 2 at cols 256, 384;
-  // k_first == 1 -> levels 2, 3 at 384, 256 (level 1 in registers).  Free slot
-  // columns become extra accumulators (TBIK_TC_NACC=2 forces two; same bits).
-  {
-    const bool k1 = p.kf == 1;
-    const int slots = k1 ? std::max(0, std::min(p.levels, 3) - 1) : std::min(p.levels, 2);
-    p.nacc = slots == 0 ? 4 : slots == 1 ? 3 : 2;
-    // accumulator 2: col 256 with four, else the one free slot (k_first 1: 256, else 384)
-    p.acc2_col = p.nacc == 4 || k1 ? 256 : 384;
-    if (const char* e = std::getenv("TBIK_TC_NACC"))
-      if (*e && std::atoi(e) >= 2 && std::atoi(e) <= p.nacc) p.nacc = std::atoi(e);
-  }
+  p.acc4 = p.levels == 0 ? 1 : 0;  // no level slot in TMEM (TBIK_TC_ACC4=0 turns it off)
+  if (const char* e = std::getenv("TBIK_TC_ACC4"))
+    if (*e && std::atoi(e) == 0) p.acc4 = 0;
   if (mc) p.ntiles = (p.ntiles + 1) / 2;  // work items are tile pairs
   p.items = static_cast<long long>(p.mblocks) * p.ntiles * p.units;
   const long long slots = mc ? sm_count() / 4 : pair ? sm_count() / 2 : sm_count();
