@@ -318,28 +318,41 @@ __device__ __forceinline__ void ar_reduce_owned(const TcParams& p, long long pai
     const int cols = min(BN, p.N - it.n0);
     if (rows <= 0) continue;
     if (cols == BN && (p.ldo & 3) == 0) {
+      // 2 float4 per thread per round, all W loads of the round in flight at once
+      // (NVLink latency-bound: two warps per SM need the ILP); L2-only loads -- the
+      // flag acquire + barrier above order them after the peers' stores.
+      constexpr int U = 2;
       const int nq = rows * (BN / 4);
-      for (int idx = rt; idx < nq; idx += 64) {
-        const size_t e4 = (static_cast<size_t>(r0 + idx / (BN / 4)) * p.ldo + it.n0) / 4 + idx % (BN / 4);
-        float4 r[8];
+      for (int base = 0; base < nq; base += 64 * U) {
+        size_t e4[U];
+        float4 r[U][8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (k < W) r[k] = __ldcv(reinterpret_cast<const float4*>(p.ar_src[k]) + e4);
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + u * 64 + rt;
+          e4[u] = idx < nq ? (static_cast<size_t>(r0 + idx / (BN / 4)) * p.ldo + it.n0) / 4 + idx % (BN / 4) : 0;
 #pragma unroll
-        for (int l = 1; l <= 3; ++l) {
-          const int st = 1 << l, h = 1 << (l - 1);
-#pragma unroll
-          for (int left = 0; left < 8; left += st)
-            if (left + h < W) {
-              r[left].x = __fadd_rn(r[left].x, r[left + h].x);
-              r[left].y = __fadd_rn(r[left].y, r[left + h].y);
-              r[left].z = __fadd_rn(r[left].z, r[left + h].z);
-              r[left].w = __fadd_rn(r[left].w, r[left + h].w);
-            }
+          for (int k = 0; k < 8; ++k)
+            if (k < W && idx < nq) r[u][k] = __ldcg(reinterpret_cast<const float4*>(p.ar_src[k]) + e4[u]);
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (k < W) reinterpret_cast<float4*>(p.ar_dst[(p.ar_rank + k) & (W - 1)])[e4] = r[0];
+        for (int u = 0; u < U; ++u) {
+          if (base + u * 64 + rt >= nq) continue;
+#pragma unroll
+          for (int l = 1; l <= 3; ++l) {
+            const int st = 1 << l, h = 1 << (l - 1);
+#pragma unroll
+            for (int left = 0; left < 8; left += st)
+              if (left + h < W) {
+                r[u][left].x = __fadd_rn(r[u][left].x, r[u][left + h].x);
+                r[u][left].y = __fadd_rn(r[u][left].y, r[u][left + h].y);
+                r[u][left].z = __fadd_rn(r[u][left].z, r[u][left + h].z);
+                r[u][left].w = __fadd_rn(r[u][left].w, r[u][left + h].w);
+              }
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (k < W) reinterpret_cast<float4*>(p.ar_dst[(p.ar_rank + k) & (W - 1)])[e4[u]] = r[u][0];
+        }
       }
     } else {
       const int ne = rows * cols;
