@@ -302,91 +302,109 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// Fused all-reduce, warps 2-3 (see the kernel): reduce this rank's items of this
-// pair from the peers' send slots, push to every rank's result slot, publish done.
-__device__ __forceinline__ void ar_reduce_owned(const TcParams& p, long long pair, long long npairs, int pid,
-                                             uint32_t rank) {
-    const int rt = threadIdx.x - 64;  // 0..63
+// Fused all-reduce of ONE owned item's 128-row half (this CTA's), by threads
+// rt = 0..nthr-1 meeting on named barrier `bar_id`: wait for the W ranks' tile
+// flags, reduce in Algorithm-2 order (collective.cpp:67-74) from the peers' send
+// slots, push the result into every rank's result slot.
+__device__ __forceinline__ void ar_reduce_item(const TcParams& p, long long item, int pid, uint32_t rank, int rt,
+                                               int nthr, int bar_id) {
   const int W = p.ar_W;
-  for (long long item = pair; item < p.items; item += npairs) {
-    if (static_cast<int>(item % W) != p.ar_rank) continue;
-    const Item it = decode(p, item, pid);
-    if (rt < W) spin_until_epoch(p.ar_flags[p.ar_rank] + ((item * 2 + rank) * W + rt), p.ar_epoch);
-    named_bar(2, 64);
-    const int r0 = it.m0 + static_cast<int>(rank) * BM;
-    const int rows = min(BM, p.M - r0);
-    const int cols = min(BN, p.N - it.n0);
-    if (rows <= 0) continue;
-    if (cols == BN && (p.ldo & 3) == 0) {
-      // 2 float4 per thread per round, all W loads of the round in flight at once
-      // (NVLink latency-bound: two warps per SM need the ILP); L2-only loads -- the
-      // flag acquire + barrier above order them after the peers' stores.
-      constexpr int U = 2;
-      const int nq = rows * (BN / 4);
-      for (int base = 0; base < nq; base += 64 * U) {
-        size_t e4[U];
-        float4 r[U][8];
+  const Item it = decode(p, item, pid);
+  if (rt < W) spin_until_epoch(p.ar_flags[p.ar_rank] + ((item * 2 + rank) * W + rt), p.ar_epoch);
+  named_bar(bar_id, nthr);
+  const int r0 = it.m0 + static_cast<int>(rank) * BM;
+  const int rows = min(BM, p.M - r0);
+  const int cols = min(BN, p.N - it.n0);
+  if (rows <= 0) return;
+  if (cols == BN && (p.ldo & 3) == 0) {
+    // 2 float4 per thread per round, all W loads of the round in flight at once
+    // (NVLink latency-bound with few warps: the ILP matters); L2-only loads -- the
+    // flag acquire + barrier above order them after the peers' stores.
+    constexpr int U = 2;
+    const int nq = rows * (BN / 4);
+    for (int base = 0; base < nq; base += nthr * U) {
+      size_t e4[U];
+      float4 r[U][8];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int idx = base + u * 64 + rt;
-          e4[u] = idx < nq ? (static_cast<size_t>(r0 + idx / (BN / 4)) * p.ldo + it.n0) / 4 + idx % (BN / 4) : 0;
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (k < W && idx < nq) r[u][k] = __ldcg(reinterpret_cast<const float4*>(p.ar_src[k]) + e4[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (base + u * 64 + rt >= nq) continue;
-#pragma unroll
-          for (int l = 1; l <= 3; ++l) {
-            const int st = 1 << l, h = 1 << (l - 1);
-#pragma unroll
-            for (int left = 0; left < 8; left += st)
-              if (left + h < W) {
-                r[u][left].x = __fadd_rn(r[u][left].x, r[u][left + h].x);
-                r[u][left].y = __fadd_rn(r[u][left].y, r[u][left + h].y);
-                r[u][left].z = __fadd_rn(r[u][left].z, r[u][left + h].z);
-                r[u][left].w = __fadd_rn(r[u][left].w, r[u][left + h].w);
-              }
-          }
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (k < W) reinterpret_cast<float4*>(p.ar_dst[(p.ar_rank + k) & (W - 1)])[e4[u]] = r[u][0];
-        }
-      }
-    } else {
-      const int ne = rows * cols;
-      for (int idx = rt; idx < ne; idx += 64) {
-        const size_t e = static_cast<size_t>(r0 + idx / cols) * p.ldo + it.n0 + idx % cols;
-        float r[8];
+      for (int u = 0; u < U; ++u) {
+        const int idx = base + u * nthr + rt;
+        e4[u] = idx < nq ? (static_cast<size_t>(r0 + idx / (BN / 4)) * p.ldo + it.n0) / 4 + idx % (BN / 4) : 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          if (k < W) r[k] = __ldcv(p.ar_src[k] + e);
+          if (k < W && idx < nq) r[u][k] = __ldcg(reinterpret_cast<const float4*>(p.ar_src[k]) + e4[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (base + u * nthr + rt >= nq) continue;
 #pragma unroll
         for (int l = 1; l <= 3; ++l) {
           const int st = 1 << l, h = 1 << (l - 1);
 #pragma unroll
           for (int left = 0; left < 8; left += st)
-            if (left + h < W) r[left] = __fadd_rn(r[left], r[left + h]);
+            if (left + h < W) {
+              r[u][left].x = __fadd_rn(r[u][left].x, r[u][left + h].x);
+              r[u][left].y = __fadd_rn(r[u][left].y, r[u][left + h].y);
+              r[u][left].z = __fadd_rn(r[u][left].z, r[u][left + h].z);
+              r[u][left].w = __fadd_rn(r[u][left].w, r[u][left + h].w);
+            }
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          if (k < W) p.ar_dst[(p.ar_rank + k) & (W - 1)][e] = r[0];
+          if (k < W) reinterpret_cast<float4*>(p.ar_dst[(p.ar_rank + k) & (W - 1)])[e4[u]] = r[u][0];
       }
     }
+  } else {
+    const int ne = rows * cols;
+    for (int idx = rt; idx < ne; idx += nthr) {
+      const size_t e = static_cast<size_t>(r0 + idx / cols) * p.ldo + it.n0 + idx % cols;
+      float r[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < W) r[k] = __ldcv(p.ar_src[k] + e);
+#pragma unroll
+      for (int l = 1; l <= 3; ++l) {
+        const int st = 1 << l, h = 1 << (l - 1);
+#pragma unroll
+        for (int left = 0; left < 8; left += st)
+          if (left + h < W) r[left] = __fadd_rn(r[left], r[left + h]);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < W) p.ar_dst[(p.ar_rank + k) & (W - 1)][e] = r[0];
+    }
   }
-  // every CTA of this rank is done with its owned items: the last one tells all peers
+  }
+
+// Warps 2-3 during the GEMM: every owned item of this pair except the pair's last
+// one, which all warps reduce together once the GEMM loops are done (the kernel's
+// tail would otherwise wait on two warps' NVLink loads).
+__device__ __forceinline__ void ar_reduce_owned(const TcParams& p, long long pair, long long npairs, int pid,
+                                                uint32_t rank) {
+  const long long last = pair < p.items ? pair + (p.items - 1 - pair) / npairs * npairs : -1;
+  for (long long item = pair; item < p.items; item += npairs)
+    if (item != last && static_cast<int>(item % p.ar_W) == p.ar_rank)
+      ar_reduce_item(p, item, pid, rank, static_cast<int>(threadIdx.x) - 64, 64, 2);
+}
+
+// After the GEMM loops, all threads of the CTA: the pair's last item if owned, then
+// (every CTA of this rank done) the last CTA publishes done[rank] to all peers.
+__device__ __forceinline__ void ar_finish(const TcParams& p, long long pair, long long npairs, int pid,
+                                          uint32_t rank) {
+  const long long last = pair < p.items ? pair + (p.items - 1 - pair) / npairs * npairs : -1;
+  if (last >= 0 && static_cast<int>(last % p.ar_W) == p.ar_rank)
+    ar_reduce_item(p, last, pid, rank, static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x), 3);
   __threadfence_system();
-  named_bar(2, 64);
-  if (rt == 0) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
     const uint32_t prev = atomicAdd(p.ar_counter, 1u);
     if (prev == gridDim.x - 1) {
       *p.ar_counter = 0;
       __threadfence_system();
-      for (int r = 0; r < W; ++r) st_release_sys(p.ar_done[r] + p.ar_rank, p.ar_epoch);
+      for (int r = 0; r < p.ar_W; ++r) st_release_sys(p.ar_done[r] + p.ar_rank, p.ar_epoch);
     }
   }
 }
+
 
 // EPI merge warps (two per TMEM lane quarter, splitting the 128 columns), ABOX
 // A rows staged per stage (128, or 64 / 32 for small M; stage count follows).  KF1 (used when k_first == 1, where every leaf completes a
@@ -818,6 +836,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     }
   }
 
+  if constexpr (AR) {
+    __syncthreads();  // every role's loop is done (the merge warps published all items)
+    ar_finish(p, pair, npairs, pid, rank);
+  }
   tc_fence_before();
   cluster_sync();
   if (warp == 2) {
