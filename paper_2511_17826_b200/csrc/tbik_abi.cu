@@ -163,19 +163,26 @@ tbik_status pad_operand(const void** p, int64_t* ld, int64_t rows, int64_t cols,
 
 int64_t tc_split_units(const GemmView& v) {
   const int64_t tiles_mn = tc_tiles(v);
-  // Split the K range of each output tile into 2^j aligned subtrees only when
-  // the machine would otherwise idle; the combine continues the same tree
-  // (Theorem 1), so the split never changes bits.  Measured on B200
-  // (tools/tune_units.py, tools/tune_small.py, K=14336 N=4096): split until the
-  // work items fill ~7/8 of the concurrent slots (74 CTA pairs / 148 CTAs) and
-  // no further (2 for 32 pair tiles, 4 for 32 single-CTA tiles); deeper splits
-  // lose to the extra subtree traffic and the per-item pipeline refill.
-  // ... and only while every unit keeps >= 16 leaves: with fewer, the per-item
-  // pipeline fill, final carry and the extra combine pass cost more than the idle
-  // SMs (tools/midm_sweep.py: K=4096 N=4096 M=256 330 -> 387 TFLOP/s unsplit).
-  const int64_t enough = tc_parallel_slots(v) * 7 / 8;
+  // Split the K range of each output tile into 2^j aligned subtrees when it pays:
+  // the split changes the wave efficiency items / (waves * slots) of the launch
+  // (74 CTA pairs / 148 CTAs), and costs ~12 bytes of extra partial-output
+  // traffic per output element (written by the GEMM, read + combined by
+  // tree_combine_vec_kernel) against 2K flops -- about 1300 / K of the GEMM's time
+  // at B200 rates.  Split while the efficiency gain exceeds that and every unit
+  // keeps >= 8 leaves.  The combine continues the same tree (Theorem 1): the
+  // split never changes bits.  Measured (tools/midm_sweep.py, e93, with the
+  // vectorised combine): K=14336 M=768 / 2048 +9 % / +3 %, K=4096 M=256 / 768
+  // +31 % / +5 % split; no split where the efficiency does not move (M=512, 1024,
+  // 1536) or K is short (K=4096 M=2048: -15 % split).
+  const int64_t slots = tc_parallel_slots(v);
+  auto eff = [&](int64_t items) {
+    const int64_t waves = (items + slots - 1) / slots;
+    return static_cast<double>(items) / static_cast<double>(waves * slots);
+  };
   int64_t units = 1;
-  while (units * 2 <= v.L && tiles_mn * units * 2 <= enough && v.T / (units * 2) >= 16) units *= 2;
+  while (units * 2 <= v.L && v.T / (units * 2) >= 8 &&
+         eff(tiles_mn * units * 2) / eff(tiles_mn * units) - 1.0 > 1300.0 / static_cast<double>(v.K) - 0.02)
+    units *= 2;
   (void)next_pow2;
   if (const char* e = std::getenv("TBIK_TC_UNITS")) {  // tuning override (power of two <= leaves)
     const int64_t u = std::atoll(e);

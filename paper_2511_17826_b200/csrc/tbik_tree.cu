@@ -61,6 +61,39 @@ __global__ void tree_combine_kernel(const float* __restrict__ ws, int64_t X, int
   out[r * ldo + c] = stack[j][0];
 }
 
+// Fast path for the common split (fold == 1, X = 2^j <= 8 subtree values, 16-byte
+// aligned rows): float4 per thread, all X loads in flight, the contiguous-halves
+// tree unrolled -- the same bits as tree_combine_kernel (each value canonicalised
+// 0 + v, merges commutative).
+template <int X>
+__global__ void tree_combine_vec_kernel(const float* __restrict__ ws, int64_t rows, int64_t cols, int64_t slice,
+                                        float* __restrict__ out, int64_t ldo) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t cq = cols / 4;
+  if (q >= rows * cq) return;
+  const int64_t r = q / cq, c = (q - r * cq) * 4;
+  float4 v[X];
+#pragma unroll
+  for (int x = 0; x < X; ++x) v[x] = *reinterpret_cast<const float4*>(ws + x * slice + r * cols + c);
+#pragma unroll
+  for (int x = 0; x < X; ++x) {
+    v[x].x = __fadd_rn(0.0f, v[x].x);
+    v[x].y = __fadd_rn(0.0f, v[x].y);
+    v[x].z = __fadd_rn(0.0f, v[x].z);
+    v[x].w = __fadd_rn(0.0f, v[x].w);
+  }
+#pragma unroll
+  for (int st = 2; st <= X; st <<= 1)
+#pragma unroll
+    for (int left = 0; left < X; left += st) {
+      v[left].x = __fadd_rn(v[left].x, v[left + st / 2].x);
+      v[left].y = __fadd_rn(v[left].y, v[left + st / 2].y);
+      v[left].z = __fadd_rn(v[left].z, v[left + st / 2].z);
+      v[left].w = __fadd_rn(v[left].w, v[left + st / 2].w);
+    }
+  *reinterpret_cast<float4*>(out + r * ldo + c) = v[0];
+}
+
 template <bool RING, bool VEC>
 __global__ void allreduce_kernel(const PartPtrs parts, int W, int64_t elems,
                                  float* __restrict__ out) {
@@ -152,6 +185,21 @@ tbik_status launch_tree_combine(const float* ws, int64_t X, int64_t fold, int64_
   const int64_t n = rows * cols;
   if (n == 0) return TBIK_OK;
   const int threads = 256;
+  const bool vec = fold == 1 && (X == 2 || X == 4 || X == 8) && cols % 4 == 0 && ldo % 4 == 0 &&
+                   (reinterpret_cast<uintptr_t>(ws) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  if (vec) {
+    const int64_t nq = n / 4;
+    const unsigned vb = static_cast<unsigned>((nq + threads - 1) / threads);
+    if (X == 2)
+      tree_combine_vec_kernel<2><<<vb, threads, 0, stream>>>(ws, rows, cols, n, out, ldo);
+    else if (X == 4)
+      tree_combine_vec_kernel<4><<<vb, threads, 0, stream>>>(ws, rows, cols, n, out, ldo);
+    else
+      tree_combine_vec_kernel<8><<<vb, threads, 0, stream>>>(ws, rows, cols, n, out, ldo);
+    TBIK_CUDA(cudaGetLastError());
+    count_launch();
+    return TBIK_OK;
+  }
   const int64_t blocks = (n + threads - 1) / threads;
   tree_combine_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(ws, X, fold, rows, cols,
                                                                             rows * cols, out, ldo);
