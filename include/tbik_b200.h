@@ -182,6 +182,73 @@ TBIK_API tbik_status tbik_tree_all_reduce_local(const float* const* partials, in
 TBIK_API tbik_status tbik_ring_reduce_local(const float* const* partials, int W, float* out,
                                    int64_t elems, void* stream);
 
+/* leaf_dot (matmul.hpp:48, matmul.cpp:69-75) on the device: *out = ascending-k
+ * fma chain from +0 over a[0..n) . b[0..n) (f32, device pointers), one thread. */
+TBIK_API tbik_status tbik_leaf_dot(const float* a, const float* b, int64_t n, float* out, void* stream);
+
+/* silu (demo.hpp:56, demo.cpp:36-45): out[i][j] = z / (1 + exp(-z)), z = x widened
+ * to f32; exp is the library's shared polynomial. */
+TBIK_API tbik_status tbik_silu(const void* x, int x_dtype, int64_t ldx, int64_t rows, int64_t cols, float* out,
+                               int64_t ldo, void* stream);
+
+/* ---- one process, several GPUs (the reference's DeviceGroup, collective.hpp:15-23) --
+ * World size W, rank r runs on device_ids[r] (ranks may share a device).  Peer
+ * access is enabled between the distinct devices; every rank gets its own
+ * stream on its device and a group-owned f32 partial buffer there. */
+typedef struct tbik_local_group tbik_local_group;
+TBIK_API tbik_status tbik_local_group_create(int world_size, const int* device_ids, tbik_local_group** out);
+TBIK_API tbik_status tbik_local_group_destroy(tbik_local_group* g);
+TBIK_API int tbik_local_group_device(const tbik_local_group* g, int rank);
+/* Rank r's stream (cudaStream_t on its device): inputs a caller uploads for rank
+ * r must be complete or ordered on it. */
+TBIK_API void* tbik_local_group_stream(const tbik_local_group* g, int rank);
+/* row_parallel_forward (layers.cpp:74-98) across the group's devices: rank r's
+ * X_shards[r] [M x K_r] (row stride ldx[r]) and W_shards[r] [K_r x N] (ldw[r])
+ * live on its device, K_r = make_row_shard_plan(K_global)[r].  Each rank's tree
+ * GEMM (global k_first) runs on its own device and stream; then rank 0's device
+ * reduces the W partials over peer memory in Algorithm-2 order into Y (on rank
+ * 0's device, ldy).  `stream` (rank 0's device) is ordered after the result. */
+TBIK_API tbik_status tbik_local_group_row_parallel_forward(tbik_local_group* g, const void* const* X_shards,
+                                                           int x_dtype, const int64_t* ldx,
+                                                           const void* const* W_shards, int w_dtype,
+                                                           const int64_t* ldw, float* Y, int64_t ldy, int64_t M,
+                                                           int64_t N, int64_t K_global, const tbik_block_config* cfg,
+                                                           int64_t c_max, int leaf_mode, void* stream);
+
+/* ---- the labelled NON-INVARIANT status quo (collective.cpp:94-106, layers.cpp:100-121) --
+ * cuBLAS GEMMs (f32 accumulate, summation order chosen by the library) and a
+ * left-to-right ring sum / NCCL all-reduce: the baseline the price of
+ * determinism is measured against.  Never used by the TBIK path. */
+/* C[M x N] f32 = A . B with cuBLAS (bf16 or f32 operands, f32 accumulate). */
+TBIK_API tbik_status tbik_baseline_gemm(const void* A, int a_dtype, int64_t lda, const void* B, int b_dtype,
+                                        int64_t ldb, float* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                                        void* stream);
+/* baseline_row_parallel_forward (layers.cpp:100-121) with `tp` simulated ranks on
+ * one device: K % tp == 0 (ShardError otherwise), rank r's cuBLAS GEMM over
+ * [r*K/tp, (r+1)*K/tp), then ring_reduce_baseline (left to right). */
+TBIK_API tbik_status tbik_baseline_row_parallel_forward_local(const void* X, int x_dtype, int64_t ldx, const void* W,
+                                                              int w_dtype, int64_t ldw, float* Y, int64_t ldy,
+                                                              int64_t M, int64_t N, int64_t K, int tp, void* stream);
+/* baseline_column_parallel_forward (layers.cpp:122-146): cuBLAS per column shard. */
+TBIK_API tbik_status tbik_baseline_column_parallel_forward_local(const void* X, int x_dtype, int64_t ldx,
+                                                                 const void* W, int w_dtype, int64_t ldw, float* Y,
+                                                                 int64_t ldy, int64_t M, int64_t N, int64_t K, int tp,
+                                                                 void* stream);
+/* NCCL communicator for the baseline across processes (one per GPU). */
+#define TBIK_NCCL_ID_BYTES 128
+TBIK_API tbik_status tbik_nccl_unique_id(void* id_out /* TBIK_NCCL_ID_BYTES */);
+TBIK_API tbik_status tbik_nccl_comm_create(int world_size, int rank, int device, const void* id, void** comm);
+TBIK_API tbik_status tbik_nccl_comm_destroy(void* comm);
+/* The status-quo row-parallel layer per rank (SURVEY 8(b) tbik_baseline_cublas_nccl):
+ * cuBLAS GEMM of this rank's shard X_shard [M x K_r] . W_shard [K_r x N], then an
+ * NCCL sum all-reduce into Y [M x N] (dense).  out_f32 = 1: f32 GEMM output and f32
+ * all-reduce (the same bytes on the wire as the TBIK tree all-reduce); 0: bf16
+ * output and bf16 all-reduce (what a serving stack does).  Y is f32 or bf16
+ * accordingly.  The summation order is NCCL's: not TP-invariant. */
+TBIK_API tbik_status tbik_baseline_cublas_nccl(void* comm, const void* X_shard, int x_dtype, int64_t ldx,
+                                               const void* W_shard, int w_dtype, int64_t ldw, void* Y, int64_t M,
+                                               int64_t N, int64_t K_shard, int out_f32, void* stream);
+
 /* ---- one-process-per-GPU groups (NVLink peer memory) -------------------- */
 
 /* A DeviceGroup (collective.hpp:15-23) whose ranks are processes, one per GPU.
@@ -222,6 +289,28 @@ TBIK_API tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* 
                                             int64_t N, int64_t K_global,
                                             const tbik_block_config* cfg, int64_t c_max,
                                             int leaf_mode, void* stream);
+
+/* A group-wide barrier (one epoch, no payload): returns once enqueued; the
+ * stream continues only after every rank reached it. */
+TBIK_API tbik_status tbik_group_barrier(tbik_group* g, void* stream);
+
+/* all_gather (collective.hpp:27-28, collective.cpp:46-50) as the column-parallel
+ * concatenation (layers.cpp:61-70): rank q's [rows x cols] block (elem_bytes 2
+ * for bf16, 4 for f32; row stride ld_local elements) lands in columns
+ * [q*cols, (q+1)*cols) of out [rows x W*cols] (row stride ld_out) on EVERY rank.
+ * Rank-indexed, never arrival-ordered; rows beyond the group capacity are moved
+ * in several epochs (every rank must pass the same rows / cols). */
+TBIK_API tbik_status tbik_group_all_gather(tbik_group* g, const void* local, int64_t rows, int64_t cols,
+                                           int64_t ld_local, int elem_bytes, void* out, int64_t ld_out,
+                                           void* stream);
+
+/* Cross-rank step of the vocab-sharded tree log-softmax (tbik_logsoftmax_merge
+ * over the group): this rank's ms_local [rows x 2] f32 (tbik_logsoftmax_shard_state
+ * of its vocab shard) is exchanged -- 8 bytes per row -- and every rank merges
+ * the W states in rank order with the contiguous-halves tree into lse[rows]
+ * (bit-identical to tbik_tree_logsoftmax_local with tp = W simulated shards). */
+TBIK_API tbik_status tbik_group_logsoftmax_merge(tbik_group* g, const float* ms_local, int64_t rows, float* lse,
+                                                 void* stream);
 
 /* ---- host-buffer entry points (the reference's Matrix in / Matrix out) ---- */
 

@@ -105,6 +105,9 @@ _SIGS = {
     "tbik_group_row_parallel_forward_hostio": (ci, [vp, vp, ci, i64, vp, ci, i64, PF, i64, i64, i64, i64, i64,
                                                     PCFG, i64, ci, i64, vp]),
     "tbik_group_tree_all_reduce": (ci, [vp, PF, PF, i64, vp]),
+    "tbik_group_barrier": (ci, [vp, vp]),
+    "tbik_group_all_gather": (ci, [vp, vp, i64, i64, i64, ci, vp, i64, vp]),
+    "tbik_group_logsoftmax_merge": (ci, [vp, PF, i64, PF, vp]),
     "tbik_group_row_parallel_forward": (ci, [vp, vp, ci, i64, vp, ci, i64, PF, i64, i64, i64, i64,
                                              PCFG, i64, ci, vp]),
     "tbik_tree_rmsnorm": (ci, [vp, ci, i64, PF, C.c_float, vp, ci, i64, i64, i64, vp]),

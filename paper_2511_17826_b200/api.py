@@ -429,6 +429,53 @@ class PeerGroup:
                                              C.c_void_p(out.data_ptr()), partial.numel(), _stream()))
         return out
 
+    def barrier(self) -> None:
+        """Device-side barrier over the group (stream-ordered)."""
+        check(lib.tbik_group_barrier(self._h, _stream()))
+
+    def all_gather(self, local, out=None):
+        """all_gather as the column-parallel concatenation (layers.cpp:61-70): rank q's
+        [rows x cols] block (bf16 or f32) -> columns [q*cols, (q+1)*cols) of
+        out [rows x W*cols] on every rank."""
+        torch = _torch()
+        p, _, ld = _mat(local, "local")
+        rows, cols = local.shape
+        out = torch.empty((rows, cols * self.world), dtype=local.dtype, device=local.device) if out is None else out
+        if out.dtype != local.dtype or out.shape[0] != rows or out.shape[1] < cols * self.world:
+            raise TbikError(ErrorCode.ShapeMismatch, "all_gather: out must be [rows, W*cols] of the same dtype")
+        po, _, ldo = _mat(out, "out")
+        check(lib.tbik_group_all_gather(self._h, p, rows, cols, ld, local.element_size(), po, ldo, _stream()))
+        return out
+
+    def log_softmax(self, logits_shard, groups_local: int, v_offset: int, targets=None, full: bool = True):
+        """Vocab-sharded tree log-softmax over the group: this rank's logits
+        [rows x V/W] (its column shard of the vocabulary, `groups_local` = G/W of the
+        canonical vocab groups) -> (lse[rows] identical on every rank, this rank's
+        log-prob columns or None, target log-probs of the targets in this shard or
+        None).  8 bytes per row cross ranks; bit-identical to log_softmax(tp=W)."""
+        torch = _torch()
+        rows, vl = logits_shard.shape
+        pl, dl, ld = _mat(logits_shard, "logits")
+        if dl != F32:
+            raise TbikError(ErrorCode.UnknownDtype, "log_softmax expects f32 logits")
+        dev = logits_shard.device
+        ms = torch.empty((rows, 2), dtype=torch.float32, device=dev)
+        check(lib.tbik_logsoftmax_shard_state(pl, ld, rows, vl, groups_local, C.c_void_p(ms.data_ptr()), _stream()))
+        lse = torch.empty(rows, dtype=torch.float32, device=dev)
+        check(lib.tbik_group_logsoftmax_merge(self._h, C.c_void_p(ms.data_ptr()), rows, C.c_void_p(lse.data_ptr()),
+                                              _stream()))
+        lp = torch.empty((rows, vl), dtype=torch.float32, device=dev) if full else None
+        tlp = tg = None
+        if targets is not None:
+            tg = targets.to(torch.int64).contiguous()
+            tlp = torch.full((rows,), float("nan"), dtype=torch.float32, device=dev)
+        if lp is not None or tlp is not None:
+            check(lib.tbik_logsoftmax_finish(pl, ld, rows, vl, C.c_void_p(lse.data_ptr()),
+                                             C.c_void_p(lp.data_ptr()) if lp is not None else None, vl,
+                                             C.c_void_p(tg.data_ptr()) if tg is not None else None, v_offset,
+                                             C.c_void_p(tlp.data_ptr()) if tlp is not None else None, _stream()))
+        return lse, lp, tlp
+
     def row_parallel_forward(self, x_shard, w_shard, K_global: int, cfg: BlockConfig | None = None,
                              c_max: int = 8, leaf: int = LEAF_TCGEN05, out=None):
         cfg = cfg or default_block_config(BF16)

@@ -219,6 +219,16 @@ tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mod
   return launch_tree_combine(ws, X, leaves ? v.kf : 1, v.M, v.N, C, ldc, s);
 }
 
+tbik_status make_view(const void* A, int adt, int64_t lda, const void* B, int bdt, int64_t ldb, int64_t M,
+                      int64_t N, int64_t K, int64_t bk, int64_t kf_global, GemmView* v) {
+  // Local plan of this view with the given (global) k_first, c_max = 1
+  // (matmul.cpp:153 via layers.cpp:85-88).
+  tbik_reduction_plan p;
+  TBIK_TRY(plan(K, bk, kf_global, 1, &p));
+  *v = GemmView{A, adt, lda, B, bdt, ldb, M, N, K, bk, p.k_first, p.tiles_total, p.leaves};
+  return TBIK_OK;
+}
+
 namespace {
 
 tbik_status check_mat(const void* p, int dt, int64_t rows, int64_t cols, int64_t ld, const char* name) {
@@ -227,16 +237,6 @@ tbik_status check_mat(const void* p, int dt, int64_t rows, int64_t cols, int64_t
   if (dt != TBIK_F32 && dt != TBIK_BF16) return set_error(TBIK_UNKNOWN_DTYPE, std::string(name) + ": dtype");
   if (ld < cols) return set_error(TBIK_BAD_ARGUMENT, std::string(name) + ": leading dimension < cols");
   if (!p) return set_error(TBIK_BAD_ARGUMENT, std::string(name) + ": null pointer");
-  return TBIK_OK;
-}
-
-tbik_status make_view(const void* A, int adt, int64_t lda, const void* B, int bdt, int64_t ldb, int64_t M,
-                      int64_t N, int64_t K, int64_t bk, int64_t kf_global, GemmView* v) {
-  // Local plan of this view with the given (global) k_first, c_max = 1
-  // (matmul.cpp:153 via layers.cpp:85-88).
-  tbik_reduction_plan p;
-  TBIK_TRY(plan(K, bk, kf_global, 1, &p));
-  *v = GemmView{A, adt, lda, B, bdt, ldb, M, N, K, bk, p.k_first, p.tiles_total, p.leaves};
   return TBIK_OK;
 }
 

@@ -37,6 +37,29 @@ void* workspace(size_t bytes, int slot = 0);
 // Counts every kernel launch issued by the library (tbik_launch_count).
 void count_launch();
 
+// ---- cross-process flags (NVLink peer memory) --------------------------------
+// Release / acquire at system scope: a flag store is ordered after this
+// thread's earlier global stores, a flag load before its later loads.
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Waits until *f reached `epoch` (wrap-safe).  Every cross-rank wait of the
+// library goes through here, so a peer that never arrives (a dead process, a
+// rank that took a different code path) ends in a trap -- a reported CUDA error
+// -- after ~17 s instead of a hung GPU.
+__device__ __forceinline__ void spin_until_epoch(const uint32_t* f, uint32_t epoch) {
+  long long n = 0;
+  while (static_cast<int32_t>(ld_acquire_sys(f) - epoch) < 0) {
+    __nanosleep(128);
+    if (++n > (1ll << 27)) __trap();
+  }
+}
+
 // ---- numerics (numerics.hpp:21-62) -----------------------------------------
 // Every f32 operation on the reduction path is an explicit round-to-nearest
 // intrinsic; the library is additionally compiled with -fmad=false so nvcc

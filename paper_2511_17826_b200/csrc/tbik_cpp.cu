@@ -1,11 +1,14 @@
-// tbik_cpp.cu -- host implementation of the C++ mirror (include/tbik_b200/tbik.hpp).
+// tbik_cpp.cu -- host implementation of the drop-in C++ API (include/tbik/*.hpp,
+// the reference's proj/include/tbik/ declarations).
 //
 // Matrix / Rng / fingerprint semantics restate the reference's
-// (matrix.cpp:11-181); every compute entry uploads operands to the current
-// CUDA device, calls the C ABI (tbik_b200.h) and downloads the result.  Errors
-// come back as tbik::TbikError with the reference's ErrorCode.
+// (matrix.cpp:11-181); every compute entry uploads operands to the device(s)
+// of the DeviceGroup, calls the C ABI (tbik_b200.h) and downloads the result.
+// Errors come back as tbik::TbikError with the reference's ErrorCode.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -221,11 +224,43 @@ BlockConfig default_block_config(Dtype dtype) {
 
 bool is_power_of_two(std::int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 
+std::int64_t log2_exact(std::int64_t v) {  // matmul.cpp:18-22
+  std::int64_t l = 0;
+  while ((std::int64_t{1} << l) < v) ++l;
+  return l;
+}
+
+namespace {
+std::atomic<int> g_default_leaf{static_cast<int>(Leaf::Fma)};  // the reference's bits unless asked otherwise
+}
+void set_default_leaf(Leaf leaf) { g_default_leaf.store(static_cast<int>(leaf)); }
+Leaf default_leaf() { return static_cast<Leaf>(g_default_leaf.load()); }
+
+float leaf_dot(const float* a, const float* b, std::int64_t n) {
+  if (n < 0) fail(ErrorCode::BadDimension, "leaf_dot: n must be >= 0");
+  const std::size_t bytes = static_cast<std::size_t>(n) * 4;
+  DevBuf da(bytes), db(bytes), dout(4);
+  if (n > 0) {
+    cuda_ok(cudaMemcpy(da.p, a, bytes, cudaMemcpyHostToDevice), "upload");
+    cuda_ok(cudaMemcpy(db.p, b, bytes, cudaMemcpyHostToDevice), "upload");
+  }
+  check_status(tbik_leaf_dot(static_cast<const float*>(da.p), static_cast<const float*>(db.p), n,
+                             static_cast<float*>(dout.p), nullptr));
+  check_status(tbik_sync(nullptr));
+  float r = 0.0f;
+  cuda_ok(cudaMemcpy(&r, dout.p, 4, cudaMemcpyDeviceToHost), "download");
+  return r;
+}
+
 ReductionPlan plan_blocks(std::int64_t K, const BlockConfig& cfg, std::int64_t c_max) {
   tbik_block_config c = c_cfg(cfg);
   tbik_reduction_plan p;
   check_status(tbik_plan_blocks(K, &c, c_max, &p));
   return ReductionPlan{p.tiles_total, p.k_first, p.leaves, p.depth};
+}
+
+Matrix tree_matmul(const Matrix& a, const Matrix& b, const BlockConfig& cfg) {
+  return tree_matmul(a, b, cfg, default_leaf());
 }
 
 Matrix tree_matmul(const Matrix& a, const Matrix& b, const BlockConfig& cfg, Leaf leaf) {
@@ -246,9 +281,46 @@ Matrix tree_matmul(const Matrix& a, const Matrix& b, const BlockConfig& cfg, Lea
 }
 
 // ---- collective.hpp --------------------------------------------------------------------
+namespace {
+int sm100_device_count() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+}  // namespace
+
 DeviceGroup::DeviceGroup(int world_size) : world_size_(world_size) {
   if (!is_power_of_two(world_size))
     fail(ErrorCode::BadWorldSize, "world size must be a power of two, got " + std::to_string(world_size));
+  // rank r on device r % device_count: DeviceGroup(8) spans the eight GPUs of an
+  // HGX node and is the reference's simulated group on a one-GPU machine.
+  const int n = sm100_device_count();
+  for (int r = 0; r < world_size; ++r) devices_.push_back(n > 0 ? r % n : 0);
+}
+
+DeviceGroup::DeviceGroup(int world_size, std::vector<int> devices) : world_size_(world_size), devices_(std::move(devices)) {
+  if (!is_power_of_two(world_size))
+    fail(ErrorCode::BadWorldSize, "world size must be a power of two, got " + std::to_string(world_size));
+  if (static_cast<int>(devices_.size()) != world_size)
+    fail(ErrorCode::BadArgument, "DeviceGroup: one device id per rank expected");
+}
+
+int DeviceGroup::device_span() const {
+  std::vector<int> d(devices_);
+  std::sort(d.begin(), d.end());
+  return static_cast<int>(std::unique(d.begin(), d.end()) - d.begin());
+}
+
+tbik_local_group* DeviceGroup::native() const {
+  if (!native_) {
+    tbik_local_group* g = nullptr;
+    check_status(tbik_local_group_create(world_size_, devices_.data(), &g));
+    native_ = std::shared_ptr<tbik_local_group>(g, [](tbik_local_group* p) { tbik_local_group_destroy(p); });
+  }
+  return native_.get();
 }
 
 std::vector<Matrix> all_gather(const DeviceGroup& group, const std::vector<Matrix>& xs) {
@@ -286,28 +358,124 @@ ShardPlan make_row_shard_plan(std::int64_t k, const BlockConfig& cfg, int tp, st
   return s;
 }
 
+namespace {
+struct DeviceScope {  // restores the caller's current device
+  int prev = 0;
+  DeviceScope() { cudaGetDevice(&prev); }
+  ~DeviceScope() { cudaSetDevice(prev); }
+};
+}  // namespace
+
+Matrix column_parallel_forward(const Matrix& x, const Matrix& w, const DeviceGroup& group, const BlockConfig& cfg) {
+  return column_parallel_forward(x, w, group, cfg, default_leaf());
+}
+
 Matrix column_parallel_forward(const Matrix& x, const Matrix& w, const DeviceGroup& group, const BlockConfig& cfg,
                                Leaf leaf) {
   if (x.cols() != w.rows()) fail(ErrorCode::ShapeMismatch, "column_parallel_forward: inner dimensions differ");
-  DevBuf dx = upload(x), dw = upload(w), dy(static_cast<std::size_t>(x.rows() * w.cols()) * 4);
+  DeviceScope scope;
   tbik_block_config c = c_cfg(cfg);
-  check_status(tbik_column_parallel_forward_local(dx.p, static_cast<int>(x.dtype()), x.cols(), dw.p,
-                                                  static_cast<int>(w.dtype()), w.cols(), static_cast<float*>(dy.p),
-                                                  w.cols(), x.rows(), w.cols(), x.cols(), group.world_size(), &c,
-                                                  static_cast<int>(leaf), nullptr));
-  check_status(tbik_sync(nullptr));
-  return download_f32(dy, x.rows(), w.cols());
+  if (group.device_span() <= 1) {
+    cuda_ok(cudaSetDevice(group.devices()[0]), "cudaSetDevice");
+    DevBuf dx = upload(x), dw = upload(w), dy(static_cast<std::size_t>(x.rows() * w.cols()) * 4);
+    check_status(tbik_column_parallel_forward_local(dx.p, static_cast<int>(x.dtype()), x.cols(), dw.p,
+                                                    static_cast<int>(w.dtype()), w.cols(), static_cast<float*>(dy.p),
+                                                    w.cols(), x.rows(), w.cols(), x.cols(), group.world_size(), &c,
+                                                    static_cast<int>(leaf), nullptr));
+    check_status(tbik_sync(nullptr));
+    return download_f32(dy, x.rows(), w.cols());
+  }
+  // ranks on their own GPUs: rank r computes its column block on devices()[r]
+  // (layers.cpp:48-72); the concatenation is the column offset of the download.
+  const ShardPlan plan = make_column_shard_plan(w.cols(), group.world_size());
+  Matrix out(x.rows(), w.cols(), Dtype::F32);
+  for (int r = 0; r < group.world_size(); ++r) {
+    const auto [b, e] = plan.bounds[static_cast<std::size_t>(r)];
+    cuda_ok(cudaSetDevice(group.devices()[static_cast<std::size_t>(r)]), "cudaSetDevice");
+    DevBuf dx = upload(x), dw = upload(w.slice_cols(b, e)), dy(static_cast<std::size_t>(x.rows() * (e - b)) * 4);
+    check_status(tbik_tree_matmul(dx.p, static_cast<int>(x.dtype()), x.cols(), dw.p, static_cast<int>(w.dtype()),
+                                  e - b, static_cast<float*>(dy.p), e - b, x.rows(), e - b, x.cols(), &c,
+                                  static_cast<int>(leaf), nullptr));
+    check_status(tbik_sync(nullptr));
+    cuda_ok(cudaMemcpy2D(out.f32_data().data() + b, static_cast<std::size_t>(w.cols()) * 4, dy.p,
+                         static_cast<std::size_t>(e - b) * 4, static_cast<std::size_t>(e - b) * 4,
+                         static_cast<std::size_t>(x.rows()), cudaMemcpyDeviceToHost),
+            "download");
+  }
+  return out;
+}
+
+Matrix row_parallel_forward(const Matrix& x, const Matrix& w, const DeviceGroup& group, const BlockConfig& cfg,
+                            std::int64_t c_max) {
+  return row_parallel_forward(x, w, group, cfg, c_max, default_leaf());
 }
 
 Matrix row_parallel_forward(const Matrix& x, const Matrix& w, const DeviceGroup& group, const BlockConfig& cfg,
                             std::int64_t c_max, Leaf leaf) {
   if (x.cols() != w.rows()) fail(ErrorCode::ShapeMismatch, "row_parallel_forward: inner dimensions differ");
-  DevBuf dx = upload(x), dw = upload(w), dy(static_cast<std::size_t>(x.rows() * w.cols()) * 4);
+  DeviceScope scope;
   tbik_block_config c = c_cfg(cfg);
-  check_status(tbik_row_parallel_forward_local(dx.p, static_cast<int>(x.dtype()), x.cols(), dw.p,
-                                               static_cast<int>(w.dtype()), w.cols(), static_cast<float*>(dy.p),
-                                               w.cols(), x.rows(), w.cols(), x.cols(), group.world_size(), &c, c_max,
-                                               static_cast<int>(leaf), nullptr));
+  if (group.device_span() <= 1) {
+    cuda_ok(cudaSetDevice(group.devices()[0]), "cudaSetDevice");
+    DevBuf dx = upload(x), dw = upload(w), dy(static_cast<std::size_t>(x.rows() * w.cols()) * 4);
+    check_status(tbik_row_parallel_forward_local(dx.p, static_cast<int>(x.dtype()), x.cols(), dw.p,
+                                                 static_cast<int>(w.dtype()), w.cols(), static_cast<float*>(dy.p),
+                                                 w.cols(), x.rows(), w.cols(), x.cols(), group.world_size(), &c, c_max,
+                                                 static_cast<int>(leaf), nullptr));
+    check_status(tbik_sync(nullptr));
+    return download_f32(dy, x.rows(), w.cols());
+  }
+  // ranks on their own GPUs (layers.cpp:74-98): rank r's K shard goes to
+  // devices()[r], its tree GEMM runs there, and rank 0's device reduces the W
+  // partials over peer memory (NVLink) in Algorithm-2 order.
+  const ShardPlan plan = make_row_shard_plan(x.cols(), cfg, group.world_size(), c_max);
+  tbik_local_group* lg = group.native();
+  std::vector<std::unique_ptr<DevBuf>> bufs;
+  std::vector<const void*> xs, ws;
+  std::vector<std::int64_t> ldx, ldw;
+  for (int r = 0; r < group.world_size(); ++r) {
+    const auto [b, e] = plan.bounds[static_cast<std::size_t>(r)];
+    cuda_ok(cudaSetDevice(group.devices()[static_cast<std::size_t>(r)]), "cudaSetDevice");
+    bufs.emplace_back(new DevBuf(upload(x.slice_cols(b, e))));
+    xs.push_back(bufs.back()->p);
+    bufs.emplace_back(new DevBuf(upload(w.slice_rows(b, e))));
+    ws.push_back(bufs.back()->p);
+    ldx.push_back(e - b);
+    ldw.push_back(w.cols());
+  }
+  cuda_ok(cudaSetDevice(group.devices()[0]), "cudaSetDevice");
+  DevBuf dy(static_cast<std::size_t>(x.rows() * w.cols()) * 4);
+  check_status(tbik_local_group_row_parallel_forward(lg, xs.data(), static_cast<int>(x.dtype()), ldx.data(), ws.data(),
+                                                     static_cast<int>(w.dtype()), ldw.data(), static_cast<float*>(dy.p),
+                                                     w.cols(), x.rows(), w.cols(), x.cols(), &c, c_max,
+                                                     static_cast<int>(leaf), nullptr));
+  check_status(tbik_sync(nullptr));
+  return download_f32(dy, x.rows(), w.cols());
+}
+
+// The status quo (layers.cpp:100-146): cuBLAS per rank + ring reduce / concat.
+Matrix baseline_row_parallel_forward(const Matrix& x, const Matrix& w, const DeviceGroup& group) {
+  if (x.cols() != w.rows()) fail(ErrorCode::ShapeMismatch, "baseline_row_parallel_forward: inner dimensions differ");
+  DeviceScope scope;
+  cuda_ok(cudaSetDevice(group.devices()[0]), "cudaSetDevice");
+  DevBuf dx = upload(x), dw = upload(w), dy(static_cast<std::size_t>(x.rows() * w.cols()) * 4);
+  check_status(tbik_baseline_row_parallel_forward_local(dx.p, static_cast<int>(x.dtype()), x.cols(), dw.p,
+                                                        static_cast<int>(w.dtype()), w.cols(), static_cast<float*>(dy.p),
+                                                        w.cols(), x.rows(), w.cols(), x.cols(), group.world_size(),
+                                                        nullptr));
+  check_status(tbik_sync(nullptr));
+  return download_f32(dy, x.rows(), w.cols());
+}
+
+Matrix baseline_column_parallel_forward(const Matrix& x, const Matrix& w, const DeviceGroup& group) {
+  if (x.cols() != w.rows()) fail(ErrorCode::ShapeMismatch, "baseline_column_parallel_forward: inner dimensions differ");
+  DeviceScope scope;
+  cuda_ok(cudaSetDevice(group.devices()[0]), "cudaSetDevice");
+  DevBuf dx = upload(x), dw = upload(w), dy(static_cast<std::size_t>(x.rows() * w.cols()) * 4);
+  check_status(tbik_baseline_column_parallel_forward_local(dx.p, static_cast<int>(x.dtype()), x.cols(), dw.p,
+                                                           static_cast<int>(w.dtype()), w.cols(),
+                                                           static_cast<float*>(dy.p), w.cols(), x.rows(), w.cols(),
+                                                           x.cols(), group.world_size(), nullptr));
   check_status(tbik_sync(nullptr));
   return download_f32(dy, x.rows(), w.cols());
 }
@@ -321,6 +489,14 @@ Matrix rmsnorm(const Matrix& x, const std::vector<float>& gamma, float eps) {
   cuda_ok(cudaMemcpy(dg.p, gamma.data(), gamma.size() * 4, cudaMemcpyHostToDevice), "upload gamma");
   check_status(tbik_tree_rmsnorm(dx.p, static_cast<int>(x.dtype()), x.cols(), static_cast<const float*>(dg.p), eps,
                                  dy.p, TBIK_F32, x.cols(), x.rows(), x.cols(), nullptr));
+  check_status(tbik_sync(nullptr));
+  return download_f32(dy, x.rows(), x.cols());
+}
+
+Matrix silu(const Matrix& x) {  // demo.cpp:36-45 with the library's exp
+  DevBuf dx = upload(x), dy(static_cast<std::size_t>(x.size()) * 4);
+  check_status(tbik_silu(dx.p, static_cast<int>(x.dtype()), x.cols(), x.rows(), x.cols(), static_cast<float*>(dy.p),
+                         x.cols(), nullptr));
   check_status(tbik_sync(nullptr));
   return download_f32(dy, x.rows(), x.cols());
 }

@@ -271,22 +271,6 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_complete() {  // all but the N most recent groups WRITTEN
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-// Bounded spin: a peer that never arrives traps (a CUDA error) instead of hanging.
-__device__ __forceinline__ void spin_until_epoch(const uint32_t* f, uint32_t epoch) {
-  long long n = 0;
-  while (static_cast<int32_t>(ld_acquire_sys(f) - epoch) < 0) {
-    __nanosleep(128);
-    if (++n > (1ll << 27)) __trap();
-  }
-}
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -1104,8 +1088,35 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   // Fused GEMM -> tree all-reduce (tbik_group.cu) for FULL pair-tile launches whose
   // output is the group's send slot.
   if (FusedAr* ar = g_fused_ar) {
-    const bool ok = pair && !mc && abox == 128 && o.mode == OUT_FULL && !o.act && p.tma_store && o.ldo == v.N && ar->W > 1 &&
+    bool ok = pair && !mc && abox == 128 && o.mode == OUT_FULL && !o.act && p.tma_store && o.ldo == v.N && ar->W > 1 &&
                     ar->W <= 8 && p.items * 2 * ar->W <= ar->flag_capacity && o.out == ar->src[ar->rank];
+    // Every CTA pair of every rank spins on peer tile flags before it exits, so
+    // the whole grid must be co-resident: cap at the clusters the occupancy
+    // calculator says fit (a static property of kernel and device, the same on
+    // every rank); a grid that would not fit takes the separate path instead.
+    static int max_ar_clusters[16] = {};
+    int adev = 0;
+    cudaGetDevice(&adev);
+    if (ok && adev >= 0 && adev < 16 && !max_ar_clusters[adev]) {
+      auto k = tc_tree_gemm_kernel<8, false, 128, true, false, false, true>;
+      const size_t sm = smem_bytes(8, 128, true, false);
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+      cudaLaunchConfig_t qc{};
+      qc.gridDim = dim3(2);
+      qc.blockDim = dim3(128 + 32 * 8);
+      qc.dynamicSmemBytes = sm;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = 2;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      qc.attrs = qa;
+      qc.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, k, &qc) != cudaSuccess || n < 1) n = 1;
+      max_ar_clusters[adev] = n;
+    }
+    if (ok && adev >= 0 && adev < 16 && nstreams > max_ar_clusters[adev]) ok = false;
     if (ok) {
       p.ar_W = ar->W;
       p.ar_rank = ar->rank;

@@ -100,15 +100,6 @@ struct GroupPtrs {
   uint32_t* done[8];     // done[] array of every rank (peer-mapped)
 };
 
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
 // Barrier A: publish "epoch ready" to every peer (block 0), wait for all W.
 __device__ __forceinline__ void barrier_ready(const GroupPtrs& g, int W, int rank, uint32_t epoch) {
   if (blockIdx.x == 0 && threadIdx.x < W) {
@@ -117,9 +108,7 @@ __device__ __forceinline__ void barrier_ready(const GroupPtrs& g, int W, int ran
   }
   if (threadIdx.x == 0) {
     const uint32_t* mine = g.flags[rank];
-    for (int r = 0; r < W; ++r)
-      while (static_cast<int32_t>(ld_acquire_sys(mine + r) - epoch) < 0) {
-      }
+    for (int r = 0; r < W; ++r) spin_until_epoch(mine + r, epoch);
   }
   __syncthreads();
 }
@@ -203,9 +192,7 @@ __global__ void group_gather_wait_copy_kernel(const uint32_t* done, int W, uint3
                                               const float* __restrict__ result, float* __restrict__ out,
                                               int64_t elems) {
   if (threadIdx.x == 0)
-    for (int r = 0; r < W; ++r)
-      while (static_cast<int32_t>(ld_acquire_sys(done + r) - epoch) < 0) {
-      }
+    for (int r = 0; r < W; ++r) spin_until_epoch(done + r, epoch);
   __syncthreads();
   if (result == out) return;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -215,6 +202,30 @@ __global__ void group_gather_wait_copy_kernel(const uint32_t* done, int W, uint3
       reinterpret_cast<float4*>(out)[i] = reinterpret_cast<const float4*>(result)[i];
   } else {
     for (int64_t i = t0; i < elems; i += stride) out[i] = result[i];
+  }
+}
+
+// Barrier A alone (one CTA): used by the collectives whose consumer kernel is a
+// plain launcher reading the peers' send slots (all-gather, (m, s) merge).
+__global__ void group_barrier_kernel(GroupPtrs g, int W, int rank, uint32_t epoch) {
+  barrier_ready(g, W, rank, epoch);
+}
+
+// All-gather (collective.cpp:46-50, layers.cpp:61-70): rank q's block sits dense
+// in its send slot ([rows][row_units] of U); out[row][q * row_units + j] = it.
+// blockIdx.y = source rank (staggered: rank r starts with r+1, own block last,
+// so the W-1 NVLink reads of a step go to W-1 different peers).
+template <typename U>
+__global__ void group_gather_copy_kernel(GroupPtrs g, int W, int rank, int64_t rows, int64_t row_units,
+                                         U* __restrict__ out, int64_t ld_out_units) {
+  const int q = (rank + 1 + static_cast<int>(blockIdx.y)) & (W - 1);
+  const U* __restrict__ src = reinterpret_cast<const U*>(g.src[q]);
+  U* dst = out + static_cast<int64_t>(q) * row_units;
+  const int64_t n = rows * row_units;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t r = i / row_units, c = i - r * row_units;
+    dst[r * ld_out_units + c] = __ldcg(src + i);  // L2 / NVLink, never a stale L1 line
   }
 }
 
@@ -318,8 +329,54 @@ float* tbik_group_send_buffer(tbik_group* g) {
 namespace {
 // max_blocks > 0 bounds every collective kernel's grid (the CTAs that can run
 // beside a GEMM occupying the other SMs).
+tbik_status check_group_operands(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_t M, int64_t N,
+                                 int64_t Kr) {
+  if (!X || !W) return set_error(TBIK_BAD_ARGUMENT, "null operand");
+  if (M < 1 || N < 1 || Kr < 1) return set_error(TBIK_BAD_DIMENSION, "dimensions must be >= 1");
+  if (ldx < Kr || ldw < N) return set_error(TBIK_BAD_ARGUMENT, "leading dimension too small");
+  return TBIK_OK;
+}
+
+GroupPtrs group_ptrs(tbik_group* g, uint32_t epoch) {
+  GroupPtrs gp{};
+  for (int r = 0; r < g->W; ++r) {
+    gp.src[r] = slot_ptr(g->peer_region[r], g->capacity, epoch);
+    gp.dst[r] = result_ptr(g->peer_region[r], g->capacity, epoch);
+    gp.flags[r] = ready_flags(g->peer_region[r], g->capacity);
+    gp.done[r] = done_flags(g->peer_region[r], g->capacity);
+  }
+  return gp;
+}
+
+// One "publish" epoch: this rank's `rows` x `row_bytes` block (row stride
+// ld_bytes) is copied densely into its send slot, then barrier A.  Afterwards
+// every peer's block of the same epoch is readable through *gp.  Slot reuse
+// follows the epoch argument at the top of this file (a rank writes slot e & 1
+// again only after barrier A of e+1, which every peer enters after its consumer
+// of epoch e finished, in stream order).
+tbik_status group_publish(tbik_group* g, const void* src, int64_t rows, int64_t row_bytes, int64_t ld_bytes,
+                          cudaStream_t s, GroupPtrs* gp) {
+  for (int r = 0; r < g->W; ++r)
+    if (!g->peer_region[r]) return set_error(TBIK_COLLECTIVE_MISMATCH, "peers not opened");
+  if (rows * row_bytes > g->capacity * static_cast<int64_t>(sizeof(float)))
+    return set_error(TBIK_COLLECTIVE_MISMATCH, "block exceeds group capacity");
+  const uint32_t epoch = ++g->epoch;
+  void* mine = slot_ptr(g->region, g->capacity, epoch);
+  if (rows > 0 && row_bytes > 0)
+    TBIK_CUDA(cudaMemcpy2DAsync(mine, row_bytes, src, ld_bytes, row_bytes, rows, cudaMemcpyDeviceToDevice, s));
+  *gp = group_ptrs(g, epoch);
+  group_barrier_kernel<<<1, 32, 0, s>>>(*gp, g->W, g->rank, epoch);
+  TBIK_CUDA(cudaGetLastError());
+  count_launch();
+  return TBIK_OK;
+}
+
+// force_two_phase: the overlapped chunk pipeline reuses a send slot as soon as
+// THIS rank's all-reduce of the slot finished, which proves every peer finished
+// reading it only on the two-phase path (its done flags); it must not take the
+// one-shot path whatever TBIK_AR_TWO_PHASE_BYTES says.
 tbik_status group_all_reduce(tbik_group* g, const float* partial, float* out, int64_t elems, cudaStream_t s,
-                             int64_t max_blocks) {
+                             int64_t max_blocks, bool force_two_phase = false) {
   if (!g || !out) return set_error(TBIK_BAD_ARGUMENT, "null argument");
   if (elems < 0 || elems > g->capacity) return set_error(TBIK_COLLECTIVE_MISMATCH, "elems exceed group capacity");
   for (int r = 0; r < g->W; ++r)
@@ -340,7 +397,7 @@ tbik_status group_all_reduce(tbik_group* g, const float* partial, float* out, in
     return e && *e ? std::atoll(e) : kTwoPhaseBytes;
   }();
   // The path must be the same on every rank: it depends only on (W, elems).
-  if (g->W > 1 && elems % 4 == 0 && elems * 4 >= two_phase_bytes) {
+  if (g->W > 1 && elems % 4 == 0 && (force_two_phase || elems * 4 >= two_phase_bytes)) {
     const int64_t n4 = elems / 4;
     const int64_t lo = n4 * g->rank / g->W, hi = n4 * (g->rank + 1) / g->W;
     int64_t blocks = (hi - lo + 255) / 256;
@@ -396,17 +453,20 @@ tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* X_shard, 
   // straight from the peers' slots and push the result into every rank's result
   // slot -- the NVLink traffic overlaps the tensor-core work of the same kernel.  A
   // short wait kernel then copies the result slot to Y once all W ranks are done.
-  // Taken when the GEMM is one FULL pair-tile launch (M > 128, >= 7/8 of the CTA
-  // pairs busy); otherwise the partial already sits in the send slot and the
-  // regular tree all-reduce runs.  The choice depends only on (M, N, K / W), i.e.
-  // it is the same on every rank.
+  // Every rank must take the same path, so the choice uses only values that are
+  // equal on every rank -- (M, N, leaf mode, W) -- never this rank's K range (the
+  // last rank of a ragged K has fewer tiles, and the K-split / skinny heuristics
+  // of tbik_tree_matmul look at it): M > 128 (pair tiles), N % 4 == 0 (TMA store).
+  // The GEMM is then launched as ONE FULL-mode pair-tile launch on every rank.
   static const bool fused_on = [] {
     const char* e = std::getenv("TBIK_GROUP_FUSED");
     return !(e && *e && std::atoi(e) == 0);
   }();
-  if (fused_on && g->W > 1 && leaf_mode == TBIK_LEAF_TCGEN05) {
+  if (fused_on && g->W > 1 && leaf_mode == TBIK_LEAF_TCGEN05 && M > 128 && N % 4 == 0 &&
+      x_dtype == TBIK_BF16 && w_dtype == TBIK_BF16) {
     for (int r = 0; r < g->W; ++r)
       if (!g->peer_region[r]) return set_error(TBIK_COLLECTIVE_MISMATCH, "peers not opened");
+    TBIK_TRY(check_group_operands(X_shard, ldx, W_shard, ldw, M, N, Kr));
     const uint32_t epoch = g->epoch + 1;
     FusedAr ar;
     ar.W = g->W;
@@ -421,11 +481,15 @@ tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* X_shard, 
     ar.counter = fused_counter(g->region, g->capacity);
     ar.flag_capacity = tile_flag_words(g->capacity, g->W);
     float* send = slot_ptr(g->region, g->capacity, epoch);
+    GemmView v;
+    TBIK_TRY(make_view(X_shard, x_dtype, ldx, W_shard, w_dtype, ldw, M, N, Kr, local.block_k, local.k_first, &v));
     FusedAr* prev = set_tc_fused_ar(&ar);
-    const tbik_status st =
-        tbik_tree_matmul(X_shard, x_dtype, ldx, W_shard, w_dtype, ldw, send, N, M, N, Kr, &local, leaf_mode, stream);
+    const tbik_status st = launch_tc_gemm(v, GemmOut{OUT_FULL, v.T, send, N, 0}, s);
     set_tc_fused_ar(prev);
     TBIK_TRY(st);
+    // launch_tc_gemm declines the fused form only for rank-uniform reasons (a grid
+    // whose clusters cannot all be co-resident, an experiment knob): then every
+    // rank has its partial in the send slot and runs the regular all-reduce.
     if (!ar.used) return group_all_reduce(g, send, Y, M * N, s, 0);
     g->epoch = epoch;
     ++g->fused;
@@ -442,7 +506,10 @@ tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* X_shard, 
   // runs beside it on a side stream.  Each chunk is one collective epoch whose
   // partial the GEMM writes straight into that epoch's peer-visible send slot;
   // the GEMM of chunk c+2 (same slot parity) waits for chunk c's all-reduce to
-  // finish, i.e. for every peer to have read the slot.  Chunking rows never
+  // finish on this rank.  The chunk all-reduces are forced onto the two-phase
+  // path, whose completion on this rank (all W done flags) proves that every
+  // peer has finished READING this rank's slot -- the one-shot path proves only
+  // that this rank finished reading the peers' slots.  Chunking rows never
   // changes bits (batch invariance), and every rank cuts the same chunks (they
   // depend only on M).  TBIK_GROUP_OVERLAP=0 disables it.
   static const bool overlap_on = [] {
@@ -450,7 +517,7 @@ tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* X_shard, 
     return !(e && *e && std::atoi(e) == 0);
   }();
   constexpr int kChunks = 4, kReserve = 16;
-  const bool overlap = overlap_on && g->W > 1 && M >= 2 * 256 && M * N * 4 >= (int64_t(8) << 20);
+  const bool overlap = overlap_on && g->W > 1 && M >= 2 * 256 && N % 4 == 0 && M * N * 4 >= (int64_t(8) << 20);
   if (!overlap) {
     // GEMM straight into the peer-visible slot of the coming epoch.
     float* send = tbik_group_send_buffer(g);
@@ -487,13 +554,79 @@ tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* X_shard, 
       st = set_error(TBIK_CUDA_ERROR, "overlap event");
       break;
     }
-    st = group_all_reduce(g, send, Y + r0 * N, rows * N, g->side, 4 * kReserve);
+    st = group_all_reduce(g, send, Y + r0 * N, rows * N, g->side, 4 * kReserve, /*force_two_phase=*/true);
     if (st == TBIK_OK && cudaEventRecord(g->ev_ar[c & 1], g->side) != cudaSuccess)
       st = set_error(TBIK_CUDA_ERROR, "overlap event");
   }
   set_tc_sm_cap(prev_cap);
   TBIK_TRY(st);
   TBIK_CUDA(cudaStreamWaitEvent(s, g->ev_ar[(c - 1) & 1], 0));
+  return TBIK_OK;
+}
+
+tbik_status tbik_group_barrier(tbik_group* g, void* stream) {
+  if (!g) return set_error(TBIK_BAD_ARGUMENT, "null group");
+  GroupPtrs gp;
+  return group_publish(g, nullptr, 0, 0, 0, static_cast<cudaStream_t>(stream), &gp);
+}
+
+tbik_status tbik_group_all_gather(tbik_group* g, const void* local, int64_t rows, int64_t cols, int64_t ld_local,
+                                  int elem_bytes, void* out, int64_t ld_out, void* stream) {
+  if (!g || !local || !out) return set_error(TBIK_BAD_ARGUMENT, "null argument");
+  if (elem_bytes != 2 && elem_bytes != 4) return set_error(TBIK_UNKNOWN_DTYPE, "all_gather: element size must be 2 or 4");
+  if (rows < 1 || cols < 1) return set_error(TBIK_BAD_DIMENSION, "all_gather: dimensions must be >= 1");
+  if (ld_local < cols || ld_out < cols * g->W) return set_error(TBIK_BAD_ARGUMENT, "all_gather: leading dimension too small");
+  if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t row_bytes = cols * elem_bytes;
+  const int64_t max_rows = g->capacity * static_cast<int64_t>(sizeof(float)) / row_bytes;
+  if (max_rows < 1) return set_error(TBIK_COLLECTIVE_MISMATCH, "all_gather: one row exceeds group capacity");
+  // 16-byte units when every row start is 16-byte aligned, else 4- or 2-byte units
+  // (a pure copy: the unit never changes the bytes).
+  const uintptr_t ob = reinterpret_cast<uintptr_t>(out);
+  const int64_t ldo_bytes = ld_out * elem_bytes;
+  const int unit = (row_bytes % 16 == 0 && ob % 16 == 0 && ldo_bytes % 16 == 0)  ? 16
+                   : (row_bytes % 4 == 0 && ob % 4 == 0 && ldo_bytes % 4 == 0) ? 4
+                                                                                : 2;
+  for (int64_t r0 = 0; r0 < rows; r0 += max_rows) {  // one epoch per chunk of rows (same chunks on every rank)
+    const int64_t nr = std::min(max_rows, rows - r0);
+    GroupPtrs gp;
+    TBIK_TRY(group_publish(g, static_cast<const char*>(local) + r0 * ld_local * elem_bytes, nr, row_bytes,
+                           ld_local * elem_bytes, s, &gp));
+    const int64_t units = nr * row_bytes / unit;
+    dim3 grid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((units + 255) / 256, 148 * 2 / g->W + 1))),
+              static_cast<unsigned>(g->W));
+    char* o = static_cast<char*>(out) + r0 * ldo_bytes;
+    if (unit == 16)
+      group_gather_copy_kernel<uint4><<<grid, 256, 0, s>>>(gp, g->W, g->rank, nr, row_bytes / 16,
+                                                           reinterpret_cast<uint4*>(o), ldo_bytes / 16);
+    else if (unit == 4)
+      group_gather_copy_kernel<uint32_t><<<grid, 256, 0, s>>>(gp, g->W, g->rank, nr, row_bytes / 4,
+                                                              reinterpret_cast<uint32_t*>(o), ldo_bytes / 4);
+    else
+      group_gather_copy_kernel<uint16_t><<<grid, 256, 0, s>>>(gp, g->W, g->rank, nr, row_bytes / 2,
+                                                              reinterpret_cast<uint16_t*>(o), ldo_bytes / 2);
+    TBIK_CUDA(cudaGetLastError());
+    count_launch();
+  }
+  return TBIK_OK;
+}
+
+tbik_status tbik_group_logsoftmax_merge(tbik_group* g, const float* ms_local, int64_t rows, float* lse, void* stream) {
+  if (!g || !ms_local || !lse) return set_error(TBIK_BAD_ARGUMENT, "null argument");
+  if (rows < 1) return set_error(TBIK_BAD_DIMENSION, "logsoftmax merge: rows must be >= 1");
+  if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t max_rows = g->capacity / 2;
+  for (int64_t r0 = 0; r0 < rows; r0 += max_rows) {
+    const int64_t nr = std::min(max_rows, rows - r0);
+    GroupPtrs gp;
+    TBIK_TRY(group_publish(g, ms_local + 2 * r0, 1, nr * 2 * static_cast<int64_t>(sizeof(float)),
+                           nr * 2 * static_cast<int64_t>(sizeof(float)), s, &gp));
+    // The W shard states meet in rank order through the contiguous-halves tree --
+    // the same merge tbik_tree_logsoftmax_local applies to simulated shards.
+    TBIK_TRY(tbik_logsoftmax_merge(gp.src, g->W, nr, lse + r0, stream));
+  }
   return TBIK_OK;
 }
 

@@ -103,6 +103,11 @@ tbik_status launch_tc_skinny(const GemmView& v, float* C, int64_t ldc, cudaStrea
 // K-split factor run_tree_gemm uses for the tcgen05 leaf (1 = one FULL launch).
 int64_t tc_split_units(const GemmView& v);
 
+// View of A[M x K] . B[K x N] with the local plan of K under the given (global)
+// k_first and c_max = 1 (matmul.cpp:153 via layers.cpp:85-88).
+tbik_status make_view(const void* A, int adt, int64_t lda, const void* B, int bdt, int64_t ldb, int64_t M,
+                      int64_t N, int64_t K, int64_t bk, int64_t kf_global, GemmView* v);
+
 // Whole tree GEMM (plan resolved by the caller): picks FULL vs split + combine.
 tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mode, cudaStream_t s);
 

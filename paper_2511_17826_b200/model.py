@@ -107,10 +107,26 @@ class DecoderWeights:
     gate_up_interleaved: bool = False  # set by TbikDecoder (gate/up columns interleaved in place)
 
 
-def random_weights(cfg: DecoderConfig, seed: int = 0, device="cuda") -> DecoderWeights:
+def _shard_cols(t, parts):
+    """Concatenate column ranges [(b, e), ...] of a 2-D tensor (contiguous copy)."""
+    import torch
+    return torch.cat([t[:, b:e] for b, e in parts], dim=1).contiguous()
+
+
+def random_weights(cfg: DecoderConfig, seed: int = 0, device="cuda", shard: Optional[tuple] = None) -> DecoderWeights:
     """Random-init weights of the named architecture, generated on the device
     from fixed per-tensor seeds (independent of TP and batch, like
-    make_demo_weights, demo.cpp:123-162)."""
+    make_demo_weights, demo.cpp:123-162).
+
+    shard = (W, r): keep only tensor-parallel rank r's part of every projection
+    (each full tensor is generated from its own seed, sliced, and freed):
+      wqkv    columns of rank r's q heads | k heads | v heads   (column-parallel)
+      wo      rows [r, r+1) * nq*D/W  = make_row_shard_plan(nq*D)[r]  (row-parallel)
+      wgu     gate_up pairs [r, r+1) * I/W, interleaved (column-parallel, SiLU*up fused)
+      wd      rows [r, r+1) * I/W     = make_row_shard_plan(I)[r]     (row-parallel)
+      lm_head columns [r, r+1) * V/W  = make_column_shard_plan(V)[r]
+    embed and the norm gains are replicated.  The values are exactly the
+    corresponding slices of shard=None's tensors."""
     import torch
     g = torch.Generator(device=device)
     counter = [seed * 1000003]
@@ -124,21 +140,46 @@ def random_weights(cfg: DecoderConfig, seed: int = 0, device="cuda") -> DecoderW
 
     H, I, D = cfg.hidden, cfg.intermediate, cfg.head_dim
     nq, nkv = cfg.n_heads, cfg.n_kv_heads
+    W, r = shard if shard is not None else (1, 0)
+    if nq % W or nkv % W or I % W or cfg.vocab % W:
+        raise api.TbikError(api.ErrorCode.ShardError, f"{cfg.name}: heads / intermediate / vocab not divisible by {W}")
+    qh, kh = nq // W, nkv // W
+    qkv_parts = [(r * qh * D, (r + 1) * qh * D), (nq * D + r * kh * D, nq * D + (r + 1) * kh * D),
+                 ((nq + nkv) * D + r * kh * D, (nq + nkv) * D + (r + 1) * kh * D)]
+
+    def cut(t, kind):
+        if W == 1:
+            return t
+        if kind == "qkv":
+            return _shard_cols(t, qkv_parts)
+        if kind == "rows":
+            n = t.shape[0] // W
+            return t[r * n:(r + 1) * n].contiguous()
+        if kind == "cols":
+            n = t.shape[1] // W
+            return t[:, r * n:(r + 1) * n].contiguous()
+        if kind == "gate_up":  # interleave the full tensor, then take rank r's pairs
+            il = api.interleave_gate_up(t)
+            n = il.shape[1] // W
+            return il[:, r * n:(r + 1) * n].contiguous()
+        raise ValueError(kind)
+
     w = DecoderWeights(embed=normal((cfg.vocab, H), 1.0))
     for _ in range(cfg.n_layers):
         lw = LayerWeights(
             ln1=normal((H,), 0.02, 1.0, torch.float32),
-            wqkv=normal((H, (nq + 2 * nkv) * D), cfg.weight_std),
-            wo=normal((nq * D, H), cfg.weight_std),
+            wqkv=cut(normal((H, (nq + 2 * nkv) * D), cfg.weight_std), "qkv"),
+            wo=cut(normal((nq * D, H), cfg.weight_std), "rows"),
             ln2=normal((H,), 0.02, 1.0, torch.float32),
-            wgu=normal((H, 2 * I), cfg.weight_std),
-            wd=normal((I, H), cfg.weight_std))
+            wgu=cut(normal((H, 2 * I), cfg.weight_std), "gate_up"),
+            wd=cut(normal((I, H), cfg.weight_std), "rows"))
         if cfg.qk_norm:
             lw.q_norm = normal((D,), 0.02, 1.0, torch.float32)
             lw.k_norm = normal((D,), 0.02, 1.0, torch.float32)
         w.layers.append(lw)
     w.ln_f = normal((H,), 0.02, 1.0, torch.float32)
-    w.lm_head = normal((H, cfg.vocab), cfg.weight_std)
+    w.lm_head = cut(normal((H, cfg.vocab), cfg.weight_std), "cols")
+    w.gate_up_interleaved = W > 1
     return w
 
 
@@ -166,11 +207,19 @@ class TbikDecoder:
         self.bcfg_down = api.BlockConfig(64, cfg.block_k_down, 128, 0)
 
     # -- building blocks ------------------------------------------------------------
+    # (simulated TP: the full weights, `tp` ranks on this GPU; ShardedDecoder
+    # overrides these with one rank's shards and the PeerGroup collectives)
+    def _heads(self):
+        return self.cfg.n_heads, self.cfg.n_kv_heads
+
     def _col(self, x, w, tp):
         return api.column_parallel_forward(x, w, api.DeviceGroup(tp), self.bcfg, self.leaf)
 
-    def _row(self, x, w, tp, cfg):
+    def _row(self, x, w, tp, cfg, k_global):
         return api.row_parallel_forward(x, w, api.DeviceGroup(tp), cfg, self.cfg.c_max, self.leaf)
+
+    def _gate_up(self, x, w, tp):
+        return api.tree_matmul_silu_mul(x, w, api.DeviceGroup(tp), self.bcfg, self.leaf)
 
     def _norm(self, x, gamma):
         import torch
@@ -205,13 +254,15 @@ class TbikDecoder:
 
     # -- forward ------------------------------------------------------------------------
     def forward(self, tokens, tp: int = 1):
-        """tokens: int64 [B, S] on the device.  Returns f32 logits [B*S, vocab]."""
+        """tokens: int64 [B, S] on the device.  Returns f32 logits [B*S, vocab]
+        (ShardedDecoder: this rank's vocab columns)."""
         import torch
         cfg, w = self.cfg, self.w
         B, S = tokens.shape
         M = B * S
         dev = tokens.device
-        H, D, nq, nkv, I = cfg.hidden, cfg.head_dim, cfg.n_heads, cfg.n_kv_heads, cfg.intermediate
+        H, D, I = cfg.hidden, cfg.head_dim, cfg.intermediate
+        nq, nkv = self._heads()  # this rank's heads (all of them with simulated TP)
         if S > cfg.max_pos:
             raise api.TbikError(api.ErrorCode.BadDimension, "sequence longer than the RoPE table")
         ids = tokens.reshape(M).contiguous()
@@ -241,10 +292,10 @@ class TbikDecoder:
             attn_fn = lib.tbik_attention_prefill_tc if self.leaf == api.LEAF_TCGEN05 else lib.tbik_attention_prefill
             check(attn_fn(_vp(q), qcols, _vp(k), kcols, _vp(v), kcols, B, S, nq, nkv, D,
                           scale, _vp(attn), qcols, self._stream()))
-            o = self._row(attn, lw.wo, tp, self.bcfg)            # f32 [M, H], tree all-reduce over tp
+            o = self._row(attn, lw.wo, tp, self.bcfg, cfg.n_heads * D)  # f32 [M, H], tree all-reduce
             a = self._residual_norm(h, o, lw.ln2)               # h = bf16(h + o); a = norm(h)
-            act = api.tree_matmul_silu_mul(a, lw.wgu, api.DeviceGroup(tp), self.bcfg, self.leaf)  # bf16 [M, I]
-            d = self._row(act, lw.wd, tp, self.bcfg_down)        # f32 [M, H]
+            act = self._gate_up(a, lw.wgu, tp)                  # bf16 [M, I / ranks]
+            d = self._row(act, lw.wd, tp, self.bcfg_down, I)     # f32 [M, H]
             nxt = w.layers[li + 1].ln1 if li + 1 < len(w.layers) else w.ln_f
             a = self._residual_norm(h, d, nxt)                  # next layer's ln1 (or ln_f)
         if not w.layers:
@@ -277,3 +328,67 @@ class TbikDecoder:
             logits = self.forward(tokens, tp)
             lse, lp, _ = self.log_probs(logits, tp, full=full_logprobs)
         return graph, (logits, lse, lp)
+
+
+class ShardedDecoder(TbikDecoder):
+    """Rank r of a W-way tensor-parallel TBIK decoder, one process per GPU
+    (the reference threads one DeviceGroup through ffn_block /
+    greedy_generate, demo.cpp:164-241).  The rank owns only its shards
+    (random_weights(shard=(W, r))):
+
+      qkv, gate_up, lm_head  column-parallel: this rank's heads / pairs / vocab
+                             columns, tree GEMM with the c_max = 1 plan (layers.cpp:48-72)
+      o_proj, down_proj      PeerGroup.row_parallel_forward: the rank's leaf groups
+                             (make_row_shard_plan) + the fixed-order tree all-reduce
+                             over NVLink peer memory (one fused kernel when M > 128)
+      attention              the rank's q heads with their kv heads (GQA), per
+                             (sequence, head) -- independent of the head split
+      norms, residual        replicated on every rank
+      log-softmax            vocab-sharded (m, s) states, 8 bytes per row exchanged
+                             (PeerGroup.log_softmax)
+
+    so logits / log-probs equal the single-GPU TP = 1 forward bit for bit.
+    Eager only: the group collectives carry host-side epoch counters that a
+    CUDA graph would freeze."""
+
+    def __init__(self, cfg: DecoderConfig, group, seed: int = 0, leaf: int = api.LEAF_TCGEN05, device="cuda",
+                 weights: Optional[DecoderWeights] = None):
+        self.group = group
+        W, r = group.world, group.rank
+        if weights is None:
+            weights = random_weights(cfg, seed, device, shard=(W, r))
+        super().__init__(cfg, weights, leaf)
+        self.W, self.r = W, r
+        self.v_local = cfg.vocab // W
+        if cfg.vocab_groups % W:
+            raise api.TbikError(api.ErrorCode.ShardError, f"vocab_groups {cfg.vocab_groups} not divisible by {W}")
+        # the rank's K ranges must be the row shard plan's (leaf-group aligned)
+        for k in (cfg.n_heads * cfg.head_dim, cfg.intermediate):
+            bcfg = self.bcfg_down if k == cfg.intermediate else self.bcfg
+            b, e = api.make_row_shard_plan(k, bcfg, W, cfg.c_max).bounds[r]
+            if (b, e) != (r * k // W, (r + 1) * k // W):
+                raise api.TbikError(api.ErrorCode.ShardError, f"row shard of K={k} is not the even split")
+
+    def _heads(self):
+        return self.cfg.n_heads // self.W, self.cfg.n_kv_heads // self.W
+
+    def _col(self, x, w, tp):
+        return api.tree_matmul(x, w, self.bcfg, self.leaf)
+
+    def _row(self, x, w, tp, cfg, k_global):
+        return self.group.row_parallel_forward(x, w, k_global, cfg, self.cfg.c_max, self.leaf)
+
+    def _gate_up(self, x, w, tp):
+        return api.tree_matmul_silu_mul(x, w, None, self.bcfg, self.leaf)
+
+    def log_probs(self, logits, tp: int = 1, targets=None, full: bool = True):
+        """(lse, this rank's log-prob columns, target log-probs of targets in this
+        rank's vocab range -- NaN elsewhere)."""
+        return self.group.log_softmax(logits, self.cfg.vocab_groups // self.W, self.r * self.v_local, targets, full)
+
+    def gather(self, shard):
+        """Rank-ordered column concatenation of a per-rank [rows x V/W] block."""
+        return self.group.all_gather(shard)
+
+    def capture(self, tokens, tp: int = 1, full_logprobs: bool = True):
+        raise api.TbikError(api.ErrorCode.BadArgument, "ShardedDecoder runs eagerly (group epochs are host state)")
