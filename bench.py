@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-forward", action="store_true",
                     help="skip the full Llama-3.1-8B forward (logits bit-identity across TP)")
+    ap.add_argument("--cpu-m", type=int, default=256,
+                    help="rows of the bounded CPU sample (the reference's rate is ~3x lower at M=16)")
     return ap.parse_args()
 
 
@@ -216,7 +218,7 @@ def run_reference(args):
     if rank != 0:
         return
     tp = args.gpus
-    m_sample = 16
+    m_sample = args.cpu_m
     import numpy as np
 
     from oracle.oracle import RefLib
@@ -252,6 +254,52 @@ def run_reference(args):
 # ------------------------------------------------------------------------------------
 # TBIK arm
 # ------------------------------------------------------------------------------------
+def sharded_forward(group, rank, world, barrier, max_over_ranks, batch=4, seq=256, reps=3):
+    """Llama-3.1-8B (32 layers, random init) prefill of batch x seq tokens with W real
+    ranks (model.ShardedDecoder: each process holds its shards; row-parallel tree
+    all-reduce, all-gather and (m, s) merge over the PeerGroup), timed as the max
+    over ranks; rank 0 checks the all-gathered logits / log-probs against the
+    single-GPU TP = 1 forward of the full weights."""
+    import torch
+
+    from paper_2511_17826_b200 import model as mdl
+    cfg = mdl.llama31_8b()
+    dec = mdl.ShardedDecoder(cfg, group, seed=3)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    tokens = torch.randint(0, cfg.vocab, (batch, seq), device="cuda", generator=g)
+    M = batch * seq
+
+    def step():
+        logits = dec.forward(tokens)
+        return logits, dec.log_probs(logits, full=True)
+
+    step()
+    torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(ev_time(step, reps))
+    logits_r, (_, lp_r, _) = step()
+    logits = dec.gather(logits_r)
+    lp = dec.gather(lp_r)
+    torch.cuda.synchronize()
+    out = {"model": cfg.name, "layers": cfg.n_layers, "batch": batch, "seq": seq, "tokens": M, "tp": world,
+           "ms": ms, "tokens_per_s": M / (ms * 1e-3),
+           "path": "ShardedDecoder: one process per GPU, rank-local weight shards, PeerGroup collectives"}
+    del dec
+    torch.cuda.empty_cache()
+    if rank == 0:
+        full = mdl.TbikDecoder(cfg, mdl.random_weights(cfg, seed=3))
+        ref_logits = full.forward(tokens, 1)
+        _, ref_lp, _ = full.log_probs(ref_logits, 1, full=True)
+        torch.cuda.synchronize()
+        out["logits_bit_identical_to_tp1"] = bool(torch.equal(logits.view(torch.int32), ref_logits.view(torch.int32)))
+        out["logprobs_bit_identical_to_tp1"] = bool(torch.equal(lp.view(torch.int32), ref_lp.view(torch.int32)))
+        del full, ref_logits, ref_lp
+        torch.cuda.empty_cache()
+    barrier()
+    return out
+
+
 def run_tbik(args):
     import torch
     import torch.distributed as dist
@@ -377,31 +425,76 @@ def run_tbik(args):
            "path": "pinned host x -> tbik_tree_matmul_hostio / tbik_group_row_parallel_forward_hostio (C ABI: "
                    "row-chunked H2D | GEMM + tree all-reduce | D2H on three streams) -> pinned host y"}
 
-    # ---- non-invariant status quo: cuBLAS bf16 (+ NCCL all-reduce) ---------------------------
+    # ---- non-invariant status quo: cuBLAS (+ NCCL all-reduce) ------------------------------------
+    # tbik_baseline_cublas_nccl (C ABI): cuBLAS GEMM of this rank's shard, then NCCL's sum
+    # all-reduce -- bf16 output + bf16 all-reduce (what a serving stack runs) and f32 output
+    # + f32 all-reduce (the same bytes per rank as the TBIK tree all-reduce).  At N = 1 the
+    # communicator has one rank (no transfer).
+    import ctypes as C
+    uid = (C.c_char * 128)()
+    if rank == 0:
+        tb.api.check(tb.lib.tbik_nccl_unique_id(uid))
+    if world > 1:
+        holder = [bytes(uid)]
+        dist.broadcast_object_list(holder, src=0)
+        uid = (C.c_char * 128).from_buffer_copy(holder[0])
+    comm = C.c_void_p()
+    tb.api.check(tb.lib.tbik_nccl_comm_create(world, rank, dev_index, uid, C.byref(comm))) if not share else None
     yb = torch.empty(M, N_OUT, device=dev, dtype=torch.bfloat16)
+    yf = torch.empty(M, N_OUT, device=dev, dtype=torch.float32)
 
-    def cublas_step():
-        torch.matmul(x, w, out=yb)
-        if world > 1 and not share:
-            dist.all_reduce(yb)
+    def cublas_step(out_f32):
+        def f():
+            if share:
+                torch.matmul(x, w, out=yb)
+                return
+            o = yf if out_f32 else yb
+            tb.api.check(tb.lib.tbik_baseline_cublas_nccl(comm, C.c_void_p(x.data_ptr()), 1, Kr,
+                                                          C.c_void_p(w.data_ptr()), 1, N_OUT, C.c_void_p(o.data_ptr()),
+                                                          M, N_OUT, Kr, 1 if out_f32 else 0,
+                                                          C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return f
 
-    for _ in range(3):
-        cublas_step()
-    barrier()
-    base_ms = max_over_ranks(ev_time(cublas_step, max(args.steps, 5)))
-    base_tf = flops / (base_ms * 1e-3) / 1e12
-    noninv = {"value": base_tf, "unit": "TFLOP/s", "ms_per_step": base_ms,
-              "path": "torch.matmul bf16 (cuBLAS)" + (" + NCCL bf16 all_reduce" if world > 1 else ""),
-              "tbik_over_baseline": value / base_tf}
+    noninv = {"path": "tbik_baseline_cublas_nccl: cuBLAS GEMM of the rank's K shard + NCCL sum all-reduce "
+                      "(order not controlled: non-invariant)"}
+    for key, out_f32 in (("bf16", False), ("f32", True)):
+        fn = cublas_step(out_f32)
+        for _ in range(3):
+            fn()
+        barrier()
+        bms = max_over_ranks(ev_time(fn, max(args.steps, 5)))
+        btf = flops / (bms * 1e-3) / 1e12
+        noninv[key] = {"value": btf, "unit": "TFLOP/s", "ms_per_step": bms, "tbik_over_baseline": value / btf,
+                       "out": f"{key} GEMM output + {key} all-reduce" if world > 1 else f"{key} GEMM output"}
+    noninv["tbik_over_baseline"] = noninv["bf16"]["tbik_over_baseline"]
+    if not share:
+        tb.lib.tbik_nccl_comm_destroy(comm)
+    del yf
 
-    # ---- TP invariance check on this GPU (simulated ranks), every run -------------------------
+    # ---- the tree all-reduce alone over NVLink (N > 1): algorithmic and bus bandwidth ---------
+    collective_bw = None
+    if group is not None:
+        part = torch.randn(M * N_OUT, device=dev, generator=g)
+        red = torch.empty_like(part)
+        barrier()
+        ar_ms = max_over_ranks(ev_time(lambda: group.tree_all_reduce(part, out=red), max(args.steps, 5)))
+        alg = 4.0 * M * N_OUT / (ar_ms * 1e-3) / 1e9
+        collective_bw = {"kernel": "tree all-reduce over peer memory (one-shot < 1 MiB, else reduce-scatter + push)",
+                         "bytes_per_rank": 4 * M * N_OUT, "ms": ar_ms, "alg_GBps": alg,
+                         "bus_GBps": alg * 2 * (world - 1) / world, "nvlink_peak_GBps_per_direction": 900.0,
+                         "bus_frac": alg * 2 * (world - 1) / world / 900.0}
+        del part, red
+
+    # ---- TP invariance at the bench config (simulated ranks on this GPU), every run -----------
+    # M = 4096 rows, the full down_proj: TP = 1/2/4/8 must give one bit pattern.
     tp_ok = None
     if rank == 0:
-        xs = x_full[:64].contiguous()
-        wf = torch.randn(K_FULL, N_OUT, device=dev, generator=g).to(torch.bfloat16)
-        outs = [tb.row_parallel_forward(xs, wf, tb.DeviceGroup(t), cfg, 8, leaf) for t in (1, 2, 4, 8)]
-        tp_ok = all(torch.equal(outs[0].view(torch.int32), o.view(torch.int32)) for o in outs[1:])
-        del wf
+        wf = (torch.randn(K_FULL, N_OUT, device=dev, generator=g).to(torch.bfloat16) if world > 1
+              else w)
+        outs = [tb.row_parallel_forward(x_full, wf, tb.DeviceGroup(t), cfg, 8, leaf) for t in (1, 2, 4, 8)]
+        tp_ok = {"M": M, "tp": [1, 2, 4, 8],
+                 "bit_identical": all(torch.equal(outs[0].view(torch.int32), o.view(torch.int32)) for o in outs[1:])}
+        del wf, outs
 
     # ---- M sweep (rank 0, N = 1) ----------------------------------------------------------------
     sweep = None
@@ -456,6 +549,16 @@ def run_tbik(args):
             forward = {"error": f"{type(e).__name__}: {e}"[:300]}
             torch.cuda.synchronize()
 
+    # ---- the north-star forward at real TP (N > 1): one process per GPU, rank shards only ----
+    forward_tp = None
+    if world > 1 and not args.no_forward:
+        del w, x, x_full, y, yb, x_host, y_host, y_step
+        torch.cuda.empty_cache()
+        try:
+            forward_tp = sharded_forward(group, rank, world, barrier, max_over_ranks)
+        except Exception as e:  # noqa: BLE001 -- the headline line must still print
+            forward_tp = {"error": f"{type(e).__name__}: {e}"[:300]}
+
     rowops = None
     if rank == 0 and world == 1 and not args.no_forward:
         torch.cuda.empty_cache()
@@ -468,7 +571,7 @@ def run_tbik(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_reference_sample(1, 16, budget_s=10.0)
+            cpu = cpu_reference_sample(1, args.cpu_m, budget_s=12.0, min_reps=2)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -490,7 +593,8 @@ def run_tbik(args):
             "collective": None if group is None else {
                 "path": "fused: one tcgen05 kernel = GEMM + tile-flag tree all-reduce over peer memory"
                         if group.fused_count() > 0 else "GEMM, then tree all-reduce kernels",
-                "fused_calls": group.fused_count()},
+                "fused_calls": group.fused_count(), "tree_all_reduce_alone": collective_bw},
+            "forward_tp": forward_tp,
             "cpu_baseline": cpu,
             "forward": forward,
             "rowops_c5": rowops,
@@ -503,10 +607,26 @@ def run_tbik(args):
         dist.destroy_process_group()
 
 
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` without a torchrun environment: launch the N
+    ranks ourselves exactly as the driver does (torch.distributed.run, one process
+    per GPU, rendezvous on 127.0.0.1) and pass rank 0's JSON line through."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
-        run_reference(args)
+        run_reference(args)  # rank 0 alone works; needs no process group
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     else:
         run_tbik(args)
 

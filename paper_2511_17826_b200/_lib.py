@@ -106,6 +106,21 @@ _SIGS = {
                                                     PCFG, i64, ci, i64, vp]),
     "tbik_group_tree_all_reduce": (ci, [vp, PF, PF, i64, vp]),
     "tbik_group_barrier": (ci, [vp, vp]),
+    "tbik_leaf_dot": (ci, [PF, PF, i64, PF, vp]),
+    "tbik_silu": (ci, [vp, ci, i64, i64, i64, PF, i64, vp]),
+    "tbik_local_group_create": (ci, [ci, C.POINTER(ci), C.POINTER(vp)]),
+    "tbik_local_group_destroy": (ci, [vp]),
+    "tbik_local_group_device": (ci, [vp, ci]),
+    "tbik_local_group_stream": (vp, [vp, ci]),
+    "tbik_local_group_row_parallel_forward": (ci, [vp, C.POINTER(vp), ci, PI64, C.POINTER(vp), ci, PI64, PF, i64,
+                                                   i64, i64, i64, PCFG, i64, ci, vp]),
+    "tbik_baseline_gemm": (ci, [vp, ci, i64, vp, ci, i64, PF, i64, i64, i64, i64, vp]),
+    "tbik_baseline_row_parallel_forward_local": (ci, [vp, ci, i64, vp, ci, i64, PF, i64, i64, i64, i64, ci, vp]),
+    "tbik_baseline_column_parallel_forward_local": (ci, [vp, ci, i64, vp, ci, i64, PF, i64, i64, i64, i64, ci, vp]),
+    "tbik_nccl_unique_id": (ci, [vp]),
+    "tbik_nccl_comm_create": (ci, [ci, ci, ci, vp, C.POINTER(vp)]),
+    "tbik_nccl_comm_destroy": (ci, [vp]),
+    "tbik_baseline_cublas_nccl": (ci, [vp, vp, ci, i64, vp, ci, i64, vp, i64, i64, i64, ci, vp]),
     "tbik_group_all_gather": (ci, [vp, vp, i64, i64, i64, ci, vp, i64, vp]),
     "tbik_group_logsoftmax_merge": (ci, [vp, PF, i64, PF, vp]),
     "tbik_group_row_parallel_forward": (ci, [vp, vp, ci, i64, vp, ci, i64, PF, i64, i64, i64, i64,
@@ -135,6 +150,7 @@ for _name, (_res, _args) in _SIGS.items():
     _fn.argtypes = _args
 
 TBIK_IPC_HANDLE_BYTES = 128
+TBIK_NCCL_ID_BYTES = 128
 
 
 def header_functions() -> list[str]:

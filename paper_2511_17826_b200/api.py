@@ -328,6 +328,86 @@ def tree_matmul_silu_mul(x, w_il, group: DeviceGroup | None = None, cfg: BlockCo
     return out
 
 
+# ---- one process, several GPUs ------------------------------------------------------------
+class LocalGroup:
+    """The reference's DeviceGroup held by ONE process with rank r on GPU
+    device_ids[r] (tbik_local_group_*): per-rank streams, peer access, and the
+    row-parallel forward whose partials meet over peer memory on rank 0's GPU."""
+
+    def __init__(self, device_ids: Sequence[int]):
+        W = len(device_ids)
+        ids = (C.c_int * W)(*device_ids)
+        h = C.c_void_p()
+        check(lib.tbik_local_group_create(W, ids, C.byref(h)))
+        self._h, self.world, self.devices = h, W, list(device_ids)
+
+    def close(self) -> None:
+        if self._h:
+            lib.tbik_local_group_destroy(self._h)
+            self._h = None
+
+    def row_parallel_forward(self, x_shards: Sequence, w_shards: Sequence, K_global: int,
+                             cfg: BlockConfig | None = None, c_max: int = 8, leaf: int = LEAF_TCGEN05, out=None):
+        """x_shards[r] / w_shards[r]: rank r's make_row_shard_plan range, on devices[r]."""
+        torch = _torch()
+        cfg = cfg or default_block_config(BF16)
+        W = self.world
+        M, N = x_shards[0].shape[0], w_shards[0].shape[1]
+        xs = (C.c_void_p * W)(*[t.data_ptr() for t in x_shards])
+        ws = (C.c_void_p * W)(*[t.data_ptr() for t in w_shards])
+        ldx = (C.c_int64 * W)(*[t.stride(0) for t in x_shards])
+        ldw = (C.c_int64 * W)(*[t.stride(0) for t in w_shards])
+        out = torch.empty((M, N), dtype=torch.float32, device=f"cuda:{self.devices[0]}") if out is None else out
+        torch.cuda.synchronize()  # inputs complete on every device (the ABI orders only rank 0's stream)
+        check(lib.tbik_local_group_row_parallel_forward(self._h, xs, _dt(x_shards[0]), ldx, ws, _dt(w_shards[0]), ldw,
+                                                        C.c_void_p(out.data_ptr()), out.stride(0), M, N, K_global,
+                                                        C.byref(cfg.c()), c_max, leaf, _stream()))
+        return out
+
+
+# ---- the labelled non-invariant status quo ----------------------------------------------
+def baseline_row_parallel_forward(x, w, group: DeviceGroup):
+    """baseline_row_parallel_forward (layers.hpp:48-49): cuBLAS per K/tp shard + ring sum."""
+    M, K = x.shape
+    N = w.shape[1]
+    px, dx, ldx = _mat(x, "X")
+    pw, dw, ldw = _mat(w, "W")
+    out = _empty_f32(M, N, x)
+    check(lib.tbik_baseline_row_parallel_forward_local(px, dx, ldx, pw, dw, ldw, C.c_void_p(out.data_ptr()), N,
+                                                       M, N, K, group.world_size(), _stream()))
+    return out
+
+
+def baseline_column_parallel_forward(x, w, group: DeviceGroup):
+    """baseline_column_parallel_forward (layers.hpp:53-54): cuBLAS per column shard."""
+    M, K = x.shape
+    N = w.shape[1]
+    px, dx, ldx = _mat(x, "X")
+    pw, dw, ldw = _mat(w, "W")
+    out = _empty_f32(M, N, x)
+    check(lib.tbik_baseline_column_parallel_forward_local(px, dx, ldx, pw, dw, ldw, C.c_void_p(out.data_ptr()), N,
+                                                          M, N, K, group.world_size(), _stream()))
+    return out
+
+
+def silu(x):
+    """silu (demo.hpp:56): z / (1 + exp(-z)) in f32 (the library's exp)."""
+    rows, cols = x.shape
+    px, dx, ldx = _mat(x, "x")
+    out = _empty_f32(rows, cols, x)
+    check(lib.tbik_silu(px, dx, ldx, rows, cols, C.c_void_p(out.data_ptr()), cols, _stream()))
+    return out
+
+
+def leaf_dot(a, b):
+    """leaf_dot (matmul.hpp:48) of two f32 device vectors: ascending fma from +0."""
+    torch = _torch()
+    out = torch.empty(1, dtype=torch.float32, device=a.device)
+    check(lib.tbik_leaf_dot(C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), a.numel(),
+                            C.c_void_p(out.data_ptr()), _stream()))
+    return out
+
+
 # ---- tree-ordered reductions ----------------------------------------------------------
 def rmsnorm(x, gamma, eps: float = 1e-5, out_dtype=None):
     """rmsnorm (demo.hpp:53) with the canonical tree sum of squares."""

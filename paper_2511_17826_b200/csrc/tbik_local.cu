@@ -207,9 +207,12 @@ tbik_status tbik_local_group_destroy(tbik_local_group* g) {
   if (!g) return TBIK_OK;
   int prev = 0;
   cudaGetDevice(&prev);
+  for (int r = 0; r < g->W; ++r) {  // shared streams belong to their owner rank only
+    cudaSetDevice(g->dev[r]);
+    if (g->stream[r] && g->owner[r] == r) cudaStreamSynchronize(g->stream[r]);
+  }
   for (int r = 0; r < g->W; ++r) {
     cudaSetDevice(g->dev[r]);
-    if (g->stream[r]) cudaStreamSynchronize(g->stream[r]);
     if (g->part[r]) cudaFree(g->part[r]);
     if (g->stream[r] && g->owner[r] == r) cudaStreamDestroy(g->stream[r]);
     if (g->done[r]) cudaEventDestroy(g->done[r]);

@@ -1,16 +1,22 @@
 // tests/cpp/tbik_verify.cpp -- the reference's acceptance checks
-// (runner.cpp:53-214), re-run through the B200 C++ mirror (tbik_b200/tbik.hpp).
-//
-// This is what a C++ caller of the reference sees after switching includes
-// from "tbik/*.hpp" to "tbik_b200/tbik.hpp": the same check bodies, the same
-// Rng streams, the same fingerprints.  Prints one line per check and exits
-// non-zero on any failure.  Driven by tests/test_gpu_cpp_api.py.
+// (runner.cpp:53-214) against the drop-in headers include/tbik/*.hpp and
+// libtbik_b200: a C++ caller of the reference keeps `#include "tbik/layers.hpp"`
+// and gets the same Rng streams, the same fingerprints, the same error codes,
+// computed on the B200.  (tests/cpp/Makefile also builds the reference's OWN
+// runner.cpp against these headers: tests/cpp/ref_verify.)  Prints one line per
+// check and exits non-zero on any failure.  Driven by tests/test_gpu_cpp_api.py.
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <set>
 #include <string>
 #include <vector>
 
-#include "tbik_b200/tbik.hpp"
+#include "tbik/collective.hpp"
+#include "tbik/demo.hpp"
+#include "tbik/layers.hpp"
+#include "tbik/matmul.hpp"
+#include "tbik_b200/peer_group.hpp"
 
 using namespace tbik;
 
@@ -141,6 +147,81 @@ void check_rmsnorm() {
   report("tree_rmsnorm_batch_invariance", ok, "8x4096 bf16");
 }
 
+// leaf_dot (matmul.hpp:48) on the GPU == the ascending fma chain; the reference's
+// leaf-order witness (witness.cpp:53-66): ascending differs from descending at seed 0.
+void check_leaf_dot_and_planner_helpers() {
+  bool ok = true;
+  for (std::uint64_t seed = 0; seed < 4; ++seed) {
+    Rng rng(seed, 7);
+    std::vector<float> a(8), b(8);
+    for (auto& v : a) v = static_cast<float>(rng.next_normal());
+    for (auto& v : b) v = static_cast<float>(rng.next_normal());
+    float asc = 0.0f, desc = 0.0f;
+    for (int k = 0; k < 8; ++k) asc = std::fma(a[k], b[k], asc);
+    for (int k = 7; k >= 0; --k) desc = std::fma(a[k], b[k], desc);
+    const float got = leaf_dot(a.data(), b.data(), 8);
+    ok = ok && f32_bit_equal(got, asc);
+    if (seed == 0) ok = ok && !f32_bit_equal(got, desc);
+  }
+  ok = ok && leaf_dot(nullptr, nullptr, 0) == 0.0f;
+  ok = ok && log2_exact(1) == 0 && log2_exact(8) == 3 && log2_exact(9) == 4 && is_power_of_two(64) &&
+       !is_power_of_two(0) && !is_power_of_two(12);
+  report("leaf_dot_and_planner_helpers", ok, "leaf-order witness seed 0, log2_exact, is_power_of_two");
+}
+
+void check_silu() {
+  const Matrix x = Matrix::from_f32(1, 6, {-20.0f, -2.0f, -0.5f, 0.0f, 0.75f, 9.0f});
+  const Matrix y = silu(x);
+  bool ok = y.dtype() == Dtype::F32;
+  double worst = 0.0;
+  for (int j = 0; j < 6; ++j) {
+    const double z = x.at(0, j), want = z / (1.0 + std::exp(-z));
+    worst = std::max(worst, std::abs(y.at(0, j) - want) / std::max(std::abs(want), 1e-6));
+  }
+  ok = ok && worst < 1e-6;
+  report("silu", ok, "max rel err vs libm " + std::to_string(worst));
+}
+
+// check_baseline_kernel_divergence (runner.cpp:216-237): the status quo gives
+// >= 2 distinct bit patterns across TP; the tree path gives exactly one.
+void check_baseline_divergence() {
+  Rng ra(1, 1), rb(1, 2);
+  const Matrix a = matrix_random_normal(ra, 4, 4096, Dtype::F32, 0.0f, 1.0f);
+  const Matrix b = matrix_random_normal(rb, 4096, 8, Dtype::F32, 0.0f, 1.0f);
+  std::set<std::uint64_t> base, tree;
+  for (int tp : {1, 2, 4, 8}) {
+    base.insert(bit_fingerprint(baseline_row_parallel_forward(a, b, DeviceGroup(tp))));
+    tree.insert(bit_fingerprint(row_parallel_forward(a, b, DeviceGroup(tp), default_block_config(Dtype::F32))));
+  }
+  const Matrix c1 = baseline_column_parallel_forward(a, b, DeviceGroup(1));
+  const bool col_ok = bit_equal(c1, baseline_column_parallel_forward(a, b, DeviceGroup(4)));
+  bool shard_err = false;
+  try {
+    baseline_row_parallel_forward(a.slice_cols(0, 4095), b.slice_rows(0, 4095), DeviceGroup(2));
+  } catch (const TbikError& e) {
+    shard_err = e.code() == ErrorCode::ShardError;
+  }
+  report("baseline_kernel_divergence", base.size() >= 2 && tree.size() == 1 && col_ok && shard_err,
+         "baseline distinct=" + std::to_string(base.size()) + " tree distinct=" + std::to_string(tree.size()));
+}
+
+// DeviceGroup with an explicit rank -> device map, and a one-rank PeerGroup.
+void check_groups() {
+  Rng ra(5, 1), rb(5, 2);
+  const Matrix a = matrix_random_normal(ra, 32, 2048, Dtype::Bf16, 0.0f, 1.0f);
+  const Matrix b = matrix_random_normal(rb, 2048, 256, Dtype::Bf16, 0.0f, 1.0f);
+  const BlockConfig cfg = default_block_config(Dtype::Bf16);
+  const Matrix ref = row_parallel_forward(a, b, DeviceGroup(1), cfg);
+  const DeviceGroup g4(4, {0, 0, 0, 0});
+  bool ok = g4.device_span() == 1 && bit_equal(ref, row_parallel_forward(a, b, g4, cfg));
+  const DeviceGroup g8(8);
+  ok = ok && static_cast<int>(g8.devices().size()) == 8 && bit_equal(ref, row_parallel_forward(a, b, g8, cfg));
+  PeerGroup pg(1, 0, 0, 32 * 256);
+  pg.open_peers(pg.ipc_handle());
+  ok = ok && pg.world_size() == 1 && pg.rank() == 0;
+  report("device_groups", ok, "explicit device map, DeviceGroup(8) span " + std::to_string(g8.device_span()));
+}
+
 }  // namespace
 
 int main() {
@@ -152,6 +233,10 @@ int main() {
     check_column_parallel();
     check_spec_kats();
     check_rmsnorm();
+    check_leaf_dot_and_planner_helpers();
+    check_silu();
+    check_baseline_divergence();
+    check_groups();
   } catch (const TbikError& e) {
     std::printf("FAIL exception %s (status %d)\n", e.what(), e.status());
     return 2;  // tbik_main.cpp:200-203 maps TbikError to exit 2

@@ -30,7 +30,8 @@ def main():
     xs, ws = x[:, kb:ke].contiguous(), w[kb:ke].contiguous()
     E_big = (1 << 20) + 4  # > 1 MiB of f32: the reduce-scatter + push path
     Mo, No = 1024, 2048  # >= 8 MiB of f32 output: the overlapped GEMM / all-reduce chunk pipeline
-    grp = tb.PeerGroup(world, rank, torch.cuda.current_device(), max(M * N, E_big, Mo * No), dist)
+    Mg, Ng, Kg = 2560, 2048, 12044  # ragged K: the last rank's shard is shorter (layers.cpp:42)
+    grp = tb.PeerGroup(world, rank, torch.cuda.current_device(), max(M * N, E_big, Mo * No, Mg * Ng), dist)
     ys = []
     for it in range(5):  # several epochs: exercises both send-buffer slots
         for leaf in (tb.LEAF_TCGEN05, tb.LEAF_FMA):
@@ -74,9 +75,20 @@ def main():
         yr = grp.row_parallel_forward(xr[:, kb:ke].contiguous(), wo[kb:ke].contiguous(), K, cfg, 8, tb.LEAF_TCGEN05)
         torch.cuda.synchronize()
         assert torch.equal(yr.view(torch.int32), yr_ref.view(torch.int32)), f"ragged forward differs ({it})"
+    # ragged K (the fused-vs-separate choice must not depend on the
+    # rank's own K range, or the ranks take different paths and hang)
+    xg = torch.randn(Mg, Kg, generator=g, device="cuda").to(torch.bfloat16)
+    wg = torch.randn(Kg, Ng, generator=g, device="cuda").to(torch.bfloat16)
+    gb_, ge_ = tb.make_row_shard_plan(Kg, cfg, world, 8).bounds[rank]
+    yg_ref_g = tb.row_parallel_forward(xg, wg, tb.DeviceGroup(world), cfg, 8, tb.LEAF_TCGEN05)
+    for it in range(2):
+        yg = grp.row_parallel_forward(xg[:, gb_:ge_].contiguous(), wg[gb_:ge_].contiguous(), Kg, cfg, 8,
+                                      tb.LEAF_TCGEN05)
+        torch.cuda.synchronize()
+        assert torch.equal(yg.view(torch.int32), yg_ref_g.view(torch.int32)), f"ragged-K forward differs ({it})"
     fused = grp.fused_count()
     if os.environ.get("TBIK_GROUP_FUSED", "1") != "0":
-        assert fused == 5, f"fused GEMM + all-reduce kernel ran {fused} times, expected 5"
+        assert fused == 7, f"fused GEMM + all-reduce kernel ran {fused} times, expected 7"
     else:
         assert fused == 0
     # host-buffer pipeline through the group: chunked epochs, same bits as the device call
