@@ -61,6 +61,23 @@ def env_rank():
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
+class StdoutToStderr:
+    """Route fd 1 to fd 2 while native libraries initialise (NCCL prints its version
+    banner on stdout): the bench's stdout carries exactly one JSON line."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -316,10 +333,11 @@ def run_tbik(args):
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
     if world > 1:
-        if share:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
+        with StdoutToStderr():
+            if share:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=dev)
     leaf = tb.LEAF_TCGEN05 if args.leaf == "tc" else tb.LEAF_FMA
     cfg = tb.BlockConfig(64, 256, 128, 0)
     M = args.m
@@ -439,7 +457,9 @@ def run_tbik(args):
         dist.broadcast_object_list(holder, src=0)
         uid = (C.c_char * 128).from_buffer_copy(holder[0])
     comm = C.c_void_p()
-    tb.api.check(tb.lib.tbik_nccl_comm_create(world, rank, dev_index, uid, C.byref(comm))) if not share else None
+    if not share:
+        with StdoutToStderr():
+            tb.api.check(tb.lib.tbik_nccl_comm_create(world, rank, dev_index, uid, C.byref(comm)))
     yb = torch.empty(M, N_OUT, device=dev, dtype=torch.bfloat16)
     yf = torch.empty(M, N_OUT, device=dev, dtype=torch.float32)
 

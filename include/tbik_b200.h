@@ -96,6 +96,16 @@ TBIK_API int tbik_device_available(void);
 /* Block until all work queued by this library on `stream` finished; reports
  * any asynchronous device fault. */
 TBIK_API tbik_status tbik_sync(void* stream);
+/* Schedule overrides (tuning and the schedule-invariance tests): change HOW work
+ * is cut and launched -- tile shapes, K splits, raster, pipeline depth, which
+ * kernel variant, fused vs separate collectives -- never the per-element
+ * arithmetic (every schedule is tested bit-identical).  Process-wide; the
+ * library reads no environment variables.  Names: tc_pair, tc_abox, tc_group_m,
+ * tc_units, tc_deep, tc_acc4, tc_skinny, sk_mt, sk_units, sk_leaf, sk_bn,
+ * fma_v1, group_fused, group_overlap, ar_two_phase_bytes.  value < 0 unsets one
+ * knob, name NULL unsets all; an unknown name is TBIK_BAD_ARGUMENT.  Every rank
+ * of a group must use the same group_* / ar_* settings. */
+TBIK_API tbik_status tbik_set_schedule(const char* name, int64_t value);
 /* Number of kernels this library has launched in this process (all devices).
  * bench.py reports the delta over its timed region as gpu_launches. */
 TBIK_API uint64_t tbik_launch_count(void);

@@ -23,6 +23,7 @@ falls back to the CPU.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 from dataclasses import dataclass
@@ -95,6 +96,28 @@ def device_available() -> bool:
 def launch_count() -> int:
     """Kernels launched by libtbik_b200 so far in this process."""
     return int(lib.tbik_launch_count())
+
+
+SCHEDULE_KNOBS = ("tc_pair", "tc_abox", "tc_group_m", "tc_units", "tc_deep", "tc_acc4", "tc_skinny", "sk_mt",
+                  "sk_units", "sk_leaf", "sk_bn", "fma_v1", "group_fused", "group_overlap", "ar_two_phase_bytes")
+
+
+def set_schedule(name, value: int = -1) -> None:
+    """tbik_set_schedule: override one launch-schedule choice (value < 0 unsets;
+    name None clears all).  Schedules never change bits -- the tests prove it."""
+    check(lib.tbik_set_schedule(name.encode() if name is not None else None, int(value)))
+
+
+@contextlib.contextmanager
+def schedule(**knobs):
+    """with schedule(tc_pair=0, sk_units=2): ... -- overrides inside, all cleared after."""
+    set_schedule(None)
+    try:
+        for k, v in knobs.items():
+            set_schedule(k, v)
+        yield
+    finally:
+        set_schedule(None)
 
 
 # ---- tensor helpers -----------------------------------------------------------------

@@ -6,7 +6,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -24,6 +26,25 @@ std::atomic<uint64_t> g_launches{0};
 }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+constexpr int64_t kUnset = INT64_MIN;
+std::atomic<int64_t> g_knobs[KNOB_COUNT];
+struct KnobInit {
+  KnobInit() {
+    for (auto& k : g_knobs) k.store(kUnset);
+  }
+} g_knob_init;
+const char* const kKnobNames[KNOB_COUNT] = {
+    "tc_pair",  "tc_abox", "tc_group_m", "tc_units",       "tc_deep",         "tc_acc4",
+    "tc_skinny", "sk_mt",  "sk_units",   "sk_leaf",        "sk_bn",           "fma_v1",
+    "group_fused", "group_overlap", "ar_two_phase_bytes"};
+}  // namespace
+
+int64_t knob(Knob k, int64_t dflt) {
+  const int64_t v = g_knobs[k].load(std::memory_order_relaxed);
+  return v == kUnset ? dflt : v;
+}
 
 tbik_status set_error(tbik_status st, const std::string& what) {
   g_last_error = what;
@@ -48,18 +69,21 @@ struct Arena {
   void* ptr = nullptr;
   size_t bytes = 0;
 };
+constexpr int kSlots = 12;
 std::mutex g_ws_mu;
-Arena g_ws[16][12];
+// (device, stream) -> slots.  std::map nodes never move, so a returned pointer
+// stays valid until that same key grows the slot.
+std::map<std::pair<int, uintptr_t>, std::array<Arena, kSlots>> g_ws;
 }  // namespace
 
-void* workspace(size_t bytes, int slot) {
+void* workspace(size_t bytes, int slot, cudaStream_t stream) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16 || slot < 0 || slot >= 12) return nullptr;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || slot < 0 || slot >= kSlots) return nullptr;
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  Arena& a = g_ws[dev][slot];
+  Arena& a = g_ws[{dev, reinterpret_cast<uintptr_t>(stream)}][slot];
   if (a.bytes >= bytes && a.ptr) return a.ptr;
   if (a.ptr) {
-    cudaDeviceSynchronize();
+    cudaStreamSynchronize(stream);  // work queued on this stream may still read the old buffer
     cudaFree(a.ptr);
     a.ptr = nullptr;
     a.bytes = 0;
@@ -153,7 +177,7 @@ tbik_status pad_operand(const void** p, int64_t* ld, int64_t rows, int64_t cols,
   const bool ok = (*ld % 8 == 0) && (reinterpret_cast<uintptr_t>(*p) & 15) == 0;
   if (ok) return TBIK_OK;
   const int64_t ldp = (cols + 7) / 8 * 8;
-  void* buf = workspace(static_cast<size_t>(rows) * ldp * 2, slot);
+  void* buf = workspace(static_cast<size_t>(rows) * ldp * 2, slot, s);
   if (!buf) return set_error(TBIK_CUDA_ERROR, "tc gemm: padding buffer allocation failed");
   TBIK_CUDA(cudaMemcpy2DAsync(buf, ldp * 2, *p, *ld * 2, cols * 2, rows, cudaMemcpyDeviceToDevice, s));
   *p = buf;
@@ -184,8 +208,8 @@ int64_t tc_split_units(const GemmView& v) {
          eff(tiles_mn * units * 2) / eff(tiles_mn * units) - 1.0 > 1300.0 / static_cast<double>(v.K) - 0.02)
     units *= 2;
   (void)next_pow2;
-  if (const char* e = std::getenv("TBIK_TC_UNITS")) {  // tuning override (power of two <= leaves)
-    const int64_t u = std::atoll(e);
+  {  // schedule knob tc_units (power of two <= leaves; same bits)
+    const int64_t u = knob(KNOB_TC_UNITS, 0);
     if (u >= 1 && u <= v.L && (u & (u - 1)) == 0) units = u;
   }
   return units;
@@ -203,7 +227,7 @@ tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mod
       GemmOut o{OUT_FULL, v.T, C, ldc, 0};
       return launch_tc_gemm(v, o, s);
     }
-    float* ws = static_cast<float*>(workspace(slice * units * sizeof(float), 0));
+    float* ws = static_cast<float*>(workspace(slice * units * sizeof(float), 0, s));
     if (!ws) return set_error(TBIK_CUDA_ERROR, "workspace allocation failed");
     GemmOut o{OUT_UNITS, v.T / units, ws, v.N, static_cast<int64_t>(slice)};
     TBIK_TRY(launch_tc_gemm(v, o, s));
@@ -212,7 +236,7 @@ tbik_status run_tree_gemm(const GemmView& v, float* C, int64_t ldc, int leaf_mod
   if (leaf_mode != TBIK_LEAF_FMA) return set_error(TBIK_BAD_ARGUMENT, "unknown leaf mode");
   const bool leaves = v.M <= 64 && slice * v.T * sizeof(float) <= (size_t(1) << 28);
   const int64_t X = leaves ? v.T : v.L;
-  float* ws = static_cast<float*>(workspace(slice * X * sizeof(float), 0));
+  float* ws = static_cast<float*>(workspace(slice * X * sizeof(float), 0, s));
   if (!ws) return set_error(TBIK_CUDA_ERROR, "workspace allocation failed");
   GemmOut o{leaves ? OUT_LEAVES : OUT_GROUPS, leaves ? 1 : v.kf, ws, v.N, static_cast<int64_t>(slice)};
   TBIK_TRY(launch_fma_gemm(v, o, s));
@@ -278,6 +302,19 @@ const char* tbik_status_string(int st) {
 }
 
 const char* tbik_last_error(void) { return g_last_error.c_str(); }
+tbik_status tbik_set_schedule(const char* name, int64_t value) {
+  if (!name) {  // NULL: clear every override
+    for (auto& k : g_knobs) k.store(kUnset);
+    return TBIK_OK;
+  }
+  for (int i = 0; i < KNOB_COUNT; ++i)
+    if (std::strcmp(name, kKnobNames[i]) == 0) {
+      g_knobs[i].store(value < 0 ? kUnset : value);
+      return TBIK_OK;
+    }
+  return set_error(TBIK_BAD_ARGUMENT, std::string("unknown schedule knob '") + name + "'");
+}
+
 int tbik_version(void) { return 100; }
 uint64_t tbik_launch_count(void) { return g_launches.load(); }
 
@@ -364,7 +401,7 @@ tbik_status tbik_tree_matmul_silu_mul(const void* A, int a_dtype, int64_t lda, c
     return launch_tc_gemm(v, o, s);
   }
   // split launches / exact leaf: f32 tree GEMM, then the same SiLU*up as a kernel
-  float* tmp = static_cast<float*>(workspace(static_cast<size_t>(M) * N * sizeof(float), 10));
+  float* tmp = static_cast<float*>(workspace(static_cast<size_t>(M) * N * sizeof(float), 10, s));
   if (!tmp) return set_error(TBIK_CUDA_ERROR, "workspace allocation failed");
   TBIK_TRY(run_tree_gemm(v, tmp, N, leaf_mode, s));
   return launch_silu_mul_il(tmp, N, M, I, static_cast<uint16_t*>(act), ld_act, s);
@@ -464,7 +501,7 @@ tbik_status tbik_row_parallel_forward_local(const void* X, int x_dtype, int64_t 
   }
   const size_t slice = static_cast<size_t>(M) * N;
   const size_t pitch = (slice + 3) & ~size_t(3);  // keep every partial 16-byte aligned
-  float* parts = static_cast<float*>(workspace(pitch * tp * sizeof(float), 2));
+  float* parts = static_cast<float*>(workspace(pitch * tp * sizeof(float), 2, s));
   if (!parts) return set_error(TBIK_CUDA_ERROR, "partials allocation failed");
   PartPtrs pp{};
   for (int r = 0; r < tp; ++r) {
@@ -478,7 +515,7 @@ tbik_status tbik_row_parallel_forward_local(const void* X, int x_dtype, int64_t 
     pp.p[r] = parts + pitch * r;
   }
   if (ldy == N) return launch_allreduce(pp, tp, Y, static_cast<int64_t>(slice), false, (reinterpret_cast<uintptr_t>(Y) & 15) == 0, s);
-  float* tmp = static_cast<float*>(workspace(slice * sizeof(float), 3));
+  float* tmp = static_cast<float*>(workspace(slice * sizeof(float), 3, s));
   if (!tmp) return set_error(TBIK_CUDA_ERROR, "allocation failed");
   TBIK_TRY(launch_allreduce(pp, tp, tmp, static_cast<int64_t>(slice), false, true, s));
   TBIK_CUDA(cudaMemcpy2DAsync(Y, ldy * sizeof(float), tmp, N * sizeof(float), N * sizeof(float), M,

@@ -30,9 +30,12 @@ int current_device_checked();  // -1 when no sm_100 device
     if (s_ != TBIK_OK) return s_;               \
   } while (0)
 
-// Per-device scratch arena shared by the launchers (grown on demand; the
-// first call at a given size must not be inside CUDA graph capture).
-void* workspace(size_t bytes, int slot = 0);
+// Scratch arena of the launchers, one per (device, stream): calls on different
+// streams (or host threads driving different streams) never share a buffer.
+// Grown on demand -- the first call at a given size on a stream must not be
+// inside CUDA graph capture; growing synchronises that stream before the old
+// buffer is freed.  A stream must not be driven by two host threads at once.
+void* workspace(size_t bytes, int slot, cudaStream_t stream);
 
 // Counts every kernel launch issued by the library (tbik_launch_count).
 void count_launch();

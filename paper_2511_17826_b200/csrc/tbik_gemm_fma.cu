@@ -278,11 +278,9 @@ tbik_status launch_v2(const GemmView& v, const GemmOut& o, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>((v.N + 127) / 128), static_cast<unsigned>((v.M + 127) / 128),
             static_cast<unsigned>(units));
   if (grid.y > 65535 || grid.z > 65535) return set_error(TBIK_UNSUPPORTED, "fma gemm: grid too large");
-  static bool attr = false;
-  if (!attr) {
-    TBIK_CUDA(cudaFuncSetAttribute(fma_tree_gemm_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, V2_SMEM));
-    attr = true;
-  }
+  // per launch: the attribute belongs to the current device's context (a host call
+  // of ~1 us, next to a kernel of >= 10 us)
+  TBIK_CUDA(cudaFuncSetAttribute(fma_tree_gemm_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, V2_SMEM));
   fma_tree_gemm_v2<<<grid, 256, V2_SMEM, s>>>(static_cast<const uint16_t*>(v.A), v.lda,
                                               static_cast<const uint16_t*>(v.B), v.ldb, v.M, v.N, v.K, v.bk, v.kf,
                                               v.T, o.mode, o.out, o.ldo, o.unit_stride);
@@ -324,7 +322,7 @@ tbik_status launch_fma_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s)
     // block_k a multiple of its 32-wide K chunk (a pure scheduling choice: same bits).
     const bool v2 = v.M > 32 && v.K % 8 == 0 && v.N % 8 == 0 && v.lda % 8 == 0 && v.ldb % 8 == 0 &&
                     v.bk % V2_KC == 0 && (reinterpret_cast<uintptr_t>(v.A) & 15) == 0 &&
-                    (reinterpret_cast<uintptr_t>(v.B) & 15) == 0 && !std::getenv("TBIK_FMA_V1");
+                    (reinterpret_cast<uintptr_t>(v.B) & 15) == 0 && knob(KNOB_FMA_V1, 0) == 0;
     if (v2) return launch_v2(v, o, s);
     return launch_typed<uint16_t, uint16_t>(v, o, s);
   }

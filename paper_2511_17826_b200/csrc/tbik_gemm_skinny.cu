@@ -449,17 +449,13 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
   }
 }
 
-int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e && *e ? std::atoi(e) : dflt;
-}
 
 }  // namespace
 
-// The skinny variant serves M <= 128 bf16 views (TBIK_TC_SKINNY=0 turns it off, a
-// pure scheduling choice: the same bits).
+// The skinny variant serves M <= 128 bf16 views (knob tc_skinny = 0 turns it off,
+// a pure scheduling choice: the same bits).
 bool tc_use_skinny(const GemmView& v) {
-  if (env_int("TBIK_TC_SKINNY", 1) == 0) return false;
+  if (knob(KNOB_TC_SKINNY, 1) == 0) return false;
   return v.adt == TBIK_BF16 && v.bdt == TBIK_BF16 && v.M >= 1 && v.M <= SK_MAX_M && v.bk % SK_KSTAGE == 0 &&
          v.N <= (int64_t{1} << 30) && v.K <= (int64_t{1} << 30);
 }
@@ -467,7 +463,7 @@ bool tc_use_skinny(const GemmView& v) {
 tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaStream_t s) {
   GemmView v = v_in;
   int mt = v.M <= 16 ? 16 : v.M <= 32 ? 32 : v.M <= 64 ? 64 : 128;
-  const int force_mt = env_int("TBIK_SK_MT", 0);  // tuning knob: a wider token tile (same bits)
+  const int force_mt = static_cast<int>(knob(KNOB_SK_MT, 0));  // tuning knob: a wider token tile (same bits)
   if ((force_mt == 32 || force_mt == 64 || force_mt == 128) && force_mt >= mt) mt = force_mt;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -489,18 +485,18 @@ tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaSt
   // sizes (measured, tools/decode_bench.py: TP=4 shard M >= 64 -11..16 %, TP=8
   // -2..5 %; TP=1/2 stay faster with 128 columns and K units).
   int bn = (v.N + SK_BN - 1) / SK_BN * std::min<int64_t>(v.L, SK_MAX_UNITS) <= want / 2 ? 64 : SK_BN;
-  const int force_bn = env_int("TBIK_SK_BN", 0);  // tuning knob (same bits)
+  const int force_bn = static_cast<int>(knob(KNOB_SK_BN, 0));  // tuning knob (same bits)
   if (force_bn == 64 || force_bn == 128) bn = force_bn;
   p.bn = bn;
   p.ntiles = static_cast<int>((v.N + bn - 1) / bn);
   // Units: aligned 2^j-group subtrees (<= 8, one cluster) until the items cover
   // ~7/8 of the SMs (K=14336 N=4096: 4 units, 128 CTAs; measured best vs 2 / 8).
-  // TBIK_SK_UNITS / TBIK_SK_LEAF override (tuning knobs; same bits).
+  // Knobs sk_units / sk_leaf override (tuning knobs; same bits).
   const int max_levels = mt == 16 ? sk_max_levels<16>() : mt == 32 ? sk_max_levels<32>()
                        : mt == 64 ? sk_max_levels<64>() : sk_max_levels<128>();
   int64_t units = 1;
   while (units * 2 <= v.L && units * 2 <= SK_MAX_UNITS && p.ntiles * units * 2 <= want) units *= 2;
-  const int force_u = env_int("TBIK_SK_UNITS", 0);
+  const int force_u = static_cast<int>(knob(KNOB_SK_UNITS, 0));
   if (force_u >= 1 && force_u <= v.L && force_u <= SK_MAX_UNITS && (force_u & (force_u - 1)) == 0) units = force_u;
   int lv = 0;
   while ((int64_t{1} << lv) < v.L / units) ++lv;
@@ -508,7 +504,7 @@ tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaSt
   // Single-leaf units (clusters of T CTAs of one leaf each) measured slower than one
   // unit per tile for the TP=8 down_proj shard (T = 7: 15 vs 9 us at M = 16, CUDA
   // graph; the per-CTA prologue outweighs 64 KB of weights), so they are opt-in.
-  const int force_leaf = env_int("TBIK_SK_LEAF", 0);
+  const int force_leaf = static_cast<int>(knob(KNOB_SK_LEAF, 0));
   const bool leaf_units = force_leaf != 0 && v.kf > 1 && v.T <= SK_MAX_UNITS;
   if (leaf_units) {
     p.units = static_cast<int>(v.T);

@@ -46,9 +46,10 @@
 // the tensor core's block_k-long accumulation.  Nothing in
 // the per-element arithmetic depends on M, the tile position, the unit split, the
 // raster or the TP shard -> batch- and TP-invariant by construction.
-#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <set>
 #include <string>
 
 #include "tbik_common.cuh"
@@ -100,22 +101,21 @@ constexpr int stages_for(int abox, bool pair, bool deep = false) {
   return deep ? (pair ? (abox == 32 ? 15 : abox == 64 ? 11 : 8) : (abox == 32 ? 9 : abox == 64 ? 7 : 6))
               : (pair ? (abox == 32 ? 12 : abox == 64 ? 9 : STAGES) : (abox == 32 ? 7 : abox == 64 ? 6 : 4));
 }
-// Per merge warp: level-3 slab (32 rows x its columns) that doubles as output
-// staging; 16 merge warps own 32 columns each (4 KB, one staging box).
-constexpr int warp_region_bytes(bool deep, int epi = 8) {
-  return deep || epi == 16 ? OUT_BUF_BYTES : L3_WARP_BYTES;
-}
-constexpr size_t smem_bytes(int epi, int abox, bool pair, bool deep = false) {
+// Per merge warp: level-3 slab (32 rows x its 64 columns) that doubles as output
+// staging (DEEP: one 4 KB staging box only).
+constexpr int MERGE_WARPS = 8;
+constexpr int warp_region_bytes(bool deep) { return deep ? OUT_BUF_BYTES : L3_WARP_BYTES; }
+constexpr size_t smem_bytes(int abox, bool pair, bool deep = false) {
   return 1024 + static_cast<size_t>(a_region_bytes(abox, stages_for(abox, pair, deep))) +
          static_cast<size_t>(stages_for(abox, pair, deep)) * b_stage_bytes(pair) + 1024 +
-         static_cast<size_t>(epi) * warp_region_bytes(deep, epi);
+         static_cast<size_t>(MERGE_WARPS) * warp_region_bytes(deep);
 }
-static_assert(smem_bytes(8, 32, true) <= 232448 && smem_bytes(8, 64, true) <= 232448 &&
-                  smem_bytes(8, 128, true) <= 232448 && smem_bytes(8, 32, false) <= 232448 &&
-                  smem_bytes(8, 64, false) <= 232448 && smem_bytes(8, 128, false) <= 232448 &&
-                  smem_bytes(8, 32, true, true) <= 232448 && smem_bytes(8, 64, true, true) <= 232448 &&
-                  smem_bytes(8, 128, true, true) <= 232448 && smem_bytes(8, 32, false, true) <= 232448 &&
-                  smem_bytes(8, 64, false, true) <= 232448 && smem_bytes(8, 128, false, true) <= 232448,
+static_assert(smem_bytes(32, true) <= 232448 && smem_bytes(64, true) <= 232448 && smem_bytes(128, true) <= 232448 &&
+                  smem_bytes(32, false) <= 232448 && smem_bytes(64, false) <= 232448 &&
+                  smem_bytes(128, false) <= 232448 && smem_bytes(32, true, true) <= 232448 &&
+                  smem_bytes(64, true, true) <= 232448 && smem_bytes(128, true, true) <= 232448 &&
+                  smem_bytes(32, false, true) <= 232448 && smem_bytes(64, false, true) <= 232448 &&
+                  smem_bytes(128, false, true) <= 232448,
               "shared memory budget");
 
 struct TcParams {
@@ -133,9 +133,7 @@ struct TcParams {
   long long unit_stride;
   float* scratch;  // [gridDim.x][levels-3][BN][BM] when levels > 3
   int tma_store;   // 1: results leave through tmC (TMA), 0: direct row stores
-  int pf;          // L2 prefetch distance in K chunks (0: off; measured slower, kept as a knob)
   int group_m;     // raster: M-blocks that share one pass over W
-  int mc;          // 1: clusters of two pairs on adjacent N tiles share A (ntiles counts tile pairs)
   int acc4;        // 1: four TMEM accumulators (items without tree levels leave cols 256-511 free)
   uint16_t* act;   // non-null: SiLU*up epilogue -- columns interleave gate (even) / up (odd);
   long long ld_act;  //   act[row][j] = bf16(silu(g[2j]) * g[2j+1]) replaces the f32 store
@@ -147,9 +145,6 @@ struct TcParams {
   uint32_t* ar_flags[8];
   uint32_t* ar_done[8];
   uint32_t* ar_counter;
-  int debug;       // TBIK_TC_DEBUG (perf experiments only; wrong results): 1 = skip the merge,
-                   // 2 = skip the output store, 4 = skip the tree above level 0,
-                   // 8 = skip the scratch levels, 16 = direct (non-TMA) output stores
 };
 
 // ---- cluster / 2-CTA PTX -----------------------------------------------------------
@@ -186,23 +181,6 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMa
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
       : "memory");
 }
-// L2 prefetch of a future TMA tile (no shared memory, no barrier).
-__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int32_t c0, int32_t c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(c0), "r"(c1)
-               : "memory");
-}
-// 2SM TMA multicast: the box lands at the same offset in every CTA of `mask`;
-// each destination pair's leader barrier (same offset) counts its bytes.
-__device__ __forceinline__ void tma_load_2d_2sm_mc(void* smem_dst, const CUtensorMap* map, uint32_t leader_bar,
-                                                   uint16_t mask, int32_t c0, int32_t c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%4, %5}], [%2], %3;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "h"(mask), "r"(c0), "r"(c1)
-      : "memory");
-}
 __device__ __forceinline__ void umma_bf16_2cta(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                                uint32_t accumulate) {
   asm volatile(
@@ -232,7 +210,7 @@ struct Item {
   int m0, n0, unit, t_begin, t_end;
 };
 
-__device__ __forceinline__ Item decode(const TcParams& p, long long item, int pid = 0) {
+__device__ __forceinline__ Item decode(const TcParams& p, long long item) {
   Item it;
   it.unit = static_cast<int>(item % p.units);
   const long long rest = item / p.units;
@@ -244,7 +222,7 @@ __device__ __forceinline__ Item decode(const TcParams& p, long long item, int pi
   const int mb = g * group_m + idx % gm;
   const int nt = idx / gm;
   it.m0 = mb * p.tile_m;
-  it.n0 = (p.mc ? 2 * nt + pid : nt) * BN;
+  it.n0 = nt * BN;
   it.t_begin = it.unit * p.tiles_per_unit;
   it.t_end = min(p.T, it.t_begin + p.tiles_per_unit);
   return it;
@@ -290,10 +268,10 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // rt = 0..nthr-1 meeting on named barrier `bar_id`: wait for the W ranks' tile
 // flags, reduce in Algorithm-2 order (collective.cpp:67-74) from the peers' send
 // slots, push the result into every rank's result slot.
-__device__ __forceinline__ void ar_reduce_item(const TcParams& p, long long item, int pid, uint32_t rank, int rt,
-                                               int nthr, int bar_id) {
+__device__ __forceinline__ void ar_reduce_item(const TcParams& p, long long item, uint32_t rank, int rt, int nthr,
+                                               int bar_id) {
   const int W = p.ar_W;
-  const Item it = decode(p, item, pid);
+  const Item it = decode(p, item);
   if (rt < W) spin_until_epoch(p.ar_flags[p.ar_rank] + ((item * 2 + rank) * W + rt), p.ar_epoch);
   named_bar(bar_id, nthr);
   const int r0 = it.m0 + static_cast<int>(rank) * BM;
@@ -362,21 +340,19 @@ __device__ __forceinline__ void ar_reduce_item(const TcParams& p, long long item
 // Warps 2-3 during the GEMM: every owned item of this pair except the pair's last
 // one, which all warps reduce together once the GEMM loops are done (the kernel's
 // tail would otherwise wait on two warps' NVLink loads).
-__device__ __forceinline__ void ar_reduce_owned(const TcParams& p, long long pair, long long npairs, int pid,
-                                                uint32_t rank) {
+__device__ __forceinline__ void ar_reduce_owned(const TcParams& p, long long pair, long long npairs, uint32_t rank) {
   const long long last = pair < p.items ? pair + (p.items - 1 - pair) / npairs * npairs : -1;
   for (long long item = pair; item < p.items; item += npairs)
     if (item != last && static_cast<int>(item % p.ar_W) == p.ar_rank)
-      ar_reduce_item(p, item, pid, rank, static_cast<int>(threadIdx.x) - 64, 64, 2);
+      ar_reduce_item(p, item, rank, static_cast<int>(threadIdx.x) - 64, 64, 2);
 }
 
 // After the GEMM loops, all threads of the CTA: the pair's last item if owned, then
 // (every CTA of this rank done) the last CTA publishes done[rank] to all peers.
-__device__ __forceinline__ void ar_finish(const TcParams& p, long long pair, long long npairs, int pid,
-                                          uint32_t rank) {
+__device__ __forceinline__ void ar_finish(const TcParams& p, long long pair, long long npairs, uint32_t rank) {
   const long long last = pair < p.items ? pair + (p.items - 1 - pair) / npairs * npairs : -1;
   if (last >= 0 && static_cast<int>(last % p.ar_W) == p.ar_rank)
-    ar_reduce_item(p, last, pid, rank, static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x), 3);
+    ar_reduce_item(p, last, rank, static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x), 3);
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -390,13 +366,15 @@ __device__ __forceinline__ void ar_finish(const TcParams& p, long long pair, lon
 }
 
 
-// EPI merge warps (two per TMEM lane quarter, splitting the 128 columns), ABOX
-// A rows staged per stage (128, or 64 / 32 for small M; stage count follows).  KF1 (used when k_first == 1, where every leaf completes a
-// group): tree level 1 never touches TMEM -- an even group stays in registers
-// and the odd sibling merges into it, so a pair of leaves costs two accumulator
-// drains instead of two drains + a level-1 store + load.
+// EPI = 8 merge warps (two per TMEM lane quarter, splitting the 128 columns).
+// ABOX A rows staged per stage (128, or 64 / 32 for small M; stage count follows).
+// KF1 (used when k_first == 1, where every leaf completes a group): tree level 1
+// never touches TMEM -- an even group stays in registers and the odd sibling
+// merges into it, so a pair of leaves costs two accumulator drains instead of two
+// drains + a level-1 store + load.
 // AR: the fused tree all-reduce variant (pair tiles, FULL mode; tbik_group.cu).
-template <int EPI, bool KF1, int ABOX, bool PAIR, bool DEEP, bool MC = false, bool AR = false>
+constexpr int EPI = MERGE_WARPS;
+template <bool KF1, int ABOX, bool PAIR, bool DEEP, bool AR = false>
 __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     tc_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const TcParams p) {
@@ -420,23 +398,19 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // MC: clusters of 4 = two CTA pairs (pid 0/1) on adjacent N tiles of the same
-  // M block; each pair's CTA r loads half of the shared 128-row A tile and
-  // multicasts it to CTA r of the other pair.
   const uint32_t crank = PAIR ? cluster_rank() : 0;
   const uint32_t rank = crank & 1;  // rank within the CTA pair
-  const int pid = MC ? static_cast<int>(crank >> 1) : 0;
   const uint32_t leader_rank = crank & ~1u;
   const bool leader = rank == 0;
-  const long long pair = MC ? blockIdx.x >> 2 : PAIR ? blockIdx.x >> 1 : blockIdx.x;  // work-item stream
-  const long long npairs = MC ? gridDim.x >> 2 : PAIR ? gridDim.x >> 1 : gridDim.x;
+  const long long pair = PAIR ? blockIdx.x >> 1 : blockIdx.x;  // work-item stream
+  const long long npairs = PAIR ? gridDim.x >> 1 : gridDim.x;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], PAIR ? 2 : 1);  // one arrive.expect_tx per CTA (leader's copy used)
-      mbar_init(&empty[s], MC ? 2 : 1);  // a multicast commit from each pair leader that reads the stage
+      mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 4; ++b) {
       mbar_init(&tfull[b], 1);   // multicast commit
@@ -463,21 +437,12 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (long long item = pair; item < p.items; item += npairs) {
-        const Item it = decode(p, item, pid);
+        const Item it = decode(p, item);
         const int am = it.m0 + static_cast<int>(rank) * BM;
         const int bn = it.n0 + static_cast<int>(rank) * (BN / 2);
-        const int k_end = min(it.t_end * p.bk, p.K);
         for (int t = it.t_begin; t < it.t_end; ++t) {
           const int nch = tile_chunks(p, t);
           for (int c = 0; c < nch; ++c) {
-            if (p.pf) {  // warm L2 for the chunk pf stages ahead (its DRAM latency overlaps)
-              const int kp = t * p.bk + (c + p.pf) * KSTAGE;
-              if (kp < k_end) {
-                tma_prefetch_l2(&tmA, kp, am);
-                tma_prefetch_l2(&tmB, bn, kp);
-                if constexpr (!PAIR) tma_prefetch_l2(&tmB, bn + BN / 2, kp);
-              }
-            }
             mbar_wait(&empty[stage], phase ^ 1);
             const uint32_t fb = full_leader0 + stage * 8;
             if (leader)
@@ -485,11 +450,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             else
               mbar_arrive_expect_tx_cluster(fb, TX_BYTES);
             const int k = t * p.bk + c * KSTAGE;
-            if constexpr (MC) {  // my half of the pair-shared A tile, to both pairs
-              tma_load_2d_2sm_mc(sA + stage * A_STRIDE + pid * (A_STAGE_BYTES / 2), &tmA, fb,
-                                 static_cast<uint16_t>(0x5u << rank), k, am + pid * (BM / 2));
-              tma_load_2d_2sm(sB + stage * B_STAGE, &tmB, fb, bn, k);
-            } else if constexpr (PAIR) {
+            if constexpr (PAIR) {
               tma_load_2d_2sm(sA + stage * A_STRIDE, &tmA, fb, k, am);
               tma_load_2d_2sm(sB + stage * B_STAGE, &tmB, fb, bn, k);
             } else {  // all 128 columns: two 64-column atoms
@@ -513,7 +474,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       uint32_t phase = 0;
       uint32_t acc_iter = 0;
       for (long long item = pair; item < p.items; item += npairs) {
-        const Item it = decode(p, item, pid);
+        const Item it = decode(p, item);
         for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
           const int buf = p.acc4 ? acc_iter & 3 : acc_iter & 1;
           const uint32_t use = p.acc4 ? acc_iter >> 2 : acc_iter >> 1;
@@ -539,9 +500,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               else
                 umma_bf16(d, adesc, bdesc, IDESC_1CTA, (c | kk) != 0 ? 1u : 0u);
             }
-            if constexpr (MC)
-              umma_commit_2cta(&empty[stage], 0xF);  // both pairs read this stage's A
-            else if constexpr (PAIR)
+            if constexpr (PAIR)
               umma_commit_2cta(&empty[stage], 0x3);
             else
               umma_commit(&empty[stage]);
@@ -565,7 +524,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     // Algorithm-2 order (collective.cpp:67-74) straight from the peers' send slots
     // and push the result into every rank's result slot over NVLink -- while the
     // tensor cores of the same SM already work on the next items.
-    ar_reduce_owned(p, pair, npairs, pid, rank);
+    ar_reduce_owned(p, pair, npairs, rank);
   }
   } else {
     // ---------------- merge warps (the TBIK reduction), both CTAs ----------------
@@ -589,14 +548,14 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             ? p.scratch + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - FS + 1) * (BM * BN) +
                            static_cast<size_t>(col0) * BM + static_cast<size_t>(row_in_tile) * 4
             : nullptr;
-    uint8_t* l3 = sL3 + (warp - 4) * warp_region_bytes(DEEP, EPI);  // [COLS/4][32 lanes][float4] (+ staging)
-    constexpr bool ONE_BOX = DEEP || EPI == 16;  // a single staging box per warp
+    uint8_t* l3 = sL3 + (warp - 4) * warp_region_bytes(DEEP);  // [COLS/4][32 lanes][float4] (+ staging)
+    constexpr bool ONE_BOX = DEEP;  // a single staging box per warp
 
     float g[COLS];  // level 0: the running leaf-group value
     int xb = 0;      // output staging buffer toggle
     uint32_t acc_iter = 0;
     for (long long item = pair; item < p.items; item += npairs) {
-      const Item it = decode(p, item, pid);
+      const Item it = decode(p, item);
       const int grow = it.m0 + static_cast<int>(rank) * BM + row_in_tile;
       const bool row_ok = grow < p.M;
       const int ncols = min(COLS, p.N - it.n0 - col0);
@@ -614,12 +573,10 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         // are in registers.
         uint32_t r[NCH < 2 ? 2 : NCH][32];
         const bool odd = KF1 && p.levels >= 1 && (groups_done & 1u);
-        if (!(p.debug & 1)) {
 #pragma unroll
-          for (int c = 0; c < NCH; ++c) tmem_ld32r(acc + c * 32, r[c]);
+        for (int c = 0; c < NCH; ++c) tmem_ld32r(acc + c * 32, r[c]);
 #pragma unroll
-          for (int c = 0; c < NCH; ++c) tmem_wait_ld_dep(r[c]);
-        }
+        for (int c = 0; c < NCH; ++c) tmem_wait_ld_dep(r[c]);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -628,7 +585,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           else
             mbar_arrive_cluster(tempty_leader0 + buf * 8);
         }
-        if (p.debug & 1) continue;
         int unit_out = p.mode == OUT_UNITS ? it.unit : 0;
         if (p.mode == OUT_LEAVES) {
           // verification dump: the raw leaf P_t goes to slice t
@@ -661,7 +617,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         }
         if (!KF1 && ++t_in_group < p.kf) continue;
         t_in_group = 0;
-        if (p.debug & 4) continue;
 
         // Binary counter over completed groups (levels 1..p.levels, matmul.cpp:107-123):
         // levels 1-2 in TMEM columns [256, 512), deeper levels (touched once per 8+
@@ -698,7 +653,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
                 g[i + 3] = __fadd_rn(g[i + 3], x.w);
               }
               __syncwarp();  // the region may become output staging right after
-            } else if (!(p.debug & 8)) {
+            } else {
               const float* sp = scratch_base + static_cast<size_t>(level - FS) * (BM * BN);
 #pragma unroll
               for (int i = 0; i < COLS; i += 4) {
@@ -730,7 +685,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
               for (int i = 0; i < COLS; i += 4)
                 *reinterpret_cast<float4*>(l3 + ((i / 4) * 32 + lane) * 16) =
                     make_float4(g[i], g[i + 1], g[i + 2], g[i + 3]);
-            } else if (!(p.debug & 8)) {
+            } else {
               float* sp = scratch_base + static_cast<size_t>(level - FS) * (BM * BN);
 #pragma unroll
               for (int i = 0; i < COLS; i += 4)
@@ -740,7 +695,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           }
         }
         }  // the carry left the top level: g is this unit's complete (sub)tree
-        if (p.debug & 2) continue;
         if (p.act) {
           // fused SiLU(gate) * up (tb_silu_mul_bf16, the same ops as tbik_silu_mul):
           // this thread's 64 columns are 32 (gate, up) pairs -> 32 bf16 outputs
@@ -822,7 +776,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 
   if constexpr (AR) {
     __syncthreads();  // every role's loop is done (the merge warps published all items)
-    ar_finish(p, pair, npairs, pid, rank);
+    ar_finish(p, pair, npairs, rank);
   }
   tc_fence_before();
   cluster_sync();
@@ -934,38 +888,36 @@ bool tc_supported(const GemmView& v, std::string* why) {
   return true;
 }
 
-bool tc_use_wide(const GemmView& v);
 // Single-CTA 128 x 128 tiles when every row fits one CTA (M <= 128): the pair
-// tile's second 128 rows would be MMA work on padding.  TBIK_TC_PAIR=0/1 forces
-// the choice (a pure scheduling knob: same bits).
+// tile's second 128 rows would be MMA work on padding.  Schedule knob tc_pair
+// forces the choice (a pure scheduling knob: same bits).
 bool tc_use_pair(const GemmView& v) {
-  if (const char* e = std::getenv("TBIK_TC_PAIR"))
-    if (*e) return std::atoi(e) != 0;
+  const int64_t k = knob(KNOB_TC_PAIR, -1);
+  if (k == 0 || k == 1) return k == 1;
   return v.M > BM;
 }
 
-int64_t tc_pair_tiles(const GemmView& v) {
-  if (tc_use_wide(v)) return tc_wide_pair_tiles(v);
-  return ((v.M + PAIR_M - 1) / PAIR_M) * ((v.N + BN - 1) / BN);
-}
+int64_t tc_pair_tiles(const GemmView& v) { return ((v.M + PAIR_M - 1) / PAIR_M) * ((v.N + BN - 1) / BN); }
 
-int64_t tc_parallel_slots(const GemmView& v) { return tc_use_wide(v) || tc_use_pair(v) ? sm_count() / 2 : sm_count(); }
+int64_t tc_parallel_slots(const GemmView& v) { return tc_use_pair(v) ? sm_count() / 2 : sm_count(); }
 
 int64_t tc_tiles(const GemmView& v) {
-  if (tc_use_wide(v) || tc_use_pair(v)) return tc_pair_tiles(v);
+  if (tc_use_pair(v)) return tc_pair_tiles(v);
   return ((v.M + BM - 1) / BM) * ((v.N + BN - 1) / BN);
 }
 
 // Diagnostics build only (see tools/tc_stats.py); the production kernel carries no counters.
 int tc_debug_stats(unsigned long long*, int) { return 0; }
 
-// 256 x 256 pair tiles (tbik_gemm_tc_wide.cu) when the level-1 traffic allows it;
-// TBIK_TC_WIDE=0/1 forces the choice (a pure scheduling knob: same bits).
-bool tc_use_wide(const GemmView& v) {
-  const char* e = std::getenv("TBIK_TC_WIDE");
-  if (e && *e) return std::atoi(e) != 0;
-  return false;
+namespace {
+// cudaFuncSetAttribute applies to one device context: remembered per (device, kernel).
+bool attr_done(int dev, const void* kern) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  return !done.insert({dev, kern}).second;
 }
+}  // namespace
 
 tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t s) {
   GemmView v = v_in;
@@ -976,24 +928,16 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   std::string why;
   if (!tc_supported(v, &why)) return set_error(TBIK_UNSUPPORTED, why);
   if (o.mode == OUT_GROUPS) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: GROUPS mode is FMA-only");
-  if (tc_use_wide(v) && !o.act) return launch_tc_gemm_wide(v, o, s);
   // A rows staged per stage: the fewest that still cover every row of the pair
-  // tile's leader CTA (TBIK_TC_ABOX overrides, a pure scheduling knob).
+  // tile's leader CTA (knob tc_abox overrides, a pure scheduling knob).
   int abox = v.M <= 32 ? 32 : v.M <= 64 ? 64 : 128;
-  if (const char* e = std::getenv("TBIK_TC_ABOX")) {
-    const int a = std::atoi(e);
-    if ((a == 32 && v.M <= 32) || (a == 64 && v.M <= 64) || a == 128) abox = a;
+  {
+    const int64_t a = knob(KNOB_TC_ABOX, 0);
+    if ((a == 32 && v.M <= 32) || (a == 64 && v.M <= 64) || a == 128) abox = static_cast<int>(a);
   }
-  // MC (experiment knob TBIK_TC_MC=1): clusters of two pairs sharing the A tile
-  // through TMA multicast (pair tiles with 128-row A staging only).
-  const bool mc_req = [] {
-    const char* e = std::getenv("TBIK_TC_MC");
-    return e && *e && std::atoi(e) != 0;
-  }();
-  const bool mc = mc_req && tc_use_pair(v) && !tc_use_wide(v) && abox == 128;
   CUtensorMap mA, mB;
   TBIK_TRY(make_map_2d(&mA, v.A, static_cast<uint64_t>(v.K), static_cast<uint64_t>(v.M),
-                       static_cast<uint64_t>(v.lda) * 2, KSTAGE, static_cast<uint32_t>(mc ? BM / 2 : abox)));
+                       static_cast<uint64_t>(v.lda) * 2, KSTAGE, static_cast<uint32_t>(abox)));
   TBIK_TRY(make_map_2d(&mB, v.B, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.K),
                        static_cast<uint64_t>(v.ldb) * 2, BN / 2, KSTAGE));
   TcParams p{};
@@ -1025,54 +969,39 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
     p.units = static_cast<int>((v.T + p.tiles_per_unit - 1) / p.tiles_per_unit);
     if (o.mode == OUT_FULL && p.units != 1) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: FULL needs 1 unit");
   }
-  static const int dbg = [] {
-    const char* e = std::getenv("TBIK_TC_DEBUG");
-    return e ? std::atoi(e) : 0;
-  }();
-  p.debug = dbg;
-  static const int pf = [] {
-    const char* e = std::getenv("TBIK_TC_PF");
-    return e && *e ? std::atoi(e) : 0;
-  }();
-  p.pf = pf;
-  {  // raster knob (pure scheduling, same bits), read per launch
-    const char* e = std::getenv("TBIK_TC_GROUP_M");
-    const int gm = e && *e ? std::atoi(e) : GROUP_M;
-    p.group_m = gm >= 1 ? gm : GROUP_M;
+  {  // raster knob (pure scheduling, same bits)
+    const int64_t gm = knob(KNOB_TC_GROUP_M, GROUP_M);
+    p.group_m = gm >= 1 ? static_cast<int>(gm) : GROUP_M;
   }
   const bool pair = tc_use_pair(v);
   p.tile_m = pair ? PAIR_M : BM;
   p.mblocks = static_cast<int>((v.M + p.tile_m - 1) / p.tile_m);
   p.ntiles = static_cast<int>((v.N + BN - 1) / BN);
-  p.mc = mc ? 1 : 0;
-  p.acc4 = p.levels == 0 ? 1 : 0;  // no level slot in TMEM (TBIK_TC_ACC4=0 turns it off)
-  if (const char* e = std::getenv("TBIK_TC_ACC4"))
-    if (*e && std::atoi(e) == 0) p.acc4 = 0;
-  if (mc) p.ntiles = (p.ntiles + 1) / 2;  // work items are tile pairs
+  p.acc4 = p.levels == 0 && knob(KNOB_TC_ACC4, 1) != 0 ? 1 : 0;  // no level slot in TMEM: 4 accumulators
   p.items = static_cast<long long>(p.mblocks) * p.ntiles * p.units;
-  const long long slots = mc ? sm_count() / 4 : pair ? sm_count() / 2 : sm_count();
+  const long long slots = pair ? sm_count() / 2 : sm_count();
   const long long nstreams = p.items < slots ? p.items : slots;
-  dim3 grid(static_cast<unsigned>(mc ? 4 * nstreams : pair ? 2 * nstreams : nstreams));
+  dim3 grid(static_cast<unsigned>(pair ? 2 * nstreams : nstreams));
   const bool kf1 = p.kf == 1;
   // DEEP (see stages_for) when the items have at most 2 tree levels, or when there
   // are at most 2 waves of them: short launches are bound by load latency and the
   // extra stages pay for level 3 in scratch (K=14336, N=4096: M=256..1024 +5..9%,
   // M=2048 even; profiles/r01_tc_deep_midm.txt).  With 3+ levels and many waves
   // the on-chip level 3 measured faster (1146 vs 1108 TFLOP/s at the bench shape).
-  // TBIK_TC_DEEP=0/1 forces it (a pure scheduling knob -- same bits).
   // ... but not with 4+ levels (k_first = 1, K = 4096: 16 groups per item), where two
   // scratch levels cost more than the extra stages buy (tools/midm_sweep.py: o_proj
   // K=4096 N=4096 M=512..1024 +8-11 % without DEEP, down_proj K=14336 unchanged).
   // k_first == 1 keeps levels 1-3 off shared memory, so DEEP is free up to 3 levels
-  // there and the shared-memory level 4 beats scratch above.
+  // there and the shared-memory level 4 beats scratch above.  Knob tc_deep forces it.
   bool deep = kf1 ? p.levels <= 3 : p.levels <= 2 || (p.items <= 2 * slots && p.levels <= 3);
-  if (const char* e = std::getenv("TBIK_TC_DEEP"))
-    if (*e) deep = std::atoi(e) != 0;
-  if (mc) deep = false;
+  {
+    const int64_t k = knob(KNOB_TC_DEEP, -1);
+    if (k == 0 || k == 1) deep = k == 1;
+  }
   const int first_scratch = (kf1 ? 4 : 3) + (deep ? 0 : 1);
   if (p.levels >= first_scratch) {
     const size_t n = static_cast<size_t>(grid.x) * (p.levels - first_scratch + 1) * BM * BN;
-    p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1));
+    p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1, s));
     if (!p.scratch) return set_error(TBIK_CUDA_ERROR, "tc gemm: scratch allocation failed");
   }
   // Results leave through a TMA store when the output is 16-byte addressable.
@@ -1080,43 +1009,54 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   std::memset(&mC, 0, sizeof(mC));
   const uint64_t ustride = o.mode != OUT_FULL ? static_cast<uint64_t>(o.unit_stride)
                                               : static_cast<uint64_t>(o.ldo) * static_cast<uint64_t>(v.M);
-  p.tma_store = !o.act && !(dbg & 16) && (reinterpret_cast<uintptr_t>(o.out) & 15) == 0 && o.ldo % 4 == 0 &&
-                ustride % 4 == 0;
+  p.tma_store = !o.act && (reinterpret_cast<uintptr_t>(o.out) & 15) == 0 && o.ldo % 4 == 0 && ustride % 4 == 0;
   if (p.tma_store)
     TBIK_TRY(make_map_out(&mC, o.out, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.M),
                           static_cast<uint64_t>(p.units), static_cast<uint64_t>(o.ldo) * 4, ustride * 4));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  using Kern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
   // Fused GEMM -> tree all-reduce (tbik_group.cu) for FULL pair-tile launches whose
   // output is the group's send slot.
   if (FusedAr* ar = g_fused_ar) {
-    bool ok = pair && !mc && abox == 128 && o.mode == OUT_FULL && !o.act && p.tma_store && o.ldo == v.N && ar->W > 1 &&
-                    ar->W <= 8 && p.items * 2 * ar->W <= ar->flag_capacity && o.out == ar->src[ar->rank];
-    // Every CTA pair of every rank spins on peer tile flags before it exits, so
-    // the whole grid must be co-resident: cap at the clusters the occupancy
-    // calculator says fit (a static property of kernel and device, the same on
-    // every rank); a grid that would not fit takes the separate path instead.
-    static int max_ar_clusters[16] = {};
-    int adev = 0;
-    cudaGetDevice(&adev);
-    if (ok && adev >= 0 && adev < 16 && !max_ar_clusters[adev]) {
-      auto k = tc_tree_gemm_kernel<8, false, 128, true, false, false, true>;
-      const size_t sm = smem_bytes(8, 128, true, false);
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-      cudaLaunchConfig_t qc{};
-      qc.gridDim = dim3(2);
-      qc.blockDim = dim3(128 + 32 * 8);
-      qc.dynamicSmemBytes = sm;
-      cudaLaunchAttribute qa[1];
-      qa[0].id = cudaLaunchAttributeClusterDimension;
-      qa[0].val.clusterDim.x = 2;
-      qa[0].val.clusterDim.y = 1;
-      qa[0].val.clusterDim.z = 1;
-      qc.attrs = qa;
-      qc.numAttrs = 1;
-      int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, k, &qc) != cudaSuccess || n < 1) n = 1;
-      max_ar_clusters[adev] = n;
+    bool ok = pair && abox == 128 && o.mode == OUT_FULL && !o.act && p.tma_store && o.ldo == v.N && ar->W > 1 &&
+              ar->W <= 8 && p.items * 2 * ar->W <= ar->flag_capacity && o.out == ar->src[ar->rank];
+    // Every CTA pair of every rank spins on peer tile flags before it exits, so the
+    // whole grid must be co-resident: cap at the clusters the occupancy calculator
+    // says fit (a static property of kernel and device, the same on every rank); a
+    // grid that would not fit takes the separate path instead.
+    if (ok) {
+      static std::mutex mu;
+      static std::map<int, int> max_clusters;
+      std::lock_guard<std::mutex> lk(mu);
+      auto f = max_clusters.find(dev);
+      if (f == max_clusters.end()) {
+        const Kern k = deep ? (kf1 ? tc_tree_gemm_kernel<true, 128, true, true, true>
+                                   : tc_tree_gemm_kernel<false, 128, true, true, true>)
+                            : (kf1 ? tc_tree_gemm_kernel<true, 128, true, false, true>
+                                   : tc_tree_gemm_kernel<false, 128, true, false, true>);
+        const size_t sm = smem_bytes(128, true, deep);
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+        cudaLaunchConfig_t qc{};
+        qc.gridDim = dim3(2);
+        qc.blockDim = dim3(128 + 32 * EPI);
+        qc.dynamicSmemBytes = sm;
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = 2;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        qc.attrs = qa;
+        qc.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k, &qc) != cudaSuccess || n < 1) {
+          cudaGetLastError();
+          n = 1;
+        }
+        f = max_clusters.emplace(dev, n).first;
+      }
+      if (nstreams > f->second) ok = false;
     }
-    if (ok && adev >= 0 && adev < 16 && nstreams > max_ar_clusters[adev]) ok = false;
     if (ok) {
       p.ar_W = ar->W;
       p.ar_rank = ar->rank;
@@ -1131,41 +1071,25 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
       ar->used = true;
     }
   }
-  using Kern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
-#define TBIK_TC_K(D, P)                                                                                  \
-  {{tc_tree_gemm_kernel<8, false, 32, P, D>, tc_tree_gemm_kernel<8, true, 32, P, D>},                   \
-   {tc_tree_gemm_kernel<8, false, 64, P, D>, tc_tree_gemm_kernel<8, true, 64, P, D>},                   \
-   {tc_tree_gemm_kernel<8, false, 128, P, D>, tc_tree_gemm_kernel<8, true, 128, P, D>}}
+#define TBIK_TC_K(D, P)                                                                                        \
+  {{tc_tree_gemm_kernel<false, 32, P, D>, tc_tree_gemm_kernel<true, 32, P, D>},                               \
+   {tc_tree_gemm_kernel<false, 64, P, D>, tc_tree_gemm_kernel<true, 64, P, D>},                               \
+   {tc_tree_gemm_kernel<false, 128, P, D>, tc_tree_gemm_kernel<true, 128, P, D>}}
   static const Kern table[2][2][3][2] = {{TBIK_TC_K(false, false), TBIK_TC_K(false, true)},
                                          {TBIK_TC_K(true, false), TBIK_TC_K(true, true)}};
 #undef TBIK_TC_K
   const int ai = abox == 32 ? 0 : abox == 64 ? 1 : 2;
-  // EPI16 (experiment knob TBIK_TC_EPI=16): 16 merge warps of 32 columns, pair
-  // tiles with 128-row staging, not DEEP / MC.
-  const bool epi16 = [] {
-    const char* e = std::getenv("TBIK_TC_EPI");
-    return e && std::atoi(e) == 16;
-  }() && pair && abox == 128 && !deep && !mc && p.ar_W <= 1;
   const bool ar_on = p.ar_W > 1;
-  const Kern kern = ar_on ? (deep ? (kf1 ? tc_tree_gemm_kernel<8, true, 128, true, true, false, true>
-                                         : tc_tree_gemm_kernel<8, false, 128, true, true, false, true>)
-                                  : (kf1 ? tc_tree_gemm_kernel<8, true, 128, true, false, false, true>
-                                         : tc_tree_gemm_kernel<8, false, 128, true, false, false, true>))
-                   : mc ? (kf1 ? tc_tree_gemm_kernel<8, true, 128, true, false, true>
-                              : tc_tree_gemm_kernel<8, false, 128, true, false, true>)
-                   : epi16 ? (kf1 ? tc_tree_gemm_kernel<16, true, 128, true, false, false>
-                                  : tc_tree_gemm_kernel<16, false, 128, true, false, false>)
-                           : table[deep][pair][ai][kf1];
-  const int epi = epi16 ? 16 : 8;
-  const int nthreads = 128 + 32 * epi;
-  const size_t smem = smem_bytes(epi, abox, pair, deep);
-  static bool attr_set[16][2][3][2][2][2][2][2] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 16 && !attr_set[dev][pair][ai][kf1][deep][mc][epi16][ar_on]) {
+  const Kern kern = ar_on ? (deep ? (kf1 ? tc_tree_gemm_kernel<true, 128, true, true, true>
+                                         : tc_tree_gemm_kernel<false, 128, true, true, true>)
+                                  : (kf1 ? tc_tree_gemm_kernel<true, 128, true, false, true>
+                                         : tc_tree_gemm_kernel<false, 128, true, false, true>))
+                          : table[deep][pair][ai][kf1];
+  const int nthreads = 128 + 32 * EPI;
+  const size_t smem = smem_bytes(abox, pair, deep);
+  if (!attr_done(dev, reinterpret_cast<const void*>(kern))) {
     TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     if (pair) TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-    attr_set[dev][pair][ai][kf1][deep][mc][epi16][ar_on] = true;
   }
   cudaLaunchConfig_t lc{};
   lc.gridDim = grid;
@@ -1174,27 +1098,11 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   lc.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = mc ? 4 : pair ? 2 : 1;
+  attr[0].val.clusterDim.x = pair ? 2 : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  if (mc) {
-    // 4-CTA clusters must fit inside a GPC: the persistent grid is sized to the
-    // clusters that can be co-resident (not SMs / 4), or the surplus ones would
-    // run as a second wave after everyone else.
-    static int max_clusters[16] = {};
-    if (dev >= 0 && dev < 16 && !max_clusters[dev]) {
-      int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, kern, &lc) != cudaSuccess || n < 1) n = sm_count() / 4;
-      max_clusters[dev] = n;
-    }
-    const long long cap = dev >= 0 && dev < 16 ? max_clusters[dev] : sm_count() / 4;
-    if (nstreams > cap) {
-      lc.gridDim = dim3(static_cast<unsigned>(4 * cap));
-      if (p.levels >= first_scratch && !p.scratch) return set_error(TBIK_CUDA_ERROR, "tc gemm: scratch");
-    }
-  }
   TBIK_CUDA(cudaLaunchKernelEx(&lc, kern, mA, mB, mC, p));
   count_launch();
   return TBIK_OK;

@@ -392,10 +392,7 @@ tbik_status group_all_reduce(tbik_group* g, const float* partial, float* out, in
     gp.flags[r] = ready_flags(g->peer_region[r], g->capacity);
     gp.done[r] = done_flags(g->peer_region[r], g->capacity);
   }
-  static const int64_t two_phase_bytes = [] {
-    const char* e = std::getenv("TBIK_AR_TWO_PHASE_BYTES");  // schedule knob only: same bits either way
-    return e && *e ? std::atoll(e) : kTwoPhaseBytes;
-  }();
+  const int64_t two_phase_bytes = knob(KNOB_AR_TWO_PHASE_BYTES, kTwoPhaseBytes);  // schedule only: same bits
   // The path must be the same on every rank: it depends only on (W, elems).
   if (g->W > 1 && elems % 4 == 0 && (force_two_phase || elems * 4 >= two_phase_bytes)) {
     const int64_t n4 = elems / 4;
@@ -446,7 +443,7 @@ tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* X_shard, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t xsz = x_dtype == TBIK_BF16 ? 2 : 4;
 
-  // Fused GEMM -> all-reduce (one kernel, tile by tile; TBIK_GROUP_FUSED=0 disables):
+  // Fused GEMM -> all-reduce (one kernel, tile by tile; schedule knob group_fused = 0 disables):
   // the tcgen05 GEMM writes its partial into this epoch's peer-visible send slot,
   // publishes every finished 256 x 128 tile to the tile's owner rank (item % W), and
   // warps 2-3 of every CTA reduce the tiles this rank owns in Algorithm-2 order
@@ -458,10 +455,7 @@ tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* X_shard, 
   // last rank of a ragged K has fewer tiles, and the K-split / skinny heuristics
   // of tbik_tree_matmul look at it): M > 128 (pair tiles), N % 4 == 0 (TMA store).
   // The GEMM is then launched as ONE FULL-mode pair-tile launch on every rank.
-  static const bool fused_on = [] {
-    const char* e = std::getenv("TBIK_GROUP_FUSED");
-    return !(e && *e && std::atoi(e) == 0);
-  }();
+  const bool fused_on = knob(KNOB_GROUP_FUSED, 1) != 0;
   if (fused_on && g->W > 1 && leaf_mode == TBIK_LEAF_TCGEN05 && M > 128 && N % 4 == 0 &&
       x_dtype == TBIK_BF16 && w_dtype == TBIK_BF16) {
     for (int r = 0; r < g->W; ++r)
@@ -511,11 +505,8 @@ tbik_status tbik_group_row_parallel_forward(tbik_group* g, const void* X_shard, 
   // peer has finished READING this rank's slot -- the one-shot path proves only
   // that this rank finished reading the peers' slots.  Chunking rows never
   // changes bits (batch invariance), and every rank cuts the same chunks (they
-  // depend only on M).  TBIK_GROUP_OVERLAP=0 disables it.
-  static const bool overlap_on = [] {
-    const char* e = std::getenv("TBIK_GROUP_OVERLAP");
-    return !(e && *e && std::atoi(e) == 0);
-  }();
+  // depend only on M).  Schedule knob group_overlap = 0 disables it.
+  const bool overlap_on = knob(KNOB_GROUP_OVERLAP, 1) != 0;
   constexpr int kChunks = 4, kReserve = 16;
   const bool overlap = overlap_on && g->W > 1 && M >= 2 * 256 && N % 4 == 0 && M * N * 4 >= (int64_t(8) << 20);
   if (!overlap) {

@@ -12,12 +12,13 @@
 // so PCIe runs in both directions at once and the GEMM hides under the
 // transfers.  Splitting the rows is invisible in the bits: every output row is
 // the same function of its own A row at any M (batch invariance; the per-element
-// tree never depends on M).  Double-buffered staging in the per-device arena
+// tree never depends on M).  Double-buffered staging in the caller stream's arena
 // (slots 4-7); cross-stream order through events only, so the call returns as
 // soon as the work is enqueued and `stream` is ordered after the last D2H.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -34,14 +35,15 @@ struct HostIoCtx {
   cudaEvent_t start, h2d_done[2], comp_done[2], d2h_done[2];
 };
 std::mutex g_hio_mu;
-HostIoCtx g_hio[16];
+// One copy-stream pair + events per (device, caller stream): two callers on two
+// streams never share staging buffers (workspace is keyed the same way) or events.
+std::map<std::pair<int, uintptr_t>, HostIoCtx> g_hio;
 
-tbik_status ctx_for_device(HostIoCtx** out) {
+tbik_status ctx_for_stream(cudaStream_t s, HostIoCtx** out) {
   int dev = 0;
   TBIK_CUDA(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 16) return set_error(TBIK_BAD_ARGUMENT, "device index out of range");
   std::lock_guard<std::mutex> lk(g_hio_mu);
-  HostIoCtx& c = g_hio[dev];
+  HostIoCtx& c = g_hio[{dev, reinterpret_cast<uintptr_t>(s)}];
   if (!c.init) {
     TBIK_CUDA(cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking));
     TBIK_CUDA(cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking));
@@ -72,7 +74,7 @@ template <class F>
 tbik_status pipeline(const void* A_host, int adt, int64_t lda, int64_t K, float* C_host, int64_t ldc, int64_t M,
                      int64_t N, int64_t chunk, cudaStream_t s, F compute) {
   HostIoCtx* cx = nullptr;
-  TBIK_TRY(ctx_for_device(&cx));
+  TBIK_TRY(ctx_for_stream(s, &cx));
   // Row chunks: a fixed size when the caller asks for one; by default ramped
   // (128, 256, then up to 512, then 256, 128) so the pipeline fills and drains on
   // small copies while the bulk moves in large ones.
@@ -96,8 +98,8 @@ tbik_status pipeline(const void* A_host, int adt, int64_t lda, int64_t K, float*
   char* dA[2];
   float* dC[2];
   for (int b = 0; b < 2; ++b) {
-    dA[b] = static_cast<char*>(workspace(a_bytes, 4 + b));
-    dC[b] = static_cast<float*>(workspace(c_bytes, 6 + b));
+    dA[b] = static_cast<char*>(workspace(a_bytes, 4 + b, s));
+    dC[b] = static_cast<float*>(workspace(c_bytes, 6 + b, s));
     if (!dA[b] || !dC[b]) return set_error(TBIK_CUDA_ERROR, "host-io staging allocation failed");
   }
   TBIK_CUDA(cudaEventRecord(cx->start, s));

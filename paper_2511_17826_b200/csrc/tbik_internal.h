@@ -77,9 +77,29 @@ struct FusedAr {
   bool used = false;
 };
 FusedAr* set_tc_fused_ar(FusedAr* ctx);
-// The 256 x 256 pair-tile variant (tbik_gemm_tc_wide.cu).
-tbik_status launch_tc_gemm_wide(const GemmView& v, const GemmOut& o, cudaStream_t s);
-int64_t tc_wide_pair_tiles(const GemmView& v);
+
+// Schedule overrides (tbik_set_schedule): how the work is cut and launched, never
+// the per-element arithmetic.  Process-wide, set only through the C ABI (the
+// library reads no environment variables).  knob() returns `dflt` when unset.
+enum Knob {
+  KNOB_TC_PAIR,          // 0/1: single-CTA 128x128 vs CTA-pair 256x128 tiles
+  KNOB_TC_ABOX,          // 32/64/128: A rows staged per pipeline stage
+  KNOB_TC_GROUP_M,       // raster: M blocks sharing one pass over W
+  KNOB_TC_UNITS,         // K split of every output tile (power of two <= leaf groups)
+  KNOB_TC_DEEP,          // 0/1: tree level 3 in scratch + deeper pipeline
+  KNOB_TC_ACC4,          // 0: never four TMEM accumulators
+  KNOB_TC_SKINNY,        // 0: no swap-AB kernel for M <= 128
+  KNOB_SK_MT,            // skinny token tile 32/64/128
+  KNOB_SK_UNITS,         // skinny K units
+  KNOB_SK_LEAF,          // 1: skinny single-leaf units
+  KNOB_SK_BN,            // skinny weight tile 64/128
+  KNOB_FMA_V1,           // 1: the first FMA-leaf kernel
+  KNOB_GROUP_FUSED,      // 0: no fused GEMM + all-reduce kernel
+  KNOB_GROUP_OVERLAP,    // 0: no chunked GEMM / all-reduce overlap
+  KNOB_AR_TWO_PHASE_BYTES,  // payload bytes from which the group all-reduce is two-phase
+  KNOB_COUNT
+};
+int64_t knob(Knob k, int64_t dflt);
 
 tbik_status launch_tree_combine(const float* ws, int64_t X, int64_t fold, int64_t rows,
                                 int64_t cols, float* out, int64_t ldo, cudaStream_t s);

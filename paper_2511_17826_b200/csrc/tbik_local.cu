@@ -290,7 +290,7 @@ tbik_status tbik_local_group_row_parallel_forward(tbik_local_group* g, const voi
     if (ldy == N) {
       st = launch_allreduce(pp, g->W, Y, M * N, false, (reinterpret_cast<uintptr_t>(Y) & 15) == 0, s0);
     } else {
-      float* tmp = static_cast<float*>(workspace(bytes, 3));
+      float* tmp = static_cast<float*>(workspace(bytes, 3, s0));
       st = tmp ? launch_allreduce(pp, g->W, tmp, M * N, false, true, s0)
                : set_error(TBIK_CUDA_ERROR, "workspace allocation failed");
       if (st == TBIK_OK && cudaMemcpy2DAsync(Y, ldy * 4, tmp, N * 4, N * 4, M, cudaMemcpyDeviceToDevice, s0) != cudaSuccess)
@@ -325,7 +325,7 @@ tbik_status tbik_baseline_row_parallel_forward_local(const void* X, int x_dtype,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t width = K / tp;
   const size_t slice = static_cast<size_t>(M) * N;
-  float* parts = static_cast<float*>(workspace(slice * tp * sizeof(float), 11));
+  float* parts = static_cast<float*>(workspace(slice * tp * sizeof(float), 11, s));
   if (!parts) return set_error(TBIK_CUDA_ERROR, "workspace allocation failed");
   PartPtrs pp{};
   for (int r = 0; r < tp; ++r) {

@@ -585,9 +585,9 @@ tbik_status tbik_embedding(const void* table, int64_t V, int64_t H, const int64_
   if (!table || !ids || !out) return set_error(TBIK_BAD_ARGUMENT, "null argument");
   if (rows < 1 || H < 1 || V < 1) return set_error(TBIK_BAD_DIMENSION, "embedding: dimensions must be >= 1");
   TBIK_TRY(need_device());
-  int* bad = static_cast<int*>(workspace(16, 3));
-  if (!bad) return set_error(TBIK_CUDA_ERROR, "workspace");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int* bad = static_cast<int*>(workspace(16, 3, s));
+  if (!bad) return set_error(TBIK_CUDA_ERROR, "workspace");
   TBIK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
   embed_kernel<<<static_cast<unsigned>(rows), 256, 0, s>>>(static_cast<const uint16_t*>(table), H, ids, V,
                                                            static_cast<uint16_t*>(out), bad);
@@ -657,11 +657,8 @@ tbik_status tbik_attention_prefill(const void* q, int64_t ldq, const void* k, in
     return set_error(TBIK_BAD_ARGUMENT, "attention: 16-byte aligned rows required");
   TBIK_TRY(need_device());
   const size_t smem = (static_cast<size_t>(AK) * AKP + static_cast<size_t>(AQ) * (seq_len + 1) + 4 * AQ) * 4;
-  static size_t attr = 0;
-  if (attr < smem) {
-    TBIK_CUDA(cudaFuncSetAttribute(attn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr = smem;
-  }
+  // per launch: the attribute is per device context
+  TBIK_CUDA(cudaFuncSetAttribute(attn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   dim3 grid(static_cast<unsigned>(n_q_heads), static_cast<unsigned>(batch),
             static_cast<unsigned>((seq_len + AQ - 1) / AQ));
   attn2_kernel<<<grid, 4 * AQ, smem, static_cast<cudaStream_t>(stream)>>>(
@@ -688,11 +685,7 @@ tbik_status tbik_attention_prefill_tc(const void* q, int64_t ldq, const void* k,
   dim3 grid(static_cast<unsigned>(n_q_heads), static_cast<unsigned>(batch),
             static_cast<unsigned>((seq_len + FQ - 1) / FQ));
   constexpr size_t fsmem = 2 * 2 * FSTAGE * sizeof(uint16_t);
-  static bool fattr = false;
-  if (!fattr) {
-    TBIK_CUDA(cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem)));
-    fattr = true;
-  }
+  TBIK_CUDA(cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem)));
   attn_mma_kernel<<<grid, 128, fsmem, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(q), ldq, static_cast<const uint16_t*>(k), ldk, static_cast<const uint16_t*>(v), ldv,
       seq_len, n_q_heads, n_kv_heads, scale_log2, static_cast<uint16_t*>(out), ldo);

@@ -524,7 +524,7 @@ tbik_status tbik_logsoftmax_shard_state(const float* logits, int64_t ld, int64_t
   if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t n = v_local / groups;
-  MS* gs = static_cast<MS*>(workspace(static_cast<size_t>(rows) * groups * sizeof(MS), 3));
+  MS* gs = static_cast<MS*>(workspace(static_cast<size_t>(rows) * groups * sizeof(MS), 3, s));
   if (!gs) return set_error(TBIK_CUDA_ERROR, "workspace allocation failed");
   const bool vec = (reinterpret_cast<uintptr_t>(logits) & 15) == 0 && ld % 4 == 0 && n % 4 == 0;
   dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>(groups));
@@ -578,7 +578,7 @@ tbik_status tbik_tree_logsoftmax_local(const float* logits, int64_t ld, int64_t 
   if (V % tp || groups % tp)
     return set_error(TBIK_SHARD_ERROR, "vocab / groups not divisible by tp=" + std::to_string(tp));
   const int64_t vl = V / tp;
-  float* ms = static_cast<float*>(workspace(static_cast<size_t>(rows) * 2 * tp * sizeof(float), 2));
+  float* ms = static_cast<float*>(workspace(static_cast<size_t>(rows) * 2 * tp * sizeof(float), 2, static_cast<cudaStream_t>(stream)));
   if (!ms) return set_error(TBIK_CUDA_ERROR, "workspace allocation failed");
   PartPtrs pp{};
   for (int r = 0; r < tp; ++r) {

@@ -311,9 +311,10 @@ class TbikDecoder:
         """Capture one forward + log-softmax over the static token tensor `tokens`
         into a CUDA graph (no per-launch host cost on replay; bits unchanged).
         Returns (graph, (logits, lse, logprobs)); refill `tokens` in place and call
-        graph.replay().  Two eager warm-up passes size the library's workspaces
-        first, so nothing is allocated inside the capture; a later call that grows
-        a workspace (a larger shape) invalidates the graph."""
+        graph.replay().  Two eager warm-up passes on the capture stream size that
+        stream's library workspaces first, so nothing is allocated inside the
+        capture; a later call on the same stream that grows a workspace (a larger
+        shape) invalidates the graph."""
         import torch
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
@@ -324,7 +325,8 @@ class TbikDecoder:
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
+        # capture on the warm-up stream: the library's scratch arenas are per stream
+        with torch.cuda.graph(graph, stream=side):
             logits = self.forward(tokens, tp)
             lse, lp, _ = self.log_probs(logits, tp, full=full_logprobs)
         return graph, (logits, lse, lp)

@@ -20,6 +20,7 @@ def main():
     world = int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    tb.set_schedule("group_fused", int(os.environ.get("TBIK_GROUP_FUSED", "1")))
     M, K, N = 64, 14336, 1024
     g = torch.Generator(device="cuda")
     g.manual_seed(7)

@@ -273,13 +273,10 @@ def test_errors(tb, cuda):
 # every launch-shape knob is a scheduling choice: pair / single-CTA tiles, 256-wide
 # pair tiles, A rows staged per stage, raster grouping, K split -- same bits
 # ---------------------------------------------------------------------------------
-SCHEDULES = [{}, {"TBIK_TC_WIDE": "1"}, {"TBIK_TC_GROUP_M": "1"}, {"TBIK_TC_GROUP_M": "3", "TBIK_TC_UNITS": "2"},
-             {"TBIK_TC_PAIR": "0"}, {"TBIK_TC_PAIR": "0", "TBIK_TC_UNITS": "4"}, {"TBIK_TC_PAIR": "1"},
-             {"TBIK_TC_ABOX": "32"}, {"TBIK_TC_ABOX": "64", "TBIK_TC_PAIR": "1"}, {"TBIK_TC_DEEP": "1"},
-             {"TBIK_TC_SKINNY": "0"}, {"TBIK_SK_UNITS": "1"}, {"TBIK_SK_UNITS": "2", "TBIK_SK_LEAF": "0"},
-             {"TBIK_SK_UNITS": "8"}, {"TBIK_SK_BN": "64"}]
-ENV_KNOBS = ("TBIK_TC_WIDE", "TBIK_TC_GROUP_M", "TBIK_TC_UNITS", "TBIK_TC_PAIR", "TBIK_TC_ABOX", "TBIK_TC_DEEP",
-             "TBIK_TC_SKINNY", "TBIK_SK_UNITS", "TBIK_SK_LEAF", "TBIK_SK_BN")
+SCHEDULES = [{}, {"tc_group_m": 1}, {"tc_group_m": 3, "tc_units": 2}, {"tc_pair": 0}, {"tc_pair": 0, "tc_units": 4},
+             {"tc_pair": 1}, {"tc_abox": 32}, {"tc_abox": 64, "tc_pair": 1}, {"tc_deep": 1}, {"tc_deep": 0},
+             {"tc_acc4": 0}, {"tc_skinny": 0}, {"sk_units": 1}, {"sk_units": 2, "sk_leaf": 0}, {"sk_units": 8},
+             {"sk_bn": 64}, {"sk_mt": 128}]
 
 
 @pytest.mark.parametrize("M,K,N", [(300, 14336, 640), (64, 4096, 512), (513, 6144, 384), (20, 4096, 200),
@@ -290,13 +287,10 @@ def test_tc_schedules_invisible(tb, cuda, orc, M, K, N, monkeypatch):
     w = torch.randn(K, N, device=cuda).to(torch.bfloat16)
     cfg = tb.BlockConfig(64, 256, 128, 0)
     outs, leaves = [], []
-    for env in SCHEDULES:
-        for k in ENV_KNOBS:
-            monkeypatch.delenv(k, raising=False)
-        for k, v in env.items():
-            monkeypatch.setenv(k, v)
-        outs.append(tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05))
-        leaves.append(tb.tree_matmul_leaves(x, w, cfg, tb.LEAF_TCGEN05))
+    for knobs in SCHEDULES:
+        with tb.schedule(**knobs):
+            outs.append(tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05))
+            leaves.append(tb.tree_matmul_leaves(x, w, cfg, tb.LEAF_TCGEN05))
     for env, o in zip(SCHEDULES[1:], outs[1:]):
         assert torch.equal(outs[0].view(torch.int32), o.view(torch.int32)), f"schedule {env} changed the bits"
     for env, lv in zip(SCHEDULES[1:], leaves[1:]):
@@ -316,19 +310,14 @@ def test_skinny_matches_wide(tb, cuda, M, K, N, monkeypatch):
     x = torch.randn(M, K, device=cuda).to(torch.bfloat16)
     w = torch.randn(K, N, device=cuda).to(torch.bfloat16)
     cfg = tb.BlockConfig(64, 256, 128, 0)
-    monkeypatch.setenv("TBIK_TC_SKINNY", "0")
-    ref = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
-    monkeypatch.setenv("TBIK_TC_SKINNY", "1")
+    with tb.schedule(tc_skinny=0):
+        ref = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
     L = tb.plan_blocks(K, cfg, 1).leaves
-    for bn in ("128", "64"):  # 128-column tiles (MMA M = 128) / 64-column tiles (M = 64)
-        monkeypatch.setenv("TBIK_SK_BN", bn)
-        for u in [0] + [u for u in (1, 2, 4, 8) if u <= L]:
-            if u:
-                monkeypatch.setenv("TBIK_SK_UNITS", str(u))
-            y = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+    for bn in (128, 64):  # 128-column tiles (MMA M = 128) / 64-column tiles (M = 64)
+        for u in [-1] + [u for u in (1, 2, 4, 8) if u <= L]:
+            with tb.schedule(tc_skinny=1, sk_bn=bn, sk_units=u):
+                y = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
             assert torch.equal(y.view(torch.int32), ref.view(torch.int32)), f"skinny bn={bn} units={u} changed the bits"
-        monkeypatch.delenv("TBIK_SK_UNITS", raising=False)
-    monkeypatch.delenv("TBIK_SK_BN")
 
 
 @pytest.mark.parametrize("leaf_split", ["0", "1"])
@@ -339,12 +328,11 @@ def test_skinny_tp_shards(tb, cuda, leaf_split, monkeypatch):
     x = torch.randn(16, 14336, device=cuda).to(torch.bfloat16)
     w = torch.randn(14336, 1024, device=cuda).to(torch.bfloat16)
     cfg = tb.BlockConfig(64, 256, 128, 0)
-    monkeypatch.setenv("TBIK_TC_SKINNY", "0")
-    ref = tb.row_parallel_forward(x, w, tb.DeviceGroup(1), cfg, 8, tb.LEAF_TCGEN05)
-    monkeypatch.setenv("TBIK_TC_SKINNY", "1")
-    monkeypatch.setenv("TBIK_SK_LEAF", leaf_split)
+    with tb.schedule(tc_skinny=0):
+        ref = tb.row_parallel_forward(x, w, tb.DeviceGroup(1), cfg, 8, tb.LEAF_TCGEN05)
     for tp in (1, 2, 4, 8):
-        y = tb.row_parallel_forward(x, w, tb.DeviceGroup(tp), cfg, 8, tb.LEAF_TCGEN05)
+        with tb.schedule(tc_skinny=1, sk_leaf=int(leaf_split)):
+            y = tb.row_parallel_forward(x, w, tb.DeviceGroup(tp), cfg, 8, tb.LEAF_TCGEN05)
         assert torch.equal(y.view(torch.int32), ref.view(torch.int32)), f"tp={tp}"
 
 
@@ -433,16 +421,16 @@ def test_random_shapes_both_leaves(tb, cuda, orc, M, K, N, bk):
 
 
 @pytest.mark.parametrize("M,K,N", [(2560, 3072, 2048), (4096, 14336, 4096), (700, 25600, 5120)])
-def test_tc_wide_tiles_and_split_tail(tb, cuda, M, K, N, monkeypatch):
-    """256 x 256 pair tiles (split accumulator halves, level 1 in TMEM, deeper levels
-    in scratch) and the 256 x 128 half items of a short last round give the bits
-    of the 256 x 128 kernel (80 / 256 tiles on 74 pairs: split tail; 3 x 20: none)."""
+def test_tc_deep_and_acc_variants(tb, cuda, M, K, N):
+    """DEEP (level 3 in scratch + deeper pipeline) vs on-chip level 3, and the four-
+    accumulator variant on and off, at large shapes: the same bits."""
     g = torch.Generator(device=cuda).manual_seed(K + N)
     x = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
     w = torch.randn(K, N, device=cuda, generator=g).to(torch.bfloat16)
     cfg = tb.BlockConfig(64, 256 if K % 256 == 0 and K != 25600 else 128, 128, 0)
-    monkeypatch.setenv("TBIK_TC_WIDE", "0")
-    want = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
-    monkeypatch.setenv("TBIK_TC_WIDE", "1")
-    got = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
-    assert torch.equal(want.view(torch.int32), got.view(torch.int32))
+    with tb.schedule(tc_deep=0):
+        want = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+    for knobs in ({"tc_deep": 1}, {"tc_units": 2, "tc_acc4": 0}, {"tc_units": 2}):
+        with tb.schedule(**knobs):
+            got = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+        assert torch.equal(want.view(torch.int32), got.view(torch.int32)), knobs

@@ -9,6 +9,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2511_17826_b200 as tb  # noqa: E402
+from tools.timing import graph_time  # noqa: E402
 
 K, N = 14336, 4096
 cfg = tb.BlockConfig(64, 256, 128, 0)
@@ -36,21 +37,11 @@ def cold(fn, reps=50):
 
 
 def stream(fn, reps=40):
-    for i in range(4):
-        fn(i)
-    torch.cuda.synchronize()
-    s, e = ev(), ev()
-    s.record()
-    for i in range(reps):
-        fn(i % 4)
-    e.record()
-    torch.cuda.synchronize()
-    return s.elapsed_time(e) * 1e3 / reps
+    return graph_time(fn, reps=reps, rot=4)
 
 
-def set_env(env):
-    for k, v in env.items():
-        os.environ[k] = v
+def graph_time_20(fn):
+    return graph_time(fn, reps=20, rot=4)
 
 
 for M in Ms:
@@ -58,12 +49,11 @@ for M in Ms:
     y = torch.empty(M, N, device="cuda")
     yb = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     out = [f"M={M:4d}"]
-    for name, env in (("wide", {"TBIK_TC_SKINNY": "0"}), ("skinny", {"TBIK_TC_SKINNY": "1"})):
-        set_env(env)
+    for name, knobs in (("wide", {"tc_skinny": 0}), ("skinny", {"tc_skinny": 1})):
         f = lambda i: tb.tree_matmul(x, ws[i], cfg, tb.LEAF_TCGEN05, out=y)  # noqa: E731
-        c, st = cold(f), stream(f)
+        with tb.schedule(**knobs):
+            c, st = cold(f), stream(f)
         out.append(f"{name} cold {c:5.1f} stream {st:5.1f} us ({K * N * 2 / st / 1e3:5.0f} GB/s)")
-    os.environ.pop("TBIK_TC_SKINNY", None)
     f = lambda i: torch.matmul(x, ws[i], out=yb)  # noqa: E731
     c, st = cold(f), stream(f)
     out.append(f"cublas cold {c:5.1f} stream {st:5.1f} us ({K * N * 2 / st / 1e3:5.0f} GB/s)")
@@ -74,25 +64,6 @@ for M in Ms:
 # host path (~10 us per call) would otherwise hide these few-us kernels.
 
 
-def graph_time(fn, reps=20):
-    for i in range(4):
-        fn(i)
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        for i in range(reps):
-            fn(i % 4)
-    g.replay()
-    torch.cuda.synchronize()
-    s, e = ev(), ev()
-    s.record()
-    for _ in range(5):
-        g.replay()
-    e.record()
-    torch.cuda.synchronize()
-    return s.elapsed_time(e) * 1e3 / (5 * reps)
-
-
 for tp in (1, 2, 4, 8):
     Ks = K // tp
     cfg_s = tb.BlockConfig(64, 256, 128, 7)
@@ -101,19 +72,17 @@ for tp in (1, 2, 4, 8):
         y = torch.empty(M, N, device="cuda")
         wsh = [w[:Ks] for w in ws]
         out = [f"graph TP={tp} shard K={Ks:5d} M={M:3d}"]
-        for name, env in (("wide", {"TBIK_TC_SKINNY": "0"}), ("skinny", {"TBIK_TC_SKINNY": "1"}),
-                          ("sk_leaf", {"TBIK_TC_SKINNY": "1", "TBIK_SK_LEAF": "1"}),
-                          ("sk_noleaf", {"TBIK_TC_SKINNY": "1", "TBIK_SK_LEAF": "0"}),
-                          ("sk_u2", {"TBIK_TC_SKINNY": "1", "TBIK_SK_UNITS": "2", "TBIK_SK_LEAF": "0"}),
-                          ("sk_u4", {"TBIK_TC_SKINNY": "1", "TBIK_SK_UNITS": "4", "TBIK_SK_LEAF": "0"}),
-                          ("sk_bn64", {"TBIK_TC_SKINNY": "1", "TBIK_SK_BN": "64"}),
-                          ("sk_bn128", {"TBIK_TC_SKINNY": "1", "TBIK_SK_BN": "128"})):
-            set_env(env)
+        for name, knobs in (("wide", {"tc_skinny": 0}), ("skinny", {"tc_skinny": 1}),
+                            ("sk_leaf", {"tc_skinny": 1, "sk_leaf": 1}),
+                            ("sk_noleaf", {"tc_skinny": 1, "sk_leaf": 0}),
+                            ("sk_u2", {"tc_skinny": 1, "sk_units": 2, "sk_leaf": 0}),
+                            ("sk_u4", {"tc_skinny": 1, "sk_units": 4, "sk_leaf": 0}),
+                            ("sk_bn64", {"tc_skinny": 1, "sk_bn": 64}),
+                            ("sk_bn128", {"tc_skinny": 1, "sk_bn": 128})):
             f = lambda i: tb.tree_matmul(x, wsh[i], cfg_s, tb.LEAF_TCGEN05, out=y)  # noqa: E731
-            st = graph_time(f)
-            for k in env:
-                os.environ.pop(k, None)
+            with tb.schedule(**knobs):
+                st = graph_time_20(f)
             out.append(f"{name} {st:5.1f}")
         yb = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-        out.append(f"cublas {graph_time(lambda i: torch.matmul(x, wsh[i], out=yb)):5.1f} us")
+        out.append(f"cublas {graph_time_20(lambda i: torch.matmul(x, wsh[i], out=yb)):5.1f} us")
         print(" | ".join(out), flush=True)
