@@ -373,17 +373,8 @@ __device__ __forceinline__ void ar_finish(const TcParams& p, long long pair, lon
 // merges into it, so a pair of leaves costs two accumulator drains instead of two
 // drains + a level-1 store + load.
 // AR: the fused tree all-reduce variant (pair tiles, FULL mode; tbik_group.cu).
-// R1 (k_first > 1, at most 3 tree levels, pair tiles): tree level 1 lives in
-// registers too -- an even group's value stays in g while the odd group folds its
-// k_first leaves into g1, and the two meet in registers -- so levels 2-3 take the
-// TMEM slots, no level touches shared memory, and the DEEP shared-memory layout
-// (8 pipeline stages) applies.  The merge warpgroups raise their register budget
-// to 232 with setmaxnreg (warpgroup 0 -- TMA producer, MMA issuer, TMEM
-// allocator -- drops to 40) to hold g, g1 and both TMEM load chunks.  The
-// increase is served only from what the decrease released (384 x 168 registers
-// at launch: 128 x (168 - 40) = 256 x (232 - 168)); asking for more blocks forever.
 constexpr int EPI = MERGE_WARPS;
-template <bool KF1, int ABOX, bool PAIR, bool DEEP, bool AR = false, bool R1 = false>
+template <bool KF1, int ABOX, bool PAIR, bool DEEP, bool AR = false>
 __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     tc_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const TcParams p) {
@@ -439,7 +430,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp < 4) {
-  if constexpr (R1) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
     if (elect_one()) {
@@ -538,7 +528,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   }
   } else {
     // ---------------- merge warps (the TBIK reduction), both CTAs ----------------
-    if constexpr (R1) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
     constexpr int COLS = BN * 4 / EPI;  // columns owned by this thread (64)
     constexpr int NCH = COLS / 32;
     const int q = warp & 3;  // a warp may only touch TMEM lanes 32*(warp%4)..
@@ -552,9 +541,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     // k_first == 1 keeps level 1 in registers, so its TMEM columns hold level 3
     // (off the shared-memory port the MMA operand reads saturate); scratch from 4.
     // ... and shared memory (when not DEEP) holds level 4.
-    // R1 maps the levels like KF1: 1 in registers, 2-3 in TMEM, 4 in smem, 5+ scratch.
-    constexpr bool REG1 = KF1 || R1;                      // tree level 1 in registers
-    constexpr int SL = REG1 ? 4 : 3;                       // the shared-memory level
+    constexpr int SL = KF1 ? 4 : 3;                        // the shared-memory level
     constexpr int FS = DEEP ? SL : SL + 1;                 // first scratch level
     float* scratch_base =
         p.levels >= FS
@@ -564,8 +551,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     uint8_t* l3 = sL3 + (warp - 4) * warp_region_bytes(DEEP);  // [COLS/4][32 lanes][float4] (+ staging)
     constexpr bool ONE_BOX = DEEP;  // a single staging box per warp
 
-    float g[COLS];             // level 0: the running leaf-group value (R1: of even groups)
-    float g1[R1 ? COLS : 1];   // R1: level 0 of odd groups (g holds level 1 meanwhile)
+    float g[COLS];  // level 0: the running leaf-group value
     int xb = 0;      // output staging buffer toggle
     uint32_t acc_iter = 0;
     for (long long item = pair; item < p.items; item += npairs) {
@@ -586,7 +572,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         // with); the accumulator goes back to the MMA issuer as soon as the values
         // are in registers.
         uint32_t r[NCH < 2 ? 2 : NCH][32];
-        const bool odd = REG1 && p.levels >= 1 && (groups_done & 1u);
+        const bool odd = KF1 && p.levels >= 1 && (groups_done & 1u);
 #pragma unroll
         for (int c = 0; c < NCH; ++c) tmem_ld32r(acc + c * 32, r[c]);
 #pragma unroll
@@ -610,7 +596,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         } else {
         // level 0: g = ((0 + P_0) + P_1) + ... + P_{kf-1}   (matmul.cpp:100-125; 0 + P
         // canonicalises a -0 leaf like matmul.cpp:101-103)
-        if (KF1 && odd) {
+        if (odd) {
           // level 1 in registers: g holds the previous group S1 (kept since the even
           // leaf); the new group (0 + P) merges with it, new + old (matmul.cpp:107-123)
 #pragma unroll
@@ -618,19 +604,6 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i)
               g[c * 32 + i] = __fadd_rn(__fadd_rn(0.0f, __uint_as_float(r[c][i])), g[c * 32 + i]);
-        } else if (R1 && odd) {
-          // the odd group folds into g1 while g keeps the even group (level 1)
-          if (t_in_group == 0) {
-#pragma unroll
-            for (int c = 0; c < NCH; ++c)
-#pragma unroll
-              for (int i = 0; i < 32; ++i) g1[c * 32 + i] = __fadd_rn(0.0f, __uint_as_float(r[c][i]));
-          } else {
-#pragma unroll
-            for (int c = 0; c < NCH; ++c)
-#pragma unroll
-              for (int i = 0; i < 32; ++i) g1[c * 32 + i] = __fadd_rn(g1[c * 32 + i], __uint_as_float(r[c][i]));
-          }
         } else if (KF1 || t_in_group == 0) {  // KF1 <=> k_first == 1: every leaf starts a group
 #pragma unroll
           for (int c = 0; c < NCH; ++c)
@@ -648,15 +621,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         // Binary counter over completed groups (levels 1..p.levels, matmul.cpp:107-123):
         // levels 1-2 in TMEM columns [256, 512), deeper levels (touched once per 8+
         // groups) in L2-resident scratch.
-        if (REG1 && p.levels >= 1 && !odd) {  // even group: stays in registers as level 1
+        if (KF1 && p.levels >= 1 && !odd) {  // even group: stays in registers as level 1
           ++groups_done;
           continue;
-        }
-        if constexpr (R1) {
-          if (odd) {  // level 1: the odd group meets the even one, new + old (matmul.cpp:107-123)
-#pragma unroll
-            for (int i = 0; i < COLS; ++i) g[i] = __fadd_rn(g1[i], g[i]);
-          }
         }
         if (p.levels >= 1) {
           int level = 1;
@@ -666,7 +633,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             level = 2;
           }
           while (c_bits & 1u) {
-            if (REG1 ? (level == 2 || level == 3) : level <= 2) {
+            if (KF1 ? (level == 2 || level == 3) : level <= 2) {
               const uint32_t slot = lane_base + (level == 2 ? SLOT_LVL2 : SLOT_LVL1);
 #pragma unroll
               for (int c = 0; c < NCH; ++c) tmem_ld32r(slot + c * 32, r[c]);
@@ -701,7 +668,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
             ++level;
           }
           if (level <= p.levels) {
-            if (REG1 ? (level == 2 || level == 3) : level <= 2) {
+            if (KF1 ? (level == 2 || level == 3) : level <= 2) {
               const uint32_t slot = lane_base + (level == 2 ? SLOT_LVL2 : SLOT_LVL1);
 #pragma unroll
               for (int c = 0; c < NCH; ++c) {
@@ -1031,33 +998,7 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
     const int64_t k = knob(KNOB_TC_DEEP, -1);
     if (k == 0 || k == 1) deep = k == 1;
   }
-  // R1 (level 1 in registers, 8 stages, no shared-memory level): pair tiles with
-  // 128-row A staging, k_first > 1, 1..3 tree levels, f32 output, not the fused
-  // all-reduce instantiation (schedule knob tc_r1 = 0 turns it off; same bits).
-  bool r1 = pair && abox == 128 && !kf1 && p.levels >= 1 && p.levels <= 3 && !o.act && knob(KNOB_TC_R1, 1) != 0 &&
-            !g_fused_ar;
-  if (r1) {
-    // setmaxnreg only redistributes the registers the launch allocated: the
-    // merge warpgroups' increase to 232 needs exactly 168 per thread at launch
-    // (the register count ptxas chose under __launch_bounds__(384, 1)).  Checked
-    // once per device; any other count would block forever, so R1 is then off.
-    static std::mutex mu;
-    static std::map<int, bool> regs_ok;
-    int d = 0;
-    cudaGetDevice(&d);
-    std::lock_guard<std::mutex> lk(mu);
-    auto f = regs_ok.find(d);
-    if (f == regs_ok.end()) {
-      cudaFuncAttributes fa{};
-      const bool ok = cudaFuncGetAttributes(&fa, tc_tree_gemm_kernel<false, 128, true, true, false, true>) ==
-                          cudaSuccess && fa.numRegs == 168;
-      if (!ok) cudaGetLastError();
-      f = regs_ok.emplace(d, ok).first;
-    }
-    r1 = f->second;
-  }
-  if (r1) deep = true;  // the DEEP shared-memory layout: no level reaches shared memory or scratch
-  const int first_scratch = (kf1 || r1 ? 4 : 3) + (deep ? 0 : 1);
+  const int first_scratch = (kf1 ? 4 : 3) + (deep ? 0 : 1);
   if (p.levels >= first_scratch) {
     const size_t n = static_cast<size_t>(grid.x) * (p.levels - first_scratch + 1) * BM * BN;
     p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1, s));
@@ -1139,8 +1080,7 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
 #undef TBIK_TC_K
   const int ai = abox == 32 ? 0 : abox == 64 ? 1 : 2;
   const bool ar_on = p.ar_W > 1;
-  const Kern kern = r1 ? tc_tree_gemm_kernel<false, 128, true, true, false, true>
-                  : ar_on ? (deep ? (kf1 ? tc_tree_gemm_kernel<true, 128, true, true, true>
+  const Kern kern = ar_on ? (deep ? (kf1 ? tc_tree_gemm_kernel<true, 128, true, true, true>
                                          : tc_tree_gemm_kernel<false, 128, true, true, true>)
                                   : (kf1 ? tc_tree_gemm_kernel<true, 128, true, false, true>
                                          : tc_tree_gemm_kernel<false, 128, true, false, true>))

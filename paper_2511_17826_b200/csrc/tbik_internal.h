@@ -97,7 +97,6 @@ enum Knob {
   KNOB_GROUP_FUSED,      // 0: no fused GEMM + all-reduce kernel
   KNOB_GROUP_OVERLAP,    // 0: no chunked GEMM / all-reduce overlap
   KNOB_AR_TWO_PHASE_BYTES,  // payload bytes from which the group all-reduce is two-phase
-  KNOB_TC_R1,            // 0: no register-level-1 variant of the pair kernel
   KNOB_COUNT
 };
 int64_t knob(Knob k, int64_t dflt);

@@ -276,7 +276,7 @@ def test_errors(tb, cuda):
 SCHEDULES = [{}, {"tc_group_m": 1}, {"tc_group_m": 3, "tc_units": 2}, {"tc_pair": 0}, {"tc_pair": 0, "tc_units": 4},
              {"tc_pair": 1}, {"tc_abox": 32}, {"tc_abox": 64, "tc_pair": 1}, {"tc_deep": 1}, {"tc_deep": 0},
              {"tc_acc4": 0}, {"tc_skinny": 0}, {"sk_units": 1}, {"sk_units": 2, "sk_leaf": 0}, {"sk_units": 8},
-             {"sk_bn": 64}, {"sk_mt": 128}, {"tc_r1": 0}, {"tc_r1": 0, "tc_deep": 1}]
+             {"sk_bn": 64}, {"sk_mt": 128}]
 
 
 @pytest.mark.parametrize("M,K,N", [(300, 14336, 640), (64, 4096, 512), (513, 6144, 384), (20, 4096, 200),
@@ -430,8 +430,7 @@ def test_tc_deep_and_acc_variants(tb, cuda, M, K, N):
     cfg = tb.BlockConfig(64, 256 if K % 256 == 0 and K != 25600 else 128, 128, 0)
     with tb.schedule(tc_deep=0):
         want = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
-    for knobs in ({"tc_deep": 1}, {"tc_units": 2, "tc_acc4": 0}, {"tc_units": 2}, {"tc_r1": 0}, {"tc_r1": 1},
-                  {"tc_r1": 0, "tc_deep": 1}):
+    for knobs in ({"tc_deep": 1}, {"tc_units": 2, "tc_acc4": 0}, {"tc_units": 2}, {"tc_deep": 0, "tc_units": 4}):
         with tb.schedule(**knobs):
             got = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
         assert torch.equal(want.view(torch.int32), got.view(torch.int32)), knobs
