@@ -469,7 +469,19 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader CTA only) ----------------
-    if (leader && elect_one()) {
+    // The whole warp runs the loop (its control values are warp-uniform, so they
+    // live in uniform registers) and one elected lane issues.  Descriptors are
+    // built once and advanced by constant offsets: round 1's per-MMA descriptor
+    // arithmetic -- ~90 dependent instructions per 64-K stage on a single thread
+    // -- kept the MMA issuer, not the operand feed, on the critical path
+    // (ncu source-level samples, profiles/r02_ncu_mma_issuer.md).
+    if (leader) {
+      // SW128 descriptors (umma_desc_sw128): lo = start >> 4 | LBO >> 4 << 16, hi =
+      // SBO >> 4 | version bit 46 | layout SWIZZLE_128B (bits 61-63).  Shared
+      // addresses stay below 2^18, so the 14-bit start field never carries.
+      constexpr uint32_t DESC_HI = (1024u >> 4) | (1u << 14) | (2u << 29);
+      const uint32_t a_lo0 = (smem_u32(sA) >> 4) | ((16u >> 4) << 16);                 // A: K-major
+      const uint32_t b_lo0 = (smem_u32(sB) >> 4) | ((uint32_t(B_STAGE_BYTES) >> 4) << 16);  // B: MN-major
       int stage = 0;
       uint32_t phase = 0;
       uint32_t acc_iter = 0;
@@ -485,34 +497,40 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           for (int c = 0; c < nch; ++c) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            const uint32_t a_base = smem_u32(sA + stage * A_STRIDE);
-            const uint32_t b_base = smem_u32(sB + stage * B_STAGE);
+            const uint32_t a_lo = a_lo0 + static_cast<uint32_t>(stage) * (A_STRIDE >> 4);
+            const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(stage) * (B_STAGE >> 4);
+            if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < KSTAGE / 16; ++kk) {
-              // A: K-major SW128, +32 B per 16-element K step inside the 128 B atom.
-              const uint64_t adesc = umma_desc_sw128(a_base + kk * 32, 16, 1024);
-              // B: MN-major SW128, 64-column atoms 8 KB apart (LBO; one atom per CTA
-              // in a pair, two in a single CTA); 8-row K groups 1 KB apart (SBO);
-              // +16 K rows (2 KB) per step.
-              const uint64_t bdesc = umma_desc_sw128(b_base + kk * 2048, B_STAGE_BYTES, 1024);
+              for (int kk = 0; kk < KSTAGE / 16; ++kk) {
+                // A: +32 B per 16-element K step inside the 128 B swizzle atom.
+                // B: 64-column atoms B_STAGE_BYTES apart (LBO; one atom per CTA in a
+                // pair, two in a single CTA), 8-row K groups 1 KB apart (SBO), +16 K
+                // rows (2 KB) per step.
+                const uint64_t adesc = (static_cast<uint64_t>(DESC_HI) << 32) | (a_lo + kk * (32 >> 4));
+                const uint64_t bdesc = (static_cast<uint64_t>(DESC_HI) << 32) | (b_lo + kk * (2048 >> 4));
+                if constexpr (PAIR)
+                  umma_bf16_2cta(d, adesc, bdesc, IDESC, (c | kk) != 0 ? 1u : 0u);
+                else
+                  umma_bf16(d, adesc, bdesc, IDESC_1CTA, (c | kk) != 0 ? 1u : 0u);
+              }
               if constexpr (PAIR)
-                umma_bf16_2cta(d, adesc, bdesc, IDESC, (c | kk) != 0 ? 1u : 0u);
+                umma_commit_2cta(&empty[stage], 0x3);
               else
-                umma_bf16(d, adesc, bdesc, IDESC_1CTA, (c | kk) != 0 ? 1u : 0u);
+                umma_commit(&empty[stage]);
             }
-            if constexpr (PAIR)
-              umma_commit_2cta(&empty[stage], 0x3);
-            else
-              umma_commit(&empty[stage]);
+            __syncwarp();
             if (++stage == NST) {
               stage = 0;
               phase ^= 1;
             }
           }
-          if constexpr (PAIR)
-            umma_commit_2cta(&tfull[buf], static_cast<uint16_t>(0x3u << leader_rank));
-          else
-            umma_commit(&tfull[buf]);
+          if (elect_one()) {
+            if constexpr (PAIR)
+              umma_commit_2cta(&tfull[buf], static_cast<uint16_t>(0x3u << leader_rank));
+            else
+              umma_commit(&tfull[buf]);
+          }
+          __syncwarp();
         }
       }
     }

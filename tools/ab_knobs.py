@@ -11,7 +11,7 @@ import paper_2511_17826_b200 as tb  # noqa: E402
 
 SHAPES = [(4096, 14336, 4096), (2048, 14336, 4096), (1024, 14336, 4096), (4096, 4096, 4096), (4096, 4096, 28672),
           (2048, 25600, 5120)]
-VARIANTS = [("default", {}), ("r1_off", {"tc_r1": 0}), ("r1_off_deep", {"tc_r1": 0, "tc_deep": 1})]
+VARIANTS = [("default", {}), ("deep1", {"tc_deep": 1}), ("deep0", {"tc_deep": 0})]
 
 
 def ev_time(fn, reps=20):
