@@ -148,6 +148,18 @@ TBIK_API tbik_status tbik_tree_matmul_silu_mul(const void* A, int a_dtype, int64
                                       int64_t I, int64_t K, const tbik_block_config* cfg, int leaf_mode,
                                       void* stream);
 
+/* The lm_head projection with the log-softmax's first pass fused:
+ * C [M x N] f32 logits = tree_matmul(A, B) as tbik_tree_matmul, and chunk_ms
+ * [M x ld_chunks states] (>= groups * ceil(N / groups / 16) per row; 2 f32 each) = the (m, s) state of every 16-column
+ * chunk of each vocab group, computed by the tcgen05 GEMM's epilogue on the f32
+ * logits in registers (when the GEMM is one FULL launch and N / groups % 16 == 0;
+ * otherwise by a pass over C -- the same bits).  Feed chunk_ms to
+ * tbik_logsoftmax_shard_state_chunks. */
+TBIK_API tbik_status tbik_tree_matmul_logits(const void* A, int a_dtype, int64_t lda, const void* B, int b_dtype,
+                                             int64_t ldb, float* C, int64_t ldc, float* chunk_ms, int64_t ld_chunks,
+                                             int64_t M, int64_t N, int64_t K, int64_t groups,
+                                             const tbik_block_config* cfg, int leaf_mode, void* stream);
+
 /* Debug / verification entry: write every leaf partial product P_t
  * (t = 0..tiles_total-1) to leaves[t][M][N] (f32, dense) using the given leaf
  * mode.  tests/ feed these to the CPU oracle's tree to check the tree logic
@@ -372,12 +384,23 @@ TBIK_API tbik_status tbik_tree_rmsnorm(const void* X, int x_dtype, int64_t ldx, 
                               int64_t cols, void* stream);
 
 /* Vocab-sharded tree log-softmax, step 1: the (m, s) state of every one of
- * `groups` contiguous vocab groups of this shard (logits [rows x v_local] f32),
+ * `groups` contiguous vocab groups of this shard (logits [rows x v_local] f32:
+ * 16-logit chunk states meeting by pairwise levels inside a group),
  * then merged over the shard's groups by the canonical tree.  ms_out is
  * rows x 2 f32 ({m, s} per row) -- 8 bytes per row to exchange. */
 TBIK_API tbik_status tbik_logsoftmax_shard_state(const float* logits, int64_t ld, int64_t rows,
                                         int64_t v_local, int64_t groups, float* ms_out,
                                         void* stream);
+/* The same step 1 from the (m, s) states of the logits' 16-column chunks
+ * (chunk_ms rows x (groups * ceil(v_local / groups / 16)) x 2 f32, chunks restart at
+ * every group), as written by tbik_tree_matmul_logits or tbik_logsoftmax_chunk_states:
+ * the logits are not read again.  Same bits as tbik_logsoftmax_shard_state. */
+TBIK_API tbik_status tbik_logsoftmax_shard_state_chunks(const float* chunk_ms, int64_t ld_chunks, int64_t rows,
+                                                        int64_t v_local, int64_t groups, float* ms_out, void* stream);
+/* The chunk states of a logit block (the non-fused producer); ld_chunks = states per
+ * row of chunk_ms (>= groups * ceil(v_local / groups / 16)). */
+TBIK_API tbik_status tbik_logsoftmax_chunk_states(const float* logits, int64_t ld, int64_t rows, int64_t v_local,
+                                                  int64_t groups, float* chunk_ms, int64_t ld_chunks, void* stream);
 /* Step 2: merge W shard states (rank order, contiguous-halves tree) into
  * lse[rows] = m + log(s).  W a power of two. */
 TBIK_API tbik_status tbik_logsoftmax_merge(const float* const* ms_parts, int W, int64_t rows, float* lse,

@@ -105,6 +105,7 @@ class Oracle(_Lib):
         L.tbo_log.argtypes = [f32]
         L.tbo_tree_logsoftmax.argtypes = [PF, i64, i64, i64, PF, PF, PI64, PF]
         L.tbo_logsoftmax_group_states.argtypes = [PF, i64, i64, i64, PF, PF]
+        L.tbo_logsoftmax_chunk_states.argtypes = [PF, i64, i64, i64, PF, PF]
         L.tbo_silu_mul.argtypes = [PF, i64, i64, i64, vp, i64]
         L.tbo_residual_add.argtypes = [vp, i64, PF, i64, i64, i64]
         L.tbo_rope.argtypes = [PF, i64, i64, C.c_int, C.c_int, vp, PF, PF, vp, i64, i64]
@@ -275,6 +276,18 @@ class Oracle(_Lib):
             tg.ctypes.data_as(PI64) if tg is not None else None,
             tlp.ctypes.data_as(PF) if tlp is not None else None), "tree_logsoftmax")
         return lse, lp, tlp
+
+    def logsoftmax_chunk_states(self, logits, groups=8):
+        """(m, s) of every 16-logit chunk (chunks restart at each vocab group):
+        rows x (groups * ceil(V / groups / 16)) each."""
+        x = np.ascontiguousarray(logits, np.float32)
+        rows, V = x.shape
+        nc = (V // groups + 15) // 16
+        m = np.empty((rows, groups * nc), np.float32)
+        s = np.empty((rows, groups * nc), np.float32)
+        _check(self.lib.tbo_logsoftmax_chunk_states(x.ctypes.data_as(PF), rows, V, groups, m.ctypes.data_as(PF),
+                                                    s.ctypes.data_as(PF)), "chunk_states")
+        return m, s
 
     def logsoftmax_group_states(self, logits, groups=8):
         rows, V = logits.shape

@@ -641,16 +641,15 @@ float tbo_log(float x) { /* x > 0, finite */
  *                  s = s1 * exp(m1 - m) + s2 * exp(m2 - m)   (mul, mul, add)
  * Canonical tree for a row of V logits cut into G contiguous equal vocab
  * groups (G a power of two >= the largest TP size; V % G == 0):
- *   * within a group of n = V / G logits: chunks of 4 consecutive logits,
- *     lane l in [0,256) owns chunks l, l+256, ... (ascending); it consumes them
- *     in BLOCKS of 8 of its chunks (<= 32 logits, ascending element order):
- *       block state: m_b = sequential max (x > m ? x : m) over the block from
- *       its first element; s_b = ((0 + e_0) + e_1) + ... with e_i =
- *       exp(x_i - m_b) in ascending element order; m_b == -inf -> empty;
- *     the lane state is the left fold merge(merge(B_0, B_1), B_2) ... of its
- *     block states (two-pass inside a register-sized block: no serial
- *     max-rescale chain per element);
- *   * the 256 lane states are merged by the contiguous-halves tree;
+ *   * within a group of n = V / G logits: CHUNKS of 16 consecutive logits from
+ *     the group start (the last chunk of a group may be shorter when n % 16);
+ *     chunk state: m_c = sequential max (x > m ? x : m) from its first element,
+ *     s_c = ((0 + e_0) + e_1) + ... with e_i = exp(x_i - m_c) in ascending
+ *     element order; m_c == -inf -> empty (-inf, 0);
+ *   * the chunk states of a group meet by PAIRWISE LEVELS: each level merges
+ *     (2i, 2i+1) -> i, an odd last state passes up unchanged, until one is left
+ *     (chunk-local states are what the lm_head GEMM epilogue can emit: a 16-column
+ *     chunk never leaves one thread's registers there);
  *   * the G group states are merged by the contiguous-halves tree.
  * A TP rank owning G/TP consecutive groups computes exactly a subtree, so
  * the cross-rank merge of (m, s) pairs (8 bytes per row per rank) continues
@@ -677,45 +676,59 @@ static tbo_ms ms_tree(const tbo_ms* v, int64_t n) {
   return ms_merge(ms_tree(v, h), ms_tree(v + h, n - h));
 }
 
-#define TBO_MS_BLOCK 8 /* chunks of 4 logits per lane block */
+#define TBO_MS_CHUNK 16 /* logits per chunk state */
+
+/* State of the chunk x[0..cnt), cnt <= TBO_MS_CHUNK. */
+static tbo_ms ms_chunk(const float* x, int64_t cnt) {
+  float m = x[0];
+  for (int64_t e = 1; e < cnt; ++e) m = x[e] > m ? x[e] : m;
+  tbo_ms st = {-INFINITY, 0.0f};
+  if (m == -INFINITY) return st;
+  float sum = 0.0f;
+  for (int64_t e = 0; e < cnt; ++e) sum = sum + tbo_exp(x[e] - m);
+  st.m = m;
+  st.s = sum;
+  return st;
+}
+
+/* Pairwise levels over v[0..n) (in place). */
+static tbo_ms ms_levels(tbo_ms* v, int64_t n) {
+  while (n > 1) {
+    const int64_t h = n / 2;
+    for (int64_t i = 0; i < h; ++i) v[i] = ms_merge(v[2 * i], v[2 * i + 1]);
+    if (n & 1) v[h] = v[n - 1];
+    n = h + (n & 1);
+  }
+  return v[0];
+}
 
 static tbo_ms ms_group(const float* x, int64_t n) {
-  const int64_t nchunks = (n + 3) / 4;
-  tbo_ms lanes[TBO_LANES];
-  for (int l = 0; l < TBO_LANES; ++l) {
-    tbo_ms st = {-INFINITY, 0.0f};
-    for (int64_t c0 = l; c0 < nchunks; c0 += (int64_t)TBO_LANES * TBO_MS_BLOCK) {
-      /* one block: chunks c0, c0+256, ... (at most TBO_MS_BLOCK of them) */
-      float m = -INFINITY;
-      int first = 1;
-      for (int j = 0; j < TBO_MS_BLOCK; ++j) {
-        const int64_t c = c0 + (int64_t)j * TBO_LANES;
-        if (c >= nchunks) break;
-        for (int64_t e = c * 4; e < c * 4 + 4 && e < n; ++e) {
-          if (first) {
-            m = x[e];
-            first = 0;
-          } else {
-            m = x[e] > m ? x[e] : m;
-          }
-        }
-      }
-      tbo_ms b = {-INFINITY, 0.0f};
-      if (m != -INFINITY) {
-        float sum = 0.0f;
-        for (int j = 0; j < TBO_MS_BLOCK; ++j) {
-          const int64_t c = c0 + (int64_t)j * TBO_LANES;
-          if (c >= nchunks) break;
-          for (int64_t e = c * 4; e < c * 4 + 4 && e < n; ++e) sum = sum + tbo_exp(x[e] - m);
-        }
-        b.m = m;
-        b.s = sum;
-      }
-      st = ms_merge(st, b);
-    }
-    lanes[l] = st;
+  const int64_t nc = (n + TBO_MS_CHUNK - 1) / TBO_MS_CHUNK;
+  tbo_ms* v = (tbo_ms*)malloc((size_t)nc * sizeof(tbo_ms));
+  for (int64_t c = 0; c < nc; ++c) {
+    const int64_t cnt = n - c * TBO_MS_CHUNK < TBO_MS_CHUNK ? n - c * TBO_MS_CHUNK : TBO_MS_CHUNK;
+    v[c] = ms_chunk(x + c * TBO_MS_CHUNK, cnt);
   }
-  return ms_tree(lanes, TBO_LANES);
+  tbo_ms r = ms_levels(v, nc);
+  free(v);
+  return r;
+}
+
+/* Chunk states of a [rows x V] block with groups of n = V / G (chunks restart at
+ * every group start): out_m / out_s are rows x (G * ceil(n / 16)). */
+int tbo_logsoftmax_chunk_states(const float* logits, int64_t rows, int64_t V, int64_t G, float* out_m,
+                                float* out_s) {
+  if (!is_pow2(G) || V % G != 0) return TBO_SHARD_ERROR;
+  const int64_t n = V / G, nc = (n + TBO_MS_CHUNK - 1) / TBO_MS_CHUNK;
+  for (int64_t i = 0; i < rows; ++i)
+    for (int64_t g = 0; g < G; ++g)
+      for (int64_t c = 0; c < nc; ++c) {
+        const int64_t cnt = n - c * TBO_MS_CHUNK < TBO_MS_CHUNK ? n - c * TBO_MS_CHUNK : TBO_MS_CHUNK;
+        const tbo_ms st = ms_chunk(logits + i * V + g * n + c * TBO_MS_CHUNK, cnt);
+        out_m[(i * G + g) * nc + c] = st.m;
+        out_s[(i * G + g) * nc + c] = st.s;
+      }
+  return TBO_OK;
 }
 
 /* Per-group (m, s) states: out_m/out_s are rows x G. */

@@ -13,6 +13,7 @@ from .api import (BF16, F32, LEAF_FMA, LEAF_TCGEN05, BlockConfig, DeviceGroup,  
                   rmsnorm, row_parallel_forward, sync, tree_all_reduce, tree_all_reduce_per_rank,
                   tree_matmul, tree_matmul_hostio, tree_matmul_leaves, tree_matmul_silu_mul,
                   interleave_gate_up, LocalGroup, baseline_row_parallel_forward,
-                  baseline_column_parallel_forward, silu, leaf_dot, set_schedule, schedule)
+                  baseline_column_parallel_forward, silu, leaf_dot, set_schedule, schedule,
+                  tree_matmul_logits, column_parallel_logits, chunk_states_per_row)
 
 __version__ = "0.1.0"

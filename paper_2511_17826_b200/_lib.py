@@ -128,6 +128,9 @@ _SIGS = {
                                              PCFG, i64, ci, vp]),
     "tbik_tree_rmsnorm": (ci, [vp, ci, i64, PF, C.c_float, vp, ci, i64, i64, i64, vp]),
     "tbik_logsoftmax_shard_state": (ci, [PF, i64, i64, i64, i64, PF, vp]),
+    "tbik_logsoftmax_shard_state_chunks": (ci, [PF, i64, i64, i64, i64, PF, vp]),
+    "tbik_logsoftmax_chunk_states": (ci, [PF, i64, i64, i64, i64, PF, i64, vp]),
+    "tbik_tree_matmul_logits": (ci, [vp, ci, i64, vp, ci, i64, PF, i64, PF, i64, i64, i64, i64, i64, PCFG, ci, vp]),
     "tbik_logsoftmax_merge": (ci, [C.POINTER(vp), ci, i64, PF, vp]),
     "tbik_logsoftmax_finish": (ci, [PF, i64, i64, i64, PF, PF, i64, vp, i64, PF, vp]),
     "tbik_tree_logsoftmax_local": (ci, [PF, i64, i64, i64, i64, ci, PF, PF, i64, vp, PF, vp]),

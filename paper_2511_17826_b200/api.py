@@ -447,14 +447,98 @@ def rmsnorm(x, gamma, eps: float = 1e-5, out_dtype=None):
     return out
 
 
-def log_softmax(logits, groups: int = 8, tp: int = 1, targets=None, full: bool = True):
+def chunk_states_per_row(V: int, groups: int) -> int:
+    """(m, s) chunk states per row of a V-wide logit block cut into `groups` vocab
+    groups: 16-logit chunks, restarting at every group."""
+    return groups * ((V // groups + 15) // 16)
+
+
+def tree_matmul_logits(a, w, groups: int, cfg: BlockConfig | None = None, leaf: int = LEAF_TCGEN05, out=None,
+                       chunks=None):
+    """The lm_head with the log-softmax's first pass fused (tbik_tree_matmul_logits):
+    returns (logits [M, N] f32, chunk states [M, states, 2] f32) -- the states come
+    from the tcgen05 GEMM's epilogue when it is one FULL launch, else from a pass
+    over the logits (same bits)."""
+    torch = _torch()
+    cfg = cfg or default_block_config(BF16)
+    M, K = a.shape
+    N = w.shape[1]
+    pa, da, lda = _mat(a, "A")
+    pw, dw, ldw = _mat(w, "W")
+    out = _empty_f32(M, N, a) if out is None else out
+    pc, _, ldc = _mat(out, "C")
+    nst = chunk_states_per_row(N, groups)
+    chunks = torch.empty((M, nst, 2), dtype=torch.float32, device=a.device) if chunks is None else chunks
+    check(lib.tbik_tree_matmul_logits(pa, da, lda, pw, dw, ldw, pc, ldc, C.c_void_p(chunks.data_ptr()),
+                                      chunks.stride(0) // 2, M, N, K, groups, C.byref(cfg.c()), leaf, _stream()))
+    return out, chunks
+
+
+def column_parallel_logits(x, w, group: DeviceGroup, groups: int, cfg: BlockConfig | None = None,
+                           leaf: int = LEAF_TCGEN05):
+    """column_parallel_forward of the lm_head (layers.cpp:48-72) with the fused chunk
+    states: simulated rank r owns vocab columns [r V/tp, (r+1) V/tp) = groups
+    [r G/tp, (r+1) G/tp); its logits and chunk states land at their offsets."""
+    torch = _torch()
+    tp = group.world_size()
+    M = x.shape[0]
+    V = w.shape[1]
+    if V % tp or groups % tp:
+        raise TbikError(ErrorCode.ShardError, "lm_head: vocab / groups not divisible by tp")
+    vl, gl = V // tp, groups // tp
+    logits = torch.empty((M, V), dtype=torch.float32, device=x.device)
+    nst = chunk_states_per_row(V, groups)
+    chunks = torch.empty((M, nst, 2), dtype=torch.float32, device=x.device)
+    ns = chunk_states_per_row(vl, gl)
+    for r in range(tp):
+        tree_matmul_logits(x, w[:, r * vl:(r + 1) * vl], gl, cfg, leaf, out=logits[:, r * vl:(r + 1) * vl],
+                           chunks=chunks[:, r * ns:(r + 1) * ns])
+    return logits, chunks
+
+
+def _finish(logits, lse, v_offset, targets, full, lp, tlp):
+    pl, _, ld = _mat(logits, "logits")
+    rows, vl = logits.shape
+    if lp is not None or tlp is not None:
+        check(lib.tbik_logsoftmax_finish(pl, ld, rows, vl, C.c_void_p(lse.data_ptr()),
+                                         C.c_void_p(lp.data_ptr()) if lp is not None else None,
+                                         lp.stride(0) if lp is not None else vl,
+                                         C.c_void_p(targets.data_ptr()) if targets is not None else None, v_offset,
+                                         C.c_void_p(tlp.data_ptr()) if tlp is not None else None, _stream()))
+
+
+def log_softmax(logits, groups: int = 8, tp: int = 1, targets=None, full: bool = True, chunks=None):
     """Vocab-sharded tree log-softmax over `tp` simulated shards.
-    Returns (lse[rows], logprobs[rows, V] or None, target_logprobs[rows] or None)."""
+    Returns (lse[rows], logprobs[rows, V] or None, target_logprobs[rows] or None).
+    `chunks`: the logits' 16-column (m, s) chunk states (tree_matmul_logits /
+    column_parallel_logits) -- then the first pass does not re-read the logits."""
     torch = _torch()
     rows, V = logits.shape
     pl, dl, ld = _mat(logits, "logits")
     if dl != F32:
         raise TbikError(ErrorCode.UnknownDtype, "log_softmax expects f32 logits")
+    if chunks is not None:
+        if tp < 1 or tp & (tp - 1) or V % tp or groups % tp:
+            raise TbikError(ErrorCode.ShardError, "log_softmax: vocab / groups not divisible by tp")
+        vl, gl = V // tp, groups // tp
+        ns = chunk_states_per_row(vl, gl)
+        ms = torch.empty((tp, rows, 2), dtype=torch.float32, device=logits.device)
+        for r in range(tp):
+            check(lib.tbik_logsoftmax_shard_state_chunks(C.c_void_p(chunks[:, r * ns:].data_ptr()),
+                                                         chunks.stride(0) // 2, rows, vl, gl,
+                                                         C.c_void_p(ms[r].data_ptr()), _stream()))
+        lse = torch.empty(rows, dtype=torch.float32, device=logits.device)
+        check(lib.tbik_logsoftmax_merge(_ptr_array([ms[r] for r in range(tp)]), tp, rows,
+                                        C.c_void_p(lse.data_ptr()), _stream()))
+        lp = torch.empty((rows, V), dtype=torch.float32, device=logits.device) if full else None
+        tg = tlp = None
+        if targets is not None:
+            tg = targets.to(torch.int64).contiguous()
+            tlp = torch.empty(rows, dtype=torch.float32, device=logits.device)
+        for r in range(tp):
+            _finish(logits[:, r * vl:(r + 1) * vl], lse, r * vl, tg, full,
+                    lp[:, r * vl:(r + 1) * vl] if lp is not None else None, tlp)
+        return lse, lp, tlp
     lse = torch.empty(rows, dtype=torch.float32, device=logits.device)
     lp = torch.empty((rows, V), dtype=torch.float32, device=logits.device) if full else None
     tlp = None
@@ -550,7 +634,8 @@ class PeerGroup:
         check(lib.tbik_group_all_gather(self._h, p, rows, cols, ld, local.element_size(), po, ldo, _stream()))
         return out
 
-    def log_softmax(self, logits_shard, groups_local: int, v_offset: int, targets=None, full: bool = True):
+    def log_softmax(self, logits_shard, groups_local: int, v_offset: int, targets=None, full: bool = True,
+                    chunks=None):
         """Vocab-sharded tree log-softmax over the group: this rank's logits
         [rows x V/W] (its column shard of the vocabulary, `groups_local` = G/W of the
         canonical vocab groups) -> (lse[rows] identical on every rank, this rank's
@@ -563,7 +648,12 @@ class PeerGroup:
             raise TbikError(ErrorCode.UnknownDtype, "log_softmax expects f32 logits")
         dev = logits_shard.device
         ms = torch.empty((rows, 2), dtype=torch.float32, device=dev)
-        check(lib.tbik_logsoftmax_shard_state(pl, ld, rows, vl, groups_local, C.c_void_p(ms.data_ptr()), _stream()))
+        if chunks is not None:  # the lm_head epilogue's chunk states: the logits are not re-read
+            check(lib.tbik_logsoftmax_shard_state_chunks(C.c_void_p(chunks.data_ptr()), chunks.stride(0) // 2, rows, vl,
+                                                         groups_local, C.c_void_p(ms.data_ptr()), _stream()))
+        else:
+            check(lib.tbik_logsoftmax_shard_state(pl, ld, rows, vl, groups_local, C.c_void_p(ms.data_ptr()),
+                                                  _stream()))
         lse = torch.empty(rows, dtype=torch.float32, device=dev)
         check(lib.tbik_group_logsoftmax_merge(self._h, C.c_void_p(ms.data_ptr()), rows, C.c_void_p(lse.data_ptr()),
                                               _stream()))

@@ -407,6 +407,37 @@ tbik_status tbik_tree_matmul_silu_mul(const void* A, int a_dtype, int64_t lda, c
   return launch_silu_mul_il(tmp, N, M, I, static_cast<uint16_t*>(act), ld_act, s);
 }
 
+tbik_status tbik_tree_matmul_logits(const void* A, int a_dtype, int64_t lda, const void* B, int b_dtype, int64_t ldb,
+                                    float* C, int64_t ldc, float* chunk_ms, int64_t ld_chunks, int64_t M, int64_t N,
+                                    int64_t K, int64_t groups, const tbik_block_config* cfg, int leaf_mode,
+                                    void* stream) {
+  if (!cfg || !chunk_ms) return set_error(TBIK_BAD_ARGUMENT, "null argument");
+  TBIK_TRY(check_mat(A, a_dtype, M, K, lda, "A"));
+  TBIK_TRY(check_mat(B, b_dtype, K, N, ldb, "B"));
+  TBIK_TRY(check_mat(C, TBIK_F32, M, N, ldc, "C"));
+  if (groups < 1 || (groups & (groups - 1)) || N % groups)
+    return set_error(TBIK_SHARD_ERROR, "logits: groups must be a power of two dividing N");
+  TBIK_TRY(require_device());
+  GemmView v;
+  TBIK_TRY(make_view(A, a_dtype, lda, B, b_dtype, ldb, M, N, K, cfg->block_k, cfg->k_first, &v));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t n = N / groups, nc = (n + 15) / 16;
+  if (ld_chunks < groups * nc) return set_error(TBIK_BAD_ARGUMENT, "logits: ld_chunks < groups * chunks per group");
+  // The chunk states come out of the tcgen05 GEMM's epilogue when the GEMM is one
+  // FULL pair-tile launch (M > 128; not the skinny or K-split schedules) and chunks
+  // are absolute 16-column blocks (n % 16 == 0); otherwise a pass over the logits
+  // computes the same states (tb_ms_chunk16 in both) -- a pure scheduling choice.
+  if (leaf_mode == TBIK_LEAF_TCGEN05 && n % 16 == 0 && M > 128 && !tc_use_skinny(v) && tc_split_units(v) <= 1 &&
+      tc_supported(v, nullptr) && (reinterpret_cast<uintptr_t>(chunk_ms) & 7) == 0) {
+    GemmOut o{OUT_FULL, v.T, C, ldc, 0};
+    o.ms = chunk_ms;
+    o.ld_ms = 2 * ld_chunks;
+    return launch_tc_gemm(v, o, s);
+  }
+  TBIK_TRY(run_tree_gemm(v, C, ldc, leaf_mode, s));
+  return tbik_logsoftmax_chunk_states(C, ldc, M, N, groups, chunk_ms, ld_chunks, stream);
+}
+
 tbik_status tbik_tree_matmul_leaves(const void* A, int a_dtype, int64_t lda, const void* B, int b_dtype,
                                     int64_t ldb, float* leaves, int64_t M, int64_t N, int64_t K,
                                     const tbik_block_config* cfg, int leaf_mode, void* stream) {

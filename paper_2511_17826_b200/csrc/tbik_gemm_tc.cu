@@ -137,6 +137,8 @@ struct TcParams {
   int acc4;        // 1: four TMEM accumulators (items without tree levels leave cols 256-511 free)
   uint16_t* act;   // non-null: SiLU*up epilogue -- columns interleave gate (even) / up (odd);
   long long ld_act;  //   act[row][j] = bf16(silu(g[2j]) * g[2j+1]) replaces the f32 store
+  float2* ms_out;  // non-null (FULL mode): also the log-softmax (m, s) state of every 16-column
+  long long ld_ms; //   chunk (tb_ms_chunk16): ms_out[row][col / 16] -- the lm_head epilogue
   // Fused tree all-reduce (ar_W > 1; FULL mode, pair tiles): owner(item) = item % ar_W.
   int ar_W, ar_rank;
   uint32_t ar_epoch;
@@ -373,8 +375,11 @@ __device__ __forceinline__ void ar_finish(const TcParams& p, long long pair, lon
 // merges into it, so a pair of leaves costs two accumulator drains instead of two
 // drains + a level-1 store + load.
 // AR: the fused tree all-reduce variant (pair tiles, FULL mode; tbik_group.cu).
+// MSE: the lm_head variant -- the epilogue also emits the log-softmax (m, s) state
+// of every 16-column chunk (a separate instantiation: the exp code would otherwise
+// cost the plain GEMM registers).
 constexpr int EPI = MERGE_WARPS;
-template <bool KF1, int ABOX, bool PAIR, bool DEEP, bool AR = false>
+template <bool KF1, int ABOX, bool PAIR, bool DEEP, bool AR = false, bool MSE = false>
 __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     tc_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const TcParams p) {
@@ -713,6 +718,23 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           }
         }
         }  // the carry left the top level: g is this unit's complete (sub)tree
+        if (MSE && row_ok) {
+          // lm_head: the (m, s) state of each of this thread's four 16-column chunks,
+          // computed on the final f32 logits in registers (F2: the log-softmax's
+          // first pass never re-reads the logits from HBM)
+#pragma unroll
+          for (int j = 0; j < COLS / TB_MS_CHUNK; ++j) {
+            const int col = it.n0 + col0 + j * TB_MS_CHUNK;
+            if (col < p.N) {
+              float v[TB_MS_CHUNK];
+#pragma unroll
+              for (int i = 0; i < TB_MS_CHUNK; ++i) v[i] = g[j * TB_MS_CHUNK + i];
+              float cm, cs;
+              tb_ms_chunk16(v, cm, cs);
+              p.ms_out[static_cast<size_t>(grow) * p.ld_ms + col / TB_MS_CHUNK] = make_float2(cm, cs);
+            }
+          }
+        }
         if (p.act) {
           // fused SiLU(gate) * up (tb_silu_mul_bf16, the same ops as tbik_silu_mul):
           // this thread's 64 columns are 32 (gate, up) pairs -> 32 bf16 outputs
@@ -971,6 +993,10 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   p.unit_stride = o.unit_stride;
   p.act = o.act;
   p.ld_act = o.ld_act;
+  p.ms_out = reinterpret_cast<float2*>(o.ms);
+  p.ld_ms = o.ld_ms / 2;
+  if (o.ms && (o.mode != OUT_FULL || o.act || (reinterpret_cast<uintptr_t>(o.ms) & 7) || (o.ld_ms & 1)))
+    return set_error(TBIK_BAD_ARGUMENT, "tc gemm: chunk (m, s) epilogue needs FULL mode, f32 output, 8-byte states");
   if (o.act && (o.mode != OUT_FULL || v.N % 2)) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: SiLU epilogue needs FULL mode and even N");
   if (o.mode == OUT_LEAVES) {
     p.tiles_per_unit = 1;
@@ -1098,7 +1124,14 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
 #undef TBIK_TC_K
   const int ai = abox == 32 ? 0 : abox == 64 ? 1 : 2;
   const bool ar_on = p.ar_W > 1;
-  const Kern kern = ar_on ? (deep ? (kf1 ? tc_tree_gemm_kernel<true, 128, true, true, true>
+  const bool mse = p.ms_out != nullptr;
+  if (mse && !(pair && abox == 128 && !ar_on))
+    return set_error(TBIK_UNSUPPORTED, "tc gemm: the chunk (m, s) epilogue runs on 256-row pair tiles only");
+  const Kern kern = mse ? (deep ? (kf1 ? tc_tree_gemm_kernel<true, 128, true, true, false, true>
+                                       : tc_tree_gemm_kernel<false, 128, true, true, false, true>)
+                                : (kf1 ? tc_tree_gemm_kernel<true, 128, true, false, false, true>
+                                       : tc_tree_gemm_kernel<false, 128, true, false, false, true>))
+                  : ar_on ? (deep ? (kf1 ? tc_tree_gemm_kernel<true, 128, true, true, true>
                                          : tc_tree_gemm_kernel<false, 128, true, true, true>)
                                   : (kf1 ? tc_tree_gemm_kernel<true, 128, true, false, true>
                                          : tc_tree_gemm_kernel<false, 128, true, false, true>))

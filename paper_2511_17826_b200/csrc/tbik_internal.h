@@ -45,6 +45,8 @@ struct GemmOut {
   int64_t unit_stride; // elements between workspace slices
   uint16_t* act = nullptr;  // FULL only: write bf16(silu(gate) * up) of interleaved column pairs here
   int64_t ld_act = 0;       //   (row stride in elements; `out` is unused then)
+  float* ms = nullptr;      // FULL only (tcgen05): also write the (m, s) state of every 16-column
+  int64_t ld_ms = 0;        //   log-softmax chunk: ms[row][2 * (col / 16) + {0, 1}] (row stride ld_ms floats)
 };
 
 tbik_status launch_fma_gemm(const GemmView& v, const GemmOut& o, cudaStream_t s);

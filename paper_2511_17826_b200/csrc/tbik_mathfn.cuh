@@ -142,6 +142,49 @@ __device__ __forceinline__ void tb_exp_nonpos_normal2(float a, float b, float& e
   f2_unpack(f2_mul(y, f2_pack(__uint_as_float(sl), __uint_as_float(sh))), ea, eb);
 }
 
+// (m, s) state of one 16-logit log-softmax chunk held in registers (the canonical
+// chunk of tbo_tree_logsoftmax): m = sequential max (x > m ? x : m) from v[0],
+// s = ((0 + e_0) + e_1) + ... + e_15, e_i = exp(x_i - m) in ascending order;
+// all -inf -> (-inf, 0).  Shared by the log-softmax kernels and the lm_head GEMM
+// epilogue so both produce the same bits.
+constexpr int TB_MS_CHUNK = 16;
+__device__ __forceinline__ void tb_ms_chunk16(const float (&v)[TB_MS_CHUNK], float& m_out, float& s_out) {
+  const float NEG_INF = __int_as_float(0xFF800000);
+  // fmaxf gives the sequential compare's bits unless the maximum is a zero (only
+  // its sign is ambiguous): redo those in order (NaN is outside the contract).
+  float m = v[0], lo = v[0];
+#pragma unroll
+  for (int k = 1; k < TB_MS_CHUNK; ++k) {
+    m = fmaxf(m, v[k]);
+    lo = fminf(lo, v[k]);
+  }
+  if (m == 0.0f) {
+    m = v[0];
+#pragma unroll
+    for (int k = 1; k < TB_MS_CHUNK; ++k) m = v[k] > m ? v[k] : m;
+  }
+  float sum = 0.0f;
+  if (m != NEG_INF) {
+    // every x - m >= lo - m (rounding is monotone): when that is >= -86 no element
+    // needs tb_exp_nonpos's underflow handling -> the packed two-lane polynomial
+    if (__fsub_rn(lo, m) >= -86.0f) {
+      const unsigned long long m2 = f2_pack(m, m);
+#pragma unroll
+      for (int k = 0; k < TB_MS_CHUNK; k += 2) {
+        float d0, d1, e0, e1;
+        f2_unpack(f2_sub(f2_pack(v[k], v[k + 1]), m2), d0, d1);
+        tb_exp_nonpos_normal2(d0, d1, e0, e1);
+        sum = __fadd_rn(__fadd_rn(sum, e0), e1);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < TB_MS_CHUNK; ++k) sum = __fadd_rn(sum, tb_exp_nonpos(__fsub_rn(v[k], m)));
+    }
+  }
+  m_out = m;
+  s_out = m == NEG_INF ? 0.0f : sum;
+}
+
 // bf16(silu(z) * up), silu(z) = z / (1 + exp(-z))  (demo.cpp:36-45, :171-174) -- the
 // one definition used by the SiLU*up kernel and the gate_up GEMM epilogue.
 __device__ __forceinline__ uint16_t tb_silu_mul_bf16(float z, float up) {

@@ -55,24 +55,6 @@ __device__ __forceinline__ float block_tree_sum(float v, float* sh) {
   return sh[8];
 }
 
-__device__ __forceinline__ MS block_tree_ms(MS v, MS* sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    MS o{__shfl_xor_sync(0xffffffffu, v.m, d), __shfl_xor_sync(0xffffffffu, v.s, d)};
-    v = (lane & d) ? ms_merge(o, v) : ms_merge(v, o);  // always merge(lower, upper)
-  }
-  if (lane == 0) sh[warp] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const MS a = ms_merge(sh[0], sh[1]), b = ms_merge(sh[2], sh[3]);
-    const MS c = ms_merge(sh[4], sh[5]), d = ms_merge(sh[6], sh[7]);
-    sh[8] = ms_merge(ms_merge(a, b), ms_merge(c, d));
-  }
-  __syncthreads();
-  return sh[8];
-}
-
 // ---- RMSNorm ------------------------------------------------------------------
 // Pass 1 folds lane l's 16-byte chunks (l, l+256, ...) with an fma chain and
 // keeps the first CACHE of them in registers; pass 2 revisits the same chunks
@@ -278,114 +260,84 @@ __global__ void __launch_bounds__(LANES) residual_rmsnorm_kernel(uint16_t* __res
 }
 
 // ---- log-softmax ----------------------------------------------------------------
-// Group states: one CTA per (row, group) of n = v_local / groups logits.  Lane l
-// owns chunks l, l+256, ... of 4 logits and consumes them in blocks of MSB of its
-// chunks (tbo_tree_logsoftmax): block max (sequential, ascending), then
-// s = ((0 + exp(x_0 - m)) + exp(x_1 - m)) + ...; blocks fold left with ms_merge.
-// The block's 32 logits stay in registers between the two passes.
-constexpr int MSB = 8;
-
-template <bool VEC>
-__global__ void __launch_bounds__(LANES, 4) ms_group_kernel(const float* __restrict__ logits, int64_t ld, int64_t n,
-                                                         int64_t groups, MS* __restrict__ out) {
-  __shared__ MS sh[9];
-  const int64_t row = blockIdx.x, g = blockIdx.y;
-  const float* x = logits + row * ld + g * n;
-  const int64_t nch = (n + 3) / 4;
-  const float NEG_INF = __int_as_float(0xFF800000);
-  MS st{NEG_INF, 0.0f};
-  const int64_t nfull = n / 4;  // chunks holding 4 logits
-  for (int64_t c0 = threadIdx.x; c0 < nch; c0 += static_cast<int64_t>(LANES) * MSB) {
-    float v[MSB * 4];
-    MS b{NEG_INF, 0.0f};
-    if (VEC && c0 + static_cast<int64_t>(MSB - 1) * LANES < nfull) {
-      // full block: MSB float4 loads, no guards
+// Group states (tbo_tree_logsoftmax): one CTA per (row, group) of n = v_local /
+// groups logits.  The group is cut into chunks of 16 logits from its start (the
+// last possibly shorter); chunk c's (m, s) state is computed by thread c % 256
+// from the logits (tb_ms_chunk16 -- the function the lm_head GEMM epilogue uses)
+// or, FROM_STATES, read from a chunk-state array that epilogue (or
+// chunk_states_kernel) wrote; the chunk states then meet by pairwise levels in
+// shared memory ((2i, 2i+1) -> i, an odd last state passes up).
+__device__ __forceinline__ MS chunk_state_mem(const float* __restrict__ x, int cnt, bool vec) {
+  float v[TB_MS_CHUNK];
+  if (vec && cnt == TB_MS_CHUNK) {
 #pragma unroll
-      for (int j = 0; j < MSB; ++j) {
-        const float4 q = *reinterpret_cast<const float4*>(x + (c0 + static_cast<int64_t>(j) * LANES) * 4);
-        v[4 * j] = q.x;
-        v[4 * j + 1] = q.y;
-        v[4 * j + 2] = q.z;
-        v[4 * j + 3] = q.w;
-      }
-      // canonical max: sequential m = x > m ? x : m.  fmaxf gives the same bits
-      // unless the maximum is a zero (only its sign is ambiguous): redo those.
-      float m = v[0], lo = v[0];
-#pragma unroll
-      for (int k = 1; k < MSB * 4; ++k) {
-        m = fmaxf(m, v[k]);
-        lo = fminf(lo, v[k]);
-      }
-      if (m == 0.0f) {
-        m = v[0];
-#pragma unroll
-        for (int k = 1; k < MSB * 4; ++k) m = v[k] > m ? v[k] : m;
-      }
-      if (m != NEG_INF) {
-        float sum = 0.0f;
-        // every x - m >= lo - m (rounding is monotone): when that is >= -86 no
-        // element needs tb_exp_nonpos's underflow handling (NaNs agree either way)
-        if (__fsub_rn(lo, m) >= -86.0f) {
-          const unsigned long long m2 = f2_pack(m, m);
-#pragma unroll
-          for (int k = 0; k < MSB * 4; k += 2) {
-            float d0, d1, e0, e1;
-            f2_unpack(f2_sub(f2_pack(v[k], v[k + 1]), m2), d0, d1);
-            tb_exp_nonpos_normal2(d0, d1, e0, e1);
-            sum = __fadd_rn(__fadd_rn(sum, e0), e1);
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < MSB * 4; ++k) sum = __fadd_rn(sum, tb_exp_nonpos(__fsub_rn(v[k], m)));
-        }
-        b = MS{m, sum};
-      }
-    } else {
-      // the lane's last (partial) block: nv < MSB chunks, the last possibly ragged;
-      // loops stop at nv so the absent chunks cost nothing
-      int nv = 0;
-#pragma unroll
-      for (int j = 0; j < MSB; ++j)
-        if (c0 + static_cast<int64_t>(j) * LANES < nch) nv = j + 1;
-      const int64_t clast = c0 + static_cast<int64_t>(nv - 1) * LANES;
-      const int last_cnt = n - clast * 4 < 4 ? static_cast<int>(n - clast * 4) : 4;
-#pragma unroll
-      for (int j = 0; j < MSB; ++j) {
-        if (j >= nv) break;
-        const int64_t e0 = (c0 + static_cast<int64_t>(j) * LANES) * 4;
-        if (VEC && (j < nv - 1 || last_cnt == 4)) {
-          const float4 q = *reinterpret_cast<const float4*>(x + e0);
-          v[4 * j] = q.x;
-          v[4 * j + 1] = q.y;
-          v[4 * j + 2] = q.z;
-          v[4 * j + 3] = q.w;
-        } else {
-          const int cj = j < nv - 1 ? 4 : last_cnt;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) v[4 * j + i] = i < cj ? x[e0 + i] : NEG_INF;
-        }
-      }
-      const int nel = (nv - 1) * 4 + last_cnt;  // valid logits, in ascending order
-      float m = v[0];
-#pragma unroll
-      for (int k = 1; k < MSB * 4; ++k) {
-        if (k >= nel) break;
-        m = v[k] > m ? v[k] : m;
-      }
-      if (m != NEG_INF) {
-        float sum = 0.0f;
-#pragma unroll
-        for (int k = 0; k < MSB * 4; ++k) {
-          if (k >= nel) break;
-          sum = __fadd_rn(sum, tb_exp_nonpos(__fsub_rn(v[k], m)));
-        }
-        b = MS{m, sum};
-      }
+    for (int q = 0; q < 4; ++q) {
+      const float4 f = reinterpret_cast<const float4*>(x)[q];
+      v[4 * q] = f.x;
+      v[4 * q + 1] = f.y;
+      v[4 * q + 2] = f.z;
+      v[4 * q + 3] = f.w;
     }
-    st = ms_merge(st, b);
+  } else {
+    // a ragged chunk: -inf padding adds exp(-inf) = +0 terms (the sum is never -0)
+    // and never wins the max -- the bits of the cnt-element chunk
+#pragma unroll
+    for (int k = 0; k < TB_MS_CHUNK; ++k) v[k] = k < cnt ? x[k] : __int_as_float(0xFF800000);
   }
-  const MS r = block_tree_ms(st, sh);
-  if (threadIdx.x == 0) out[row * groups + g] = r;
+  MS r;
+  tb_ms_chunk16(v, r.m, r.s);
+  return r;
+}
+
+template <bool FROM_STATES, bool VEC>
+__global__ void __launch_bounds__(LANES) ms_group_kernel(const float* __restrict__ logits, int64_t ld, int64_t n,
+                                                         const float2* __restrict__ chunks, int64_t ld_chunks,
+                                                         int64_t groups, MS* __restrict__ out) {
+  extern __shared__ MS ms_buf[];  // 2 x nc states (ping-pong)
+  const int64_t row = blockIdx.x, g = blockIdx.y;
+  const int nc = static_cast<int>((n + TB_MS_CHUNK - 1) / TB_MS_CHUNK);
+  MS* a = ms_buf;
+  MS* b = ms_buf + nc;
+  for (int c = threadIdx.x; c < nc; c += LANES) {
+    if constexpr (FROM_STATES) {
+      const float2 f = chunks[row * ld_chunks + g * nc + c];
+      a[c] = MS{f.x, f.y};
+    } else {
+      const int64_t e0 = static_cast<int64_t>(c) * TB_MS_CHUNK;
+      const int cnt = n - e0 < TB_MS_CHUNK ? static_cast<int>(n - e0) : TB_MS_CHUNK;
+      a[c] = chunk_state_mem(logits + row * ld + g * n + e0, cnt, VEC);
+    }
+  }
+  __syncthreads();
+  int cnt = nc;
+  while (cnt > 1) {
+    const int h = cnt >> 1;
+    for (int i = threadIdx.x; i < h; i += LANES) b[i] = ms_merge(a[2 * i], a[2 * i + 1]);
+    if ((cnt & 1) && threadIdx.x == 0) b[h] = a[cnt - 1];
+    __syncthreads();
+    MS* t = a;
+    a = b;
+    b = t;
+    cnt = h + (cnt & 1);
+  }
+  if (threadIdx.x == 0) out[row * groups + g] = a[0];
+}
+
+// Chunk states of a [rows x v_local] logit block, groups of n (chunks restart at
+// every group): the non-fused producer of the FROM_STATES input.
+template <bool VEC>
+__global__ void chunk_states_kernel(const float* __restrict__ logits, int64_t ld, int64_t n, int64_t groups,
+                                    float2* __restrict__ out, int64_t ld_out) {
+  const int64_t row = blockIdx.y;
+  const int64_t nc = (n + TB_MS_CHUNK - 1) / TB_MS_CHUNK;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < groups * nc;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t g = i / nc, c = i - g * nc;
+    const int64_t e0 = c * TB_MS_CHUNK;
+    const int cnt = n - e0 < TB_MS_CHUNK ? static_cast<int>(n - e0) : TB_MS_CHUNK;
+    const MS r = chunk_state_mem(logits + row * ld + g * n + e0, cnt, VEC);
+    out[row * ld_out + i] = make_float2(r.m, r.s);
+  }
 }
 
 // Contiguous-halves tree over `count` (power of two) states per row.
@@ -511,30 +463,77 @@ tbik_status tbik_residual_rmsnorm(void* h, int64_t ldh, const float* f, int64_t 
   return tbik_tree_rmsnorm(h, TBIK_BF16, ldh, gamma, eps, y, TBIK_BF16, ldy, rows, cols, stream);
 }
 
-tbik_status tbik_logsoftmax_shard_state(const float* logits, int64_t ld, int64_t rows, int64_t v_local, int64_t groups,
-                                        float* ms_out, void* stream) {
-  if (!logits || !ms_out) return set_error(TBIK_BAD_ARGUMENT, "null argument");
+namespace {
+tbik_status shard_state_impl(const float* logits, int64_t ld, const float2* chunks, int64_t ld_chunks, int64_t rows,
+                             int64_t v_local, int64_t groups, float* ms_out, cudaStream_t s) {
+  if (!ms_out || (!logits && !chunks)) return set_error(TBIK_BAD_ARGUMENT, "null argument");
   if (rows < 1 || v_local < 1) return set_error(TBIK_BAD_DIMENSION, "logsoftmax: dimensions must be >= 1");
   if (groups < 1 || (groups & (groups - 1)) || v_local % groups)
     return set_error(TBIK_SHARD_ERROR, "logsoftmax: shard of " + std::to_string(v_local) +
                                            " logits is not a power-of-two number of equal groups (" +
                                            std::to_string(groups) + ")");
-  if (ld < v_local) return set_error(TBIK_BAD_ARGUMENT, "logsoftmax: ld < v_local");
+  if (logits && ld < v_local) return set_error(TBIK_BAD_ARGUMENT, "logsoftmax: ld < v_local");
   if (rows > 0x7FFFFFFF || groups > 65535) return set_error(TBIK_UNSUPPORTED, "logsoftmax: grid too large");
-  if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t n = v_local / groups;
+  const int64_t nc = (n + TB_MS_CHUNK - 1) / TB_MS_CHUNK;
+  const size_t smem = static_cast<size_t>(2 * nc) * sizeof(MS);
+  if (chunks && ld_chunks < groups * nc) return set_error(TBIK_BAD_ARGUMENT, "logsoftmax: ld_chunks too small");
+  if (smem > 200 * 1024)
+    return set_error(TBIK_UNSUPPORTED, "logsoftmax: vocab group of " + std::to_string(n) +
+                                           " logits exceeds one CTA's chunk buffer; use more groups");
+  if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
   MS* gs = static_cast<MS*>(workspace(static_cast<size_t>(rows) * groups * sizeof(MS), 3, s));
   if (!gs) return set_error(TBIK_CUDA_ERROR, "workspace allocation failed");
-  const bool vec = (reinterpret_cast<uintptr_t>(logits) & 15) == 0 && ld % 4 == 0 && n % 4 == 0;
+  const bool vec = logits && (reinterpret_cast<uintptr_t>(logits) & 15) == 0 && ld % 4 == 0 && n % 4 == 0;
   dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>(groups));
-  if (vec)
-    ms_group_kernel<true><<<grid, LANES, 0, s>>>(logits, ld, n, groups, gs);
-  else
-    ms_group_kernel<false><<<grid, LANES, 0, s>>>(logits, ld, n, groups, gs);
+  auto kern = chunks ? ms_group_kernel<true, false> : vec ? ms_group_kernel<false, true> : ms_group_kernel<false, false>;
+  if (smem > 48 * 1024)
+    TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kern<<<grid, LANES, smem, s>>>(logits, ld, n, chunks, ld_chunks, groups, gs);
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   ms_rows_kernel<<<static_cast<unsigned>((rows + 127) / 128), 128, 0, s>>>(gs, rows, groups, ms_out);
+  TBIK_CUDA(cudaGetLastError());
+  count_launch();
+  return TBIK_OK;
+}
+}  // namespace
+
+tbik_status tbik_logsoftmax_shard_state(const float* logits, int64_t ld, int64_t rows, int64_t v_local, int64_t groups,
+                                        float* ms_out, void* stream) {
+  if (!logits) return set_error(TBIK_BAD_ARGUMENT, "null logits");
+  return shard_state_impl(logits, ld, nullptr, 0, rows, v_local, groups, ms_out, static_cast<cudaStream_t>(stream));
+}
+
+tbik_status tbik_logsoftmax_shard_state_chunks(const float* chunk_ms, int64_t ld_chunks, int64_t rows, int64_t v_local,
+                                               int64_t groups, float* ms_out, void* stream) {
+  if (!chunk_ms) return set_error(TBIK_BAD_ARGUMENT, "null chunk states");
+  if (reinterpret_cast<uintptr_t>(chunk_ms) & 7) return set_error(TBIK_BAD_ARGUMENT, "chunk states: 8-byte alignment");
+  return shard_state_impl(nullptr, 0, reinterpret_cast<const float2*>(chunk_ms), ld_chunks, rows, v_local, groups,
+                          ms_out, static_cast<cudaStream_t>(stream));
+}
+
+tbik_status tbik_logsoftmax_chunk_states(const float* logits, int64_t ld, int64_t rows, int64_t v_local,
+                                         int64_t groups, float* chunk_ms, int64_t ld_chunks, void* stream) {
+  if (!logits || !chunk_ms) return set_error(TBIK_BAD_ARGUMENT, "null argument");
+  if (rows < 1 || v_local < 1) return set_error(TBIK_BAD_DIMENSION, "logsoftmax: dimensions must be >= 1");
+  if (groups < 1 || (groups & (groups - 1)) || v_local % groups)
+    return set_error(TBIK_SHARD_ERROR, "logsoftmax: groups must be a power of two dividing the shard");
+  if (ld < v_local) return set_error(TBIK_BAD_ARGUMENT, "logsoftmax: ld < v_local");
+  if (rows > 65535) return set_error(TBIK_UNSUPPORTED, "logsoftmax: > 65535 rows per call");
+  if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
+  const int64_t n = v_local / groups, nc = (n + TB_MS_CHUNK - 1) / TB_MS_CHUNK;
+  if (ld_chunks < groups * nc) return set_error(TBIK_BAD_ARGUMENT, "logsoftmax: ld_chunks too small");
+  if (reinterpret_cast<uintptr_t>(chunk_ms) & 7) return set_error(TBIK_BAD_ARGUMENT, "chunk states: 8-byte alignment");
+  const bool vec = (reinterpret_cast<uintptr_t>(logits) & 15) == 0 && ld % 4 == 0 && n % 4 == 0;
+  dim3 grid(static_cast<unsigned>(std::min<int64_t>((groups * nc + 255) / 256, 64)), static_cast<unsigned>(rows));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (vec)
+    chunk_states_kernel<true><<<grid, 256, 0, s>>>(logits, ld, n, groups, reinterpret_cast<float2*>(chunk_ms),
+                                                   ld_chunks);
+  else
+    chunk_states_kernel<false><<<grid, 256, 0, s>>>(logits, ld, n, groups, reinterpret_cast<float2*>(chunk_ms),
+                                                    ld_chunks);
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;

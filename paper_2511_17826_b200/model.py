@@ -300,11 +300,26 @@ class TbikDecoder:
             a = self._residual_norm(h, d, nxt)                  # next layer's ln1 (or ln_f)
         if not w.layers:
             a = self._norm(h, w.ln_f)
-        return self._col(a, w.lm_head, tp)                      # f32 logits [M, vocab]
+        return self._head(a, tp)                                # f32 logits [M, vocab]
+
+    # The lm_head's epilogue also emits the log-softmax's 16-column (m, s) chunk
+    # states (F2); log_probs() of the same logits consumes them instead of
+    # re-reading the logits.  Matched by identity + version of the logits tensor.
+    def _head(self, a, tp):
+        logits, chunks = api.column_parallel_logits(a, self.w.lm_head, api.DeviceGroup(tp), self.cfg.vocab_groups,
+                                                    self.bcfg, self.leaf)
+        self._chunk_cache = (logits, logits._version, chunks)
+        return logits
+
+    def _cached_chunks(self, logits):
+        c = getattr(self, "_chunk_cache", None)
+        if c is not None and c[0] is logits and c[1] == logits._version:
+            return c[2]
+        return None
 
     def log_probs(self, logits, tp: int = 1, targets=None, full: bool = True):
         """Vocab-sharded tree log-softmax over `tp` simulated vocab shards."""
-        return api.log_softmax(logits, self.cfg.vocab_groups, tp, targets, full)
+        return api.log_softmax(logits, self.cfg.vocab_groups, tp, targets, full, chunks=self._cached_chunks(logits))
 
     # -- CUDA graphs -------------------------------------------------------------------
     def capture(self, tokens, tp: int = 1, full_logprobs: bool = True):
@@ -383,10 +398,17 @@ class ShardedDecoder(TbikDecoder):
     def _gate_up(self, x, w, tp):
         return api.tree_matmul_silu_mul(x, w, None, self.bcfg, self.leaf)
 
+    def _head(self, a, tp):
+        logits, chunks = api.tree_matmul_logits(a, self.w.lm_head, self.cfg.vocab_groups // self.W, self.bcfg,
+                                                self.leaf)
+        self._chunk_cache = (logits, logits._version, chunks)
+        return logits
+
     def log_probs(self, logits, tp: int = 1, targets=None, full: bool = True):
         """(lse, this rank's log-prob columns, target log-probs of targets in this
         rank's vocab range -- NaN elsewhere)."""
-        return self.group.log_softmax(logits, self.cfg.vocab_groups // self.W, self.r * self.v_local, targets, full)
+        return self.group.log_softmax(logits, self.cfg.vocab_groups // self.W, self.r * self.v_local, targets, full,
+                                      chunks=self._cached_chunks(logits))
 
     def gather(self, shard):
         """Rank-ordered column concatenation of a per-rank [rows x V/W] block."""

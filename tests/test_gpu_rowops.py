@@ -113,3 +113,56 @@ def test_logsoftmax_wide_range_blocks(tb, cuda, orc):
         lse, lp, _ = tb.log_softmax(to_dev(x), 8, tp, full=True)
         assert np.array_equal(bits(lse.cpu().numpy()), bits(lse_w)), f"lse tp={tp}"
         assert np.array_equal(bits(lp.cpu().numpy()), bits(lp_w)), f"logprobs tp={tp}"
+
+
+# ---- F2: the lm_head epilogue emits the log-softmax's chunk states -------------------
+@pytest.mark.parametrize("M,K,V,G", [(300, 512, 2 * 16032, 8), (1000, 1024, 4096, 8), (64, 512, 4096, 8),
+                                     (300, 512, 8 * 250, 8), (257, 4096, 18992 * 2, 2)])
+def test_lm_head_chunk_states_fused(tb, cuda, orc, M, K, V, G):
+    """tree_matmul_logits: the (m, s) state of every 16-logit chunk, from the tcgen05
+    epilogue (M > 128, V/G % 16 == 0) or the fallback pass (M = 64: skinny GEMM;
+    V/G = 250: ragged chunks), equals the oracle's chunk states of the same logits
+    bit for bit, and the log-softmax from them equals the log-softmax from the logits
+    at every simulated TP."""
+    g = torch.Generator(device=cuda).manual_seed(M + V)
+    x = (torch.randn(M, K, generator=g, device=cuda) * 0.5).to(torch.bfloat16)
+    w = (torch.randn(K, V, generator=g, device=cuda) * 0.2).to(torch.bfloat16)
+    cfg = tb.BlockConfig(64, 256, 128, 0)
+    logits, chunks = tb.tree_matmul_logits(x, w, G, cfg)
+    assert torch.equal(logits.view(torch.int32), tb.tree_matmul(x, w, cfg).view(torch.int32))
+    m_w, s_w = orc.logsoftmax_chunk_states(logits.cpu().numpy(), G)
+    c = chunks.cpu().numpy()
+    assert np.array_equal(bits(c[..., 0]), bits(m_w)) and np.array_equal(bits(c[..., 1]), bits(s_w))
+    targets = torch.randint(0, V, (M,), generator=g, device=cuda)
+    for tp in (1, 2, G):
+        a = tb.log_softmax(logits, G, tp, targets, full=True)
+        b = tb.log_softmax(logits, G, tp, targets, full=True, chunks=chunks)
+        lg, ck = tb.column_parallel_logits(x, w, tb.DeviceGroup(tp), G, cfg)
+        d = tb.log_softmax(lg, G, tp, targets, full=True, chunks=ck)
+        for u, v_ in zip(a, b):
+            assert torch.equal(u.view(torch.int32), v_.view(torch.int32)), f"tp={tp}"
+        for u, v_ in zip(a, d):
+            assert torch.equal(u.view(torch.int32), v_.view(torch.int32)), f"column-parallel tp={tp}"
+    lse_w, _, _ = orc.tree_logsoftmax(logits.cpu().numpy(), G, full=False)
+    assert np.array_equal(bits(a[0].cpu().numpy()), bits(lse_w))
+
+
+def test_chunk_states_masked_and_wide(tb, cuda, orc):
+    """-inf logits (masked vocab), whole masked chunks, and chunks whose spread leaves
+    the fast exp range: the chunk-state pass equals the oracle."""
+    rng = np.random.default_rng(11)
+    V, G = 8 * 1024, 8
+    x = (rng.standard_normal((5, V)) * 3).astype(np.float32)
+    x[0, ::7] = -np.inf
+    x[1, 32:64] = -np.inf
+    x[2, ::33] -= 150.0
+    x[3, :] = 0.0
+    x[3, 5] = -0.0
+    dx = to_dev(x)
+    ns = tb.chunk_states_per_row(V, G)
+    ck = torch.empty(5, ns, 2, device=cuda)
+    tb.api.check(tb.lib.tbik_logsoftmax_chunk_states(
+        tb.api.C.c_void_p(dx.data_ptr()), V, 5, V, G, tb.api.C.c_void_p(ck.data_ptr()), ns, tb.api._stream()))
+    m_w, s_w = orc.logsoftmax_chunk_states(x, G)
+    c = ck.cpu().numpy()
+    assert np.array_equal(bits(c[..., 0]), bits(m_w)) and np.array_equal(bits(c[..., 1]), bits(s_w))
