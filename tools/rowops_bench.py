@@ -111,7 +111,39 @@ def run(M=4096, H=5120, V=151936, groups=8, tps=(1, 2, 4, 8), reps=20):
     ref_lp = torch.log_softmax(logits.double(), -1)
     res["max_abs_err_vs_f64"] = float((ref[1].double() - ref_lp).abs().max())
     out["log_softmax"] = res
-    del logits, ref, ref_lp
+    del ref, ref_lp
+    torch.cuda.empty_cache()
+
+    # ---- F2: lm_head + log-softmax, unfused vs the epilogue-fused chunk states -----------
+    # (M tokens x hidden H) . (H x V) bf16 lm_head, then lse + target log-probs: unfused =
+    # tree GEMM, then the log-softmax reads the 4 M V logits again; fused = the GEMM's
+    # epilogue writes the 16-logit (m, s) chunk states (0.5 B per logit) and the first
+    # pass reads those instead.  Same bits (tested).
+    del logits
+    torch.cuda.empty_cache()
+    xa = (torch.randn(M, H, device=dev, generator=g) * 0.5).to(torch.bfloat16)
+    wl = (torch.randn(H, V, device=dev, generator=g) * 0.02).to(torch.bfloat16)
+    cfg = tb.BlockConfig(64, 256, 128, 0)
+    lg = torch.empty(M, V, device=dev)
+
+    def unfused():
+        tb.tree_matmul(xa, wl, cfg, out=lg)
+        tb.log_softmax(lg, groups, 1, targets, False)
+
+    ck = torch.empty(M, tb.chunk_states_per_row(V, groups), 2, device=dev)
+
+    def fused():
+        tb.tree_matmul_logits(xa, wl, groups, cfg, out=lg, chunks=ck)
+        tb.log_softmax(lg, groups, 1, targets, False, chunks=ck)
+
+    ms_u = ev_ms(unfused, max(reps // 4, 3))
+    ms_f = ev_ms(fused, max(reps // 4, 3))
+    ms_g = ev_ms(lambda: tb.tree_matmul(xa, wl, cfg, out=lg), max(reps // 4, 3))
+    out["lm_head_logsoftmax"] = {"M": M, "H": H, "V": V, "gemm_ms": ms_g, "unfused_ms": ms_u, "fused_ms": ms_f,
+                                 "saved_ms": ms_u - ms_f,
+                                 "path": "tree_matmul + log_softmax(logits) vs tree_matmul_logits + "
+                                         "log_softmax(chunk states); target log-probs, L2 flushed before each call"}
+    del xa, wl, lg, ck
     torch.cuda.empty_cache()
 
     # ---- tree all-reduce of W row-parallel partials (simulated ranks, one GPU's HBM) -------
