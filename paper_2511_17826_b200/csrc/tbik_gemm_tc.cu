@@ -55,10 +55,13 @@
 #include "tbik_common.cuh"
 #include "tbik_internal.h"
 #include "tbik_mathfn.cuh"
+#include "tbik_pair.cuh"
 
 namespace tbik_b200 {
 
 namespace {
+
+using namespace pair_ptx;
 
 constexpr int BM = 128;     // rows per CTA (the pair covers 256)
 constexpr int PAIR_M = 256;
@@ -149,65 +152,6 @@ struct TcParams {
   uint32_t* ar_counter;
 };
 
-// ---- cluster / 2-CTA PTX -----------------------------------------------------------
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t mapa(uint32_t smem_addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// Remote arrives use the default (.release, CTA-scope) semantics: the data they
-// guard is either async-proxy (TMA bytes are counted by complete_tx) or TMEM
-// (ordered by tcgen05.fence::before_thread_sync), so no cluster-scope fence is
-// needed -- a .release.cluster arrive costs a MEMBAR + ERRBAR per call.
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr), "r"(bytes)
-               : "memory");
-}
-// 2SM TMA: data lands in this CTA's smem, completion bytes go to the leader's barrier.
-__device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* map, uint32_t leader_bar,
-                                                int32_t c0, int32_t c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void umma_bf16_2cta(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                               uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-// Arrive on the barrier at the same smem offset in every CTA of `mask`.
-__device__ __forceinline__ void umma_commit_2cta(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_alloc_2cta(uint32_t* smem_result, uint32_t ncols) {
-  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_result)),
-               "r"(ncols));
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-}
-__device__ __forceinline__ void tmem_dealloc_2cta(uint32_t taddr, uint32_t ncols) {
-  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
-}
-
 struct Item {
   int m0, n0, unit, t_begin, t_end;
 };
@@ -236,24 +180,6 @@ __device__ __forceinline__ int tile_chunks(const TcParams& p, int t) {
   return (kh + KSTAGE - 1) / KSTAGE;
 }
 
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int x, int y, int z) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
-               "r"(src), "r"(x), "r"(y), "r"(z)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_complete() {  // all but the N most recent groups WRITTEN
-  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void named_bar(int id, int threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
 // Publish "my half of item `item` is in my send slot" to the item's owner rank:
 // flags[owner][(item * 2 + cta) * W + my_rank] = epoch.
 __device__ __forceinline__ void ar_publish(const TcParams& p, long long item, uint32_t cta) {
@@ -261,9 +187,6 @@ __device__ __forceinline__ void ar_publish(const TcParams& p, long long item, ui
   __threadfence_system();
   const int owner = static_cast<int>(item % p.ar_W);
   st_release_sys(p.ar_flags[owner] + ((item * 2 + cta) * p.ar_W + p.ar_rank), p.ar_epoch);
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // Fused all-reduce of ONE owned item's 128-row half (this CTA's), by threads
@@ -902,6 +825,11 @@ tbik_status tc_make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, u
   return make_map_2d(map, base, inner, outer, row_stride_bytes, box_inner, box_outer);
 }
 
+tbik_status tc_make_map_out(CUtensorMap* map, float* base, uint64_t n, uint64_t m, uint64_t units,
+                            uint64_t row_stride_bytes, uint64_t unit_stride_bytes) {
+  return make_map_out(map, base, n, m, units, row_stride_bytes, unit_stride_bytes);
+}
+
 FusedAr* set_tc_fused_ar(FusedAr* ctx) {
   FusedAr* old = g_fused_ar;
   g_fused_ar = ctx;
@@ -968,6 +896,11 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   std::string why;
   if (!tc_supported(v, &why)) return set_error(TBIK_UNSUPPORTED, why);
   if (o.mode == OUT_GROUPS) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: GROUPS mode is FMA-only");
+  // 256 x 256 pair tiles (tbik_gemm_tc_w.cu) for plain FULL / UNITS launches.
+  if (!g_fused_ar && tc_use_pair(v) && tc_wide_supported(v, o) && tc_wide_wanted(v)) {
+    const tbik_status st = launch_tc_wide(v, o, s);
+    if (st != TBIK_UNSUPPORTED) return st;
+  }
   // A rows staged per stage: the fewest that still cover every row of the pair
   // tile's leader CTA (knob tc_abox overrides, a pure scheduling knob).
   int abox = v.M <= 32 ? 32 : v.M <= 64 ? 64 : 128;

@@ -99,6 +99,8 @@ enum Knob {
   KNOB_GROUP_FUSED,      // 0: no fused GEMM + all-reduce kernel
   KNOB_GROUP_OVERLAP,    // 0: no chunked GEMM / all-reduce overlap
   KNOB_AR_TWO_PHASE_BYTES,  // payload bytes from which the group all-reduce is two-phase
+  KNOB_TC_WIDE,          // 0/1: 256 x 256 pair tiles (tbik_gemm_tc_w.cu)
+  KNOB_TC_WIDE_TAIL,     // 0: no 256 x 128 half items in the wide kernel's last wave
   KNOB_COUNT
 };
 int64_t knob(Knob k, int64_t dflt);
@@ -121,6 +123,12 @@ tbik_status launch_silu_mul_il(const float* gu, int64_t ld, int64_t rows, int64_
 // whole tree (units finished in-kernel) into C.  Same bits as launch_tc_gemm.
 bool tc_use_skinny(const GemmView& v);
 tbik_status launch_tc_skinny(const GemmView& v, float* C, int64_t ldc, cudaStream_t s);
+
+// 256 x 256 pair-tile variant of launch_tc_gemm (tbik_gemm_tc_w.cu): FULL / UNITS
+// modes without epilogues; same bits as the 256 x 128 kernel.
+bool tc_wide_supported(const GemmView& v, const GemmOut& o);
+bool tc_wide_wanted(const GemmView& v);
+tbik_status launch_tc_wide(const GemmView& v, const GemmOut& o, cudaStream_t s);
 
 // K-split factor run_tree_gemm uses for the tcgen05 leaf (1 = one FULL launch).
 int64_t tc_split_units(const GemmView& v);
