@@ -87,14 +87,19 @@ def load_peaks():
         return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic(M, tp):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+def load_traffic_key(key):
+    """dram bytes (read + write) per launch from the committed ncu capture
+    (profiles/ncu_traffic.json, tools/traffic_capture.py)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            t = json.load(f)
-        return t.get(f"M{M}_tp{tp}")
+            return json.load(f).get(key)
     except Exception:  # noqa: BLE001
         return None
+
+
+def load_traffic(M, tp):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    return load_traffic_key(f"M{M}_tp{tp}")
 
 
 class Clocks:
@@ -555,6 +560,8 @@ def run_tbik(args):
             tp_shards["tp"].append(t)
             tp_shards["per_rank_ms"].append(ms_t)
             tp_shards["per_rank_tflops"].append(2.0 * M * N_OUT * (ke0 - kb0) / (ms_t * 1e-3) / 1e12)
+            tp_shards.setdefault("traffic", []).append(load_traffic(M, 1) if t == 1 else
+                                                        load_traffic_key(f"M{M}_shard_tp{t}"))
             del xs_t, ws_t, yt
 
     # ---- the metric's second half: bit-exact logits across TP on the Llama forward ----

@@ -56,9 +56,26 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def line(name, nbytes, ms, peak):
+_TRAFFIC = None
+
+
+def traffic(key):
+    """Cold-cache DRAM bytes (read + write) per call from the committed ncu capture
+    (profiles/ncu_traffic.json, tools/traffic_capture.py), or None."""
+    global _TRAFFIC
+    if _TRAFFIC is None:
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                _TRAFFIC = json.load(f)
+        except Exception:  # noqa: BLE001
+            _TRAFFIC = {}
+    return _TRAFFIC.get(key)
+
+
+def line(name, nbytes, ms, peak, key=None):
     gbs = nbytes / (ms * 1e-3) / 1e9
-    return {"kernel": name, "ms": ms, "alg_bytes": nbytes, "GB/s": gbs, "frac_of_hbm": gbs / peak}
+    return {"kernel": name, "ms": ms, "alg_bytes": nbytes, "GB/s": gbs, "frac_of_hbm": gbs / peak,
+            "traffic": traffic(key) if key else None}
 
 
 def run(M=4096, H=5120, V=151936, groups=8, tps=(1, 2, 4, 8), reps=20):
@@ -73,7 +90,7 @@ def run(M=4096, H=5120, V=151936, groups=8, tps=(1, 2, 4, 8), reps=20):
     x = torch.randn(M, H, device=dev, generator=g).to(torch.bfloat16)
     gamma = (1 + 0.02 * torch.randn(H, device=dev, generator=g))
     ms = ev_ms(lambda: tb.rmsnorm(x, gamma, 1e-6, out_dtype=torch.bfloat16), reps)
-    out["rmsnorm_bf16"] = line("tree_rmsnorm_kernel (bf16->bf16)", 4.0 * M * H + 4 * H, ms, peak)
+    out["rmsnorm_bf16"] = line("tree_rmsnorm_kernel (bf16->bf16)", 4.0 * M * H + 4 * H, ms, peak, "rmsnorm_bf16")
     ms_t = ev_ms(lambda: (x.float() * torch.rsqrt(x.float().pow(2).mean(-1, keepdim=True) + 1e-6)
                           * gamma).to(torch.bfloat16), reps)
     out["rmsnorm_bf16"]["torch_eager_ms"] = ms_t
@@ -102,8 +119,10 @@ def run(M=4096, H=5120, V=151936, groups=8, tps=(1, 2, 4, 8), reps=20):
             same = (torch.equal(ref[0].view(torch.int32), lse.view(torch.int32))
                     and torch.equal(ref[1].view(torch.int32), lp.view(torch.int32))
                     and torch.equal(ref[2].view(torch.int32), tlp.view(torch.int32)))
-        res[f"tp{tp}"] = {"full": line("log-softmax full (ms_group + merge + finish)", full_bytes, ms_full, peak),
-                          "target_logprobs": line("log-prob of targets", tgt_bytes, ms_tgt, peak),
+        res[f"tp{tp}"] = {"full": line("log-softmax full (ms_group + merge + finish)", full_bytes, ms_full, peak,
+                                       f"log_softmax_full_tp{tp}"),
+                          "target_logprobs": line("log-prob of targets", tgt_bytes, ms_tgt, peak,
+                                                  f"log_softmax_targets_tp{tp}"),
                           "bit_identical_to_tp1": bool(same)}
         del lse, lp, tlp
     ms_t = ev_ms(lambda: torch.log_softmax(logits, -1), reps)
@@ -154,7 +173,7 @@ def run(M=4096, H=5120, V=151936, groups=8, tps=(1, 2, 4, 8), reps=20):
         y = torch.empty(E, device=dev)
         grp = tb.DeviceGroup(W)
         ms = ev_ms(lambda: tb.tree_all_reduce(grp, parts), reps)
-        ar[f"W{W}"] = line("allreduce_kernel (Algorithm 2 order)", 4.0 * (W + 1) * E, ms, peak)
+        ar[f"W{W}"] = line("allreduce_kernel (Algorithm 2 order)", 4.0 * (W + 1) * E, ms, peak, f"allreduce_W{W}")
         del parts, y
     out["tree_all_reduce_local"] = ar
     return out
