@@ -406,6 +406,7 @@ def run_tbik(args):
 
     # ---- the dominant kernel on its own (roofline) -----------------------------------
     k_ms = ev_time(lambda: tb.tree_matmul(x, w, cfg, leaf, out=y), max(args.steps, 5))
+    k_name = tb.last_kernel() or ("tc_tree_gemm_kernel" if leaf else "fma_tree_gemm_kernel")
     k_flops = 2.0 * M * N_OUT * Kr
     achieved = k_flops / (k_ms * 1e-3) / 1e12
     peak_tf, peak_hbm, peak_src = load_peaks()
@@ -418,7 +419,7 @@ def run_tbik(args):
     else:
         gbs = bytes_alg / (k_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": gbs, "peak": peak_hbm, "unit": "GB/s", "frac": gbs / peak_hbm}
-    roof.update({"traffic": load_traffic(M, world), "kernel": "tc_tree_gemm_kernel" if leaf else "fma_tree_gemm_kernel",
+    roof.update({"traffic": load_traffic(M, world), "kernel": k_name,
                  "kernel_ms": k_ms, "flops_per_launch": k_flops, "alg_bytes_per_launch": bytes_alg,
                  "peak_source": peak_src, "share_of_step": k_ms / ms if ms else None})
 

@@ -109,6 +109,10 @@ TBIK_API tbik_status tbik_set_schedule(const char* name, int64_t value);
 /* Number of kernels this library has launched in this process (all devices).
  * bench.py reports the delta over its timed region as gpu_launches. */
 TBIK_API uint64_t tbik_launch_count(void);
+/* Name of the last tree-GEMM kernel this host thread launched (tc_tree_gemm_kernel,
+ * tc_w192_tree_gemm_kernel, tc_wide_tree_gemm_kernel, tc_skinny_kernel,
+ * fma_tree_gemm_v2, ...); "" before the first.  Diagnostics: which schedule ran. */
+TBIK_API const char* tbik_last_kernel(void);
 /* Diagnostics: when TBIK_TC_STATS=1, the last tcgen05 GEMM launch records per-CTA
  * wait-cycle counters (8 per CTA: producer empty-wait, MMA tempty-wait, MMA
  * full-wait, merge tfull-wait, producer loop, merge loop, merge busy, unused);

@@ -7,7 +7,7 @@ reference C++ API (proj/include/tbik/*.hpp).  See DESIGN.md.
 from ._lib import ErrorCode, TbikError, header_functions, lib  # noqa: F401
 from .api import (BF16, F32, LEAF_FMA, LEAF_TCGEN05, BlockConfig, DeviceGroup,  # noqa: F401
                   PeerGroup, ReductionPlan, ShardPlan, all_gather, column_parallel_forward,
-                  default_block_config, device_available, launch_count, exchange_handles, log_softmax,
+                  default_block_config, device_available, launch_count, last_kernel, exchange_handles, log_softmax,
                   matrix_read, matrix_write,
                   make_column_shard_plan, make_row_shard_plan, plan_blocks, ring_reduce_baseline,
                   rmsnorm, row_parallel_forward, sync, tree_all_reduce, tree_all_reduce_per_rank,

@@ -80,6 +80,7 @@ _SIGS = {
     "tbik_device_available": (ci, []),
     "tbik_sync": (ci, [vp]),
     "tbik_launch_count": (C.c_uint64, []),
+    "tbik_last_kernel": (C.c_char_p, []),
     "tbik_set_schedule": (ci, [C.c_char_p, i64]),
     "tbik_default_block_config": (ci, [ci, PCFG]),
     "tbik_plan_blocks": (ci, [i64, PCFG, i64, C.POINTER(ReductionPlanC)]),

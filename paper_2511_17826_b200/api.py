@@ -98,6 +98,11 @@ def launch_count() -> int:
     return int(lib.tbik_launch_count())
 
 
+def last_kernel() -> str:
+    """tbik_last_kernel: the last tree-GEMM kernel this thread launched."""
+    return lib.tbik_last_kernel().decode()
+
+
 SCHEDULE_KNOBS = ("tc_pair", "tc_abox", "tc_group_m", "tc_units", "tc_deep", "tc_acc4", "tc_skinny", "sk_mt",
                   "sk_units", "sk_leaf", "sk_bn", "fma_v1", "group_fused", "group_overlap", "ar_two_phase_bytes", "tc_wide", "tc_wide_tail")
 

@@ -25,7 +25,14 @@ thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
 }
 
-void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+namespace {
+thread_local const char* g_last_kernel = "";
+}
+
+void count_launch(const char* kernel) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (kernel) g_last_kernel = kernel;
+}
 
 namespace {
 constexpr int64_t kUnset = INT64_MIN;
@@ -317,6 +324,7 @@ tbik_status tbik_set_schedule(const char* name, int64_t value) {
 
 int tbik_version(void) { return 100; }
 uint64_t tbik_launch_count(void) { return g_launches.load(); }
+const char* tbik_last_kernel(void) { return tbik_b200::g_last_kernel; }
 
 int tbik_device_available(void) {
   int n = 0;

@@ -38,7 +38,8 @@ int current_device_checked();  // -1 when no sm_100 device
 void* workspace(size_t bytes, int slot, cudaStream_t stream);
 
 // Counts every kernel launch issued by the library (tbik_launch_count).
-void count_launch();
+// `kernel` (GEMM launchers): remembered per host thread for tbik_last_kernel().
+void count_launch(const char* kernel = nullptr);
 
 // ---- cross-process flags (NVLink peer memory) --------------------------------
 // Release / acquire at system scope: a flag store is ordered after this

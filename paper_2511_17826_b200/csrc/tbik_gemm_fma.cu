@@ -285,7 +285,7 @@ tbik_status launch_v2(const GemmView& v, const GemmOut& o, cudaStream_t s) {
                                               static_cast<const uint16_t*>(v.B), v.ldb, v.M, v.N, v.K, v.bk, v.kf,
                                               v.T, o.mode, o.out, o.ldo, o.unit_stride);
   TBIK_CUDA(cudaGetLastError());
-  count_launch();
+  count_launch("fma_tree_gemm_v2");
   return TBIK_OK;
 }
 
@@ -300,7 +300,7 @@ tbik_status launch_cfg(const GemmView& v, const GemmOut& o, cudaStream_t s) {
       static_cast<const TA*>(v.A), v.lda, static_cast<const TB*>(v.B), v.ldb, v.M, v.N, v.K, v.bk,
       v.kf, v.T, o.mode, o.out, o.ldo, o.unit_stride);
   TBIK_CUDA(cudaGetLastError());
-  count_launch();
+  count_launch("fma_tree_gemm_kernel");
   return TBIK_OK;
 }
 

@@ -564,7 +564,7 @@ tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaSt
   lc.numAttrs = 1;
   TBIK_CUDA(cudaLaunchKernelEx(&lc, kern, mW, mX, p));
   TBIK_CUDA(cudaGetLastError());
-  count_launch();
+  count_launch("tc_skinny_kernel");
   return TBIK_OK;
 }
 

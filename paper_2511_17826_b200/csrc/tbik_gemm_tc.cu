@@ -772,7 +772,8 @@ EncodeTiledFn get_encode_fn() {
 }
 
 tbik_status make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride_bytes,
-                        uint32_t box_inner, uint32_t box_outer) {
+                        uint32_t box_inner, uint32_t box_outer,
+                        CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return set_error(TBIK_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
@@ -780,7 +781,7 @@ tbik_status make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(TBIK_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
   return TBIK_OK;
@@ -823,6 +824,17 @@ int sm_count() {
 tbik_status tc_make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                            uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
   return make_map_2d(map, base, inner, outer, row_stride_bytes, box_inner, box_outer);
+}
+
+// 32-byte swizzle (16-column bf16 boxes): the MN-major B atoms of the 256x192 kernel.
+tbik_status tc_make_map_2d_sw32(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                                uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+  return make_map_2d(map, base, inner, outer, row_stride_bytes, box_inner, box_outer, CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+tbik_status tc_make_map_2d_sw64(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                                uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+  return make_map_2d(map, base, inner, outer, row_stride_bytes, box_inner, box_outer, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 tbik_status tc_make_map_out(CUtensorMap* map, float* base, uint64_t n, uint64_t m, uint64_t units,
@@ -896,10 +908,13 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   std::string why;
   if (!tc_supported(v, &why)) return set_error(TBIK_UNSUPPORTED, why);
   if (o.mode == OUT_GROUPS) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: GROUPS mode is FMA-only");
-  // 256 x 256 pair tiles (tbik_gemm_tc_w.cu) for plain FULL / UNITS launches.
-  if (!g_fused_ar && tc_use_pair(v) && tc_wide_supported(v, o) && tc_wide_wanted(v)) {
-    const tbik_status st = launch_tc_wide(v, o, s);
-    if (st != TBIK_UNSUPPORTED) return st;
+  // 256 x 256 / 256 x 192 pair tiles (tbik_gemm_tc_w*.cu) for plain FULL / UNITS launches.
+  if (!g_fused_ar && tc_use_pair(v) && tc_wide_supported(v, o)) {
+    const int wv = tc_wide_variant(v);
+    if (wv != 0) {
+      const tbik_status st = wv == 2 ? launch_tc_w192(v, o, s) : launch_tc_wide(v, o, s);
+      if (st != TBIK_UNSUPPORTED) return st;
+    }
   }
   // A rows staged per stage: the fewest that still cover every row of the pair
   // tile's leader CTA (knob tc_abox overrides, a pure scheduling knob).
@@ -1088,7 +1103,7 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   lc.attrs = attr;
   lc.numAttrs = 1;
   TBIK_CUDA(cudaLaunchKernelEx(&lc, kern, mA, mB, mC, p));
-  count_launch();
+  count_launch(ar_on ? "tc_tree_gemm_kernel (fused all-reduce)" : "tc_tree_gemm_kernel");
   return TBIK_OK;
 }
 

@@ -471,16 +471,17 @@ bool tc_wide_supported(const GemmView& v, const GemmOut& o) {
          (reinterpret_cast<uintptr_t>(o.out) & 15) == 0 && o.ldo % 4 == 0 && ustride % 4 == 0;
 }
 
-// Default: only where it measured faster than the 256 x 128 kernel -- long K
-// (>= 16384: the tile's tree-level traffic through shared memory is amortised over
-// many leaves), k_first > 1 (k_first == 1 puts two more levels in scratch) and
-// M >= 1024 (profiles/r02_wide_tiles.md: Qwen3-32B down_proj K=25600 N=5120
-// M=2048 530 vs 597 us; Llama down_proj K=14336 and every K=4096 shape slower).
-// Knob tc_wide forces it either way.
-bool tc_wide_wanted(const GemmView& v) {
+// Which pair-tile kernel a plain FULL / UNITS launch takes (measured,
+// profiles/r02_w192_tiles.md): 256 x 192 tiles from M >= 2048 whenever k_first > 1
+// (Llama down_proj M = 4096 +4 %, TP shards K = 7168 / 3584 / 1792 +6..14 %, Qwen3-32B
+// down_proj +30..40 %, K=5120 N=10240 +25 %); k_first == 1 (K = 4096: 16 groups, two
+// scratch levels) and M < 2048 (88 tiles or fewer on 74 CTA pairs at N = 4096) stay on
+// 256 x 128.  256 x 256 tiles are never faster than 256 x 192 and remain a schedule
+// option.  Knob tc_wide forces a variant (0 / 1 / 2).
+int tc_wide_variant(const GemmView& v) {
   const int64_t k = knob(KNOB_TC_WIDE, -1);
-  if (k >= 0) return k >= 1;
-  return v.M >= 1024 && v.K >= 16384 && v.kf > 1;
+  if (k >= 0 && k <= 2) return static_cast<int>(k);
+  return v.M >= 2048 && v.kf > 1 ? 2 : 0;
 }
 
 tbik_status launch_tc_wide(const GemmView& v, const GemmOut& o, cudaStream_t s) {
@@ -556,7 +557,7 @@ tbik_status launch_tc_wide(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   lc.attrs = attr;
   lc.numAttrs = 1;
   TBIK_CUDA(cudaLaunchKernelEx(&lc, kern, mA, mB, mC, p));
-  count_launch();
+  count_launch("tc_wide_tree_gemm_kernel");
   return TBIK_OK;
 }
 

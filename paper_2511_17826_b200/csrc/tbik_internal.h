@@ -99,7 +99,7 @@ enum Knob {
   KNOB_GROUP_FUSED,      // 0: no fused GEMM + all-reduce kernel
   KNOB_GROUP_OVERLAP,    // 0: no chunked GEMM / all-reduce overlap
   KNOB_AR_TWO_PHASE_BYTES,  // payload bytes from which the group all-reduce is two-phase
-  KNOB_TC_WIDE,          // 0/1: 256 x 256 pair tiles (tbik_gemm_tc_w.cu)
+  KNOB_TC_WIDE,          // 0: 256 x 128, 1: 256 x 256 (tbik_gemm_tc_w.cu), 2: 256 x 192 (tbik_gemm_tc_w192.cu)
   KNOB_TC_WIDE_TAIL,     // 0: no 256 x 128 half items in the wide kernel's last wave
   KNOB_COUNT
 };
@@ -127,8 +127,11 @@ tbik_status launch_tc_skinny(const GemmView& v, float* C, int64_t ldc, cudaStrea
 // 256 x 256 pair-tile variant of launch_tc_gemm (tbik_gemm_tc_w.cu): FULL / UNITS
 // modes without epilogues; same bits as the 256 x 128 kernel.
 bool tc_wide_supported(const GemmView& v, const GemmOut& o);
-bool tc_wide_wanted(const GemmView& v);
+// 0: the 256 x 128 kernel, 1: 256 x 256 tiles (tbik_gemm_tc_w.cu), 2: 256 x 192 tiles
+// (tbik_gemm_tc_w192.cu); knob tc_wide overrides.
+int tc_wide_variant(const GemmView& v);
 tbik_status launch_tc_wide(const GemmView& v, const GemmOut& o, cudaStream_t s);
+tbik_status launch_tc_w192(const GemmView& v, const GemmOut& o, cudaStream_t s);
 
 // K-split factor run_tree_gemm uses for the tcgen05 leaf (1 = one FULL launch).
 int64_t tc_split_units(const GemmView& v);

@@ -436,15 +436,17 @@ def test_tc_deep_and_acc_variants(tb, cuda, M, K, N):
         assert torch.equal(want.view(torch.int32), got.view(torch.int32)), knobs
 
 
-# 256 x 256 pair tiles (N = 256 MMAs, tbik_gemm_tc_w.cu) vs the 256 x 128 kernel:
-# the tile shape, the MMA's N, the half-item tail and the shared-memory / scratch
-# level placement are schedule choices -- the same bits
+# 256 x 256 (N = 256 MMAs, tbik_gemm_tc_w.cu) and 256 x 192 pair tiles (N = 192 / 96
+# MMAs, 64B / 32B-swizzled B atoms, tbik_gemm_tc_w192.cu) vs the 256 x 128 kernel: the
+# tile shape, the MMA's N, the half-item tail, the operand layouts and the TMEM /
+# shared-memory / scratch level placement are schedule choices -- the same bits
 @pytest.mark.parametrize("M,K,N,bk,kf,knobs", [
     (512, 14336, 512, 256, 0, {}), (1024, 4096, 1024, 256, 0, {}), (300, 2048, 200, 256, 0, {}),
     (777, 3000, 520, 256, 0, {}), (1024, 14336, 1024, 256, 0, {"tc_units": 2}),
     (1024, 4096, 2304, 256, 4, {}), (2048, 1792, 1024, 256, 0, {}), (1536, 8192, 1280, 128, 0, {}),
     (4096, 14336, 4096, 256, 0, {}), (4096, 14336, 4096, 256, 0, {"tc_wide_tail": 0}),
-    (2048, 25600, 5120, 128, 0, {})])
+    (2048, 25600, 5120, 128, 0, {}), (1000, 4096, 4000, 256, 0, {}), (2304, 3584, 4096, 256, 7, {}),
+    (4096, 4096, 4096, 256, 0, {})])
 def test_wide_tiles_bit_identical(tb, cuda, M, K, N, bk, kf, knobs):
     g = torch.Generator(device=cuda).manual_seed(M + K + N)
     x = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
@@ -452,6 +454,9 @@ def test_wide_tiles_bit_identical(tb, cuda, M, K, N, bk, kf, knobs):
     cfg = tb.BlockConfig(64, bk, 128, kf)
     with tb.schedule(tc_wide=0, **{k: v for k, v in knobs.items() if k == "tc_units"}):
         want = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
-    with tb.schedule(tc_wide=1, **knobs):
-        got = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
-    assert torch.equal(want.view(torch.int32), got.view(torch.int32)), (M, K, N, knobs)
+        assert tb.last_kernel() in ("tc_tree_gemm_kernel", "tc_skinny_kernel")
+    for wv, name in ((1, "tc_wide_tree_gemm_kernel"), (2, "tc_w192_tree_gemm_kernel")):
+        with tb.schedule(tc_wide=wv, **knobs):
+            got = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+            assert tb.last_kernel() == name
+        assert torch.equal(want.view(torch.int32), got.view(torch.int32)), (M, K, N, knobs, name)

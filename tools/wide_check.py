@@ -47,6 +47,8 @@ def check():
         (1024, 6144, 768, 320, 0, {}),           # block_k = 320
         (640, 4096, 2304, 256, 4, {}),           # explicit k_first
         (2048, 25600, 5120, 128, 0, {}),         # Qwen3-32B down_proj
+        (1000, 4096, 4000, 256, 0, {}),          # N not a multiple of 192 / 96
+        (2048, 14336, 4096, 256, 0, {"tc_units": 2}),
     ]
     ok = True
     for M, K, N, bk, kf, knobs in cases:
@@ -54,21 +56,25 @@ def check():
         w = torch.randn(K, N, device="cuda", generator=g).to(torch.bfloat16)
         cfg = tb.BlockConfig(64, bk, 128, kf)
         ref = run(x, w, cfg, {"tc_wide": 0, **{k: v for k, v in knobs.items() if k == "tc_units"}})
-        y = run(x, w, cfg, {"tc_wide": 1, **knobs})
-        same = torch.equal(ref.view(torch.int32), y.view(torch.int32))
-        ok &= same
-        nbad = int((ref.view(torch.int32) != y.view(torch.int32)).sum())
-        print(f"M={M} K={K} N={N} bk={bk} kf={kf} {knobs}: {'bit-identical' if same else f'DIFFER ({nbad})'}",
-              flush=True)
+        res = []
+        for wv in (1, 2):
+            y = run(x, w, cfg, {"tc_wide": wv, **knobs})
+            same = torch.equal(ref.view(torch.int32), y.view(torch.int32))
+            ok &= same
+            nbad = int((ref.view(torch.int32) != y.view(torch.int32)).sum())
+            res.append(f"w{256 if wv == 1 else 192} {'bit-identical' if same else f'DIFFER ({nbad})'}")
+        print(f"M={M} K={K} N={N} bk={bk} kf={kf} {knobs}: {' | '.join(res)}", flush=True)
     print("ALL BIT-IDENTICAL" if ok else "MISMATCH", flush=True)
     return ok
 
 
-SHAPES = [(4096, 14336, 4096), (2048, 14336, 4096), (1024, 14336, 4096), (4096, 4096, 4096), (2048, 4096, 4096),
-          (4096, 4096, 28672), (4096, 1792, 4096), (1024, 25600, 5120), (2048, 25600, 5120), (4096, 25600, 5120),
-          (4096, 5120, 10240)]
-VARIANTS = [("narrow", {"tc_wide": 0}), ("wide", {"tc_wide": 1}), ("wide_notail", {"tc_wide": 1, "tc_wide_tail": 0}),
-            ("wide_gm4", {"tc_wide": 1, "tc_group_m": 4})]
+SHAPES = [(4096, 14336, 4096), (2048, 14336, 4096), (1024, 14336, 4096), (512, 14336, 4096),
+          (4096, 7168, 4096), (4096, 3584, 4096), (4096, 1792, 4096), (1024, 1792, 4096),
+          (4096, 4096, 4096), (2048, 4096, 4096), (4096, 4096, 28672), (1024, 4096, 6144),
+          (1024, 25600, 5120), (2048, 25600, 5120), (4096, 25600, 5120), (4096, 5120, 10240), (2048, 3200, 5120)]
+VARIANTS = [("narrow", {"tc_wide": 0}), ("w256", {"tc_wide": 1}), ("w192", {"tc_wide": 2}),
+            ("w192_notail", {"tc_wide": 2, "tc_wide_tail": 0}), ("w192_gm4", {"tc_wide": 2, "tc_group_m": 4}),
+            ("w192_gm16", {"tc_wide": 2, "tc_group_m": 16})]
 
 
 def timing(shapes):
