@@ -472,16 +472,16 @@ bool tc_wide_supported(const GemmView& v, const GemmOut& o) {
 }
 
 // Which pair-tile kernel a plain FULL / UNITS launch takes (measured,
-// profiles/r02_w192_tiles.md): 256 x 192 tiles from M >= 2048 whenever k_first > 1
-// (Llama down_proj M = 4096 +4 %, TP shards K = 7168 / 3584 / 1792 +6..14 %, Qwen3-32B
-// down_proj +30..40 %, K=5120 N=10240 +25 %); k_first == 1 (K = 4096: 16 groups, two
-// scratch levels) and M < 2048 (88 tiles or fewer on 74 CTA pairs at N = 4096) stay on
-// 256 x 128.  256 x 256 tiles are never faster than 256 x 192 and remain a schedule
-// option.  Knob tc_wide forces a variant (0 / 1 / 2).
+// profiles/r02_w192_tiles.md): 256 x 192 tiles from M >= 2048 -- Llama down_proj
+// M = 4096 +7 %, TP shards K = 7168 / 3584 / 1792 +3..14 %, k_first = 1 shapes
+// (K = 4096) +4..12 %, Qwen3-32B down_proj +30..46 %; below M = 2048 (88 tiles or fewer
+// on 74 CTA pairs at N = 4096) the 256 x 128 kernel with its K-split units wins.
+// 256 x 256 tiles are never faster than 256 x 192 and remain a schedule option.  Knob
+// tc_wide forces a variant (0 / 1 / 2).
 int tc_wide_variant(const GemmView& v) {
   const int64_t k = knob(KNOB_TC_WIDE, -1);
   if (k >= 0 && k <= 2) return static_cast<int>(k);
-  return v.M >= 2048 && v.kf > 1 ? 2 : 0;
+  return v.M >= 2048 ? 2 : 0;
 }
 
 tbik_status launch_tc_wide(const GemmView& v, const GemmOut& o, cudaStream_t s) {

@@ -59,7 +59,8 @@ constexpr int BM = 128;      // rows per CTA (the pair covers 256)
 constexpr int BNT = 192;     // columns per full tile (MMA N)
 constexpr int HN = 96;       // columns per merge thread / per half item
 constexpr int KSTAGE = 64;
-constexpr int NST = 6;
+// Stages: 6, or 5 when a second tree level is kept on chip (RL below).
+constexpr int nst(bool rl) { return rl ? 5 : 6; }
 constexpr int A_BYTES = BM * KSTAGE * 2;    // 16 KB
 // B atoms: full tiles stage this CTA's 96 columns as three 32-column 64B-swizzle atoms
 // (4 KB each), half items its 48 columns as three 16-column 32B-swizzle atoms (2 KB).
@@ -75,9 +76,11 @@ constexpr int LVL_WARP_BYTES = 32 * SCOLS * 4;  // 4 KB = one 32 x 32 f32 output
 constexpr int GROUP_M = 8;
 constexpr uint32_t IDESC_FULL = umma_idesc_bf16(256, BNT, /*a_mn_major=*/0, /*b_mn_major=*/1);
 constexpr uint32_t IDESC_HALF = umma_idesc_bf16(256, HN, 0, 1);
-constexpr size_t SMEM_BYTES =
-    1024 + static_cast<size_t>(NST) * (A_BYTES + B_BYTES) + static_cast<size_t>(MERGE_WARPS) * LVL_WARP_BYTES + 256;
-static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+constexpr size_t smem_bytes(bool rl) {
+  return 1024 + static_cast<size_t>(nst(rl)) * (A_BYTES + B_BYTES) +
+         static_cast<size_t>(MERGE_WARPS) * LVL_WARP_BYTES * (rl ? 2 : 1) + 256;
+}
+static_assert(smem_bytes(false) <= 232448 && smem_bytes(true) <= 232448, "shared memory budget");
 static_assert(2 * BNT + 2 * TCOLS == 512, "TMEM budget");
 
 struct W3Params {
@@ -155,6 +158,7 @@ __device__ __forceinline__ float4 ld_last(const float* p, uint64_t pol) {
   return v;
 }
 
+template <int NST>
 __device__ __forceinline__ void ring_next(int& stage, uint32_t& phase) {
   if (++stage == NST) {
     stage = 0;
@@ -195,17 +199,22 @@ __device__ __forceinline__ void emit_parked_box(uint8_t* stg, uint32_t lvl_t, in
   stage_and_store_box(stg, v, tmC, col + c * 32, row0, unit, lane);
 }
 
-template <bool KF1>
+// RL: the level above the TMEM level lives on chip too -- 64 of a thread's columns in
+// registers, 32 in a second 4 KB shared-memory slab per warp (5 stages then, and the
+// accumulator drained one 32-column chunk at a time to make register room).
+template <bool KF1, bool RL>
 __global__ void __launch_bounds__(NTHREADS, 1)
     tc_w192_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmC,
                              const W3Params p) {
+  constexpr int NST = nst(RL);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + NST * A_BYTES;
   uint8_t* sLvl = sB + NST * B_BYTES;  // per merge warp: a third of the TMEM level / output staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(sLvl + MERGE_WARPS * LVL_WARP_BYTES);
+  uint8_t* sLvl2 = sLvl + MERGE_WARPS * LVL_WARP_BYTES;  // RL: a third of the register level
+  uint64_t* full = reinterpret_cast<uint64_t*>(sLvl2 + (RL ? MERGE_WARPS * LVL_WARP_BYTES : 0));
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
@@ -272,7 +281,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               tma_load_2d_2sm(sA + stage * A_BYTES, &tmA, fb, k, am);
               for (int a = 0; a < 3; ++a)
                 tma_load_2d_2sm(sB + stage * B_BYTES + a * atom_bytes, mb, fb, bn + a * atom, k);
-              ring_next(stage, phase);
+              ring_next<NST>(stage, phase);
             }
           }
         }
@@ -320,7 +329,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               umma_commit_2cta(&empty[stage], 0x3);
             }
             __syncwarp();
-            ring_next(stage, phase);
+            ring_next<NST>(stage, phase);
           }
           if (elect_one()) umma_commit_2cta(&tfull[buf], static_cast<uint16_t>(0x3u << leader_rank));
           __syncwarp();
@@ -339,7 +348,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t lvl_t = tmem_base + lane_off + 2 * BNT + j * TCOLS;  // TMEM part of the TMEM level
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), leader_rank);
     constexpr int TL = KF1 ? 2 : 1;  // the TMEM (+ shared-memory third) tree level
-    constexpr int FS = TL + 1;       // first scratch level
+    constexpr int RLV = RL ? TL + 1 : 0;  // the register (+ shared-memory third) level
+    constexpr int FS = RL ? TL + 2 : TL + 1;  // first scratch level
     float* scratch_base =
         p.levels >= FS ? p.scratch +
                              static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - FS + 1) * (BM * BNT) +
@@ -348,6 +358,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // shared-memory third of the TMEM level: [8 float4 columns][32 lanes][float4]; after
     // the tile's carry, one 128B-swizzled 32 x 32 output box
     uint8_t* lvl_s = sLvl + (warp - 4) * LVL_WARP_BYTES;
+    uint8_t* lvl2_s = sLvl2 + (warp - 4) * LVL_WARP_BYTES;
+    float l2r[RL ? TCOLS : 1];
     const uint64_t pol_last = l2_policy_evict_last();
     const uint64_t pol_first = l2_policy_evict_first();
     float g[HN];
@@ -384,24 +396,47 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const bool odd = KF1 && p.levels >= 1 && (groups_done & 1u);
         const bool first = KF1 || t_in_group == 0;
         {
-          // all three 32-column chunks in flight, one wait, then the accumulator goes back
+          // all three 32-column chunks in flight, one wait, then the accumulator goes
+          // back (RL: one chunk at a time -- the register level needs the room)
+          constexpr int NR = RL ? 1 : HN / 32;
           uint32_t r[HN / 32][32];
 #pragma unroll
-          for (int c = 0; c < HN / 32; ++c) tmem_ld32r(acc + c * 32, r[c]);
+          for (int c = 0; c < HN / 32; ++c) {
+            if (c % NR == 0) {
 #pragma unroll
-          for (int c = 0; c < HN / 32; ++c) tmem_wait_ld_dep(r[c]);
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if (leader)
-              mbar_arrive(&tempty[buf]);
-            else
-              mbar_arrive_cluster(tempty_leader0 + buf * 8);
+              for (int d = 0; d < NR; ++d) tmem_ld32r(acc + (c + d) * 32, r[c + d]);
+#pragma unroll
+              for (int d = 0; d < NR; ++d) tmem_wait_ld_dep(r[c + d]);
+            }
+            if (c == HN / 32 - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {
+                if (leader)
+                  mbar_arrive(&tempty[buf]);
+                else
+                  mbar_arrive_cluster(tempty_leader0 + buf * 8);
+              }
+            }
+            if (RL) {  // fold this chunk now: its registers are reused by the next
+              if (odd) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  g[c * 32 + i] = __fadd_rn(__fadd_rn(0.0f, __uint_as_float(r[c][i])), g[c * 32 + i]);
+              } else if (first) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(0.0f, __uint_as_float(r[c][i]));
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], __uint_as_float(r[c][i]));
+              }
+            }
           }
           // level 0: g = ((0 + P_0) + P_1) + ... + P_{kf-1}   (matmul.cpp:100-125); for
           // k_first == 1 an odd group merges with its even sibling kept in g (level 1
           // in registers): g = (0 + P) + g  (matmul.cpp:107-123, new + old)
-          if (odd) {
+          if (RL) {
+          } else if (odd) {
 #pragma unroll
             for (int c = 0; c < HN / 32; ++c)
 #pragma unroll
@@ -456,18 +491,34 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 g[TCOLS + i + 2] = __fadd_rn(g[TCOLS + i + 2], x.z);
                 g[TCOLS + i + 3] = __fadd_rn(g[TCOLS + i + 3], x.w);
               }
+            } else if (RL && level == RLV) {
+#pragma unroll
+              for (int i = 0; i < TCOLS; ++i) g[i] = __fadd_rn(g[i], l2r[i]);
+#pragma unroll
+              for (int i = 0; i < SCOLS; i += 4) {
+                const float4 x = *reinterpret_cast<const float4*>(lvl2_s + ((i / 4) * 32 + lane) * 16);
+                g[TCOLS + i] = __fadd_rn(g[TCOLS + i], x.x);
+                g[TCOLS + i + 1] = __fadd_rn(g[TCOLS + i + 1], x.y);
+                g[TCOLS + i + 2] = __fadd_rn(g[TCOLS + i + 2], x.z);
+                g[TCOLS + i + 3] = __fadd_rn(g[TCOLS + i + 3], x.w);
+              }
             } else {
               // all 24 loads in flight at once: one L2 round trip per level, not six
               const float* sp = scratch_base + static_cast<size_t>(level - FS) * (BM * BNT);
-              float4 x[HN / 4];
+              constexpr int NB = RL ? 2 : 1;  // RL: two batches (register room)
 #pragma unroll
-              for (int u = 0; u < HN / 4; ++u) x[u] = ld_last(sp + 4 * u * BM, pol_first);
+              for (int b = 0; b < NB; ++b) {
+                float4 x[HN / 4 / NB];
 #pragma unroll
-              for (int u = 0; u < HN / 4; ++u) {
-                g[4 * u] = __fadd_rn(g[4 * u], x[u].x);
-                g[4 * u + 1] = __fadd_rn(g[4 * u + 1], x[u].y);
-                g[4 * u + 2] = __fadd_rn(g[4 * u + 2], x[u].z);
-                g[4 * u + 3] = __fadd_rn(g[4 * u + 3], x[u].w);
+                for (int u = 0; u < HN / 4 / NB; ++u) x[u] = ld_last(sp + 4 * (b * HN / 4 / NB + u) * BM, pol_first);
+#pragma unroll
+                for (int u = 0; u < HN / 4 / NB; ++u) {
+                  const int c = 4 * (b * HN / 4 / NB + u);
+                  g[c] = __fadd_rn(g[c], x[u].x);
+                  g[c + 1] = __fadd_rn(g[c + 1], x[u].y);
+                  g[c + 2] = __fadd_rn(g[c + 2], x[u].z);
+                  g[c + 3] = __fadd_rn(g[c + 3], x[u].w);
+                }
               }
             }
             c_bits >>= 1;
@@ -489,6 +540,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 *reinterpret_cast<float4*>(lvl_s + ((i / 4) * 32 + lane) * 16) =
                     make_float4(g[TCOLS + i], g[TCOLS + i + 1], g[TCOLS + i + 2], g[TCOLS + i + 3]);
               tmem_wait_st();
+            } else if (RL && level == RLV) {
+#pragma unroll
+              for (int i = 0; i < TCOLS; ++i) l2r[i] = g[i];
+#pragma unroll
+              for (int i = 0; i < SCOLS; i += 4)
+                *reinterpret_cast<float4*>(lvl2_s + ((i / 4) * 32 + lane) * 16) =
+                    make_float4(g[TCOLS + i], g[TCOLS + i + 1], g[TCOLS + i + 2], g[TCOLS + i + 3]);
             } else {
               float* sp = scratch_base + static_cast<size_t>(level - FS) * (BM * BNT);
 #pragma unroll
@@ -556,7 +614,7 @@ int sm_count_dev() {
 // setmaxnreg only redistributes the registers the launch allocated: the merge
 // warpgroups' 232 need exactly 168 per thread at launch (384 x 168 = 128 x 40 +
 // 256 x 232).  Checked once per (device, kernel); otherwise this path is off.
-bool regs_ok(int dev, const void* kern) {
+bool regs_ok(int dev, const void* kern, size_t smem) {
   static std::mutex mu;
   static std::map<std::pair<int, const void*>, bool> ok;
   std::lock_guard<std::mutex> lk(mu);
@@ -567,7 +625,7 @@ bool regs_ok(int dev, const void* kern) {
   if (!good) cudaGetLastError();
   ok[{dev, kern}] = good;
   if (good) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM_BYTES));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
   }
   return good;
@@ -579,10 +637,13 @@ tbik_status launch_tc_w192(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   if (!tc_wide_supported(v, o)) return set_error(TBIK_UNSUPPORTED, "tc w192: unsupported launch");
   const int kf1 = v.kf == 1;
   using Kern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const W3Params);
-  const Kern kern = kf1 ? tc_w192_tree_gemm_kernel<true> : tc_w192_tree_gemm_kernel<false>;
+  const bool rl = knob(KNOB_TC_W192_RL, 1) != 0;
+  const Kern kern = rl ? (kf1 ? tc_w192_tree_gemm_kernel<true, true> : tc_w192_tree_gemm_kernel<false, true>)
+                       : (kf1 ? tc_w192_tree_gemm_kernel<true, false> : tc_w192_tree_gemm_kernel<false, false>);
+  const size_t smem = smem_bytes(rl);
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!regs_ok(dev, reinterpret_cast<const void*>(kern)))
+  if (!regs_ok(dev, reinterpret_cast<const void*>(kern), smem))
     return set_error(TBIK_UNSUPPORTED, "tc w192: kernel register count is not 168");
   W3Params p{};
   p.M = static_cast<int>(v.M);
@@ -620,7 +681,7 @@ tbik_status launch_tc_w192(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   }
   p.items = p.full_items + 2 * (tiles - p.full_items);
   const long long npairs = p.items < slots ? p.items : slots;
-  const int FS = kf1 ? 3 : 2;
+  const int FS = (kf1 ? 3 : 2) + (rl ? 1 : 0);
   if (p.levels >= FS) {
     const size_t n = static_cast<size_t>(2 * npairs) * (p.levels - FS + 1) * BM * BNT;
     p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1, s));
@@ -640,7 +701,7 @@ tbik_status launch_tc_w192(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(static_cast<unsigned>(2 * npairs));
   lc.blockDim = dim3(NTHREADS);
-  lc.dynamicSmemBytes = SMEM_BYTES;
+  lc.dynamicSmemBytes = smem;
   lc.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -100,7 +100,8 @@ enum Knob {
   KNOB_GROUP_OVERLAP,    // 0: no chunked GEMM / all-reduce overlap
   KNOB_AR_TWO_PHASE_BYTES,  // payload bytes from which the group all-reduce is two-phase
   KNOB_TC_WIDE,          // 0: 256 x 128, 1: 256 x 256 (tbik_gemm_tc_w.cu), 2: 256 x 192 (tbik_gemm_tc_w192.cu)
-  KNOB_TC_WIDE_TAIL,     // 0: no 256 x 128 half items in the wide kernel's last wave
+  KNOB_TC_WIDE_TAIL,     // 0: no half items in the wide kernels' last wave
+  KNOB_TC_W192_RL,       // 0: 256 x 192 kernel without the register tree level (6 stages)
   KNOB_COUNT
 };
 int64_t knob(Knob k, int64_t dflt);

@@ -455,8 +455,9 @@ def test_wide_tiles_bit_identical(tb, cuda, M, K, N, bk, kf, knobs):
     with tb.schedule(tc_wide=0, **{k: v for k, v in knobs.items() if k == "tc_units"}):
         want = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
         assert tb.last_kernel() in ("tc_tree_gemm_kernel", "tc_skinny_kernel")
-    for wv, name in ((1, "tc_wide_tree_gemm_kernel"), (2, "tc_w192_tree_gemm_kernel")):
-        with tb.schedule(tc_wide=wv, **knobs):
+    for kv, name in (({"tc_wide": 1}, "tc_wide_tree_gemm_kernel"), ({"tc_wide": 2}, "tc_w192_tree_gemm_kernel"),
+                     ({"tc_wide": 2, "tc_w192_rl": 0}, "tc_w192_tree_gemm_kernel")):
+        with tb.schedule(**kv, **knobs):
             got = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
             assert tb.last_kernel() == name
-        assert torch.equal(want.view(torch.int32), got.view(torch.int32)), (M, K, N, knobs, name)
+        assert torch.equal(want.view(torch.int32), got.view(torch.int32)), (M, K, N, knobs, kv)

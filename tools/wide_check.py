@@ -57,12 +57,12 @@ def check():
         cfg = tb.BlockConfig(64, bk, 128, kf)
         ref = run(x, w, cfg, {"tc_wide": 0, **{k: v for k, v in knobs.items() if k == "tc_units"}})
         res = []
-        for wv in (1, 2):
-            y = run(x, w, cfg, {"tc_wide": wv, **knobs})
+        for name, kv in (("w256", {"tc_wide": 1}), ("w192", {"tc_wide": 2}), ("w192_norl", {"tc_wide": 2, "tc_w192_rl": 0})):
+            y = run(x, w, cfg, {**kv, **knobs})
             same = torch.equal(ref.view(torch.int32), y.view(torch.int32))
             ok &= same
             nbad = int((ref.view(torch.int32) != y.view(torch.int32)).sum())
-            res.append(f"w{256 if wv == 1 else 192} {'bit-identical' if same else f'DIFFER ({nbad})'}")
+            res.append(f"{name} {'bit-identical' if same else f'DIFFER ({nbad})'}")
         print(f"M={M} K={K} N={N} bk={bk} kf={kf} {knobs}: {' | '.join(res)}", flush=True)
     print("ALL BIT-IDENTICAL" if ok else "MISMATCH", flush=True)
     return ok
@@ -73,8 +73,8 @@ SHAPES = [(4096, 14336, 4096), (2048, 14336, 4096), (1024, 14336, 4096), (512, 1
           (4096, 4096, 4096), (2048, 4096, 4096), (4096, 4096, 28672), (1024, 4096, 6144),
           (1024, 25600, 5120), (2048, 25600, 5120), (4096, 25600, 5120), (4096, 5120, 10240), (2048, 3200, 5120)]
 VARIANTS = [("narrow", {"tc_wide": 0}), ("w256", {"tc_wide": 1}), ("w192", {"tc_wide": 2}),
-            ("w192_notail", {"tc_wide": 2, "tc_wide_tail": 0}), ("w192_gm4", {"tc_wide": 2, "tc_group_m": 4}),
-            ("w192_gm16", {"tc_wide": 2, "tc_group_m": 16})]
+            ("w192_norl", {"tc_wide": 2, "tc_w192_rl": 0}), ("w192_notail", {"tc_wide": 2, "tc_wide_tail": 0}),
+            ("w192_gm4", {"tc_wide": 2, "tc_group_m": 4})]
 
 
 def timing(shapes):
