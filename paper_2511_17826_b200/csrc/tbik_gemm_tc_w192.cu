@@ -60,7 +60,7 @@ constexpr int BNT = 192;     // columns per full tile (MMA N)
 constexpr int HN = 96;       // columns per merge thread / per half item
 constexpr int KSTAGE = 64;
 // Stages: 6, or 5 when a second tree level is kept on chip (RL below).
-constexpr int nst(bool rl) { return rl ? 5 : 6; }
+constexpr int nst(bool rl) { return 6; }
 constexpr int A_BYTES = BM * KSTAGE * 2;    // 16 KB
 // B atoms: full tiles stage this CTA's 96 columns as three 32-column 64B-swizzle atoms
 // (4 KB each), half items its 48 columns as three 16-column 32B-swizzle atoms (2 KB).
@@ -73,12 +73,15 @@ constexpr int NTHREADS = 128 + 32 * MERGE_WARPS;
 constexpr int TCOLS = 64;                   // TMEM columns of the TMEM level per thread
 constexpr int SCOLS = HN - TCOLS;           // shared-memory columns of it (32)
 constexpr int LVL_WARP_BYTES = 32 * SCOLS * 4;  // 4 KB = one 32 x 32 f32 output box
+constexpr int RCOLS = 72;                   // register columns of the register level per thread
+constexpr int S2COLS = HN - RCOLS;          // its shared-memory columns (24)
+constexpr int LVL2_WARP_BYTES = 32 * S2COLS * 4;  // 3 KB
 constexpr int GROUP_M = 8;
 constexpr uint32_t IDESC_FULL = umma_idesc_bf16(256, BNT, /*a_mn_major=*/0, /*b_mn_major=*/1);
 constexpr uint32_t IDESC_HALF = umma_idesc_bf16(256, HN, 0, 1);
 constexpr size_t smem_bytes(bool rl) {
   return 1024 + static_cast<size_t>(nst(rl)) * (A_BYTES + B_BYTES) +
-         static_cast<size_t>(MERGE_WARPS) * LVL_WARP_BYTES * (rl ? 2 : 1) + 256;
+         static_cast<size_t>(MERGE_WARPS) * (LVL_WARP_BYTES + (rl ? LVL2_WARP_BYTES : 0)) + 256;
 }
 static_assert(smem_bytes(false) <= 232448 && smem_bytes(true) <= 232448, "shared memory budget");
 static_assert(2 * BNT + 2 * TCOLS == 512, "TMEM budget");
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t* sB = smem + NST * A_BYTES;
   uint8_t* sLvl = sB + NST * B_BYTES;  // per merge warp: a third of the TMEM level / output staging
   uint8_t* sLvl2 = sLvl + MERGE_WARPS * LVL_WARP_BYTES;  // RL: a third of the register level
-  uint64_t* full = reinterpret_cast<uint64_t*>(sLvl2 + (RL ? MERGE_WARPS * LVL_WARP_BYTES : 0));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sLvl2 + (RL ? MERGE_WARPS * LVL2_WARP_BYTES : 0));
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
@@ -358,8 +361,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // shared-memory third of the TMEM level: [8 float4 columns][32 lanes][float4]; after
     // the tile's carry, one 128B-swizzled 32 x 32 output box
     uint8_t* lvl_s = sLvl + (warp - 4) * LVL_WARP_BYTES;
-    uint8_t* lvl2_s = sLvl2 + (warp - 4) * LVL_WARP_BYTES;
-    float l2r[RL ? TCOLS : 1];
+    uint8_t* lvl2_s = sLvl2 + (warp - 4) * LVL2_WARP_BYTES;
+    float l2r[RL ? RCOLS : 1];
     const uint64_t pol_last = l2_policy_evict_last();
     const uint64_t pol_first = l2_policy_evict_first();
     float g[HN];
@@ -493,14 +496,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
             } else if (RL && level == RLV) {
 #pragma unroll
-              for (int i = 0; i < TCOLS; ++i) g[i] = __fadd_rn(g[i], l2r[i]);
+              for (int i = 0; i < RCOLS; ++i) g[i] = __fadd_rn(g[i], l2r[i]);
 #pragma unroll
-              for (int i = 0; i < SCOLS; i += 4) {
+              for (int i = 0; i < S2COLS; i += 4) {
                 const float4 x = *reinterpret_cast<const float4*>(lvl2_s + ((i / 4) * 32 + lane) * 16);
-                g[TCOLS + i] = __fadd_rn(g[TCOLS + i], x.x);
-                g[TCOLS + i + 1] = __fadd_rn(g[TCOLS + i + 1], x.y);
-                g[TCOLS + i + 2] = __fadd_rn(g[TCOLS + i + 2], x.z);
-                g[TCOLS + i + 3] = __fadd_rn(g[TCOLS + i + 3], x.w);
+                g[RCOLS + i] = __fadd_rn(g[RCOLS + i], x.x);
+                g[RCOLS + i + 1] = __fadd_rn(g[RCOLS + i + 1], x.y);
+                g[RCOLS + i + 2] = __fadd_rn(g[RCOLS + i + 2], x.z);
+                g[RCOLS + i + 3] = __fadd_rn(g[RCOLS + i + 3], x.w);
               }
             } else {
               // all 24 loads in flight at once: one L2 round trip per level, not six
@@ -542,11 +545,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               tmem_wait_st();
             } else if (RL && level == RLV) {
 #pragma unroll
-              for (int i = 0; i < TCOLS; ++i) l2r[i] = g[i];
+              for (int i = 0; i < RCOLS; ++i) l2r[i] = g[i];
 #pragma unroll
-              for (int i = 0; i < SCOLS; i += 4)
+              for (int i = 0; i < S2COLS; i += 4)
                 *reinterpret_cast<float4*>(lvl2_s + ((i / 4) * 32 + lane) * 16) =
-                    make_float4(g[TCOLS + i], g[TCOLS + i + 1], g[TCOLS + i + 2], g[TCOLS + i + 3]);
+                    make_float4(g[RCOLS + i], g[RCOLS + i + 1], g[RCOLS + i + 2], g[RCOLS + i + 3]);
             } else {
               float* sp = scratch_base + static_cast<size_t>(level - FS) * (BM * BNT);
 #pragma unroll
