@@ -205,6 +205,15 @@ int64_t tc_split_units(const GemmView& v) {
   // vectorised combine): K=14336 M=768 / 2048 +9 % / +3 %, K=4096 M=256 / 768
   // +31 % / +5 % split; no split where the efficiency does not move (M=512, 1024,
   // 1536) or K is short (K=4096 M=2048: -15 % split).
+  {  // 256 x 192 tiles choose their own split (tbik_gemm_tc_w.cu)
+    const int64_t w = tc_w192_units(v);
+    if (w > 0 && tc_wide_variant(v) == 2) {
+      int64_t units = w <= v.L && v.T / w >= 8 ? w : 1;
+      const int64_t u = knob(KNOB_TC_UNITS, 0);
+      if (u >= 1 && u <= v.L && (u & (u - 1)) == 0) units = u;
+      return units;
+    }
+  }
   const int64_t slots = tc_parallel_slots(v);
   auto eff = [&](int64_t items) {
     const int64_t waves = (items + slots - 1) / slots;

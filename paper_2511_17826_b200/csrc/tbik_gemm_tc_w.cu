@@ -471,17 +471,27 @@ bool tc_wide_supported(const GemmView& v, const GemmOut& o) {
          (reinterpret_cast<uintptr_t>(o.out) & 15) == 0 && o.ldo % 4 == 0 && ustride % 4 == 0;
 }
 
-// Which pair-tile kernel a plain FULL / UNITS launch takes (measured,
-// profiles/r02_w192_tiles.md): 256 x 192 tiles from M >= 2048 -- Llama down_proj
-// M = 4096 +7 %, TP shards K = 7168 / 3584 / 1792 +3..14 %, k_first = 1 shapes
-// (K = 4096) +4..12 %, Qwen3-32B down_proj +30..46 %; below M = 2048 (88 tiles or fewer
-// on 74 CTA pairs at N = 4096) the 256 x 128 kernel with its K-split units wins.
-// 256 x 256 tiles are never faster than 256 x 192 and remain a schedule option.  Knob
-// tc_wide forces a variant (0 / 1 / 2).
+// Which pair-tile kernel a plain FULL / UNITS launch takes, and with how many K-split
+// units (measured, profiles/r02_w192_tiles.md): 256 x 192 tiles whenever there are
+// enough of them for the 74 CTA pairs -- >= 120 tiles (M=1024 N>=6144, M>=1536 N=4096:
+// Llama down_proj M=4096 +10 %, M=1536 +15 %, lm_head M=1024 +8 %, TP shards +3..14 %,
+// k_first = 1 shapes +4..12 %), or >= 80 tiles with K >= 8192 as two K units (M=1024:
+// down_proj +2 %, Qwen3-32B down_proj K=25600 +48 %); otherwise the 256 x 128 kernel
+// with its own split rule (M=1024 K=4096 N=4096: 41.5 vs 45.9 us).  256 x 256 tiles are
+// never faster than 256 x 192 and remain a schedule option.  Knob tc_wide forces a
+// variant (0 / 1 / 2), tc_units the split.
+int64_t tc_w192_units(const GemmView& v) {
+  if (v.M <= 128) return 0;
+  const int64_t tiles = ((v.M + 255) / 256) * ((v.N + 191) / 192);
+  if (tiles >= 120) return 1;
+  if (tiles >= 80 && v.K >= 8192) return 2;
+  return 0;
+}
+
 int tc_wide_variant(const GemmView& v) {
   const int64_t k = knob(KNOB_TC_WIDE, -1);
   if (k >= 0 && k <= 2) return static_cast<int>(k);
-  return v.M >= 2048 ? 2 : 0;
+  return tc_w192_units(v) > 0 ? 2 : 0;
 }
 
 tbik_status launch_tc_wide(const GemmView& v, const GemmOut& o, cudaStream_t s) {

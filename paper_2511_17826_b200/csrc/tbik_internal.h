@@ -131,6 +131,9 @@ bool tc_wide_supported(const GemmView& v, const GemmOut& o);
 // 0: the 256 x 128 kernel, 1: 256 x 256 tiles (tbik_gemm_tc_w.cu), 2: 256 x 192 tiles
 // (tbik_gemm_tc_w192.cu); knob tc_wide overrides.
 int tc_wide_variant(const GemmView& v);
+// K-split units the 256 x 192 kernel wants for v by default (1 or 2), 0 when it is
+// not the default kernel for v.
+int64_t tc_w192_units(const GemmView& v);
 tbik_status launch_tc_wide(const GemmView& v, const GemmOut& o, cudaStream_t s);
 tbik_status launch_tc_w192(const GemmView& v, const GemmOut& o, cudaStream_t s);
 

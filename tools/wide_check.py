@@ -72,7 +72,9 @@ SHAPES = [(4096, 14336, 4096), (2048, 14336, 4096), (1024, 14336, 4096), (512, 1
           (4096, 7168, 4096), (4096, 3584, 4096), (4096, 1792, 4096), (1024, 1792, 4096),
           (4096, 4096, 4096), (2048, 4096, 4096), (4096, 4096, 28672), (1024, 4096, 6144),
           (1024, 25600, 5120), (2048, 25600, 5120), (4096, 25600, 5120), (4096, 5120, 10240), (2048, 3200, 5120)]
-VARIANTS = [("narrow", {"tc_wide": 0}), ("w256", {"tc_wide": 1}), ("w192", {"tc_wide": 2}),
+MID_VARIANTS = [("narrow", {"tc_wide": 0}), ("w192", {"tc_wide": 2}), ("w192_u1", {"tc_wide": 2, "tc_units": 1}),
+                ("w192_u2", {"tc_wide": 2, "tc_units": 2}), ("w192_u4", {"tc_wide": 2, "tc_units": 4})]
+VARIANTS = MID_VARIANTS if os.environ.get("MID") else [("narrow", {"tc_wide": 0}), ("w256", {"tc_wide": 1}), ("w192", {"tc_wide": 2}),
             ("w192_norl", {"tc_wide": 2, "tc_w192_rl": 0}), ("w192_notail", {"tc_wide": 2, "tc_wide_tail": 0}),
             ("w192_gm4", {"tc_wide": 2, "tc_group_m": 4})]
 
