@@ -102,7 +102,7 @@ TBIK_API tbik_status tbik_sync(void* stream);
  * arithmetic (every schedule is tested bit-identical).  Process-wide; the
  * library reads no environment variables.  Names: tc_pair, tc_abox, tc_group_m,
  * tc_units, tc_deep, tc_acc4, tc_skinny, sk_mt, sk_units, sk_leaf, sk_bn,
- * fma_v1, group_fused, group_overlap, ar_two_phase_bytes, tc_wide, tc_wide_tail, tc_w192_rl.  value < 0 unsets one
+ * fma_v1, group_fused, group_overlap, ar_two_phase_bytes, tc_wide, tc_wide_tail.  value < 0 unsets one
  * knob, name NULL unsets all; an unknown name is TBIK_BAD_ARGUMENT.  Every rank
  * of a group must use the same group_* / ar_* settings. */
 TBIK_API tbik_status tbik_set_schedule(const char* name, int64_t value);
@@ -110,7 +110,7 @@ TBIK_API tbik_status tbik_set_schedule(const char* name, int64_t value);
  * bench.py reports the delta over its timed region as gpu_launches. */
 TBIK_API uint64_t tbik_launch_count(void);
 /* Name of the last tree-GEMM kernel this host thread launched (tc_tree_gemm_kernel,
- * tc_w192_tree_gemm_kernel, tc_wide_tree_gemm_kernel, tc_skinny_kernel,
+ * tc_w192_tree_gemm_kernel, tc_skinny_kernel,
  * fma_tree_gemm_v2, ...); "" before the first.  Diagnostics: which schedule ran. */
 TBIK_API const char* tbik_last_kernel(void);
 /* Diagnostics: when TBIK_TC_STATS=1, the last tcgen05 GEMM launch records per-CTA

@@ -45,7 +45,7 @@ struct KnobInit {
 const char* const kKnobNames[KNOB_COUNT] = {
     "tc_pair",  "tc_abox", "tc_group_m", "tc_units",       "tc_deep",         "tc_acc4",
     "tc_skinny", "sk_mt",  "sk_units",   "sk_leaf",        "sk_bn",           "fma_v1",
-    "group_fused", "group_overlap", "ar_two_phase_bytes", "tc_wide", "tc_wide_tail", "tc_w192_rl"};
+    "group_fused", "group_overlap", "ar_two_phase_bytes", "tc_wide", "tc_wide_tail"};
 }  // namespace
 
 int64_t knob(Knob k, int64_t dflt) {
@@ -205,9 +205,9 @@ int64_t tc_split_units(const GemmView& v) {
   // vectorised combine): K=14336 M=768 / 2048 +9 % / +3 %, K=4096 M=256 / 768
   // +31 % / +5 % split; no split where the efficiency does not move (M=512, 1024,
   // 1536) or K is short (K=4096 M=2048: -15 % split).
-  {  // 256 x 192 tiles choose their own split (tbik_gemm_tc_w.cu)
+  {  // 256 x 192 tiles choose their own split (tbik_gemm_tc_w192.cu)
     const int64_t w = tc_w192_units(v);
-    if (w > 0 && tc_wide_variant(v) == 2) {
+    if (w > 0 && tc_wide_variant(v) != 0) {
       int64_t units = w <= v.L && v.T / w >= 8 ? w : 1;
       const int64_t u = knob(KNOB_TC_UNITS, 0);
       if (u >= 1 && u <= v.L && (u & (u - 1)) == 0) units = u;

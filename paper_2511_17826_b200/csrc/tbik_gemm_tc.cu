@@ -908,11 +908,10 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   std::string why;
   if (!tc_supported(v, &why)) return set_error(TBIK_UNSUPPORTED, why);
   if (o.mode == OUT_GROUPS) return set_error(TBIK_BAD_ARGUMENT, "tc gemm: GROUPS mode is FMA-only");
-  // 256 x 256 / 256 x 192 pair tiles (tbik_gemm_tc_w*.cu) for plain FULL / UNITS launches.
+  // 256 x 192 pair tiles (tbik_gemm_tc_w192.cu) for plain FULL / UNITS launches.
   if (!g_fused_ar && tc_use_pair(v) && tc_wide_supported(v, o)) {
-    const int wv = tc_wide_variant(v);
-    if (wv != 0) {
-      const tbik_status st = wv == 2 ? launch_tc_w192(v, o, s) : launch_tc_wide(v, o, s);
+    if (tc_wide_variant(v) != 0) {
+      const tbik_status st = launch_tc_w192(v, o, s);
       if (st != TBIK_UNSUPPORTED) return st;
     }
   }

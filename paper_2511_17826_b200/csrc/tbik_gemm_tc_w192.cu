@@ -12,16 +12,19 @@
 // for 128 x N x 64 MACs:
 //   N = 128 (tbik_gemm_tc.cu)   1.5 wavefronts per MMA cycle -> <= 67 % tensor-busy
 //   N = 192 (this kernel)       1.17                         -> <= 85 %
-//   N = 256 (tbik_gemm_tc_w.cu) 1.0                          -> <= 100 %, but two
+//   N = 256                     1.0                          -> <= 100 %, but two
 //                               accumulators fill TMEM and the tree levels then pay
-//                               for shared memory through the same port.
+//                               for shared memory through the same port (built and
+//                               removed: profiles/r02_wide_tiles.md).
 // At N = 192 two accumulators take 384 TMEM columns and the other 128 hold 2/3 of the
 // tree level that is touched every other group (level 1; level 2 when k_first == 1);
 // its last third (32 columns per thread) sits in shared memory -- a 4 KB slab per merge
 // warp that also stages the output boxes of the TMA stores once the tile's carry has
-// consumed the level.  Deeper levels (touched once per 4+ groups) live in L2-resident
-// scratch.  Shared memory: 6 stages of {A 16 KB (128B swizzle), B 12 KB (six 16-column
-// 32B-swizzle atoms)} = 2304 MMA cycles in flight.
+// consumed the level.  The next level lives in 72 registers per thread + a 3 KB slab
+// per warp (the accumulator is drained one 32-column chunk at a time to make room);
+// deeper levels (touched once per 8+ groups) in L2-resident scratch.  Shared memory:
+// 6 stages of {A 16 KB (128B swizzle), B 12 KB (three 32-column 64B-swizzle atoms; six
+// 16-column 32B atoms for half items)} = 2304 MMA cycles in flight, 230.7 KB in all.
 //
 // Warp roles (384 threads, one CTA per SM, setmaxnreg 40 / 232):
 //   warp 0      TMA producer (2SM TMA, completion on the leader's barrier)
@@ -59,8 +62,7 @@ constexpr int BM = 128;      // rows per CTA (the pair covers 256)
 constexpr int BNT = 192;     // columns per full tile (MMA N)
 constexpr int HN = 96;       // columns per merge thread / per half item
 constexpr int KSTAGE = 64;
-// Stages: 6, or 5 when a second tree level is kept on chip (RL below).
-constexpr int nst(bool rl) { return 6; }
+constexpr int NST = 6;
 constexpr int A_BYTES = BM * KSTAGE * 2;    // 16 KB
 // B atoms: full tiles stage this CTA's 96 columns as three 32-column 64B-swizzle atoms
 // (4 KB each), half items its 48 columns as three 16-column 32B-swizzle atoms (2 KB).
@@ -79,11 +81,9 @@ constexpr int LVL2_WARP_BYTES = 32 * S2COLS * 4;  // 3 KB
 constexpr int GROUP_M = 8;
 constexpr uint32_t IDESC_FULL = umma_idesc_bf16(256, BNT, /*a_mn_major=*/0, /*b_mn_major=*/1);
 constexpr uint32_t IDESC_HALF = umma_idesc_bf16(256, HN, 0, 1);
-constexpr size_t smem_bytes(bool rl) {
-  return 1024 + static_cast<size_t>(nst(rl)) * (A_BYTES + B_BYTES) +
-         static_cast<size_t>(MERGE_WARPS) * (LVL_WARP_BYTES + (rl ? LVL2_WARP_BYTES : 0)) + 256;
-}
-static_assert(smem_bytes(false) <= 232448 && smem_bytes(true) <= 232448, "shared memory budget");
+constexpr size_t SMEM_BYTES = 1024 + static_cast<size_t>(NST) * (A_BYTES + B_BYTES) +
+                              static_cast<size_t>(MERGE_WARPS) * (LVL_WARP_BYTES + LVL2_WARP_BYTES) + 256;
+static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 static_assert(2 * BNT + 2 * TCOLS == 512, "TMEM budget");
 
 struct W3Params {
@@ -161,7 +161,6 @@ __device__ __forceinline__ float4 ld_last(const float* p, uint64_t pol) {
   return v;
 }
 
-template <int NST>
 __device__ __forceinline__ void ring_next(int& stage, uint32_t& phase) {
   if (++stage == NST) {
     stage = 0;
@@ -202,22 +201,18 @@ __device__ __forceinline__ void emit_parked_box(uint8_t* stg, uint32_t lvl_t, in
   stage_and_store_box(stg, v, tmC, col + c * 32, row0, unit, lane);
 }
 
-// RL: the level above the TMEM level lives on chip too -- 64 of a thread's columns in
-// registers, 32 in a second 4 KB shared-memory slab per warp (5 stages then, and the
-// accumulator drained one 32-column chunk at a time to make register room).
-template <bool KF1, bool RL>
+template <bool KF1>
 __global__ void __launch_bounds__(NTHREADS, 1)
     tc_w192_tree_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmC,
                              const W3Params p) {
-  constexpr int NST = nst(RL);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + NST * A_BYTES;
   uint8_t* sLvl = sB + NST * B_BYTES;  // per merge warp: a third of the TMEM level / output staging
-  uint8_t* sLvl2 = sLvl + MERGE_WARPS * LVL_WARP_BYTES;  // RL: a third of the register level
-  uint64_t* full = reinterpret_cast<uint64_t*>(sLvl2 + (RL ? MERGE_WARPS * LVL2_WARP_BYTES : 0));
+  uint8_t* sLvl2 = sLvl + MERGE_WARPS * LVL_WARP_BYTES;  // per merge warp: a quarter of the register level
+  uint64_t* full = reinterpret_cast<uint64_t*>(sLvl2 + MERGE_WARPS * LVL2_WARP_BYTES);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
@@ -284,7 +279,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               tma_load_2d_2sm(sA + stage * A_BYTES, &tmA, fb, k, am);
               for (int a = 0; a < 3; ++a)
                 tma_load_2d_2sm(sB + stage * B_BYTES + a * atom_bytes, mb, fb, bn + a * atom, k);
-              ring_next<NST>(stage, phase);
+              ring_next(stage, phase);
             }
           }
         }
@@ -332,7 +327,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               umma_commit_2cta(&empty[stage], 0x3);
             }
             __syncwarp();
-            ring_next<NST>(stage, phase);
+            ring_next(stage, phase);
           }
           if (elect_one()) umma_commit_2cta(&tfull[buf], static_cast<uint16_t>(0x3u << leader_rank));
           __syncwarp();
@@ -351,8 +346,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t lvl_t = tmem_base + lane_off + 2 * BNT + j * TCOLS;  // TMEM part of the TMEM level
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), leader_rank);
     constexpr int TL = KF1 ? 2 : 1;  // the TMEM (+ shared-memory third) tree level
-    constexpr int RLV = RL ? TL + 1 : 0;  // the register (+ shared-memory third) level
-    constexpr int FS = RL ? TL + 2 : TL + 1;  // first scratch level
+    constexpr int RLV = TL + 1;      // the register (+ shared-memory quarter) level
+    constexpr int FS = TL + 2;       // first scratch level
     float* scratch_base =
         p.levels >= FS ? p.scratch +
                              static_cast<size_t>(blockIdx.x) * static_cast<size_t>(p.levels - FS + 1) * (BM * BNT) +
@@ -362,7 +357,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // the tile's carry, one 128B-swizzled 32 x 32 output box
     uint8_t* lvl_s = sLvl + (warp - 4) * LVL_WARP_BYTES;
     uint8_t* lvl2_s = sLvl2 + (warp - 4) * LVL2_WARP_BYTES;
-    float l2r[RL ? RCOLS : 1];
+    float l2r[RCOLS];
     const uint64_t pol_last = l2_policy_evict_last();
     const uint64_t pol_first = l2_policy_evict_first();
     float g[HN];
@@ -399,18 +394,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const bool odd = KF1 && p.levels >= 1 && (groups_done & 1u);
         const bool first = KF1 || t_in_group == 0;
         {
-          // all three 32-column chunks in flight, one wait, then the accumulator goes
-          // back (RL: one chunk at a time -- the register level needs the room)
-          constexpr int NR = RL ? 1 : HN / 32;
+          // one 32-column chunk at a time (the register level needs the room), each
+          // folded as it arrives; the accumulator goes back after the last load
           uint32_t r[HN / 32][32];
 #pragma unroll
           for (int c = 0; c < HN / 32; ++c) {
-            if (c % NR == 0) {
-#pragma unroll
-              for (int d = 0; d < NR; ++d) tmem_ld32r(acc + (c + d) * 32, r[c + d]);
-#pragma unroll
-              for (int d = 0; d < NR; ++d) tmem_wait_ld_dep(r[c + d]);
-            }
+            tmem_ld32r(acc + c * 32, r[c]);
+            tmem_wait_ld_dep(r[c]);
             if (c == HN / 32 - 1) {
               tc_fence_before();
               __syncwarp();
@@ -421,40 +411,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                   mbar_arrive_cluster(tempty_leader0 + buf * 8);
               }
             }
-            if (RL) {  // fold this chunk now: its registers are reused by the next
-              if (odd) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                  g[c * 32 + i] = __fadd_rn(__fadd_rn(0.0f, __uint_as_float(r[c][i])), g[c * 32 + i]);
-              } else if (first) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(0.0f, __uint_as_float(r[c][i]));
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], __uint_as_float(r[c][i]));
-              }
-            }
-          }
-          // level 0: g = ((0 + P_0) + P_1) + ... + P_{kf-1}   (matmul.cpp:100-125); for
-          // k_first == 1 an odd group merges with its even sibling kept in g (level 1
-          // in registers): g = (0 + P) + g  (matmul.cpp:107-123, new + old)
-          if (RL) {
-          } else if (odd) {
-#pragma unroll
-            for (int c = 0; c < HN / 32; ++c)
+            // level 0: g = ((0 + P_0) + P_1) + ... + P_{kf-1}   (matmul.cpp:100-125); for
+            // k_first == 1 an odd group merges with its even sibling kept in g (level 1
+            // in registers): g = (0 + P) + g  (matmul.cpp:107-123, new + old)
+            if (odd) {
 #pragma unroll
               for (int i = 0; i < 32; ++i)
                 g[c * 32 + i] = __fadd_rn(__fadd_rn(0.0f, __uint_as_float(r[c][i])), g[c * 32 + i]);
-          } else if (first) {
-#pragma unroll
-            for (int c = 0; c < HN / 32; ++c)
+            } else if (first) {
 #pragma unroll
               for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(0.0f, __uint_as_float(r[c][i]));
-          } else {
-#pragma unroll
-            for (int c = 0; c < HN / 32; ++c)
+            } else {
 #pragma unroll
               for (int i = 0; i < 32; ++i) g[c * 32 + i] = __fadd_rn(g[c * 32 + i], __uint_as_float(r[c][i]));
+            }
           }
         }
         if (parked > 0) {  // next parked box of the previous tile (3 - parked = 1, then 2)
@@ -494,7 +464,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 g[TCOLS + i + 2] = __fadd_rn(g[TCOLS + i + 2], x.z);
                 g[TCOLS + i + 3] = __fadd_rn(g[TCOLS + i + 3], x.w);
               }
-            } else if (RL && level == RLV) {
+            } else if (level == RLV) {
 #pragma unroll
               for (int i = 0; i < RCOLS; ++i) g[i] = __fadd_rn(g[i], l2r[i]);
 #pragma unroll
@@ -508,7 +478,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             } else {
               // all 24 loads in flight at once: one L2 round trip per level, not six
               const float* sp = scratch_base + static_cast<size_t>(level - FS) * (BM * BNT);
-              constexpr int NB = RL ? 2 : 1;  // RL: two batches (register room)
+              constexpr int NB = 2;  // two batches of loads (register room)
 #pragma unroll
               for (int b = 0; b < NB; ++b) {
                 float4 x[HN / 4 / NB];
@@ -543,7 +513,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 *reinterpret_cast<float4*>(lvl_s + ((i / 4) * 32 + lane) * 16) =
                     make_float4(g[TCOLS + i], g[TCOLS + i + 1], g[TCOLS + i + 2], g[TCOLS + i + 3]);
               tmem_wait_st();
-            } else if (RL && level == RLV) {
+            } else if (level == RLV) {
 #pragma unroll
               for (int i = 0; i < RCOLS; ++i) l2r[i] = g[i];
 #pragma unroll
@@ -617,7 +587,7 @@ int sm_count_dev() {
 // setmaxnreg only redistributes the registers the launch allocated: the merge
 // warpgroups' 232 need exactly 168 per thread at launch (384 x 168 = 128 x 40 +
 // 256 x 232).  Checked once per (device, kernel); otherwise this path is off.
-bool regs_ok(int dev, const void* kern, size_t smem) {
+bool regs_ok(int dev, const void* kern) {
   static std::mutex mu;
   static std::map<std::pair<int, const void*>, bool> ok;
   std::lock_guard<std::mutex> lk(mu);
@@ -628,7 +598,7 @@ bool regs_ok(int dev, const void* kern, size_t smem) {
   if (!good) cudaGetLastError();
   ok[{dev, kern}] = good;
   if (good) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM_BYTES));
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
   }
   return good;
@@ -636,17 +606,47 @@ bool regs_ok(int dev, const void* kern, size_t smem) {
 
 }  // namespace
 
+// FULL / UNITS launches of pair tiles with a 16-byte addressable f32 output (TMA
+// stores) and no epilogue; any block_k (the stage ring streams a leaf).
+bool tc_wide_supported(const GemmView& v, const GemmOut& o) {
+  const int64_t ustride = o.mode != OUT_FULL ? o.unit_stride : o.ldo * v.M;
+  return (o.mode == OUT_FULL || o.mode == OUT_UNITS) && !o.act && !o.ms && v.M > BM &&
+         (reinterpret_cast<uintptr_t>(o.out) & 15) == 0 && o.ldo % 4 == 0 && ustride % 4 == 0;
+}
+
+// Which pair-tile kernel a plain FULL / UNITS launch takes, and with how many K-split
+// units (measured, profiles/r02_w192_tiles.md): 256 x 192 tiles whenever there are
+// enough of them for the 74 CTA pairs -- >= 120 tiles (M=1024 N>=6144, M>=1536 N=4096:
+// Llama down_proj M=4096 +10 %, M=1536 +15 %, lm_head M=1024 +8 %, TP shards +3..14 %,
+// k_first = 1 shapes +4..12 %), or >= 80 tiles with K >= 8192 as two K units (M=1024:
+// down_proj +2 %, Qwen3-32B down_proj K=25600 +48 %); otherwise the 256 x 128 kernel
+// with its own split rule (M=1024 K=4096 N=4096: 41.5 vs 45.9 us).  256 x 256 tiles are
+// never faster than 256 x 192 (built, measured and removed in round 2:
+// profiles/r02_wide_tiles.md).  Knob tc_wide forces the choice (0: 256 x 128,
+// 1: 256 x 192), tc_units the split.
+int64_t tc_w192_units(const GemmView& v) {
+  if (v.M <= 128) return 0;
+  const int64_t tiles = ((v.M + 255) / 256) * ((v.N + 191) / 192);
+  if (tiles >= 120) return 1;
+  if (tiles >= 80 && v.K >= 8192) return 2;
+  return 0;
+}
+
+int tc_wide_variant(const GemmView& v) {
+  const int64_t k = knob(KNOB_TC_WIDE, -1);
+  if (k == 0) return 0;
+  if (k >= 1) return 1;
+  return tc_w192_units(v) > 0 ? 1 : 0;
+}
+
 tbik_status launch_tc_w192(const GemmView& v, const GemmOut& o, cudaStream_t s) {
   if (!tc_wide_supported(v, o)) return set_error(TBIK_UNSUPPORTED, "tc w192: unsupported launch");
   const int kf1 = v.kf == 1;
   using Kern = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const W3Params);
-  const bool rl = knob(KNOB_TC_W192_RL, 1) != 0;
-  const Kern kern = rl ? (kf1 ? tc_w192_tree_gemm_kernel<true, true> : tc_w192_tree_gemm_kernel<false, true>)
-                       : (kf1 ? tc_w192_tree_gemm_kernel<true, false> : tc_w192_tree_gemm_kernel<false, false>);
-  const size_t smem = smem_bytes(rl);
+  const Kern kern = kf1 ? tc_w192_tree_gemm_kernel<true> : tc_w192_tree_gemm_kernel<false>;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!regs_ok(dev, reinterpret_cast<const void*>(kern), smem))
+  if (!regs_ok(dev, reinterpret_cast<const void*>(kern)))
     return set_error(TBIK_UNSUPPORTED, "tc w192: kernel register count is not 168");
   W3Params p{};
   p.M = static_cast<int>(v.M);
@@ -684,7 +684,7 @@ tbik_status launch_tc_w192(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   }
   p.items = p.full_items + 2 * (tiles - p.full_items);
   const long long npairs = p.items < slots ? p.items : slots;
-  const int FS = (kf1 ? 3 : 2) + (rl ? 1 : 0);
+  const int FS = kf1 ? 4 : 3;
   if (p.levels >= FS) {
     const size_t n = static_cast<size_t>(2 * npairs) * (p.levels - FS + 1) * BM * BNT;
     p.scratch = static_cast<float*>(workspace(n * sizeof(float), 1, s));
@@ -704,7 +704,7 @@ tbik_status launch_tc_w192(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(static_cast<unsigned>(2 * npairs));
   lc.blockDim = dim3(NTHREADS);
-  lc.dynamicSmemBytes = smem;
+  lc.dynamicSmemBytes = SMEM_BYTES;
   lc.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;

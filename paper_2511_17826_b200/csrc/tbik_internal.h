@@ -99,9 +99,8 @@ enum Knob {
   KNOB_GROUP_FUSED,      // 0: no fused GEMM + all-reduce kernel
   KNOB_GROUP_OVERLAP,    // 0: no chunked GEMM / all-reduce overlap
   KNOB_AR_TWO_PHASE_BYTES,  // payload bytes from which the group all-reduce is two-phase
-  KNOB_TC_WIDE,          // 0: 256 x 128, 1: 256 x 256 (tbik_gemm_tc_w.cu), 2: 256 x 192 (tbik_gemm_tc_w192.cu)
+  KNOB_TC_WIDE,          // 0: 256 x 128 tiles, 1: 256 x 192 tiles (tbik_gemm_tc_w192.cu)
   KNOB_TC_WIDE_TAIL,     // 0: no half items in the wide kernels' last wave
-  KNOB_TC_W192_RL,       // 0: 256 x 192 kernel without the register tree level (6 stages)
   KNOB_COUNT
 };
 int64_t knob(Knob k, int64_t dflt);
@@ -125,16 +124,14 @@ tbik_status launch_silu_mul_il(const float* gu, int64_t ld, int64_t rows, int64_
 bool tc_use_skinny(const GemmView& v);
 tbik_status launch_tc_skinny(const GemmView& v, float* C, int64_t ldc, cudaStream_t s);
 
-// 256 x 256 pair-tile variant of launch_tc_gemm (tbik_gemm_tc_w.cu): FULL / UNITS
+// 256 x 192 pair-tile variant of launch_tc_gemm (tbik_gemm_tc_w192.cu): FULL / UNITS
 // modes without epilogues; same bits as the 256 x 128 kernel.
 bool tc_wide_supported(const GemmView& v, const GemmOut& o);
-// 0: the 256 x 128 kernel, 1: 256 x 256 tiles (tbik_gemm_tc_w.cu), 2: 256 x 192 tiles
-// (tbik_gemm_tc_w192.cu); knob tc_wide overrides.
+// 0: the 256 x 128 kernel, 1: 256 x 192 tiles; knob tc_wide overrides.
 int tc_wide_variant(const GemmView& v);
 // K-split units the 256 x 192 kernel wants for v by default (1 or 2), 0 when it is
 // not the default kernel for v.
 int64_t tc_w192_units(const GemmView& v);
-tbik_status launch_tc_wide(const GemmView& v, const GemmOut& o, cudaStream_t s);
 tbik_status launch_tc_w192(const GemmView& v, const GemmOut& o, cudaStream_t s);
 
 // K-split factor run_tree_gemm uses for the tcgen05 leaf (1 = one FULL launch).

@@ -1,4 +1,4 @@
-"""256 x 256 pair tiles (tbik_gemm_tc_w.cu) vs the 256 x 128 kernel: bit equality on
+"""256 x 192 pair tiles (tbik_gemm_tc_w192.cu) vs the 256 x 128 kernel: bit equality on
 ragged / split / k_first = 1 / TP-shard shapes, then device time per call (CUDA
 events, 20 back-to-back calls) for the schedule variants.
 usage: python tools/wide_check.py [check] [time] [M K N ...]"""
@@ -57,7 +57,7 @@ def check():
         cfg = tb.BlockConfig(64, bk, 128, kf)
         ref = run(x, w, cfg, {"tc_wide": 0, **{k: v for k, v in knobs.items() if k == "tc_units"}})
         res = []
-        for name, kv in (("w256", {"tc_wide": 1}), ("w192", {"tc_wide": 2}), ("w192_norl", {"tc_wide": 2, "tc_w192_rl": 0})):
+        for name, kv in (("w192", {"tc_wide": 1}),):
             y = run(x, w, cfg, {**kv, **knobs})
             same = torch.equal(ref.view(torch.int32), y.view(torch.int32))
             ok &= same
@@ -72,11 +72,11 @@ SHAPES = [(4096, 14336, 4096), (2048, 14336, 4096), (1024, 14336, 4096), (512, 1
           (4096, 7168, 4096), (4096, 3584, 4096), (4096, 1792, 4096), (1024, 1792, 4096),
           (4096, 4096, 4096), (2048, 4096, 4096), (4096, 4096, 28672), (1024, 4096, 6144),
           (1024, 25600, 5120), (2048, 25600, 5120), (4096, 25600, 5120), (4096, 5120, 10240), (2048, 3200, 5120)]
-MID_VARIANTS = [("narrow", {"tc_wide": 0}), ("w192", {"tc_wide": 2}), ("w192_u1", {"tc_wide": 2, "tc_units": 1}),
-                ("w192_u2", {"tc_wide": 2, "tc_units": 2}), ("w192_u4", {"tc_wide": 2, "tc_units": 4})]
-VARIANTS = MID_VARIANTS if os.environ.get("MID") else [("narrow", {"tc_wide": 0}), ("w256", {"tc_wide": 1}), ("w192", {"tc_wide": 2}),
-            ("w192_norl", {"tc_wide": 2, "tc_w192_rl": 0}), ("w192_notail", {"tc_wide": 2, "tc_wide_tail": 0}),
-            ("w192_gm4", {"tc_wide": 2, "tc_group_m": 4})]
+MID_VARIANTS = [("narrow", {"tc_wide": 0}), ("w192", {"tc_wide": 1}), ("w192_u1", {"tc_wide": 1, "tc_units": 1}),
+                ("w192_u2", {"tc_wide": 1, "tc_units": 2}), ("w192_u4", {"tc_wide": 1, "tc_units": 4})]
+VARIANTS = MID_VARIANTS if os.environ.get("MID") else [
+    ("narrow", {"tc_wide": 0}), ("w192", {"tc_wide": 1}), ("w192_notail", {"tc_wide": 1, "tc_wide_tail": 0}),
+    ("w192_gm4", {"tc_wide": 1, "tc_group_m": 4})]
 
 
 def timing(shapes):
