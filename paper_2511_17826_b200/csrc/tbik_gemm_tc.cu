@@ -827,6 +827,23 @@ tbik_status tc_make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, u
 }
 
 // 32-byte swizzle (16-column bf16 boxes): the MN-major B atoms of the 256x192 kernel.
+// bf16 [1][M][N] output of the SiLU*up epilogue, no swizzle (box rows of box_n
+// elements), as a 3D map so the kernels' TMA-store helper serves it unchanged.
+tbik_status tc_make_map_act(CUtensorMap* map, uint16_t* base, uint64_t n, uint64_t m, uint64_t row_stride_bytes,
+                            uint32_t box_n, uint32_t box_m) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return set_error(TBIK_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {n, m, 1};
+  cuuint64_t strides[2] = {row_stride_bytes, row_stride_bytes * m};
+  cuuint32_t box[3] = {box_n, box_m, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(TBIK_CUDA_ERROR, "cuTensorMapEncodeTiled(act) failed: " + std::to_string(r));
+  return TBIK_OK;
+}
+
 tbik_status tc_make_map_2d_sw32(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                                 uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
   return make_map_2d(map, base, inner, outer, row_stride_bytes, box_inner, box_outer, CU_TENSOR_MAP_SWIZZLE_32B);

@@ -41,6 +41,7 @@
 
 #include "tbik_common.cuh"
 #include "tbik_internal.h"
+#include "tbik_mathfn.cuh"
 #include "tbik_pair.cuh"
 
 namespace tbik_b200 {
@@ -53,6 +54,8 @@ tbik_status tc_make_map_2d_sw64(CUtensorMap* map, const void* base, uint64_t inn
                                 uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
 tbik_status tc_make_map_out(CUtensorMap* map, float* base, uint64_t n, uint64_t m, uint64_t units,
                             uint64_t row_stride_bytes, uint64_t unit_stride_bytes);
+tbik_status tc_make_map_act(CUtensorMap* map, uint16_t* base, uint64_t n, uint64_t m, uint64_t row_stride_bytes,
+                            uint32_t box_n, uint32_t box_m);
 
 namespace {
 
@@ -98,6 +101,7 @@ struct W3Params {
   long long full_items;  // items [0, full_items) are 256 x 192 tiles ...
   long long items;       // ... the rest 256 x 96 halves of the remaining tiles
   float* scratch;        // [gridDim.x][levels - FS + 1][BNT / 4][BM][4]
+  int act;               // 1: SiLU*up epilogue -- tmC maps the bf16 [M][N/2] output instead
 };
 
 struct W3Item {
@@ -534,6 +538,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // output boxes one after the other (128B swizzle, conflict-free 16-byte stores)
         // for TMA stores that clip ragged edges.
         const int unit_out = p.mode == OUT_UNITS ? it.unit : 0;
+        if (p.act) {
+          // fused SiLU(gate) * up (tb_silu_mul_bf16, the same ops as tbik_silu_mul): the
+          // thread's 96 columns are 48 (gate, up) pairs -> 48 bf16 = one 96-byte row of a
+          // 32 x 48 bf16 box staged in the dead level slab, one TMA store per warp
+          __syncwarp();
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+#pragma unroll
+          for (int q8 = 0; q8 < HN / 16; ++q8) {
+            uint32_t w4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c = q8 * 16 + 4 * e;
+              w4[e] = static_cast<uint32_t>(tb_silu_mul_bf16(g[c], g[c + 1])) |
+                      (static_cast<uint32_t>(tb_silu_mul_bf16(g[c + 2], g[c + 3])) << 16);
+            }
+            *reinterpret_cast<uint4*>(lvl_s + lane * (HN / 2 * 2) + q8 * 16) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tmC, smem_u32(lvl_s), col_base / 2, grow - lane, 0);
+            bulk_commit();
+          }
+          continue;
+        }
         while (parked > 0) {  // a tile of a single leaf: the previous tile's boxes go first
           emit_parked_box(lvl_s, lvl_t, 3 - parked, &tmC, pk_col, pk_row, pk_unit, lane);
           --parked;
@@ -609,9 +639,12 @@ bool regs_ok(int dev, const void* kern) {
 // FULL / UNITS launches of pair tiles with a 16-byte addressable f32 output (TMA
 // stores) and no epilogue; any block_k (the stage ring streams a leaf).
 bool tc_wide_supported(const GemmView& v, const GemmOut& o) {
+  if (o.ms || v.M <= BM) return false;
+  if (o.act)  // the SiLU*up epilogue: FULL, even N, a 16-byte addressable bf16 output
+    return o.mode == OUT_FULL && v.N % 2 == 0 && (reinterpret_cast<uintptr_t>(o.act) & 15) == 0 && o.ld_act % 8 == 0;
   const int64_t ustride = o.mode != OUT_FULL ? o.unit_stride : o.ldo * v.M;
-  return (o.mode == OUT_FULL || o.mode == OUT_UNITS) && !o.act && !o.ms && v.M > BM &&
-         (reinterpret_cast<uintptr_t>(o.out) & 15) == 0 && o.ldo % 4 == 0 && ustride % 4 == 0;
+  return (o.mode == OUT_FULL || o.mode == OUT_UNITS) && (reinterpret_cast<uintptr_t>(o.out) & 15) == 0 &&
+         o.ldo % 4 == 0 && ustride % 4 == 0;
 }
 
 // Which pair-tile kernel a plain FULL / UNITS launch takes, and with how many K-split
@@ -697,10 +730,16 @@ tbik_status launch_tc_w192(const GemmView& v, const GemmOut& o, cudaStream_t s) 
                                static_cast<uint64_t>(v.ldb) * 2, ATOM_F, KSTAGE));
   TBIK_TRY(tc_make_map_2d_sw32(&mBh, v.B, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.K),
                                static_cast<uint64_t>(v.ldb) * 2, ATOM_H, KSTAGE));
-  const uint64_t ustride = o.mode != OUT_FULL ? static_cast<uint64_t>(o.unit_stride)
-                                              : static_cast<uint64_t>(o.ldo) * static_cast<uint64_t>(v.M);
-  TBIK_TRY(tc_make_map_out(&mC, o.out, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.M),
-                           static_cast<uint64_t>(p.units), static_cast<uint64_t>(o.ldo) * 4, ustride * 4));
+  if (o.act) {
+    p.act = 1;
+    TBIK_TRY(tc_make_map_act(&mC, o.act, static_cast<uint64_t>(v.N / 2), static_cast<uint64_t>(v.M),
+                             static_cast<uint64_t>(o.ld_act) * 2, HN / 2, 32));
+  } else {
+    const uint64_t ustride = o.mode != OUT_FULL ? static_cast<uint64_t>(o.unit_stride)
+                                                : static_cast<uint64_t>(o.ldo) * static_cast<uint64_t>(v.M);
+    TBIK_TRY(tc_make_map_out(&mC, o.out, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.M),
+                             static_cast<uint64_t>(p.units), static_cast<uint64_t>(o.ldo) * 4, ustride * 4));
+  }
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(static_cast<unsigned>(2 * npairs));
   lc.blockDim = dim3(NTHREADS);

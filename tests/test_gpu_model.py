@@ -244,3 +244,27 @@ def test_residual_rmsnorm_fused_equals_two_kernels(tb, cuda, rows, cols):
     y2 = tb.rmsnorm(h2, gamma, 1e-5, out_dtype=torch.bfloat16)
     assert torch.equal(h1.view(torch.int16), h2.view(torch.int16))
     assert torch.equal(y1.view(torch.int16), y2.view(torch.int16))
+
+
+@pytest.mark.parametrize("M,inter", [(300, 1024), (1024, 1536), (2048, 1000)])
+def test_fused_silu_gate_up_256x192_tiles(tb, cuda, M, inter):
+    """The SiLU*up epilogue of the 256x192 pair-tile kernel (bf16 box staged in the dead
+    tree-level slab, TMA store) == the 256x128 kernel's == tree GEMM + tbik_silu_mul."""
+    K = 4096
+    g = torch.Generator(device=cuda).manual_seed(M + inter)
+    x = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(K, 2 * inter, device=cuda, generator=g) * 0.02).to(torch.bfloat16)
+    cfg = tb.BlockConfig(64, 256, 128, 0)
+    w_il = tb.interleave_gate_up(w)
+    with tb.schedule(tc_wide=0):
+        ref = tb.tree_matmul_silu_mul(x, w_il, tb.DeviceGroup(1), cfg, tb.LEAF_TCGEN05)
+    for tp in (1, 2):
+        with tb.schedule(tc_wide=1):
+            act = tb.tree_matmul_silu_mul(x, w_il, tb.DeviceGroup(tp), cfg, tb.LEAF_TCGEN05)
+            kern = tb.last_kernel()
+        torch.cuda.synchronize()
+        # a rank's slice of a 1000-pair output is not 16-byte aligned: the 256x128
+        # kernel's epilogue (direct stores) takes it
+        aligned = (inter // tp) % 8 == 0
+        assert kern == ("tc_w192_tree_gemm_kernel" if aligned else "tc_tree_gemm_kernel")
+        assert torch.equal(act.view(torch.int16), ref.view(torch.int16)), f"tp={tp}"
