@@ -638,6 +638,9 @@ bool regs_ok(int dev, const void* kern) {
 
 // FULL / UNITS launches of pair tiles with a 16-byte addressable f32 output (TMA
 // stores) and no epilogue; any block_k (the stage ring streams a leaf).
+// The lm_head's chunk (m, s) epilogue stays on the 256x128 kernel: on 256x192 tiles
+// its exp work at the tile end cost more than the tile saves (M=1024 K=4096 V=128256:
+// 1083.6 vs 1062.5 us, tools/lm_head_w192.py).
 bool tc_wide_supported(const GemmView& v, const GemmOut& o) {
   if (o.ms || v.M <= BM) return false;
   if (o.act)  // the SiLU*up epilogue: FULL, even N, a 16-byte addressable bf16 output
