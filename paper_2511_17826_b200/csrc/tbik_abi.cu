@@ -440,12 +440,14 @@ tbik_status tbik_tree_matmul_logits(const void* A, int a_dtype, int64_t lda, con
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t n = N / groups, nc = (n + 15) / 16;
   if (ld_chunks < groups * nc) return set_error(TBIK_BAD_ARGUMENT, "logits: ld_chunks < groups * chunks per group");
-  // The chunk states come out of the tcgen05 GEMM's epilogue when the GEMM is one
-  // FULL pair-tile launch (M > 128; not the skinny or K-split schedules) and chunks
+  // The chunk states come out of the 256x128 tcgen05 GEMM's epilogue when the GEMM is
+  // one FULL pair-tile launch (M > 128; not the skinny or K-split schedules, and not a
+  // shape where the 256x192 kernel is the default: its plain GEMM + a pass over the
+  // logits measured faster than the 256x128 epilogue, tools/lm_head_w192.py) and chunks
   // are absolute 16-column blocks (n % 16 == 0); otherwise a pass over the logits
   // computes the same states (tb_ms_chunk16 in both) -- a pure scheduling choice.
   if (leaf_mode == TBIK_LEAF_TCGEN05 && n % 16 == 0 && M > 128 && !tc_use_skinny(v) && tc_split_units(v) <= 1 &&
-      tc_supported(v, nullptr) && (reinterpret_cast<uintptr_t>(chunk_ms) & 7) == 0) {
+      tc_wide_variant(v) == 0 && tc_supported(v, nullptr) && (reinterpret_cast<uintptr_t>(chunk_ms) & 7) == 0) {
     GemmOut o{OUT_FULL, v.T, C, ldc, 0};
     o.ms = chunk_ms;
     o.ld_ms = 2 * ld_chunks;
