@@ -460,3 +460,33 @@ def test_wide_tiles_bit_identical(tb, cuda, M, K, N, bk, kf, knobs):
             got = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
             assert tb.last_kernel() == name
         assert torch.equal(want.view(torch.int32), got.view(torch.int32)), (M, K, N, knobs, kv)
+
+
+def _wide_random_shapes(n):
+    rng = np.random.default_rng(192)
+    out = []
+    for _ in range(n):
+        M = int(rng.integers(129, 2600))
+        N = int(rng.integers(1, 1400))
+        K = int(rng.integers(16, 7000))
+        bk = int(rng.choice([64, 128, 256]))
+        T = (K + bk - 1) // bk  # k_first: 0 (the planner's) or T / 2^j (a feasible plan)
+        kfs = [0] + [T >> j for j in range(0, 12) if T % (1 << j) == 0 and T >> j >= 1]
+        kf = int(rng.choice(kfs))
+        out.append((M, K, N, bk, kf))
+    return out
+
+
+@pytest.mark.parametrize("M,K,N,bk,kf", _wide_random_shapes(12))
+def test_wide_tiles_random_shapes(tb, cuda, M, K, N, bk, kf):
+    """256x192 vs 256x128 pair tiles on random ragged shapes, block_k and k_first (N
+    down to 1: tiles past N, empty half items; K down to 16: a partial single stage)."""
+    g = torch.Generator(device=cuda).manual_seed(M * 7 + N)
+    x = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    w = torch.randn(K, N, device=cuda, generator=g).to(torch.bfloat16)
+    cfg = tb.BlockConfig(64, bk, 128, kf)
+    with tb.schedule(tc_wide=0):
+        want = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+    with tb.schedule(tc_wide=1):
+        got = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+    assert torch.equal(want.view(torch.int32), got.view(torch.int32)), (M, K, N, bk, kf)
