@@ -101,6 +101,25 @@ def test_tc_tree_over_gpu_leaves(tb, cuda, orc, M, K, N):
     assert np.array_equal(bits(got), bits(want)), f"mismatches: {(bits(got) != bits(want)).sum()}"
 
 
+@pytest.mark.parametrize("M,K,N,kf", [(300, 4096, 384, 0), (520, 14336, 200, 0), (1100, 6144, 500, 3)])
+def test_w192_tree_over_gpu_leaves(tb, cuda, orc, M, K, N, kf):
+    """The 256x192 kernel (forced) == the oracle tree applied to the GPU's own leaves,
+    bit for bit: its TMEM / register / shared-memory / scratch tree levels and half
+    items are the reference's tree (matmul.cpp:100-125)."""
+    a, b = gen(orc, 5 + M, M, K, N)
+    cfg = tb.BlockConfig(64, 256, 128, kf)
+    da, db = to_dev(a), to_dev(b)
+    with tb.schedule(tc_wide=1):
+        y = tb.tree_matmul(da, db, cfg, tb.LEAF_TCGEN05)
+        assert tb.last_kernel() == "tc_w192_tree_gemm_kernel"
+    leaves = tb.tree_matmul_leaves(da, db, cfg, tb.LEAF_TCGEN05)
+    torch.cuda.synchronize()
+    plan = tb.plan_blocks(K, cfg, 1)
+    want = orc.tree_over_leaves(leaves.cpu().numpy(), plan.k_first)
+    got = y.cpu().numpy()
+    assert np.array_equal(bits(got), bits(want)), f"mismatches: {(bits(got) != bits(want)).sum()}"
+
+
 def test_tc_leaf_error_bound(tb, cuda, orc):
     """The tcgen05 leaf against exact (f64) arithmetic, next to the reference's own
     fma-chain leaf: both are held to |P - exact| <= 2^-21 * sum_k |a_k b_k|
