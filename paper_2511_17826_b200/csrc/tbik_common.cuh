@@ -90,6 +90,18 @@ __device__ __forceinline__ uint16_t f32_to_bf16_bits(float x) {
   return static_cast<uint16_t>((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
 }
 
+// Two bf16_round results packed (lo in bits 0-15): the hardware RNE conversion
+// (cvt.rn.bf16x2.f32: the same bits as f32_to_bf16_bits for every non-NaN input,
+// subnormals and overflow to infinity included), NaN canonicalised to 0x7FC0 like
+// numerics.hpp:49-56.
+__device__ __forceinline__ uint32_t bf16x2_bits(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  if (lo != lo) r = (r & 0xFFFF0000u) | 0x7FC0u;
+  if (hi != hi) r = (r & 0x0000FFFFu) | 0x7FC00000u;
+  return r;
+}
+
 // ---- PTX wrappers ------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

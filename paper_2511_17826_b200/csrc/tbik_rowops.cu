@@ -74,17 +74,10 @@ __device__ __forceinline__ void store_chunk<float>(float* y, const float* r, int
 template <>
 __device__ __forceinline__ void store_chunk<uint16_t>(uint16_t* y, const float* r, int n) {
   if (n == 8) {
-    uint4 o;
-    o.x = f32_to_bf16_bits(r[0]) | (static_cast<uint32_t>(f32_to_bf16_bits(r[1])) << 16);
-    o.y = f32_to_bf16_bits(r[2]) | (static_cast<uint32_t>(f32_to_bf16_bits(r[3])) << 16);
-    o.z = f32_to_bf16_bits(r[4]) | (static_cast<uint32_t>(f32_to_bf16_bits(r[5])) << 16);
-    o.w = f32_to_bf16_bits(r[6]) | (static_cast<uint32_t>(f32_to_bf16_bits(r[7])) << 16);
-    *reinterpret_cast<uint4*>(y) = o;
+    *reinterpret_cast<uint4*>(y) =
+        make_uint4(bf16x2_bits(r[0], r[1]), bf16x2_bits(r[2], r[3]), bf16x2_bits(r[4], r[5]), bf16x2_bits(r[6], r[7]));
   } else if (n == 4) {
-    uint2 o;
-    o.x = f32_to_bf16_bits(r[0]) | (static_cast<uint32_t>(f32_to_bf16_bits(r[1])) << 16);
-    o.y = f32_to_bf16_bits(r[2]) | (static_cast<uint32_t>(f32_to_bf16_bits(r[3])) << 16);
-    *reinterpret_cast<uint2*>(y) = o;
+    *reinterpret_cast<uint2*>(y) = make_uint2(bf16x2_bits(r[0], r[1]), bf16x2_bits(r[2], r[3]));
   }
 }
 
@@ -119,8 +112,23 @@ __device__ __forceinline__ void norm_chunk(const uint4& raw, const float* __rest
   float gm[CH], r[CH];
 #pragma unroll
   for (int i = 0; i < CH; i += 4) *reinterpret_cast<float4*>(gm + i) = *reinterpret_cast<const float4*>(gamma + e0 + i);
+  // div_rn_rcp with its range guard hoisted out of the element loop: the reciprocal
+  // form for all CH elements, and -- rarely -- the whole chunk again by division
+  // (in range both give RN(n / d), so the redo changes no in-range element)
+  bool redo = false;
 #pragma unroll
-  for (int i = 0; i < CH; ++i) r[i] = div_rn_rcp(__fmul_rn(load_as_f32(v + i), gm[i]), denom, rcp);
+  for (int i = 0; i < CH; ++i) {
+    const float n = __fmul_rn(load_as_f32(v + i), gm[i]);
+    const float q0 = __fmul_rn(n, rcp);
+    const float e = __fmaf_rn(-q0, denom, n);
+    r[i] = __fmaf_rn(e, rcp, q0);
+    const float aq = fabsf(q0);
+    redo |= aq < 0x1p-100f || aq > 0x1p100f;
+  }
+  if (redo) {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) r[i] = __fdiv_rn(__fmul_rn(load_as_f32(v + i), gm[i]), denom);
+  }
   store_chunk<TY>(y + e0, r, CH);
 }
 

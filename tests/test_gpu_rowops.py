@@ -166,3 +166,29 @@ def test_chunk_states_masked_and_wide(tb, cuda, orc):
     m_w, s_w = orc.logsoftmax_chunk_states(x, G)
     c = ck.cpu().numpy()
     assert np.array_equal(bits(c[..., 0]), bits(m_w)) and np.array_equal(bits(c[..., 1]), bits(s_w))
+
+
+def test_tree_rmsnorm_bf16_out_special_values(tb, cuda, orc):
+    """bf16 output through the hardware RNE pair conversion: gamma drives results into
+    overflow (inf), bf16-subnormal and tie-to-even territory and through NaN; every
+    element equals bf16_round of the f32 result (RNE, canonical NaN 0x7FC0,
+    numerics.hpp:49-56) and the f32 path stays bit-exact with the oracle."""
+    rows, cols = 3, 4096
+    x = orc.random_normal(11, 1, rows, cols, "bf16")
+    gamma = np.ones(cols, dtype=np.float32)
+    gamma[0::7] = 3e38          # overflow -> +-inf
+    gamma[1::7] = 1e-40         # f32-subnormal products -> bf16 subnormals / zeros
+    gamma[2::7] = np.nan        # NaN results
+    gamma[3::7] = 1.0 + 2.0 ** -8   # results near bf16 rounding ties
+    gamma[4::7] = -2.5e-39
+    want = orc.tree_rmsnorm(x, gamma, 1e-5)
+    got32 = tb.rmsnorm(to_dev(x), to_dev(gamma), 1e-5).cpu().numpy()
+    nan = np.isnan(want)  # f32 NaN payloads are outside parity (SPEC.md:31); NaN-ness is not
+    assert np.array_equal(np.isnan(got32), nan)
+    assert np.array_equal(bits(got32)[~nan], bits(want)[~nan])
+    got16 = tb.rmsnorm(to_dev(x), to_dev(gamma), 1e-5, out_dtype=torch.bfloat16).cpu().view(torch.int16).numpy()
+    u = want.view(np.uint32).astype(np.uint64)  # bf16_round, vectorised (RNE, canonical NaN)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    r[np.isnan(want)] = 0x7FC0
+    assert orc.bf16_round(float(want.flat[5])) == int(r.flat[5])  # the restatement agrees with the oracle's
+    assert np.array_equal(got16, r.view(np.int16).reshape(got16.shape))
