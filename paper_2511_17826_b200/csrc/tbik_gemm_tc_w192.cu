@@ -4,7 +4,10 @@
 // Same arithmetic as tc_tree_gemm_kernel (tbik_gemm_tc.cu): every leaf is the
 // block_k/16 tcgen05.mma.cta_group::2 K=16 steps into a zeroed TMEM accumulator,
 // then the reference's fold and binary tree (matmul.cpp:100-125) in __fadd_rn; the
-// MMA's N changes no element's sum (tests/test_gpu_gemm.py::test_w192_tiles_bit_identical).
+// MMA's N changes no element's sum (tests/test_gpu_gemm.py: test_wide_tiles_bit_identical,
+// test_wide_tiles_random_shapes, test_w192_tree_over_gpu_leaves).  Epilogues: f32
+// output (FULL or K-split units) or the fused bf16 SiLU(gate)*up of interleaved
+// gate/up columns.
 //
 // Why this width (profiles/r02_w192_tiles.md): the SM's shared-memory data port
 // (~128 B/clk) carries the tensor core's operand reads AND the TMA writes of the same
