@@ -37,7 +37,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <cstdio>
 #include <string>
+#include <vector>
 
 #include "tbik_common.cuh"
 #include "tbik_internal.h"
@@ -47,13 +49,13 @@ namespace tbik_b200 {
 // tbik_gemm_tc.cu (tensor-map helpers shared by the tcgen05 kernels)
 tbik_status tc_make_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                            uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+tbik_status tc_make_map_2d_sw64(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                                uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
 
 namespace {
 
 constexpr int SK_BN = 128;                  // weight columns per tile (BNW = 128: MMA M = 128)
-constexpr int SK_KSTAGE = 64;               // K per pipeline stage
-constexpr int SK_W_ATOM = 64 * SK_KSTAGE * 2;  // one 64-column SW128 atom: 8 KB
-constexpr int SK_W_STAGE = 2 * SK_W_ATOM;   // 16 KB
+constexpr int SK_KSTAGE = 64;               // K granularity of a stage (KS = 64 or 128 per stage)
 constexpr int SK_TMEM_COLS = 512;
 constexpr int SK_SMEM_LIMIT = 232448;
 constexpr int SK_MAX_UNITS = 8;
@@ -71,17 +73,26 @@ constexpr int sk_nacc() { return MT >= 128 ? 2 : 4; }
 // BNW = weight columns per tile: 128 (MMA M = 128, all TMEM lanes) or 64 (MMA
 // M = 64: rows land in TMEM lanes 0-15 of each 32-lane quarter, CUTLASS
 // mma_traits_sm100.hpp "half subpartitions" atom) -- twice the tiles for short K.
-template <int BNW>
-constexpr int sk_w_stage() { return BNW / 64 * SK_W_ATOM; }
-template <int MT, int BNW = 128>
-constexpr int sk_stages() { return (SK_SMEM_LIMIT - 2048) / (sk_w_stage<BNW>() + MT * 128); }
-template <int MT, int BNW = 128>
+// KS = K rows per stage: the W box is {64 columns, KS rows} (one SW128 atom column
+// of KS / 8 1-KB row groups); X arrives as KS / 64 boxes of {64 K, MT tokens}.
+// Taller W boxes stream faster from L2 (tools/micro/tma_ingest.cu: the time of an
+// L2-resident shard follows the number of boxes, not their bytes).
+template <int KS>
+constexpr int sk_w_atom() { return 64 * KS * 2; }
+template <int BNW, int KS = 64>
+constexpr int sk_w_stage() { return BNW * KS * 2; }
+template <int MT, int KS = 64>
+constexpr int sk_x_stage() { return MT * 128 * (KS / 64); }
+template <int MT, int BNW = 128, int KS = 64>
+constexpr int sk_stages() { return (SK_SMEM_LIMIT - 2048) / (sk_w_stage<BNW, KS>() + sk_x_stage<MT, KS>()); }
+template <int MT, int BNW = 128, int KS = 64>
 constexpr size_t sk_smem() {
-  return 1024 + static_cast<size_t>(sk_stages<MT, BNW>()) * (sk_w_stage<BNW>() + MT * 128) + 512;
+  return 1024 + static_cast<size_t>(sk_stages<MT, BNW, KS>()) * (sk_w_stage<BNW, KS>() + sk_x_stage<MT, KS>()) + 512;
 }
 static_assert(sk_smem<16>() <= SK_SMEM_LIMIT && sk_smem<32>() <= SK_SMEM_LIMIT && sk_smem<64>() <= SK_SMEM_LIMIT &&
                   sk_smem<128>() <= SK_SMEM_LIMIT && sk_smem<16, 64>() <= SK_SMEM_LIMIT &&
-                  sk_smem<128, 64>() <= SK_SMEM_LIMIT,
+                  sk_smem<128, 64>() <= SK_SMEM_LIMIT && sk_smem<128, 128, 128>() <= SK_SMEM_LIMIT &&
+                  sk_stages<128, 128, 128>() >= 3,
               "skinny smem budget");
 // Tree levels that fit in TMEM next to the accumulators.
 template <int MT>
@@ -100,6 +111,7 @@ struct SkParams {
   int bn;              // weight columns per tile (the kernel's BNW)
   float* out;
   long long ldo;
+  unsigned long long* trace;  // diagnostics (TBIK_SK_TRACE): per-CTA phase clocks, else null
 };
 
 __device__ __forceinline__ void tmem_ld16r(uint32_t taddr, uint32_t (&r)[16]) {
@@ -155,30 +167,37 @@ struct SkItem {
 // Units of one tile are adjacent items, so they run in the same wave and the
 // tile's finish starts as soon as its slowest unit is done.
 __device__ __forceinline__ SkItem sk_decode(const SkParams& p, long long item) {
-  SkItem it;
-  it.unit = static_cast<int>(item % p.units);
-  it.n0 = static_cast<int>(item / p.units) * p.bn;
+  SkItem it;  // 32-bit division (items < 2^31, checked at launch)
+  const uint32_t i = static_cast<uint32_t>(item), u = static_cast<uint32_t>(p.units);
+  it.unit = static_cast<int>(i % u);
+  it.n0 = static_cast<int>(i / u) * p.bn;
   it.t_begin = it.unit * p.tiles_per_unit;
   it.t_end = min(p.T, it.t_begin + p.tiles_per_unit);
   return it;
 }
+template <int KS>
 __device__ __forceinline__ int sk_chunks(const SkParams& p, int t) {
   const int kt0 = t * p.bk;
   const int kh = (kt0 + p.bk <= p.K) ? p.bk : p.K - kt0;
-  return (kh + SK_KSTAGE - 1) / SK_KSTAGE;
+  return (kh + KS - 1) / KS;
 }
 
-template <int MT, int BNW>
+template <int MT, int BNW, int KS>
 __global__ void __launch_bounds__(sk_threads<MT>(), 1)
     tc_skinny_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                      const SkParams p) {
-  constexpr int NST = sk_stages<MT, BNW>();
-  constexpr int W_STAGE = sk_w_stage<BNW>();
-  constexpr int LPQ = BNW / 4;  // valid TMEM lanes (tile columns) per 32-lane quarter
+  constexpr int NST = sk_stages<MT, BNW, KS>();
+  constexpr int W_ATOM = sk_w_atom<KS>();
+  constexpr int W_STAGE = sk_w_stage<BNW, KS>();
+  // MMA M = 64 for BNW = 32 (the rows past the tile are a repeat of its 32-column
+  // atom, computed and never read); TMEM lanes holding rows per 32-lane quarter:
+  constexpr int MMA_M = BNW < 64 ? 64 : BNW;
+  constexpr int LPQ = MMA_M / 4;
   constexpr int NACC = sk_nacc<MT>();
-  constexpr int X_STAGE = MT * 128;
+  constexpr int X_BOX = MT * 128;
+  constexpr int X_STAGE = sk_x_stage<MT, KS>();
   constexpr uint32_t TX_BYTES = W_STAGE + X_STAGE;
-  constexpr uint32_t IDESC = umma_idesc_bf16(BNW, MT, /*a_mn_major=*/1, /*b_mn_major=*/0);
+  constexpr uint32_t IDESC = umma_idesc_bf16(MMA_M, MT, /*a_mn_major=*/1, /*b_mn_major=*/0);
   constexpr int TPW = sk_tpw<MT>();
   constexpr int NMW = sk_merge_warps<MT>();
   constexpr int NCH = TPW / 16;
@@ -195,8 +214,16 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const long long t0 = clock64();
+#define SK_TRACE(i) \
+  if (p.trace) p.trace[blockIdx.x * 16 + (i)] = static_cast<unsigned long long>(clock64() - t0)
 
   if (warp == 0 && lane == 0) {
+    if (p.trace) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      p.trace[blockIdx.x * 16 + 15] = gt;
+    }
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmX);
     for (int s = 0; s < NST; ++s) {
@@ -214,6 +241,12 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the prologue above (barriers, TMEM, descriptor
+  // prefetch, instruction fetch) may overlap the previous kernel's tail; operands
+  // and the output are touched only after that kernel has completed (a no-op when
+  // launched without the attribute).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) SK_TRACE(1);
 
   if (warp == 0) {
     if (elect_one()) {
@@ -222,15 +255,18 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
       for (long long item = blockIdx.x; item < p.items; item += gridDim.x) {
         const SkItem it = sk_decode(p, item);
         for (int t = it.t_begin; t < it.t_end; ++t) {
-          const int nch = sk_chunks(p, t);
+          const int nch = sk_chunks<KS>(p, t);
           for (int c = 0; c < nch; ++c) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], TX_BYTES);
-            const int k = t * p.bk + c * SK_KSTAGE;
+            const int k = t * p.bk + c * KS;
             uint8_t* w = sW + stage * W_STAGE;
             tma_load_2d(w, &tmW, &full[stage], it.n0, k);
-            if constexpr (BNW == 128) tma_load_2d(w + SK_W_ATOM, &tmW, &full[stage], it.n0 + 64, k);
-            tma_load_2d(sX + stage * X_STAGE, &tmX, &full[stage], k, 0);
+            if constexpr (BNW == 128) tma_load_2d(w + W_ATOM, &tmW, &full[stage], it.n0 + 64, k);
+#pragma unroll
+            for (int j = 0; j < KS / 64; ++j)
+              tma_load_2d(sX + stage * X_STAGE + j * X_BOX, &tmX, &full[stage], k + 64 * j, 0);
+            if (item == blockIdx.x && t == it.t_begin && c == 0) SK_TRACE(2);
             if (++stage == NST) {
               stage = 0;
               phase ^= 1;
@@ -238,6 +274,11 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
           }
         }
       }
+      SK_TRACE(3);
+      // Every load of this CTA is issued: the next kernel may begin its prologue
+      // (dependents launch once every CTA of this grid has triggered or exited, so
+      // later-wave CTAs are never starved of SMs).
+      asm volatile("griddepcontrol.launch_dependents;");
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -245,27 +286,38 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t acc_iter = 0;
+      long long full_wait = 0, acc_wait = 0;
       for (long long item = blockIdx.x; item < p.items; item += gridDim.x) {
         const SkItem it = sk_decode(p, item);
         for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
           const int buf = acc_iter % NACC;
           const uint32_t use = acc_iter / NACC;
+          const long long w1 = p.trace ? clock64() : 0;
           mbar_wait(&tempty[buf], (use & 1) ^ 1);
+          if (p.trace) acc_wait += clock64() - w1;
           tc_fence_after();
           const uint32_t d = tmem_base + buf * MT;
-          const int nch = sk_chunks(p, t);
+          const int nch = sk_chunks<KS>(p, t);
           for (int c = 0; c < nch; ++c) {
+            const long long w0 = p.trace ? clock64() : 0;
             mbar_wait(&full[stage], phase);
+            if (p.trace) full_wait += clock64() - w0;
             tc_fence_after();
+            if (item == blockIdx.x && t == it.t_begin && c == 0) SK_TRACE(4);
             const uint32_t w_base = smem_u32(sW + stage * W_STAGE);
             const uint32_t x_base = smem_u32(sX + stage * X_STAGE);
 #pragma unroll
-            for (int kk = 0; kk < SK_KSTAGE / 16; ++kk) {
-              // A = W: MN-major SW128, two 64-column atoms 8 KB apart (LBO), 8-row K
+            for (int kk = 0; kk < KS / 16; ++kk) {
+              // A = W: MN-major SW128, two 64-column atoms W_ATOM apart (LBO), 8-row K
               // groups 1 KB apart (SBO), +16 K rows (2 KB) per step.
-              const uint64_t adesc = umma_desc_sw128(w_base + kk * 2048, SK_W_ATOM, 1024);
-              // B = X: K-major SW128, +32 B per 16-element K step inside the 128 B row.
-              const uint64_t bdesc = umma_desc_sw128(x_base + kk * 32, 16, 1024);
+              uint64_t adesc;
+              if constexpr (BNW == 32)  // SW64 MN-major: one 32-column atom (LBO 0), +1 KB per step
+                adesc = (umma_desc_sw128(w_base + kk * 1024, 0, 512) & ~(uint64_t{7} << 61)) | (uint64_t{4} << 61);
+              else
+                adesc = umma_desc_sw128(w_base + kk * 2048, W_ATOM, 1024);
+              // B = X: K-major SW128, one box per 64 K, +32 B per 16-element K step
+              // inside the 128 B row.
+              const uint64_t bdesc = umma_desc_sw128(x_base + (kk >> 2) * X_BOX + (kk & 3) * 32, 16, 1024);
               umma_bf16(d, adesc, bdesc, IDESC, (c | kk) != 0 ? 1u : 0u);
             }
             umma_commit(&empty[stage]);
@@ -276,6 +328,11 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
           }
           umma_commit(&tfull[buf]);
         }
+      }
+      SK_TRACE(5);
+      if (p.trace) {
+        p.trace[blockIdx.x * 16 + 10] = static_cast<unsigned long long>(full_wait);
+        p.trace[blockIdx.x * 16 + 11] = static_cast<unsigned long long>(acc_wait);
       }
     }
     __syncwarp();
@@ -288,7 +345,8 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
     for (long long item = blockIdx.x; item < p.items; item += gridDim.x) {
       const SkItem it = sk_decode(p, item);
       const int n = it.n0 + q * LPQ + lane;
-      const bool lane_ok = lane < LPQ;  // BNW = 64: lanes 16-31 of a quarter hold no row
+      // BNW = 64: lanes 16-31 of a quarter hold no row; BNW = 32: nor quarters 2-3
+      const bool lane_ok = lane < LPQ && q * LPQ < BNW;
       int t_in_group = 0;
       uint32_t groups_done = 0;
       for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
@@ -345,11 +403,19 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
         }
       }
       // g: this unit's value for column n, tokens h0 .. h0 + TPW - 1
+      if (warp == 4 && lane == 0) SK_TRACE(6);
       if (p.units == 1) {
+        // Straight-line code that runs once per tile: each store is a predicate, a
+        // store and a pointer bump (the tail's instructions are fetched cold, so
+        // their count is what costs: ~14 per store with per-token index math).
         if (lane_ok && n < p.N) {
+          const int mlim = p.M - h0;
+          float* dst = p.out + static_cast<size_t>(h0) * p.ldo + n;
 #pragma unroll
-          for (int m = 0; m < TPW; ++m)
-            if (h0 + m < p.M) p.out[static_cast<size_t>(h0 + m) * p.ldo + n] = g[m];
+          for (int m = 0; m < TPW; ++m) {
+            if (m < mlim) *dst = g[m];
+            dst += p.ldo;
+          }
         }
       } else {
         // cluster mode (one item per CTA): publish the unit value in shared memory
@@ -370,7 +436,11 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
   //             for subtree units, k_first for leaf units)
   //   result  = contiguous-halves tree over the groups (binary counter, new + old)
   // -- the order of tree_combine_kernel (tbik_tree.cu) and of the reference.
-  cluster_sync_all();
+  if (warp == 4 && lane == 0) SK_TRACE(7);
+  // (a lone CTA needs no cluster barrier: its release fence waits for every
+  // outstanding global store, ~1000 cycles)
+  if (p.units > 1) cluster_sync_all();
+  if (threadIdx.x == 0) SK_TRACE(8);
   if (p.units > 1) {
     // work items: (row, 4-column quad) of this CTA's row slice, 16-byte DSMEM loads
     // from every unit, spread over all warps (their roles are done), two items in
@@ -439,7 +509,9 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
       }
     }
   }
-  cluster_sync_all();  // peers may still read this CTA's shared memory
+  if (p.units > 1) cluster_sync_all();  // peers may still read this CTA's shared memory
+  if (threadIdx.x == 0) SK_TRACE(9);
+#undef SK_TRACE
 
   tc_fence_before();
   __syncthreads();
@@ -449,6 +521,27 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
   }
 }
 
+
+struct SkKernel {
+  void (*kern)(const CUtensorMap, const CUtensorMap, const SkParams);
+  size_t smem;
+  int threads;
+};
+template <int MT, int BNW, int KS>
+SkKernel sk_entry() {
+  return SkKernel{tc_skinny_kernel<MT, BNW, KS>, sk_smem<MT, BNW, KS>(), sk_threads<MT>()};
+}
+template <int BNW, int KS>
+SkKernel sk_select_mt(int mt) {
+  static_assert(sk_stages<128, BNW, KS>() >= 3, "skinny stages");
+  return mt == 16 ? sk_entry<16, BNW, KS>() : mt == 32 ? sk_entry<32, BNW, KS>()
+       : mt == 64 ? sk_entry<64, BNW, KS>() : sk_entry<128, BNW, KS>();
+}
+SkKernel sk_select(int mt, int bn, int ks) {
+  if (bn == 128) return ks == 128 ? sk_select_mt<128, 128>(mt) : sk_select_mt<128, 64>(mt);
+  if (bn == 32) return ks == 128 ? sk_select_mt<32, 128>(mt) : sk_select_mt<32, 64>(mt);
+  return ks == 128 ? sk_select_mt<64, 128>(mt) : sk_select_mt<64, 64>(mt);
+}
 
 }  // namespace
 
@@ -479,14 +572,25 @@ tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaSt
   p.T = static_cast<int>(v.T);
   p.out = C;
   p.ldo = ldc;
+  // Diagnostics (schedule knob sk_trace = 1): per-CTA phase clocks, their means
+  // printed to stderr after each call (synchronises the stream).
+  const bool trace = knob(KNOB_SK_TRACE, 0) != 0;
+  static unsigned long long* trace_buf = nullptr;
+  if (trace && !trace_buf && cudaMalloc(&trace_buf, 4096 * 16 * 8) != cudaSuccess) trace_buf = nullptr;
+  p.trace = trace ? trace_buf : nullptr;
   const int64_t want = static_cast<int64_t>(sms) * 7 / 8;
   // Tile width: 64-column tiles (MMA M = 64) when 128-column tiles cover at most
   // half the SMs even with the deepest K split -- short K (TP shards) at decode
   // sizes (measured, tools/decode_bench.py: TP=4 shard M >= 64 -11..16 %, TP=8
   // -2..5 %; TP=1/2 stay faster with 128 columns and K units).
-  int bn = (v.N + SK_BN - 1) / SK_BN * std::min<int64_t>(v.L, SK_MAX_UNITS) <= want / 2 ? 64 : SK_BN;
+  // (32-column tiles -- MMA M = 64 over a repeated 32-column atom -- are a knob
+  // only: a CTA's time is its MMA count (~37 cycles per M = 64 MMA however narrow
+  // the tile, tools/micro/small_mma.cu), so twice the CTAs did not help the TP = 8
+  // shard: 6.9 vs 6.7 us.)
+  const int64_t kunits = std::min<int64_t>(v.L, SK_MAX_UNITS);
+  int bn = (v.N + SK_BN - 1) / SK_BN * kunits <= want / 2 ? 64 : SK_BN;
   const int force_bn = static_cast<int>(knob(KNOB_SK_BN, 0));  // tuning knob (same bits)
-  if (force_bn == 64 || force_bn == 128) bn = force_bn;
+  if (force_bn == 32 || force_bn == 64 || force_bn == 128) bn = force_bn;
   p.bn = bn;
   p.ntiles = static_cast<int>((v.N + bn - 1) / bn);
   // Units: aligned 2^j-group subtrees (<= 8, one cluster) until the items cover
@@ -524,30 +628,35 @@ tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaSt
     p.log_groups = lg;
   }
   p.items = static_cast<long long>(p.ntiles) * p.units;
+  if (p.items >= (int64_t{1} << 31)) return TBIK_UNSUPPORTED;
   TBIK_TRY(pad_operand(&v.A, &v.lda, v.M, v.K, 8, s));
   TBIK_TRY(pad_operand(&v.B, &v.ldb, v.K, v.N, 9, s));
+  // K rows per stage: 128 (one 16 KB W box per 64 columns) whenever the leaf is a
+  // multiple of 128; knob sk_ks = 64 restores 64-row boxes (same bits: the MMA
+  // sequence per leaf is unchanged).
+  int ks = v.bk % 128 == 0 ? 128 : 64;
+  const int force_ks = static_cast<int>(knob(KNOB_SK_KS, 0));
+  if (force_ks == 64 || (force_ks == 128 && v.bk % 128 == 0)) ks = force_ks;
   CUtensorMap mW, mX;
-  TBIK_TRY(tc_make_map_2d(&mW, v.B, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.K),
-                          static_cast<uint64_t>(v.ldb) * 2, 64, SK_KSTAGE));
+  if (bn == 32)
+    TBIK_TRY(tc_make_map_2d_sw64(&mW, v.B, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.K),
+                                 static_cast<uint64_t>(v.ldb) * 2, 32, static_cast<uint32_t>(ks)));
+  else
+    TBIK_TRY(tc_make_map_2d(&mW, v.B, static_cast<uint64_t>(v.N), static_cast<uint64_t>(v.K),
+                            static_cast<uint64_t>(v.ldb) * 2, 64, static_cast<uint32_t>(ks)));
   TBIK_TRY(tc_make_map_2d(&mX, v.A, static_cast<uint64_t>(v.K), static_cast<uint64_t>(v.M),
                           static_cast<uint64_t>(v.lda) * 2, SK_KSTAGE, static_cast<uint32_t>(mt)));
-  using Kern = void (*)(const CUtensorMap, const CUtensorMap, const SkParams);
-  const Kern kern = bn == 128 ? (mt == 16 ? tc_skinny_kernel<16, 128> : mt == 32 ? tc_skinny_kernel<32, 128>
-                                 : mt == 64 ? tc_skinny_kernel<64, 128> : tc_skinny_kernel<128, 128>)
-                              : (mt == 16 ? tc_skinny_kernel<16, 64> : mt == 32 ? tc_skinny_kernel<32, 64>
-                                 : mt == 64 ? tc_skinny_kernel<64, 64> : tc_skinny_kernel<128, 64>);
-  const size_t smem = bn == 128 ? (mt == 16 ? sk_smem<16, 128>() : mt == 32 ? sk_smem<32, 128>()
-                                   : mt == 64 ? sk_smem<64, 128>() : sk_smem<128, 128>())
-                                : (mt == 16 ? sk_smem<16, 64>() : mt == 32 ? sk_smem<32, 64>()
-                                   : mt == 64 ? sk_smem<64, 64>() : sk_smem<128, 64>());
-  const int threads = mt == 16 ? sk_threads<16>() : mt == 32 ? sk_threads<32>() : mt == 64 ? sk_threads<64>()
-                                                                                          : sk_threads<128>();
-  static bool attr_set[16][4][2] = {};
-  const int mi = mt == 16 ? 0 : mt == 32 ? 1 : mt == 64 ? 2 : 3, bi = bn == 128 ? 1 : 0;
-  if (dev >= 0 && dev < 16 && !attr_set[dev][mi][bi]) {
-    TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr_set[dev][mi][bi] = true;
+  const SkKernel sel = sk_select(mt, bn, ks);
+  static bool attr_set[16][4][3][2] = {};
+  const int mi = mt == 16 ? 0 : mt == 32 ? 1 : mt == 64 ? 2 : 3, bi = bn == 128 ? 2 : bn == 64 ? 1 : 0,
+            ki = ks == 128 ? 1 : 0;
+  if (dev >= 0 && dev < 16 && !attr_set[dev][mi][bi][ki]) {
+    TBIK_CUDA(cudaFuncSetAttribute(sel.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sel.smem)));
+    attr_set[dev][mi][bi][ki] = true;
   }
+  const size_t smem = sel.smem;
+  const int threads = sel.threads;
+  const auto kern = sel.kern;
   // X = 1: persistent over tiles; X > 1: one CTA per (tile, unit), clusters of X.
   const long long grid = p.units > 1 ? p.items : (p.items < sms ? p.items : sms);
   cudaLaunchConfig_t lc{};
@@ -555,16 +664,38 @@ tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaSt
   lc.blockDim = dim3(static_cast<unsigned>(threads));
   lc.dynamicSmemBytes = smem;
   lc.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(p.units);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // Programmatic dependent launch (knob sk_pdl = 0 turns it off): the prologue
+  // overlaps the previous kernel when that kernel triggers its dependents.
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
-  lc.numAttrs = 1;
+  lc.numAttrs = knob(KNOB_SK_PDL, 1) != 0 ? 2 : 1;
   TBIK_CUDA(cudaLaunchKernelEx(&lc, kern, mW, mX, p));
   TBIK_CUDA(cudaGetLastError());
   count_launch("tc_skinny_kernel");
+  if (p.trace && grid <= 4096) {
+    std::vector<unsigned long long> h(static_cast<size_t>(grid) * 16);
+    TBIK_CUDA(cudaStreamSynchronize(s));
+    TBIK_CUDA(cudaMemcpy(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost));
+    double mean[16] = {0};
+    unsigned long long g_lo = ~0ull, g_hi = 0;
+    for (long long b = 0; b < grid; ++b) {
+      for (int i = 1; i < 12; ++i) mean[i] += static_cast<double>(h[b * 16 + i]) / static_cast<double>(grid);
+      g_lo = std::min(g_lo, h[b * 16 + 15]);
+      g_hi = std::max(g_hi, h[b * 16 + 15]);
+    }
+    std::fprintf(stderr,
+                 "sk_trace grid %lld ks %d bn %d mt %d | setup %.0f tma0 %.0f mma0 %.0f tma_end %.0f mma_end %.0f "
+                 "merge_end %.0f out_end %.0f csync %.0f exit %.0f clk | mma waits: data %.0f acc %.0f | CTA start "
+                 "spread %llu ns\n",
+                 grid, ks, bn, mt, mean[1], mean[2], mean[4], mean[3], mean[5], mean[6], mean[7], mean[8], mean[9],
+                 mean[10], mean[11], g_hi - g_lo);
+  }
   return TBIK_OK;
 }
 

@@ -94,13 +94,16 @@ enum Knob {
   KNOB_SK_MT,            // skinny token tile 32/64/128
   KNOB_SK_UNITS,         // skinny K units
   KNOB_SK_LEAF,          // 1: skinny single-leaf units
-  KNOB_SK_BN,            // skinny weight tile 64/128
+  KNOB_SK_BN,            // skinny weight tile 32/64/128
   KNOB_FMA_V1,           // 1: the first FMA-leaf kernel
   KNOB_GROUP_FUSED,      // 0: no fused GEMM + all-reduce kernel
   KNOB_GROUP_OVERLAP,    // 0: no chunked GEMM / all-reduce overlap
   KNOB_AR_TWO_PHASE_BYTES,  // payload bytes from which the group all-reduce is two-phase
   KNOB_TC_WIDE,          // 0: 256 x 128 tiles, 1: 256 x 192 tiles (tbik_gemm_tc_w192.cu)
   KNOB_TC_WIDE_TAIL,     // 0: no half items in the wide kernels' last wave
+  KNOB_SK_KS,            // skinny K rows per stage / W box: 64 or 128
+  KNOB_SK_PDL,           // 0: skinny kernel without programmatic dependent launch
+  KNOB_SK_TRACE,         // 1: skinny phase clocks to stderr (diagnostics)
   KNOB_COUNT
 };
 int64_t knob(Knob k, int64_t dflt);

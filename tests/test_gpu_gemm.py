@@ -295,7 +295,7 @@ def test_errors(tb, cuda):
 SCHEDULES = [{}, {"tc_group_m": 1}, {"tc_group_m": 3, "tc_units": 2}, {"tc_pair": 0}, {"tc_pair": 0, "tc_units": 4},
              {"tc_pair": 1}, {"tc_abox": 32}, {"tc_abox": 64, "tc_pair": 1}, {"tc_deep": 1}, {"tc_deep": 0},
              {"tc_acc4": 0}, {"tc_skinny": 0}, {"sk_units": 1}, {"sk_units": 2, "sk_leaf": 0}, {"sk_units": 8},
-             {"sk_bn": 64}, {"sk_mt": 128}]
+             {"sk_bn": 64}, {"sk_bn": 32}, {"sk_mt": 128}]
 
 
 @pytest.mark.parametrize("M,K,N", [(300, 14336, 640), (64, 4096, 512), (513, 6144, 384), (20, 4096, 200),
@@ -323,7 +323,8 @@ def test_tc_schedules_invisible(tb, cuda, orc, M, K, N, monkeypatch):
 # kernel for every token-width class, unit split, leaf split and TP shard view
 @pytest.mark.parametrize("M,K,N", [(1, 14336, 4096), (16, 14336, 640), (17, 4096, 1000), (33, 6144, 384),
                                    (64, 25600, 256), (65, 14336, 512), (128, 8192, 256), (5, 777, 300),
-                                   (16, 4096, 40000)])  # > 148 tiles: persistent CTAs over several tiles
+                                   (16, 4096, 40000),  # > 148 tiles: persistent CTAs over several tiles
+                                   (16, 1792, 333), (100, 1792, 4098)])  # row strides not a multiple of 4
 def test_skinny_matches_wide(tb, cuda, M, K, N, monkeypatch):
     torch.manual_seed(1000 + M)
     x = torch.randn(M, K, device=cuda).to(torch.bfloat16)
@@ -332,11 +333,13 @@ def test_skinny_matches_wide(tb, cuda, M, K, N, monkeypatch):
     with tb.schedule(tc_skinny=0):
         ref = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
     L = tb.plan_blocks(K, cfg, 1).leaves
-    for bn in (128, 64):  # 128-column tiles (MMA M = 128) / 64-column tiles (M = 64)
+    for bn in (128, 64, 32):  # 128-column tiles (MMA M = 128) / 64 (M = 64) / 32 (M = 64, half used)
         for u in [-1] + [u for u in (1, 2, 4, 8) if u <= L]:
-            with tb.schedule(tc_skinny=1, sk_bn=bn, sk_units=u):
-                y = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
-            assert torch.equal(y.view(torch.int32), ref.view(torch.int32)), f"skinny bn={bn} units={u} changed the bits"
+            for ks in (128, 64):  # K rows per stage / W box
+                with tb.schedule(tc_skinny=1, sk_bn=bn, sk_units=u, sk_ks=ks):
+                    y = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+                assert torch.equal(y.view(torch.int32), ref.view(torch.int32)), \
+                    f"skinny bn={bn} units={u} ks={ks} changed the bits"
 
 
 @pytest.mark.parametrize("leaf_split", ["0", "1"])

@@ -49,7 +49,9 @@ for M in Ms:
     y = torch.empty(M, N, device="cuda")
     yb = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     out = [f"M={M:4d}"]
-    for name, knobs in (("wide", {"tc_skinny": 0}), ("skinny", {"tc_skinny": 1})):
+    for name, knobs in (("wide", {"tc_skinny": 0}), ("skinny", {"tc_skinny": 1}),
+                        ("skinny ks64", {"tc_skinny": 1, "sk_ks": 64}),
+                        ("skinny nopdl", {"tc_skinny": 1, "sk_pdl": 0})):
         f = lambda i: tb.tree_matmul(x, ws[i], cfg, tb.LEAF_TCGEN05, out=y)  # noqa: E731
         with tb.schedule(**knobs):
             c, st = cold(f), stream(f)
@@ -77,8 +79,13 @@ for tp in (1, 2, 4, 8):
                             ("sk_noleaf", {"tc_skinny": 1, "sk_leaf": 0}),
                             ("sk_u2", {"tc_skinny": 1, "sk_units": 2, "sk_leaf": 0}),
                             ("sk_u4", {"tc_skinny": 1, "sk_units": 4, "sk_leaf": 0}),
+                            ("sk_bn32", {"tc_skinny": 1, "sk_bn": 32}),
                             ("sk_bn64", {"tc_skinny": 1, "sk_bn": 64}),
-                            ("sk_bn128", {"tc_skinny": 1, "sk_bn": 128})):
+                            ("sk_bn128", {"tc_skinny": 1, "sk_bn": 128}),
+                            ("sk_ks64", {"tc_skinny": 1, "sk_ks": 64}),
+                            ("sk_bn64_ks64", {"tc_skinny": 1, "sk_bn": 64, "sk_ks": 64}),
+                            ("sk_bn128_ks64", {"tc_skinny": 1, "sk_bn": 128, "sk_ks": 64}),
+                            ("sk_nopdl", {"tc_skinny": 1, "sk_pdl": 0})):
             f = lambda i: tb.tree_matmul(x, wsh[i], cfg_s, tb.LEAF_TCGEN05, out=y)  # noqa: E731
             with tb.schedule(**knobs):
                 st = graph_time_20(f)

@@ -1,0 +1,10 @@
+#!/bin/bash
+# r02: skinny kernel phase clocks (TBIK_SK_TRACE) on decode shards.
+mkdir -p gpurun_out
+( for ks in 64 128; do
+  for shape in "16 1792 4096 7" "128 1792 4096 7" "16 14336 4096 0" "16 3584 4096 7"; do
+    echo "== ks=$ks shape=$shape"
+    timeout 120 python tools/prof_decode.py $shape 4 --knob sk_ks=$ks --knob sk_trace=1 2>&1 | grep sk_trace | tail -2
+  done
+done ) > gpurun_out/r02_sk_trace.txt 2>&1
+cat gpurun_out/r02_sk_trace.txt

@@ -35,6 +35,19 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, uint64_t*
       : "memory");
 }
 
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// 3D mode (transposed == 2): one box {64 cols, rows, cols / 64} covers the strip's
+// 64-column slabs of `rows` rows in one TMA instruction.
+// X mode (transposed == 3): the strip is a token block X[M = cols][K] streamed in
+// K: {64 K, M rows} boxes (boxes_per_stage of them per stage), or (transposed == 4)
+// one 3D box {64 K, M rows, boxes_per_stage} per stage.
 // One thread streams the strip: keeps NST box loads in flight, consumes in order.
 __global__ void ingest(const __grid_constant__ CUtensorMap tm, int K, int cols, int boxes_per_stage, int nst,
                        int rows, int transposed, unsigned long long* cyc) {
@@ -52,7 +65,9 @@ __global__ void ingest(const __grid_constant__ CUtensorMap tm, int K, int cols, 
   for (; issued < nst && issued < nk; ++issued) {
     mbar_expect(&full[issued], stage_bytes);
     for (int b = 0; b < boxes_per_stage; ++b)
-      if (transposed)  // [N][K]: inner = K (rows of the strip's box), outer = N
+      if (transposed == 2) {
+        if (b == 0) tma3d(sm + issued * stage_bytes, &tm, &full[issued], 0, issued * rows, n0 / 64);
+      } else if (transposed == 1)  // [N][K]: inner = K (rows of the strip's box), outer = N
         tma2d(sm + issued * stage_bytes + b * box_bytes, &tm, &full[issued], issued * rows, n0 + b * (cols / boxes_per_stage));
       else
         tma2d(sm + issued * stage_bytes + b * box_bytes, &tm, &full[issued], n0 + b * (cols / boxes_per_stage), issued * rows);
@@ -64,7 +79,9 @@ __global__ void ingest(const __grid_constant__ CUtensorMap tm, int K, int cols, 
       const int si = issued % nst;
       mbar_expect(&full[si], stage_bytes);
       for (int b = 0; b < boxes_per_stage; ++b)
-        if (transposed)
+        if (transposed == 2) {
+          if (b == 0) tma3d(sm + si * stage_bytes, &tm, &full[si], 0, issued * rows, n0 / 64);
+        } else if (transposed == 1)
           tma2d(sm + si * stage_bytes + b * box_bytes, &tm, &full[si], issued * rows, n0 + b * (cols / boxes_per_stage));
         else
           tma2d(sm + si * stage_bytes + b * box_bytes, &tm, &full[si], n0 + b * (cols / boxes_per_stage), issued * rows);
@@ -87,9 +104,10 @@ int main() {
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
   EncFn enc = reinterpret_cast<EncFn>(fn);
+  EncFn enc3 = enc;
   unsigned long long* dc;
   cudaMalloc(&dc, 8 * 512);
-  cudaFuncSetAttribute(ingest, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+  cudaFuncSetAttribute(ingest, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
   struct V { int cols, boxes, nst, rows, tr; CUtensorMapSwizzle sw; const char* name; };
   std::vector<V> vs = {{64, 1, 16, 64, 0, CU_TENSOR_MAP_SWIZZLE_128B, "[K][N] 64-col strips, 64-row boxes"},
                        {32, 1, 16, 64, 0, CU_TENSOR_MAP_SWIZZLE_64B, "[K][N] 32-col strips, 64B rows"},
@@ -97,7 +115,23 @@ int main() {
                        {64, 1, 16, 32, 0, CU_TENSOR_MAP_SWIZZLE_128B, "[K][N] 64-col strips, 32-row boxes"},
                        {64, 1, 8, 128, 0, CU_TENSOR_MAP_SWIZZLE_128B, "[K][N] 64-col strips, 128-row boxes"},
                        {64, 1, 16, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B, "[N][K] 64-row strips, 64-K boxes"},
-                       {32, 1, 16, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B, "[N][K] 32-row strips, 64-K boxes"}};
+                       {32, 1, 16, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B, "[N][K] 32-row strips, 64-K boxes"},
+                       // in-flight depth: latency- or service-bound?
+                       {64, 1, 4, 64, 0, CU_TENSOR_MAP_SWIZZLE_128B, "64-row boxes, NST 4"},
+                       {64, 1, 8, 64, 0, CU_TENSOR_MAP_SWIZZLE_128B, "64-row boxes, NST 8"},
+                       {64, 1, 24, 64, 0, CU_TENSOR_MAP_SWIZZLE_128B, "64-row boxes, NST 24"},
+                       {64, 1, 8, 32, 0, CU_TENSOR_MAP_SWIZZLE_128B, "32-row boxes, NST 8"},
+                       {64, 1, 32, 32, 0, CU_TENSOR_MAP_SWIZZLE_128B, "32-row boxes, NST 32"},
+                       {64, 1, 48, 32, 0, CU_TENSOR_MAP_SWIZZLE_128B, "32-row boxes, NST 48"},
+                       {64, 1, 4, 128, 0, CU_TENSOR_MAP_SWIZZLE_128B, "128-row boxes, NST 4"},
+                       {64, 1, 12, 128, 0, CU_TENSOR_MAP_SWIZZLE_128B, "128-row boxes, NST 12"},
+                       {64, 1, 4, 256, 0, CU_TENSOR_MAP_SWIZZLE_128B, "256-row boxes, NST 4"},
+                       {64, 1, 6, 256, 0, CU_TENSOR_MAP_SWIZZLE_128B, "256-row boxes, NST 6"},
+                       {32, 1, 8, 256, 0, CU_TENSOR_MAP_SWIZZLE_64B, "32-col strips, 256-row boxes, NST 8"},
+                       {32, 1, 7, 256, 0, CU_TENSOR_MAP_SWIZZLE_64B, "32-col strips, 256-row boxes, NST 7"},
+                       {128, 2, 8, 64, 2, CU_TENSOR_MAP_SWIZZLE_128B, "128-col strips, one 3D box {64,64,2}"},
+                       {128, 2, 4, 128, 2, CU_TENSOR_MAP_SWIZZLE_128B, "128-col strips, one 3D box {64,128,2}"},
+                       {256, 4, 4, 64, 2, CU_TENSOR_MAP_SWIZZLE_128B, "256-col strips, one 3D box {64,64,4}"}};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -105,11 +139,19 @@ int main() {
     CUtensorMap m;
     cuuint64_t dims[2] = {cuuint64_t(N), cuuint64_t(K)}, str[1] = {cuuint64_t(N) * 2};
     cuuint32_t box[2] = {cuuint32_t(v.cols / v.boxes), cuuint32_t(v.rows)}, es[2] = {1, 1};
-    if (v.tr) {  // the same bytes viewed as W^T: [N][K], K contiguous
+    if (v.tr == 2) {  // {64 cols, K rows, N / 64 slabs}: slab stride 128 B
+      cuuint64_t d3[3] = {64, cuuint64_t(K), cuuint64_t(N / 64)}, s3[2] = {cuuint64_t(N) * 2, 128};
+      cuuint32_t b3[3] = {64, cuuint32_t(v.rows), cuuint32_t(v.boxes)}, e3[3] = {1, 1, 1};
+      if (enc3(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, d3, s3, b3, e3, CU_TENSOR_MAP_INTERLEAVE_NONE, v.sw,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        printf("encode3 failed\n");
+        return 1;
+      }
+    } else if (v.tr) {  // the same bytes viewed as W^T: [N][K], K contiguous
       dims[0] = K; dims[1] = N; str[0] = cuuint64_t(K) * 2;
       box[0] = cuuint32_t(v.rows); box[1] = cuuint32_t(v.cols / v.boxes);
     }
-    if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, v.sw,
+    if (v.tr != 2 && enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, v.sw,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
       printf("encode failed\n");
       return 1;
