@@ -182,6 +182,83 @@ __device__ __forceinline__ int sk_chunks(const SkParams& p, int t) {
   return (kh + KS - 1) / KS;
 }
 
+// In-cluster finish of a K-split tile (see the kernel).  UNITS > 0: a compile-time
+// unit count, so the once-per-CTA code holds only what this split runs (its
+// instructions are fetched cold); UNITS = 0: any count <= SK_MAX_UNITS.
+template <int UNITS, int BNW>
+__device__ __forceinline__ void sk_finish(const SkParams& p, const uint8_t* sW) {
+  constexpr int UMAX = UNITS > 0 ? UNITS : SK_MAX_UNITS;
+  const int nu = UNITS > 0 ? UNITS : p.units;
+  // work items: (row, 4-column quad) of this CTA's row slice, 16-byte DSMEM loads
+  // from every unit, spread over all warps (their roles are done), two items in
+  // flight per thread
+  const int tid = threadIdx.x;
+  const int unit = static_cast<int>(blockIdx.x % nu);
+  const int n0 = static_cast<int>(blockIdx.x / nu) * BNW;
+  const int R = (p.M + nu - 1) / nu;
+  const int m_lo = unit * R, m_hi = min(p.M, m_lo + R);
+  const int nitems = (m_hi > m_lo ? m_hi - m_lo : 0) * (BNW / 4);
+  const uint32_t fb = smem_u32(sW);
+  uint32_t peer[UMAX];
+#pragma unroll
+  for (int x = 0; x < UMAX; ++x) peer[x] = x < nu ? dsmem_map(fb, static_cast<uint32_t>(x)) : 0u;
+#pragma unroll 2
+  for (int idx = tid; idx < nitems; idx += static_cast<int>(blockDim.x)) {
+    const int m = m_lo + idx / (BNW / 4);
+    const int c4 = (idx % (BNW / 4)) * 4;
+    const uint32_t off = static_cast<uint32_t>((m * BNW + c4) * 4);
+    float4 vals[UMAX];
+#pragma unroll
+    for (int x = 0; x < UMAX; ++x)
+      vals[x] = x < nu ? dsmem_ld_f32x4(peer[x] + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float res[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      // level-0 fold over `fold` consecutive values, then the contiguous-halves
+      // tree over the groups (binary counter, new + old)
+      float stack[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      float acc = 0.0f;
+      int gcount = 0, in_fold = 0;
+#pragma unroll
+      for (int x = 0; x < UMAX; ++x) {
+        if (x < nu) {
+          const float vx = j == 0 ? vals[x].x : j == 1 ? vals[x].y : j == 2 ? vals[x].z : vals[x].w;
+          acc = __fadd_rn(acc, vx);
+          if (++in_fold == p.fold) {
+            float v = acc;
+            int l = 0;
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+              if (((gcount >> b) & 1) && l == b) {
+                v = __fadd_rn(v, stack[b]);
+                l = b + 1;
+              }
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              if (l == b) stack[b] = v;
+            ++gcount;
+            in_fold = 0;
+            acc = 0.0f;
+          }
+        }
+      }
+      res[j] = stack[0];
+#pragma unroll
+      for (int b = 1; b < 4; ++b)
+        if (b == p.log_groups) res[j] = stack[b];
+    }
+    const int n = n0 + c4;
+    float* dst = p.out + static_cast<size_t>(m) * p.ldo + n;
+    if (n + 3 < p.N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+      *reinterpret_cast<float4*>(dst) = make_float4(res[0], res[1], res[2], res[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (n + j < p.N) dst[j] = res[j];
+    }
+  }
+}
+
 template <int MT, int BNW, int KS>
 __global__ void __launch_bounds__(sk_threads<MT>(), 1)
     tc_skinny_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
@@ -441,74 +518,10 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
   // outstanding global store, ~1000 cycles)
   if (p.units > 1) cluster_sync_all();
   if (threadIdx.x == 0) SK_TRACE(8);
-  if (p.units > 1) {
-    // work items: (row, 4-column quad) of this CTA's row slice, 16-byte DSMEM loads
-    // from every unit, spread over all warps (their roles are done), two items in
-    // flight per thread
-    const int tid = threadIdx.x;
-    const int unit = static_cast<int>(blockIdx.x % p.units);
-    const int n0 = static_cast<int>(blockIdx.x / p.units) * BNW;
-    const int R = (p.M + p.units - 1) / p.units;
-    const int m_lo = unit * R, m_hi = min(p.M, m_lo + R);
-    const int nitems = (m_hi > m_lo ? m_hi - m_lo : 0) * (BNW / 4);
-    const uint32_t fb = smem_u32(sW);
-    uint32_t peer[SK_MAX_UNITS];
-#pragma unroll
-    for (int x = 0; x < SK_MAX_UNITS; ++x) peer[x] = x < p.units ? dsmem_map(fb, static_cast<uint32_t>(x)) : 0u;
-#pragma unroll 2
-    for (int idx = tid; idx < nitems; idx += static_cast<int>(blockDim.x)) {
-      const int m = m_lo + idx / (BNW / 4);
-      const int c4 = (idx % (BNW / 4)) * 4;
-      const uint32_t off = static_cast<uint32_t>((m * BNW + c4) * 4);
-      float4 vals[SK_MAX_UNITS];
-#pragma unroll
-      for (int x = 0; x < SK_MAX_UNITS; ++x)
-        vals[x] = x < p.units ? dsmem_ld_f32x4(peer[x] + off) : make_float4(0.f, 0.f, 0.f, 0.f);
-      float res[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float stack[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-        float acc = 0.0f;
-        int gcount = 0, in_fold = 0;
-#pragma unroll
-        for (int x = 0; x < SK_MAX_UNITS; ++x) {
-          if (x < p.units) {
-            const float vx = j == 0 ? vals[x].x : j == 1 ? vals[x].y : j == 2 ? vals[x].z : vals[x].w;
-            acc = __fadd_rn(acc, vx);
-            if (++in_fold == p.fold) {
-              float v = acc;
-              int l = 0;
-#pragma unroll
-              for (int b = 0; b < 3; ++b)
-                if (((gcount >> b) & 1) && l == b) {
-                  v = __fadd_rn(v, stack[b]);
-                  l = b + 1;
-                }
-#pragma unroll
-              for (int b = 0; b < 4; ++b)
-                if (l == b) stack[b] = v;
-              ++gcount;
-              in_fold = 0;
-              acc = 0.0f;
-            }
-          }
-        }
-        res[j] = stack[0];
-#pragma unroll
-        for (int b = 1; b < 4; ++b)
-          if (b == p.log_groups) res[j] = stack[b];
-      }
-      const int n = n0 + c4;
-      float* dst = p.out + static_cast<size_t>(m) * p.ldo + n;
-      if (n + 3 < p.N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-        *reinterpret_cast<float4*>(dst) = make_float4(res[0], res[1], res[2], res[3]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (n + j < p.N) dst[j] = res[j];
-      }
-    }
-  }
+  if (p.units == 2) sk_finish<2, BNW>(p, sW);
+  else if (p.units == 4) sk_finish<4, BNW>(p, sW);
+  else if (p.units == 8) sk_finish<8, BNW>(p, sW);
+  else if (p.units > 1) sk_finish<0, BNW>(p, sW);
   if (p.units > 1) cluster_sync_all();  // peers may still read this CTA's shared memory
   if (threadIdx.x == 0) SK_TRACE(9);
 #undef SK_TRACE
