@@ -83,11 +83,19 @@ template <int BNW, int KS = 64>
 constexpr int sk_w_stage() { return BNW * KS * 2; }
 template <int MT, int KS = 64>
 constexpr int sk_x_stage() { return MT * 128 * (KS / 64); }
+// Pair mode (MT <= 64): the finishing CTA receives its partner's prefix fold,
+// [BNW columns][MT tokens] f32.
+constexpr int SK_PAIR_MAX_MT = 64;
+template <int MT, int BNW>
+constexpr int sk_prefix_bytes() { return MT <= SK_PAIR_MAX_MT ? BNW * MT * 4 : 0; }
 template <int MT, int BNW = 128, int KS = 64>
-constexpr int sk_stages() { return (SK_SMEM_LIMIT - 2048) / (sk_w_stage<BNW, KS>() + sk_x_stage<MT, KS>()); }
+constexpr int sk_stages() {
+  return (SK_SMEM_LIMIT - 2048 - sk_prefix_bytes<MT, BNW>()) / (sk_w_stage<BNW, KS>() + sk_x_stage<MT, KS>());
+}
 template <int MT, int BNW = 128, int KS = 64>
 constexpr size_t sk_smem() {
-  return 1024 + static_cast<size_t>(sk_stages<MT, BNW, KS>()) * (sk_w_stage<BNW, KS>() + sk_x_stage<MT, KS>()) + 512;
+  return 1024 + static_cast<size_t>(sk_stages<MT, BNW, KS>()) * (sk_w_stage<BNW, KS>() + sk_x_stage<MT, KS>()) +
+         sk_prefix_bytes<MT, BNW>() + 512;
 }
 static_assert(sk_smem<16>() <= SK_SMEM_LIMIT && sk_smem<32>() <= SK_SMEM_LIMIT && sk_smem<64>() <= SK_SMEM_LIMIT &&
                   sk_smem<128>() <= SK_SMEM_LIMIT && sk_smem<16, 64>() <= SK_SMEM_LIMIT &&
@@ -103,6 +111,7 @@ struct SkParams {
   int bk, kf, T;
   int ntiles;
   int units;           // X: values per tile handed to the finish (1 = the item's value is final)
+  int pair;            // 1: a tile's single leaf group split over a CTA pair (units = 2, see the kernel)
   int tiles_per_unit;  // leaves per unit
   int levels;          // tree levels inside a unit (log2 of its groups; 0 for leaf units)
   int fold;            // finish: level-0 fold length over unit values (kf for leaf units, else 1)
@@ -283,11 +292,13 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
   uint8_t* sX = sW + NST * W_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sX + NST * X_STAGE);
+  float* sPre = reinterpret_cast<float*>(sX + NST * X_STAGE);  // pair mode: partner's prefix
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + NST * X_STAGE + sk_prefix_bytes<MT, BNW>());
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + NACC;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
+  uint64_t* pre_full = tempty + NACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pre_full + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -311,13 +322,20 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], NMW);  // every merge warp
     }
+    mbar_init(pre_full, 1);
     fence_barrier_init();
+    // pair mode, finishing CTA: the partner's prefix arrives by st.async
+    if (p.pair && (blockIdx.x & 1)) mbar_arrive_expect_tx(pre_full, static_cast<uint32_t>(sk_prefix_bytes<MT, BNW>()));
   }
   if (warp == 2) tmem_alloc(tmem_slot, SK_TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // pair mode: the partner's barrier must be initialised before the leading CTA
+  // writes to it -- arrive now (relaxed: nothing to publish but the barrier
+  // init, fenced above), wait only right before the remote stores.
+  if (p.pair) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   // Programmatic dependent launch: the prologue above (barriers, TMEM, descriptor
   // prefetch, instruction fetch) may overlap the previous kernel's tail; operands
   // and the output are touched only after that kernel has completed (a no-op when
@@ -424,6 +442,52 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
       const int n = it.n0 + q * LPQ + lane;
       // BNW = 64: lanes 16-31 of a quarter hold no row; BNW = 32: nor quarters 2-3
       const bool lane_ok = lane < LPQ && q * LPQ < BNW;
+      if constexpr (MT <= SK_PAIR_MAX_MT) {
+        if (p.pair && it.unit == 1) {
+          // Pair mode, finishing CTA: its leaves (<= NACC, one accumulator each,
+          // kept in TMEM) continue the partner's prefix fold in leaf order:
+          // ((prefix + l_a) + l_a+1) + ... -- the sequential level-0 fold of the
+          // group (matmul.cpp:101-103), split at a leaf boundary.
+          const int nl = it.t_end - it.t_begin;
+          for (int j = 0; j < nl; ++j) mbar_wait(&tfull[j], 0);
+          tc_fence_after();
+          mbar_wait(pre_full, 0);
+          // (lanes past the tile's columns read column 0: in bounds, never stored)
+          const float4* pre = reinterpret_cast<const float4*>(sPre + (lane_ok ? q * LPQ + lane : 0) * MT + h0);
+#pragma unroll
+          for (int m = 0; m < TPW; m += 4) {
+            const float4 v = pre[m / 4];
+            g[m] = v.x;
+            g[m + 1] = v.y;
+            g[m + 2] = v.z;
+            g[m + 3] = v.w;
+          }
+#pragma unroll
+          for (int j = 0; j < NACC; ++j) {
+            if (j < nl) {
+              uint32_t r[NCH][16];
+#pragma unroll
+              for (int c = 0; c < NCH; ++c) tmem_ld16r(lane_base + j * MT + c * 16, r[c]);
+#pragma unroll
+              for (int c = 0; c < NCH; ++c) tmem_wait_ld16_dep(r[c]);
+#pragma unroll
+              for (int c = 0; c < NCH; ++c)
+#pragma unroll
+                for (int i = 0; i < 16; ++i) g[c * 16 + i] = __fadd_rn(g[c * 16 + i], __uint_as_float(r[c][i]));
+            }
+          }
+          if (lane_ok && n < p.N) {
+            const int mlim = p.M - h0;
+            float* dst = p.out + static_cast<size_t>(h0) * p.ldo + n;
+#pragma unroll
+            for (int m = 0; m < TPW; ++m) {
+              if (m < mlim) *dst = g[m];
+              dst += p.ldo;
+            }
+          }
+          continue;
+        }
+      }
       int t_in_group = 0;
       uint32_t groups_done = 0;
       for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
@@ -481,7 +545,25 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
       }
       // g: this unit's value for column n, tokens h0 .. h0 + TPW - 1
       if (warp == 4 && lane == 0) SK_TRACE(6);
-      if (p.units == 1) {
+      if (MT <= SK_PAIR_MAX_MT && p.pair) {
+        // Pair mode, leading CTA: g is the prefix fold of the group's first leaves;
+        // hand it to the partner ([column][token] f32) with asynchronous remote
+        // stores that complete on the partner's barrier -- no cluster barrier.
+        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+        if (lane_ok) {
+          const uint32_t dst =
+              dsmem_map(smem_u32(sPre) + static_cast<uint32_t>(((q * LPQ + lane) * MT + h0) * 4), (blockIdx.x & 1u) ^ 1u);
+          const uint32_t bar = dsmem_map(smem_u32(pre_full), (blockIdx.x & 1u) ^ 1u);
+#pragma unroll
+          for (int m = 0; m < TPW; m += 4)
+            asm volatile(
+                "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                    dst + m * 4),
+                "r"(__float_as_uint(g[m])), "r"(__float_as_uint(g[m + 1])), "r"(__float_as_uint(g[m + 2])),
+                "r"(__float_as_uint(g[m + 3])), "r"(bar)
+                : "memory");
+        }
+      } else if (p.units == 1) {
         // Straight-line code that runs once per tile: each store is a predicate, a
         // store and a pointer bump (the tail's instructions are fetched cold, so
         // their count is what costs: ~14 per store with per-token index math).
@@ -516,13 +598,14 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
   if (warp == 4 && lane == 0) SK_TRACE(7);
   // (a lone CTA needs no cluster barrier: its release fence waits for every
   // outstanding global store, ~1000 cycles)
-  if (p.units > 1) cluster_sync_all();
+  if (p.units > 1 && !p.pair) cluster_sync_all();
   if (threadIdx.x == 0) SK_TRACE(8);
-  if (p.units == 2) sk_finish<2, BNW>(p, sW);
+  if (p.pair) {
+  } else if (p.units == 2) sk_finish<2, BNW>(p, sW);
   else if (p.units == 4) sk_finish<4, BNW>(p, sW);
   else if (p.units == 8) sk_finish<8, BNW>(p, sW);
   else if (p.units > 1) sk_finish<0, BNW>(p, sW);
-  if (p.units > 1) cluster_sync_all();  // peers may still read this CTA's shared memory
+  if (p.units > 1 && !p.pair) cluster_sync_all();  // peers may still read this CTA's shared memory
   if (threadIdx.x == 0) SK_TRACE(9);
 #undef SK_TRACE
 
@@ -639,6 +722,22 @@ tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaSt
     int lg = 0;
     while ((int64_t{1} << lg) < units) ++lg;
     p.log_groups = lg;
+  }
+  // Pair mode: a tile with a single leaf group (the TP = 8 shard) and no K units
+  // runs on two CTAs -- the leading one folds the group's first leaves, the other
+  // computes the last <= NACC leaves and continues the fold from the prefix it is
+  // sent (same order, same bits).  Each CTA issues about half the small MMAs that
+  // bound it (profiles/r02_skinny_decode.md).  Knob sk_pair = 0 turns it off.
+  const int nacc = mt >= 128 ? 2 : 4;
+  if (knob(KNOB_SK_PAIR, 1) != 0 && !leaf_units && units == 1 && v.L == 1 && mt <= SK_PAIR_MAX_MT && v.T >= 2 &&
+      2 * static_cast<int64_t>(p.ntiles) <= sms) {
+    const int t1 = std::min<int>(static_cast<int>(v.T) / 2, nacc);
+    p.pair = 1;
+    p.units = 2;
+    p.tiles_per_unit = static_cast<int>(v.T) - t1;
+    p.levels = 0;
+    p.fold = 1;
+    p.log_groups = 1;
   }
   p.items = static_cast<long long>(p.ntiles) * p.units;
   if (p.items >= (int64_t{1} << 31)) return TBIK_UNSUPPORTED;

@@ -342,6 +342,24 @@ def test_skinny_matches_wide(tb, cuda, M, K, N, monkeypatch):
                     f"skinny bn={bn} units={u} ks={ks} changed the bits"
 
 
+@pytest.mark.parametrize("M,K,N,kf", [(16, 1792, 4096, 7), (1, 1792, 4096, 7), (5, 512, 1000, 2), (32, 768, 333, 3),
+                                      (16, 777, 640, 4), (16, 4096, 512, 16), (17, 2048, 4098, 8), (64, 1792, 4096, 7),
+                                      (50, 1280, 700, 5), (128, 1792, 1024, 7)])
+def test_skinny_pair_split(tb, cuda, M, K, N, kf):
+    """A tile's single leaf group split over a CTA pair (prefix fold handed over by
+    st.async, the partner continues the fold) == one CTA == the wide kernel."""
+    torch.manual_seed(K + N)
+    x = torch.randn(M, K, device=cuda).to(torch.bfloat16)
+    w = torch.randn(K, N, device=cuda).to(torch.bfloat16)
+    cfg = tb.BlockConfig(64, 256, 128, kf)
+    with tb.schedule(tc_skinny=0):
+        ref = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+    for knobs in ({"sk_pair": 1}, {"sk_pair": 0}, {"sk_pair": 1, "sk_ks": 64}, {"sk_pair": 1, "sk_bn": 128}):
+        with tb.schedule(tc_skinny=1, **knobs):
+            y = tb.tree_matmul(x, w, cfg, tb.LEAF_TCGEN05)
+        assert torch.equal(y.view(torch.int32), ref.view(torch.int32)), f"{knobs} changed the bits"
+
+
 @pytest.mark.parametrize("leaf_split", ["0", "1"])
 def test_skinny_tp_shards(tb, cuda, leaf_split, monkeypatch):
     """Row-parallel TP shards at decode size through the skinny kernel (single-leaf

@@ -85,7 +85,8 @@ for tp in (1, 2, 4, 8):
                             ("sk_ks64", {"tc_skinny": 1, "sk_ks": 64}),
                             ("sk_bn64_ks64", {"tc_skinny": 1, "sk_bn": 64, "sk_ks": 64}),
                             ("sk_bn128_ks64", {"tc_skinny": 1, "sk_bn": 128, "sk_ks": 64}),
-                            ("sk_nopdl", {"tc_skinny": 1, "sk_pdl": 0})):
+                            ("sk_nopdl", {"tc_skinny": 1, "sk_pdl": 0}),
+                            ("sk_nopair", {"tc_skinny": 1, "sk_pair": 0})):
             f = lambda i: tb.tree_matmul(x, wsh[i], cfg_s, tb.LEAF_TCGEN05, out=y)  # noqa: E731
             with tb.schedule(**knobs):
                 st = graph_time_20(f)
