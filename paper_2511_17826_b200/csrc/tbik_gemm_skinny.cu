@@ -111,7 +111,8 @@ struct SkParams {
   int bk, kf, T;
   int ntiles;
   int units;           // X: values per tile handed to the finish (1 = the item's value is final)
-  int pair;            // 1: a tile's single leaf group split over a CTA pair (units = 2, see the kernel)
+  int pair;            // CTA-pair handoff instead of the cluster finish (units = 2, see the kernel):
+                       // 1 = one leaf group split at a leaf, 2 = two subtree units
   int tiles_per_unit;  // leaves per unit
   int levels;          // tree levels inside a unit (log2 of its groups; 0 for leaf units)
   int fold;            // finish: level-0 fold length over unit values (kf for leaf units, else 1)
@@ -443,8 +444,8 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
       // BNW = 64: lanes 16-31 of a quarter hold no row; BNW = 32: nor quarters 2-3
       const bool lane_ok = lane < LPQ && q * LPQ < BNW;
       if constexpr (MT <= SK_PAIR_MAX_MT) {
-        if (p.pair && it.unit == 1) {
-          // Pair mode, finishing CTA: its leaves (<= NACC, one accumulator each,
+        if (p.pair == 1 && it.unit == 1) {
+          // Pair mode 1, finishing CTA: its leaves (<= NACC, one accumulator each,
           // kept in TMEM) continue the partner's prefix fold in leaf order:
           // ((prefix + l_a) + l_a+1) + ... -- the sequential level-0 fold of the
           // group (matmul.cpp:101-103), split at a leaf boundary.
@@ -545,10 +546,33 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
       }
       // g: this unit's value for column n, tokens h0 .. h0 + TPW - 1
       if (warp == 4 && lane == 0) SK_TRACE(6);
-      if (MT <= SK_PAIR_MAX_MT && p.pair) {
-        // Pair mode, leading CTA: g is the prefix fold of the group's first leaves;
-        // hand it to the partner ([column][token] f32) with asynchronous remote
-        // stores that complete on the partner's barrier -- no cluster barrier.
+      if (MT <= SK_PAIR_MAX_MT && p.pair == 2 && it.unit == 1) {
+        // Pair mode 2, finishing CTA: the tile is the two-leaf tree of the units'
+        // subtree values, (0 + v1) + (0 + v0) -- the cluster finish's order.
+        mbar_wait(pre_full, 0);
+        const float4* pre = reinterpret_cast<const float4*>(sPre + (lane_ok ? q * LPQ + lane : 0) * MT + h0);
+#pragma unroll
+        for (int m = 0; m < TPW; m += 4) {
+          const float4 v = pre[m / 4];
+          g[m] = __fadd_rn(__fadd_rn(0.0f, g[m]), __fadd_rn(0.0f, v.x));
+          g[m + 1] = __fadd_rn(__fadd_rn(0.0f, g[m + 1]), __fadd_rn(0.0f, v.y));
+          g[m + 2] = __fadd_rn(__fadd_rn(0.0f, g[m + 2]), __fadd_rn(0.0f, v.z));
+          g[m + 3] = __fadd_rn(__fadd_rn(0.0f, g[m + 3]), __fadd_rn(0.0f, v.w));
+        }
+        if (lane_ok && n < p.N) {
+          const int mlim = p.M - h0;
+          float* dst = p.out + static_cast<size_t>(h0) * p.ldo + n;
+#pragma unroll
+          for (int m = 0; m < TPW; ++m) {
+            if (m < mlim) *dst = g[m];
+            dst += p.ldo;
+          }
+        }
+      } else if (MT <= SK_PAIR_MAX_MT && p.pair) {
+        // Pair mode, leading CTA: g is its value (mode 1: the prefix fold of the
+        // group's first leaves; mode 2: its subtree); hand it to the partner
+        // ([column][token] f32) with asynchronous remote stores that complete on
+        // the partner's barrier -- no cluster barrier.
         asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
         if (lane_ok) {
           const uint32_t dst =
@@ -738,6 +762,11 @@ tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaSt
     p.levels = 0;
     p.fold = 1;
     p.log_groups = 1;
+  } else if (knob(KNOB_SK_PAIR, 1) != 0 && !leaf_units && units == 2 && mt <= 32) {
+    // two subtree units: the second adds the first's value (no cluster finish);
+    // not above 32 tokens, where one CTA storing every row measured slower than
+    // the finish split over both (TP = 4 shard M = 64: 11.1 vs 10.8 us)
+    p.pair = 2;
   }
   p.items = static_cast<long long>(p.ntiles) * p.units;
   if (p.items >= (int64_t{1} << 31)) return TBIK_UNSUPPORTED;

@@ -344,10 +344,13 @@ def test_skinny_matches_wide(tb, cuda, M, K, N, monkeypatch):
 
 @pytest.mark.parametrize("M,K,N,kf", [(16, 1792, 4096, 7), (1, 1792, 4096, 7), (5, 512, 1000, 2), (32, 768, 333, 3),
                                       (16, 777, 640, 4), (16, 4096, 512, 16), (17, 2048, 4098, 8), (64, 1792, 4096, 7),
-                                      (50, 1280, 700, 5), (128, 1792, 1024, 7)])
+                                      (50, 1280, 700, 5), (128, 1792, 1024, 7),
+                                      (16, 3584, 4096, 7), (64, 3584, 1024, 7), (3, 2560, 900, 5)])  # two groups: mode 2
 def test_skinny_pair_split(tb, cuda, M, K, N, kf):
-    """A tile's single leaf group split over a CTA pair (prefix fold handed over by
-    st.async, the partner continues the fold) == one CTA == the wide kernel."""
+    """CTA-pair handoffs (st.async into the partner's shared memory, no cluster
+    finish): a tile's single leaf group split at a leaf (the partner continues the
+    fold) or two subtree units (the partner adds) == one CTA / the cluster finish ==
+    the wide kernel."""
     torch.manual_seed(K + N)
     x = torch.randn(M, K, device=cuda).to(torch.bfloat16)
     w = torch.randn(K, N, device=cuda).to(torch.bfloat16)
