@@ -61,9 +61,11 @@ constexpr int SK_SMEM_LIMIT = 232448;
 constexpr int SK_MAX_UNITS = 8;
 constexpr int SK_MAX_M = 128;    // tokens = MMA N (16 / 32 / 64 / 128)  // K-split units = CTAs of one cluster (portable cluster size)
 
-// Tokens per merge thread (TPW) and merge warps (4 lane quarters x MT / TPW).
+// Tokens per merge thread (TPW) and merge warps (4 lane quarters x MT / TPW):
+// <= 32 tokens per thread, so the per-tile tail (fold, stores) is spread over
+// MT / 8 warps (TPW = 64 measured slower at M = 64 / 128).
 template <int MT>
-constexpr int sk_tpw() { return MT > 64 ? 64 : MT; }
+constexpr int sk_tpw() { return MT > 32 ? 32 : MT; }
 template <int MT>
 constexpr int sk_merge_warps() { return 4 * (MT / sk_tpw<MT>()); }
 template <int MT>
@@ -84,10 +86,12 @@ constexpr int sk_w_stage() { return BNW * KS * 2; }
 template <int MT, int KS = 64>
 constexpr int sk_x_stage() { return MT * 128 * (KS / 64); }
 // Pair mode (MT <= 64): the finishing CTA receives its partner's prefix fold,
-// [BNW columns][MT tokens] f32.
-constexpr int SK_PAIR_MAX_MT = 64;
+// [BNW columns][MT tokens] f32.  (At MT = 128 -- two accumulators, so a 5 + 2
+// leaf split, 4 stages -- it measured slower: TP = 8 shard 11.2 vs 9.9 us.)
 template <int MT, int BNW>
-constexpr int sk_prefix_bytes() { return MT <= SK_PAIR_MAX_MT ? BNW * MT * 4 : 0; }
+constexpr bool sk_pair_ok() { return MT <= 64; }
+template <int MT, int BNW>
+constexpr int sk_prefix_bytes() { return sk_pair_ok<MT, BNW>() ? BNW * MT * 4 : 0; }
 template <int MT, int BNW = 128, int KS = 64>
 constexpr int sk_stages() {
   return (SK_SMEM_LIMIT - 2048 - sk_prefix_bytes<MT, BNW>()) / (sk_w_stage<BNW, KS>() + sk_x_stage<MT, KS>());
@@ -443,7 +447,7 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
       const int n = it.n0 + q * LPQ + lane;
       // BNW = 64: lanes 16-31 of a quarter hold no row; BNW = 32: nor quarters 2-3
       const bool lane_ok = lane < LPQ && q * LPQ < BNW;
-      if constexpr (MT <= SK_PAIR_MAX_MT) {
+      if constexpr (sk_pair_ok<MT, BNW>()) {
         if (p.pair == 1 && it.unit == 1) {
           // Pair mode 1, finishing CTA: its leaves (<= NACC, one accumulator each,
           // kept in TMEM) continue the partner's prefix fold in leaf order:
@@ -546,7 +550,7 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
       }
       // g: this unit's value for column n, tokens h0 .. h0 + TPW - 1
       if (warp == 4 && lane == 0) SK_TRACE(6);
-      if (MT <= SK_PAIR_MAX_MT && p.pair == 2 && it.unit == 1) {
+      if (sk_pair_ok<MT, BNW>() && p.pair == 2 && it.unit == 1) {
         // Pair mode 2, finishing CTA: the tile is the two-leaf tree of the units'
         // subtree values, (0 + v1) + (0 + v0) -- the cluster finish's order.
         mbar_wait(pre_full, 0);
@@ -568,7 +572,7 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
             dst += p.ldo;
           }
         }
-      } else if (MT <= SK_PAIR_MAX_MT && p.pair) {
+      } else if (sk_pair_ok<MT, BNW>() && p.pair) {
         // Pair mode, leading CTA: g is its value (mode 1: the prefix fold of the
         // group's first leaves; mode 2: its subtree); hand it to the partner
         // ([column][token] f32) with asynchronous remote stores that complete on
@@ -753,7 +757,7 @@ tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaSt
   // sent (same order, same bits).  Each CTA issues about half the small MMAs that
   // bound it (profiles/r02_skinny_decode.md).  Knob sk_pair = 0 turns it off.
   const int nacc = mt >= 128 ? 2 : 4;
-  if (knob(KNOB_SK_PAIR, 1) != 0 && !leaf_units && units == 1 && v.L == 1 && mt <= SK_PAIR_MAX_MT && v.T >= 2 &&
+  if (knob(KNOB_SK_PAIR, 1) != 0 && !leaf_units && units == 1 && v.L == 1 && mt <= 64 && v.T >= 2 &&
       2 * static_cast<int64_t>(p.ntiles) <= sms) {
     const int t1 = std::min<int>(static_cast<int>(v.T) / 2, nacc);
     p.pair = 1;
