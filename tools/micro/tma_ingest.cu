@@ -5,6 +5,10 @@
 //   strip 32 cols,  64B swizzle -> 128 CTAs x 115 KB  (half the bytes per CTA, 64-byte rows)
 //   strip 128 cols as 2 x 64    -> 32 CTAs x 458 KB
 // Question: is a CTA's ingest bound by bytes or by TMA row requests?
+// Finding (profiles/r02_tma_ingest.txt): ~520-600 cycles per ring stage whatever
+// its bytes (4-32 KB), box count or in-flight depth -- a property of this one-
+// thread wait-then-reissue loop, not of TMA: the skinny kernel streams the same
+// strips twice as fast (its bound is the MMA count, tools/micro/small_mma.cu).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o tma_ingest tma_ingest.cu -lcuda
 #include <cuda.h>
 #include <cuda_runtime.h>
