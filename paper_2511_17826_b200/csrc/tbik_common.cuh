@@ -103,6 +103,12 @@ __device__ __forceinline__ uint32_t bf16x2_bits(float lo, float hi) {
 }
 
 // ---- PTX wrappers ------------------------------------------------------------
+// Programmatic dependent launch: let the next kernel of the stream (if it is
+// launched with the attribute -- the tcgen05 GEMMs) be scheduled now; it runs its
+// prologue on SMs this grid frees and waits (griddepcontrol.wait) for this grid's
+// completion before touching memory.  A no-op for kernels without PDL dependents.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -356,6 +356,11 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch (knob tc_pdl; not for the fused all-reduce form):
+  // operands, scratch and output are touched only after the previous kernel has
+  // completed; dependents may launch once every CTA got here.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
 
   if (warp < 4) {
   if (warp == 0) {
@@ -1111,13 +1116,15 @@ tbik_status launch_tc_gemm(const GemmView& v_in, const GemmOut& o, cudaStream_t 
   lc.blockDim = dim3(nthreads);
   lc.dynamicSmemBytes = smem;
   lc.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = pair ? 2 : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
-  lc.numAttrs = 1;
+  lc.numAttrs = !ar_on && knob(KNOB_TC_PDL, 1) != 0 ? 2 : 1;
   TBIK_CUDA(cudaLaunchKernelEx(&lc, kern, mA, mB, mC, p));
   count_launch(ar_on ? "tc_tree_gemm_kernel (fused all-reduce)" : "tc_tree_gemm_kernel");
   return TBIK_OK;

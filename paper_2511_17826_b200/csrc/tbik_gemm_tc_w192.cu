@@ -254,6 +254,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch (knob tc_pdl): the prologue above overlaps the
+  // previous kernel's tail; operands, scratch and output are touched only after
+  // it has completed.  Dependents may launch once every CTA got here (the grid is
+  // co-resident), to run their own prologue on the SMs this grid frees.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
@@ -751,13 +757,15 @@ tbik_status launch_tc_w192(const GemmView& v, const GemmOut& o, cudaStream_t s) 
   lc.blockDim = dim3(NTHREADS);
   lc.dynamicSmemBytes = SMEM_BYTES;
   lc.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
-  lc.numAttrs = 1;
+  lc.numAttrs = knob(KNOB_TC_PDL, 1) != 0 ? 2 : 1;
   TBIK_CUDA(cudaLaunchKernelEx(&lc, kern, mA, mB, mBh, mC, p));
   count_launch("tc_w192_tree_gemm_kernel");
   return TBIK_OK;

@@ -24,6 +24,7 @@ __device__ __forceinline__ float bf(uint16_t b) { return bf16_bits_to_f32(b); }
 // ---- embedding gather -------------------------------------------------------------
 __global__ void embed_kernel(const uint16_t* __restrict__ table, int64_t H, const int64_t* __restrict__ ids,
                              int64_t V, uint16_t* __restrict__ out, int* __restrict__ bad) {
+  pdl_trigger();
   const int64_t row = blockIdx.x;
   const int64_t id = ids[row];
   if (id < 0 || id >= V) {  // flagged; the row is zeroed so the output stays defined
@@ -44,6 +45,7 @@ __global__ void embed_kernel(const uint16_t* __restrict__ table, int64_t H, cons
 __global__ void rope_kernel(const float* __restrict__ x, int64_t ldx, int64_t col0, int heads, int D,
                             const int* __restrict__ pos, const float* __restrict__ cos_t,
                             const float* __restrict__ sin_t, uint16_t* __restrict__ out, int64_t ldo) {
+  pdl_trigger();
   const int64_t row = blockIdx.x;
   const int p = pos[row];
   const int half = D / 2;
@@ -70,6 +72,7 @@ __global__ void rope_vec_kernel(const float* __restrict__ x, int64_t ldx, int64_
                                 const int* __restrict__ pos, const float* __restrict__ cos_t,
                                 const float* __restrict__ sin_t, uint16_t* __restrict__ out, int64_t ldo,
                                 int64_t rows) {
+  pdl_trigger();
   const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
   if (row >= rows) return;
   const int half = D / 2, qpr = half / 4;  // float4 quads per half head
@@ -102,6 +105,7 @@ __global__ void rope_vec_kernel(const float* __restrict__ x, int64_t ldx, int64_
 // f32 -> bf16 copy of a column block (V of qkv, storage casts).
 __global__ void cast_kernel(const float* __restrict__ x, int64_t ldx, int64_t cols, uint16_t* __restrict__ out,
                             int64_t ldo) {
+  pdl_trigger();
   const int64_t row = blockIdx.y;
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < cols;
        j += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -131,6 +135,7 @@ __global__ void __launch_bounds__(4 * AQ, 3) attn2_kernel(const uint16_t* __rest
                                                     const uint16_t* __restrict__ k, int64_t ldk,
                                                     const uint16_t* __restrict__ v, int64_t ldv, int S, int nq,
                                                     int nkv, float scale, uint16_t* __restrict__ out, int64_t ldo) {
+  pdl_trigger();
   extern __shared__ float sm[];
   float* kv = sm;                // [AK][AKP]
   float* P = sm + AK * AKP;      // [AQ][S + 1]
@@ -337,6 +342,7 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const uint16_t* __restric
                                                        const uint16_t* __restrict__ v, int64_t ldv, int S, int nq,
                                                        int nkv, float scale_log2, uint16_t* __restrict__ out,
                                                        int64_t ldo) {
+  pdl_trigger();
   extern __shared__ __align__(16) uint16_t fsm[];  // [2 buffers][K block, V block]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -496,6 +502,7 @@ __device__ __forceinline__ uint16_t silu_mul1(float z, float up) { return tb_sil
 // fused gate_up GEMM (tbik_tree_matmul_silu_mul) when its epilogue cannot run.
 __global__ void silu_mul_il_kernel(const float* __restrict__ gu, int64_t ld, int64_t I, uint16_t* __restrict__ out,
                                    int64_t ldo) {
+  pdl_trigger();
   const int64_t row = blockIdx.y;
   const float* g = gu + row * ld;
   uint16_t* o = out + row * ldo;
@@ -508,6 +515,7 @@ __global__ void silu_mul_il_kernel(const float* __restrict__ gu, int64_t ld, int
 template <bool VEC>
 __global__ void silu_mul_kernel(const float* __restrict__ gu, int64_t ld, int64_t I, uint16_t* __restrict__ out,
                                 int64_t ldo) {
+  pdl_trigger();
   const int64_t row = blockIdx.y;
   const float* g = gu + row * ld;
   uint16_t* o = out + row * ldo;
@@ -530,6 +538,7 @@ __global__ void silu_mul_kernel(const float* __restrict__ gu, int64_t ld, int64_
 template <bool VEC>
 __global__ void residual_kernel(uint16_t* __restrict__ h, int64_t ldh, const float* __restrict__ f, int64_t ldf,
                                 int64_t cols) {
+  pdl_trigger();
   const int64_t row = blockIdx.y;
   uint16_t* hr = h + row * ldh;
   const float* fr = f + row * ldf;

@@ -136,6 +136,7 @@ template <typename TX, typename TY, bool VEC>
 __global__ void __launch_bounds__(LANES) tree_rmsnorm_kernel(const TX* __restrict__ X, int64_t ldx,
                                                              const float* __restrict__ gamma, float eps,
                                                              TY* __restrict__ Y, int64_t ldy, int64_t cols) {
+  pdl_trigger();
   __shared__ float sh[9];
   constexpr int CH = 16 / sizeof(TX);  // 8 bf16 or 4 f32 per chunk
   constexpr int CACHE = 4;
@@ -222,6 +223,7 @@ __global__ void __launch_bounds__(LANES) residual_rmsnorm_kernel(uint16_t* __res
                                                                  const float* __restrict__ F, int64_t ldf,
                                                                  const float* __restrict__ gamma, float eps,
                                                                  uint16_t* __restrict__ Y, int64_t ldy, int64_t cols) {
+  pdl_trigger();
   __shared__ float sh[9];
   constexpr int CH = 8;
   constexpr int CACHE = 4;
@@ -301,6 +303,7 @@ template <bool FROM_STATES, bool VEC>
 __global__ void __launch_bounds__(LANES) ms_group_kernel(const float* __restrict__ logits, int64_t ld, int64_t n,
                                                          const float2* __restrict__ chunks, int64_t ld_chunks,
                                                          int64_t groups, MS* __restrict__ out) {
+  pdl_trigger();
   extern __shared__ MS ms_buf[];  // 2 x nc states (ping-pong)
   const int64_t row = blockIdx.x, g = blockIdx.y;
   const int nc = static_cast<int>((n + TB_MS_CHUNK - 1) / TB_MS_CHUNK);
@@ -336,6 +339,7 @@ __global__ void __launch_bounds__(LANES) ms_group_kernel(const float* __restrict
 template <bool VEC>
 __global__ void chunk_states_kernel(const float* __restrict__ logits, int64_t ld, int64_t n, int64_t groups,
                                     float2* __restrict__ out, int64_t ld_out) {
+  pdl_trigger();
   const int64_t row = blockIdx.y;
   const int64_t nc = (n + TB_MS_CHUNK - 1) / TB_MS_CHUNK;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < groups * nc;
@@ -390,6 +394,7 @@ __global__ void finish_kernel(const float* __restrict__ logits, int64_t ld, int6
                               const float* __restrict__ lse, float* __restrict__ logprobs, int64_t ld_out,
                               const int64_t* __restrict__ targets, int64_t v_offset, float* __restrict__ tlp,
                               bool vec) {
+  pdl_trigger();
   const int64_t row = blockIdx.y;
   const float l = lse[row];
   if (logprobs) {

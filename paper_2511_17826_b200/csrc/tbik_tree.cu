@@ -43,6 +43,7 @@ __device__ __forceinline__ void tree_push(float (&stack)[kMaxTreeLevels][VEC], u
 __global__ void tree_combine_kernel(const float* __restrict__ ws, int64_t X, int64_t fold,
                                     int64_t rows, int64_t cols, int64_t slice, float* __restrict__ out,
                                     int64_t ldo) {
+  pdl_trigger();
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= rows * cols) return;
   const int64_t r = e / cols, c = e - r * cols;
@@ -68,6 +69,7 @@ __global__ void tree_combine_kernel(const float* __restrict__ ws, int64_t X, int
 template <int X>
 __global__ void tree_combine_vec_kernel(const float* __restrict__ ws, int64_t rows, int64_t cols, int64_t slice,
                                         float* __restrict__ out, int64_t ldo) {
+  pdl_trigger();
   const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t cq = cols / 4;
   if (q >= rows * cq) return;
