@@ -9,6 +9,8 @@
 
 #include <string>
 
+#include <utility>
+
 #include "tbik_b200.h"
 
 namespace tbik_b200 {
@@ -108,6 +110,28 @@ __device__ __forceinline__ uint32_t bf16x2_bits(float lo, float hi) {
 // prologue on SMs this grid frees and waits (griddepcontrol.wait) for this grid's
 // completion before touching memory.  A no-op for kernels without PDL dependents.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+// First statement of a kernel launched by launch_pdl: nothing before it reads or
+// writes global memory (returns at once for a launch without the attribute).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Launch with programmatic stream serialisation: the kernel's CTAs may be
+// scheduled while the previous kernel (one that triggers its dependents, e.g. the
+// tcgen05 GEMMs) finishes; the kernel must begin with pdl_wait().
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, kernel, std::forward<Args>(args)...);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

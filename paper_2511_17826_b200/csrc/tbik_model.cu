@@ -24,6 +24,7 @@ __device__ __forceinline__ float bf(uint16_t b) { return bf16_bits_to_f32(b); }
 // ---- embedding gather -------------------------------------------------------------
 __global__ void embed_kernel(const uint16_t* __restrict__ table, int64_t H, const int64_t* __restrict__ ids,
                              int64_t V, uint16_t* __restrict__ out, int* __restrict__ bad) {
+  pdl_wait();
   pdl_trigger();
   const int64_t row = blockIdx.x;
   const int64_t id = ids[row];
@@ -72,6 +73,7 @@ __global__ void rope_vec_kernel(const float* __restrict__ x, int64_t ldx, int64_
                                 const int* __restrict__ pos, const float* __restrict__ cos_t,
                                 const float* __restrict__ sin_t, uint16_t* __restrict__ out, int64_t ldo,
                                 int64_t rows) {
+  pdl_wait();
   pdl_trigger();
   const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
   if (row >= rows) return;
@@ -105,6 +107,7 @@ __global__ void rope_vec_kernel(const float* __restrict__ x, int64_t ldx, int64_
 // f32 -> bf16 copy of a column block (V of qkv, storage casts).
 __global__ void cast_kernel(const float* __restrict__ x, int64_t ldx, int64_t cols, uint16_t* __restrict__ out,
                             int64_t ldo) {
+  pdl_wait();
   pdl_trigger();
   const int64_t row = blockIdx.y;
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < cols;
@@ -135,6 +138,7 @@ __global__ void __launch_bounds__(4 * AQ, 3) attn2_kernel(const uint16_t* __rest
                                                     const uint16_t* __restrict__ k, int64_t ldk,
                                                     const uint16_t* __restrict__ v, int64_t ldv, int S, int nq,
                                                     int nkv, float scale, uint16_t* __restrict__ out, int64_t ldo) {
+  pdl_wait();
   pdl_trigger();
   extern __shared__ float sm[];
   float* kv = sm;                // [AK][AKP]
@@ -342,6 +346,7 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const uint16_t* __restric
                                                        const uint16_t* __restrict__ v, int64_t ldv, int S, int nq,
                                                        int nkv, float scale_log2, uint16_t* __restrict__ out,
                                                        int64_t ldo) {
+  pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) uint16_t fsm[];  // [2 buffers][K block, V block]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -629,8 +634,9 @@ tbik_status tbik_rope(const float* x, int64_t ldx, int64_t col0, int heads, int 
     const int threads = heads * head_dim / 8;
     const int tx = threads < 256 ? ((threads + 31) / 32) * 32 : 256;
     const int ty = 256 / tx;
-    rope_vec_kernel<<<static_cast<unsigned>((rows + ty - 1) / ty), dim3(tx, ty), 0, static_cast<cudaStream_t>(stream)>>>(
-        x, ldx, col0, heads, head_dim, positions, cos_table, sin_table, static_cast<uint16_t*>(out), ldo, rows);
+    TBIK_CUDA(launch_pdl(rope_vec_kernel, dim3(static_cast<unsigned>((rows + ty - 1) / ty)), dim3(tx, ty), 0,
+                         static_cast<cudaStream_t>(stream), x, ldx, col0, heads, head_dim, positions, cos_table,
+                         sin_table, static_cast<uint16_t*>(out), ldo, rows));
   } else {
     rope_kernel<<<static_cast<unsigned>(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         x, ldx, col0, heads, head_dim, positions, cos_table, sin_table, static_cast<uint16_t*>(out), ldo);
@@ -645,8 +651,8 @@ tbik_status tbik_cast_bf16(const float* x, int64_t ldx, int64_t rows, int64_t co
   if (!x || !out) return set_error(TBIK_BAD_ARGUMENT, "null argument");
   if (rows < 1 || cols < 1 || rows > 65535) return set_error(TBIK_BAD_DIMENSION, "cast: bad dimensions");
   TBIK_TRY(need_device());
-  cast_kernel<<<row_grid(rows, cols, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      x, ldx, cols, static_cast<uint16_t*>(out), ldo);
+  TBIK_CUDA(launch_pdl(cast_kernel, row_grid(rows, cols, 256), dim3(256), 0, static_cast<cudaStream_t>(stream), x, ldx,
+                       cols, static_cast<uint16_t*>(out), ldo));
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;
@@ -670,9 +676,10 @@ tbik_status tbik_attention_prefill(const void* q, int64_t ldq, const void* k, in
   TBIK_CUDA(cudaFuncSetAttribute(attn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   dim3 grid(static_cast<unsigned>(n_q_heads), static_cast<unsigned>(batch),
             static_cast<unsigned>((seq_len + AQ - 1) / AQ));
-  attn2_kernel<<<grid, 4 * AQ, smem, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint16_t*>(q), ldq, static_cast<const uint16_t*>(k), ldk, static_cast<const uint16_t*>(v), ldv,
-      seq_len, n_q_heads, n_kv_heads, scale, static_cast<uint16_t*>(out), ldo);
+  TBIK_CUDA(launch_pdl(attn2_kernel, grid, dim3(4 * AQ), smem, static_cast<cudaStream_t>(stream),
+                       static_cast<const uint16_t*>(q), ldq, static_cast<const uint16_t*>(k), ldk,
+                       static_cast<const uint16_t*>(v), ldv, seq_len, n_q_heads, n_kv_heads, scale,
+                       static_cast<uint16_t*>(out), ldo));
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;
@@ -695,9 +702,10 @@ tbik_status tbik_attention_prefill_tc(const void* q, int64_t ldq, const void* k,
             static_cast<unsigned>((seq_len + FQ - 1) / FQ));
   constexpr size_t fsmem = 2 * 2 * FSTAGE * sizeof(uint16_t);
   TBIK_CUDA(cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem)));
-  attn_mma_kernel<<<grid, 128, fsmem, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint16_t*>(q), ldq, static_cast<const uint16_t*>(k), ldk, static_cast<const uint16_t*>(v), ldv,
-      seq_len, n_q_heads, n_kv_heads, scale_log2, static_cast<uint16_t*>(out), ldo);
+  TBIK_CUDA(launch_pdl(attn_mma_kernel, grid, dim3(128), fsmem, static_cast<cudaStream_t>(stream),
+                       static_cast<const uint16_t*>(q), ldq, static_cast<const uint16_t*>(k), ldk,
+                       static_cast<const uint16_t*>(v), ldv, seq_len, n_q_heads, n_kv_heads, scale_log2,
+                       static_cast<uint16_t*>(out), ldo));
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;

@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(LANES) residual_rmsnorm_kernel(uint16_t* __res
                                                                  const float* __restrict__ F, int64_t ldf,
                                                                  const float* __restrict__ gamma, float eps,
                                                                  uint16_t* __restrict__ Y, int64_t ldy, int64_t cols) {
+  pdl_wait();
   pdl_trigger();
   __shared__ float sh[9];
   constexpr int CH = 8;
@@ -464,8 +465,9 @@ tbik_status tbik_residual_rmsnorm(void* h, int64_t ldh, const float* f, int64_t 
   if (cols % 8 == 0 && cols <= 4 * LANES * 8 && ldh % 8 == 0 && ldf % 4 == 0 && ldy % 8 == 0 && a16(h) && a16(f) &&
       a16(y) && a16(gamma)) {
     if (current_device_checked() < 0) return set_error(TBIK_NO_DEVICE, "no sm_100 device (no CPU fallback)");
-    residual_rmsnorm_kernel<<<static_cast<unsigned>(rows), LANES, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<uint16_t*>(h), ldh, f, ldf, gamma, eps, static_cast<uint16_t*>(y), ldy, cols);
+    TBIK_CUDA(launch_pdl(residual_rmsnorm_kernel, dim3(static_cast<unsigned>(rows)), dim3(LANES), 0,
+                         static_cast<cudaStream_t>(stream), static_cast<uint16_t*>(h), ldh, f, ldf, gamma, eps,
+                         static_cast<uint16_t*>(y), ldy, cols));
     TBIK_CUDA(cudaGetLastError());
     count_launch();
     return TBIK_OK;

@@ -69,6 +69,7 @@ __global__ void tree_combine_kernel(const float* __restrict__ ws, int64_t X, int
 template <int X>
 __global__ void tree_combine_vec_kernel(const float* __restrict__ ws, int64_t rows, int64_t cols, int64_t slice,
                                         float* __restrict__ out, int64_t ldo) {
+  pdl_wait();
   pdl_trigger();
   const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t cq = cols / 4;
@@ -192,12 +193,9 @@ tbik_status launch_tree_combine(const float* ws, int64_t X, int64_t fold, int64_
   if (vec) {
     const int64_t nq = n / 4;
     const unsigned vb = static_cast<unsigned>((nq + threads - 1) / threads);
-    if (X == 2)
-      tree_combine_vec_kernel<2><<<vb, threads, 0, stream>>>(ws, rows, cols, n, out, ldo);
-    else if (X == 4)
-      tree_combine_vec_kernel<4><<<vb, threads, 0, stream>>>(ws, rows, cols, n, out, ldo);
-    else
-      tree_combine_vec_kernel<8><<<vb, threads, 0, stream>>>(ws, rows, cols, n, out, ldo);
+    // programmatic dependent launch: follows the GEMM that wrote ws
+    const auto kern = X == 2 ? tree_combine_vec_kernel<2> : X == 4 ? tree_combine_vec_kernel<4> : tree_combine_vec_kernel<8>;
+    TBIK_CUDA(launch_pdl(kern, dim3(vb), dim3(threads), 0, stream, ws, rows, cols, n, out, ldo));
     TBIK_CUDA(cudaGetLastError());
     count_launch();
     return TBIK_OK;
