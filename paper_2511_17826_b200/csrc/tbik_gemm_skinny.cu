@@ -125,7 +125,7 @@ struct SkParams {
   int bn;              // weight columns per tile (the kernel's BNW)
   float* out;
   long long ldo;
-  unsigned long long* trace;  // diagnostics (TBIK_SK_TRACE): per-CTA phase clocks, else null
+  unsigned long long* trace;  // diagnostics (knob sk_trace): per-CTA phase clocks, else null
 };
 
 __device__ __forceinline__ void tmem_ld16r(uint32_t taddr, uint32_t (&r)[16]) {
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
 #pragma unroll
             for (int j = 0; j < KS / 64; ++j)
               tma_load_2d(sX + stage * X_STAGE + j * X_BOX, &tmX, &full[stage], k + 64 * j, 0);
-            if (item == blockIdx.x && t == it.t_begin && c == 0) SK_TRACE(2);
+            if (p.trace && c == 0 && t == it.t_begin && item == blockIdx.x) SK_TRACE(2);
             if (++stage == NST) {
               stage = 0;
               phase ^= 1;
@@ -386,24 +386,19 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t acc_iter = 0;
-      long long full_wait = 0, acc_wait = 0;
       for (long long item = blockIdx.x; item < p.items; item += gridDim.x) {
         const SkItem it = sk_decode(p, item);
         for (int t = it.t_begin; t < it.t_end; ++t, ++acc_iter) {
           const int buf = acc_iter % NACC;
           const uint32_t use = acc_iter / NACC;
-          const long long w1 = p.trace ? clock64() : 0;
           mbar_wait(&tempty[buf], (use & 1) ^ 1);
-          if (p.trace) acc_wait += clock64() - w1;
           tc_fence_after();
           const uint32_t d = tmem_base + buf * MT;
           const int nch = sk_chunks<KS>(p, t);
           for (int c = 0; c < nch; ++c) {
-            const long long w0 = p.trace ? clock64() : 0;
             mbar_wait(&full[stage], phase);
-            if (p.trace) full_wait += clock64() - w0;
             tc_fence_after();
-            if (item == blockIdx.x && t == it.t_begin && c == 0) SK_TRACE(4);
+            if (p.trace && c == 0 && t == it.t_begin && item == blockIdx.x) SK_TRACE(4);
             const uint32_t w_base = smem_u32(sW + stage * W_STAGE);
             const uint32_t x_base = smem_u32(sX + stage * X_STAGE);
 #pragma unroll
@@ -430,10 +425,6 @@ __global__ void __launch_bounds__(sk_threads<MT>(), 1)
         }
       }
       SK_TRACE(5);
-      if (p.trace) {
-        p.trace[blockIdx.x * 16 + 10] = static_cast<unsigned long long>(full_wait);
-        p.trace[blockIdx.x * 16 + 11] = static_cast<unsigned long long>(acc_wait);
-      }
     }
     __syncwarp();
   } else if (warp >= 4) {
@@ -830,16 +821,15 @@ tbik_status launch_tc_skinny(const GemmView& v_in, float* C, int64_t ldc, cudaSt
     double mean[16] = {0};
     unsigned long long g_lo = ~0ull, g_hi = 0;
     for (long long b = 0; b < grid; ++b) {
-      for (int i = 1; i < 12; ++i) mean[i] += static_cast<double>(h[b * 16 + i]) / static_cast<double>(grid);
+      for (int i = 1; i < 10; ++i) mean[i] += static_cast<double>(h[b * 16 + i]) / static_cast<double>(grid);
       g_lo = std::min(g_lo, h[b * 16 + 15]);
       g_hi = std::max(g_hi, h[b * 16 + 15]);
     }
     std::fprintf(stderr,
                  "sk_trace grid %lld ks %d bn %d mt %d | setup %.0f tma0 %.0f mma0 %.0f tma_end %.0f mma_end %.0f "
-                 "merge_end %.0f out_end %.0f csync %.0f exit %.0f clk | mma waits: data %.0f acc %.0f | CTA start "
-                 "spread %llu ns\n",
+                 "merge_end %.0f out_end %.0f csync %.0f exit %.0f clk | CTA start spread %llu ns\n",
                  grid, ks, bn, mt, mean[1], mean[2], mean[4], mean[3], mean[5], mean[6], mean[7], mean[8], mean[9],
-                 mean[10], mean[11], g_hi - g_lo);
+                 g_hi - g_lo);
   }
   return TBIK_OK;
 }
