@@ -7,7 +7,7 @@
 // D[n][m] = sum_k W[k][n] X[m][k] lands in TMEM with lane = weight column and
 // column = token, so a leaf drains MT x 4 bytes per lane instead of the
 // 128-row padded tile of the wide kernel (tbik_gemm_tc.cu), and shared memory
-// goes to weight stages (12 / 11 / 9 stages of 16 KB).
+// goes to weight stages.
 //
 // The per-element arithmetic is the wide kernel's: the leaf P_t is block_k/16
 // tcgen05 kind::f16 MMAs (K = 16 each) into a zeroed f32 accumulator -- each
@@ -26,13 +26,22 @@
 //             [u R, u R + R) of the tile over all X values read through DSMEM, in
 //             the fold + contiguous-halves tree order (oracle.cpp:11-20,
 //             Theorem 1).  No workspace, no second launch.
+//   pairs     (p.pair) a tile whose K range is ONE leaf group runs on a CTA
+//             pair: the leading CTA folds the first leaves, sends the prefix by
+//             st.async into the partner's shared memory (completing on its
+//             mbarrier), the partner continues the fold over its last <= NACC
+//             leaves kept in TMEM -- the same sequential level-0 order split at a
+//             leaf; two subtree units hand over the same way, (0 + v1) + (0 + v0).
 //
-// Warp roles (256 threads, one CTA per SM; persistent over tiles when X = 1):
-//   warp 0  TMA producer: {W 64k x 128n (two 64-column SW128 atoms), X MT x 64k}
+// Warp roles (one CTA per SM; persistent over tiles when X = 1):
+//   warp 0  TMA producer: per stage {W KS k x BNW n (64-column SW128 atoms, or one
+//           32-column SW64 atom), X MT x KS k as KS / 64 boxes}
 //   warp 1  MMA issuer (one elected thread), NACC TMEM accumulators in rotation
 //   warp 2  TMEM allocator (512 columns: accumulators + tree levels 1..levels)
-//   warps 4-7 merge warps: thread (q, lane) owns weight column n0 + 32q + lane
-//             for all MT tokens (TMEM lane quarter q).
+//   warps 4.. merge warps: thread (q, lane) owns weight column n0 + q LPQ + lane
+//             for TPW <= 32 tokens (TMEM lane quarter q); MT / 8 warps.
+// Launched with programmatic dependent launch (griddepcontrol.wait before the
+// first operand / output access, dependents triggered after the last load).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
