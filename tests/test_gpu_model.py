@@ -121,6 +121,27 @@ def test_llama_forward_batch_invariance(tb, cuda, llama2):
         assert torch.equal(one.view(torch.int32), full[b * 64:(b + 1) * 64].view(torch.int32)), b
 
 
+@pytest.mark.parametrize("B,S", [(2, 128), (2, 16)])
+def test_llama_forward_pdl_on_off_same_bits(tb, cuda, llama2, B, S):
+    """Programmatic dependent launch only moves kernel scheduling: the forward
+    (prefill sizes on the pair-tile GEMMs, decode sizes on the skinny kernel, each
+    GEMM following a kernel that triggered its dependents early) gives the same
+    logits with the GEMMs launched with and without the attribute, eager and
+    repeated back to back."""
+    from paper_2511_17826_b200 import model as mdl
+    cfg, w = llama2
+    dec = mdl.TbikDecoder(cfg, w)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(9)
+    tokens = torch.randint(0, cfg.vocab, (B, S), device=cuda, generator=g)
+    with tb.schedule(tc_pdl=0, sk_pdl=0):
+        ref = dec.forward(tokens, 1).clone()
+    for _ in range(3):
+        with tb.schedule(tc_pdl=1, sk_pdl=1):
+            got = dec.forward(tokens, 1)
+        assert torch.equal(got.view(torch.int32), ref.view(torch.int32))
+
+
 def test_llama_forward_graph_decode_size(tb, cuda, llama2):
     """A CUDA-graph capture of a decode-sized forward (2 x 16 tokens: every GEMM on
     the swap-AB skinny kernel, its K split in thread-block clusters) replays to
