@@ -435,6 +435,14 @@ TBIK_API tbik_status tbik_embedding(const void* table, int64_t V, int64_t H, con
 TBIK_API tbik_status tbik_rope(const float* x, int64_t ldx, int64_t col0, int heads, int head_dim,
                                const int* positions, const float* cos_table, const float* sin_table,
                                void* out, int64_t ldo, int64_t rows, void* stream);
+/* The attention inputs of one qkv projection in one launch: tbik_rope of the
+ * n_q_heads q heads (columns [0, nq hd)) into q_out [rows][nq hd], of the
+ * n_kv_heads k heads (the next nkv hd columns) into k_out [rows][nkv hd], and
+ * tbik_cast_bf16 of v (the last nkv hd columns) into v_out -- the same bits as the
+ * three calls.  head_dim % 8 == 0, 16-byte aligned f32 rows (ld % 4 == 0). */
+TBIK_API tbik_status tbik_rope_qkv(const float* qkv, int64_t ld, int n_q_heads, int n_kv_heads, int head_dim,
+                                   const int* positions, const float* cos_table, const float* sin_table,
+                                   void* q_out, void* k_out, void* v_out, int64_t rows, void* stream);
 /* storage_cast (demo.cpp:50-52): bf16_round of an f32 block. */
 TBIK_API tbik_status tbik_cast_bf16(const float* x, int64_t ldx, int64_t rows, int64_t cols, void* out,
                                     int64_t ldo, void* stream);

@@ -137,6 +137,7 @@ _SIGS = {
     "tbik_tree_logsoftmax_local": (ci, [PF, i64, i64, i64, i64, ci, PF, PF, i64, vp, PF, vp]),
     "tbik_embedding": (ci, [vp, i64, i64, vp, i64, vp, vp]),
     "tbik_rope": (ci, [PF, i64, i64, ci, ci, vp, PF, PF, vp, i64, i64, vp]),
+    "tbik_rope_qkv": (ci, [PF, i64, ci, ci, ci, vp, PF, PF, vp, vp, vp, i64, vp]),
     "tbik_cast_bf16": (ci, [PF, i64, i64, i64, vp, i64, vp]),
     "tbik_attention_prefill": (ci, [vp, i64, vp, i64, vp, i64, i64, ci, ci, ci, ci, C.c_float, vp, i64, vp]),
     "tbik_attention_prefill_tc": (ci, [vp, i64, vp, i64, vp, i64, i64, ci, ci, ci, ci, C.c_float, vp, i64, vp]),

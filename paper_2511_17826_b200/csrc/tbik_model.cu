@@ -66,6 +66,30 @@ __global__ void rope_kernel(const float* __restrict__ x, int64_t ldx, int64_t co
   }
 }
 
+// One quad of a head: out[d..d+3] and out[d+half..+3] from x[d..], x[d+half..] --
+// rope_kernel's operations, four lanes at a time.
+__device__ __forceinline__ void rope_quad(const float* xh, int d, int half, const float* cs, const float* sn_t,
+                                          uint16_t* o) {
+  const float4 a = *reinterpret_cast<const float4*>(xh + d);
+  const float4 b = *reinterpret_cast<const float4*>(xh + d + half);
+  const float4 c = *reinterpret_cast<const float4*>(cs + d);
+  const float4 sn = *reinterpret_cast<const float4*>(sn_t + d);
+  const float lo0 = __fsub_rn(__fmul_rn(a.x, c.x), __fmul_rn(b.x, sn.x));
+  const float lo1 = __fsub_rn(__fmul_rn(a.y, c.y), __fmul_rn(b.y, sn.y));
+  const float lo2 = __fsub_rn(__fmul_rn(a.z, c.z), __fmul_rn(b.z, sn.z));
+  const float lo3 = __fsub_rn(__fmul_rn(a.w, c.w), __fmul_rn(b.w, sn.w));
+  const float hi0 = __fadd_rn(__fmul_rn(b.x, c.x), __fmul_rn(a.x, sn.x));
+  const float hi1 = __fadd_rn(__fmul_rn(b.y, c.y), __fmul_rn(a.y, sn.y));
+  const float hi2 = __fadd_rn(__fmul_rn(b.z, c.z), __fmul_rn(a.z, sn.z));
+  const float hi3 = __fadd_rn(__fmul_rn(b.w, c.w), __fmul_rn(a.w, sn.w));
+  *reinterpret_cast<uint2*>(o + d) =
+      make_uint2(f32_to_bf16_bits(lo0) | (static_cast<uint32_t>(f32_to_bf16_bits(lo1)) << 16),
+                 f32_to_bf16_bits(lo2) | (static_cast<uint32_t>(f32_to_bf16_bits(lo3)) << 16));
+  *reinterpret_cast<uint2*>(o + d + half) =
+      make_uint2(f32_to_bf16_bits(hi0) | (static_cast<uint32_t>(f32_to_bf16_bits(hi1)) << 16),
+                 f32_to_bf16_bits(hi2) | (static_cast<uint32_t>(f32_to_bf16_bits(hi3)) << 16));
+}
+
 // Vectorised form (D % 8 == 0, 16-byte aligned rows): thread = (head, 4 dims d..d+3
 // of the first half); it produces out[d..d+3] and out[d+D/2..+3] with the same
 // operations as rope_kernel.  Several rows per CTA (blockDim.y).
@@ -82,25 +106,8 @@ __global__ void rope_vec_kernel(const float* __restrict__ x, int64_t ldx, int64_
   for (int e = threadIdx.x; e < heads * qpr; e += blockDim.x) {
     const int h = e / qpr, d = (e - h * qpr) * 4;
     const float* xh = x + row * ldx + col0 + h * D;
-    const float4 a = *reinterpret_cast<const float4*>(xh + d);
-    const float4 b = *reinterpret_cast<const float4*>(xh + d + half);
-    const float4 c = *reinterpret_cast<const float4*>(cos_t + static_cast<int64_t>(p) * half + d);
-    const float4 sn = *reinterpret_cast<const float4*>(sin_t + static_cast<int64_t>(p) * half + d);
-    const float lo0 = __fsub_rn(__fmul_rn(a.x, c.x), __fmul_rn(b.x, sn.x));
-    const float lo1 = __fsub_rn(__fmul_rn(a.y, c.y), __fmul_rn(b.y, sn.y));
-    const float lo2 = __fsub_rn(__fmul_rn(a.z, c.z), __fmul_rn(b.z, sn.z));
-    const float lo3 = __fsub_rn(__fmul_rn(a.w, c.w), __fmul_rn(b.w, sn.w));
-    const float hi0 = __fadd_rn(__fmul_rn(b.x, c.x), __fmul_rn(a.x, sn.x));
-    const float hi1 = __fadd_rn(__fmul_rn(b.y, c.y), __fmul_rn(a.y, sn.y));
-    const float hi2 = __fadd_rn(__fmul_rn(b.z, c.z), __fmul_rn(a.z, sn.z));
-    const float hi3 = __fadd_rn(__fmul_rn(b.w, c.w), __fmul_rn(a.w, sn.w));
-    uint16_t* o = out + row * ldo + h * D;
-    *reinterpret_cast<uint2*>(o + d) =
-        make_uint2(f32_to_bf16_bits(lo0) | (static_cast<uint32_t>(f32_to_bf16_bits(lo1)) << 16),
-                   f32_to_bf16_bits(lo2) | (static_cast<uint32_t>(f32_to_bf16_bits(lo3)) << 16));
-    *reinterpret_cast<uint2*>(o + d + half) =
-        make_uint2(f32_to_bf16_bits(hi0) | (static_cast<uint32_t>(f32_to_bf16_bits(hi1)) << 16),
-                   f32_to_bf16_bits(hi2) | (static_cast<uint32_t>(f32_to_bf16_bits(hi3)) << 16));
+    rope_quad(xh, d, half, cos_t + static_cast<int64_t>(p) * half, sin_t + static_cast<int64_t>(p) * half,
+              out + row * ldo + h * D);
   }
 }
 
@@ -113,6 +120,41 @@ __global__ void cast_kernel(const float* __restrict__ x, int64_t ldx, int64_t co
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < cols;
        j += static_cast<int64_t>(gridDim.x) * blockDim.x)
     out[row * ldo + j] = f32_to_bf16_bits(x[row * ldx + j]);
+}
+
+// The attention inputs from one f32 qkv row in ONE launch: RoPE of the nq q heads
+// (columns [0, nq D)) and the nkv k heads (the next nkv D columns) and the bf16
+// cast of v (the last nkv D) -- rope_vec_kernel's and cast_kernel's operations per
+// element, three launches folded into one (D % 8 == 0, 16-byte aligned rows).
+__global__ void rope_qkv_kernel(const float* __restrict__ x, int64_t ldx, int nq, int nkv, int D,
+                                const int* __restrict__ pos, const float* __restrict__ cos_t,
+                                const float* __restrict__ sin_t, uint16_t* __restrict__ q_out,
+                                uint16_t* __restrict__ k_out, uint16_t* __restrict__ v_out, int64_t rows) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
+  if (row >= rows) return;
+  const int half = D / 2, qpr = half / 4;
+  const int p = pos[row];
+  const float* xr = x + row * ldx;
+  const float* cs = cos_t + static_cast<int64_t>(p) * half;
+  const float* sn = sin_t + static_cast<int64_t>(p) * half;
+  const int nrope = (nq + nkv) * qpr, nv = nkv * D / 4;
+  for (int e = threadIdx.x; e < nrope + nv; e += blockDim.x) {
+    if (e < nrope) {
+      const int h = e / qpr, d = (e - h * qpr) * 4;
+      if (h < nq)
+        rope_quad(xr + h * D, d, half, cs, sn, q_out + row * nq * D + h * D);
+      else
+        rope_quad(xr + h * D, d, half, cs, sn, k_out + row * nkv * D + (h - nq) * D);
+    } else {
+      const int j = (e - nrope) * 4;
+      const float4 f = *reinterpret_cast<const float4*>(xr + (nq + nkv) * D + j);
+      *reinterpret_cast<uint2*>(v_out + row * nkv * D + j) =
+          make_uint2(f32_to_bf16_bits(f.x) | (static_cast<uint32_t>(f32_to_bf16_bits(f.y)) << 16),
+                     f32_to_bf16_bits(f.z) | (static_cast<uint32_t>(f32_to_bf16_bits(f.w)) << 16));
+    }
+  }
 }
 
 // ---- causal GQA prefill attention, tiled two-pass form -------------------------------------
@@ -641,6 +683,28 @@ tbik_status tbik_rope(const float* x, int64_t ldx, int64_t col0, int heads, int 
     rope_kernel<<<static_cast<unsigned>(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         x, ldx, col0, heads, head_dim, positions, cos_table, sin_table, static_cast<uint16_t*>(out), ldo);
   }
+  TBIK_CUDA(cudaGetLastError());
+  count_launch();
+  return TBIK_OK;
+}
+
+tbik_status tbik_rope_qkv(const float* qkv, int64_t ld, int n_q_heads, int n_kv_heads, int head_dim,
+                          const int* positions, const float* cos_table, const float* sin_table, void* q_out,
+                          void* k_out, void* v_out, int64_t rows, void* stream) {
+  if (!qkv || !positions || !cos_table || !sin_table || !q_out || !k_out || !v_out)
+    return set_error(TBIK_BAD_ARGUMENT, "null argument");
+  if (head_dim % 8 || n_q_heads < 1 || n_kv_heads < 1 || rows < 1)
+    return set_error(TBIK_BAD_DIMENSION, "rope_qkv: bad dimensions");
+  const auto a16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  if (ld % 4 || !a16(qkv) || !a16(cos_table) || !a16(sin_table) || (reinterpret_cast<uintptr_t>(q_out) & 7) ||
+      (reinterpret_cast<uintptr_t>(k_out) & 7) || (reinterpret_cast<uintptr_t>(v_out) & 7))
+    return set_error(TBIK_BAD_ARGUMENT, "rope_qkv: 16-byte aligned f32 rows and 8-byte aligned outputs required");
+  TBIK_TRY(need_device());
+  const int rows_per_cta = 2;
+  TBIK_CUDA(launch_pdl(rope_qkv_kernel, dim3(static_cast<unsigned>((rows + rows_per_cta - 1) / rows_per_cta)),
+                       dim3(256, rows_per_cta), 0, static_cast<cudaStream_t>(stream), qkv, ld, n_q_heads, n_kv_heads,
+                       head_dim, positions, cos_table, sin_table, static_cast<uint16_t*>(q_out),
+                       static_cast<uint16_t*>(k_out), static_cast<uint16_t*>(v_out), rows));
   TBIK_CUDA(cudaGetLastError());
   count_launch();
   return TBIK_OK;

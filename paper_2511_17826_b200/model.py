@@ -281,12 +281,17 @@ class TbikDecoder:
                 kn = self._qk_normed(qkv, qcols, nkv, lw.k_norm, M)
                 q = self._rope(qn, qcols, 0, nq, pos, M)
                 k = self._rope(kn, kcols, 0, nkv, pos, M)
+                v = torch.empty(M, kcols, device=dev, dtype=torch.bfloat16)
+                check(lib.tbik_cast_bf16(C.c_void_p(qkv.data_ptr() + 4 * (qcols + kcols)), ld, M, kcols, _vp(v),
+                                         kcols, self._stream()))
             else:
-                q = self._rope(qkv, ld, 0, nq, pos, M)
-                k = self._rope(qkv, ld, qcols, nkv, pos, M)
-            v = torch.empty(M, kcols, device=dev, dtype=torch.bfloat16)
-            check(lib.tbik_cast_bf16(C.c_void_p(qkv.data_ptr() + 4 * (qcols + kcols)), ld, M, kcols, _vp(v),
-                                     kcols, self._stream()))
+                # RoPE of q and k and the bf16 cast of v in one launch (same bits as
+                # tbik_rope x 2 + tbik_cast_bf16)
+                q = torch.empty(M, qcols, device=dev, dtype=torch.bfloat16)
+                k = torch.empty(M, kcols, device=dev, dtype=torch.bfloat16)
+                v = torch.empty(M, kcols, device=dev, dtype=torch.bfloat16)
+                check(lib.tbik_rope_qkv(_vp(qkv), ld, nq, nkv, D, _vp(pos), _vp(self.cos), _vp(self.sin), _vp(q),
+                                        _vp(k), _vp(v), M, self._stream()))
             attn = torch.empty(M, qcols, device=dev, dtype=torch.bfloat16)
             # tensor-core flash attention with the tcgen05 leaf, the exact order with the fma leaf
             attn_fn = lib.tbik_attention_prefill_tc if self.leaf == api.LEAF_TCGEN05 else lib.tbik_attention_prefill

@@ -121,6 +121,36 @@ def test_llama_forward_batch_invariance(tb, cuda, llama2):
         assert torch.equal(one.view(torch.int32), full[b * 64:(b + 1) * 64].view(torch.int32)), b
 
 
+@pytest.mark.parametrize("rows,nq,nkv", [(300, 32, 8), (1, 8, 8), (77, 64, 8), (1024, 32, 8)])
+def test_rope_qkv_equals_rope_and_cast(tb, cuda, rows, nq, nkv):
+    """tbik_rope_qkv (RoPE of q and k + bf16 cast of v in one launch) == two
+    tbik_rope calls and one tbik_cast_bf16, bit for bit."""
+    import ctypes as C
+    from paper_2511_17826_b200 import model as mdl
+    from paper_2511_17826_b200._lib import lib
+    cfg = mdl.llama31_8b(n_layers=1)
+    cos, sin = (torch.from_numpy(t).to(cuda) for t in mdl.rope_tables(cfg))
+    D = 128
+    g = torch.Generator(device=cuda).manual_seed(rows)
+    qkv = torch.randn(rows, (nq + 2 * nkv) * D, device=cuda, generator=g) * 3
+    pos = torch.randint(0, cfg.max_pos, (rows,), device=cuda, generator=g, dtype=torch.int32)
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    q = torch.empty(rows, nq * D, device=cuda, dtype=torch.bfloat16)
+    k = torch.empty(rows, nkv * D, device=cuda, dtype=torch.bfloat16)
+    v = torch.empty(rows, nkv * D, device=cuda, dtype=torch.bfloat16)
+    assert lib.tbik_rope_qkv(vp(qkv), qkv.stride(0), nq, nkv, D, vp(pos), vp(cos), vp(sin), vp(q), vp(k), vp(v),
+                             rows, st) == 0
+    q2, k2, v2 = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    ld = qkv.stride(0)
+    assert lib.tbik_rope(vp(qkv), ld, 0, nq, D, vp(pos), vp(cos), vp(sin), vp(q2), nq * D, rows, st) == 0
+    assert lib.tbik_rope(vp(qkv), ld, nq * D, nkv, D, vp(pos), vp(cos), vp(sin), vp(k2), nkv * D, rows, st) == 0
+    assert lib.tbik_cast_bf16(C.c_void_p(qkv.data_ptr() + 4 * (nq + nkv) * D), ld, rows, nkv * D, vp(v2), nkv * D,
+                              st) == 0
+    for a_, b_ in ((q, q2), (k, k2), (v, v2)):
+        assert torch.equal(a_.view(torch.int16), b_.view(torch.int16))
+
+
 @pytest.mark.parametrize("B,S", [(2, 128), (2, 16)])
 def test_llama_forward_pdl_on_off_same_bits(tb, cuda, llama2, B, S):
     """Programmatic dependent launch only moves kernel scheduling: the forward
