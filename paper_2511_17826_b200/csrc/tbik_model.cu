@@ -383,6 +383,10 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return static_cast<uint32_t>(f32_to_bf16_bits(lo)) | (static_cast<uint32_t>(f32_to_bf16_bits(hi)) << 16);
 }
 
+// SV1: the V block single-buffered (K double-buffered): 3 staged blocks = 52 KB,
+// four CTAs per SM instead of three; V(kb) is loaded while Q.K(kb) and the
+// softmax run.  Same MMAs in the same order either way.
+template <bool SV1>
 __global__ void __launch_bounds__(128) attn_mma_kernel(const uint16_t* __restrict__ q, int64_t ldq,
                                                        const uint16_t* __restrict__ k, int64_t ldk,
                                                        const uint16_t* __restrict__ v, int64_t ldv, int S, int nq,
@@ -390,7 +394,7 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const uint16_t* __restric
                                                        int64_t ldo) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ __align__(16) uint16_t fsm[];  // [2 buffers][K block, V block]
+  extern __shared__ __align__(16) uint16_t fsm[];  // [2 buffers][K block, V block] (SV1: K0, K1, V)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int qb = static_cast<int>(gridDim.z) - 1 - static_cast<int>(blockIdx.z), h = blockIdx.x;
@@ -400,9 +404,10 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const uint16_t* __restric
   const int last_key = min(S, (qb + 1) * FQ) - 1;
   const int nkb = last_key / FK + 1;
 
-  auto stage = [&](int kb, int buf) {  // keys past the causal end / sequence as zeros
-    uint16_t* sK = fsm + buf * 2 * FSTAGE;
-    uint16_t* sV = sK + FSTAGE;
+  auto kbuf = [&](int buf) { return SV1 ? fsm + buf * FSTAGE : fsm + buf * 2 * FSTAGE; };
+  auto vbuf = [&](int buf) { return SV1 ? fsm + 2 * FSTAGE : fsm + buf * 2 * FSTAGE + FSTAGE; };
+  // keys past the causal end / sequence as zeros
+  auto stage_part = [&](int kb, uint16_t* dst, const uint16_t* src, int64_t ld) {
 #pragma unroll
     for (int x = 0; x < FK * AD / 8 / 128; ++x) {
       const int e = tid + x * 128;
@@ -410,12 +415,22 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const uint16_t* __restric
       const int key = kb * FK + r;
       const bool ok = key <= last_key;
       const int64_t row = seq0 + (ok ? key : 0);
-      cp_async16(sK + r * FKP + c, k + row * ldk + kh * AD + c, ok);
-      cp_async16(sV + r * FKP + c, v + row * ldv + kh * AD + c, ok);
+      cp_async16(dst + r * FKP + c, src + row * ld + kh * AD + c, ok);
     }
+  };
+  auto stage = [&](int kb, int buf) {
+    stage_part(kb, kbuf(buf), k, ldk);
+    stage_part(kb, vbuf(buf), v, ldv);
     cp_async_commit();
   };
-  stage(0, 0);
+  if constexpr (SV1) {
+    stage_part(0, kbuf(0), k, ldk);
+    cp_async_commit();
+    stage_part(0, vbuf(0), v, ldv);
+    cp_async_commit();
+  } else {
+    stage(0, 0);
+  }
 
   // Q fragments (16 rows x 128 d per warp): qa[kstep][4]
   uint32_t qa[AD / 16][4];
@@ -440,15 +455,24 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const uint16_t* __restric
   const int lr = lane & 7, lm = lane >> 3;
 
   for (int kb = 0; kb < nkb; ++kb) {
-    if (kb + 1 < nkb) {
+    if constexpr (SV1) {
+      // pending: V(kb) [, K(kb + 1) issued now]; K(kb) is complete after the wait
+      if (kb + 1 < nkb) {
+        stage_part(kb + 1, kbuf((kb + 1) & 1), k, ldk);
+        cp_async_commit();
+        cp_async_wait<2>();
+      } else {
+        cp_async_wait<1>();
+      }
+    } else if (kb + 1 < nkb) {
       stage(kb + 1, (kb + 1) & 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const uint16_t* sK = fsm + (kb & 1) * 2 * FSTAGE;
-    const uint16_t* sV = sK + FSTAGE;
+    const uint16_t* sK = kbuf(kb & 1);
+    const uint16_t* sV = vbuf(kb & 1);
     // s = q . k for this warp's 16 rows x 64 keys (8 n-tiles of 8 keys).  ldmatrix x4
     // matrices: (keys n*8.., d ks*16 + 0/8) for n-tile pair (n, n+1)
     float sc[FK / 8][4];
@@ -509,6 +533,13 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const uint16_t* __restric
       o[n][2] = __fmul_rn(o[n][2], alpha[1]);
       o[n][3] = __fmul_rn(o[n][3], alpha[1]);
     }
+    if constexpr (SV1) {  // V(kb) complete (only K(kb + 1) may still be in flight)
+      if (kb + 1 < nkb)
+        cp_async_wait<1>();
+      else
+        cp_async_wait<0>();
+      __syncthreads();
+    }
     // O += P . V: B fragments of V [key][d] by ldmatrix.trans, matrices (keys ks*16 +
     // 0/8, d n*8..) for d-tile pair (n, n+1)
 #pragma unroll
@@ -521,7 +552,13 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(const uint16_t* __restric
         mma_bf16_16816(o[n + 1], pa[ks], b[2], b[3]);
       }
     }
-    __syncthreads();  // this buffer is restaged two blocks later
+    __syncthreads();  // this buffer is restaged two blocks later (SV1: V now)
+    if constexpr (SV1) {
+      if (kb + 1 < nkb) {
+        stage_part(kb + 1, vbuf(0), v, ldv);
+        cp_async_commit();
+      }
+    }
   }
   // l over the quad (xor 1 then xor 2), out = bf16(O / l)
 #pragma unroll
@@ -764,9 +801,11 @@ tbik_status tbik_attention_prefill_tc(const void* q, int64_t ldq, const void* k,
   const float scale_log2 = scale * 1.4426950408889634f;
   dim3 grid(static_cast<unsigned>(n_q_heads), static_cast<unsigned>(batch),
             static_cast<unsigned>((seq_len + FQ - 1) / FQ));
-  constexpr size_t fsmem = 2 * 2 * FSTAGE * sizeof(uint16_t);
-  TBIK_CUDA(cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem)));
-  TBIK_CUDA(launch_pdl(attn_mma_kernel, grid, dim3(128), fsmem, static_cast<cudaStream_t>(stream),
+  const bool sv1 = knob(KNOB_ATTN_SV1, 1) != 0;
+  const size_t fsmem = (sv1 ? 3 : 4) * FSTAGE * sizeof(uint16_t);
+  const auto kern = sv1 ? attn_mma_kernel<true> : attn_mma_kernel<false>;
+  TBIK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem)));
+  TBIK_CUDA(launch_pdl(kern, grid, dim3(128), fsmem, static_cast<cudaStream_t>(stream),
                        static_cast<const uint16_t*>(q), ldq, static_cast<const uint16_t*>(k), ldk,
                        static_cast<const uint16_t*>(v), ldv, seq_len, n_q_heads, n_kv_heads, scale_log2,
                        static_cast<uint16_t*>(out), ldo));

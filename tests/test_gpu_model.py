@@ -319,3 +319,27 @@ def test_fused_silu_gate_up_256x192_tiles(tb, cuda, M, inter):
         aligned = (inter // tp) % 8 == 0
         assert kern == ("tc_w192_tree_gemm_kernel" if aligned else "tc_tree_gemm_kernel")
         assert torch.equal(act.view(torch.int16), ref.view(torch.int16)), f"tp={tp}"
+
+
+@pytest.mark.parametrize("B,S,nq,nkv", [(4, 256, 32, 8), (1, 16, 8, 8), (2, 100, 16, 4), (1, 512, 8, 2), (3, 65, 8, 8)])
+def test_attention_tc_single_v_buffer_same_bits(tb, cuda, B, S, nq, nkv):
+    """The tensor-core attention with its V block single-buffered (knob attn_sv1,
+    four CTAs per SM) == the double-buffered pipeline, bit for bit."""
+    import ctypes as C
+    from paper_2511_17826_b200._lib import lib
+    D = 128
+    g = torch.Generator(device=cuda).manual_seed(S * nq)
+    q = torch.randn(B * S, nq * D, device=cuda, generator=g).to(torch.bfloat16)
+    k = torch.randn(B * S, nkv * D, device=cuda, generator=g).to(torch.bfloat16)
+    v = torch.randn(B * S, nkv * D, device=cuda, generator=g).to(torch.bfloat16)
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    outs = []
+    for sv1 in (0, 1):
+        o = torch.empty(B * S, nq * D, device=cuda, dtype=torch.bfloat16)
+        with tb.schedule(attn_sv1=sv1):
+            assert lib.tbik_attention_prefill_tc(vp(q), nq * D, vp(k), nkv * D, vp(v), nkv * D, B, S, nq, nkv, D,
+                                                 1.0 / D ** 0.5, vp(o), nq * D, st) == 0
+        outs.append(o)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
