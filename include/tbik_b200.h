@@ -103,7 +103,7 @@ TBIK_API tbik_status tbik_sync(void* stream);
  * library reads no environment variables.  Names: tc_pair, tc_abox, tc_group_m,
  * tc_units, tc_deep, tc_acc4, tc_skinny, sk_mt, sk_units, sk_leaf, sk_bn,
  * fma_v1, group_fused, group_overlap, ar_two_phase_bytes, tc_wide, tc_wide_tail,
- * sk_ks, sk_pdl, sk_trace (diagnostics: phase clocks to stderr), sk_pair, attn_sv1, tc_pdl.
+ * sk_ks, sk_pdl, sk_trace (diagnostics: phase clocks to stderr), sk_pair, attn_sv1, attn_tc5, tc_pdl.
  * value < 0 unsets one knob, name NULL unsets all; an unknown name is TBIK_BAD_ARGUMENT.  Every rank
  * of a group must use the same group_* / ar_* settings. */
 TBIK_API tbik_status tbik_set_schedule(const char* name, int64_t value);

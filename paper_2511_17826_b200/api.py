@@ -105,7 +105,7 @@ def last_kernel() -> str:
 
 SCHEDULE_KNOBS = ("tc_pair", "tc_abox", "tc_group_m", "tc_units", "tc_deep", "tc_acc4", "tc_skinny", "sk_mt",
                   "sk_units", "sk_leaf", "sk_bn", "fma_v1", "group_fused", "group_overlap", "ar_two_phase_bytes",
-                  "tc_wide", "tc_wide_tail", "sk_ks", "sk_pdl", "sk_trace", "sk_pair", "attn_sv1", "tc_pdl")
+                  "tc_wide", "tc_wide_tail", "sk_ks", "sk_pdl", "sk_trace", "sk_pair", "attn_sv1", "attn_tc5", "tc_pdl")
 
 
 def set_schedule(name, value: int = -1) -> None:

@@ -106,6 +106,7 @@ enum Knob {
   KNOB_SK_TRACE,         // 1: skinny phase clocks to stderr (diagnostics)
   KNOB_SK_PAIR,          // 0: no CTA-pair split of a single leaf group (skinny)
   KNOB_ATTN_SV1,         // 0: tensor-core attention with double-buffered V (A/B)
+  KNOB_ATTN_TC5,         // 1: tcgen05 attention form (tbik_attn_tc5.cu)
   KNOB_TC_PDL,           // 0: pair-tile GEMMs without programmatic dependent launch
   KNOB_COUNT
 };

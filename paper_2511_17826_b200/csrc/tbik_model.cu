@@ -17,6 +17,11 @@
 
 namespace tbik_b200 {
 
+// tbik_attn_tc5.cu
+tbik_status launch_attn_tc5(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
+                            int64_t batch, int S, int nq, int nkv, float scale_log2, void* out, int64_t ldo,
+                            cudaStream_t s);
+
 namespace {
 
 __device__ __forceinline__ float bf(uint16_t b) { return bf16_bits_to_f32(b); }
@@ -801,6 +806,9 @@ tbik_status tbik_attention_prefill_tc(const void* q, int64_t ldq, const void* k,
   const float scale_log2 = scale * 1.4426950408889634f;
   dim3 grid(static_cast<unsigned>(n_q_heads), static_cast<unsigned>(batch),
             static_cast<unsigned>((seq_len + FQ - 1) / FQ));
+  if (knob(KNOB_ATTN_TC5, 0) != 0)  // tcgen05 form (tbik_attn_tc5.cu): its own bits, same tolerance
+    return launch_attn_tc5(q, ldq, k, ldk, v, ldv, batch, seq_len, n_q_heads, n_kv_heads, scale_log2, out, ldo,
+                           static_cast<cudaStream_t>(stream));
   const bool sv1 = knob(KNOB_ATTN_SV1, 1) != 0;
   const size_t fsmem = (sv1 ? 3 : 4) * FSTAGE * sizeof(uint16_t);
   const auto kern = sv1 ? attn_mma_kernel<true> : attn_mma_kernel<false>;

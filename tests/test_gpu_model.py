@@ -233,12 +233,18 @@ def test_fused_silu_gate_up_equals_unfused(tb, cuda, leaf, M):
         assert torch.equal(act.view(torch.int16), ref.view(torch.int16)), f"tp={tp}"
 
 
-def test_attention_tc_invariance_and_tolerance(tb, cuda):
-    """Tensor-core flash attention: bit-identical across batch composition, head
-    sharding and reruns; within tolerance of the exact two-pass kernel and of an
-    f64 causal softmax."""
+@pytest.mark.parametrize("form,S", [("mma_sync", 200), ("tcgen05", 200), ("tcgen05", 512), ("tcgen05", 37)])
+def test_attention_tc_invariance_and_tolerance(tb, cuda, form, S):
+    """Tensor-core flash attention (the mma.sync form and the tcgen05 form, knob
+    attn_tc5): bit-identical across batch composition, head sharding and reruns;
+    within tolerance of the exact two-pass kernel and of an f64 causal softmax."""
+    with tb.schedule(attn_tc5=1 if form == "tcgen05" else 0):
+        _attention_tc_checks(tb, cuda, S)
+
+
+def _attention_tc_checks(tb, cuda, S):
     import ctypes as C
-    B, S, nq, nkv, D = 3, 200, 8, 2, 128
+    B, nq, nkv, D = 3, 8, 2, 128
     g = torch.Generator(device=cuda).manual_seed(7)
     q = (torch.randn(B * S, nq * D, device=cuda, generator=g) * 2).to(torch.bfloat16)
     k = (torch.randn(B * S, nkv * D, device=cuda, generator=g) * 2).to(torch.bfloat16)
