@@ -806,7 +806,7 @@ tbik_status tbik_attention_prefill_tc(const void* q, int64_t ldq, const void* k,
   const float scale_log2 = scale * 1.4426950408889634f;
   dim3 grid(static_cast<unsigned>(n_q_heads), static_cast<unsigned>(batch),
             static_cast<unsigned>((seq_len + FQ - 1) / FQ));
-  if (knob(KNOB_ATTN_TC5, 0) != 0)  // tcgen05 form (tbik_attn_tc5.cu): its own bits, same tolerance
+  if (knob(KNOB_ATTN_TC5, 1) != 0)  // tcgen05 form (tbik_attn_tc5.cu, default): its own bits, same tolerance
     return launch_attn_tc5(q, ldq, k, ldk, v, ldv, batch, seq_len, n_q_heads, n_kv_heads, scale_log2, out, ldo,
                            static_cast<cudaStream_t>(stream));
   const bool sv1 = knob(KNOB_ATTN_SV1, 1) != 0;

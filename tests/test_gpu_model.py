@@ -233,7 +233,8 @@ def test_fused_silu_gate_up_equals_unfused(tb, cuda, leaf, M):
         assert torch.equal(act.view(torch.int16), ref.view(torch.int16)), f"tp={tp}"
 
 
-@pytest.mark.parametrize("form,S", [("mma_sync", 200), ("tcgen05", 200), ("tcgen05", 512), ("tcgen05", 37)])
+@pytest.mark.parametrize("form,S", [("mma_sync", 200), ("tcgen05", 200), ("tcgen05", 512), ("tcgen05", 37),
+                                    ("tcgen05", 1000)])
 def test_attention_tc_invariance_and_tolerance(tb, cuda, form, S):
     """Tensor-core flash attention (the mma.sync form and the tcgen05 form, knob
     attn_tc5): bit-identical across batch composition, head sharding and reruns;
@@ -270,8 +271,9 @@ def _attention_tc_checks(tb, cuda, S):
     shard = run(tb.lib.tbik_attention_prefill_tc, q[:, 4 * D:].contiguous(), k[:, D:].contiguous(),
                 v[:, D:].contiguous(), B, nq // 2, nkv // 2)
     assert torch.equal(fast[:, 4 * D:].contiguous().view(torch.int16), shard.view(torch.int16))
-    exact = run(tb.lib.tbik_attention_prefill, q, k, v, B, nq, nkv)
-    assert (fast.float() - exact.float()).abs().max().item() < 3e-2
+    if S <= 512:  # the exact two-pass kernel's range
+        exact = run(tb.lib.tbik_attention_prefill, q, k, v, B, nq, nkv)
+        assert (fast.float() - exact.float()).abs().max().item() < 3e-2
     ref = torch.nn.functional.scaled_dot_product_attention(
         q.double().view(B, S, nq, D).transpose(1, 2),
         k.double().view(B, S, nkv, D).transpose(1, 2).repeat_interleave(nq // nkv, 1),
