@@ -55,6 +55,12 @@ __device__ __forceinline__ uint64_t t5_desc(uint32_t addr, uint32_t lbo, uint32_
   return d;
 }
 
+// The four warps that share TMEM lane group g (warps g, g + 4, g + 8, g + 12: the four
+// column quarters of the same 32 query rows) meet on named barrier 1 + g.
+__device__ __forceinline__ void row_group_sync(int g) {
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+}
+
 __global__ void __launch_bounds__(T5_THREADS, 1)
     attn_tc5_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, int S, int nq, int nkv, float scale_log2,
@@ -161,7 +167,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
       bm = fmaxf(bm, s[i]);
     }
     red_max[qtr * 128 + r] = bm;
-    __syncthreads();
+    row_group_sync(grp);
     bm = fmaxf(fmaxf(red_max[r], red_max[128 + r]), fmaxf(red_max[256 + r], red_max[384 + r]));
     const float mn = fmaxf(m, bm);
     const float mc = mn == NEG_INF ? 0.0f : __fmul_rn(mn, scale_log2);
@@ -177,7 +183,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
       pk[i / 2] = static_cast<uint32_t>(f32_to_bf16_bits(p0)) | (static_cast<uint32_t>(f32_to_bf16_bits(p1)) << 16);
     }
     red_sum[qtr * 128 + r] = ps;
-    __syncthreads();
+    row_group_sync(grp);
     // block sum: the four quarter sums in quarter order (the same in all four threads)
     ps = __fadd_rn(__fadd_rn(__fadd_rn(red_sum[r], red_sum[128 + r]), red_sum[256 + r]), red_sum[384 + r]);
     l = __fadd_rn(__fmul_rn(l, alpha), ps);

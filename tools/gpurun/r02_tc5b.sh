@@ -3,5 +3,4 @@
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_gpu_model.py -q -x -k "attention" > gpurun_out/tc5b_tests.log 2>&1; echo "rc=$?" >> gpurun_out/tc5b_tests.log
 bash tools/gpurun/r02_tc5_perf.sh > gpurun_out/tc5b_perf.txt 2>&1
-timeout 300 compute-sanitizer --tool synccheck python tools/prof_attn.py 1 4 256 > gpurun_out/tc5b_synccheck.log 2>&1; echo "rc=$?" >> gpurun_out/tc5b_synccheck.log
-tail -3 gpurun_out/tc5b_tests.log; cat gpurun_out/tc5b_perf.txt; tail -3 gpurun_out/tc5b_synccheck.log
+tail -3 gpurun_out/tc5b_tests.log; cat gpurun_out/tc5b_perf.txt
