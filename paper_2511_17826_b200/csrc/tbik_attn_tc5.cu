@@ -159,13 +159,18 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
     // ---- row softmax: 4 threads per query row (TMEM lane), 32 keys each -------------
     float s[32];
     tmem_ld32(tbase + (j & 1) * 128 + lane_off + qtr * 32, s);
+    // only the diagonal block holds keys past the query (or past the sequence end:
+    // qb * 128 < S, so every earlier block lies inside it)
+    if (j == qb) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int key = j * T5_K + qtr * 32 + i;
+        if (key > row || key >= S) s[i] = NEG_INF;
+      }
+    }
     float bm = NEG_INF;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int key = j * T5_K + qtr * 32 + i;
-      if (key > row || key >= S) s[i] = NEG_INF;
-      bm = fmaxf(bm, s[i]);
-    }
+    for (int i = 0; i < 32; ++i) bm = fmaxf(bm, s[i]);
     red_max[qtr * 128 + r] = bm;
     row_group_sync(grp);
     bm = fmaxf(fmaxf(red_max[r], red_max[128 + r]), fmaxf(red_max[256 + r], red_max[384 + r]));
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
       const float p0 = exp2f(__fsub_rn(__fmul_rn(s[i], scale_log2), mc));
       const float p1 = exp2f(__fsub_rn(__fmul_rn(s[i + 1], scale_log2), mc));
       ps = __fadd_rn(__fadd_rn(ps, p0), p1);
-      pk[i / 2] = static_cast<uint32_t>(f32_to_bf16_bits(p0)) | (static_cast<uint32_t>(f32_to_bf16_bits(p1)) << 16);
+      pk[i / 2] = bf16x2_bits(p0, p1);
     }
     red_sum[qtr * 128 + r] = ps;
     row_group_sync(grp);
@@ -242,8 +247,7 @@ __global__ void __launch_bounds__(T5_THREADS, 1)
       uint32_t w[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        w[e] = static_cast<uint32_t>(f32_to_bf16_bits(__fdiv_rn(o[i + 2 * e], l))) |
-               (static_cast<uint32_t>(f32_to_bf16_bits(__fdiv_rn(o[i + 2 * e + 1], l))) << 16);
+        w[e] = bf16x2_bits(__fdiv_rn(o[i + 2 * e], l), __fdiv_rn(o[i + 2 * e + 1], l));
       if (row < S) *reinterpret_cast<uint4*>(op + i) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
